@@ -1,0 +1,137 @@
+/*
+ * mcb200.h — C ABI of libmcb200.so, the B200 (sm_100a) implementation of the
+ * aligned-MSD / path-CV / floating-close-structure hot path of
+ * arXiv 1801.02362 (reference: /root/reference/pkg/src/metadyn_close).
+ *
+ * The reference is a pure-Python package with no FFI; its boundary is the
+ * Python call surface of geometry.py plus the SPEC.md msd-engine / colvar
+ * operations.  Each entry point below is the device primitive that a
+ * maintainer would bind (ctypes / cffi) underneath the
+ * reference call named in its comment.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller; the library
+ *    allocates nothing, frees nothing and keeps no global state.  Calls are
+ *    stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = the
+ *    legacy default stream) and re-entrant across streams and devices.
+ *  - Centred structures live as zero-padded fp64 planes [count, 3, npad]
+ *    (npad a multiple of 32, npad >= n); padding atoms carry zero weight.
+ *  - Covariances S are [.., 9] fp64 with S[b*3+g] = sum_j w_j x_{j,b} a_{j,g}
+ *    (x fitted, a reference), so that the reference's Kearsley matrix is
+ *    K = (Gx + Ga) I - 2 N_Horn(S) and eigvals[0] = the weighted MSD.
+ *  - Eigen records are [.., 20] fp64: 4 ascending eigenvalues of K, then the
+ *    4x4 eigenvector matrix row-major (columns = eigenvectors, each with its
+ *    largest-|component| positive, geometry.py:149-152).
+ *  - Return value: MC_OK or a negative status.  Per-item faults are reported
+ *    through optional uint8 flag arrays (MC_FLAG_*); the Python shim raises
+ *    the matching metadyn_close error class (errors.py:4-35).
+ */
+#ifndef MCB200_H
+#define MCB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.py:4-35) */
+#define MC_OK 0
+#define MC_ERR_INVALID_STRUCTURE (-1) /* InvalidStructureError  errors.py:8  */
+#define MC_ERR_DEGENERATE_FIT (-2)    /* DegenerateFitError     errors.py:12 */
+#define MC_ERR_CONFIG (-3)            /* ConfigError            errors.py:16 */
+#define MC_ERR_EMPTY_ACTIVE_SET (-5)  /* EmptyActiveSetError    errors.py:24 */
+#define MC_ERR_CUDA_BASE (-100)       /* -100 - cudaError_t                  */
+
+/* per-item flags */
+#define MC_FLAG_DEGENERATE 1u   /* eigvals[1]-eigvals[0] < 1e-9 (geometry.py:251-256) */
+#define MC_FLAG_NO_CONVERGE 2u  /* Jacobi exceeded 60 sweeps (geometry.py:144-145)    */
+#define MC_FLAG_NON_FINITE 4u   /* non-finite coordinates or results (geometry.py:41) */
+#define MC_FLAG_ADJ_FALLBACK 8u /* informational: Jacobi used instead of adjugate      */
+#define MC_FLAG_SIG_OVERFLOW 16u /* significant-landmark list exceeded its capacity     */
+
+/* dtypes */
+#define MC_F32 0
+#define MC_F64 1
+
+int mc_version(void);
+
+/* K1 — Structure.center / centroid batched (geometry.py:67-84).
+ * coords [count, n, 3] (dtype), weights [n] normalised (geometry.py:49-61).
+ * Writes centred planes, optional w-weighted planes, centroid [count,3],
+ * G = sum w|x_c|^2 [count], wbar = sum w x_c [count,3], mom = sum w x_c x_c^T
+ * (xx,xy,xz,yy,yz,zz) [count,6]; flags [count] (MC_FLAG_NON_FINITE). */
+int mc_center(const void* coords, int dtype, int64_t count, int32_t n, int32_t npad, const double* w_align,
+              const double* w_disp, double* planes, double* wplanes, double* centroid, double* gnorm,
+              double* wbar, double* mom, uint8_t* flags, void* stream);
+
+/* All-pairs covariance (the linear part of _kearsley_matrix, geometry.py:180-196),
+ * fp64 CUDA-core tiles: S [T, L, 9] from frame planes and w-weighted landmark planes. */
+int mc_cov_f64(const double* fplanes, const double* lwplanes, int32_t T, int32_t L, int32_t npad, double* S,
+               void* stream);
+
+/* Listed-pair covariance: S[p] for (xplanes[xi[p]], aplanes[ai[p]]) with weights w
+ * (xi/ai NULL = identity; ai[p] < 0 gives S = 0).  One warp per pair. */
+int mc_cov_pairs(const double* xplanes, const double* aplanes, const int32_t* xi, const int32_t* ai, int64_t P,
+                 int32_t npad, const double* w, double* S, void* stream);
+
+/* K3 — kearsley_fit without derivatives, dense frame x landmark (geometry.py:227-249):
+ * D [T,L] = eigvals[0]; optional rot [T,L,9], quat [T,L,4], flags [T,L].
+ * Rows with rowmask[t] == 0 are skipped (rowmask may be NULL). */
+int mc_fit_dense(const double* S, int32_t T, int32_t L, const double* gx, const double* ga,
+                 const uint8_t* rowmask, double* D, double* rot, double* quat, uint8_t* flags, void* stream);
+
+/* Listed pairs, MSD only: D[p] = eigvals[0] of (S[p], gx[xi[p]], ga[ai[p]]). */
+int mc_fit_list_msd(const double* S, int64_t P, const int32_t* xi, const int32_t* ai, const double* gx,
+                    const double* ga, double* D, void* stream);
+
+/* Full spectrum with the reference Jacobi (jacobi_eigh on K, geometry.py:106-153,
+ * 246-249): eig [P,20], quat [P,4], rot [P,9], flags [P]. */
+int mc_fit_full(const double* S, int64_t P, const int32_t* xi, const int32_t* ai, const double* gx,
+                const double* ga, double* eig, double* quat, double* rot, uint8_t* flags, void* stream);
+
+/* RotationFit.rot_grad (geometry.py:251-262 with _kearsley_matrix_grad :199-224 and
+ * _rot_quat_jacobian :167-177): out [P, n, 3, 3, 3] = dR_{bg}/dx_{k,alpha}. */
+int mc_rot_grad(const double* xplanes, const double* aplanes, const int32_t* xi, const int32_t* ai, int64_t P,
+                int32_t n, int32_t npad, const double* w, const double* eig, double* out, void* stream);
+
+/* jacobi_eigh (geometry.py:106-153) on B symmetric 4x4 matrices [B,16]:
+ * vals [B,4] ascending, vecs [B,16] row-major. */
+int mc_jacobi4(const double* mats, int64_t B, double* vals, double* vecs, uint8_t* flags, void* stream);
+
+/* K5 — close-structure driver (Alg. 2).
+ * mc_window_pairs: index lists for D(x_s, x_{s-k}), k=1..K, per walker.
+ * mc_close_scan: sequential refresh decisions, one CTA per walker, from the window
+ *   dwin [walkers*steps, K]; on-the-fly fits beyond the window.  Outputs refresh [.]
+ *   (uint8), ridx [.] (global index of the close structure y), dxy [.] = D(x, y)
+ *   (0 on the first frame), n_onthefly [walkers] (nullable).
+ * mc_xy_eig: x<->y spectrum (eig record) and R_xy for every non-refresh frame. */
+int mc_window_pairs(int32_t walkers, int32_t steps, int32_t K, int32_t* xi, int32_t* ai, void* stream);
+int mc_close_scan(const double* fplanes, const double* gx, int32_t walkers, int32_t steps, int32_t npad,
+                  const double* w, const double* dwin, int32_t K, double eps, uint8_t* refresh, int32_t* ridx,
+                  double* dxy, int32_t* n_onthefly, void* stream);
+int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, const double* w,
+              const uint8_t* refresh, const int32_t* ridx, double* xyeig, double* rxy, uint8_t* flags, void* stream);
+
+/* K4 — property-map s (Eq. 2), path-CV z, and their gradients
+ * through Eq. 4 (exact rows) or Eq. 5/6 (non-refresh rows).
+ * mc_pathcv_weights: per frame — min/LSE, s, z, significant-landmark list
+ *   (sig_idx [T,cap], sig_coef [T,cap,18]), nsig [T], fvec [T,16]; writes the
+ *   Eq. 5 distances of non-refresh rows into D.  refresh == NULL: all rows exact.
+ * mc_pathcv_grad: one pass over atoms writing ds, dz [T, n, 3] (fp64, or fp32 if out_f32). */
+int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, double* D, const double* q,
+                      const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
+                      const int32_t* ridx, const double* S, const double* rxy, const double* xyeig,
+                      const double* gx, const double* ga, const double* lmom, double* s, double* z,
+                      int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec, uint8_t* flags,
+                      void* stream);
+int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
+                   const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
+                   const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
+                   const double* xyeig, void* ds, void* dz, int32_t out_f32, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MCB200_H */

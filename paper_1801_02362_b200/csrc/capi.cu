@@ -1,0 +1,121 @@
+// extern "C" boundary of libmcb200.so (declared in include/mcb200.h).
+// Argument validation maps to the reference error taxonomy (errors.py:4-35);
+// CUDA launch errors map to MC_ERR_CUDA_BASE - cudaError_t.
+#include "../../include/mcb200.h"
+#include "launch.h"
+
+namespace {
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? MC_OK : MC_ERR_CUDA_BASE - (int)e; }
+inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool bad_pad(int32_t n, int32_t npad) { return n < 1 || npad < n || (npad % 32) != 0; }
+}  // namespace
+
+extern "C" {
+
+int mc_version(void) { return 1; }
+
+int mc_center(const void* coords, int dtype, int64_t count, int32_t n, int32_t npad, const double* w_align,
+              const double* w_disp, double* planes, double* wplanes, double* centroid, double* gnorm,
+              double* wbar, double* mom, uint8_t* flags, void* stream) {
+  if (count < 0 || (count > 0 && (!coords || !planes || !gnorm || !w_disp))) return MC_ERR_CONFIG;
+  if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
+  if (n < 2) return MC_ERR_INVALID_STRUCTURE;  // geometry.py:39-40
+  if (bad_pad(n, npad)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_center(coords, dtype, count, n, npad, w_align, w_disp, planes, wplanes, centroid,
+                                       gnorm, wbar, mom, flags, S_(stream)));
+}
+
+int mc_cov_f64(const double* fplanes, const double* lwplanes, int32_t T, int32_t L, int32_t npad, double* S,
+               void* stream) {
+  if (T < 0 || L < 0 || npad % 32 != 0 || ((int64_t)T * L > 0 && (!fplanes || !lwplanes || !S))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cov_f64(fplanes, lwplanes, T, L, npad, S, S_(stream)));
+}
+
+int mc_cov_pairs(const double* xplanes, const double* aplanes, const int32_t* xi, const int32_t* ai, int64_t P,
+                 int32_t npad, const double* w, double* S, void* stream) {
+  if (P < 0 || npad % 32 != 0 || (P > 0 && (!xplanes || !aplanes || !S))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cov_pairs(xplanes, aplanes, xi, ai, P, npad, w, S, S_(stream)));
+}
+
+int mc_fit_dense(const double* S, int32_t T, int32_t L, const double* gx, const double* ga,
+                 const uint8_t* rowmask, double* D, double* rot, double* quat, uint8_t* flags, void* stream) {
+  if (T < 0 || L < 0 || ((int64_t)T * L > 0 && (!S || !gx || !ga || !D))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_fit_dense(S, T, L, gx, ga, rowmask, D, rot, quat, flags, S_(stream)));
+}
+
+int mc_fit_list_msd(const double* S, int64_t P, const int32_t* xi, const int32_t* ai, const double* gx,
+                    const double* ga, double* D, void* stream) {
+  if (P < 0 || (P > 0 && (!S || !gx || !ga || !D))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_fit_list_msd(S, P, xi, ai, gx, ga, D, S_(stream)));
+}
+
+int mc_fit_full(const double* S, int64_t P, const int32_t* xi, const int32_t* ai, const double* gx,
+                const double* ga, double* eig, double* quat, double* rot, uint8_t* flags, void* stream) {
+  if (P < 0 || (P > 0 && (!S || !gx || !ga))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_fit_full(S, P, xi, ai, gx, ga, eig, quat, rot, flags, S_(stream)));
+}
+
+int mc_rot_grad(const double* xplanes, const double* aplanes, const int32_t* xi, const int32_t* ai, int64_t P,
+                int32_t n, int32_t npad, const double* w, const double* eig, double* out, void* stream) {
+  if (P < 0 || bad_pad(n, npad) || (P > 0 && (!xplanes || !aplanes || !w || !eig || !out))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_rot_grad(xplanes, aplanes, xi, ai, P, n, npad, w, eig, out, S_(stream)));
+}
+
+int mc_jacobi4(const double* mats, int64_t B, double* vals, double* vecs, uint8_t* flags, void* stream) {
+  if (B < 0 || (B > 0 && (!mats || !vals || !vecs))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_jacobi4(mats, B, vals, vecs, flags, S_(stream)));
+}
+
+int mc_window_pairs(int32_t walkers, int32_t steps, int32_t K, int32_t* xi, int32_t* ai, void* stream) {
+  if (walkers < 0 || steps < 0 || K < 1 || !xi || !ai) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_window_pairs(walkers, steps, K, xi, ai, S_(stream)));
+}
+
+int mc_close_scan(const double* fplanes, const double* gx, int32_t walkers, int32_t steps, int32_t npad,
+                  const double* w, const double* dwin, int32_t K, double eps, uint8_t* refresh, int32_t* ridx,
+                  double* dxy, int32_t* n_onthefly, void* stream) {
+  if (walkers < 0 || steps < 0 || K < 1 || K > 32 || npad % 32 != 0) return MC_ERR_CONFIG;
+  if (!(eps >= 0.0)) return MC_ERR_CONFIG;
+  if (walkers * (int64_t)steps > 0 && (!fplanes || !gx || !w || !dwin || !refresh || !ridx || !dxy))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_close_scan(fplanes, gx, walkers, steps, npad, w, dwin, K, eps, refresh, ridx, dxy,
+                                           n_onthefly, S_(stream)));
+}
+
+int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, const double* w,
+              const uint8_t* refresh, const int32_t* ridx, double* xyeig, double* rxy, uint8_t* flags, void* stream) {
+  if (T < 0 || npad % 32 != 0 || (T > 0 && (!fplanes || !gx || !w || !refresh || !ridx || !xyeig || !rxy)))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_xy_eig(fplanes, gx, T, npad, w, refresh, ridx, xyeig, rxy, flags, S_(stream)));
+}
+
+int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, double* D, const double* q,
+                      const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
+                      const int32_t* ridx, const double* S, const double* rxy, const double* xyeig,
+                      const double* gx, const double* ga, const double* lmom, double* s, double* z,
+                      int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec, uint8_t* flags,
+                      void* stream) {
+  if (T < 0) return MC_ERR_CONFIG;
+  if (T > 0 && L < 1) return MC_ERR_EMPTY_ACTIVE_SET;
+  if (!(lam > 0.0) || !(cutoff > 0.0) || cap < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!D || !q || !R || !fwbar || !lwbar || !s || !z || !sig_idx || !sig_coef || !nsig || !fvec))
+    return MC_ERR_CONFIG;
+  if (refresh && (!ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cv_weights(T, L, lam, cutoff, cap, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
+                                           xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags,
+                                           S_(stream)));
+}
+
+int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
+                   const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
+                   const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
+                   const double* xyeig, void* ds, void* dz, int32_t out_f32, void* stream) {
+  if (T < 0 || bad_pad(n, npad) || cap < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!fplanes || !lplanes || !w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec || !ds || !dz))
+    return MC_ERR_CONFIG;
+  if (refresh && (!ridx || !xyeig)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cv_grad(T, n, npad, cap, fplanes, lplanes, w, w_align, sig_idx, sig_coef, nsig, fvec,
+                                        refresh, ridx, xyeig, ds, dz, out_f32, S_(stream)));
+}
+
+}  // extern "C"

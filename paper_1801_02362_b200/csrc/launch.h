@@ -1,0 +1,43 @@
+// Internal host launchers (one per kernel family); capi.cu wraps them in the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mc {
+cudaError_t launch_center(const void* coords, int dtype, int64_t count, int n, int npad, const double* w_align,
+                          const double* w_disp, double* planes, double* wplanes, double* centroid, double* gnorm,
+                          double* wbar, double* mom, uint8_t* flags, cudaStream_t stream);
+cudaError_t launch_cov_f64(const double* fpl, const double* lpl, int T, int L, int npad, double* S,
+                           cudaStream_t stream);
+cudaError_t launch_cov_pairs(const double* xpl, const double* apl, const int* xi, const int* ai, int64_t P,
+                             int npad, const double* w, double* S, cudaStream_t stream);
+cudaError_t launch_fit_dense(const double* S, int T, int L, const double* gx, const double* ga,
+                             const uint8_t* rowmask, double* D, double* rot, double* quat, uint8_t* flags,
+                             cudaStream_t stream);
+cudaError_t launch_fit_list_msd(const double* S, int64_t P, const int* xi, const int* ai, const double* gx,
+                                const double* ga, double* D, cudaStream_t stream);
+cudaError_t launch_fit_full(const double* S, int64_t P, const int* xi, const int* ai, const double* gx,
+                            const double* ga, double* eig, double* quat, double* rot, uint8_t* flags,
+                            cudaStream_t stream);
+cudaError_t launch_rot_grad(const double* xpl, const double* apl, const int* xi, const int* ai, int64_t P, int n,
+                            int npad, const double* w, const double* eig, double* out, cudaStream_t stream);
+cudaError_t launch_jacobi4(const double* mats, int64_t B, double* vals, double* vecs, uint8_t* flags,
+                           cudaStream_t stream);
+cudaError_t launch_window_pairs(int walkers, int steps, int K, int* xi, int* ai, cudaStream_t stream);
+cudaError_t launch_close_scan(const double* fpl, const double* gx, int walkers, int steps, int npad,
+                              const double* w, const double* dwin, int K, double eps, uint8_t* refresh, int* ridx,
+                              double* dxy, int* n_onthefly, cudaStream_t stream);
+cudaError_t launch_xy_eig(const double* fpl, const double* gx, int64_t T, int npad, const double* w,
+                          const uint8_t* refresh, const int* ridx, double* xyeig, double* rxy, uint8_t* flags,
+                          cudaStream_t stream);
+cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, double* D, const double* q,
+                              const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
+                              const int* ridx, const double* S, const double* rxy, const double* xyeig,
+                              const double* gx, const double* ga, const double* lmom, double* s, double* z,
+                              int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
+                              cudaStream_t stream);
+cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
+                           const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
+                           const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
+                           void* ds, void* dz, int out_f32, cudaStream_t stream);
+}  // namespace mc

@@ -1,0 +1,344 @@
+// K4 — fused path-CV reduction (Eq. 2) and its gradient.
+//
+// s = sum_i q_i p_i,  z = D_min - (1/lam) ln sum_i e^{-lam (D_i - D_min)},
+// p = softmax(-lam D) with the min-D shift.
+// ds = sum_i cs_i dD_i with cs_i = -lam p_i (q_i - s);  dz = sum_i p_i dD_i.
+//
+// Every dD_i has the form (w.r.t. the centred x)
+//     2 w (x - Rhat_i a_i)  [+ <M_i, dR_xy/dx> for close-structure frames]
+// and the raw-coordinate gradient subtracts w' * sum_k (.) (the centring
+// chain rule).  Rhat_i is the exact fit rotation of (x, a_i) or, on a
+// non-refresh frame, R_xy R_{a_i y} (Eq. 5).  Because everything is linear
+// in the coefficients, the per-landmark work is folded into per-frame
+// quantities here (cv_weights_kernel) and a single pass over atoms
+// (cv_grad_kernel) writes the gradients:
+//   U_k   = sum_i c_i Rhat_i a_{i,k}               (only significant i)
+//   M     = -2 [ sum_i c_i S_i R_i^T - R_xy sum_i c_i R_i A_i R_i^T ]
+//   g_c   = <M, dR/dq_c>,  v = sum_m (q_m.g)/(l_0 - l_m) q_m
+//   dR-term_k = v^T (dK/dx_k) q_0                     (closed form, mc_math)
+// Landmarks with lam (D_i - D_min) > cutoff (default 50) contribute
+// < e^-50 relative to the leading term and are skipped.
+#include "mc_math.cuh"
+
+namespace mc {
+
+namespace {
+constexpr int WNT = 256;
+constexpr int FVEC = 16;  // sumcs, sumcz, corr_s[3], corr_z[3], v_s[4], v_z[4]
+}
+
+__device__ __forceinline__ void mat3_mul(const double* a, const double* b, double* c) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) c[i * 3 + j] = a[i * 3] * b[j] + a[i * 3 + 1] * b[3 + j] + a[i * 3 + 2] * b[6 + j];
+}
+
+__global__ void __launch_bounds__(WNT)
+cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __restrict__ D,
+                  const double* __restrict__ q, const double* __restrict__ R, const double* __restrict__ fwbar,
+                  const double* __restrict__ lwbar, const uint8_t* __restrict__ refresh,
+                  const int* __restrict__ ridx, const double* __restrict__ S, const double* __restrict__ rxy,
+                  const double* __restrict__ xyeig, const double* __restrict__ gx, const double* __restrict__ ga,
+                  const double* __restrict__ lmom, double* __restrict__ s_out, double* __restrict__ z_out,
+                  int* __restrict__ sig_idx, double* __restrict__ sig_coef, int* __restrict__ nsig,
+                  double* __restrict__ fvec, uint8_t* __restrict__ flags) {
+  __shared__ double scratch[WNT / 32];
+  __shared__ int wcount[WNT / 32];
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool approx = refresh && !refresh[t];
+  const int r = approx ? ridx[t] : t;
+  double Rxy[9];
+  if (approx) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Rxy[e] = rxy[(int64_t)t * 9 + e];
+  }
+  double* Dt = D + (int64_t)t * L;
+  // pass 1: distances (Eq. 5 on non-refresh frames) and their minimum
+  double dmin = INFINITY;
+  bool finite = true;
+  for (int i = tid; i < L; i += WNT) {
+    double d;
+    if (approx) {
+      const double* Ri = R + ((int64_t)r * L + i) * 9;
+      const double* Si = S + ((int64_t)t * L + i) * 9;
+      double Rr[9], Rh[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) Rr[e] = Ri[e];
+      mat3_mul(Rxy, Rr, Rh);
+      double dot = 0.0;
+#pragma unroll
+      for (int e = 0; e < 9; ++e) dot = fma(Rh[e], Si[e], dot);
+      d = gx[t] + ga[i] - 2.0 * dot;
+      Dt[i] = d;
+    } else {
+      d = Dt[i];
+    }
+    finite = finite && isfinite(d);
+    dmin = fmin(dmin, d);
+  }
+  dmin = block_min<WNT>(dmin, scratch);
+  const int nonfinite = __syncthreads_or(!finite);
+  // pass 2: partition function
+  double zs = 0.0, qs = 0.0;
+  for (int i = tid; i < L; i += WNT) {
+    const double e = exp(-lam * (Dt[i] - dmin));
+    zs += e;
+    qs += q[i] * e;
+  }
+  zs = block_sum<WNT>(zs, scratch);
+  qs = block_sum<WNT>(qs, scratch);
+  const double sval = qs / zs;
+  const double zval = dmin - log(zs) / lam;
+  // pass 3: ordered compaction of the significant landmarks + per-frame sums
+  double acc[44];
+#pragma unroll
+  for (int e = 0; e < 44; ++e) acc[e] = 0.0;
+  int total = 0;
+  for (int b0 = 0; b0 < L; b0 += WNT) {
+    const int i = b0 + tid;
+    double di = 0.0;
+    bool sig = false;
+    if (i < L) {
+      di = Dt[i];
+      sig = lam * (di - dmin) <= cutoff;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, sig);
+    __syncthreads();
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int pos = total + __popc(bal & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) pos += wcount[w];
+    int blk = 0;
+    for (int w = 0; w < WNT / 32; ++w) blk += wcount[w];
+    if (sig) {
+      const double p = exp(-lam * (di - dmin)) / zs;
+      const double cs = -lam * p * (q[i] - sval);
+      const double cz = p;
+      double Rh[9], Rr[9];
+      if (approx) {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Rr[e] = R[((int64_t)r * L + i) * 9 + e];
+        mat3_mul(Rxy, Rr, Rh);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Rh[e] = R[((int64_t)t * L + i) * 9 + e];
+      }
+      if (pos < cap) {
+        sig_idx[(int64_t)t * cap + pos] = i;
+        double* co = sig_coef + ((int64_t)t * cap + pos) * 18;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) { co[e] = cs * Rh[e]; co[9 + e] = cz * Rh[e]; }
+      }
+      acc[0] += cs;
+      acc[1] += cz;
+      const double wb0 = lwbar[3 * i], wb1 = lwbar[3 * i + 1], wb2 = lwbar[3 * i + 2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double rw = Rh[a * 3] * wb0 + Rh[a * 3 + 1] * wb1 + Rh[a * 3 + 2] * wb2;
+        acc[2 + a] += cs * rw;
+        acc[5 + a] += cz * rw;
+      }
+      if (approx) {
+        // S_i R_i^T and R_i A_i R_i^T (R_i = saved rotation of landmark i)
+        const double* Si = S + ((int64_t)t * L + i) * 9;
+        const double* m = lmom + 6 * (int64_t)i;
+        const double A[9] = {m[0], m[1], m[2], m[1], m[3], m[4], m[2], m[4], m[5]};
+        double SRt[9], RA[9], RAR[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            SRt[a * 3 + b] = Si[a * 3] * Rr[b * 3] + Si[a * 3 + 1] * Rr[b * 3 + 1] + Si[a * 3 + 2] * Rr[b * 3 + 2];
+        mat3_mul(Rr, A, RA);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            RAR[a * 3 + b] = RA[a * 3] * Rr[b * 3] + RA[a * 3 + 1] * Rr[b * 3 + 1] + RA[a * 3 + 2] * Rr[b * 3 + 2];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          acc[8 + e] += cs * SRt[e];
+          acc[17 + e] += cz * SRt[e];
+          acc[26 + e] += cs * RAR[e];
+          acc[35 + e] += cz * RAR[e];
+        }
+      }
+    }
+    total += blk;
+  }
+  const int nacc = approx ? 44 : 8;
+  for (int e = 0; e < nacc; ++e) acc[e] = block_sum<WNT>(acc[e], scratch);
+  if (tid != 0) return;
+  s_out[t] = sval;
+  z_out[t] = zval;
+  nsig[t] = min(total, cap);
+  double* fv = fvec + (int64_t)t * FVEC;
+  const double fw[3] = {fwbar[3 * t], fwbar[3 * t + 1], fwbar[3 * t + 2]};
+  double corr[2][3], vv[2][4];
+  for (int c = 0; c < 2; ++c) {
+    const double sumc = acc[c];
+    for (int a = 0; a < 3; ++a) corr[c][a] = 2.0 * (sumc * fw[a] - acc[2 + 3 * c + a]);
+    vv[c][0] = vv[c][1] = vv[c][2] = vv[c][3] = 0.0;
+  }
+  if (approx) {
+    const double* e = xyeig + (int64_t)t * 20;
+    double q0[4], qm[3][4], inv[3];
+    for (int rr = 0; rr < 4; ++rr) q0[rr] = e[4 + rr * 4];
+    for (int m = 0; m < 3; ++m) {
+      for (int rr = 0; rr < 4; ++rr) qm[m][rr] = e[4 + rr * 4 + m + 1];
+      inv[m] = 1.0 / (e[0] - e[m + 1]);
+    }
+    double J[4][9];
+    rot_quat_jacobian(q0, J);
+    const double yw[3] = {fwbar[3 * r], fwbar[3 * r + 1], fwbar[3 * r + 2]};
+    for (int c = 0; c < 2; ++c) {
+      // M = -2 [ SR - Rxy RAR ]
+      const double* SR = acc + 8 + 9 * c;
+      const double* RAR = acc + 26 + 9 * c;
+      double XR[9], M[9];
+      mat3_mul(Rxy, RAR, XR);
+      for (int k = 0; k < 9; ++k) M[k] = -2.0 * (SR[k] - XR[k]);
+      double g[4];
+      for (int cc = 0; cc < 4; ++cc) {
+        double sacc = 0.0;
+        for (int k = 0; k < 9; ++k) sacc += M[k] * J[cc][k];
+        g[cc] = sacc;
+      }
+      for (int m = 0; m < 3; ++m) {
+        const double h = (qm[m][0] * g[0] + qm[m][1] * g[1] + qm[m][2] * g[2] + qm[m][3] * g[3]) * inv[m];
+        for (int rr = 0; rr < 4; ++rr) vv[c][rr] += h * qm[m][rr];
+      }
+      double dsum[3];
+      dk_contract(vv[c], q0, 1.0, fw, yw, dsum);
+      for (int a = 0; a < 3; ++a) corr[c][a] += dsum[a];
+    }
+  }
+  fv[0] = acc[0];
+  fv[1] = acc[1];
+  for (int a = 0; a < 3; ++a) { fv[2 + a] = corr[0][a]; fv[5 + a] = corr[1][a]; }
+  for (int rr = 0; rr < 4; ++rr) { fv[8 + rr] = vv[0][rr]; fv[12 + rr] = vv[1][rr]; }
+  if (flags) {
+    uint8_t f = 0;
+    if (total > cap) f |= kFlagSigOverflow;
+    if (nonfinite || !isfinite(sval) || !isfinite(zval)) f |= kFlagNonFinite;
+    flags[t] = f;
+  }
+}
+
+cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, double* D, const double* q,
+                              const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
+                              const int* ridx, const double* S, const double* rxy, const double* xyeig,
+                              const double* gx, const double* ga, const double* lmom, double* s, double* z,
+                              int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
+                              cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, L, lam, cutoff, cap, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
+                                           xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
+  return cudaGetLastError();
+}
+
+namespace {
+constexpr int GNT = 128, APT = 4, GCH = 64;
+}
+
+template <typename OT>
+__global__ void __launch_bounds__(GNT)
+cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const double* __restrict__ lpl,
+               const double* __restrict__ w, const double* __restrict__ wa, const int* __restrict__ sig_idx,
+               const double* __restrict__ sig_coef, const int* __restrict__ nsig, const double* __restrict__ fvec,
+               const uint8_t* __restrict__ refresh, const int* __restrict__ ridx, const double* __restrict__ xyeig,
+               OT* __restrict__ ds, OT* __restrict__ dz) {
+  __shared__ double sc[GCH * 18];
+  __shared__ int si[GCH];
+  const int t = blockIdx.x;
+  const int k0 = blockIdx.y * GNT * APT;
+  const int tid = threadIdx.x;
+  const int ns = nsig[t];
+  double us[APT][3], uz[APT][3];
+#pragma unroll
+  for (int m = 0; m < APT; ++m)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) us[m][a] = uz[m][a] = 0.0;
+  for (int c0 = 0; c0 < ns; c0 += GCH) {
+    const int cn = min(GCH, ns - c0);
+    __syncthreads();
+    for (int e = tid; e < cn * 18; e += GNT) sc[e] = sig_coef[((int64_t)t * cap + c0) * 18 + e];
+    for (int e = tid; e < cn; e += GNT) si[e] = sig_idx[(int64_t)t * cap + c0 + e];
+    __syncthreads();
+    for (int e = 0; e < cn; ++e) {
+      const double* a = lpl + (int64_t)si[e] * 3 * npad;
+      const double* C = sc + e * 18;
+#pragma unroll
+      for (int m = 0; m < APT; ++m) {
+        const int k = k0 + tid + m * GNT;
+        if (k < n) {
+          const double a0 = a[k], a1 = a[npad + k], a2 = a[2 * npad + k];
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            us[m][b] = fma(C[b * 3], a0, fma(C[b * 3 + 1], a1, fma(C[b * 3 + 2], a2, us[m][b])));
+            uz[m][b] = fma(C[9 + b * 3], a0, fma(C[9 + b * 3 + 1], a1, fma(C[9 + b * 3 + 2], a2, uz[m][b])));
+          }
+        }
+      }
+    }
+  }
+  const double* fv = fvec + (int64_t)t * FVEC;
+  const bool approx = refresh && !refresh[t];
+  double q0[4] = {0, 0, 0, 0};
+  const double* y = nullptr;
+  if (approx) {
+    const double* e = xyeig + (int64_t)t * 20;
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) q0[rr] = e[4 + rr * 4];
+    y = fpl + (int64_t)ridx[t] * 3 * npad;
+  }
+  const double* x = fpl + (int64_t)t * 3 * npad;
+  const double vs[4] = {fv[8], fv[9], fv[10], fv[11]};
+  const double vz[4] = {fv[12], fv[13], fv[14], fv[15]};
+#pragma unroll
+  for (int m = 0; m < APT; ++m) {
+    const int k = k0 + tid + m * GNT;
+    if (k >= n) continue;
+    const double wk = w[k], wak = wa[k];
+    const double xk[3] = {x[k], x[npad + k], x[2 * npad + k]};
+    double gs[3], gz[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      gs[a] = 2.0 * wk * (fv[0] * xk[a] - us[m][a]) - wak * fv[2 + a];
+      gz[a] = 2.0 * wk * (fv[1] * xk[a] - uz[m][a]) - wak * fv[5 + a];
+    }
+    if (approx) {
+      const double yk[3] = {y[k], y[npad + k], y[2 * npad + k]};
+      double d[3];
+      dk_contract(vs, q0, wk, xk, yk, d);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gs[a] += d[a];
+      dk_contract(vz, q0, wk, xk, yk, d);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gz[a] += d[a];
+    }
+    OT* os = ds + ((int64_t)t * n + k) * 3;
+    OT* oz = dz + ((int64_t)t * n + k) * 3;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { os[a] = (OT)gs[a]; oz[a] = (OT)gz[a]; }
+  }
+}
+
+cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
+                           const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
+                           const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
+                           void* ds, void* dz, int out_f32, cudaStream_t stream) {
+  if (T <= 0 || n <= 0) return cudaSuccess;
+  dim3 grid(T, (n + GNT * APT - 1) / (GNT * APT));
+  if (out_f32)
+    cv_grad_kernel<float><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
+                                                    refresh, ridx, xyeig, (float*)ds, (float*)dz);
+  else
+    cv_grad_kernel<double><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
+                                                     refresh, ridx, xyeig, (double*)ds, (double*)dz);
+  return cudaGetLastError();
+}
+
+}  // namespace mc

@@ -1,0 +1,198 @@
+"""Batched device entry points of the hot path.
+
+* ``msd_matrix(frames, landmarks)``      all-pairs aligned MSD  [T, L]
+* ``path_cv(frames, landmarks, lam)``    s, z, ds, dz (Alg. 1, exact MSD)
+* ``close_structure_replay(...)``        Alg. 2 over a trajectory (or W walkers)
+
+They are the batched counterparts of the reference's per-structure calls
+(kearsley_fit, geometry.py:227; SPEC.md exact_distance / approx_distance /
+step_close_structure / property_map) on torch CUDA tensors, all arithmetic in
+libmcb200.so.  ``PathCV`` keeps the landmark set resident (centred planes,
+norms, moments) across calls, the way a metadynamics run reuses it every step.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from ._lib import FLAG_DEGENERATE, FLAG_NO_CONVERGE, FLAG_NON_FINITE, FLAG_SIG_OVERFLOW
+from .errors import ConfigError, DegenerateFitError, EmptyActiveSetError, InvalidStructureError, MetadynError
+
+DEFAULT_CUTOFF = 50.0   # lam*(D_i - D_min) beyond which a landmark's weight is < e^-50
+DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
+
+
+def normalise_weights(w, n, kind, device):
+    """geometry.py:49-61 on the host (argument validation), uploaded as fp64."""
+    if w is None:
+        arr = np.full(n, 1.0 / n)
+    else:
+        arr = np.array(w.detach().cpu().numpy() if torch.is_tensor(w) else w, dtype=float)
+        if arr.shape != (n,):
+            raise InvalidStructureError(f"{kind} weights must have length {n}")
+        if not np.all(np.isfinite(arr)) or np.any(arr < 0.0):
+            raise InvalidStructureError(f"{kind} weights must be finite and non-negative")
+        total = arr.sum()
+        if total <= 0.0:
+            raise InvalidStructureError(f"{kind} weights sum to zero")
+        arr = arr / total
+    npad = K.npad_for(n)
+    out = torch.zeros(npad, dtype=torch.float64, device=device)
+    out[:n] = torch.from_numpy(arr).to(device)
+    return out
+
+
+def _as_cuda(x, device=None):
+    if not torch.is_tensor(x):
+        x = torch.as_tensor(np.asarray(x))
+    if x.dtype not in (torch.float32, torch.float64):
+        x = x.to(torch.float64)
+    dev = device if device is not None else (x.device if x.is_cuda else torch.device("cuda", torch.cuda.current_device()))
+    return x.to(dev, non_blocking=True).contiguous()
+
+
+def _check_shapes(frames, landmarks):
+    if frames.ndim != 3 or frames.shape[-1] != 3:
+        raise InvalidStructureError(f"frames must be [T, n, 3], got {tuple(frames.shape)}")
+    if landmarks.ndim != 3 or landmarks.shape[-1] != 3:
+        raise InvalidStructureError(f"landmarks must be [L, n, 3], got {tuple(landmarks.shape)}")
+    if frames.shape[1] != landmarks.shape[1]:
+        raise InvalidStructureError(f"atom count mismatch: {frames.shape[1]} vs {landmarks.shape[1]}")
+    if frames.shape[1] < 2:
+        raise InvalidStructureError("a structure needs at least 2 atoms")
+    if landmarks.shape[0] < 1:
+        raise EmptyActiveSetError("no landmarks")
+
+
+def _raise_flags(flags, what):
+    if flags is None or flags.numel() == 0:
+        return
+    f = int(torch.bitwise_or.reduce(flags.flatten()).item()) if hasattr(torch.bitwise_or, "reduce") else \
+        int(np.bitwise_or.reduce(flags.flatten().cpu().numpy()))
+    if f & FLAG_NON_FINITE:
+        raise InvalidStructureError(f"{what}: non-finite coordinates or distances")
+    if f & FLAG_NO_CONVERGE:
+        raise MetadynError(f"{what}: Jacobi diagonalisation did not converge")
+
+
+def _or_flags(flags):
+    return int(np.bitwise_or.reduce(flags.flatten().cpu().numpy())) if flags.numel() else 0
+
+
+class PathCV:
+    """Resident landmark set + evaluator for s, z and their atom gradients.
+
+    landmarks [L, n, 3] (fp32/fp64, any device); lam > 0; q [L] properties
+    (default: landmark index); w / w_align the displacement and
+    alignment weights shared by every structure.
+    """
+
+    def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=DEFAULT_CUTOFF, device=None):
+        K.require_cuda()
+        lm = _as_cuda(landmarks, device)
+        if lm.ndim != 3 or lm.shape[-1] != 3:
+            raise InvalidStructureError("landmarks must be [L, n, 3]")
+        if lm.shape[0] < 1:
+            raise EmptyActiveSetError("no landmarks")
+        if not (lam > 0):
+            raise ConfigError("lambda must be positive")
+        self.device = lm.device
+        self.L, self.n = int(lm.shape[0]), int(lm.shape[1])
+        if self.n < 2:
+            raise InvalidStructureError("a structure needs at least 2 atoms")
+        self.lam = float(lam)
+        self.cutoff = float(cutoff)
+        self.w = normalise_weights(w, self.n, "displacement", self.device)
+        self.wa = normalise_weights(w_align, self.n, "alignment", self.device)
+        qq = np.arange(self.L, dtype=float) if q is None else np.asarray(
+            q.detach().cpu().numpy() if torch.is_tensor(q) else q, dtype=float)
+        if qq.shape != (self.L,):
+            raise ConfigError("q must have one value per landmark")
+        self.q = torch.from_numpy(qq).to(self.device)
+        self.lm = K.center(lm, self.wa, self.w, weighted=True, moments=True)
+        if _or_flags(self.lm.flags) & FLAG_NON_FINITE:
+            raise InvalidStructureError("landmark coordinates contain non-finite values")
+
+    # ------------------------------------------------------------------
+    def _frames(self, frames):
+        fr = _as_cuda(frames, self.device)
+        _check_shapes(fr, torch.empty((self.L, self.n, 3)))
+        c = K.center(fr, self.wa, self.w)
+        if _or_flags(c.flags) & FLAG_NON_FINITE:
+            raise InvalidStructureError("frame coordinates contain non-finite values")
+        return fr, c
+
+    def msd_matrix(self, frames, want_rot=False):
+        """Exact aligned MSD of every (frame, landmark) pair: D [T, L] fp64."""
+        _, fr = self._frames(frames)
+        S = K.cov_dense(fr, self.lm)
+        D, rot, _, flags = K.fit_dense(S, fr.g, self.lm.g, want_rot=want_rot)
+        _raise_flags(flags, "msd_matrix")
+        return (D, rot) if want_rot else D
+
+    def _cap(self, cap):
+        return int(min(self.L, 512) if cap is None else min(cap, self.L))
+
+    def evaluate(self, frames, grad=True, cap=None, out_dtype=None):
+        """Alg. 1 without neighbour list: exact D_i for every landmark."""
+        raw, fr = self._frames(frames)
+        S = K.cov_dense(fr, self.lm)
+        D, R, _, flags = K.fit_dense(S, fr.g, self.lm.g, want_rot=True)
+        _raise_flags(flags, "path_cv")
+        return self._finish(raw, fr, D, R, S, None, grad, cap, out_dtype)
+
+    def close_replay(self, frames, eps, walkers=1, grad=True, window=DEFAULT_WINDOW, cap=None, out_dtype=None):
+        """Alg. 2 replay: frames [T, n, 3] (walkers == 1) or [W, S, n, 3]."""
+        if eps is None or not (eps >= 0):
+            raise ConfigError("eps must be >= 0")
+        fr_in = _as_cuda(frames, self.device)
+        if fr_in.ndim == 4:
+            walkers, steps = int(fr_in.shape[0]), int(fr_in.shape[1])
+            fr_in = fr_in.reshape(walkers * steps, self.n, 3)
+        else:
+            steps = int(fr_in.shape[0]) // walkers
+        raw, fr = self._frames(fr_in)
+        close = K.close_decisions(fr, self.w, eps, walkers, steps, window)
+        S = K.cov_dense(fr, self.lm)
+        D, R, _, flags = K.fit_dense(S, fr.g, self.lm.g, rowmask=close["refresh"], want_rot=True)
+        _raise_flags(flags, "close_structure_replay")
+        out = self._finish(raw, fr, D, R, S, close, grad, cap, out_dtype)
+        if grad and _or_flags(close["xyflags"]) & FLAG_DEGENERATE:
+            raise DegenerateFitError("close-structure fit x<->y has a degenerate spectrum")
+        out.update(refresh=close["refresh"].bool(), dxy=close["dxy"], ridx=close["ridx"], onthefly=close["onthefly"])
+        return out
+
+    def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype):
+        cap = self._cap(cap)
+        while True:
+            wres = K.pathcv_weights(D, self.q, self.lam, R, fr, self.lm, cap, self.cutoff, close=close, S=S)
+            f = _or_flags(wres["flags"])
+            if f & FLAG_SIG_OVERFLOW and cap < self.L:
+                cap = self.L
+                continue
+            break
+        if f & FLAG_NON_FINITE:
+            raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        out = {"s": wres["s"], "z": wres["z"], "D": D}
+        if grad:
+            odt = out_dtype or (torch.float64 if raw.dtype == torch.float64 else torch.float32)
+            out["ds"], out["dz"] = K.pathcv_grad(wres, fr, self.lm, self.w, self.wa, cap, odt, close=close)
+        out["nsig"] = wres["nsig"]
+        return out
+
+
+# ---------------------------------------------------------------- functional API
+
+def msd_matrix(frames, landmarks, w=None, w_align=None):
+    """All-pairs aligned MSD (eigvals[0] of kearsley_fit for every pair)."""
+    return PathCV(landmarks, 1.0, w=w, w_align=w_align).msd_matrix(frames)
+
+
+def path_cv(frames, landmarks, lam, q=None, w=None, w_align=None, grad=True):
+    return PathCV(landmarks, lam, q, w, w_align).evaluate(frames, grad=grad)
+
+
+def close_structure_replay(frames, landmarks, lam, eps, q=None, w=None, w_align=None, grad=True, walkers=1):
+    return PathCV(landmarks, lam, q, w, w_align).close_replay(frames, eps, walkers=walkers, grad=grad)

@@ -1,0 +1,182 @@
+"""Thin torch-tensor wrappers over the C ABI (one per libmcb200 entry point).
+
+Torch provides device memory and the current stream; every arithmetic step
+runs in libmcb200.so.  Shapes follow include/mcb200.h.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream_ptr
+from .errors import DeviceError
+
+F64 = torch.float64
+I32 = torch.int32
+U8 = torch.uint8
+
+
+def require_cuda(t=None):
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
+    if t is not None and not t.is_cuda:
+        raise DeviceError("expected a CUDA tensor")
+    _lib.load()
+
+
+def npad_for(n):
+    return ((int(n) + 31) // 32) * 32
+
+
+class Centred:
+    """Centred planes + per-structure scalars of a batch of structures."""
+
+    __slots__ = ("planes", "wplanes", "centroid", "g", "wbar", "mom", "flags", "n", "npad", "count")
+
+    def __init__(self, planes, wplanes, centroid, g, wbar, mom, flags, n, npad):
+        self.planes, self.wplanes, self.centroid, self.g = planes, wplanes, centroid, g
+        self.wbar, self.mom, self.flags = wbar, mom, flags
+        self.n, self.npad, self.count = n, npad, planes.shape[0]
+
+
+def center(coords, w_align, w_disp, weighted=False, moments=False, recenter=True):
+    """K1: coords [B, n, 3] (f32/f64, CUDA) -> Centred.  w_* are [n] fp64 CUDA tensors."""
+    require_cuda(coords)
+    coords = coords.contiguous()
+    b, n, _ = coords.shape
+    npad = npad_for(n)
+    dev = coords.device
+    dt = _lib.MC_F64 if coords.dtype == torch.float64 else _lib.MC_F32
+    if coords.dtype not in (torch.float32, torch.float64):
+        raise DeviceError("coords must be float32 or float64")
+    planes = torch.empty((b, 3, npad), dtype=F64, device=dev)
+    wplanes = torch.empty((b, 3, npad), dtype=F64, device=dev) if weighted else None
+    centroid = torch.empty((b, 3), dtype=F64, device=dev)
+    g = torch.empty((b,), dtype=F64, device=dev)
+    wbar = torch.empty((b, 3), dtype=F64, device=dev)
+    mom = torch.empty((b, 6), dtype=F64, device=dev) if moments else None
+    flags = torch.empty((b,), dtype=U8, device=dev)
+    call("mc_center", ptr(coords), dt, b, n, npad, ptr(w_align) if recenter else None, ptr(w_disp), ptr(planes),
+         ptr(wplanes), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
+    return Centred(planes, wplanes, centroid, g, wbar, mom, flags, n, npad)
+
+
+def cov_dense(fr: Centred, lm: Centred):
+    """S [T, L, 9] fp64 from frame planes and weighted landmark planes."""
+    T, L = fr.count, lm.count
+    S = torch.empty((T, L, 9), dtype=F64, device=fr.planes.device)
+    call("mc_cov_f64", ptr(fr.planes), ptr(lm.wplanes), T, L, fr.npad, ptr(S), stream_ptr())
+    return S
+
+
+def cov_pairs(xplanes, aplanes, xi, ai, npad, w):
+    P = int(xi.shape[0]) if xi is not None else int(xplanes.shape[0])
+    S = torch.empty((P, 9), dtype=F64, device=xplanes.device)
+    call("mc_cov_pairs", ptr(xplanes), ptr(aplanes), ptr(xi), ptr(ai), P, npad, ptr(w), ptr(S), stream_ptr())
+    return S
+
+
+def fit_dense(S, gx, ga, rowmask=None, D=None, want_rot=True, want_quat=False, want_flags=True):
+    T, L = S.shape[0], S.shape[1]
+    dev = S.device
+    D = torch.empty((T, L), dtype=F64, device=dev) if D is None else D
+    rot = torch.empty((T, L, 9), dtype=F64, device=dev) if want_rot else None
+    quat = torch.empty((T, L, 4), dtype=F64, device=dev) if want_quat else None
+    flags = torch.zeros((T, L), dtype=U8, device=dev) if want_flags else None
+    call("mc_fit_dense", ptr(S), T, L, ptr(gx), ptr(ga), ptr(rowmask), ptr(D), ptr(rot), ptr(quat), ptr(flags),
+         stream_ptr())
+    return D, rot, quat, flags
+
+
+def fit_list_msd(S, xi, ai, gx, ga):
+    P = int(S.shape[0])
+    D = torch.empty((P,), dtype=F64, device=S.device)
+    call("mc_fit_list_msd", ptr(S), P, ptr(xi), ptr(ai), ptr(gx), ptr(ga), ptr(D), stream_ptr())
+    return D
+
+
+def fit_full(S, gx, ga, xi=None, ai=None):
+    P = int(S.shape[0])
+    dev = S.device
+    eig = torch.empty((P, 20), dtype=F64, device=dev)
+    quat = torch.empty((P, 4), dtype=F64, device=dev)
+    rot = torch.empty((P, 9), dtype=F64, device=dev)
+    flags = torch.empty((P,), dtype=U8, device=dev)
+    call("mc_fit_full", ptr(S), P, ptr(xi), ptr(ai), ptr(gx), ptr(ga), ptr(eig), ptr(quat), ptr(rot), ptr(flags),
+         stream_ptr())
+    return eig, quat, rot, flags
+
+
+def rot_grad(xplanes, aplanes, n, npad, w, eig, xi=None, ai=None):
+    P = int(eig.shape[0])
+    out = torch.empty((P, n, 3, 3, 3), dtype=F64, device=eig.device)
+    call("mc_rot_grad", ptr(xplanes), ptr(aplanes), ptr(xi), ptr(ai), P, n, npad, ptr(w), ptr(eig), ptr(out),
+         stream_ptr())
+    return out
+
+
+def jacobi4(mats):
+    mats = mats.contiguous()
+    B = int(mats.shape[0])
+    vals = torch.empty((B, 4), dtype=F64, device=mats.device)
+    vecs = torch.empty((B, 4, 4), dtype=F64, device=mats.device)
+    flags = torch.empty((B,), dtype=U8, device=mats.device)
+    call("mc_jacobi4", ptr(mats), B, ptr(vals), ptr(vecs), ptr(flags), stream_ptr())
+    return vals, vecs, flags
+
+
+def close_decisions(fr: Centred, w, eps, walkers, steps, window=8):
+    """Window fits + sequential scan + x<->y spectra.  Returns a dict of device tensors."""
+    dev = fr.planes.device
+    P = walkers * steps * window
+    xi = torch.empty((P,), dtype=I32, device=dev)
+    ai = torch.empty((P,), dtype=I32, device=dev)
+    call("mc_window_pairs", walkers, steps, window, ptr(xi), ptr(ai), stream_ptr())
+    Swin = cov_pairs(fr.planes, fr.planes, xi, ai, fr.npad, w)
+    dwin = fit_list_msd(Swin, xi, ai, fr.g, fr.g)
+    T = walkers * steps
+    refresh = torch.empty((T,), dtype=U8, device=dev)
+    ridx = torch.empty((T,), dtype=I32, device=dev)
+    dxy = torch.empty((T,), dtype=F64, device=dev)
+    fly = torch.zeros((walkers,), dtype=I32, device=dev)
+    call("mc_close_scan", ptr(fr.planes), ptr(fr.g), walkers, steps, fr.npad, ptr(w), ptr(dwin), window, float(eps),
+         ptr(refresh), ptr(ridx), ptr(dxy), ptr(fly), stream_ptr())
+    xyeig = torch.zeros((T, 20), dtype=F64, device=dev)
+    rxy = torch.empty((T, 9), dtype=F64, device=dev)
+    xyflags = torch.empty((T,), dtype=U8, device=dev)
+    call("mc_xy_eig", ptr(fr.planes), ptr(fr.g), T, fr.npad, ptr(w), ptr(refresh), ptr(ridx), ptr(xyeig), ptr(rxy),
+         ptr(xyflags), stream_ptr())
+    return {"refresh": refresh, "ridx": ridx, "dxy": dxy, "xyeig": xyeig, "rxy": rxy, "xyflags": xyflags,
+            "onthefly": fly}
+
+
+def pathcv_weights(D, q, lam, R, fr: Centred, lm: Centred, cap, cutoff=50.0, close=None, S=None):
+    T, L = D.shape
+    dev = D.device
+    s = torch.empty((T,), dtype=F64, device=dev)
+    z = torch.empty((T,), dtype=F64, device=dev)
+    sig_idx = torch.empty((T, cap), dtype=I32, device=dev)
+    sig_coef = torch.empty((T, cap, 18), dtype=F64, device=dev)
+    nsig = torch.empty((T,), dtype=I32, device=dev)
+    fvec = torch.empty((T, 16), dtype=F64, device=dev)
+    flags = torch.empty((T,), dtype=U8, device=dev)
+    c = close or {}
+    call("mc_pathcv_weights", T, L, float(lam), float(cutoff), cap, ptr(D), ptr(q), ptr(R), ptr(fr.wbar), ptr(lm.wbar),
+         ptr(c.get("refresh")), ptr(c.get("ridx")), ptr(S if close else None), ptr(c.get("rxy")), ptr(c.get("xyeig")),
+         ptr(fr.g if close else None), ptr(lm.g if close else None), ptr(lm.mom if close else None),
+         ptr(s), ptr(z), ptr(sig_idx), ptr(sig_coef), ptr(nsig), ptr(fvec), ptr(flags), stream_ptr())
+    return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags}
+
+
+def pathcv_grad(wres, fr: Centred, lm: Centred, w, w_align, cap, out_dtype=F64, close=None):
+    T, n = fr.count, fr.n
+    dev = fr.planes.device
+    ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
+    dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
+    c = close or {}
+    call("mc_pathcv_grad", T, n, fr.npad, cap, ptr(fr.planes), ptr(lm.planes), ptr(w), ptr(w_align),
+         ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(c.get("refresh")),
+         ptr(c.get("ridx")), ptr(c.get("xyeig")), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0,
+         stream_ptr())
+    return ds, dz

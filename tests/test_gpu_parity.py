@@ -1,0 +1,196 @@
+"""GPU parity: libmcb200 kernels vs the CPU oracle / reference golden vectors.
+
+Tolerances (north_star): MSD, s, z within 1e-6 relative (1e-9 absolute for
+near-identical pairs); gradients within 1e-5 relative; refresh decisions
+identical frame by frame.  The fp64 path is far tighter than that, and the
+asserts below say so explicitly where they are tighter.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1801_02362_b200 import engine, kernels as K, synth
+
+pytestmark = pytest.mark.gpu
+
+MSD_RTOL, MSD_ATOL = 1e-6, 1e-9
+GRAD_RTOL = 1e-5
+
+
+def assert_msd(got, ref, rtol=MSD_RTOL, atol=MSD_ATOL):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    err = np.abs(got - ref)
+    tol = np.maximum(rtol * np.abs(ref), atol)
+    bad = err > tol
+    assert not bad.any(), f"{bad.sum()} of {bad.size} outside tolerance; worst {err.max():.3e}"
+
+
+def assert_grad(got, ref, rtol=GRAD_RTOL):
+    got = np.asarray(got, dtype=float)
+    ref = np.asarray(ref, dtype=float)
+    # per-frame relative to that frame's largest gradient component
+    scale = np.abs(ref).reshape(ref.shape[0], -1).max(axis=1)
+    err = np.abs(got - ref).reshape(ref.shape[0], -1).max(axis=1)
+    assert np.all(err <= rtol * np.maximum(scale, 1e-300)), f"worst rel {np.max(err / np.maximum(scale, 1e-300)):.3e}"
+
+
+def _fits(golden):
+    g = golden("fits.npz")
+    for i in range(int(g["count"])):
+        yield {k.split("_", 1)[1]: g[k] for k in g.files if k.startswith(f"{i}_")}
+
+
+def test_fit_kernels_vs_reference_golden(golden, cuda_device):
+    for c in _fits(golden):
+        n = int(c["n"])
+        w = torch.zeros(K.npad_for(n), dtype=torch.float64, device=cuda_device)
+        w[:n] = torch.from_numpy(c["w"])
+        x = torch.from_numpy(c["xc"])[None].to(cuda_device)
+        a = torch.from_numpy(c["ac"])[None].to(cuda_device)
+        xc = K.center(x, None, w, recenter=False)
+        ac = K.center(a, None, w, recenter=False)
+        S = K.cov_pairs(xc.planes, ac.planes, None, None, xc.npad, w)
+        eig, quat, rot, flags = K.fit_full(S, xc.g, ac.g)
+        eig = eig.cpu().numpy()[0]
+        np.testing.assert_allclose(eig[:4], c["eigvals"], rtol=0, atol=1e-13)
+        np.testing.assert_allclose(rot.cpu().numpy()[0].reshape(3, 3), c["rot"], atol=1e-9)
+        if c["kind"] not in ("same", "rotated"):
+            np.testing.assert_allclose(quat.cpu().numpy()[0], c["quat"], atol=1e-10)
+        # fast path (Newton + adjugate)
+        D, R, Q, fl = K.fit_dense(S.reshape(1, 1, 9), xc.g, ac.g, want_quat=True)
+        assert_msd(D.cpu().numpy()[0, 0], c["eigvals"][0], rtol=1e-9, atol=1e-13)
+        np.testing.assert_allclose(R.cpu().numpy()[0, 0].reshape(3, 3), c["rot"], atol=1e-7)
+        if not bool(c["degenerate"]):
+            assert not (int(flags.item()) & 1)
+            rg = K.rot_grad(xc.planes, ac.planes, n, xc.npad, w, torch.from_numpy(eig[None]).to(cuda_device))
+            ref = c["rot_grad"]
+            scale = max(1.0, np.abs(ref).max())
+            np.testing.assert_allclose(rg.cpu().numpy()[0] / scale, ref / scale, atol=1e-9)
+
+
+def test_jacobi4_vs_reference_golden(golden, cuda_device):
+    g = golden("jacobi.npz")
+    vals, vecs, flags = K.jacobi4(torch.from_numpy(g["mats"].reshape(-1, 16)).to(cuda_device))
+    scale = np.maximum(1.0, np.abs(g["mats"]).max(axis=(1, 2)))[:, None]
+    np.testing.assert_allclose(vals.cpu().numpy() / scale, g["vals"] / scale, atol=1e-13)
+    np.testing.assert_allclose(vecs.cpu().numpy(), g["vecs"], atol=1e-9)
+    assert int(flags.max()) == 0
+
+
+def test_msd_matrix_config0_and_config1_slice(cuda_device):
+    wl = synth.config0()
+    D = engine.msd_matrix(torch.from_numpy(wl.frames).to(cuda_device), wl.landmarks).cpu().numpy()
+    assert_msd(D, O.batch_msd_matrix(wl.frames, wl.landmarks))
+    wl1 = synth.config1(T=300, L=120)
+    D = engine.msd_matrix(wl1.frames, wl1.landmarks).cpu().numpy()
+    assert_msd(D, O.batch_msd_matrix(wl1.frames, wl1.landmarks))
+
+
+def test_msd_matrix_weights_and_fp32_inputs(cuda_device):
+    rng = np.random.default_rng(3)
+    n = 37
+    w = rng.uniform(0.1, 1.0, n)
+    wa = rng.uniform(0.1, 1.0, n)
+    wl = synth.config0(seed=5, T=50, L=30, N=n)
+    D = engine.msd_matrix(wl.frames, wl.landmarks, w=w, w_align=wa).cpu().numpy()
+    assert_msd(D, O.batch_msd_matrix(wl.frames, wl.landmarks, w=w, w_align=wa))
+    f32 = wl.frames.astype(np.float32)
+    l32 = wl.landmarks.astype(np.float32)
+    D = engine.msd_matrix(f32, l32).cpu().numpy()
+    assert_msd(D, O.batch_msd_matrix(f32.astype(float), l32.astype(float)))
+
+
+def test_path_cv_config0_full(cuda_device):
+    wl = synth.config0()
+    out = engine.path_cv(wl.frames, wl.landmarks, wl.lam)
+    ref = O.batch_path_cv_exact(wl.frames, wl.landmarks, wl.lam)
+    assert_msd(out["D"].cpu().numpy(), ref["D"])
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    assert_grad(out["ds"].cpu().numpy(), ref["ds"])
+    assert_grad(out["dz"].cpu().numpy(), ref["dz"])
+
+
+def test_path_cv_vs_per_pair_oracle_with_rot_term(golden, cuda_device):
+    """Against the literal Eq. 4 oracle (dR term included) on reference-fit slices."""
+    g = golden("pathcv0.npz")
+    out = engine.path_cv(g["frames"], g["landmarks"], float(g["lam"]))
+    ref = O.path_cv_exact(g["frames"], g["landmarks"], float(g["lam"]))
+    assert_msd(out["D"].cpu().numpy(), g["D"])
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    assert_grad(out["ds"].cpu().numpy(), ref["ds"])
+    assert_grad(out["dz"].cpu().numpy(), ref["dz"])
+
+
+def test_path_cv_weighted(cuda_device):
+    rng = np.random.default_rng(4)
+    n = 9
+    w = rng.uniform(0.1, 1.0, n)
+    wa = rng.uniform(0.1, 1.0, n)
+    wl = synth.config0(seed=6, T=6, L=8, N=n)
+    out = engine.path_cv(wl.frames, wl.landmarks, wl.lam, w=w, w_align=wa)
+    ref = O.path_cv_exact(wl.frames, wl.landmarks, wl.lam, w=w, w_align=wa)
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    assert_grad(out["ds"].cpu().numpy(), ref["ds"])
+    assert_grad(out["dz"].cpu().numpy(), ref["dz"])
+
+
+def test_close_replay_vs_reference_run(golden, cuda_device):
+    g = golden("close.npz")
+    out = engine.close_structure_replay(g["frames"], g["landmarks"], 100.0, float(g["eps"]))
+    np.testing.assert_array_equal(out["refresh"].cpu().numpy(), g["refresh"])
+    assert_msd(out["dxy"].cpu().numpy(), g["dxy"])
+    assert_msd(out["D"].cpu().numpy(), g["D"])
+
+
+def test_close_replay_gradients_vs_oracle(cuda_device):
+    g_wl = synth.config0(seed=8, T=40, L=10, N=12)
+    # small eps so that both refresh and approximate frames occur
+    frames = g_wl.frames.copy()
+    rng = np.random.default_rng(1)
+    base = frames[0] - frames[0].mean(0)
+    for t in range(frames.shape[0]):
+        frames[t] = base + np.cumsum(rng.normal(0, 0.002, size=(t + 1, 12, 3)), axis=0)[-1]
+    frames = synth.rigid_motion(rng, frames)
+    eps = 3e-4
+    lam = 50.0
+    ref = O.close_structure_replay(frames, g_wl.landmarks, lam, eps)
+    assert 0 < ref["refresh"].sum() < len(ref["refresh"])
+    out = engine.close_structure_replay(frames, g_wl.landmarks, lam, eps)
+    np.testing.assert_array_equal(out["refresh"].cpu().numpy(), ref["refresh"])
+    assert_msd(out["dxy"].cpu().numpy(), ref["dxy"])
+    assert_msd(out["D"].cpu().numpy(), ref["D"])
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    assert_grad(out["ds"].cpu().numpy(), ref["ds"])
+    assert_grad(out["dz"].cpu().numpy(), ref["dz"])
+
+
+def test_close_replay_config1_slice_decisions(cuda_device):
+    wl = synth.config1(T=400, L=60)
+    ref = O.close_structure_replay(wl.frames, wl.landmarks, wl.lam, wl.eps, grad=False)
+    out = engine.close_structure_replay(wl.frames, wl.landmarks, wl.lam, wl.eps, grad=False)
+    np.testing.assert_array_equal(out["refresh"].cpu().numpy(), ref["refresh"])
+    assert_msd(out["dxy"].cpu().numpy(), ref["dxy"])
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    # and with a large eps, so most frames take the approximate path
+    eps = 50 * wl.eps
+    ref = O.close_structure_replay(wl.frames[:120], wl.landmarks, wl.lam, eps, grad=False)
+    out = engine.close_structure_replay(wl.frames[:120], wl.landmarks, wl.lam, eps, grad=False)
+    np.testing.assert_array_equal(out["refresh"].cpu().numpy(), ref["refresh"])
+    assert ref["refresh"].sum() < 100
+    assert_msd(out["D"].cpu().numpy(), ref["D"])
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+
+
+def test_eps_zero_equals_exact(cuda_device):
+    wl = synth.config0(seed=2, T=30, L=12, N=15)
+    ex = engine.path_cv(wl.frames, wl.landmarks, wl.lam)
+    cl = engine.close_structure_replay(wl.frames, wl.landmarks, wl.lam, 0.0)
+    assert bool(cl["refresh"].all())
+    np.testing.assert_allclose(cl["s"].cpu().numpy(), ex["s"].cpu().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(cl["ds"].cpu().numpy(), ex["ds"].cpu().numpy(), atol=1e-14)
