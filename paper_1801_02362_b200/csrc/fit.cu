@@ -176,7 +176,7 @@ rot_grad_kernel(const double* __restrict__ xpl, const double* __restrict__ apl, 
 #pragma unroll
     for (int al = 0; al < 3; ++al) coef[m][al] = c[al] * inv[m];
   }
-  double* o = out + ((int64_t)p * n + k) * 81;
+  double* o = out + ((int64_t)p * n + k) * 27;
 #pragma unroll
   for (int al = 0; al < 3; ++al) {
     double dq[4];
@@ -184,7 +184,7 @@ rot_grad_kernel(const double* __restrict__ xpl, const double* __restrict__ apl, 
     for (int r = 0; r < 4; ++r) dq[r] = coef[0][al] * qm[0][r] + coef[1][al] * qm[1][r] + coef[2][al] * qm[2][r];
 #pragma unroll
     for (int bg = 0; bg < 9; ++bg)
-      o[al * 27 + bg] = dq[0] * J[0][bg] + dq[1] * J[1][bg] + dq[2] * J[2][bg] + dq[3] * J[3][bg];
+      o[al * 9 + bg] =dq[0] * J[0][bg] + dq[1] * J[1][bg] + dq[2] * J[2][bg] + dq[3] * J[3][bg];
   }
 }
 
