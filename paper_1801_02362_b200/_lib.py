@@ -113,9 +113,46 @@ def check(status, what=""):
     raise DeviceError(f"{what}: status {status}")
 
 
+COUNTERS = {"launches": 0}
+_PROFILE = None  # list of (name, start_event, end_event) while profiling
+
+
+def start_profile():
+    global _PROFILE
+    _PROFILE = []
+
+
+def stop_profile():
+    """Stop recording; returns {name: (count, total_ms)} (synchronises)."""
+    global _PROFILE
+    import torch
+
+    rec, _PROFILE = _PROFILE, None
+    torch.cuda.synchronize()
+    out = {}
+    for name, e0, e1 in rec or []:
+        c, t = out.get(name, (0, 0.0))
+        out[name] = (c + 1, t + e0.elapsed_time(e1))
+    return out
+
+
 def call(name, *args):
+    """Invoke one C entry point (each launches exactly one kernel)."""
     lib = load()
-    check(getattr(lib, name)(*args), name)
+    fn = getattr(lib, name)
+    COUNTERS["launches"] += 1
+    if _PROFILE is not None:
+        import torch
+
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = fn(*args)
+        e1.record()
+        _PROFILE.append((name, e0, e1))
+    else:
+        st = fn(*args)
+    check(st, name)
 
 
 def ptr(t):
