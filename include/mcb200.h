@@ -130,6 +130,24 @@ int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
                    const double* xyeig, void* ds, void* dz, int32_t out_f32, void* stream);
 
+/* Per-pair DistanceResult gradients of the reference-facing API:
+ * exact_distance (Eq. 3/4) and approx_distance (Eq. 5/6,
+ * SPEC.md:124-132).  Pair p = (frame xi[p], reference ai[p]) with rotation rot[p]
+ * (exact: R_{a x}; approximate: the saved R_{a y}).  approx[p] != 0 selects Eq. 5/6
+ * with close structure yi[p] (a frame index), S[p] = cov(x, a), amom = reference
+ * second moments, xyeig/rxy = x<->y fit; value[p] receives Eq. 5 on those pairs.
+ * grad [P, n, 3] w.r.t. the raw (uncentred) frame coordinates. */
+int mc_pair_grad(int64_t P, int32_t n, int32_t npad, const double* xplanes, const double* aplanes, const int32_t* xi,
+                 const int32_t* ai, const double* rot, const double* w, const double* w_align, const double* xwbar,
+                 const double* awbar, const int32_t* approx, const int32_t* yi, const double* S, const double* amom,
+                 const double* xyeig, const double* rxy, const double* gx, const double* ga, double* value,
+                 double* grad, void* stream);
+
+/* property_map over supplied distances D [L] (+ grads [L,n,3]):
+ * out[0] = s, out[1] = z; ds, dz [n,3] when grads != NULL. */
+int mc_property_map(int32_t L, int32_t n, const double* D, const double* grads, const double* q, double lam,
+                    double* out, double* ds, double* dz, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,9 @@ _SIGS = {
     "mc_pathcv_weights": [_I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P, _P, _P, _P, _P, _P, _P],
     "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
+    "mc_pair_grad": [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                     _P, _P],
+    "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],
 }
 
 # optional entry points (present once the tensor path is built)

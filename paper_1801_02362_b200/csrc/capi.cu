@@ -118,4 +118,24 @@ int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double
                                         refresh, ridx, xyeig, ds, dz, out_f32, S_(stream)));
 }
 
+int mc_pair_grad(int64_t P, int32_t n, int32_t npad, const double* xplanes, const double* aplanes, const int32_t* xi,
+                 const int32_t* ai, const double* rot, const double* w, const double* w_align, const double* xwbar,
+                 const double* awbar, const int32_t* approx, const int32_t* yi, const double* S, const double* amom,
+                 const double* xyeig, const double* rxy, const double* gx, const double* ga, double* value,
+                 double* grad, void* stream) {
+  if (P < 0 || bad_pad(n, npad)) return MC_ERR_CONFIG;
+  if (P > 0 && (!xplanes || !aplanes || !xi || !ai || !rot || !w || !w_align || !xwbar || !awbar || !grad))
+    return MC_ERR_CONFIG;
+  if (approx && (!yi || !S || !amom || !xyeig || !rxy || !gx || !ga || !value)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_pair_grad(P, n, npad, xplanes, aplanes, xi, ai, rot, w, w_align, xwbar, awbar, approx,
+                                          yi, S, amom, xyeig, rxy, gx, ga, value, grad, S_(stream)));
+}
+
+int mc_property_map(int32_t L, int32_t n, const double* D, const double* grads, const double* q, double lam,
+                    double* out, double* ds, double* dz, void* stream) {
+  if (L < 1) return MC_ERR_EMPTY_ACTIVE_SET;
+  if (!(lam > 0.0) || !D || !q || !out || (grads && (n < 1 || !ds || !dz))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_property_map(L, n, D, grads, q, lam, out, ds, dz, S_(stream)));
+}
+
 }  // extern "C"

@@ -40,4 +40,11 @@ cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, c
                            const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
                            void* ds, void* dz, int out_f32, cudaStream_t stream);
+cudaError_t launch_pair_grad(int64_t P, int n, int npad, const double* xpl, const double* apl, const int* xi,
+                             const int* ai, const double* rot, const double* w, const double* wa, const double* xwbar,
+                             const double* awbar, const int* approx, const int* yi, const double* S,
+                             const double* amom, const double* xyeig, const double* rxy, const double* gx,
+                             const double* ga, double* value, double* grad, cudaStream_t stream);
+cudaError_t launch_property_map(int L, int n, const double* D, const double* grads, const double* q, double lam,
+                                double* out, double* ds, double* dz, cudaStream_t stream);
 }  // namespace mc
