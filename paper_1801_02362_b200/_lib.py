@@ -60,8 +60,8 @@ _SIGS = {
 
 # optional entry points (present once the tensor path is built)
 _OPTIONAL = {
-    "mc_center_split": [_P, _I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "mc_msd_tf32": [_P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P],
+    "mc_center_split": [_P, ctypes.c_int, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
+    "mc_msd_tf32": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P],
     "mc_refine_pairs": [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P],
     "mc_candidates": [_P, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P],
     "mc_pathcv_weights_sparse": [_I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

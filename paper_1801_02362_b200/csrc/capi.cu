@@ -138,4 +138,24 @@ int mc_property_map(int32_t L, int32_t n, const double* D, const double* grads, 
   return cuda_status(mc::launch_property_map(L, n, D, grads, q, lam, out, ds, dz, S_(stream)));
 }
 
+int mc_center_split(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
+                    const double* w_disp, int32_t weighted, float* hi, float* lo, double* centroid, double* gnorm,
+                    double* wbar, double* mom, uint8_t* flags, void* stream) {
+  if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
+  if (n < 2) return MC_ERR_INVALID_STRUCTURE;
+  if (count < 0 || kpad < n || kpad % 16 != 0) return MC_ERR_CONFIG;
+  if (count > 0 && (!coords || !w_align || !w_disp || !hi || !lo || !gnorm)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_center_split(coords, dtype, count, n, kpad, w_align, w_disp, weighted, hi, lo, centroid,
+                                             gnorm, wbar, mom, flags, S_(stream)));
+}
+
+int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const float* llo, const double* gx,
+                const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+                void* stream) {
+  if (T < 0 || L < 0 || kpad % 16 != 0 || kpad < 16 || ldd < L) return MC_ERR_CONFIG;
+  if ((int64_t)T * L > 0 && (!fhi || !flo || !lhi || !llo || !gx || !ga || !D)) return MC_ERR_CONFIG;
+  if (3LL * T > 0x7fffffffLL || 3LL * L > 0x7fffffffLL) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_msd_tf32(fhi, flo, lhi, llo, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
+}
+
 }  // extern "C"

@@ -47,4 +47,10 @@ cudaError_t launch_pair_grad(int64_t P, int n, int npad, const double* xpl, cons
                              const double* ga, double* value, double* grad, cudaStream_t stream);
 cudaError_t launch_property_map(int L, int n, const double* D, const double* grads, const double* q, double lam,
                                 double* out, double* ds, double* dz, cudaStream_t stream);
+cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
+                                const double* w_disp, int weighted, float* hi, float* lo, double* centroid,
+                                double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream);
+cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
+                            const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                            cudaStream_t stream);
 }  // namespace mc

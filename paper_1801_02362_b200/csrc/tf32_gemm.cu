@@ -1,0 +1,422 @@
+// K1s + K2/K3 — fp32-coordinate path (configs 2/3/4).
+//
+// K1s  center_split_kernel: centre each structure in fp64 (geometry.py:67-76),
+//      optionally fold the displacement weights w_j into the operand, and
+//      split every centred coordinate v into two TF32 values hi + lo
+//      (hi = rna_tf32(v), lo = rna_tf32(v - hi)), written plane-major
+//      [3][B][kpad] fp32 so each plane of a structure tile is one TMA box.
+//
+// K2   msd_tf32_kernel: the all-pairs 3x3 covariance
+//        S[t,l][b][g] = sum_j x_{t,j,b} (w_j a_{l,j,g})
+//      as a dense contraction on the 5th-gen tensor cores with the 3xTF32
+//      scheme (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM), and
+// K3   fused into its epilogue: Horn's lambda_max by fp64 Newton and the MSD
+//      estimate D = Gx + Ga - 2 lambda_max (mc_math.cuh), written as fp32.
+//
+// Tile: 128 frames (TMEM lanes) x 48 landmarks.  For every frame plane b a
+// separate accumulator D_b[128 x 144] holds columns (g, l) = g*48 + l, so
+// the 9 entries S[b][g] of a pair live in the SAME TMEM lane and one
+// epilogue thread owns whole pairs (no cross-lane shuffles, no padding of
+// the 3-row structure to 4).  Per 8-atom k-step: 3 planes x 3 split terms
+// = 9 tcgen05.mma (M=128, N=144, K=8, kind::tf32), A = frame plane tile,
+// B = the 3 landmark planes stacked (144 rows).  Operands stream through a
+// 3-stage TMA (SWIZZLE_64B, 16 atoms per stage) -> smem -> UMMA pipeline.
+// Warp roles (256 threads, persistent over tiles, landmark tiles fastest so
+// the landmark operand stays L2-resident while a frame tile is in use):
+//   warp 0: TMA producer   warp 1: MMA issuer (one elected lane)
+//   warp 2: TMEM allocator warps 4-7: epilogue (TMEM lane quarter = warp%4)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "mc_math.cuh"
+
+namespace mc {
+
+// ------------------------------------------------------------------ K1s
+__device__ __forceinline__ float tf32_rna(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT)
+center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, const double* __restrict__ w_align,
+                    const double* __restrict__ w_disp, int weighted, float* __restrict__ hi, float* __restrict__ lo,
+                    double* __restrict__ centroid, double* __restrict__ gnorm, double* __restrict__ wbar,
+                    double* __restrict__ mom, uint8_t* __restrict__ flags) {
+  __shared__ double scratch[NT / 32];
+  const int64_t b = blockIdx.x;
+  const T* x = coords + b * (int64_t)n * 3;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  bool finite = true;
+  for (int j = threadIdx.x; j < n; j += NT) {
+    const double wa = w_align[j];
+    const double x0 = (double)x[3 * j], x1 = (double)x[3 * j + 1], x2 = (double)x[3 * j + 2];
+    finite = finite && isfinite(x0) && isfinite(x1) && isfinite(x2);
+    c0 += wa * x0; c1 += wa * x1; c2 += wa * x2;
+  }
+  c0 = block_sum<NT>(c0, scratch);
+  c1 = block_sum<NT>(c1, scratch);
+  c2 = block_sum<NT>(c2, scratch);
+  const int nonfinite = __syncthreads_or(!finite);
+  double g = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, m00 = 0, m01 = 0, m02 = 0, m11 = 0, m12 = 0, m22 = 0;
+  const int64_t plane = B * (int64_t)kpad;
+  for (int j = threadIdx.x; j < kpad; j += NT) {
+    double v[3] = {0.0, 0.0, 0.0};
+    double w = 0.0;
+    if (j < n) {
+      w = w_disp[j];
+      v[0] = (double)x[3 * j] - c0;
+      v[1] = (double)x[3 * j + 1] - c1;
+      v[2] = (double)x[3 * j + 2] - c2;
+    }
+    const double wx0 = w * v[0], wx1 = w * v[1], wx2 = w * v[2];
+    g += wx0 * v[0] + wx1 * v[1] + wx2 * v[2];
+    b0 += wx0; b1 += wx1; b2 += wx2;
+    m00 += wx0 * v[0]; m01 += wx0 * v[1]; m02 += wx0 * v[2];
+    m11 += wx1 * v[1]; m12 += wx1 * v[2]; m22 += wx2 * v[2];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const double val = weighted ? w * v[p] : v[p];
+      const float h = tf32_rna((float)val);
+      const float l = tf32_rna((float)(val - (double)h));
+      hi[p * plane + b * kpad + j] = h;
+      lo[p * plane + b * kpad + j] = l;
+    }
+  }
+  g = block_sum<NT>(g, scratch);
+  if (wbar) { b0 = block_sum<NT>(b0, scratch); b1 = block_sum<NT>(b1, scratch); b2 = block_sum<NT>(b2, scratch); }
+  if (mom) {
+    m00 = block_sum<NT>(m00, scratch); m01 = block_sum<NT>(m01, scratch); m02 = block_sum<NT>(m02, scratch);
+    m11 = block_sum<NT>(m11, scratch); m12 = block_sum<NT>(m12, scratch); m22 = block_sum<NT>(m22, scratch);
+  }
+  if (threadIdx.x == 0) {
+    if (centroid) { centroid[3 * b] = c0; centroid[3 * b + 1] = c1; centroid[3 * b + 2] = c2; }
+    gnorm[b] = g;
+    if (wbar) { wbar[3 * b] = b0; wbar[3 * b + 1] = b1; wbar[3 * b + 2] = b2; }
+    if (mom) {
+      mom[6 * b] = m00; mom[6 * b + 1] = m01; mom[6 * b + 2] = m02;
+      mom[6 * b + 3] = m11; mom[6 * b + 4] = m12; mom[6 * b + 5] = m22;
+    }
+    if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
+  }
+}
+
+cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
+                                const double* w_disp, int weighted, float* hi, float* lo, double* centroid,
+                                double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream) {
+  if (B <= 0) return cudaSuccess;
+  if (dtype == 0)
+    center_split_kernel<float, 256><<<(unsigned)B, 256, 0, stream>>>((const float*)coords, B, n, kpad, w_align,
+                                                                     w_disp, weighted, hi, lo, centroid, gnorm, wbar,
+                                                                     mom, flags);
+  else
+    center_split_kernel<double, 256><<<(unsigned)B, 256, 0, stream>>>((const double*)coords, B, n, kpad, w_align,
+                                                                      w_disp, weighted, hi, lo, centroid, gnorm, wbar,
+                                                                      mom, flags);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K2/K3
+namespace gemm {
+constexpr int BM = 128;            // frames per tile (TMEM lanes)
+constexpr int BL = 48;             // landmarks per tile
+constexpr int BN = 3 * BL;         // 144 accumulator columns per frame plane
+constexpr int KB = 16;             // atoms per pipeline stage (64 B rows, SWIZZLE_64B)
+constexpr int STAGES = 3;
+constexpr int A_BYTES = BM * KB * 4;        // 8 KB: one (plane, hi|lo) frame tile
+constexpr int B_BYTES = BN * KB * 4;        // 9 KB: hi or lo, 3 landmark planes stacked
+constexpr int BP_BYTES = BL * KB * 4;       // 3 KB: one landmark plane box
+constexpr int STAGE_BYTES = 6 * A_BYTES + 2 * B_BYTES;  // 66 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int TMEM_COLS = 512;
+constexpr int NT = 256;
+// instruction descriptor: D=F32 (bits 4-5 = 1), A=B=TF32 (2), K-major, N>>3, M>>4
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}  // namespace gemm
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// SM100 UMMA shared-memory descriptor, K-major, SWIZZLE_64B (64 B rows,
+// 8-row groups 512 B apart): start>>4 | LBO=1 | SBO=32 | version 1 | layout 4
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(gemm::IDESC), "r"(accum));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// MSD estimate from an fp32 covariance (fp64 finalisation)
+__device__ __forceinline__ double msd_from_S32(const float* s, double gx, double ga) {
+  double S[9];
+#pragma unroll
+  for (int e = 0; e < 9; ++e) S[e] = (double)s[e];
+  const Sym4 n = horn(S);
+  return gx + ga - 2.0 * newton_lmax(n, 0.5 * (gx + ga));
+}
+
+__global__ void __launch_bounds__(gemm::NT, 1)
+msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__ CUtensorMap mfl,
+                const __grid_constant__ CUtensorMap mlh, const __grid_constant__ CUtensorMap mll,
+                const double* __restrict__ gx, const double* __restrict__ ga, int T, int L, int kpad,
+                float* __restrict__ D, int64_t ldd) {
+  using namespace gemm;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntm = (T + BM - 1) / BM, ntl = (L + BL - 1) / BL;
+  const int ntiles = ntm * ntl;
+  const int nkb = kpad / KB;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mfh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mfl)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mlh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mll)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tm = tile / ntl, tl = tile - tm * ntl;
+        const int t0 = tm * BM, l0 = tl * BL;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = kb * KB;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            tma_load_2d(&mfh, &full[stage], st + (2 * p) * A_BYTES, k0, p * T + t0);
+            tma_load_2d(&mfl, &full[stage], st + (2 * p + 1) * A_BYTES, k0, p * T + t0);
+          }
+          uint8_t* bh = st + 6 * A_BYTES;
+          uint8_t* bl = bh + B_BYTES;
+#pragma unroll
+          for (int g = 0; g < 3; ++g) {
+            tma_load_2d(&mlh, &full[stage], bh + g * BP_BYTES, k0, g * L + l0);
+            tma_load_2d(&mll, &full[stage], bl + g * BP_BYTES, k0, g * L + l0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      mbar_wait(tempty, (it & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t bh = st + 6 * A_BYTES, bl = bh + B_BYTES;
+#pragma unroll
+          for (int k = 0; k < KB / 8; ++k) {
+            const uint32_t koff = k * 32;  // 8 tf32 = 32 B inside the 64 B swizzled row
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+              const uint32_t d = tmem_base + p * BN;
+              const uint64_t ah = umma_desc_sw64(st + (2 * p) * A_BYTES + koff);
+              const uint64_t al = umma_desc_sw64(st + (2 * p + 1) * A_BYTES + koff);
+              const uint64_t dbh = umma_desc_sw64(bh + koff);
+              const uint64_t dbl = umma_desc_sw64(bl + koff);
+              umma_tf32(d, ah, dbh, (kb | k) != 0);
+              umma_tf32(d, ah, dbl, 1u);
+              umma_tf32(d, al, dbh, 1u);
+            }
+          }
+          umma_commit(&empty[stage]);
+          if (kb == nkb - 1) umma_commit(tfull);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: lane = frame, whole 3x3 blocks per thread
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int tm = tile / ntl, tl = tile - tm * ntl;
+      const int t = tm * BM + row;
+      const int l0 = tl * BL;
+      mbar_wait(tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const double gxt = t < T ? gx[t] : 0.0;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BL / 8; ++c) {
+        float v[9][8];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int g = 0; g < 3; ++g) tmem_ld8(lane_base + p * BN + g * BL + c * 8, v[p * 3 + g]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (t < T) {
+          float out[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int l = l0 + c * 8 + i;
+            float s[9];
+#pragma unroll
+            for (int e = 0; e < 9; ++e) s[e] = v[e][i];
+            out[i] = l < L ? (float)msd_from_S32(s, gxt, ga[l]) : 0.0f;
+          }
+          float* dst = D + (int64_t)t * ldd + l0 + c * 8;
+          if (l0 + c * 8 + 8 <= L && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(out[4], out[5], out[6], out[7]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (l0 + c * 8 + i < L) dst[i] = out[i];
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(gemm::TMEM_COLS));
+  }
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int kpad, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kpad * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)gemm::KB, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
+                            const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                            cudaStream_t stream) {
+  using namespace gemm;
+  if (T <= 0 || L <= 0) return cudaSuccess;
+  CUtensorMap mfh, mfl, mlh, mll;
+  if (!make_map(&mfh, fh, 3LL * T, kpad, BM) || !make_map(&mfl, fl, 3LL * T, kpad, BM) ||
+      !make_map(&mlh, lh, 3LL * L, kpad, BL) || !make_map(&mll, ll, 3LL * L, kpad, BL))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(msd_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ntiles = ((T + BM - 1) / BM) * ((L + BL - 1) / BL);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int g = grid > 0 ? grid : (ntiles < nsm ? ntiles : nsm);
+  msd_tf32_kernel<<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, T, L, kpad, D, ldd);
+  return cudaGetLastError();
+}
+
+}  // namespace mc

@@ -180,3 +180,49 @@ def pathcv_grad(wres, fr: Centred, lm: Centred, w, w_align, cap, out_dtype=F64, 
          ptr(c.get("ridx")), ptr(c.get("xyeig")), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0,
          stream_ptr())
     return ds, dz
+
+
+# ---------------------------------------------------------------- fp32 / tensor-core path
+
+def kpad_for(n):
+    return ((int(n) + 15) // 16) * 16
+
+
+class Split:
+    """TF32 hi/lo plane-major operands [3, B, kpad] + per-structure scalars."""
+
+    __slots__ = ("hi", "lo", "centroid", "g", "wbar", "mom", "flags", "n", "kpad", "count")
+
+    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad):
+        self.hi, self.lo, self.centroid, self.g, self.wbar, self.mom, self.flags = hi, lo, centroid, g, wbar, mom, flags
+        self.n, self.kpad, self.count = n, kpad, hi.shape[1]
+
+
+def center_split(coords, w_align, w_disp, weighted, moments=False):
+    """K1s: centre, optionally fold w into the operand, split into TF32 hi/lo planes."""
+    require_cuda(coords)
+    coords = coords.contiguous()
+    b, n, _ = coords.shape
+    kpad = kpad_for(n)
+    dev = coords.device
+    dt = _lib.MC_F64 if coords.dtype == torch.float64 else _lib.MC_F32
+    hi = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
+    lo = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
+    centroid = torch.empty((b, 3), dtype=F64, device=dev)
+    g = torch.empty((b,), dtype=F64, device=dev)
+    wbar = torch.empty((b, 3), dtype=F64, device=dev)
+    mom = torch.empty((b, 6), dtype=F64, device=dev) if moments else None
+    flags = torch.empty((b,), dtype=U8, device=dev)
+    call("mc_center_split", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0, ptr(hi),
+         ptr(lo), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
+    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad)
+
+
+def msd_tf32(fr: Split, lm: Split, D=None, grid=0):
+    """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L])."""
+    T, L = fr.count, lm.count
+    if D is None:
+        D = torch.empty((T, L), dtype=torch.float32, device=fr.hi.device)
+    call("mc_msd_tf32", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo), ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D),
+         D.stride(0), grid, stream_ptr())
+    return D

@@ -1,0 +1,47 @@
+"""GPU tests of the tcgen05 3xTF32 covariance + fused MSD estimate (K1s/K2/K3)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1801_02362_b200 import engine, kernels as K, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _estimate(frames, landmarks, w=None, wa=None):
+    dev = torch.device("cuda:0")
+    fr = torch.as_tensor(frames).to(dev)
+    lm = torch.as_tensor(landmarks).to(dev)
+    n = fr.shape[1]
+    wv = engine.normalise_weights(w, n, "d", dev)
+    wav = engine.normalise_weights(wa, n, "a", dev)
+    fs = K.center_split(fr, wav, wv, weighted=False)
+    ls = K.center_split(lm, wav, wv, weighted=True)
+    D = K.msd_tf32(fs, ls)
+    torch.cuda.synchronize()
+    return D.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("T,L,n", [(128, 48, 16), (300, 100, 100), (257, 97, 1000)])
+def test_tf32_estimate_close_to_exact(T, L, n, cuda_device):
+    wl = synth.config2(seed=7, T=T, L=L, N=n)
+    est = _estimate(wl.frames, wl.landmarks)
+    ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64))
+    err = np.abs(est - ref)
+    print(f"T={T} L={L} n={n}: max abs err {err.max():.3e}, median {np.median(err):.3e}, "
+          f"max rel err (D>0.2) {np.max(err[ref > 0.2] / ref[ref > 0.2]) if (ref > 0.2).any() else 0:.3e}")
+    # 3xTF32 + fp32 accumulation: absolute error well below 1e-5 (the refinement
+    # threshold in engine.py is derived from this bound)
+    assert err.max() < 5e-6 * max(1.0, n / 1000) ** 0.5 + 2e-6
+
+
+def test_tf32_weighted(cuda_device):
+    rng = np.random.default_rng(2)
+    n = 77
+    w, wa = rng.uniform(0.1, 1, n), rng.uniform(0.1, 1, n)
+    wl = synth.config2(seed=8, T=130, L=50, N=n)
+    est = _estimate(wl.frames, wl.landmarks, w, wa)
+    ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), w=w, w_align=wa)
+    assert np.abs(est - ref).max() < 5e-6
