@@ -118,17 +118,49 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
  * mc_pathcv_weights: per frame — min/LSE, s, z, significant-landmark list
  *   (sig_idx [T,cap], sig_coef [T,cap,18]), nsig [T], fvec [T,16]; writes the
  *   Eq. 5 distances of non-refresh rows into D.  refresh == NULL: all rows exact.
- * mc_pathcv_grad: one pass over atoms writing ds, dz [T, n, 3] (fp64, or fp32 if out_f32). */
-int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, double* D, const double* q,
-                      const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
-                      const int32_t* ridx, const double* S, const double* rxy, const double* xyeig,
-                      const double* gx, const double* ga, const double* lmom, double* s, double* z,
-                      int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec, uint8_t* flags,
-                      void* stream);
+ *   Rows are dense (ld = L, rowlo = rowcnt = NULL) or sparse windows: row t of
+ *   D/R (stride ld) holds landmarks rowlo[t] .. rowlo[t]+rowcnt[t]-1 (the
+ *   refined candidates of the tensor-core path; landmarks outside a window
+ *   have lam (D - D_min) > cutoff and weight < e^-cutoff).
+ * mc_pathcv_grad: one pass over atoms writing ds, dz [T, n, 3] (fp64, or fp32 if
+ *   out_f32).  Coordinates from centred fp64 planes, or (fplanes/lplanes NULL)
+ *   from raw fp32 AoS input + fp64 centroids. */
+int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
+                      const int32_t* rowcnt, double* D, const double* q, const double* R, const double* fwbar,
+                      const double* lwbar, const uint8_t* refresh, const int32_t* ridx, const double* S,
+                      const double* rxy, const double* xyeig, const double* gx, const double* ga, const double* lmom,
+                      double* s, double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec,
+                      uint8_t* flags, void* stream);
 int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
-                   const double* xyeig, void* ds, void* dz, int32_t out_f32, void* stream);
+                   const double* xyeig, void* ds, void* dz, int32_t out_f32, const float* fraw, const double* fcen,
+                   const float* lraw, const double* lcen, void* stream);
+
+/* ---- fp32-coordinate path (configs 2-4): tensor-core estimate + exact refinement ----
+ * mc_center_split (K1s, geometry.py:67-76 + operand prep): centre in fp64, optionally
+ *   fold w into the operand (weighted), split into TF32 hi/lo planes [3, count, kpad]
+ *   (kpad % 16 == 0); G, centroid, wbar, mom as mc_center.
+ * mc_msd_tf32 (K2+K3, _kearsley_matrix + eigvals[0] of geometry.py:180-249): all-pairs
+ *   3x3 covariance on tcgen05 (3xTF32, TMEM accumulators, TMA pipeline) with the
+ *   fp64 Newton lambda_max in the epilogue -> MSD estimate D [T, ldd] fp32.  grid 0 = #SMs.
+ * mc_candidates: per frame D_min and the landmark window {lam (D - D_min) <= thr}.
+ * mc_sort_by_key: counting sort of frames by window start (workspace bins [nbins]).
+ * mc_refine: exact fp64 covariance + fit of the in-window pairs (or, with lo = cnt =
+ *   NULL, of all pairs: the dense exact MSD matrix into Dd). */
+int mc_center_split(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
+                    const double* w_disp, int32_t weighted, float* hi, float* lo, double* centroid, double* gnorm,
+                    double* wbar, double* mom, uint8_t* flags, void* stream);
+int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const float* llo, const double* gx,
+                const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+                void* stream);
+int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
+                  int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
+int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream);
+int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
+              const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
+              const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
+              float* Dd, int64_t ldd, uint8_t* flags, void* stream);
 
 /* Per-pair DistanceResult gradients of the reference-facing API:
  * exact_distance (Eq. 3/4) and approx_distance (Eq. 5/6,

@@ -50,23 +50,22 @@ _SIGS = {
     "mc_window_pairs": [_I32, _I32, _I32, _P, _P, _P],
     "mc_close_scan": [_P, _P, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P, _P, _P],
     "mc_xy_eig": [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P],
-    "mc_pathcv_weights": [_I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                          _P, _P, _P, _P, _P, _P, _P, _P],
-    "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
+    "mc_pathcv_weights": [_I32, _I32, _D, _D, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                          _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32,
+                       _P, _P, _P, _P, _P],
+    "mc_center_split": [_P, ctypes.c_int, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
+    "mc_msd_tf32": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P],
+    "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _I32, _P, _P, _P, _P, _P],
+    "mc_sort_by_key": [_P, _I32, _I32, _P, _P, _P],
+    "mc_refine": [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P],
     "mc_pair_grad": [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],
 }
 
-# optional entry points (present once the tensor path is built)
-_OPTIONAL = {
-    "mc_center_split": [_P, ctypes.c_int, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
-    "mc_msd_tf32": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P],
-    "mc_refine_pairs": [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P],
-    "mc_candidates": [_P, _I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P],
-    "mc_pathcv_weights_sparse": [_I32, _I32, _D, _D, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                 _P, _P, _P],
-}
+# optional entry points (none at present)
+_OPTIONAL = {}
 
 _lib = None
 

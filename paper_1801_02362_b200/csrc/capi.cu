@@ -89,33 +89,63 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
   return cuda_status(mc::launch_xy_eig(fplanes, gx, T, npad, w, refresh, ridx, xyeig, rxy, flags, S_(stream)));
 }
 
-int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, double* D, const double* q,
-                      const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
-                      const int32_t* ridx, const double* S, const double* rxy, const double* xyeig,
-                      const double* gx, const double* ga, const double* lmom, double* s, double* z,
-                      int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec, uint8_t* flags,
-                      void* stream) {
+int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
+                      const int32_t* rowcnt, double* D, const double* q, const double* R, const double* fwbar,
+                      const double* lwbar, const uint8_t* refresh, const int32_t* ridx, const double* S,
+                      const double* rxy, const double* xyeig, const double* gx, const double* ga, const double* lmom,
+                      double* s, double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec,
+                      uint8_t* flags, void* stream) {
   if (T < 0) return MC_ERR_CONFIG;
   if (T > 0 && L < 1) return MC_ERR_EMPTY_ACTIVE_SET;
   if (!(lam > 0.0) || !(cutoff > 0.0) || cap < 1) return MC_ERR_CONFIG;
+  if ((rowlo == nullptr) != (rowcnt == nullptr)) return MC_ERR_CONFIG;
+  if (!rowcnt && ld != L) return MC_ERR_CONFIG;
   if (T > 0 && (!D || !q || !R || !fwbar || !lwbar || !s || !z || !sig_idx || !sig_coef || !nsig || !fvec))
     return MC_ERR_CONFIG;
-  if (refresh && (!ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_cv_weights(T, L, lam, cutoff, cap, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
-                                           xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags,
-                                           S_(stream)));
+  if (refresh && (rowcnt || !ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cv_weights(T, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh,
+                                           ridx, S, rxy, xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec,
+                                           flags, S_(stream)));
 }
 
 int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
-                   const double* xyeig, void* ds, void* dz, int32_t out_f32, void* stream) {
+                   const double* xyeig, void* ds, void* dz, int32_t out_f32, const float* fraw, const double* fcen,
+                   const float* lraw, const double* lcen, void* stream) {
   if (T < 0 || bad_pad(n, npad) || cap < 1) return MC_ERR_CONFIG;
-  if (T > 0 && (!fplanes || !lplanes || !w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec || !ds || !dz))
-    return MC_ERR_CONFIG;
-  if (refresh && (!ridx || !xyeig)) return MC_ERR_CONFIG;
+  if (T > 0 && (!w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec || !ds || !dz)) return MC_ERR_CONFIG;
+  if (T > 0 && !fplanes && !(fraw && fcen)) return MC_ERR_CONFIG;
+  if (T > 0 && !lplanes && !(lraw && lcen)) return MC_ERR_CONFIG;
+  if (refresh && (!ridx || !xyeig || !fplanes)) return MC_ERR_CONFIG;
   return cuda_status(mc::launch_cv_grad(T, n, npad, cap, fplanes, lplanes, w, w_align, sig_idx, sig_coef, nsig, fvec,
-                                        refresh, ridx, xyeig, ds, dz, out_f32, S_(stream)));
+                                        refresh, ridx, xyeig, ds, dz, out_f32, fraw, fcen, lraw, lcen, S_(stream)));
+}
+
+int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
+                  int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
+  if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0)) return MC_ERR_CONFIG;
+  if (T > 0 && (!D || !lo || !cnt)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_candidates(D, T, L, ldd, lam, thr, cap, lo, cnt, dmin, flags, S_(stream)));
+}
+
+int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream) {
+  if (T < 0 || nbins < 1 || (T > 0 && (!key || !bins || !perm))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_sort_by_key(key, T, nbins, bins, perm, S_(stream)));
+}
+
+int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
+              const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
+              const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
+              float* Dd, int64_t ldd, uint8_t* flags, void* stream) {
+  if (T < 0 || L < 1 || n < 2) return MC_ERR_CONFIG;
+  if ((lo == nullptr) != (cnt == nullptr)) return MC_ERR_CONFIG;
+  if (T > 0 && (!frames || !fcentroid || !landmarks || !lcentroid || !w || !gx || !ga)) return MC_ERR_CONFIG;
+  if (!Dex && !Dd) return MC_ERR_CONFIG;
+  if ((Dex || Rex) && cap < 1) return MC_ERR_CONFIG;
+  if (Dd && ldd < L) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_refine(frames, fcentroid, landmarks, lcentroid, w, gx, ga, T, L, n, perm, lo, cnt, cap,
+                                       Dex, Rex, Dd, ldd, flags, S_(stream)));
 }
 
 int mc_pair_grad(int64_t P, int32_t n, int32_t npad, const double* xplanes, const double* aplanes, const int32_t* xi,

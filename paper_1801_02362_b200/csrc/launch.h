@@ -30,7 +30,8 @@ cudaError_t launch_close_scan(const double* fpl, const double* gx, int walkers, 
 cudaError_t launch_xy_eig(const double* fpl, const double* gx, int64_t T, int npad, const double* w,
                           const uint8_t* refresh, const int* ridx, double* xyeig, double* rxy, uint8_t* flags,
                           cudaStream_t stream);
-cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, double* D, const double* q,
+cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
+                              const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
                               const int* ridx, const double* S, const double* rxy, const double* xyeig,
                               const double* gx, const double* ga, const double* lmom, double* s, double* z,
@@ -39,7 +40,15 @@ cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, 
 cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
                            const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
-                           void* ds, void* dz, int out_f32, cudaStream_t stream);
+                           void* ds, void* dz, int out_f32, const float* fraw, const double* fcen,
+                           const float* lraw, const double* lcen, cudaStream_t stream);
+cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, int cap, int* lo,
+                              int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
+cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);
+cudaError_t launch_refine(const float* fr, const double* fc, const float* lr, const double* lc, const double* w,
+                          const double* gx, const double* ga, int T, int L, int n, const int* perm, const int* lo,
+                          const int* cnt, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
+                          cudaStream_t stream);
 cudaError_t launch_pair_grad(int64_t P, int n, int npad, const double* xpl, const double* apl, const int* xi,
                              const int* ai, const double* rot, const double* w, const double* wa, const double* xwbar,
                              const double* awbar, const int* approx, const int* yi, const double* S,

@@ -35,7 +35,8 @@ __device__ __forceinline__ void mat3_mul(const double* a, const double* b, doubl
 }
 
 __global__ void __launch_bounds__(WNT)
-cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __restrict__ D,
+cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, int ld, const int* __restrict__ rowlo,
+                  const int* __restrict__ rowcnt, double* __restrict__ D,
                   const double* __restrict__ q, const double* __restrict__ R, const double* __restrict__ fwbar,
                   const double* __restrict__ lwbar, const uint8_t* __restrict__ refresh,
                   const int* __restrict__ ridx, const double* __restrict__ S, const double* __restrict__ rxy,
@@ -54,15 +55,19 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __re
 #pragma unroll
     for (int e = 0; e < 9; ++e) Rxy[e] = rxy[(int64_t)t * 9 + e];
   }
-  double* Dt = D + (int64_t)t * L;
+  // row layout: dense rows (ld = L, landmark = column) or sparse windows
+  // (row t holds landmarks rowlo[t] .. rowlo[t] + rowcnt[t] - 1, stride ld)
+  double* Dt = D + (int64_t)t * ld;
+  const int nrow = rowcnt ? rowcnt[t] : L;
+  const int off = rowlo ? rowlo[t] : 0;
   // pass 1: distances (Eq. 5 on non-refresh frames) and their minimum
   double dmin = INFINITY;
   bool finite = true;
-  for (int i = tid; i < L; i += WNT) {
+  for (int i = tid; i < nrow; i += WNT) {
     double d;
     if (approx) {
-      const double* Ri = R + ((int64_t)r * L + i) * 9;
-      const double* Si = S + ((int64_t)t * L + i) * 9;
+      const double* Ri = R + ((int64_t)r * ld + i) * 9;
+      const double* Si = S + ((int64_t)t * ld + i) * 9;
       double Rr[9], Rh[9];
 #pragma unroll
       for (int e = 0; e < 9; ++e) Rr[e] = Ri[e];
@@ -82,10 +87,10 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __re
   const int nonfinite = __syncthreads_or(!finite);
   // pass 2: partition function
   double zs = 0.0, qs = 0.0;
-  for (int i = tid; i < L; i += WNT) {
+  for (int i = tid; i < nrow; i += WNT) {
     const double e = exp(-lam * (Dt[i] - dmin));
     zs += e;
-    qs += q[i] * e;
+    qs += q[off + i] * e;
   }
   zs = block_sum<WNT>(zs, scratch);
   qs = block_sum<WNT>(qs, scratch);
@@ -96,11 +101,11 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __re
 #pragma unroll
   for (int e = 0; e < 44; ++e) acc[e] = 0.0;
   int total = 0;
-  for (int b0 = 0; b0 < L; b0 += WNT) {
+  for (int b0 = 0; b0 < nrow; b0 += WNT) {
     const int i = b0 + tid;
     double di = 0.0;
     bool sig = false;
-    if (i < L) {
+    if (i < nrow) {
       di = Dt[i];
       sig = lam * (di - dmin) <= cutoff;
     }
@@ -114,26 +119,27 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __re
     for (int w = 0; w < WNT / 32; ++w) blk += wcount[w];
     if (sig) {
       const double p = exp(-lam * (di - dmin)) / zs;
-      const double cs = -lam * p * (q[i] - sval);
+      const int li = off + i;
+      const double cs = -lam * p * (q[li] - sval);
       const double cz = p;
       double Rh[9], Rr[9];
       if (approx) {
 #pragma unroll
-        for (int e = 0; e < 9; ++e) Rr[e] = R[((int64_t)r * L + i) * 9 + e];
+        for (int e = 0; e < 9; ++e) Rr[e] = R[((int64_t)r * ld + i) * 9 + e];
         mat3_mul(Rxy, Rr, Rh);
       } else {
 #pragma unroll
-        for (int e = 0; e < 9; ++e) Rh[e] = R[((int64_t)t * L + i) * 9 + e];
+        for (int e = 0; e < 9; ++e) Rh[e] = R[((int64_t)t * ld + i) * 9 + e];
       }
       if (pos < cap) {
-        sig_idx[(int64_t)t * cap + pos] = i;
+        sig_idx[(int64_t)t * cap + pos] = li;
         double* co = sig_coef + ((int64_t)t * cap + pos) * 18;
 #pragma unroll
         for (int e = 0; e < 9; ++e) { co[e] = cs * Rh[e]; co[9 + e] = cz * Rh[e]; }
       }
       acc[0] += cs;
       acc[1] += cz;
-      const double wb0 = lwbar[3 * i], wb1 = lwbar[3 * i + 1], wb2 = lwbar[3 * i + 2];
+      const double wb0 = lwbar[3 * li], wb1 = lwbar[3 * li + 1], wb2 = lwbar[3 * li + 2];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const double rw = Rh[a * 3] * wb0 + Rh[a * 3 + 1] * wb1 + Rh[a * 3 + 2] * wb2;
@@ -142,8 +148,8 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __re
       }
       if (approx) {
         // S_i R_i^T and R_i A_i R_i^T (R_i = saved rotation of landmark i)
-        const double* Si = S + ((int64_t)t * L + i) * 9;
-        const double* m = lmom + 6 * (int64_t)i;
+        const double* Si = S + ((int64_t)t * ld + i) * 9;
+        const double* m = lmom + 6 * (int64_t)li;
         const double A[9] = {m[0], m[1], m[2], m[1], m[3], m[4], m[2], m[4], m[5]};
         double SRt[9], RA[9], RAR[9];
 #pragma unroll
@@ -227,14 +233,15 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, double* __re
   }
 }
 
-cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, double* D, const double* q,
+cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
+                              const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
                               const int* ridx, const double* S, const double* rxy, const double* xyeig,
                               const double* gx, const double* ga, const double* lmom, double* s, double* z,
                               int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
                               cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, L, lam, cutoff, cap, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
+  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
                                            xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
   return cudaGetLastError();
 }
@@ -249,7 +256,11 @@ cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const d
                const double* __restrict__ w, const double* __restrict__ wa, const int* __restrict__ sig_idx,
                const double* __restrict__ sig_coef, const int* __restrict__ nsig, const double* __restrict__ fvec,
                const uint8_t* __restrict__ refresh, const int* __restrict__ ridx, const double* __restrict__ xyeig,
-               OT* __restrict__ ds, OT* __restrict__ dz) {
+               OT* __restrict__ ds, OT* __restrict__ dz, const float* __restrict__ fraw,
+               const double* __restrict__ fcen, const float* __restrict__ lraw, const double* __restrict__ lcen) {
+  // Coordinates come either from centred fp64 planes (fpl/lpl) or, on the
+  // fp32 path, from the raw AoS input recentred on the fly with the fp64
+  // centroids (fraw/fcen, lraw/lcen) — no fp64 copy of the big operands.
   __shared__ double sc[GCH * 18];
   __shared__ int si[GCH];
   const int t = blockIdx.x;
@@ -268,13 +279,21 @@ cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const d
     for (int e = tid; e < cn; e += GNT) si[e] = sig_idx[(int64_t)t * cap + c0 + e];
     __syncthreads();
     for (int e = 0; e < cn; ++e) {
-      const double* a = lpl + (int64_t)si[e] * 3 * npad;
+      const int li = si[e];
+      const double* a = lpl ? lpl + (int64_t)li * 3 * npad : nullptr;
+      const float* ar = lpl ? nullptr : lraw + (int64_t)li * n * 3;
+      const double c0 = lpl ? 0.0 : lcen[3 * li], c1 = lpl ? 0.0 : lcen[3 * li + 1], c2 = lpl ? 0.0 : lcen[3 * li + 2];
       const double* C = sc + e * 18;
 #pragma unroll
       for (int m = 0; m < APT; ++m) {
         const int k = k0 + tid + m * GNT;
         if (k < n) {
-          const double a0 = a[k], a1 = a[npad + k], a2 = a[2 * npad + k];
+          double a0, a1, a2;
+          if (a) {
+            a0 = a[k]; a1 = a[npad + k]; a2 = a[2 * npad + k];
+          } else {
+            a0 = (double)ar[3 * k] - c0; a1 = (double)ar[3 * k + 1] - c1; a2 = (double)ar[3 * k + 2] - c2;
+          }
 #pragma unroll
           for (int b = 0; b < 3; ++b) {
             us[m][b] = fma(C[b * 3], a0, fma(C[b * 3 + 1], a1, fma(C[b * 3 + 2], a2, us[m][b])));
@@ -294,7 +313,9 @@ cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const d
     for (int rr = 0; rr < 4; ++rr) q0[rr] = e[4 + rr * 4];
     y = fpl + (int64_t)ridx[t] * 3 * npad;
   }
-  const double* x = fpl + (int64_t)t * 3 * npad;
+  const double* x = fpl ? fpl + (int64_t)t * 3 * npad : nullptr;
+  const float* xr = fpl ? nullptr : fraw + (int64_t)t * n * 3;
+  const double fc0 = fpl ? 0.0 : fcen[3 * t], fc1 = fpl ? 0.0 : fcen[3 * t + 1], fc2 = fpl ? 0.0 : fcen[3 * t + 2];
   const double vs[4] = {fv[8], fv[9], fv[10], fv[11]};
   const double vz[4] = {fv[12], fv[13], fv[14], fv[15]};
 #pragma unroll
@@ -302,7 +323,12 @@ cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const d
     const int k = k0 + tid + m * GNT;
     if (k >= n) continue;
     const double wk = w[k], wak = wa[k];
-    const double xk[3] = {x[k], x[npad + k], x[2 * npad + k]};
+    double xk[3];
+    if (x) {
+      xk[0] = x[k]; xk[1] = x[npad + k]; xk[2] = x[2 * npad + k];
+    } else {
+      xk[0] = (double)xr[3 * k] - fc0; xk[1] = (double)xr[3 * k + 1] - fc1; xk[2] = (double)xr[3 * k + 2] - fc2;
+    }
     double gs[3], gz[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -329,15 +355,18 @@ cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const d
 cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
                            const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
-                           void* ds, void* dz, int out_f32, cudaStream_t stream) {
+                           void* ds, void* dz, int out_f32, const float* fraw, const double* fcen,
+                           const float* lraw, const double* lcen, cudaStream_t stream) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   dim3 grid(T, (n + GNT * APT - 1) / (GNT * APT));
   if (out_f32)
     cv_grad_kernel<float><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
-                                                    refresh, ridx, xyeig, (float*)ds, (float*)dz);
+                                                    refresh, ridx, xyeig, (float*)ds, (float*)dz, fraw, fcen, lraw,
+                                                    lcen);
   else
     cv_grad_kernel<double><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
-                                                     refresh, ridx, xyeig, (double*)ds, (double*)dz);
+                                                     refresh, ridx, xyeig, (double*)ds, (double*)dz, fraw, fcen, lraw,
+                                                     lcen);
   return cudaGetLastError();
 }
 

@@ -183,6 +183,101 @@ class PathCV:
         return out
 
 
+class PathCVTC:
+    """fp32-coordinate path (configs 2-4): tcgen05 3xTF32 screening + exact refinement.
+
+    evaluate():  K1s split -> K2/K3 tensor-core MSD estimate of every pair ->
+    per-frame candidate window {lam (D_est - D_min) <= cutoff + margin} ->
+    frames sorted by window -> exact fp64 refit of the candidates (CUDA
+    cores) -> K4 weights on the exact windows -> gradient pass on the raw
+    fp32 coordinates.  Landmarks outside a window carry weight < e^-cutoff
+    relative to the leading term.
+
+    msd_matrix(exact=True): the dense exact matrix (every pair refit in fp64;
+    the 3xTF32 estimate error, ~1e-7..1e-5 absolute, cannot certify the
+    1e-6 relative tolerance); exact=False returns the estimate.
+    """
+
+    def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None):
+        K.require_cuda()
+        lm = _as_cuda(landmarks, device).float().contiguous()
+        if lm.ndim != 3 or lm.shape[-1] != 3:
+            raise InvalidStructureError("landmarks must be [L, n, 3]")
+        if lm.shape[0] < 1:
+            raise EmptyActiveSetError("no landmarks")
+        if not (lam > 0):
+            raise ConfigError("lambda must be positive")
+        self.device = lm.device
+        self.L, self.n = int(lm.shape[0]), int(lm.shape[1])
+        if self.n < 2:
+            raise InvalidStructureError("a structure needs at least 2 atoms")
+        self.lam, self.cutoff = float(lam), float(cutoff)
+        self.window_cap = int(min(window_cap, self.L))
+        self.w = normalise_weights(w, self.n, "displacement", self.device)
+        self.wa = normalise_weights(w_align, self.n, "alignment", self.device)
+        qq = np.arange(self.L, dtype=float) if q is None else np.asarray(
+            q.detach().cpu().numpy() if torch.is_tensor(q) else q, dtype=float)
+        if qq.shape != (self.L,):
+            raise ConfigError("q must have one value per landmark")
+        self.q = torch.from_numpy(qq).to(self.device)
+        self.lraw = lm
+        self.ls = K.center_split(lm, self.wa, self.w, weighted=True, moments=True)
+        if _or_flags(self.ls.flags) & FLAG_NON_FINITE:
+            raise InvalidStructureError("landmark coordinates contain non-finite values")
+        # estimate error margin (in units of lam * D): the 3xTF32 + fp32-accumulation
+        # error grows ~ sqrt(n); measured max 6.4e-6 (n=1000) and 6.4e-5 (n=10000)
+        self.est_err = 2e-8 * self.n
+        self.margin = 2.0 + self.lam * self.est_err
+
+    def _frames(self, frames):
+        fr = _as_cuda(frames, self.device)
+        if fr.dtype != torch.float32:
+            fr = fr.float()
+        _check_shapes(fr, self.lraw)
+        fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False)
+        if _or_flags(fs.flags) & FLAG_NON_FINITE:
+            raise InvalidStructureError("frame coordinates contain non-finite values")
+        return fr.contiguous(), fs
+
+    def estimate(self, frames):
+        fr, fs = self._frames(frames)
+        return K.msd_tf32(fs, self.ls), fr, fs
+
+    def msd_matrix(self, frames, exact=True):
+        fr, fs = self._frames(frames)
+        D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
+        if not exact:
+            return K.msd_tf32(fs, self.ls, D)
+        _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D)
+        _raise_flags(flags, "msd_matrix")
+        return D
+
+    def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False):
+        Dest, fr, fs = self.estimate(frames)
+        cap = self.window_cap
+        while True:
+            lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap)
+            if (_or_flags(cflags) & FLAG_SIG_OVERFLOW) and cap < self.L:
+                cap = min(self.L, 4 * cap)
+                continue
+            break
+        perm = K.sort_by_key(lo, self.L)
+        Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap)
+        _raise_flags(rflags, "path_cv refine")
+        wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
+                                rowcnt=cnt)
+        if _or_flags(wres["flags"]) & FLAG_NON_FINITE:
+            raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
+               "nsig": wres["nsig"]}
+        if grad:
+            out["ds"], out["dz"] = K.pathcv_grad(wres, fs, self.ls, self.w, self.wa, cap, out_dtype,
+                                                 raw=(fr, self.lraw))
+        if return_estimate:
+            out["D_est"] = Dest
+        return out
+
+
 # ---------------------------------------------------------------- functional API
 
 def msd_matrix(frames, landmarks, w=None, w_align=None):

@@ -151,8 +151,10 @@ def close_decisions(fr: Centred, w, eps, walkers, steps, window=8):
             "onthefly": fly}
 
 
-def pathcv_weights(D, q, lam, R, fr: Centred, lm: Centred, cap, cutoff=50.0, close=None, S=None):
-    T, L = D.shape
+def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L=None, rowlo=None, rowcnt=None):
+    """K4 weights.  D/R rows are dense [T, L] or sparse windows [T, ld] (rowlo/rowcnt)."""
+    T, ld = D.shape
+    L = ld if L is None else L
     dev = D.device
     s = torch.empty((T,), dtype=F64, device=dev)
     z = torch.empty((T,), dtype=F64, device=dev)
@@ -162,24 +164,71 @@ def pathcv_weights(D, q, lam, R, fr: Centred, lm: Centred, cap, cutoff=50.0, clo
     fvec = torch.empty((T, 16), dtype=F64, device=dev)
     flags = torch.empty((T,), dtype=U8, device=dev)
     c = close or {}
-    call("mc_pathcv_weights", T, L, float(lam), float(cutoff), cap, ptr(D), ptr(q), ptr(R), ptr(fr.wbar), ptr(lm.wbar),
+    call("mc_pathcv_weights", T, L, float(lam), float(cutoff), cap, ld, ptr(rowlo), ptr(rowcnt), ptr(D), ptr(q), ptr(R),
+         ptr(fr.wbar), ptr(lm.wbar),
          ptr(c.get("refresh")), ptr(c.get("ridx")), ptr(S if close else None), ptr(c.get("rxy")), ptr(c.get("xyeig")),
          ptr(fr.g if close else None), ptr(lm.g if close else None), ptr(lm.mom if close else None),
          ptr(s), ptr(z), ptr(sig_idx), ptr(sig_coef), ptr(nsig), ptr(fvec), ptr(flags), stream_ptr())
     return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags}
 
 
-def pathcv_grad(wres, fr: Centred, lm: Centred, w, w_align, cap, out_dtype=F64, close=None):
+def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=None):
+    """K4 gradient pass.  fr/lm: Centred (fp64 planes) or, with raw=(frames, landmarks)
+    fp32 AoS tensors, Split objects (centroids used to recentre on the fly)."""
     T, n = fr.count, fr.n
-    dev = fr.planes.device
+    dev = wres["s"].device
     ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
     dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
     c = close or {}
-    call("mc_pathcv_grad", T, n, fr.npad, cap, ptr(fr.planes), ptr(lm.planes), ptr(w), ptr(w_align),
+    if raw is None:
+        fpl, lpl, fraw, fcen, lraw, lcen = fr.planes, lm.planes, None, None, None, None
+        npad = fr.npad
+    else:
+        fpl = lpl = None
+        fraw, lraw = raw
+        fcen, lcen = fr.centroid, lm.centroid
+        npad = npad_for(n)
+    call("mc_pathcv_grad", T, n, npad, cap, ptr(fpl), ptr(lpl), ptr(w), ptr(w_align),
          ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(c.get("refresh")),
          ptr(c.get("ridx")), ptr(c.get("xyeig")), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0,
-         stream_ptr())
+         ptr(fraw), ptr(fcen), ptr(lraw), ptr(lcen), stream_ptr())
     return ds, dz
+
+
+def candidates(D, lam, thr, cap, L=None):
+    """Per-frame D_min and the window of landmarks with lam (D - D_min) <= thr."""
+    T = D.shape[0]
+    L = D.shape[1] if L is None else L
+    dev = D.device
+    lo = torch.empty((T,), dtype=I32, device=dev)
+    cnt = torch.empty((T,), dtype=I32, device=dev)
+    dmin = torch.empty((T,), dtype=torch.float32, device=dev)
+    flags = torch.empty((T,), dtype=U8, device=dev)
+    call("mc_candidates", ptr(D), T, L, D.stride(0), float(lam), float(thr), cap, ptr(lo), ptr(cnt), ptr(dmin),
+         ptr(flags), stream_ptr())
+    return lo, cnt, dmin, flags
+
+
+def sort_by_key(key, nbins):
+    T = key.shape[0]
+    bins = torch.empty((nbins,), dtype=I32, device=key.device)
+    perm = torch.empty((T,), dtype=I32, device=key.device)
+    call("mc_sort_by_key", ptr(key), T, nbins, ptr(bins), ptr(perm), stream_ptr())
+    return perm
+
+
+def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None):
+    """Exact fp64 fits of the in-window pairs (sparse) or of all pairs (dense, into Dd)."""
+    T, n = frames.shape[0], frames.shape[1]
+    L = landmarks.shape[0]
+    dev = frames.device
+    Dex = torch.empty((T, cap), dtype=F64, device=dev) if cap else None
+    Rex = torch.empty((T, cap, 9), dtype=F64, device=dev) if (cap and want_rot) else None
+    flags = torch.zeros((T,), dtype=U8, device=dev)
+    call("mc_refine", ptr(frames), ptr(fsplit.centroid), ptr(landmarks), ptr(lsplit.centroid), ptr(w), ptr(fsplit.g),
+         ptr(lsplit.g), T, L, n, ptr(perm), ptr(lo), ptr(cnt), cap, ptr(Dex), ptr(Rex), ptr(Dd),
+         Dd.stride(0) if Dd is not None else 0, ptr(flags), stream_ptr())
+    return Dex, Rex, flags
 
 
 # ---------------------------------------------------------------- fp32 / tensor-core path

@@ -37,6 +37,42 @@ def test_tf32_estimate_close_to_exact(T, L, n, cuda_device):
     assert err.max() < 5e-6 * max(1.0, n / 1000) ** 0.5 + 2e-6
 
 
+def assert_msd(got, ref, rtol=1e-6, atol=1e-9):
+    err = np.abs(np.asarray(got, dtype=float) - ref)
+    tol = np.maximum(rtol * np.abs(ref), atol)
+    assert (err <= tol).all(), f"{(err > tol).sum()} pairs outside tolerance, worst {err.max():.3e}"
+
+
+def test_exact_dense_msd_matrix_config2_slice(cuda_device):
+    """Config-2 shape slice (n=1000, fp32): every pair within 1e-6 rel / 1e-9 abs."""
+    wl = synth.config2(T=160, L=120)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam)
+    D = pcv.msd_matrix(wl.frames).cpu().numpy()
+    ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64))
+    assert_msd(D, ref)
+
+
+def test_pathcv_tc_config4_slice_vs_oracle(cuda_device):
+    """Config-4 generator at reduced size: s, z (1e-6) and gradients (1e-5) vs the fp64 oracle."""
+    wl = synth.config4(T=48, L=512, N=600)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam)
+    out = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    for key in ("ds", "dz"):
+        got, r = out[key].cpu().numpy(), ref[key]
+        scale = np.abs(r).reshape(r.shape[0], -1).max(axis=1)
+        err = np.abs(got - r).reshape(r.shape[0], -1).max(axis=1)
+        assert np.all(err <= 1e-5 * scale), f"{key}: worst rel {np.max(err / scale):.3e}"
+    # the exact window values agree with the oracle's D
+    lo = out["window_lo"].cpu().numpy()
+    cnt = out["window_cnt"].cpu().numpy()
+    Dw = out["D_window"].cpu().numpy()
+    for t in range(0, 48, 7):
+        assert_msd(Dw[t, : cnt[t]], ref["D"][t, lo[t]: lo[t] + cnt[t]])
+
+
 def test_tf32_weighted(cuda_device):
     rng = np.random.default_rng(2)
     n = 77
