@@ -4,12 +4,16 @@
     python bench.py [--config C] [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 A "step" is one pass of the hot path over one batch of the config's synthetic
-input (BASELINE.json configs; inputs resident in HBM for ``value``; host
-pinned buffers with H2D/D2H inside the timed region for ``e2e``).  Multi-GPU
-runs are launched with torchrun; the work is sharded per DESIGN.md
-("Multi-GPU"), timed with CUDA events and reduced as the max over ranks.
-``--impl reference`` times the C restatement of the reference CPU path
-(oracle/c, all host cores) on a bounded sample of the same workload.
+input (BASELINE.json configs).  ``value`` is whole-job throughput with the
+inputs resident in HBM; ``e2e`` is the same metric through the public API
+with host (pinned) inputs, H2D and the D2H of the step's result inside the
+timed region.  Multi-GPU runs (torchrun) shard the frames across ranks (no
+data-path collective), time with CUDA events and take
+the max over ranks.  ``--impl reference`` times the C restatement of the
+reference CPU path (oracle/c, all host cores) on a bounded sample.
+
+Default workload: config 4 (the largest config, the one BASELINE.json's
+1/2/4/8-GPU scaling is stated on) — path-CV frames/s.
 """
 
 from __future__ import annotations
@@ -21,7 +25,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -94,48 +97,55 @@ class ClockSampler:
                 pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [v for v in (num(r[1]) for r in rows) if v is not None]
+        smax = [v for v in (num(r[2]) for r in rows) if v is not None]
+        power = [v for v in (num(r[3]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
         loaded = [s for s in sm if smax and s > 0.5 * max(smax)] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(rows)}
-
-
-# ----------------------------------------------------------------- workloads
-def load_workload(cfg, small=False):
-    from paper_1801_02362_b200 import synth
-
-    if cfg == 0:
-        return synth.config0()
-    if cfg == 1:
-        return synth.config1(T=2000) if small else synth.config1()
-    raise SystemExit(f"config {cfg} not wired into bench.py yet")
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(power) if power else None}
 
 
 CONFIG_NAMES = {
     0: "config0: path-CV N=22 L=20 T=1000 fp64 exact",
     1: "config1: close-structure N=304 L=500 T=20000 fp64",
+    2: "config2: all-pairs MSD matrix T=65536 L=4096 N=1000 fp32 (exact)",
+    4: "config4: path-CV s,z,grads N=10000 L=8192 T=131072 fp32",
 }
+CONFIG_SHAPES = {2: dict(seed=2, T=65536, L=4096, N=1000, n_endpoints=16),
+                 4: dict(seed=4, T=131072, L=8192, N=10000, n_endpoints=32)}
 
 
-class OursConfig01:
-    """Configs 0/1: fp64 path-CV (exact) / close-structure replay."""
+# ----------------------------------------------------------------- runners
+class Config01:
+    """Configs 0/1: fp64 exact path-CV / close-structure replay (replicas across ranks)."""
 
-    def __init__(self, cfg, wl, device):
+    metric, unit, dtype = "path-CV frames/s", "frames/s", "f64"
+
+    def __init__(self, cfg, device, rank, world):
         import torch
 
-        from paper_1801_02362_b200 import engine
+        from paper_1801_02362_b200 import engine, synth
 
-        self.cfg, self.wl, self.device = cfg, wl, device
-        self.pcv = engine.PathCV(torch.from_numpy(wl.landmarks).to(device), wl.lam, wl.q)
-        self.frames_dev = torch.from_numpy(wl.frames).to(device)
-        self.frames_host = torch.from_numpy(wl.frames).pin_memory()
-        self.T, self.n = wl.frames.shape[0], wl.frames.shape[1]
+        self.cfg, self.device = cfg, device
+        self.wl = synth.config0() if cfg == 0 else synth.config1()
+        self.pcv = engine.PathCV(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q)
+        self.frames_dev = torch.from_numpy(self.wl.frames).to(device)
+        self.frames_host = torch.from_numpy(self.wl.frames).pin_memory()
+        self.T, self.n, self.L = self.wl.frames.shape[0], self.wl.frames.shape[1], self.wl.landmarks.shape[0]
         self.last = None
+        self.parallelism = f"replicas x{world}" if world > 1 else "single"
+        self.scaling = "weak"
 
-    def step(self, frames):
+    def _step(self, frames):
         if self.cfg == 0:
             self.last = self.pcv.evaluate(frames, grad=True)
         else:
@@ -143,44 +153,173 @@ class OursConfig01:
         return self.last
 
     def step_device(self):
-        return self.step(self.frames_dev)
+        return self._step(self.frames_dev)
 
     def step_e2e(self):
         import torch
 
-        out = self.step(self.frames_host.to(self.device, non_blocking=True))
+        out = self._step(self.frames_host.to(self.device, non_blocking=True))
         res = [out["s"], out["z"]] + ([out["refresh"], out["dxy"]] if self.cfg == 1 else [])
         host = [r.to("cpu", non_blocking=True) for r in res]
         torch.cuda.current_stream().synchronize()
         return host
 
     def e2e_bytes(self):
-        h2d = self.frames_host.numel() * self.frames_host.element_size()
-        d2h = self.T * 8 * 2 + (self.T * 9 if self.cfg == 1 else 0)
+        return self.frames_host.numel() * 8, self.T * 16 + (self.T * 9 if self.cfg == 1 else 0)
+
+    def units(self):
+        return self.T
+
+    def kernel_work(self, name):
+        T, n, L = self.T, self.n, self.L
+        npad = ((n + 31) // 32) * 32
+        if name == "mc_cov_f64":
+            return "fp64_flop", 18.0 * n * T * L
+        if name == "mc_fit_dense":
+            return "bytes", T * L * (72 + 8 + 72 + 1)
+        if name == "mc_pathcv_weights":
+            return "bytes", T * L * 8 * 2
+        if name == "mc_pathcv_grad":
+            return "bytes", T * npad * 3 * 8 + T * n * 3 * 8 * 2
+        if name == "mc_center":
+            return "bytes", T * n * 3 * 8 + T * 3 * npad * 8
+        return "bytes", 0.0
+
+    def extra(self):
+        d = {}
+        if self.cfg == 1 and self.last is not None:
+            d["refresh_fraction"] = float(self.last["refresh"].float().mean().item())
+        return d
+
+
+class ConfigTC:
+    """Configs 2/4: fp32 path on tcgen05 (3xTF32 estimate) + exact fp64 refinement.
+    Frames are sharded across ranks; landmarks are replicated (no collective)."""
+
+    def __init__(self, cfg, device, rank, world, frames_override=None):
+        import torch
+
+        from paper_1801_02362_b200 import engine, synth
+
+        self.cfg, self.device = cfg, device
+        shp = dict(CONFIG_SHAPES[cfg])
+        if frames_override:
+            shp["T"] = frames_override
+        T_all = shp["T"]
+        per = (T_all + world - 1) // world
+        off = rank * per
+        cnt = max(0, min(per, T_all - off))
+        self.wl = synth.interp_config_device(shp["seed"], T_all, shp["L"], shp["N"], shp["n_endpoints"], device,
+                                             frame_offset=off, frame_count=cnt)
+        self.T_all, self.T = T_all, cnt
+        self.n, self.L = shp["N"], shp["L"]
+        self.pcv = engine.PathCVTC(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q)
+        self.frames_dev = self.wl.frames
+        self.chunk = 8192
+        try:
+            self.frames_host = self.frames_dev.cpu().pin_memory()
+            self.host_kind = "pinned"
+        except RuntimeError:
+            self.frames_host = self.frames_dev.cpu()
+            self.host_kind = "pageable (pinning failed)"
+        self.parallelism = f"frame-sharded dp{world}" if world > 1 else "single"
+        self.scaling = "strong"
+        self.last = None
+        if cfg == 2:
+            self.metric, self.unit = "aligned-MSD pairs/s", "pairs/s"
+            self.D = torch.empty((self.T, self.L), dtype=torch.float32, device=device)
+        else:
+            self.metric, self.unit = "path-CV frames/s", "frames/s"
+        self.dtype = "f32 in / tf32x3 tensor + f64 exact"
+
+    def _step(self, frames, D=None):
+        if self.cfg == 2:
+            self.last = self.pcv.msd_matrix(frames) if D is None else self._msd_into(frames, D)
+        else:
+            self.last = self.pcv.evaluate(frames, grad=True)
+        return self.last
+
+    def _msd_into(self, frames, D):
+        from paper_1801_02362_b200 import kernels as K
+
+        fr, fs = self.pcv._frames(frames)
+        K.refine(fr, fs, self.pcv.lraw, self.pcv.ls, self.pcv.w, Dd=D)
+        return D
+
+    def step_device(self):
+        return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
+
+    def step_e2e(self):
+        """Public API with host frames: chunked H2D -> evaluate -> D2H of the result."""
+        import torch
+
+        outs = []
+        for c0 in range(0, self.T, self.chunk):
+            fr = self.frames_host[c0:c0 + self.chunk].to(self.device, non_blocking=True)
+            if self.cfg == 2:
+                D = self._step(fr)
+                outs.append(D.to("cpu", non_blocking=True))
+            else:
+                o = self._step(fr)
+                outs.append(o["s"].to("cpu", non_blocking=True))
+                outs.append(o["z"].to("cpu", non_blocking=True))
+        torch.cuda.current_stream().synchronize()
+        return outs
+
+    def e2e_bytes(self):
+        h2d = self.T * self.n * 3 * 4
+        d2h = self.T * self.L * 4 if self.cfg == 2 else self.T * 16
         return h2d, d2h
 
-    units_per_step = property(lambda self: self.T)
-    metric = "path-CV frames/s"
-    unit = "frames/s"
+    def units(self):
+        return self.T * self.L if self.cfg == 2 else self.T
+
+    def kernel_work(self, name):
+        T, n, L = self.T, self.n, self.L
+        if name == "mc_msd_tf32":
+            return "tensor_flop", 3.0 * 18.0 * n * T * L
+        if name == "mc_refine":
+            return "fp64_flop", 18.0 * n * T * L if self.cfg == 2 else 0.0
+        if name == "mc_center_split":
+            return "bytes", T * n * 3 * 4 + 2 * T * 3 * (((n + 15) // 16) * 16) * 4
+        if name == "mc_pathcv_grad":
+            return "bytes", T * n * 3 * 4 + T * n * 3 * 4 * 2
+        if name == "mc_candidates":
+            return "bytes", T * L * 4
+        return "bytes", 0.0
+
+    def extra(self):
+        d = {"pairs_per_step": self.T * self.L, "host_buffers": self.host_kind}
+        if self.cfg == 4 and self.last is not None:
+            d["mean_window"] = float(self.last["window_cnt"].float().mean().item())
+            d["mean_significant"] = float(self.last["nsig"].float().mean().item())
+        return d
 
 
-# algorithmic work per kernel launch
-def kernel_work(name, runner):
-    """(kind, amount) per launch: kind 'bytes' (HBM roofline) or 'flop'."""
-    T, n = runner.T, runner.n
-    L = runner.wl.landmarks.shape[0]
-    npad = ((n + 31) // 32) * 32
-    if name == "mc_cov_f64":
-        return "fp64_flop", 18.0 * n * T * L
-    if name == "mc_fit_dense":
-        return "bytes", T * L * (72 + 8 + 72 + 1)
-    if name == "mc_pathcv_weights":
-        return "bytes", T * L * 8 * 2
-    if name == "mc_pathcv_grad":
-        return "bytes", T * npad * 3 * 8 + T * n * 3 * 8 * 2
-    if name == "mc_center":
-        return "bytes", T * n * 3 * 8 + T * 3 * npad * 8
-    return "bytes", 0.0
+def tf32_peak_measure(device):
+    """cuBLAS TF32 GEMM rate on this box (cross-check of the derived peak)."""
+    import torch
+
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn((8192, 8192), device=device)
+        b = torch.randn((8192, 8192), device=device)
+        for _ in range(3):
+            a @ b
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(5):
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = False
 
 
 def run_ours(args, rank, world, local_rank):
@@ -197,10 +336,8 @@ def run_ours(args, rank, world, local_rank):
         dist_mod.init_process_group("nccl", device_id=device)
         dist = dist_mod
     cfg = args.config
-    wl = load_workload(cfg)
-    runner = OursConfig01(cfg, wl, device)
-    # configs 0/1 do not shard (sequential close-structure chain; tiny config 0):
-    # every rank runs an independent replica
+    runner = Config01(cfg, device, rank, world) if cfg in (0, 1) else ConfigTC(cfg, device, rank, world,
+                                                                               args.frames)
     for _ in range(args.warmup):
         runner.step_device()
     torch.cuda.synchronize()
@@ -229,123 +366,171 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         ms = timed(runner.step_device, args.steps)
     clocks = clk.summary()
-    launches = (_lib.COUNTERS["launches"] - launches0) // max(1, args.steps) * args.steps
+    launches = _lib.COUNTERS["launches"] - launches0
     # end-to-end through the public API with host buffers
     runner.step_e2e()
     ms_e2e = timed(runner.step_e2e, args.steps)
     h2d, d2h = runner.e2e_bytes()
-    # per-kernel live timing (CUDA events around each launch, on the launch stream)
+    # live per-kernel timing: CUDA events around each launch on the launch stream
+    nprof = max(1, min(args.steps, 2))
     _lib.start_profile()
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(nprof):
         runner.step_device()
     prof = _lib.stop_profile()
     pk = peaks()
     total = sum(t for _, t in prof.values()) or 1.0
-    top = max(prof.items(), key=lambda kv: kv[1][1])
-    name, (cnt, tms) = top
+    name, (cnt, tms) = max(prof.items(), key=lambda kv: kv[1][1])
     avg_ms = tms / cnt
-    kind, amount = kernel_work(name, runner)
+    kind, amount = runner.kernel_work(name)
+    tf32_cublas = tf32_peak_measure(device) if kind == "tensor_flop" and rank == 0 else None
     if kind == "bytes":
-        achieved = amount / (avg_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s", "frac": achieved / pk["hbm"]}
+        ach = amount / (avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
+                "peak_src": pk["src"]}
+    elif kind == "tensor_flop":
+        ach = amount / (avg_ms * 1e-3) / 1e12
+        peak = pk["bf16"] / 2.0
+        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "peak_src": f"TF32 = bf16_tflops/2 from {pk['src']} (TF32 runs at half the bf16 rate)",
+                "cublas_tf32_measured": tf32_cublas, "flop_basis": "executed 3xTF32 (3 x 18 n per pair)"}
     else:
-        achieved = amount / (avg_ms * 1e-3) / 1e12
-        fp64_peak = 37.0  # TF/s nominal B200 FP64 (no measured figure in MEASURED_PEAKS.json)
-        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "peak_src": "nominal B200 FP64 (not measured)"}
-    roof.update({"kernel": name, "share_of_step": tms / total, "avg_launch_ms": avg_ms, "traffic": None,
-                 "peak_src": roof.get("peak_src", pk["src"])})
-    kernels = {k: {"launches": c, "ms_per_step": t / max(1, min(args.steps, 3)), "share": t / total}
+        ach = amount / (avg_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,
+                "peak_src": "nominal B200 FP64 37 TF/s (not measured)"}
+    roof.update({"kernel": name, "share_of_step": tms / total, "avg_launch_ms": avg_ms, "traffic": None})
+    kernels = {k: {"launches": c, "ms_per_step": t / nprof, "share": t / total}
                for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
-    units = runner.units_per_step * world
+    units = runner.units() * world if runner.scaling == "weak" else runner.units()
+    if dist and runner.scaling == "strong":
+        t = torch.tensor([float(units)], device=device, dtype=torch.float64)
+        dist.all_reduce(t)
+        units = float(t.item())
     line = {
         "metric": runner.metric, "value": units / (ms * 1e-3), "unit": runner.unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth.py)",
-        "config": {"workload": CONFIG_NAMES[cfg], "frames_per_rank": runner.T, "landmarks": int(wl.landmarks.shape[0]),
-                   "atoms": runner.n, "parallelism": f"replicas x{world}" if world > 1 else "single",
-                   "l2": "inputs re-read each step; working set (S/R/D buffers) > L2"},
-        "e2e": {"value": units / (ms_e2e * 1e-3), "unit": runner.unit, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e},
+        "scaling": runner.scaling, "vs_baseline": None, "dtype": runner.dtype,
+        "data": "synthetic (seeded; synth.py, configs 2/4 generated on device)",
+        "config": {"workload": CONFIG_NAMES[cfg], "frames_per_rank": runner.T, "landmarks": runner.L,
+                   "atoms": runner.n, "parallelism": runner.parallelism,
+                   "l2": "working set > L2 (126 MB): frames/operands re-read from HBM every step"},
+        "e2e": {"value": units / (ms_e2e * 1e-3), "unit": runner.unit, "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h * world, "ms_per_step": ms_e2e},
         "gpu_launches": launches, "clocks": clocks, "roofline": roof, "kernels": kernels,
     }
-    if cfg == 1 and runner.last is not None:
-        line["config"]["refresh_fraction"] = float(runner.last["refresh"].float().mean().item())
+    line["config"].update(runner.extra())
     if rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, wl, args)
+        line["cpu_baseline"] = cpu_baseline(cfg, runner, args)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
-def cpu_baseline(cfg, wl, args, seconds=12.0):
+def _cpu_fn(cfg, wl):
+    from oracle import c_oracle as C
+
+    if cfg == 0:
+        return lambda fr: C.path_cv_exact(fr, wl.landmarks, wl.lam, wl.q)
+    if cfg == 1:
+        return lambda fr: C.close_replay(fr, wl.landmarks, wl.lam, wl.eps, wl.q)
+    if cfg == 2:
+        return lambda fr: C.msd_matrix(fr, wl.landmarks[:256])
+    return lambda fr: C.path_cv_exact(fr, wl.landmarks, wl.lam, wl.q)
+
+
+def cpu_baseline(cfg, runner, args, seconds=12.0):
     """C restatement of the reference CPU path on a bounded sample (all host cores)."""
     from oracle import c_oracle as C
 
     threads = C.max_threads()
-    frames = wl.frames
-    if cfg == 0:
-        fn = lambda fr: C.path_cv_exact(fr, wl.landmarks, wl.lam, wl.q)  # noqa: E731
-    else:
-        fn = lambda fr: C.close_replay(fr, wl.landmarks, wl.lam, wl.eps, wl.q)  # noqa: E731
-    # calibrate the sample to ~`seconds` of CPU work
-    k = min(frames.shape[0], 64)
+    wl = runner.wl
+    frames = wl.frames if cfg in (0, 1) else wl.frames[:256].double().cpu().numpy()
+    fn = _cpu_fn(cfg, wl)
+    k = min(frames.shape[0], 4 if cfg in (2, 4) else 64)
     t0 = time.perf_counter()
     fn(frames[:k])
     dt = time.perf_counter() - t0
-    k2 = int(min(frames.shape[0], max(k, k * seconds / max(dt, 1e-6))))
-    t0 = time.perf_counter()
-    fn(frames[:k2])
-    dt = time.perf_counter() - t0
-    return {"value": k2 / dt, "unit": "frames/s", "cores": threads, "kind": "port",
-            "sample": f"first {k2} frames of the {CONFIG_NAMES[cfg].split(':')[0]} workload, "
-                      f"oracle/c (C restatement of geometry.py + SPEC msd/colvar), OpenMP {threads} threads"}
+    if cfg in (0, 1):
+        k2 = int(min(frames.shape[0], max(k, k * seconds / max(dt, 1e-6))))
+        t0 = time.perf_counter()
+        fn(frames[:k2])
+        dt = time.perf_counter() - t0
+    else:
+        k2 = k
+    if cfg == 2:
+        value, unit = k2 * 256 / dt, "pairs/s"
+        sample = f"{k2} frames x 256 landmarks of config2 (exact kearsley fits)"
+    else:
+        value, unit = k2 / dt, "frames/s"
+        sample = f"{k2} frames of the {CONFIG_NAMES[cfg].split(':')[0]} workload"
+    return {"value": value, "unit": unit, "cores": threads, "kind": "port",
+            "sample": sample + f", oracle/c (C restatement of geometry.py + SPEC msd/colvar), OpenMP {threads} threads"}
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the C port of the reference CPU path, rank 0 only, all host cores."""
     if rank != 0:
         return
-    cfg = args.config
-    wl = load_workload(cfg)
     from oracle import c_oracle as C
+    from paper_1801_02362_b200 import synth
 
+    cfg = args.config
     threads = C.max_threads()
-    frames = wl.frames
-    L = wl.landmarks.shape[0]
-    if cfg == 0:
-        fn = lambda fr: C.path_cv_exact(fr, wl.landmarks, wl.lam, wl.q)  # noqa: E731
-        sample = frames
+    if cfg in (0, 1):
+        wl = synth.config0() if cfg == 0 else synth.config1()
+        sample = wl.frames if cfg == 0 else wl.frames[:1000]
+        L, n = wl.landmarks.shape[0], wl.frames.shape[1]
     else:
-        fn = lambda fr: C.close_replay(fr, wl.landmarks, wl.lam, wl.eps, wl.q)  # noqa: E731
-        sample = frames[:1000]
+        shp = CONFIG_SHAPES[cfg]
+        rng_frames = 16 if cfg == 2 else 4
+        wl = _host_sample(cfg, rng_frames)
+        sample = wl.frames
+        L, n = wl.landmarks.shape[0], shp["N"]
+    fn = _cpu_fn(cfg, wl)
     for _ in range(args.warmup):
-        fn(sample[: max(1, len(sample) // 10)])
+        fn(sample[: max(1, len(sample) // 4)])
     t0 = time.perf_counter()
     for _ in range(args.steps):
         fn(sample)
     dt = (time.perf_counter() - t0) / args.steps
-    v = len(sample) / dt
+    if cfg == 2:
+        v, unit, metric = len(sample) * 256 / dt, "pairs/s", "aligned-MSD pairs/s"
+    else:
+        v, unit, metric = len(sample) / dt, "frames/s", "path-CV frames/s"
     line = {
-        "impl": "reference", "metric": "path-CV frames/s", "value": v, "unit": "frames/s", "n_gpus": world,
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth.py)",
-        "config": {"workload": CONFIG_NAMES[cfg], "frames_per_step": len(sample), "landmarks": L,
-                   "atoms": int(frames.shape[1])},
-        "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{len(sample)} frames per step, oracle/c OpenMP {threads} threads"},
-        "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": CONFIG_NAMES[cfg], "frames_per_step": len(sample), "landmarks": L, "atoms": n},
+        "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "port",
+                         "sample": f"{len(sample)} frames per step" + (" x 256 landmarks" if cfg == 2 else "") +
+                                   f", oracle/c OpenMP {threads} threads"},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def _host_sample(cfg, nframes):
+    """A few frames of config 2/4 on the host (numpy generator path) for the CPU arm."""
+    from paper_1801_02362_b200 import synth
+
+    shp = CONFIG_SHAPES[cfg]
+    rng = np.random.default_rng(shp["seed"])
+    ends = rng.normal(0.0, 0.3, size=(shp["n_endpoints"], shp["N"], 3))
+    lms = synth.make_landmarks(rng, ends, shp["L"], dtype=np.float32)
+    fr, _, _ = synth._interp_frames(rng, ends, shp["L"], nframes, shp["N"], 1e-3, 0.5, np.float32)
+    wl = synth._finish(f"config{cfg}-sample", fr.astype(np.float64), lms)
+    return wl
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, default=int(os.environ.get("MC_BENCH_CONFIG", 1)))
+    ap.add_argument("--config", type=int, default=int(os.environ.get("MC_BENCH_CONFIG", 4)))
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=0, help="override T (configs 2/4) for quick runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))

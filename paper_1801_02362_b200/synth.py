@@ -206,3 +206,52 @@ def config4(seed=4, T=131072, L=8192, N=10000, n_endpoints=32):
 
 
 CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
+
+
+def interp_config_device(seed, T, L, N, n_endpoints, device, frame_offset=0, frame_count=None,
+                         sigma_lo=1e-3, sigma_hi=0.5, chunk=4096):
+    """Configs 2/4 generated on the GPU (torch RNG): same distributions as
+    config2/config4 above, for full-size benchmark runs where host generation
+    of 10^9..10^10 coordinates would dominate.  Landmarks and endpoints come
+    from numpy (seeded) so lambda is identical on every rank; frames
+    [frame_offset, frame_offset + frame_count) are drawn from a per-chunk
+    seeded torch generator, so shards of a multi-GPU run are disjoint slices
+    of one global frame set."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    ends = rng.normal(0.0, 0.3, size=(n_endpoints, N, 3))
+    lms = make_landmarks(rng, ends, L, dtype=np.float32)
+    wl = _finish(f"device{seed}", None, lms)
+    frame_count = T - frame_offset if frame_count is None else frame_count
+    ends_t = torch.from_numpy(ends).to(device=device, dtype=torch.float32)
+    frames = torch.empty((frame_count, N, 3), dtype=torch.float32, device=device)
+    n_seg = n_endpoints - 1
+    for c0 in range(frame_offset - frame_offset % chunk, frame_offset + frame_count, chunk):
+        g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + c0 // chunk)
+        cn = min(chunk, T - c0)
+        p = torch.rand(cn, generator=g, device=device, dtype=torch.float64) * (L - 1)
+        sig = torch.exp(torch.empty(cn, device=device, dtype=torch.float64).uniform_(
+            math.log(sigma_lo), math.log(sigma_hi), generator=g))
+        u = (p / (L - 1)).clamp(0, 1) * n_seg
+        seg = u.long().clamp(max=n_seg - 1)
+        f = (u - seg).float()[:, None, None]
+        base = (1 - f) * ends_t[seg] + f * ends_t[seg + 1]
+        base += torch.randn(base.shape, generator=g, device=device) * sig.float()[:, None, None]
+        q = torch.randn((cn, 4), generator=g, device=device, dtype=torch.float64)
+        q = q / q.norm(dim=1, keepdim=True)
+        q0, q1, q2, q3 = q.unbind(1)
+        rot = torch.stack([
+            torch.stack([q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2)], -1),
+            torch.stack([2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1)], -1),
+            torch.stack([2 * (q1 * q3 - q0 * q2), 2 * (q2 * q3 + q0 * q1), q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3], -1),
+        ], -2).float()
+        trans = (torch.rand((cn, 1, 3), generator=g, device=device) * 2 - 1)
+        blk = torch.einsum("kab,kjb->kja", rot, base) + trans
+        a = max(c0, frame_offset)
+        b = min(c0 + cn, frame_offset + frame_count)
+        if b > a:
+            frames[a - frame_offset: b - frame_offset] = blk[a - c0: b - c0]
+    wl.frames = frames
+    wl.meta["generator"] = "device (torch, per-chunk seeded)"
+    return wl
