@@ -124,7 +124,8 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
  *   have lam (D - D_min) > cutoff and weight < e^-cutoff).
  * mc_pathcv_grad: one pass over atoms writing ds, dz [T, n, 3] (fp64, or fp32 if
  *   out_f32).  Coordinates from centred fp64 planes, or (fplanes/lplanes NULL)
- *   from raw fp32 AoS input + fp64 centroids. */
+ *   from raw fp32 AoS input + fp64 centroids.  perm (nullable): frame visiting order
+ *   (the candidate sort, so neighbouring CTAs share landmarks in L2). */
 int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
                       const int32_t* rowcnt, double* D, const double* q, const double* R, const double* fwbar,
                       const double* lwbar, const uint8_t* refresh, const int32_t* ridx, const double* S,
@@ -135,7 +136,7 @@ int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
                    const double* xyeig, void* ds, void* dz, int32_t out_f32, const float* fraw, const double* fcen,
-                   const float* lraw, const double* lcen, void* stream);
+                   const float* lraw, const double* lcen, const int32_t* perm, void* stream);
 
 /* ---- fp32-coordinate path (configs 2-4): tensor-core estimate + exact refinement ----
  * mc_center_split (K1s, geometry.py:67-76 + operand prep): centre in fp64, optionally

@@ -112,14 +112,15 @@ int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
                    const double* xyeig, void* ds, void* dz, int32_t out_f32, const float* fraw, const double* fcen,
-                   const float* lraw, const double* lcen, void* stream) {
+                   const float* lraw, const double* lcen, const int32_t* perm, void* stream) {
   if (T < 0 || bad_pad(n, npad) || cap < 1) return MC_ERR_CONFIG;
   if (T > 0 && (!w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec || !ds || !dz)) return MC_ERR_CONFIG;
   if (T > 0 && !fplanes && !(fraw && fcen)) return MC_ERR_CONFIG;
   if (T > 0 && !lplanes && !(lraw && lcen)) return MC_ERR_CONFIG;
   if (refresh && (!ridx || !xyeig || !fplanes)) return MC_ERR_CONFIG;
   return cuda_status(mc::launch_cv_grad(T, n, npad, cap, fplanes, lplanes, w, w_align, sig_idx, sig_coef, nsig, fvec,
-                                        refresh, ridx, xyeig, ds, dz, out_f32, fraw, fcen, lraw, lcen, S_(stream)));
+                                        refresh, ridx, xyeig, ds, dz, out_f32, fraw, fcen, lraw, lcen, perm,
+                                        S_(stream)));
 }
 
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,

@@ -257,13 +257,14 @@ cv_grad_kernel(int n, int npad, int cap, const double* __restrict__ fpl, const d
                const double* __restrict__ sig_coef, const int* __restrict__ nsig, const double* __restrict__ fvec,
                const uint8_t* __restrict__ refresh, const int* __restrict__ ridx, const double* __restrict__ xyeig,
                OT* __restrict__ ds, OT* __restrict__ dz, const float* __restrict__ fraw,
-               const double* __restrict__ fcen, const float* __restrict__ lraw, const double* __restrict__ lcen) {
+               const double* __restrict__ fcen, const float* __restrict__ lraw, const double* __restrict__ lcen,
+               const int* __restrict__ perm) {
   // Coordinates come either from centred fp64 planes (fpl/lpl) or, on the
   // fp32 path, from the raw AoS input recentred on the fly with the fp64
   // centroids (fraw/fcen, lraw/lcen) — no fp64 copy of the big operands.
   __shared__ double sc[GCH * 18];
   __shared__ int si[GCH];
-  const int t = blockIdx.x;
+  const int t = perm ? perm[blockIdx.x] : blockIdx.x;  // sorted order: neighbours share landmarks in L2
   const int k0 = blockIdx.y * GNT * APT;
   const int tid = threadIdx.x;
   const int ns = nsig[t];
@@ -356,17 +357,17 @@ cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, c
                            const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
                            void* ds, void* dz, int out_f32, const float* fraw, const double* fcen,
-                           const float* lraw, const double* lcen, cudaStream_t stream) {
+                           const float* lraw, const double* lcen, const int* perm, cudaStream_t stream) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   dim3 grid(T, (n + GNT * APT - 1) / (GNT * APT));
   if (out_f32)
     cv_grad_kernel<float><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
                                                     refresh, ridx, xyeig, (float*)ds, (float*)dz, fraw, fcen, lraw,
-                                                    lcen);
+                                                    lcen, perm);
   else
     cv_grad_kernel<double><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
                                                      refresh, ridx, xyeig, (double*)ds, (double*)dz, fraw, fcen, lraw,
-                                                     lcen);
+                                                     lcen, perm);
   return cudaGetLastError();
 }
 

@@ -272,7 +272,7 @@ class PathCVTC:
                "nsig": wres["nsig"]}
         if grad:
             out["ds"], out["dz"] = K.pathcv_grad(wres, fs, self.ls, self.w, self.wa, cap, out_dtype,
-                                                 raw=(fr, self.lraw))
+                                                 raw=(fr, self.lraw), perm=perm)
         if return_estimate:
             out["D_est"] = Dest
         return out

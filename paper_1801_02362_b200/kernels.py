@@ -172,7 +172,7 @@ def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L
     return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags}
 
 
-def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=None):
+def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=None, perm=None):
     """K4 gradient pass.  fr/lm: Centred (fp64 planes) or, with raw=(frames, landmarks)
     fp32 AoS tensors, Split objects (centroids used to recentre on the fly)."""
     T, n = fr.count, fr.n
@@ -191,7 +191,7 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
     call("mc_pathcv_grad", T, n, npad, cap, ptr(fpl), ptr(lpl), ptr(w), ptr(w_align),
          ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(c.get("refresh")),
          ptr(c.get("ridx")), ptr(c.get("xyeig")), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0,
-         ptr(fraw), ptr(fcen), ptr(lraw), ptr(lcen), stream_ptr())
+         ptr(fraw), ptr(fcen), ptr(lraw), ptr(lcen), ptr(perm), stream_ptr())
     return ds, dz
 
 
