@@ -199,6 +199,21 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Grouped tile order: GROUP_M frame tiles x all landmark tiles per group, frame
+// tile fastest inside a group, so the ~148 concurrently running CTAs (which
+// advance through K in near lockstep) cover ~4 frame tiles x ~37 landmark
+// tiles and both operands are re-used out of L2 instead of streaming every
+// landmark tile from HBM once per frame tile.
+__device__ __forceinline__ void tile_coords(int tile, int ntm, int ntl, int& tm, int& tl) {
+  constexpr int GROUP_M = 4;
+  const int gsize = GROUP_M * ntl;
+  const int g = tile / gsize;
+  const int r = tile - g * gsize;
+  const int gm = min(GROUP_M, ntm - g * GROUP_M);
+  tl = r / gm;
+  tm = g * GROUP_M + (r - tl * gm);
+}
+
 // MSD estimate from an fp32 covariance (fp64 finalisation)
 __device__ __forceinline__ double msd_from_S32(const float* s, double gx, double ga) {
   double S[9];
@@ -255,7 +270,8 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tm = tile / ntl, tl = tile - tm * ntl;
+        int tm, tl;
+        tile_coords(tile, ntm, ntl, tm, tl);
         const int t0 = tm * BM, l0 = tl * BL;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -320,7 +336,8 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
     const int row = q * 32 + lane;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      const int tm = tile / ntl, tl = tile - tm * ntl;
+      int tm, tl;
+      tile_coords(tile, ntm, ntl, tm, tl);
       const int t = tm * BM + row;
       const int l0 = tl * BL;
       mbar_wait(tfull, it & 1);
