@@ -123,6 +123,18 @@ int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double
                                         S_(stream)));
 }
 
+int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const float* lraw,
+                         const double* lcen, const double* w, const double* w_align, const int32_t* sig_idx,
+                         const double* sig_coef, const int32_t* nsig, const double* fvec, const int32_t* perm,
+                         void* ds, void* dz, int32_t out_f32, void* stream) {
+  if (T < 0 || n < 2 || cap < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!fraw || !fcen || !lraw || !lcen || !w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec ||
+                !ds || !dz))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cv_grad_block(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, sig_idx, sig_coef, nsig,
+                                              fvec, perm, ds, dz, out_f32, S_(stream)));
+}
+
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
                   int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
   if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0)) return MC_ERR_CONFIG;

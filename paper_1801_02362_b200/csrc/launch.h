@@ -42,6 +42,10 @@ cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, c
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
                            void* ds, void* dz, int out_f32, const float* fraw, const double* fcen,
                            const float* lraw, const double* lcen, const int* perm, cudaStream_t stream);
+cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
+                                 const double* lcen, const double* w, const double* wa, const int* sig_idx,
+                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
+                                 void* ds, void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, int cap, int* lo,
                               int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);

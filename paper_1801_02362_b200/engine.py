@@ -271,8 +271,8 @@ class PathCVTC:
         out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
                "nsig": wres["nsig"]}
         if grad:
-            out["ds"], out["dz"] = K.pathcv_grad(wres, fs, self.ls, self.w, self.wa, cap, out_dtype,
-                                                 raw=(fr, self.lraw), perm=perm)
+            out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap,
+                                                       perm, out_dtype)
         if return_estimate:
             out["D_est"] = Dest
         return out

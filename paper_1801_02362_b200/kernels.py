@@ -195,6 +195,18 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
     return ds, dz
 
 
+def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32):
+    """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames."""
+    T, n = frames.shape[0], frames.shape[1]
+    dev = frames.device
+    ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
+    dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
+    call("mc_pathcv_grad_block", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
+         ptr(w_align), ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(perm),
+         ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0, stream_ptr())
+    return ds, dz
+
+
 def candidates(D, lam, thr, cap, L=None):
     """Per-frame D_min and the window of landmarks with lam (D - D_min) <= thr."""
     T = D.shape[0]
