@@ -100,18 +100,26 @@ cv_grad_block_kernel(int T, int n, int cap, const float* __restrict__ fraw, cons
         }
         __syncthreads();
       }
+      // software-pipelined landmark loop: the next landmark's coordinates are
+      // in flight while the current one feeds 8 x 18 FMAs (the L2 latency is
+      // otherwise exposed at 8 warps/SM).  Coefficients outside a frame's list
+      // are zero in sC, so the loop body is branch-free.
+      float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+      if (on && wn > 0) {
+        const float* p = lraw + ((int64_t)w0 * n + k) * 3;
+        p0 = p[0]; p1 = p[1]; p2 = p[2];
+      }
       for (int l = 0; l < wn; ++l) {
         const int li = w0 + l;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        if (on) {
-          const float* p = lraw + ((int64_t)li * n + k) * 3;
-          a0 = (double)p[0] - lcen[3 * li];
-          a1 = (double)p[1] - lcen[3 * li + 1];
-          a2 = (double)p[2] - lcen[3 * li + 2];
+        const double a0 = (double)p0 - lcen[3 * li];
+        const double a1 = (double)p1 - lcen[3 * li + 1];
+        const double a2 = (double)p2 - lcen[3 * li + 2];
+        if (on && l + 1 < wn) {
+          const float* p = lraw + ((int64_t)(li + 1) * n + k) * 3;
+          p0 = p[0]; p1 = p[1]; p2 = p[2];
         }
 #pragma unroll
         for (int f = 0; f < GG; ++f) {
-          if (li < s_flo[f] || li >= s_fhi[f]) continue;  // warp-uniform
           const double2* C2 = reinterpret_cast<const double2*>(sC[f][l]);
           double C[18];
 #pragma unroll
