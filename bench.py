@@ -118,6 +118,7 @@ CONFIG_NAMES = {
     0: "config0: path-CV N=22 L=20 T=1000 fp64 exact",
     1: "config1: close-structure N=304 L=500 T=20000 fp64",
     2: "config2: all-pairs MSD matrix T=65536 L=4096 N=1000 fp32 (exact)",
+    3: "config3: multi-walker close structure W=256 x 1000 steps N=2500 L=2048 fp32",
     4: "config4: path-CV s,z,grads N=10000 L=8192 T=131072 fp32",
 }
 CONFIG_SHAPES = {2: dict(seed=2, T=65536, L=4096, N=1000, n_endpoints=16),
@@ -188,6 +189,72 @@ class Config01:
     def extra(self):
         d = {}
         if self.cfg == 1 and self.last is not None:
+            d["refresh_fraction"] = float(self.last["refresh"].float().mean().item())
+        return d
+
+
+class Config3:
+    """Config 3: W walkers x 1000 steps, each with its own floating close structure
+    (fp32 coordinates, fp64 finalisation; exact fp64 path).  Walkers are sharded
+    across ranks (independent objects, no collective)."""
+
+    metric, unit, dtype = "path-CV frames/s", "frames/s", "f32 in / f64 exact"
+
+    def __init__(self, device, rank, world, walkers_override=None):
+        from paper_1801_02362_b200 import dist as D
+        from paper_1801_02362_b200 import engine, synth
+
+        W = walkers_override or 256
+        self.steps, self.n, self.L = 1000, 2500, 2048
+        off, cnt = D.shard_range(W, rank, world)
+        self.wl = synth.walkers_device(3, W, self.steps, self.n, self.L, device, off, cnt)
+        self.device = device
+        self.W_all, self.Wloc = W, cnt
+        self.T = cnt * self.steps
+        import torch
+
+        self.pcv = engine.PathCV(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q)
+        self.frames_dev = self.wl.frames
+        try:
+            self.frames_host = self.frames_dev.cpu().pin_memory()
+        except RuntimeError:
+            self.frames_host = self.frames_dev.cpu()
+        self.parallelism = f"walker-sharded dp{world}" if world > 1 else "single"
+        self.scaling = "strong"
+        self.last = None
+
+    def _step(self, frames):
+        self.last = self.pcv.close_replay(frames, self.wl.eps, grad=True)
+        return self.last
+
+    def step_device(self):
+        return self._step(self.frames_dev)
+
+    def step_e2e(self):
+        import torch
+
+        out = self._step(self.frames_host.to(self.device, non_blocking=True))
+        host = [out[k].to("cpu", non_blocking=True) for k in ("s", "z", "refresh", "dxy")]
+        torch.cuda.current_stream().synchronize()
+        return host
+
+    def e2e_bytes(self):
+        return self.T * self.n * 12, self.T * (8 + 8 + 1 + 8)
+
+    def units(self):
+        return self.T
+
+    def kernel_work(self, name):
+        T, n, L = self.T, self.n, self.L
+        if name == "mc_cov_f64":
+            return "fp64_flop", 18.0 * n * T * L
+        if name == "mc_fit_dense":
+            return "bytes", T * L * (72 + 8 + 72 + 1)
+        return "bytes", 0.0
+
+    def extra(self):
+        d = {"walkers": self.W_all, "walkers_per_rank": self.Wloc, "steps": self.steps}
+        if self.last is not None:
             d["refresh_fraction"] = float(self.last["refresh"].float().mean().item())
         return d
 
@@ -336,8 +403,12 @@ def run_ours(args, rank, world, local_rank):
         dist_mod.init_process_group("nccl", device_id=device)
         dist = dist_mod
     cfg = args.config
-    runner = Config01(cfg, device, rank, world) if cfg in (0, 1) else ConfigTC(cfg, device, rank, world,
-                                                                               args.frames)
+    if cfg in (0, 1):
+        runner = Config01(cfg, device, rank, world)
+    elif cfg == 3:
+        runner = Config3(device, rank, world, args.walkers)
+    else:
+        runner = ConfigTC(cfg, device, rank, world, args.frames)
     for _ in range(args.warmup):
         runner.step_device()
     torch.cuda.synchronize()
@@ -431,7 +502,7 @@ def _cpu_fn(cfg, wl):
 
     if cfg == 0:
         return lambda fr: C.path_cv_exact(fr, wl.landmarks, wl.lam, wl.q)
-    if cfg == 1:
+    if cfg in (1, 3):
         return lambda fr: C.close_replay(fr, wl.landmarks, wl.lam, wl.eps, wl.q)
     if cfg == 2:
         return lambda fr: C.msd_matrix(fr, wl.landmarks[:256])
@@ -444,13 +515,18 @@ def cpu_baseline(cfg, runner, args, seconds=12.0):
 
     threads = C.max_threads()
     wl = runner.wl
-    frames = wl.frames if cfg in (0, 1) else wl.frames[:256].double().cpu().numpy()
+    if cfg in (0, 1):
+        frames = wl.frames
+    elif cfg == 3:
+        frames = wl.frames[0].double().cpu().numpy()  # walker 0's trajectory (sequential chain)
+    else:
+        frames = wl.frames[:256].double().cpu().numpy()
     fn = _cpu_fn(cfg, wl)
-    k = min(frames.shape[0], 4 if cfg in (2, 4) else 64)
+    k = min(frames.shape[0], 4 if cfg in (2, 4) else (16 if cfg == 3 else 64))
     t0 = time.perf_counter()
     fn(frames[:k])
     dt = time.perf_counter() - t0
-    if cfg in (0, 1):
+    if cfg in (0, 1, 3):
         k2 = int(min(frames.shape[0], max(k, k * seconds / max(dt, 1e-6))))
         t0 = time.perf_counter()
         fn(frames[:k2])
@@ -480,6 +556,10 @@ def run_reference(args, rank, world):
         wl = synth.config0() if cfg == 0 else synth.config1()
         sample = wl.frames if cfg == 0 else wl.frames[:1000]
         L, n = wl.landmarks.shape[0], wl.frames.shape[1]
+    elif cfg == 3:
+        wl = synth.walkers_device(3, 256, 1000, 2500, 2048, "cpu", 0, 1)
+        sample = wl.frames[0, :60].double().numpy()
+        L, n = 2048, 2500
     else:
         shp = CONFIG_SHAPES[cfg]
         rng_frames = 16 if cfg == 2 else 4
@@ -531,6 +611,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=0, help="override T (configs 2/4) for quick runs")
+    ap.add_argument("--walkers", type=int, default=0, help="override W (config 3) for quick runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))

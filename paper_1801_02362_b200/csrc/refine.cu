@@ -172,20 +172,31 @@ refine_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int e = 0; e < 9; ++e) acc[a][c][e] = 0.0;
-    double rf[3], rl[3];
+    // raw fp32 loads are issued one chunk ahead (gload) and only converted /
+    // recentred when they are staged (sstore), so the load latency overlaps
+    // the previous chunk's FMAs instead of stalling at the issue point
+    float pf[3], pl[3];
+    double pw;
+    bool vf, vl;
     auto gload = [&](int k0) {
       const int j = k0 + ls_atom;
-      if (my_t >= 0 && j < n) {
+      vf = my_t >= 0 && j < n;
+      vl = my_l < L && j < n;
+      if (vf) {
         const float* p = fr + ((int64_t)my_t * n + j) * 3;
-        rf[0] = (double)p[0] - fcx; rf[1] = (double)p[1] - fcy; rf[2] = (double)p[2] - fcz;
-      } else { rf[0] = rf[1] = rf[2] = 0.0; }
-      if (my_l < L && j < n) {
+        pf[0] = p[0]; pf[1] = p[1]; pf[2] = p[2];
+      }
+      if (vl) {
         const float* p = lr + ((int64_t)my_l * n + j) * 3;
-        const double wj = w[j];
-        rl[0] = wj * ((double)p[0] - lcx); rl[1] = wj * ((double)p[1] - lcy); rl[2] = wj * ((double)p[2] - lcz);
-      } else { rl[0] = rl[1] = rl[2] = 0.0; }
+        pl[0] = p[0]; pl[1] = p[1]; pl[2] = p[2];
+        pw = w[j];
+      }
     };
     auto sstore = [&](int buf) {
+      const double rf[3] = {vf ? (double)pf[0] - fcx : 0.0, vf ? (double)pf[1] - fcy : 0.0,
+                            vf ? (double)pf[2] - fcz : 0.0};
+      const double rl[3] = {vl ? pw * ((double)pl[0] - lcx) : 0.0, vl ? pw * ((double)pl[1] - lcy) : 0.0,
+                            vl ? pw * ((double)pl[2] - lcz) : 0.0};
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
         sF[buf][(ls_atom * 3 + b) * RRS + ls_struct] = rf[b];

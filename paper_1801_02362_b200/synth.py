@@ -208,6 +208,44 @@ def config4(seed=4, T=131072, L=8192, N=10000, n_endpoints=32):
 CONFIGS = {0: config0, 1: config1, 2: config2, 3: config3, 4: config4}
 
 
+def walkers_device(seed, W, steps, N, L, device, walker_offset=0, walker_count=None, step_noise=0.003,
+                   n_endpoints=2, eps_factor=0.1):
+    """Config 3 generated on the GPU: same distributions as ``config3`` (per-walker
+    accumulated coordinate noise from a start on the path, fresh rigid motion per
+    step).  Landmarks, lambda, eps and the walker starts come from numpy (seeded)
+    so every rank agrees; walker w's trajectory is drawn from a generator seeded
+    by (seed, w), so walker shards are slices of one global walker set."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    ends = rng.normal(0.0, 0.3, size=(n_endpoints, N, 3))
+    lms = make_landmarks(rng, ends, L, dtype=np.float32)
+    p0 = rng.uniform(0.0, L - 1, size=W)
+    wl = _finish(f"walkers{seed}", None, lms, eps_factor=eps_factor)
+    walker_count = W - walker_offset if walker_count is None else walker_count
+    starts = torch.from_numpy(path_points(ends, p0[walker_offset:walker_offset + walker_count], L)).to(device)
+    frames = torch.empty((walker_count, steps, N, 3), dtype=torch.float32, device=device)
+    for k in range(walker_count):
+        g = torch.Generator(device=device).manual_seed(seed * 7_919 + walker_offset + k)
+        start = starts[k] + torch.randn((N, 3), generator=g, device=device, dtype=torch.float64) * 0.02
+        noise = torch.randn((steps, N, 3), generator=g, device=device, dtype=torch.float64) * step_noise
+        noise[0] = 0.0
+        cur = start[None] + torch.cumsum(noise, dim=0)
+        q = torch.randn((steps, 4), generator=g, device=device, dtype=torch.float64)
+        q = q / q.norm(dim=1, keepdim=True)
+        q0, q1, q2, q3 = q.unbind(1)
+        rot = torch.stack([
+            torch.stack([q0 * q0 + q1 * q1 - q2 * q2 - q3 * q3, 2 * (q1 * q2 - q0 * q3), 2 * (q1 * q3 + q0 * q2)], -1),
+            torch.stack([2 * (q1 * q2 + q0 * q3), q0 * q0 - q1 * q1 + q2 * q2 - q3 * q3, 2 * (q2 * q3 - q0 * q1)], -1),
+            torch.stack([2 * (q1 * q3 - q0 * q2), 2 * (q2 * q3 + q0 * q1), q0 * q0 - q1 * q1 - q2 * q2 + q3 * q3], -1),
+        ], -2)
+        trans = torch.rand((steps, 1, 3), generator=g, device=device, dtype=torch.float64) * 2 - 1
+        frames[k] = (torch.einsum("kab,kjb->kja", rot, cur) + trans).float()
+    wl.frames = frames
+    wl.meta.update(generator="device (torch, per-walker seeded)", p0=p0)
+    return wl
+
+
 def interp_config_device(seed, T, L, N, n_endpoints, device, frame_offset=0, frame_count=None,
                          sigma_lo=1e-3, sigma_hi=0.5, chunk=4096):
     """Configs 2/4 generated on the GPU (torch RNG): same distributions as

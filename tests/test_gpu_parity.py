@@ -194,3 +194,22 @@ def test_eps_zero_equals_exact(cuda_device):
     assert bool(cl["refresh"].all())
     np.testing.assert_allclose(cl["s"].cpu().numpy(), ex["s"].cpu().numpy(), rtol=1e-12)
     np.testing.assert_allclose(cl["ds"].cpu().numpy(), ex["ds"].cpu().numpy(), atol=1e-14)
+
+
+def test_config3_walkers_slice_vs_oracle(cuda_device):
+    """Config-3 generator (device) at reduced size: per-walker close structure,
+    refresh logs identical, s/z/gradients vs the per-walker oracle replay."""
+    from paper_1801_02362_b200 import synth as S
+
+    wl = S.walkers_device(3, 256, 40, 60, 48, cuda_device, walker_offset=5, walker_count=3)
+    out = engine.close_structure_replay(wl.frames, wl.landmarks, wl.lam, wl.eps)
+    fr = wl.frames.double().cpu().numpy()
+    for k in range(3):
+        ref = O.close_structure_replay(fr[k], wl.landmarks.astype(np.float64), wl.lam, wl.eps)
+        sl = slice(k * 40, (k + 1) * 40)
+        np.testing.assert_array_equal(out["refresh"].cpu().numpy()[sl], ref["refresh"])
+        np.testing.assert_allclose(out["s"].cpu().numpy()[sl], ref["s"], rtol=1e-6)
+        np.testing.assert_allclose(out["z"].cpu().numpy()[sl], ref["z"], rtol=1e-6, atol=1e-9)
+        assert_grad(out["ds"].cpu().numpy()[sl], ref["ds"])
+        assert_grad(out["dz"].cpu().numpy()[sl], ref["dz"])
+    assert 0 < out["refresh"].sum() < 120
