@@ -14,7 +14,7 @@ from .errors import (ConfigError, DegenerateFitError, DeviceError, EmptyActiveSe
                      InvalidStructureError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcb200.so")
+LIB_PATH = os.environ.get("MCB200_LIB") or os.path.join(_HERE, "libmcb200.so")
 
 MC_OK = 0
 MC_ERR_INVALID_STRUCTURE = -1

@@ -121,10 +121,17 @@ cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n,
 // ------------------------------------------------------------------ K2/K3
 namespace gemm {
 constexpr int BM = 128;            // frames per tile (TMEM lanes)
-constexpr int BL = 48;             // landmarks per tile
+#ifndef MC_TF32_BL
+#define MC_TF32_BL 48
+#endif
+#ifndef MC_TF32_KB
+#define MC_TF32_KB 16
+#endif
+constexpr int BL = MC_TF32_BL;     // landmarks per tile
 constexpr int BN = 3 * BL;         // 144 accumulator columns per frame plane
-constexpr int KB = 16;             // atoms per pipeline stage (64 B rows, SWIZZLE_64B)
-constexpr int STAGES = 3;
+constexpr int KB = MC_TF32_KB;     // atoms per pipeline stage: 16 -> 64 B rows (SWIZZLE_64B), 8 -> 32 B (SWIZZLE_32B)
+constexpr int ROWB = KB * 4;       // bytes per operand row in shared memory
+constexpr int STAGES = KB == 16 ? 3 : 6;
 constexpr int A_BYTES = BM * KB * 4;        // 8 KB: one (plane, hi|lo) frame tile
 constexpr int B_BYTES = BN * KB * 4;        // 9 KB: hi or lo, 3 landmark planes stacked
 constexpr int BP_BYTES = BL * KB * 4;       // 3 KB: one landmark plane box
@@ -173,8 +180,9 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
 // SM100 UMMA shared-memory descriptor, K-major, SWIZZLE_64B (64 B rows,
 // 8-row groups 512 B apart): start>>4 | LBO=1 | SBO=32 | version 1 | layout 4
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+  // SBO = 8 rows x ROWB bytes; layout 4 = SWIZZLE_64B, 6 = SWIZZLE_32B
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * gemm::ROWB) >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)(gemm::ROWB == 64 ? 4 : 6) << 61);
 }
 
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
@@ -406,7 +414,7 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int kpad, int box
   cuuint32_t box[2] = {(cuuint32_t)gemm::KB, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, gemm::ROWB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
