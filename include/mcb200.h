@@ -161,6 +161,11 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
                          const double* lcen, const double* w, const double* w_align, const int32_t* sig_idx,
                          const double* sig_coef, const int32_t* nsig, const double* fvec, const int32_t* perm,
                          void* ds, void* dz, int32_t out_f32, void* stream);
+/* mc_msd_tf32 on CTA pairs (tcgen05.mma.cta_group::2, M = 256 frames per pair):
+ * same inputs/outputs; each SM stages half of the landmark operand. */
+int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const float* llo, const double* gx,
+                    const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+                    void* stream);
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
                   int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream);

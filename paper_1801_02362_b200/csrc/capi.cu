@@ -123,6 +123,15 @@ int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double
                                         S_(stream)));
 }
 
+int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const float* llo, const double* gx,
+                    const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+                    void* stream) {
+  if (T < 0 || L < 0 || kpad % 16 != 0 || kpad < 16 || ldd < L) return MC_ERR_CONFIG;
+  if ((int64_t)T * L > 0 && (!fhi || !flo || !lhi || !llo || !gx || !ga || !D)) return MC_ERR_CONFIG;
+  if (3LL * T > 0x7fffffffLL || 3LL * L > 0x7fffffffLL) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_msd_tf32_2sm(fhi, flo, lhi, llo, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
+}
+
 int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const float* lraw,
                          const double* lcen, const double* w, const double* w_align, const int32_t* sig_idx,
                          const double* sig_coef, const int32_t* nsig, const double* fvec, const int32_t* perm,

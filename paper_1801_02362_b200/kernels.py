@@ -279,11 +279,16 @@ def center_split(coords, w_align, w_disp, weighted, moments=False):
     return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad)
 
 
-def msd_tf32(fr: Split, lm: Split, D=None, grid=0):
-    """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L])."""
+TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "1") == "1"
+
+
+def msd_tf32(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
+    """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L]).
+    two_sm (default: env MC_TF32_2SM, on) selects the CTA-pair kernel."""
     T, L = fr.count, lm.count
     if D is None:
         D = torch.empty((T, L), dtype=torch.float32, device=fr.hi.device)
-    call("mc_msd_tf32", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo), ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D),
+    name = "mc_msd_tf32_2sm" if (TF32_2SM if two_sm is None else two_sm) else "mc_msd_tf32"
+    call(name, ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo), ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D),
          D.stride(0), grid, stream_ptr())
     return D
