@@ -284,6 +284,12 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
+#ifdef MC_TF32_NOTMA
+          // diagnostic build only: MMAs run on stale shared memory, no operand traffic
+          mbar_arrive(&full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
+#endif
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           const int k0 = kb * KB;
 #pragma unroll
@@ -319,16 +325,18 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
 #pragma unroll
           for (int k = 0; k < KB / 8; ++k) {
             const uint32_t koff = k * 32;  // 8 tf32 = 32 B inside the 64 B swizzled row
+            const uint64_t dbh = umma_desc_sw64(bh + koff);
+            const uint64_t dbl = umma_desc_sw64(bl + koff);
+            // term-major order: consecutive MMAs target different accumulators,
+            // so no MMA waits on the read-modify-write of the one before it
 #pragma unroll
-            for (int p = 0; p < 3; ++p) {
-              const uint32_t d = tmem_base + p * BN;
-              const uint64_t ah = umma_desc_sw64(st + (2 * p) * A_BYTES + koff);
-              const uint64_t al = umma_desc_sw64(st + (2 * p + 1) * A_BYTES + koff);
-              const uint64_t dbh = umma_desc_sw64(bh + koff);
-              const uint64_t dbl = umma_desc_sw64(bl + koff);
-              umma_tf32(d, ah, dbh, (kb | k) != 0);
-              umma_tf32(d, ah, dbl, 1u);
-              umma_tf32(d, al, dbh, 1u);
+            for (int term = 0; term < 3; ++term) {
+#pragma unroll
+              for (int p = 0; p < 3; ++p) {
+                const uint32_t d = tmem_base + p * BN;
+                const uint64_t a = umma_desc_sw64(st + (2 * p + (term == 2 ? 1 : 0)) * A_BYTES + koff);
+                umma_tf32(d, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
+              }
             }
           }
           umma_commit(&empty[stage]);

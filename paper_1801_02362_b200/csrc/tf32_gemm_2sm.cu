@@ -237,16 +237,17 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
 #pragma unroll
             for (int k = 0; k < KB / 8; ++k) {
               const uint32_t koff = k * 32;
+              const uint64_t dbh = desc_sw64(bh + koff);
+              const uint64_t dbl = desc_sw64(bl + koff);
+              // term-major: consecutive MMAs hit different accumulators
 #pragma unroll
-              for (int p = 0; p < 3; ++p) {
-                const uint32_t d = tmem_base + p * BN;
-                const uint64_t ah = desc_sw64(st + (2 * p) * A_BYTES + koff);
-                const uint64_t al = desc_sw64(st + (2 * p + 1) * A_BYTES + koff);
-                const uint64_t dbh = desc_sw64(bh + koff);
-                const uint64_t dbl = desc_sw64(bl + koff);
-                mma2_tf32(d, ah, dbh, (kb | k) != 0);
-                mma2_tf32(d, ah, dbl, 1u);
-                mma2_tf32(d, al, dbh, 1u);
+              for (int term = 0; term < 3; ++term) {
+#pragma unroll
+                for (int p = 0; p < 3; ++p) {
+                  const uint32_t d = tmem_base + p * BN;
+                  const uint64_t a = desc_sw64(st + (2 * p + (term == 2 ? 1 : 0)) * A_BYTES + koff);
+                  mma2_tf32(d, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
+                }
               }
             }
             commit2_both(&empty[stage]);
