@@ -20,7 +20,7 @@ constexpr int RS = TF + 2;          // padded row stride (doubles), keeps double
 constexpr int LOADS = TF * 3 * KC / NT;  // 3 per thread per operand
 }
 
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 2)
 cov_f64_kernel(const double* __restrict__ fpl, const double* __restrict__ lpl, int T, int L, int npad,
                double* __restrict__ S) {
   __shared__ __align__(16) double sF[2][KC * 3 * RS];

@@ -121,7 +121,7 @@ constexpr int RLOADS = RF * RKC / RNT;  // atoms*structures per thread per chunk
 // Frame group g = perm[32g .. 32g+32); its window = union of [lo_t, lo_t+cnt_t).
 // Outputs per in-window pair: Dex[t*cap + (l - lo_t)] (fp64), Rex[...*9] (nullable),
 // and when dense (lo == nullptr) Dd[t*ldd + l] (fp32).
-__global__ void __launch_bounds__(RNT)
+__global__ void __launch_bounds__(RNT, 2)
 refine_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const float* __restrict__ lr,
               const double* __restrict__ lc, const double* __restrict__ w, const double* __restrict__ gx,
               const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,

@@ -73,6 +73,32 @@ def test_pathcv_tc_config4_slice_vs_oracle(cuda_device):
         assert_msd(Dw[t, : cnt[t]], ref["D"][t, lo[t]: lo[t] + cnt[t]])
 
 
+def test_cta_pair_kernel_matches_single_cta_kernel(cuda_device):
+    """cta_group::2 and cta_group::1 variants compute the same sums (ragged T, L)."""
+    wl = synth.config2(seed=9, T=300, L=101, N=333)
+    dev = torch.device("cuda:0")
+    n = wl.frames.shape[1]
+    w = engine.normalise_weights(None, n, "d", dev)
+    fs = K.center_split(torch.from_numpy(wl.frames).to(dev), w, w, weighted=False)
+    ls = K.center_split(torch.from_numpy(wl.landmarks).to(dev), w, w, weighted=True)
+    d1 = K.msd_tf32(fs, ls, two_sm=False).cpu().numpy()
+    d2 = K.msd_tf32(fs, ls, two_sm=True).cpu().numpy()
+    ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64))
+    assert np.abs(d1 - ref).max() < 5e-6 and np.abs(d2 - ref).max() < 5e-6
+    assert np.abs(d1 - d2).max() < 2e-6
+
+
+def test_window_cap_overflow_retries_with_wider_windows(cuda_device):
+    """A window cap smaller than the significant set triggers the wider retry; results unchanged."""
+    wl = synth.config4(T=24, L=256, N=200)
+    ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam, window_cap=4)
+    out = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    assert int(out["window_cnt"].max()) > 4
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+
+
 def test_tf32_weighted(cuda_device):
     rng = np.random.default_rng(2)
     n = 77
