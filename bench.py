@@ -317,12 +317,31 @@ class ConfigTC:
         return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
 
     def step_e2e(self):
-        """Public API with host frames: chunked H2D -> evaluate -> D2H of the result."""
+        """Public API with host frames: chunked H2D on a copy stream, double-buffered
+        against the compute of the previous chunk, then D2H of the result."""
         import torch
 
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        comp = torch.cuda.current_stream()
+        cps = self._copy_stream
         outs = []
-        for c0 in range(0, self.T, self.chunk):
-            fr = self.frames_host[c0:c0 + self.chunk].to(self.device, non_blocking=True)
+        chunks = list(range(0, self.T, self.chunk))
+
+        def issue(c0):
+            with torch.cuda.stream(cps):
+                buf = self.frames_host[c0:c0 + self.chunk].to(self.device, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cps)
+            return buf, ev
+
+        nxt = issue(chunks[0]) if chunks else None
+        for i, c0 in enumerate(chunks):
+            fr, ev = nxt
+            if i + 1 < len(chunks):
+                nxt = issue(chunks[i + 1])
+            comp.wait_event(ev)
+            fr.record_stream(comp)
             if self.cfg == 2:
                 D = self._step(fr)
                 outs.append(D.to("cpu", non_blocking=True))
@@ -330,7 +349,7 @@ class ConfigTC:
                 o = self._step(fr)
                 outs.append(o["s"].to("cpu", non_blocking=True))
                 outs.append(o["z"].to("cpu", non_blocking=True))
-        torch.cuda.current_stream().synchronize()
+        comp.synchronize()
         return outs
 
     def e2e_bytes(self):
@@ -343,7 +362,7 @@ class ConfigTC:
 
     def kernel_work(self, name):
         T, n, L = self.T, self.n, self.L
-        if name == "mc_msd_tf32":
+        if name in ("mc_msd_tf32", "mc_msd_tf32_2sm"):
             return "tensor_flop", 3.0 * 18.0 * n * T * L
         if name == "mc_refine":
             return "fp64_flop", 18.0 * n * T * L if self.cfg == 2 else 0.0
@@ -460,9 +479,14 @@ def run_ours(args, rank, world, local_rank):
                 "peak_src": pk["src"]}
     elif kind == "tensor_flop":
         ach = amount / (avg_ms * 1e-3) / 1e12
-        peak = pk["bf16"] / 2.0
+        # the kernel runs for ~1 s inside a multi-second step: the sustained
+        # (power-capped) figure is the right denominator; burst reported beside it
+        sustained = pk.get("bf16_sustained") or pk["bf16"]
+        peak = sustained / 2.0
         roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "peak_src": f"TF32 = bf16_tflops/2 from {pk['src']} (TF32 runs at half the bf16 rate)",
+                "peak_src": f"TF32 = bf16_tflops_sustained/2 from {pk['src']} (TF32 runs at half the bf16 rate; "
+                            "kernel timed inside a long step)",
+                "peak_burst": pk["bf16"] / 2.0, "frac_of_burst": ach / (pk["bf16"] / 2.0),
                 "cublas_tf32_measured": tf32_cublas, "flop_basis": "executed 3xTF32 (3 x 18 n per pair)"}
     else:
         ach = amount / (avg_ms * 1e-3) / 1e12

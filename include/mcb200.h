@@ -115,6 +115,9 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
 
 /* K4 — property-map s (Eq. 2), path-CV z, and their gradients
  * through Eq. 4 (exact rows) or Eq. 5/6 (non-refresh rows).
+ * Both process frames t0 .. t0+T-1 of the (global) frame arrays; the
+ * significant-list buffers (sig_idx, sig_coef, nsig, fvec, flags) are local to
+ * the launch (row t - t0), so long trajectories are processed in chunks.
  * mc_pathcv_weights: per frame — min/LSE, s, z, significant-landmark list
  *   (sig_idx [T,cap], sig_coef [T,cap,18]), nsig [T], fvec [T,16]; writes the
  *   Eq. 5 distances of non-refresh rows into D.  refresh == NULL: all rows exact.
@@ -126,13 +129,13 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
  *   out_f32).  Coordinates from centred fp64 planes, or (fplanes/lplanes NULL)
  *   from raw fp32 AoS input + fp64 centroids.  perm (nullable): frame visiting order
  *   (the candidate sort, so neighbouring CTAs share landmarks in L2). */
-int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
+int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
                       const int32_t* rowcnt, double* D, const double* q, const double* R, const double* fwbar,
                       const double* lwbar, const uint8_t* refresh, const int32_t* ridx, const double* S,
                       const double* rxy, const double* xyeig, const double* gx, const double* ga, const double* lmom,
                       double* s, double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec,
                       uint8_t* flags, void* stream);
-int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
+int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
                    const double* xyeig, void* ds, void* dz, int32_t out_f32, const float* fraw, const double* fcen,

@@ -50,9 +50,9 @@ _SIGS = {
     "mc_window_pairs": [_I32, _I32, _I32, _P, _P, _P],
     "mc_close_scan": [_P, _P, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P, _P, _P],
     "mc_xy_eig": [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P],
-    "mc_pathcv_weights": [_I32, _I32, _D, _D, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+    "mc_pathcv_weights": [_I32, _I32, _I32, _D, _D, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32,
+    "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
     "mc_center_split": [_P, ctypes.c_int, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
     "mc_msd_tf32": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P],

@@ -89,13 +89,13 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
   return cuda_status(mc::launch_xy_eig(fplanes, gx, T, npad, w, refresh, ridx, xyeig, rxy, flags, S_(stream)));
 }
 
-int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
+int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
                       const int32_t* rowcnt, double* D, const double* q, const double* R, const double* fwbar,
                       const double* lwbar, const uint8_t* refresh, const int32_t* ridx, const double* S,
                       const double* rxy, const double* xyeig, const double* gx, const double* ga, const double* lmom,
                       double* s, double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec,
                       uint8_t* flags, void* stream) {
-  if (T < 0) return MC_ERR_CONFIG;
+  if (T < 0 || t0 < 0) return MC_ERR_CONFIG;
   if (T > 0 && L < 1) return MC_ERR_EMPTY_ACTIVE_SET;
   if (!(lam > 0.0) || !(cutoff > 0.0) || cap < 1) return MC_ERR_CONFIG;
   if ((rowlo == nullptr) != (rowcnt == nullptr)) return MC_ERR_CONFIG;
@@ -103,21 +103,26 @@ int mc_pathcv_weights(int32_t T, int32_t L, double lam, double cutoff, int32_t c
   if (T > 0 && (!D || !q || !R || !fwbar || !lwbar || !s || !z || !sig_idx || !sig_coef || !nsig || !fvec))
     return MC_ERR_CONFIG;
   if (refresh && (rowcnt || !ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_cv_weights(T, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh,
+  return cuda_status(mc::launch_cv_weights(T, t0, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh,
                                            ridx, S, rxy, xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec,
                                            flags, S_(stream)));
 }
 
-int mc_pathcv_grad(int32_t T, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
+int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,
                    const double* xyeig, void* ds, void* dz, int32_t out_f32, const float* fraw, const double* fcen,
                    const float* lraw, const double* lcen, const int32_t* perm, void* stream) {
-  if (T < 0 || bad_pad(n, npad) || cap < 1) return MC_ERR_CONFIG;
+  if (T < 0 || t0 < 0 || bad_pad(n, npad) || cap < 1) return MC_ERR_CONFIG;
   if (T > 0 && (!w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec || !ds || !dz)) return MC_ERR_CONFIG;
+  if (t0 > 0 && !(fplanes && lplanes && !perm)) return MC_ERR_CONFIG;  // chunked launches: planes path only
   if (T > 0 && !fplanes && !(fraw && fcen)) return MC_ERR_CONFIG;
   if (T > 0 && !lplanes && !(lraw && lcen)) return MC_ERR_CONFIG;
   if (refresh && (!ridx || !xyeig || !fplanes)) return MC_ERR_CONFIG;
+  if (fplanes && lplanes && !perm)  // fp64 planes: the frame-group blocked pass (grad_block.cu)
+    return cuda_status(mc::launch_cv_grad_block_planes(T, t0, n, npad, cap, fplanes, lplanes, w, w_align, sig_idx,
+                                                       sig_coef, nsig, fvec, refresh, ridx, xyeig, ds, dz, out_f32,
+                                                       S_(stream)));
   return cuda_status(mc::launch_cv_grad(T, n, npad, cap, fplanes, lplanes, w, w_align, sig_idx, sig_coef, nsig, fvec,
                                         refresh, ridx, xyeig, ds, dz, out_f32, fraw, fcen, lraw, lcen, perm,
                                         S_(stream)));

@@ -30,7 +30,7 @@ cudaError_t launch_close_scan(const double* fpl, const double* gx, int walkers, 
 cudaError_t launch_xy_eig(const double* fpl, const double* gx, int64_t T, int npad, const double* w,
                           const uint8_t* refresh, const int* ridx, double* xyeig, double* rxy, uint8_t* flags,
                           cudaStream_t stream);
-cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
+cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
                               const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
                               const int* ridx, const double* S, const double* rxy, const double* xyeig,
@@ -49,6 +49,11 @@ cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const
                                  const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                  const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
                                  void* ds, void* dz, int out_f32, cudaStream_t stream);
+cudaError_t launch_cv_grad_block_planes(int T, int t0, int n, int npad, int cap, const double* fpl, const double* lpl,
+                                        const double* w, const double* wa, const int* sig_idx,
+                                        const double* sig_coef, const int* nsig, const double* fvec,
+                                        const uint8_t* refresh, const int* ridx, const double* xyeig, void* ds,
+                                        void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, int cap, int* lo,
                               int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);

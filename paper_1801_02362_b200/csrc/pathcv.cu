@@ -35,7 +35,7 @@ __device__ __forceinline__ void mat3_mul(const double* a, const double* b, doubl
 }
 
 __global__ void __launch_bounds__(WNT)
-cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, int ld, const int* __restrict__ rowlo,
+cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* __restrict__ rowlo,
                   const int* __restrict__ rowcnt, double* __restrict__ D,
                   const double* __restrict__ q, const double* __restrict__ R, const double* __restrict__ fwbar,
                   const double* __restrict__ lwbar, const uint8_t* __restrict__ refresh,
@@ -46,7 +46,9 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, int ld, cons
                   double* __restrict__ fvec, uint8_t* __restrict__ flags) {
   __shared__ double scratch[WNT / 32];
   __shared__ int wcount[WNT / 32];
-  const int t = blockIdx.x;
+  // frame t (global index; rows of D/S/R and the per-frame inputs) and its
+  // chunk-local slot tl (the significant-list outputs of this launch)
+  const int t = t0 + blockIdx.x, tl = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool approx = refresh && !refresh[t];
   const int r = approx ? ridx[t] : t;
@@ -132,8 +134,8 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, int ld, cons
         for (int e = 0; e < 9; ++e) Rh[e] = R[((int64_t)t * ld + i) * 9 + e];
       }
       if (pos < cap) {
-        sig_idx[(int64_t)t * cap + pos] = li;
-        double* co = sig_coef + ((int64_t)t * cap + pos) * 18;
+        sig_idx[(int64_t)tl * cap + pos] = li;
+        double* co = sig_coef + ((int64_t)tl * cap + pos) * 18;
 #pragma unroll
         for (int e = 0; e < 9; ++e) { co[e] = cs * Rh[e]; co[9 + e] = cz * Rh[e]; }
       }
@@ -179,8 +181,8 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, int ld, cons
   if (tid != 0) return;
   s_out[t] = sval;
   z_out[t] = zval;
-  nsig[t] = min(total, cap);
-  double* fv = fvec + (int64_t)t * FVEC;
+  nsig[tl] = min(total, cap);
+  double* fv = fvec + (int64_t)tl * FVEC;
   const double fw[3] = {fwbar[3 * t], fwbar[3 * t + 1], fwbar[3 * t + 2]};
   double corr[2][3], vv[2][4];
   for (int c = 0; c < 2; ++c) {
@@ -229,11 +231,11 @@ cv_weights_kernel(int T, int L, double lam, double cutoff, int cap, int ld, cons
     uint8_t f = 0;
     if (total > cap) f |= kFlagSigOverflow;
     if (nonfinite || !isfinite(sval) || !isfinite(zval)) f |= kFlagNonFinite;
-    flags[t] = f;
+    flags[tl] = f;
   }
 }
 
-cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
+cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
                               const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
                               const int* ridx, const double* S, const double* rxy, const double* xyeig,
@@ -241,7 +243,7 @@ cudaError_t launch_cv_weights(int T, int L, double lam, double cutoff, int cap, 
                               int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
                               cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
+  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, t0, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
                                            xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
   return cudaGetLastError();
 }

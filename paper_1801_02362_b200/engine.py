@@ -164,22 +164,43 @@ class PathCV:
         out.update(refresh=close["refresh"].bool(), dxy=close["dxy"], ridx=close["ridx"], onthefly=close["onthefly"])
         return out
 
+    # significant-list buffers per chunk are bounded to ~this many bytes
+    CHUNK_BYTES = 4 << 30
+
     def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype):
-        cap = self._cap(cap)
-        while True:
-            wres = K.pathcv_weights(D, self.q, self.lam, R, fr, self.lm, cap, self.cutoff, close=close, S=S)
-            f = _or_flags(wres["flags"])
-            if f & FLAG_SIG_OVERFLOW and cap < self.L:
-                cap = self.L
-                continue
-            break
-        if f & FLAG_NON_FINITE:
-            raise InvalidStructureError("non-finite distances in the path-CV reduction")
-        out = {"s": wres["s"], "z": wres["z"], "D": D}
+        T = D.shape[0]
+        cap0 = self._cap(cap)
+        dev = D.device
+        s = torch.empty((T,), dtype=torch.float64, device=dev)
+        z = torch.empty((T,), dtype=torch.float64, device=dev)
+        nsig = torch.empty((T,), dtype=torch.int32, device=dev)
+        ds = dz = None
         if grad:
             odt = out_dtype or (torch.float64 if raw.dtype == torch.float64 else torch.float32)
-            out["ds"], out["dz"] = K.pathcv_grad(wres, fr, self.lm, self.w, self.wa, cap, odt, close=close)
-        out["nsig"] = wres["nsig"]
+            ds = torch.empty((T, self.n, 3), dtype=odt, device=dev)
+            dz = torch.empty((T, self.n, 3), dtype=odt, device=dev)
+        t0 = 0
+        while t0 < T:
+            cap = cap0
+            chunk = max(8, min(T - t0, self.CHUNK_BYTES // (cap * 160)))
+            while True:
+                wres = K.pathcv_weights(D, self.q, self.lam, R, fr, self.lm, cap, self.cutoff, close=close, S=S,
+                                        t0=t0, count=chunk, s=s, z=z)
+                f = _or_flags(wres["flags"])
+                if f & FLAG_SIG_OVERFLOW and cap < self.L:
+                    cap = self.L
+                    chunk = max(8, min(chunk, self.CHUNK_BYTES // (cap * 160)))
+                    continue
+                break
+            if f & FLAG_NON_FINITE:
+                raise InvalidStructureError("non-finite distances in the path-CV reduction")
+            nsig[t0:t0 + chunk] = wres["nsig"]
+            if grad:
+                K.pathcv_grad(wres, fr, self.lm, self.w, self.wa, cap, odt, close=close, ds=ds, dz=dz)
+            t0 += chunk
+        out = {"s": s, "z": z, "D": D, "nsig": nsig}
+        if grad:
+            out["ds"], out["dz"] = ds, dz
         return out
 
 

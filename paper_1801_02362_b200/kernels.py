@@ -151,34 +151,39 @@ def close_decisions(fr: Centred, w, eps, walkers, steps, window=8):
             "onthefly": fly}
 
 
-def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L=None, rowlo=None, rowcnt=None):
-    """K4 weights.  D/R rows are dense [T, L] or sparse windows [T, ld] (rowlo/rowcnt)."""
-    T, ld = D.shape
+def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L=None, rowlo=None, rowcnt=None,
+                   t0=0, count=None, s=None, z=None):
+    """K4 weights for frames t0 .. t0+count-1.  D/R rows are dense [T, L] or sparse
+    windows [T, ld] (rowlo/rowcnt); the significant-list outputs are chunk-local."""
+    Ttot, ld = D.shape
+    T = Ttot - t0 if count is None else count
     L = ld if L is None else L
     dev = D.device
-    s = torch.empty((T,), dtype=F64, device=dev)
-    z = torch.empty((T,), dtype=F64, device=dev)
+    s = torch.empty((Ttot,), dtype=F64, device=dev) if s is None else s
+    z = torch.empty((Ttot,), dtype=F64, device=dev) if z is None else z
     sig_idx = torch.empty((T, cap), dtype=I32, device=dev)
     sig_coef = torch.empty((T, cap, 18), dtype=F64, device=dev)
     nsig = torch.empty((T,), dtype=I32, device=dev)
     fvec = torch.empty((T, 16), dtype=F64, device=dev)
     flags = torch.empty((T,), dtype=U8, device=dev)
     c = close or {}
-    call("mc_pathcv_weights", T, L, float(lam), float(cutoff), cap, ld, ptr(rowlo), ptr(rowcnt), ptr(D), ptr(q), ptr(R),
+    call("mc_pathcv_weights", T, t0, L, float(lam), float(cutoff), cap, ld, ptr(rowlo), ptr(rowcnt), ptr(D), ptr(q), ptr(R),
          ptr(fr.wbar), ptr(lm.wbar),
          ptr(c.get("refresh")), ptr(c.get("ridx")), ptr(S if close else None), ptr(c.get("rxy")), ptr(c.get("xyeig")),
          ptr(fr.g if close else None), ptr(lm.g if close else None), ptr(lm.mom if close else None),
          ptr(s), ptr(z), ptr(sig_idx), ptr(sig_coef), ptr(nsig), ptr(fvec), ptr(flags), stream_ptr())
-    return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags}
+    return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags,
+            "t0": t0, "count": T}
 
 
-def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=None, perm=None):
-    """K4 gradient pass.  fr/lm: Centred (fp64 planes) or, with raw=(frames, landmarks)
-    fp32 AoS tensors, Split objects (centroids used to recentre on the fly)."""
-    T, n = fr.count, fr.n
+def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=None, perm=None, ds=None, dz=None):
+    """K4 gradient pass for the frames of ``wres`` (t0, count).  fr/lm: Centred (fp64
+    planes) or, with raw=(frames, landmarks) fp32 AoS tensors, Split objects."""
+    Ttot, n = fr.count, fr.n
+    t0, T = wres.get("t0", 0), wres.get("count", Ttot)
     dev = wres["s"].device
-    ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
-    dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
+    ds = torch.empty((Ttot, n, 3), dtype=out_dtype, device=dev) if ds is None else ds
+    dz = torch.empty((Ttot, n, 3), dtype=out_dtype, device=dev) if dz is None else dz
     c = close or {}
     if raw is None:
         fpl, lpl, fraw, fcen, lraw, lcen = fr.planes, lm.planes, None, None, None, None
@@ -188,7 +193,7 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
         fraw, lraw = raw
         fcen, lcen = fr.centroid, lm.centroid
         npad = npad_for(n)
-    call("mc_pathcv_grad", T, n, npad, cap, ptr(fpl), ptr(lpl), ptr(w), ptr(w_align),
+    call("mc_pathcv_grad", T, t0, n, npad, cap, ptr(fpl), ptr(lpl), ptr(w), ptr(w_align),
          ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(c.get("refresh")),
          ptr(c.get("ridx")), ptr(c.get("xyeig")), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0,
          ptr(fraw), ptr(fcen), ptr(lraw), ptr(lcen), ptr(perm), stream_ptr())
