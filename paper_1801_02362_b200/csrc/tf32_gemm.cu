@@ -26,6 +26,7 @@
 //   warp 0: TMA producer   warp 1: MMA issuer (one elected lane)
 //   warp 2: TMEM allocator warps 4-7: epilogue (TMEM lane quarter = warp%4)
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "mc_math.cuh"
@@ -39,27 +40,70 @@ __device__ __forceinline__ float tf32_rna(float v) {
   return __uint_as_float(r);
 }
 
-template <typename T, int NT>
+// Operand formats.  TF32: hi/lo fp32 words holding TF32 values, unscaled.
+// F16: hi/lo IEEE halves of the structure's values times a power of two 2^e
+// chosen so every |value| < 2^14 (no overflow, no subnormal loss that
+// matters); hi + lo carries the same 22 significant bits as the TF32 pair,
+// the fp32 accumulation is identical, and the MMA (kind::f16, K = 16) moves
+// twice the atoms per byte and per tensor-core cycle.  scale_inv[b] = 2^-e
+// undoes the scaling exactly in the epilogue.
+struct OpTF32 {
+  using E = float;
+  static __device__ __forceinline__ void split(double v, E& h, E& l) {
+    h = tf32_rna((float)v);
+    l = tf32_rna((float)(v - (double)h));
+  }
+};
+struct OpF16 {
+  using E = __half;
+  static __device__ __forceinline__ void split(double v, E& h, E& l) {
+    h = __double2half(v);
+    l = __double2half(v - (double)__half2float(h));
+  }
+};
+
+template <typename T, typename OP, int NT>
 __global__ void __launch_bounds__(NT)
 center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, const double* __restrict__ w_align,
-                    const double* __restrict__ w_disp, int weighted, float* __restrict__ hi, float* __restrict__ lo,
-                    double* __restrict__ centroid, double* __restrict__ gnorm, double* __restrict__ wbar,
-                    double* __restrict__ mom, uint8_t* __restrict__ flags) {
+                    const double* __restrict__ w_disp, int weighted, typename OP::E* __restrict__ hi,
+                    typename OP::E* __restrict__ lo, double* __restrict__ scale_inv, double* __restrict__ centroid,
+                    double* __restrict__ gnorm, double* __restrict__ wbar, double* __restrict__ mom,
+                    uint8_t* __restrict__ flags) {
   __shared__ double scratch[NT / 32];
   const int64_t b = blockIdx.x;
   const T* x = coords + b * (int64_t)n * 3;
-  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, xmax = 0.0, wmax = 0.0;
   bool finite = true;
   for (int j = threadIdx.x; j < n; j += NT) {
     const double wa = w_align[j];
     const double x0 = (double)x[3 * j], x1 = (double)x[3 * j + 1], x2 = (double)x[3 * j + 2];
     finite = finite && isfinite(x0) && isfinite(x1) && isfinite(x2);
     c0 += wa * x0; c1 += wa * x1; c2 += wa * x2;
+    if (scale_inv) {
+      xmax = fmax(xmax, fmax(fabs(x0), fmax(fabs(x1), fabs(x2))));
+      if (weighted) wmax = fmax(wmax, fabs(w_disp[j]));
+    }
   }
   c0 = block_sum<NT>(c0, scratch);
   c1 = block_sum<NT>(c1, scratch);
   c2 = block_sum<NT>(c2, scratch);
   const int nonfinite = __syncthreads_or(!finite);
+  // power-of-two operand scale from a bound on |value| (F16 only)
+  double scale = 1.0;
+  if (scale_inv) {
+    double bound = -block_min<NT>(-xmax, scratch);
+    if (weighted) bound *= -block_min<NT>(-wmax, scratch);
+    // |x_j - c| <= 2 max|x| (c is a convex combination of the x_j)
+    bound *= 2.0;
+    int e = 0;
+    if (bound > 0.0 && isfinite(bound)) {
+      frexp(bound, &e);  // bound < 2^e
+      e = 14 - e;
+    }
+    e = max(-1000, min(1000, e));
+    scale = ldexp(1.0, e);
+    if (threadIdx.x == 0) scale_inv[b] = ldexp(1.0, -e);
+  }
   double g = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, m00 = 0, m01 = 0, m02 = 0, m11 = 0, m12 = 0, m22 = 0;
   const int64_t plane = B * (int64_t)kpad;
   for (int j = threadIdx.x; j < kpad; j += NT) {
@@ -78,9 +122,9 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
     m11 += wx1 * v[1]; m12 += wx1 * v[2]; m22 += wx2 * v[2];
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
-      const double val = weighted ? w * v[p] : v[p];
-      const float h = tf32_rna((float)val);
-      const float l = tf32_rna((float)(val - (double)h));
+      const double val = (weighted ? w * v[p] : v[p]) * scale;
+      typename OP::E h, l;
+      OP::split(val, h, l);
       hi[p * plane + b * kpad + j] = h;
       lo[p * plane + b * kpad + j] = l;
     }
@@ -108,13 +152,27 @@ cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n,
                                 double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream) {
   if (B <= 0) return cudaSuccess;
   if (dtype == 0)
-    center_split_kernel<float, 256><<<(unsigned)B, 256, 0, stream>>>((const float*)coords, B, n, kpad, w_align,
-                                                                     w_disp, weighted, hi, lo, centroid, gnorm, wbar,
-                                                                     mom, flags);
+    center_split_kernel<float, OpTF32, 256><<<(unsigned)B, 256, 0, stream>>>(
+        (const float*)coords, B, n, kpad, w_align, w_disp, weighted, hi, lo, nullptr, centroid, gnorm, wbar, mom, flags);
   else
-    center_split_kernel<double, 256><<<(unsigned)B, 256, 0, stream>>>((const double*)coords, B, n, kpad, w_align,
-                                                                      w_disp, weighted, hi, lo, centroid, gnorm, wbar,
-                                                                      mom, flags);
+    center_split_kernel<double, OpTF32, 256><<<(unsigned)B, 256, 0, stream>>>(
+        (const double*)coords, B, n, kpad, w_align, w_disp, weighted, hi, lo, nullptr, centroid, gnorm, wbar, mom, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
+                                  const double* w_disp, int weighted, void* hi, void* lo, double* scale_inv,
+                                  double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
+                                  cudaStream_t stream) {
+  if (B <= 0) return cudaSuccess;
+  if (dtype == 0)
+    center_split_kernel<float, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
+        (const float*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hi, (__half*)lo, scale_inv, centroid,
+        gnorm, wbar, mom, flags);
+  else
+    center_split_kernel<double, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
+        (const double*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hi, (__half*)lo, scale_inv, centroid,
+        gnorm, wbar, mom, flags);
   return cudaGetLastError();
 }
 
@@ -124,24 +182,31 @@ constexpr int BM = 128;            // frames per tile (TMEM lanes)
 #ifndef MC_TF32_BL
 #define MC_TF32_BL 48
 #endif
-#ifndef MC_TF32_KB
-#define MC_TF32_KB 16
-#endif
 constexpr int BL = MC_TF32_BL;     // landmarks per tile
 constexpr int BN = 3 * BL;         // 144 accumulator columns per frame plane
-constexpr int KB = MC_TF32_KB;     // atoms per pipeline stage: 16 -> 64 B rows (SWIZZLE_64B), 8 -> 32 B (SWIZZLE_32B)
-constexpr int ROWB = KB * 4;       // bytes per operand row in shared memory
-constexpr int STAGES = KB == 16 ? 3 : 6;
-constexpr int A_BYTES = BM * KB * 4;        // 8 KB: one (plane, hi|lo) frame tile
-constexpr int B_BYTES = BN * KB * 4;        // 9 KB: hi or lo, 3 landmark planes stacked
-constexpr int BP_BYTES = BL * KB * 4;       // 3 KB: one landmark plane box
+constexpr int ROWB = 64;           // bytes per operand row per stage (SWIZZLE_64B): 16 tf32 / 32 f16 atoms
+constexpr int STAGES = 3;
+constexpr int A_BYTES = BM * ROWB;          // 8 KB: one (plane, hi|lo) frame tile
+constexpr int B_BYTES = BN * ROWB;          // 9 KB: hi or lo, 3 landmark planes stacked
+constexpr int BP_BYTES = BL * ROWB;         // 3 KB: one landmark plane box
 constexpr int STAGE_BYTES = 6 * A_BYTES + 2 * B_BYTES;  // 66 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
 constexpr int NT = 256;
-// instruction descriptor: D=F32 (bits 4-5 = 1), A=B=TF32 (2), K-major, N>>3, M>>4
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }  // namespace gemm
+
+// per-operand-format constants: element size, atoms per stage, and the MMA
+// instruction descriptor (D = F32 (bits 4-5 = 1), A = B = TF32 (2) or F16 (0),
+// K-major, N >> 3, M >> 4); one MMA consumes 32 B of each row in both formats
+template <bool F16>
+struct Fmt {
+  static constexpr int ESZ = F16 ? 2 : 4;
+  static constexpr int KB = gemm::ROWB / ESZ;
+  static constexpr uint32_t AB = F16 ? 0u : 2u;
+  __host__ __device__ static constexpr uint32_t idesc(int n, int m) {
+    return (1u << 4) | (AB << 7) | (AB << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+  }
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -180,21 +245,34 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
 // SM100 UMMA shared-memory descriptor, K-major, SWIZZLE_64B (64 B rows,
 // 8-row groups 512 B apart): start>>4 | LBO=1 | SBO=32 | version 1 | layout 4
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
-  // SBO = 8 rows x ROWB bytes; layout 4 = SWIZZLE_64B, 6 = SWIZZLE_32B
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * gemm::ROWB) >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)(gemm::ROWB == 64 ? 4 : 6) << 61);
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(gemm::IDESC), "r"(accum));
+template <bool F16>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  constexpr uint32_t idesc = Fmt<F16>::idesc(gemm::BN, gemm::BM);
+  if (F16)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
+// Commit with the barrier's GENERIC address.  Measured (tools/mma_probe.cu):
+// the .shared::cluster form (a cluster-window address) stalls the issuing
+// thread for roughly the MMA pipeline depth on every commit (one commit per 18
+// MMAs: 649 TF32 TF/s); the generic local-shared address does not (908 TF/s).
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(
+                   reinterpret_cast<uint64_t>(bar))
                : "memory");
 }
 
@@ -222,21 +300,24 @@ __device__ __forceinline__ void tile_coords(int tile, int ntm, int ntl, int& tm,
   tm = g * GROUP_M + (r - tl * gm);
 }
 
-// MSD estimate from an fp32 covariance (fp64 finalisation)
-__device__ __forceinline__ double msd_from_S32(const float* s, double gx, double ga) {
+// MSD estimate from an fp32 covariance (fp64 finalisation); sc undoes the
+// operand scaling of the F16 format (an exact power of two; 1 for TF32)
+__device__ __forceinline__ double msd_from_S32(const float* s, double gx, double ga, double sc = 1.0) {
   double S[9];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) S[e] = (double)s[e];
+  for (int e = 0; e < 9; ++e) S[e] = (double)s[e] * sc;
   const Sym4 n = horn(S);
   return gx + ga - 2.0 * newton_lmax(n, 0.5 * (gx + ga));
 }
 
+template <bool F16>
 __global__ void __launch_bounds__(gemm::NT, 1)
 msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__ CUtensorMap mfl,
                 const __grid_constant__ CUtensorMap mlh, const __grid_constant__ CUtensorMap mll,
-                const double* __restrict__ gx, const double* __restrict__ ga, int T, int L, int kpad,
-                float* __restrict__ D, int64_t ldd) {
+                const double* __restrict__ gx, const double* __restrict__ ga, const double* __restrict__ fsc,
+                const double* __restrict__ lsc, int T, int L, int kpad, float* __restrict__ D, int64_t ldd) {
   using namespace gemm;
+  constexpr int KB = Fmt<F16>::KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -323,8 +404,8 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
           const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t bh = st + 6 * A_BYTES, bl = bh + B_BYTES;
 #pragma unroll
-          for (int k = 0; k < KB / 8; ++k) {
-            const uint32_t koff = k * 32;  // 8 tf32 = 32 B inside the 64 B swizzled row
+          for (int k = 0; k < ROWB / 32; ++k) {
+            const uint32_t koff = k * 32;  // one MMA = 32 B (8 tf32 / 16 f16) inside the 64 B swizzled row
             const uint64_t dbh = umma_desc_sw64(bh + koff);
             const uint64_t dbl = umma_desc_sw64(bl + koff);
             // term-major order: consecutive MMAs target different accumulators,
@@ -335,7 +416,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
               for (int p = 0; p < 3; ++p) {
                 const uint32_t d = tmem_base + p * BN;
                 const uint64_t a = umma_desc_sw64(st + (2 * p + (term == 2 ? 1 : 0)) * A_BYTES + koff);
-                umma_tf32(d, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
+                umma<F16>(d, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
               }
             }
           }
@@ -359,6 +440,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
       mbar_wait(tfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const double gxt = t < T ? gx[t] : 0.0;
+      const double fst = (F16 && t < T) ? fsc[t] : 1.0;
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < BL / 8; ++c) {
@@ -376,7 +458,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
             float s[9];
 #pragma unroll
             for (int e = 0; e < 9; ++e) s[e] = v[e][i];
-            out[i] = l < L ? (float)msd_from_S32(s, gxt, ga[l]) : 0.0f;
+            out[i] = l < L ? (float)msd_from_S32(s, gxt, ga[l], F16 ? fst * lsc[l] : 1.0) : 0.0f;
           }
           float* dst = D + (int64_t)t * ldd + l0 + c * 8;
           if (l0 + c * 8 + 8 <= L && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -414,32 +496,38 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool make_map(CUtensorMap* m, const float* base, int64_t rows, int kpad, int box_rows) {
+}  // namespace
+
+// 2-D map over a plane-major operand [rows][kpad] of esz-byte elements; one
+// box = 64 B of atoms x box_rows rows, SWIZZLE_64B (shared with tf32_gemm_2sm.cu)
+bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int kpad, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kpad * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)gemm::KB, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kpad * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(gemm::ROWB / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, gemm::ROWB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
-}  // namespace
 
-cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
-                            const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
-                            cudaStream_t stream) {
+template <bool F16>
+static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, const void* ll, const double* gx,
+                                const double* ga, const double* fsc, const double* lsc, int T, int L, int kpad,
+                                float* D, int64_t ldd, int grid, cudaStream_t stream) {
   using namespace gemm;
   if (T <= 0 || L <= 0) return cudaSuccess;
+  if (kpad % Fmt<F16>::KB) return cudaErrorInvalidValue;
+  constexpr int esz = Fmt<F16>::ESZ;
   CUtensorMap mfh, mfl, mlh, mll;
-  if (!make_map(&mfh, fh, 3LL * T, kpad, BM) || !make_map(&mfl, fl, 3LL * T, kpad, BM) ||
-      !make_map(&mlh, lh, 3LL * L, kpad, BL) || !make_map(&mll, ll, 3LL * L, kpad, BL))
+  if (!make_operand_map(&mfh, fh, esz, 3LL * T, kpad, BM) || !make_operand_map(&mfl, fl, esz, 3LL * T, kpad, BM) ||
+      !make_operand_map(&mlh, lh, esz, 3LL * L, kpad, BL) || !make_operand_map(&mll, ll, esz, 3LL * L, kpad, BL))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(msd_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(msd_tf32_kernel<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -448,8 +536,20 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int g = grid > 0 ? grid : (ntiles < nsm ? ntiles : nsm);
-  msd_tf32_kernel<<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, T, L, kpad, D, ldd);
+  msd_tf32_kernel<F16><<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, fsc, lsc, T, L, kpad, D, ldd);
   return cudaGetLastError();
+}
+
+cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
+                            const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                            cudaStream_t stream) {
+  return launch_gemm1<false>(fh, fl, lh, ll, gx, ga, nullptr, nullptr, T, L, kpad, D, ldd, grid, stream);
+}
+
+cudaError_t launch_msd_f16(const void* fh, const void* fl, const void* lh, const void* ll, const double* fsc,
+                           const double* lsc, const double* gx, const double* ga, int T, int L, int kpad, float* D,
+                           int64_t ldd, int grid, cudaStream_t stream) {
+  return launch_gemm1<true>(fh, fl, lh, ll, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
 }
 
 }  // namespace mc

@@ -28,8 +28,7 @@ constexpr int BL = 48;             // landmarks per tile
 constexpr int BN = 3 * BL;         // 144 accumulator columns per frame axis
 constexpr int BNH = BN / 2;        // 72 landmark rows staged per CTA
 constexpr int BOX = 24;            // landmark rows per TMA box (3 boxes per CTA per hi|lo)
-constexpr int KB = 16;             // atoms per stage (64 B rows, SWIZZLE_64B)
-constexpr int ROWB = KB * 4;
+constexpr int ROWB = 64;           // bytes per operand row per stage (SWIZZLE_64B): 16 tf32 / 32 f16 atoms
 constexpr int STAGES = 3;
 constexpr int A_BYTES = BM * ROWB;          // 8 KB
 constexpr int B_BYTES = BNH * ROWB;         // 4.5 KB
@@ -38,8 +37,11 @@ constexpr int STAGE_BYTES = 6 * A_BYTES + 2 * B_BYTES;  // 57 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
 constexpr int NT = 256;
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)((2 * BM) >> 4) << 24);
+template <bool F16>
+__host__ __device__ constexpr uint32_t idesc() {  // D = F32, A = B = TF32 (2) or F16 (0), K-major, N >> 3, M >> 4
+  return (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) | ((uint32_t)(BN >> 3) << 17) |
+         ((uint32_t)((2 * BM) >> 4) << 24);
+}
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // clears the CTA-rank bit: the pair leader's smem window
 }  // namespace g2
 
@@ -60,17 +62,30 @@ __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(c));
 }
 
-// bounded wait: a protocol bug traps (clean context error) instead of hanging the GPU
+// bounded wait: a protocol bug traps (clean context error) instead of hanging the GPU.
+// CTA-scope acquire for barriers completed by TMA / tcgen05.commit (an
+// .acquire.cluster poll invalidates the L1 on every try, CCTL.IVALL in SASS);
+// cluster scope only where a peer thread's generic writes must be observed.
+template <bool CLUSTER = false>
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(s32(b)), "r"(parity)
-        : "memory");
+    if (CLUSTER)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(s32(b)), "r"(parity)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(s32(b)), "r"(parity)
+          : "memory");
     if (done) return;
     if (it > (1u << 28)) __trap();
   }
@@ -80,10 +95,10 @@ __device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
 }
 
-// arrive on the pair leader's barrier (same smem offset in CTA rank 0)
-__device__ __forceinline__ void bar_arrive_leader(uint64_t* b) {
+// arrive on CTA `to`'s barrier at the same smem offset
+__device__ __forceinline__ void bar_arrive_remote(uint64_t* b, uint32_t to) {
   uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(s32(b)));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(s32(b)), "r"(to));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
@@ -100,12 +115,20 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
-__device__ __forceinline__ void mma2_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(g2::IDESC), "r"(acc));
+template <bool F16>
+__device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  if (F16)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(g2::idesc<true>()), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(g2::idesc<false>()), "r"(acc));
 }
 
 __device__ __forceinline__ void commit2_both(uint64_t* bar) {
@@ -136,21 +159,23 @@ __device__ __forceinline__ void tile2_coords(int tile, int ntm, int ntl, int& tm
   tm = g * GROUP_M + (r - tl * gm);
 }
 
-__device__ __forceinline__ double msd_from_S32_(const float* s, double gx, double ga) {
+__device__ __forceinline__ double msd_from_S32_(const float* s, double gx, double ga, double sc) {
   double S[9];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) S[e] = (double)s[e];
+  for (int e = 0; e < 9; ++e) S[e] = (double)s[e] * sc;
   const Sym4 n = horn(S);
   return gx + ga - 2.0 * newton_lmax(n, 0.5 * (gx + ga));
 }
 }  // namespace
 
+template <bool F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(g2::NT, 1)
 msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__ CUtensorMap mfl,
                     const __grid_constant__ CUtensorMap mlh, const __grid_constant__ CUtensorMap mll,
-                    const double* __restrict__ gx, const double* __restrict__ ga, int T, int L, int kpad,
-                    float* __restrict__ D, int64_t ldd) {
+                    const double* __restrict__ gx, const double* __restrict__ ga, const double* __restrict__ fsc,
+                    const double* __restrict__ lsc, int T, int L, int kpad, float* __restrict__ D, int64_t ldd) {
   using namespace g2;
+  constexpr int KB = ROWB / (F16 ? 2 : 4);  // atoms per stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -226,7 +251,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
       uint32_t phase = 0;
       int it = 0;
       for (int tile = cid; tile < ntiles; tile += ncl, ++it) {
-        bar_wait(tempty, (it & 1) ^ 1);
+        bar_wait<true>(tempty, (it & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         for (int kb = 0; kb < nkb; ++kb) {
           bar_wait(&full[stage], phase);
@@ -235,7 +260,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
             const uint32_t st = s32(smem + stage * STAGE_BYTES);
             const uint32_t bh = st + 6 * A_BYTES, bl = bh + B_BYTES;
 #pragma unroll
-            for (int k = 0; k < KB / 8; ++k) {
+            for (int k = 0; k < ROWB / 32; ++k) {
               const uint32_t koff = k * 32;
               const uint64_t dbh = desc_sw64(bh + koff);
               const uint64_t dbl = desc_sw64(bl + koff);
@@ -246,7 +271,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
                 for (int p = 0; p < 3; ++p) {
                   const uint32_t d = tmem_base + p * BN;
                   const uint64_t a = desc_sw64(st + (2 * p + (term == 2 ? 1 : 0)) * A_BYTES + koff);
-                  mma2_tf32(d, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
+                  mma2<F16>(d, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
                 }
               }
             }
@@ -270,6 +295,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
       bar_wait(tfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const double gxt = t < T ? gx[t] : 0.0;
+      const double fst = (F16 && t < T) ? fsc[t] : 1.0;
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < BL / 8; ++c) {
@@ -287,7 +313,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
             float s[9];
 #pragma unroll
             for (int e = 0; e < 9; ++e) s[e] = v[e][i];
-            out[i] = l < L ? (float)msd_from_S32_(s, gxt, ga[l]) : 0.0f;
+            out[i] = l < L ? (float)msd_from_S32_(s, gxt, ga[l], F16 ? fst * lsc[l] : 1.0) : 0.0f;
           }
           float* dst = D + (int64_t)t * ldd + l0 + c * 8;
           if (l0 + c * 8 + 8 <= L && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -302,7 +328,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) bar_arrive_leader(tempty);
+      if (lane == 0) bar_arrive_remote(tempty, 0);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -313,44 +339,24 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
   }
 }
 
-namespace {
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
+bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int kpad, int box_rows);
 
-bool map2(CUtensorMap* m, const float* base, int64_t rows, int kpad, int box_rows) {
-  auto enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kpad * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)g2::KB, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-}  // namespace
-
-cudaError_t launch_msd_tf32_2sm(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
-                                const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
-                                cudaStream_t stream) {
+template <bool F16>
+static cudaError_t launch_gemm2(const void* fh, const void* fl, const void* lh, const void* ll, const double* gx,
+                                const double* ga, const double* fsc, const double* lsc, int T, int L, int kpad,
+                                float* D, int64_t ldd, int grid, cudaStream_t stream) {
   using namespace g2;
   if (T <= 0 || L <= 0) return cudaSuccess;
+  constexpr int esz = F16 ? 2 : 4;
+  if (kpad % (ROWB / esz)) return cudaErrorInvalidValue;
   CUtensorMap mfh, mfl, mlh, mll;
-  if (!map2(&mfh, fh, 3LL * T, kpad, BM) || !map2(&mfl, fl, 3LL * T, kpad, BM) ||
-      !map2(&mlh, lh, 3LL * L, kpad, BOX) || !map2(&mll, ll, 3LL * L, kpad, BOX))
+  if (!make_operand_map(&mfh, fh, esz, 3LL * T, kpad, BM) || !make_operand_map(&mfl, fl, esz, 3LL * T, kpad, BM) ||
+      !make_operand_map(&mlh, lh, esz, 3LL * L, kpad, BOX) || !make_operand_map(&mll, ll, esz, 3LL * L, kpad, BOX))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(msd_tf32_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e =
+        cudaFuncSetAttribute(msd_tf32_2sm_kernel<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -361,8 +367,21 @@ cudaError_t launch_msd_tf32_2sm(const float* fh, const float* fl, const float* l
   int clusters = grid > 0 ? grid / 2 : nsm / 2;
   if (clusters > ntiles) clusters = ntiles;
   if (clusters < 1) clusters = 1;
-  msd_tf32_2sm_kernel<<<2 * clusters, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, T, L, kpad, D, ldd);
+  msd_tf32_2sm_kernel<F16><<<2 * clusters, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, fsc, lsc, T, L,
+                                                                     kpad, D, ldd);
   return cudaGetLastError();
+}
+
+cudaError_t launch_msd_tf32_2sm(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
+                                const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                                cudaStream_t stream) {
+  return launch_gemm2<false>(fh, fl, lh, ll, gx, ga, nullptr, nullptr, T, L, kpad, D, ldd, grid, stream);
+}
+
+cudaError_t launch_msd_f16_2sm(const void* fh, const void* fl, const void* lh, const void* ll, const double* fsc,
+                               const double* lsc, const double* gx, const double* ga, int T, int L, int kpad, float* D,
+                               int64_t ldd, int grid, cudaStream_t stream) {
+  return launch_gemm2<true>(fh, fl, lh, ll, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
 }
 
 }  // namespace mc

@@ -222,8 +222,10 @@ class PathCVTC:
     1e-6 relative tolerance); exact=False returns the estimate.
     """
 
-    def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None):
+    def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
+                 operand_fmt=None):
         K.require_cuda()
+        self.fmt = operand_fmt or K.OPERAND_FMT
         lm = _as_cuda(landmarks, device).float().contiguous()
         if lm.ndim != 3 or lm.shape[-1] != 3:
             raise InvalidStructureError("landmarks must be [L, n, 3]")
@@ -245,11 +247,12 @@ class PathCVTC:
             raise ConfigError("q must have one value per landmark")
         self.q = torch.from_numpy(qq).to(self.device)
         self.lraw = lm
-        self.ls = K.center_split(lm, self.wa, self.w, weighted=True, moments=True)
+        self.ls = K.center_split(lm, self.wa, self.w, weighted=True, moments=True, fmt=self.fmt)
         if _or_flags(self.ls.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("landmark coordinates contain non-finite values")
-        # estimate error margin (in units of lam * D): the 3xTF32 + fp32-accumulation
-        # error grows ~ sqrt(n); measured max 6.4e-6 (n=1000) and 6.4e-5 (n=10000)
+        # estimate error margin (in units of lam * D): the split (22 significant bits,
+        # TF32 or scaled-F16 pair) + fp32-accumulation error grows ~ sqrt(n); measured
+        # max 6.4e-6 (n=1000) and 6.4e-5 (n=10000)
         self.est_err = 2e-8 * self.n
         self.margin = 2.0 + self.lam * self.est_err
 
@@ -258,20 +261,20 @@ class PathCVTC:
         if fr.dtype != torch.float32:
             fr = fr.float()
         _check_shapes(fr, self.lraw)
-        fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False)
+        fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False, fmt=self.fmt)
         if _or_flags(fs.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("frame coordinates contain non-finite values")
         return fr.contiguous(), fs
 
     def estimate(self, frames):
         fr, fs = self._frames(frames)
-        return K.msd_tf32(fs, self.ls), fr, fs
+        return K.msd_estimate(fs, self.ls), fr, fs
 
     def msd_matrix(self, frames, exact=True):
         fr, fs = self._frames(frames)
         D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
         if not exact:
-            return K.msd_tf32(fs, self.ls, D)
+            return K.msd_estimate(fs, self.ls, D)
         _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D)
         _raise_flags(flags, "msd_matrix")
         return D

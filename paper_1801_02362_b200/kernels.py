@@ -250,50 +250,78 @@ def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, c
 
 # ---------------------------------------------------------------- fp32 / tensor-core path
 
-def kpad_for(n):
-    return ((int(n) + 15) // 16) * 16
+def kpad_for(n, fmt="tf32"):
+    q = 32 if fmt == "f16" else 16
+    return ((int(n) + q - 1) // q) * q
+
+
+OPERAND_FMT = __import__("os").environ.get("MC_OPERAND_FMT", "f16")
 
 
 class Split:
-    """TF32 hi/lo plane-major operands [3, B, kpad] + per-structure scalars."""
+    """Split operand planes [3, B, kpad] (TF32 fp32 words or scaled IEEE halves)
+    + per-structure scalars (scale = 2^-e for the F16 format, else None)."""
 
-    __slots__ = ("hi", "lo", "centroid", "g", "wbar", "mom", "flags", "n", "kpad", "count")
+    __slots__ = ("hi", "lo", "scale", "fmt", "centroid", "g", "wbar", "mom", "flags", "n", "kpad", "count")
 
-    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad):
+    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale=None, fmt="tf32"):
         self.hi, self.lo, self.centroid, self.g, self.wbar, self.mom, self.flags = hi, lo, centroid, g, wbar, mom, flags
+        self.scale, self.fmt = scale, fmt
         self.n, self.kpad, self.count = n, kpad, hi.shape[1]
 
 
-def center_split(coords, w_align, w_disp, weighted, moments=False):
-    """K1s: centre, optionally fold w into the operand, split into TF32 hi/lo planes."""
+def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None):
+    """K1s: centre, optionally fold w into the operand, split into hi/lo planes
+    (fmt "f16": power-of-two scaled IEEE halves, "tf32": TF32 words; default
+    env MC_OPERAND_FMT, f16)."""
     require_cuda(coords)
+    fmt = fmt or OPERAND_FMT
+    if fmt not in ("f16", "tf32"):
+        raise ValueError(f"operand format {fmt!r}")
     coords = coords.contiguous()
     b, n, _ = coords.shape
-    kpad = kpad_for(n)
+    kpad = kpad_for(n, fmt)
     dev = coords.device
     dt = _lib.MC_F64 if coords.dtype == torch.float64 else _lib.MC_F32
-    hi = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
-    lo = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
+    et = torch.float16 if fmt == "f16" else torch.float32
+    hi = torch.empty((3, b, kpad), dtype=et, device=dev)
+    lo = torch.empty((3, b, kpad), dtype=et, device=dev)
+    scale = torch.empty((b,), dtype=F64, device=dev) if fmt == "f16" else None
     centroid = torch.empty((b, 3), dtype=F64, device=dev)
     g = torch.empty((b,), dtype=F64, device=dev)
     wbar = torch.empty((b, 3), dtype=F64, device=dev)
     mom = torch.empty((b, 6), dtype=F64, device=dev) if moments else None
     flags = torch.empty((b,), dtype=U8, device=dev)
-    call("mc_center_split", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0, ptr(hi),
-         ptr(lo), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
-    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad)
+    if fmt == "f16":
+        call("mc_center_split16", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
+             ptr(hi), ptr(lo), ptr(scale), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
+    else:
+        call("mc_center_split", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
+             ptr(hi), ptr(lo), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
+    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt)
 
 
 TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "1") == "1"
 
 
-def msd_tf32(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
-    """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L]).
-    two_sm (default: env MC_TF32_2SM, on) selects the CTA-pair kernel."""
+def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
+    """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L]),
+    in the operand format of the splits.  two_sm (default: env MC_TF32_2SM, on)
+    selects the CTA-pair kernel."""
+    if fr.fmt != lm.fmt or fr.kpad != lm.kpad:
+        raise ValueError("frame and landmark splits differ in format / padding")
     T, L = fr.count, lm.count
     if D is None:
         D = torch.empty((T, L), dtype=torch.float32, device=fr.hi.device)
-    name = "mc_msd_tf32_2sm" if (TF32_2SM if two_sm is None else two_sm) else "mc_msd_tf32"
-    call(name, ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo), ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D),
-         D.stride(0), grid, stream_ptr())
+    pair = TF32_2SM if two_sm is None else two_sm
+    if fr.fmt == "f16":
+        call("mc_msd_f16_2sm" if pair else "mc_msd_f16", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo),
+             ptr(fr.scale), ptr(lm.scale), ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid,
+             stream_ptr())
+    else:
+        call("mc_msd_tf32_2sm" if pair else "mc_msd_tf32", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo),
+             ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())
     return D
+
+
+msd_tf32 = msd_estimate

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--n", type=int, default=10000)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--check", type=int, default=64, help="frames checked against the exact path")
+    ap.add_argument("--fmt", default="f16", choices=["f16", "tf32"])
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(0)
@@ -36,8 +37,8 @@ def main():
     sig = torch.exp(torch.empty(T, device=dev).uniform_(np.log(1e-3), np.log(0.5), generator=g))
     fr = (base + torch.randn((T, n, 3), generator=g, device=dev) * sig[:, None, None]).float()
     w = engine.normalise_weights(None, n, "d", dev)
-    fs = K.center_split(fr, w, w, weighted=False)
-    ls = K.center_split(lm, w, w, weighted=True)
+    fs = K.center_split(fr, w, w, weighted=False, fmt=args.fmt)
+    ls = K.center_split(lm, w, w, weighted=True, fmt=args.fmt)
     D = torch.empty((T, L), dtype=torch.float32, device=dev)
     K.msd_tf32(fs, ls, D)
     torch.cuda.synchronize()
@@ -49,7 +50,7 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.iters
     flop = 3.0 * 18.0 * n * T * L
-    out = {"T": T, "L": L, "n": n, "ms": ms, "tf32_tflops_executed": flop / ms / 1e9,
+    out = {"fmt": args.fmt, "two_sm": K.TF32_2SM, "T": T, "L": L, "n": n, "ms": ms, "tflops_executed": flop / ms / 1e9,
            "useful_tflops": flop / 3 / ms / 1e9, "pairs_per_s": T * L / ms * 1e3}
     if args.check:
         c = args.check
