@@ -170,21 +170,22 @@ int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const 
                     const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                     void* stream);
 /* Same contraction with an FP16 operand format (kind::f16 tcgen05.mma, K = 16):
- * mc_center_split16 scales each structure by a power of two 2^e (max |value| < 2^14)
- *   and splits into IEEE-half hi/lo planes [3, count, kpad] (kpad % 32 == 0);
- *   scale_inv[count] = 2^-e.  hi + lo keeps 22 significant bits, like the TF32 pair.
- * mc_msd_f16 / mc_msd_f16_2sm: as mc_msd_tf32 / _2sm, S rescaled by
+ * mc_center_split16 scales each structure by a power of two 2^e (max |value| < 2^14),
+ *   splits into IEEE-half hi + lo (22 significant bits, like the TF32 pair) and writes
+ *   them interleaved, hl [3, count, 2 kpad] (kpad % 32 == 0): per 32-atom block
+ *   [hi x32 | lo x32], one 128 B line; scale_inv[count] = 2^-e.
+ * mc_msd_f16 / mc_msd_f16_2sm: as mc_msd_tf32 / _2sm on hl operands, S rescaled by
  *   fscale[t] * lscale[l] (exact) before the fp64 Newton epilogue.  Half the operand
  *   bytes and twice the tensor-core rate of the TF32 format per atom. */
 int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
-                      const double* w_disp, int32_t weighted, void* hi, void* lo, double* scale_inv, double* centroid,
+                      const double* w_disp, int32_t weighted, void* hl, double* scale_inv, double* centroid,
                       double* gnorm, double* wbar, double* mom, uint8_t* flags, void* stream);
-int mc_msd_f16(const void* fhi, const void* flo, const void* lhi, const void* llo, const double* fscale,
-               const double* lscale, const double* gx, const double* ga, int32_t T, int32_t L, int32_t kpad, float* D,
-               int64_t ldd, int32_t grid, void* stream);
-int mc_msd_f16_2sm(const void* fhi, const void* flo, const void* lhi, const void* llo, const double* fscale,
-                   const double* lscale, const double* gx, const double* ga, int32_t T, int32_t L, int32_t kpad,
-                   float* D, int64_t ldd, int32_t grid, void* stream);
+int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
+               const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+               void* stream);
+int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
+                   const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+                   void* stream);
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
                   int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream);

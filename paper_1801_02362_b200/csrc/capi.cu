@@ -216,41 +216,38 @@ int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const floa
 }
 
 int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
-                      const double* w_disp, int32_t weighted, void* hi, void* lo, double* scale_inv, double* centroid,
+                      const double* w_disp, int32_t weighted, void* hl, double* scale_inv, double* centroid,
                       double* gnorm, double* wbar, double* mom, uint8_t* flags, void* stream) {
   if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
   if (n < 2) return MC_ERR_INVALID_STRUCTURE;
   if (count < 0 || kpad < n || kpad % 32 != 0) return MC_ERR_CONFIG;
-  if (count > 0 && (!coords || !w_align || !w_disp || !hi || !lo || !scale_inv || !gnorm)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_center_split16(coords, dtype, count, n, kpad, w_align, w_disp, weighted, hi, lo,
-                                               scale_inv, centroid, gnorm, wbar, mom, flags, S_(stream)));
+  if (count > 0 && (!coords || !w_align || !w_disp || !hl || !scale_inv || !gnorm)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_center_split16(coords, dtype, count, n, kpad, w_align, w_disp, weighted, hl, scale_inv,
+                                               centroid, gnorm, wbar, mom, flags, S_(stream)));
 }
 
-static int msd_f16_args(const void* fhi, const void* flo, const void* lhi, const void* llo, const double* fsc,
-                        const double* lsc, const double* gx, const double* ga, int32_t T, int32_t L, int32_t kpad,
-                        const float* D, int64_t ldd) {
+static int msd_f16_args(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
+                        const double* ga, int32_t T, int32_t L, int32_t kpad, const float* D, int64_t ldd) {
   if (T < 0 || L < 0 || kpad % 32 != 0 || kpad < 32 || ldd < L) return MC_ERR_CONFIG;
-  if ((int64_t)T * L > 0 && (!fhi || !flo || !lhi || !llo || !fsc || !lsc || !gx || !ga || !D)) return MC_ERR_CONFIG;
+  if ((int64_t)T * L > 0 && (!fhl || !lhl || !fsc || !lsc || !gx || !ga || !D)) return MC_ERR_CONFIG;
   if (3LL * T > 0x7fffffffLL || 3LL * L > 0x7fffffffLL) return MC_ERR_CONFIG;
   return MC_OK;
 }
 
-int mc_msd_f16(const void* fhi, const void* flo, const void* lhi, const void* llo, const double* fscale,
-               const double* lscale, const double* gx, const double* ga, int32_t T, int32_t L, int32_t kpad, float* D,
-               int64_t ldd, int32_t grid, void* stream) {
-  const int st = msd_f16_args(fhi, flo, lhi, llo, fscale, lscale, gx, ga, T, L, kpad, D, ldd);
+int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
+               const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+               void* stream) {
+  const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd);
   if (st != MC_OK) return st;
-  return cuda_status(
-      mc::launch_msd_f16(fhi, flo, lhi, llo, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
+  return cuda_status(mc::launch_msd_f16(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
 }
 
-int mc_msd_f16_2sm(const void* fhi, const void* flo, const void* lhi, const void* llo, const double* fscale,
-                   const double* lscale, const double* gx, const double* ga, int32_t T, int32_t L, int32_t kpad,
-                   float* D, int64_t ldd, int32_t grid, void* stream) {
-  const int st = msd_f16_args(fhi, flo, lhi, llo, fscale, lscale, gx, ga, T, L, kpad, D, ldd);
+int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
+                   const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
+                   void* stream) {
+  const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd);
   if (st != MC_OK) return st;
-  return cuda_status(
-      mc::launch_msd_f16_2sm(fhi, flo, lhi, llo, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
+  return cuda_status(mc::launch_msd_f16_2sm(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
 }
 
 }  // extern "C"

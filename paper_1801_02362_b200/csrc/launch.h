@@ -75,13 +75,12 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
                             const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
                             cudaStream_t stream);
 cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
-                                  const double* w_disp, int weighted, void* hi, void* lo, double* scale_inv,
-                                  double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
-                                  cudaStream_t stream);
-cudaError_t launch_msd_f16(const void* fh, const void* fl, const void* lh, const void* ll, const double* fsc,
-                           const double* lsc, const double* gx, const double* ga, int T, int L, int kpad, float* D,
-                           int64_t ldd, int grid, cudaStream_t stream);
-cudaError_t launch_msd_f16_2sm(const void* fh, const void* fl, const void* lh, const void* ll, const double* fsc,
-                               const double* lsc, const double* gx, const double* ga, int T, int L, int kpad, float* D,
-                               int64_t ldd, int grid, cudaStream_t stream);
+                                  const double* w_disp, int weighted, void* hl, double* scale_inv, double* centroid,
+                                  double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream);
+cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
+                           const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                           cudaStream_t stream);
+cudaError_t launch_msd_f16_2sm(const void* fhl, const void* lhl, const double* fsc, const double* lsc,
+                               const double* gx, const double* ga, int T, int L, int kpad, float* D, int64_t ldd,
+                               int grid, cudaStream_t stream);
 }  // namespace mc

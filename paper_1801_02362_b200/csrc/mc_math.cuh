@@ -53,8 +53,20 @@ __device__ __forceinline__ Sym4 horn(const double* S) {
 
 // Largest eigenvalue of a traceless symmetric 4x4 by Newton on its
 // characteristic polynomial P(l) = l^4 + c2 l^2 + c1 l + c0, started from
-// an upper bound (monotone convergence from the right of the largest root).
-__device__ __forceinline__ double newton_lmax(const Sym4& n, double lam0) {
+// an upper bound (monotone convergence from the right of the largest root):
+// min(lam0, sqrt(3/4 tr N^2)) -- for a traceless 4x4, lmax^2 <= 3/4 sum l_i^2
+// (exact when the three other eigenvalues are equal, e.g. identical
+// structures), which cuts the iteration count for distant pairs, whose
+// lmax sits far below the Cauchy-Schwarz bound (Gx + Ga) / 2.
+// FAST (screening estimates only): stop at |step| <= 1e-10 |l| (quadratic
+// convergence leaves ~1e-20 relative) and divide by a refined hardware
+// reciprocal instead of the IEEE division.
+struct Quartic {
+  double c2, c1, c0;  // P(l) = l^4 + c2 l^2 + c1 l + c0
+  double ub;          // sqrt(3/4 tr N^2) >= lambda_max
+};
+
+__device__ __forceinline__ Quartic charpoly(const Sym4& n) {
   // tr(N^2), tr(N^3), det(N)
   const double a00 = n.a00, a01 = n.a01, a02 = n.a02, a03 = n.a03;
   const double a11 = n.a11, a12 = n.a12, a13 = n.a13, a22 = n.a22, a23 = n.a23, a33 = n.a33;
@@ -86,24 +98,64 @@ __device__ __forceinline__ double newton_lmax(const Sym4& n, double lam0) {
   const double c2m = a02 * a33 - a03 * a23;
   const double c1m = a02 * a23 - a03 * a22;
   const double c0m = a02 * a13 - a03 * a12;
-  const double det = s0 * c5 - s1 * c4 + s2 * c3 + s3 * c2m - s4 * c1m + s5 * c0m;
-  const double c2 = -0.5 * tr2;
-  const double c1 = -tr3 / 3.0;
-  const double c0 = det;
-  double lam = lam0;
-  for (int it = 0; it < 80; ++it) {
-    const double l2 = lam * lam;
-    const double b = (l2 + c2) * lam;
-    const double a = b + c1;
-    const double p = a * lam + c0;
-    const double dp = 2.0 * l2 * lam + b + a;
-    if (!(dp != 0.0)) break;
-    const double delta = p / dp;
-    const double nl = lam - delta;
-    if (!(fabs(delta) > 1e-15 * fabs(nl))) { lam = nl; break; }
-    lam = nl;
+  Quartic q;
+  q.c0 = s0 * c5 - s1 * c4 + s2 * c3 + s3 * c2m - s4 * c1m + s5 * c0m;
+  q.c2 = -0.5 * tr2;
+  q.c1 = -tr3 / 3.0;
+  q.ub = sqrt(0.75 * tr2) * (1.0 + 1e-12);
+  return q;
+}
+
+__device__ __forceinline__ double newton_start(const Quartic& q, double lam0) {
+  const double lam = fmin(lam0, q.ub);
+  return lam == lam ? lam : lam0;
+}
+
+// One Newton step on P; returns true once converged (lam then final).
+template <bool FAST>
+__device__ __forceinline__ bool newton_step(const Quartic& q, double& lam) {
+  const double l2 = lam * lam;
+  const double b = (l2 + q.c2) * lam;
+  const double a = b + q.c1;
+  const double p = a * lam + q.c0;
+  const double dp = 2.0 * l2 * lam + b + a;
+  if (!(dp != 0.0)) return true;
+  double delta;
+  if (FAST) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(dp));
+    r = fma(r, fma(-dp, r, 1.0), r);
+    r = fma(r, fma(-dp, r, 1.0), r);
+    delta = p * r;
+    if (!isfinite(delta)) delta = p / dp;
+  } else {
+    delta = p / dp;
   }
+  const double nl = lam - delta;
+  lam = nl;
+  return !(fabs(delta) > (FAST ? 1e-10 : 1e-15) * fabs(nl));
+}
+
+template <bool FAST = false>
+__device__ __forceinline__ double newton_lmax(const Sym4& n, double lam0) {
+  const Quartic q = charpoly(n);
+  double lam = newton_start(q, lam0);
+  for (int it = 0; it < 80; ++it)
+    if (newton_step<FAST>(q, lam)) break;
   return lam;
+}
+
+// K independent pairs iterated in lockstep: the fp64 Newton chain is
+// latency-bound, so interleaving K chains per thread fills the pipe, and a
+// thread pays max (not sum) of the K iteration counts.  Screening estimates.
+template <int K>
+__device__ __forceinline__ void newton_lmax_batch(const Quartic (&q)[K], double (&lam)[K]) {
+  unsigned done = 0;
+  for (int it = 0; it < 80 && done != (1u << K) - 1u; ++it) {
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (!((done >> i) & 1u) && newton_step<true>(q[i], lam[i])) done |= 1u << i;
+  }
 }
 
 // Eigenvector of N for eigenvalue lam from the adjugate of (N - lam I):

@@ -30,6 +30,7 @@
 #include <cudaTypedefs.h>
 
 #include "mc_math.cuh"
+#include "tc_epilogue.cuh"
 
 namespace mc {
 
@@ -49,6 +50,7 @@ __device__ __forceinline__ float tf32_rna(float v) {
 // undoes the scaling exactly in the epilogue.
 struct OpTF32 {
   using E = float;
+  static constexpr bool kInterleave = false;
   static __device__ __forceinline__ void split(double v, E& h, E& l) {
     h = tf32_rna((float)v);
     l = tf32_rna((float)(v - (double)h));
@@ -56,6 +58,9 @@ struct OpTF32 {
 };
 struct OpF16 {
   using E = __half;
+  // rows of 2 kpad halves: per 32-atom block [hi x32 | lo x32] = one 128 B
+  // line, so one SWIZZLE_128B TMA box row carries both parts of a k-block
+  static constexpr bool kInterleave = true;
   static __device__ __forceinline__ void split(double v, E& h, E& l) {
     h = __double2half(v);
     l = __double2half(v - (double)__half2float(h));
@@ -125,8 +130,14 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
       const double val = (weighted ? w * v[p] : v[p]) * scale;
       typename OP::E h, l;
       OP::split(val, h, l);
-      hi[p * plane + b * kpad + j] = h;
-      lo[p * plane + b * kpad + j] = l;
+      if (OP::kInterleave) {
+        const int64_t o = 2 * (p * plane + b * kpad) + (j >> 5) * 64 + (j & 31);
+        hi[o] = h;
+        hi[o + 32] = l;
+      } else {
+        hi[p * plane + b * kpad + j] = h;
+        lo[p * plane + b * kpad + j] = l;
+      }
     }
   }
   g = block_sum<NT>(g, scratch);
@@ -161,17 +172,16 @@ cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n,
 }
 
 cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
-                                  const double* w_disp, int weighted, void* hi, void* lo, double* scale_inv,
-                                  double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
-                                  cudaStream_t stream) {
+                                  const double* w_disp, int weighted, void* hl, double* scale_inv, double* centroid,
+                                  double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream) {
   if (B <= 0) return cudaSuccess;
   if (dtype == 0)
     center_split_kernel<float, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
-        (const float*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hi, (__half*)lo, scale_inv, centroid,
+        (const float*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
         gnorm, wbar, mom, flags);
   else
     center_split_kernel<double, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
-        (const double*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hi, (__half*)lo, scale_inv, centroid,
+        (const double*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
         gnorm, wbar, mom, flags);
   return cudaGetLastError();
 }
@@ -185,14 +195,25 @@ constexpr int BM = 128;            // frames per tile (TMEM lanes)
 constexpr int BL = MC_TF32_BL;     // landmarks per tile
 constexpr int BN = 3 * BL;         // 144 accumulator columns per frame plane
 constexpr int ROWB = 64;           // bytes per operand row per stage (SWIZZLE_64B): 16 tf32 / 32 f16 atoms
-constexpr int STAGES = 3;
+#ifndef MC_STAGES
+#define MC_STAGES 3
+#endif
+constexpr int STAGES = MC_STAGES;
 constexpr int A_BYTES = BM * ROWB;          // 8 KB: one (plane, hi|lo) frame tile
 constexpr int B_BYTES = BN * ROWB;          // 9 KB: hi or lo, 3 landmark planes stacked
 constexpr int BP_BYTES = BL * ROWB;         // 3 KB: one landmark plane box
 constexpr int STAGE_BYTES = 6 * A_BYTES + 2 * B_BYTES;  // 66 KB
+// F16 (interleaved hi|lo rows, SWIZZLE_128B): per stage 32 atoms, 128 B rows
+constexpr int A2_BYTES = BM * 128;          // 16 KB: one frame plane tile, hi and lo
+constexpr int BP2_BYTES = BL * 128;         // 6 KB: one landmark plane box, hi and lo
+static_assert(3 * A2_BYTES + 3 * BP2_BYTES == STAGE_BYTES, "both formats stage 66 KB");
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
-constexpr int NT = 256;
+// warps 4.. are the epilogue: two per TMEM lane quarter, each finishing half
+// of the 8-landmark column chunks, so the latency-bound fp64 Newton runs on
+// two warps per SM sub-partition and the accumulator is released sooner
+constexpr int EPI_WARPS = 8;
+constexpr int NT = 32 * (4 + EPI_WARPS);
 }  // namespace gemm
 
 // per-operand-format constants: element size, atoms per stage, and the MMA
@@ -249,6 +270,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
+// K-major SWIZZLE_128B (128 B rows, 8-row groups 1024 B apart), layout 2
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 template <bool F16>
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
   constexpr uint32_t idesc = Fmt<F16>::idesc(gemm::BN, gemm::BM);
@@ -290,8 +317,11 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8]) {
 // advance through K in near lockstep) cover ~4 frame tiles x ~37 landmark
 // tiles and both operands are re-used out of L2 instead of streaming every
 // landmark tile from HBM once per frame tile.
+#ifndef MC_GROUP_M
+#define MC_GROUP_M 4
+#endif
 __device__ __forceinline__ void tile_coords(int tile, int ntm, int ntl, int& tm, int& tl) {
-  constexpr int GROUP_M = 4;
+  constexpr int GROUP_M = MC_GROUP_M;
   const int gsize = GROUP_M * ntl;
   const int g = tile / gsize;
   const int r = tile - g * gsize;
@@ -300,15 +330,6 @@ __device__ __forceinline__ void tile_coords(int tile, int ntm, int ntl, int& tm,
   tm = g * GROUP_M + (r - tl * gm);
 }
 
-// MSD estimate from an fp32 covariance (fp64 finalisation); sc undoes the
-// operand scaling of the F16 format (an exact power of two; 1 for TF32)
-__device__ __forceinline__ double msd_from_S32(const float* s, double gx, double ga, double sc = 1.0) {
-  double S[9];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) S[e] = (double)s[e] * sc;
-  const Sym4 n = horn(S);
-  return gx + ga - 2.0 * newton_lmax(n, 0.5 * (gx + ga));
-}
 
 template <bool F16>
 __global__ void __launch_bounds__(gemm::NT, 1)
@@ -340,7 +361,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -363,7 +384,16 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
         tile_coords(tile, ntm, ntl, tm, tl);
         const int t0 = tm * BM, l0 = tl * BL;
         for (int kb = 0; kb < nkb; ++kb) {
+#ifdef MC_DIAG_TRACE
+          // diagnostic build only: CTA 0 logs producer wait intervals into D (results invalid)
+          long long* trace = reinterpret_cast<long long*>(D + (int64_t)T * ldd);
+          const int ev = tile == blockIdx.x ? kb : -1;
+          if (blockIdx.x == 0 && ev >= 0 && ev < 4096) trace[4 * ev + 0] = clock64();
           mbar_wait(&empty[stage], phase ^ 1);
+          if (blockIdx.x == 0 && ev >= 0 && ev < 4096) trace[4 * ev + 1] = clock64();
+#else
+          mbar_wait(&empty[stage], phase ^ 1);
+#endif
           uint8_t* st = smem + stage * STAGE_BYTES;
 #ifdef MC_TF32_NOTMA
           // diagnostic build only: MMAs run on stale shared memory, no operand traffic
@@ -371,19 +401,42 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
 #endif
+#if defined(MC_DIAG_NOA)
+          if (!F16) mbar_expect_tx(&full[stage], STAGE_BYTES); else asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(3 * BP2_BYTES) : "memory");
+#elif defined(MC_DIAG_NOB)
+          if (!F16) mbar_expect_tx(&full[stage], STAGE_BYTES); else asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(3 * A2_BYTES) : "memory");
+#else
           mbar_expect_tx(&full[stage], STAGE_BYTES);
-          const int k0 = kb * KB;
+#endif
+          if constexpr (F16) {
+            const int c0 = kb * 64;  // [hi x32 | lo x32] per k-block
+#if defined(MC_DIAG_NOA) || defined(MC_DIAG_NOB)
+            // diagnostic builds only: drop one operand's traffic (results invalid)
+            mbar_arrive(&full[stage]);
+#endif
+#ifndef MC_DIAG_NOA
 #pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            tma_load_2d(&mfh, &full[stage], st + (2 * p) * A_BYTES, k0, p * T + t0);
-            tma_load_2d(&mfl, &full[stage], st + (2 * p + 1) * A_BYTES, k0, p * T + t0);
-          }
-          uint8_t* bh = st + 6 * A_BYTES;
-          uint8_t* bl = bh + B_BYTES;
+            for (int p = 0; p < 3; ++p) tma_load_2d(&mfh, &full[stage], st + p * A2_BYTES, c0, p * T + t0);
+#endif
+#ifndef MC_DIAG_NOB
 #pragma unroll
-          for (int g = 0; g < 3; ++g) {
-            tma_load_2d(&mlh, &full[stage], bh + g * BP_BYTES, k0, g * L + l0);
-            tma_load_2d(&mll, &full[stage], bl + g * BP_BYTES, k0, g * L + l0);
+            for (int g = 0; g < 3; ++g)
+              tma_load_2d(&mlh, &full[stage], st + 3 * A2_BYTES + g * BP2_BYTES, c0, g * L + l0);
+#endif
+          } else {
+            const int k0 = kb * KB;
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+              tma_load_2d(&mfh, &full[stage], st + (2 * p) * A_BYTES, k0, p * T + t0);
+              tma_load_2d(&mfl, &full[stage], st + (2 * p + 1) * A_BYTES, k0, p * T + t0);
+            }
+            uint8_t* bh = st + 6 * A_BYTES;
+            uint8_t* bl = bh + B_BYTES;
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+              tma_load_2d(&mlh, &full[stage], bh + g * BP_BYTES, k0, g * L + l0);
+              tma_load_2d(&mll, &full[stage], bl + g * BP_BYTES, k0, g * L + l0);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -395,17 +448,51 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
     uint32_t phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+#ifdef MC_DIAG_TRACE
+      if (blockIdx.x == 0 && lane == 0 && it < 256)
+        reinterpret_cast<long long*>(D + (int64_t)T * ldd)[4 * 4096 + 2 * it] = clock64();
       mbar_wait(tempty, (it & 1) ^ 1);
+      if (blockIdx.x == 0 && lane == 0 && it < 256)
+        reinterpret_cast<long long*>(D + (int64_t)T * ldd)[4 * 4096 + 2 * it + 1] = clock64();
+#else
+      mbar_wait(tempty, (it & 1) ^ 1);
+#endif
       asm volatile("tcgen05.fence::after_thread_sync;");
       for (int kb = 0; kb < nkb; ++kb) {
+#ifdef MC_DIAG_TRACE
+        long long* trace = reinterpret_cast<long long*>(D + (int64_t)T * ldd);
+        const int ev = tile == blockIdx.x ? kb : -1;
+        if (blockIdx.x == 0 && lane == 0 && ev >= 0 && ev < 4096) trace[4 * ev + 2] = clock64();
         mbar_wait(&full[stage], phase);
+        if (blockIdx.x == 0 && lane == 0 && ev >= 0 && ev < 4096) trace[4 * ev + 3] = clock64();
+#else
+        mbar_wait(&full[stage], phase);
+#endif
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
           const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
+          if constexpr (F16) {
+            // 128 B rows: hi atoms at byte 0..63, lo at 64..127; one MMA = 16 atoms = 32 B
+            const uint32_t bb = st + 3 * A2_BYTES;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint32_t koff = k * 32;
+              const uint64_t dbh = umma_desc_sw128(bb + koff);
+              const uint64_t dbl = umma_desc_sw128(bb + 64 + koff);
+#pragma unroll
+              for (int term = 0; term < 3; ++term) {
+#pragma unroll
+                for (int p = 0; p < 3; ++p) {
+                  const uint64_t a = umma_desc_sw128(st + p * A2_BYTES + (term == 2 ? 64 : 0) + koff);
+                  umma<F16>(tmem_base + p * BN, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
+                }
+              }
+            }
+          } else {
           const uint32_t bh = st + 6 * A_BYTES, bl = bh + B_BYTES;
 #pragma unroll
           for (int k = 0; k < ROWB / 32; ++k) {
-            const uint32_t koff = k * 32;  // one MMA = 32 B (8 tf32 / 16 f16) inside the 64 B swizzled row
+            const uint32_t koff = k * 32;  // one MMA = 32 B (8 tf32) inside the 64 B swizzled row
             const uint64_t dbh = umma_desc_sw64(bh + koff);
             const uint64_t dbl = umma_desc_sw64(bl + koff);
             // term-major order: consecutive MMAs target different accumulators,
@@ -420,6 +507,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
               }
             }
           }
+          }
           umma_commit(&empty[stage]);
           if (kb == nkb - 1) umma_commit(tfull);
         }
@@ -430,6 +518,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
   } else if (warp >= 4) {
     // ---------------- epilogue: lane = frame, whole 3x3 blocks per thread
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int row = q * 32 + lane;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -439,27 +528,32 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
       const int l0 = tl * BL;
       mbar_wait(tfull, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef MC_DIAG_TRACE
+      if (blockIdx.x == 0 && lane == 0 && it < 256)
+        reinterpret_cast<long long*>(D + (int64_t)T * ldd)[5 * 4096 + 16 * it + 2 * (warp - 4)] = clock64();
+#endif
       const double gxt = t < T ? gx[t] : 0.0;
       const double fst = (F16 && t < T) ? fsc[t] : 1.0;
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BL / 8; ++c) {
+      for (int c = half; c < BL / 8; c += EPI_WARPS / 4) {
         float v[9][8];
 #pragma unroll
         for (int p = 0; p < 3; ++p)
 #pragma unroll
           for (int g = 0; g < 3; ++g) tmem_ld8(lane_base + p * BN + g * BL + c * 8, v[p * 3 + g]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifdef MC_DIAG_TRACE
+        long long tq0 = clock64();
+#endif
         if (t < T) {
           float out[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int l = l0 + c * 8 + i;
-            float s[9];
-#pragma unroll
-            for (int e = 0; e < 9; ++e) s[e] = v[e][i];
-            out[i] = l < L ? (float)msd_from_S32(s, gxt, ga[l], F16 ? fst * lsc[l] : 1.0) : 0.0f;
-          }
+          msd8_estimate(v, gxt, ga, fst, F16 ? lsc : nullptr, l0 + c * 8, L, out);
+#ifdef MC_DIAG_TRACE
+          __syncwarp();
+          if (blockIdx.x == 0 && lane == 0 && it < 256 && warp == 4)
+            reinterpret_cast<long long*>(D + (int64_t)T * ldd)[6 * 4096 + 8 * it + c] = clock64() - tq0;
+#endif
           float* dst = D + (int64_t)t * ldd + l0 + c * 8;
           if (l0 + c * 8 + 8 <= L && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
             reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
@@ -473,6 +567,10 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
+#ifdef MC_DIAG_TRACE
+      if (blockIdx.x == 0 && lane == 0 && it < 256)
+        reinterpret_cast<long long*>(D + (int64_t)T * ldd)[5 * 4096 + 16 * it + 2 * (warp - 4) + 1] = clock64();
+#endif
       if (lane == 0) mbar_arrive(tempty);
     }
   }
@@ -498,18 +596,22 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 }  // namespace
 
-// 2-D map over a plane-major operand [rows][kpad] of esz-byte elements; one
-// box = 64 B of atoms x box_rows rows, SWIZZLE_64B (shared with tf32_gemm_2sm.cu)
-bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int kpad, int box_rows) {
+// 2-D map over a plane-major operand [rows][row_elems] of esz-byte elements;
+// one box = box_rows rows x 64 B (SWIZZLE_64B: TF32 hi or lo planes) or x 128 B
+// (SWIZZLE_128B: interleaved F16 hi|lo rows).  Shared with tf32_gemm_2sm.cu.
+bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t row_elems, int box_rows,
+                      bool sw128) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)kpad * esz};
-  cuuint32_t box[2] = {(cuuint32_t)(gemm::ROWB / esz), (cuuint32_t)box_rows};
+  const int box_bytes = sw128 ? 128 : 64;
+  cuuint64_t dims[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_elems * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(box_bytes / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -522,9 +624,19 @@ static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, 
   if (kpad % Fmt<F16>::KB) return cudaErrorInvalidValue;
   constexpr int esz = Fmt<F16>::ESZ;
   CUtensorMap mfh, mfl, mlh, mll;
-  if (!make_operand_map(&mfh, fh, esz, 3LL * T, kpad, BM) || !make_operand_map(&mfl, fl, esz, 3LL * T, kpad, BM) ||
-      !make_operand_map(&mlh, lh, esz, 3LL * L, kpad, BL) || !make_operand_map(&mll, ll, esz, 3LL * L, kpad, BL))
+  if (F16) {
+    // interleaved rows of 2 kpad halves; the lo maps are unused
+    if (!make_operand_map(&mfh, fh, esz, 3LL * T, 2LL * kpad, BM, true) ||
+        !make_operand_map(&mlh, lh, esz, 3LL * L, 2LL * kpad, BL, true))
+      return cudaErrorInvalidValue;
+    mfl = mfh;
+    mll = mlh;
+  } else if (!make_operand_map(&mfh, fh, esz, 3LL * T, kpad, BM, false) ||
+             !make_operand_map(&mfl, fl, esz, 3LL * T, kpad, BM, false) ||
+             !make_operand_map(&mlh, lh, esz, 3LL * L, kpad, BL, false) ||
+             !make_operand_map(&mll, ll, esz, 3LL * L, kpad, BL, false)) {
     return cudaErrorInvalidValue;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(msd_tf32_kernel<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -546,10 +658,10 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
   return launch_gemm1<false>(fh, fl, lh, ll, gx, ga, nullptr, nullptr, T, L, kpad, D, ldd, grid, stream);
 }
 
-cudaError_t launch_msd_f16(const void* fh, const void* fl, const void* lh, const void* ll, const double* fsc,
-                           const double* lsc, const double* gx, const double* ga, int T, int L, int kpad, float* D,
-                           int64_t ldd, int grid, cudaStream_t stream) {
-  return launch_gemm1<true>(fh, fl, lh, ll, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
+cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
+                           const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                           cudaStream_t stream) {
+  return launch_gemm1<true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
 }
 
 }  // namespace mc

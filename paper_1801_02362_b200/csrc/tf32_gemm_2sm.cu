@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include "mc_math.cuh"
+#include "tc_epilogue.cuh"
 
 namespace mc {
 
@@ -34,9 +35,17 @@ constexpr int A_BYTES = BM * ROWB;          // 8 KB
 constexpr int B_BYTES = BNH * ROWB;         // 4.5 KB
 constexpr int BOX_BYTES = BOX * ROWB;       // 1.5 KB
 constexpr int STAGE_BYTES = 6 * A_BYTES + 2 * B_BYTES;  // 57 KB
+// F16 interleaved hi|lo 128 B rows (SWIZZLE_128B): 3 A planes x 16 KB + 72 B rows
+constexpr int A2_BYTES = BM * 128;
+constexpr int BOX2_BYTES = BOX * 128;
+static_assert(3 * A2_BYTES + 3 * BOX2_BYTES == STAGE_BYTES, "both formats stage 57 KB");
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int TMEM_COLS = 512;
-constexpr int NT = 256;
+// warps 4.. are the epilogue: two per TMEM lane quarter, each finishing half
+// of the 8-landmark column chunks, so the latency-bound fp64 Newton runs on
+// two warps per SM sub-partition and the accumulator is released sooner
+constexpr int EPI_WARPS = 8;
+constexpr int NT = 32 * (4 + EPI_WARPS);
 template <bool F16>
 __host__ __device__ constexpr uint32_t idesc() {  // D = F32, A = B = TF32 (2) or F16 (0), K-major, N >> 3, M >> 4
   return (1u << 4) | ((F16 ? 0u : 2u) << 7) | ((F16 ? 0u : 2u) << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -115,6 +124,11 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
 }
 
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 template <bool F16>
 __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
   if (F16)
@@ -159,13 +173,6 @@ __device__ __forceinline__ void tile2_coords(int tile, int ntm, int ntl, int& tm
   tm = g * GROUP_M + (r - tl * gm);
 }
 
-__device__ __forceinline__ double msd_from_S32_(const float* s, double gx, double ga, double sc) {
-  double S[9];
-#pragma unroll
-  for (int e = 0; e < 9; ++e) S[e] = (double)s[e] * sc;
-  const Sym4 n = horn(S);
-  return gx + ga - 2.0 * newton_lmax(n, 0.5 * (gx + ga));
-}
 }  // namespace
 
 template <bool F16>
@@ -200,7 +207,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
     bar_init(tfull, 1);
-    bar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
+    bar_init(tempty, 2 * EPI_WARPS);  // epilogue warps of both CTAs (used on the leader)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -225,6 +232,19 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
           bar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * STAGE_BYTES;
           if (rank == 0) bar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          if constexpr (F16) {
+            const int c0 = kb * 64;
+#pragma unroll
+            for (int p = 0; p < 3; ++p) tma2_load(&mfh, &full[stage], st + p * A2_BYTES, c0, p * T + t0);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const int r = (int)rank * BNH + q * BOX;
+              const int g = r / BL, l = r - g * BL;
+              tma2_load(&mlh, &full[stage], st + 3 * A2_BYTES + q * BOX2_BYTES, c0, g * L + l0 + l);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           const int k0 = kb * KB;
 #pragma unroll
           for (int p = 0; p < 3; ++p) {
@@ -258,6 +278,23 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (lane == 0) {
             const uint32_t st = s32(smem + stage * STAGE_BYTES);
+            if constexpr (F16) {
+              const uint32_t bb = st + 3 * A2_BYTES;
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const uint32_t koff = k * 32;
+                const uint64_t dbh = desc_sw128(bb + koff);
+                const uint64_t dbl = desc_sw128(bb + 64 + koff);
+#pragma unroll
+                for (int term = 0; term < 3; ++term) {
+#pragma unroll
+                  for (int p = 0; p < 3; ++p) {
+                    const uint64_t a = desc_sw128(st + p * A2_BYTES + (term == 2 ? 64 : 0) + koff);
+                    mma2<F16>(tmem_base + p * BN, a, term == 1 ? dbl : dbh, (term | kb | k) != 0 ? 1u : 0u);
+                  }
+                }
+              }
+            } else {
             const uint32_t bh = st + 6 * A_BYTES, bl = bh + B_BYTES;
 #pragma unroll
             for (int k = 0; k < ROWB / 32; ++k) {
@@ -275,6 +312,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
                 }
               }
             }
+            }
             commit2_both(&empty[stage]);
             if (kb == nkb - 1) commit2_both(tfull);
           }
@@ -285,6 +323,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     const int row = q * 32 + lane;
     int it = 0;
     for (int tile = cid; tile < ntiles; tile += ncl, ++it) {
@@ -298,7 +337,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
       const double fst = (F16 && t < T) ? fsc[t] : 1.0;
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BL / 8; ++c) {
+      for (int c = half; c < BL / 8; c += EPI_WARPS / 4) {
         float v[9][8];
 #pragma unroll
         for (int p = 0; p < 3; ++p)
@@ -307,14 +346,7 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (t < T) {
           float out[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int l = l0 + c * 8 + i;
-            float s[9];
-#pragma unroll
-            for (int e = 0; e < 9; ++e) s[e] = v[e][i];
-            out[i] = l < L ? (float)msd_from_S32_(s, gxt, ga[l], F16 ? fst * lsc[l] : 1.0) : 0.0f;
-          }
+          msd8_estimate(v, gxt, ga, fst, F16 ? lsc : nullptr, l0 + c * 8, L, out);
           float* dst = D + (int64_t)t * ldd + l0 + c * 8;
           if (l0 + c * 8 + 8 <= L && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
             reinterpret_cast<float4*>(dst)[0] = make_float4(out[0], out[1], out[2], out[3]);
@@ -339,7 +371,8 @@ msd_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_consta
   }
 }
 
-bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int kpad, int box_rows);
+bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, int64_t row_elems, int box_rows,
+                      bool sw128);
 
 template <bool F16>
 static cudaError_t launch_gemm2(const void* fh, const void* fl, const void* lh, const void* ll, const double* gx,
@@ -350,9 +383,18 @@ static cudaError_t launch_gemm2(const void* fh, const void* fl, const void* lh, 
   constexpr int esz = F16 ? 2 : 4;
   if (kpad % (ROWB / esz)) return cudaErrorInvalidValue;
   CUtensorMap mfh, mfl, mlh, mll;
-  if (!make_operand_map(&mfh, fh, esz, 3LL * T, kpad, BM) || !make_operand_map(&mfl, fl, esz, 3LL * T, kpad, BM) ||
-      !make_operand_map(&mlh, lh, esz, 3LL * L, kpad, BOX) || !make_operand_map(&mll, ll, esz, 3LL * L, kpad, BOX))
+  if (F16) {
+    if (!make_operand_map(&mfh, fh, esz, 3LL * T, 2LL * kpad, BM, true) ||
+        !make_operand_map(&mlh, lh, esz, 3LL * L, 2LL * kpad, BOX, true))
+      return cudaErrorInvalidValue;
+    mfl = mfh;
+    mll = mlh;
+  } else if (!make_operand_map(&mfh, fh, esz, 3LL * T, kpad, BM, false) ||
+             !make_operand_map(&mfl, fl, esz, 3LL * T, kpad, BM, false) ||
+             !make_operand_map(&mlh, lh, esz, 3LL * L, kpad, BOX, false) ||
+             !make_operand_map(&mll, ll, esz, 3LL * L, kpad, BOX, false)) {
     return cudaErrorInvalidValue;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -378,10 +420,10 @@ cudaError_t launch_msd_tf32_2sm(const float* fh, const float* fl, const float* l
   return launch_gemm2<false>(fh, fl, lh, ll, gx, ga, nullptr, nullptr, T, L, kpad, D, ldd, grid, stream);
 }
 
-cudaError_t launch_msd_f16_2sm(const void* fh, const void* fl, const void* lh, const void* ll, const double* fsc,
-                               const double* lsc, const double* gx, const double* ga, int T, int L, int kpad, float* D,
-                               int64_t ldd, int grid, cudaStream_t stream) {
-  return launch_gemm2<true>(fh, fl, lh, ll, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
+cudaError_t launch_msd_f16_2sm(const void* fhl, const void* lhl, const double* fsc, const double* lsc,
+                               const double* gx, const double* ga, int T, int L, int kpad, float* D, int64_t ldd,
+                               int grid, cudaStream_t stream) {
+  return launch_gemm2<true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
 }
 
 }  // namespace mc

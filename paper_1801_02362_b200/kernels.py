@@ -259,8 +259,9 @@ OPERAND_FMT = __import__("os").environ.get("MC_OPERAND_FMT", "f16")
 
 
 class Split:
-    """Split operand planes [3, B, kpad] (TF32 fp32 words or scaled IEEE halves)
-    + per-structure scalars (scale = 2^-e for the F16 format, else None)."""
+    """Split operand planes: TF32 hi/lo fp32 words [3, B, kpad] each, or (F16) one
+    interleaved tensor hi [3, B, 2 kpad] of scaled IEEE halves (lo None) with
+    scale = 2^-e per structure; + per-structure scalars."""
 
     __slots__ = ("hi", "lo", "scale", "fmt", "centroid", "g", "wbar", "mom", "flags", "n", "kpad", "count")
 
@@ -283,9 +284,12 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None):
     kpad = kpad_for(n, fmt)
     dev = coords.device
     dt = _lib.MC_F64 if coords.dtype == torch.float64 else _lib.MC_F32
-    et = torch.float16 if fmt == "f16" else torch.float32
-    hi = torch.empty((3, b, kpad), dtype=et, device=dev)
-    lo = torch.empty((3, b, kpad), dtype=et, device=dev)
+    if fmt == "f16":  # interleaved [hi x32 | lo x32] rows
+        hi = torch.empty((3, b, 2 * kpad), dtype=torch.float16, device=dev)
+        lo = None
+    else:
+        hi = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
+        lo = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
     scale = torch.empty((b,), dtype=F64, device=dev) if fmt == "f16" else None
     centroid = torch.empty((b, 3), dtype=F64, device=dev)
     g = torch.empty((b,), dtype=F64, device=dev)
@@ -294,14 +298,14 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None):
     flags = torch.empty((b,), dtype=U8, device=dev)
     if fmt == "f16":
         call("mc_center_split16", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
-             ptr(hi), ptr(lo), ptr(scale), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
+             ptr(hi), ptr(scale), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
     else:
         call("mc_center_split", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
              ptr(hi), ptr(lo), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
     return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt)
 
 
-TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "1") == "1"
+TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "0") == "1"
 
 
 def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
@@ -315,9 +319,8 @@ def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
         D = torch.empty((T, L), dtype=torch.float32, device=fr.hi.device)
     pair = TF32_2SM if two_sm is None else two_sm
     if fr.fmt == "f16":
-        call("mc_msd_f16_2sm" if pair else "mc_msd_f16", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo),
-             ptr(fr.scale), ptr(lm.scale), ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid,
-             stream_ptr())
+        call("mc_msd_f16_2sm" if pair else "mc_msd_f16", ptr(fr.hi), ptr(lm.hi), ptr(fr.scale), ptr(lm.scale),
+             ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())
     else:
         call("mc_msd_tf32_2sm" if pair else "mc_msd_tf32", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo),
              ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())
