@@ -1,6 +1,8 @@
 // extern "C" boundary of libmcb200.so (declared in include/mcb200.h).
 // Argument validation maps to the reference error taxonomy (errors.py:4-35);
 // CUDA launch errors map to MC_ERR_CUDA_BASE - cudaError_t.
+#include <cstdlib>
+
 #include "../../include/mcb200.h"
 #include "launch.h"
 
@@ -145,8 +147,17 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
   if (T > 0 && (!fraw || !fcen || !lraw || !lcen || !w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec ||
                 !ds || !dz))
     return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_cv_grad_block(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, sig_idx, sig_coef, nsig,
-                                              fvec, perm, ds, dz, out_f32, S_(stream)));
+  // fp64 tensor-core (DMMA) contraction by default; MC_GRAD_VECTOR=1 selects the
+  // CUDA-core kernel (grad_block.cu) for A/B comparison
+  static const bool vec = [] {
+    const char* e = getenv("MC_GRAD_VECTOR");
+    return e && e[0] == '1';
+  }();
+  if (vec)
+    return cuda_status(mc::launch_cv_grad_block(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, sig_idx, sig_coef,
+                                                nsig, fvec, perm, ds, dz, out_f32, S_(stream)));
+  return cuda_status(mc::launch_cv_grad_dmma(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, sig_idx, sig_coef, nsig,
+                                             fvec, perm, ds, dz, out_f32, S_(stream)));
 }
 
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,

@@ -1,0 +1,247 @@
+// K4 gradient pass of the fp32-coordinate path on the fp64 tensor cores.
+//
+// Same result as cv_grad_block_kernel<OT, false> (grad_block.cu):
+//   ds_t,k = 2 w_k (sum_i cs_i x_k - U^s_k) - w'_k corr^s_t,
+//   U^s_k  = sum_{i in sig(t)} (cs_i Rhat_i) a_{i,k}          (same for z),
+// but the contraction U is issued as a real fp64 GEMM on DMMA
+// (mma.sync m8n8k4 f64, exact fp64 products and sums):
+//   C[r, k] = sum_kk A[r, kk] B[kk, k],   r = (frame f, s|z, axis b)  (48 rows
+//   for a group of 8 sorted frames), kk = (landmark l - wlo, axis g) over the
+//   group's window union, B[kk, k] = centred landmark coordinate a_{l,k,g}.
+// The vector kernel re-reads all 18 coefficients of a (frame, landmark) from
+// shared memory for every atom; here one A fragment (1 double per lane) feeds
+// 4 DMMAs and one B fragment 6, so the fp64 pipe rather than shared memory
+// sets the pace.  Coefficients are staged once per CTA (2048 atoms); the raw
+// fp32 landmark coordinates stream through a 6-stage cp.async ring (4
+// landmarks x 256 atoms per stage, coalesced) and are converted / centred
+// when a B fragment is read (once per 6 DMMAs).
+#include "mc_math.cuh"
+
+namespace mc {
+
+namespace {
+constexpr int DG = 8;              // frames per group
+constexpr int DR = 6 * DG;         // 48 GEMM rows
+constexpr int DWMAX = 96;          // landmarks per staged window chunk
+constexpr int DKMAX = 3 * DWMAX;   // 288 kk columns
+constexpr int AST = 292;           // sA row stride (doubles): 4 mod 16 -> conflict-free 8x4 fragments
+constexpr int DNA = 256;           // atoms per sub-tile (8 warps x 32)
+constexpr int DKC = 24;            // kk rows per B chunk (8 landmarks)
+constexpr int LROW = 3 * DNA + 8;  // raw floats per staged landmark row (+8: bank shift between landmarks)
+constexpr int NST = 3;             // cp.async ring stages
+constexpr int DNT = 256;
+constexpr int DATOMS = 2048;       // atoms per CTA
+constexpr int CHL = DKC / 3;       // landmarks per chunk
+constexpr int LPT = CHL * DNA * 3 / DNT;  // 24 raw floats per thread per chunk
+constexpr int XPT = DG * DNA * 3 / DNT;  // 24 frame floats per thread per sub-tile
+constexpr int DSMEM = DR * AST * (int)sizeof(double) + DKMAX * (int)sizeof(double) +
+                      NST * CHL * LROW * (int)sizeof(float) + DG * 3 * DNA * (int)sizeof(float);
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+}  // namespace
+
+template <typename OT>
+__global__ void __launch_bounds__(DNT, 1)
+cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const double* __restrict__ fcen,
+                    const float* __restrict__ lraw, const double* __restrict__ lcen, const double* __restrict__ w,
+                    const double* __restrict__ wa, const int* __restrict__ sig_idx,
+                    const double* __restrict__ sig_coef, const int* __restrict__ nsig,
+                    const double* __restrict__ fvec, const int* __restrict__ perm, OT* __restrict__ ds,
+                    OT* __restrict__ dz) {
+  extern __shared__ __align__(16) double dsm[];
+  double* sA = dsm;                                       // [DR][AST] coefficients
+  double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
+  float* sR = reinterpret_cast<float*>(sLc + DKMAX);      // [NST][CHL][LROW] raw landmark floats
+  float* sX = sR + NST * CHL * LROW;                      // [DG][3 DNA] raw frame floats of the sub-tile
+  __shared__ int s_t[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
+  __shared__ double s_fc[DG][3], s_fv[DG][8];
+  __shared__ int s_wlo, s_whi;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;  // mma groupID / threadID_in_group
+  if (tid < DG) {
+    const int k = blockIdx.x * DG + tid;
+    int t = -1, ns = 0;
+    if (k < T) {
+      t = perm ? perm[k] : k;
+      ns = nsig[t];
+    }
+    s_t[tid] = t;
+    s_ns[tid] = ns;
+    s_flo[tid] = (t >= 0 && ns > 0) ? sig_idx[(int64_t)t * cap] : 0x7fffffff;
+    s_fhi[tid] = (t >= 0 && ns > 0) ? sig_idx[(int64_t)t * cap + ns - 1] + 1 : -1;
+    if (t >= 0) {
+      for (int a = 0; a < 3; ++a) s_fc[tid][a] = fcen[3 * t + a];
+      const double* fv = fvec + (int64_t)t * 16;
+      for (int e = 0; e < 8; ++e) s_fv[tid][e] = fv[e];  // sumcs, sumcz, corr_s[3], corr_z[3]
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int a = 0x7fffffff, b = -1;
+    for (int f = 0; f < DG; ++f) { a = min(a, s_flo[f]); b = max(b, s_fhi[f]); }
+    s_wlo = a;
+    s_whi = b;
+  }
+  __syncthreads();
+  const int wlo = s_wlo, whi = s_whi;
+  const bool restage = whi - wlo > DWMAX;
+  bool staged = false;
+  const int katom0 = blockIdx.y * DATOMS;
+  const int katom1 = min(n, katom0 + DATOMS);
+  for (int a0 = katom0; a0 < katom1; a0 += DNA) {
+    // the epilogue's frame coordinates: one cp.async group issued now, long
+    // complete by the time the contraction below has finished
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int e = tid + u * DNT;  // [0, DG * 3 DNA)
+      const int f = e / (3 * DNA), r = e - f * (3 * DNA);
+      const int t = s_t[f];
+      const bool ok = t >= 0 && a0 + r / 3 < n;
+      cp_async4(sX + e, fraw + ((int64_t)(ok ? t : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+    }
+    cp_commit();
+    double c[6][4][2];
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[m][j][0] = c[m][j][1] = 0.0;
+    for (int w0 = wlo; w0 < whi; w0 += DWMAX) {
+      const int wn = min(DWMAX, whi - w0);
+      if (restage || !staged) {  // block-uniform
+        staged = true;
+        __syncthreads();
+        for (int e = tid; e < DR * AST; e += DNT) sA[e] = 0.0;
+        for (int e = tid; e < DKMAX; e += DNT) sLc[e] = e < 3 * wn ? lcen[3 * w0 + e] : 0.0;
+        __syncthreads();
+        for (int f = 0; f < DG; ++f) {
+          const int t = s_t[f];
+          if (t < 0) continue;
+          const int ns = s_ns[f];
+          const int* idx = sig_idx + (int64_t)t * cap;
+          const double* co = sig_coef + (int64_t)t * cap * 18;
+          for (int e = tid; e < ns * 18; e += DNT) {
+            const int s = e / 18, e18 = e - s * 18;
+            const int l = idx[s] - w0;
+            if (l >= 0 && l < wn) {
+              const int sz = e18 / 9, b = (e18 % 9) / 3, g = e18 % 3;
+              sA[(f * 6 + sz * 3 + b) * AST + l * 3 + g] = co[e];
+            }
+          }
+        }
+        __syncthreads();
+      }
+      const int nch = (3 * wn + DKC - 1) / DKC;
+      // stage chunk ch (landmarks w0 + CHL ch .., atoms a0 .. a0 + DNA) into ring slot ch % NST;
+      // out-of-range elements are zero-filled (their coefficients are zero too)
+      auto issue = [&](int ch) {
+        float* dst = sR + (ch % NST) * CHL * LROW;
+#pragma unroll
+        for (int u = 0; u < LPT; ++u) {
+          const int e = tid + u * DNT;  // [0, CHL * 3 DNA)
+          const int q = e / (3 * DNA), r = e - q * (3 * DNA);
+          const int li = w0 + ch * CHL + q;
+          const bool ok = ch < nch && li < w0 + wn && a0 + r / 3 < n;
+          cp_async4(dst + q * LROW + r, lraw + ((int64_t)(ok ? li : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+        }
+        cp_commit();
+      };
+#pragma unroll
+      for (int st = 0; st < NST - 1; ++st) issue(st);
+      for (int ch = 0; ch < nch; ++ch) {
+        cp_wait<NST - 2>();
+        __syncthreads();
+        issue(ch + NST - 1);
+        const float* rb = sR + (ch % NST) * CHL * LROW + (warp * 32 + gq) * 3;
+#pragma unroll
+        for (int s = 0; s < DKC / 4; ++s) {
+          const int kc = s * 4 + tq;            // kk within the chunk
+          const int q = kc / 3, g = kc - q * 3;
+          const int kk = ch * DKC + kc;
+          const double lcg = sLc[kk];
+          double a[6], b[4];
+#pragma unroll
+          for (int m = 0; m < 6; ++m) a[m] = sA[(m * 8 + gq) * AST + kk];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[j] = (double)rb[q * LROW + j * 24 + g] - lcg;
+#pragma unroll
+          for (int m = 0; m < 6; ++m)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma(c[m][j], a[m], b[j]);
+        }
+      }
+      cp_wait<0>();
+      __syncthreads();
+    }
+    // epilogue: each accumulator element is one (frame, s|z, axis, atom) output.
+    // Loads of a half (3 row tiles x 8 atoms) are batched ahead of its stores.
+    double wk[4][2], wak[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = a0 + warp * 32 + j * 8 + 2 * tq + e;
+        wk[j][e] = k < n ? w[k] : 0.0;
+        wak[j][e] = k < n ? wa[k] : 0.0;
+      }
+    cp_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      const int r = m * 8 + gq;
+      const int f = r / 6, sz = (r % 6) / 3, b = r % 3;
+      const int t = s_t[f];
+      if (t < 0) continue;
+      const double cx = s_fc[f][b], sc = s_fv[f][sz], corr = s_fv[f][2 + sz * 3 + b];
+      OT* __restrict__ out = sz ? dz : ds;
+      const float* xs = sX + f * 3 * DNA + b;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int al = warp * 32 + j * 8 + 2 * tq + e;
+          const int k = a0 + al;
+          if (k >= n) continue;
+          const double x = (double)xs[3 * al] - cx;
+          out[((int64_t)t * n + k) * 3 + b] = (OT)(2.0 * wk[j][e] * (sc * x - c[m][j][e]) - wak[j][e] * corr);
+        }
+    }
+    __syncthreads();  // sX is refilled by the next sub-tile
+  }
+}
+
+cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
+                                const double* lcen, const double* w, const double* wa, const int* sig_idx,
+                                const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
+                                void* ds, void* dz, int out_f32, cudaStream_t stream) {
+  if (T <= 0 || n <= 0) return cudaSuccess;
+  dim3 grid((T + DG - 1) / DG, (n + DATOMS - 1) / DATOMS);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(cv_grad_dmma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(cv_grad_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (out_f32)
+    cv_grad_dmma_kernel<float><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,
+                                                            sig_coef, nsig, fvec, perm, (float*)ds, (float*)dz);
+  else
+    cv_grad_dmma_kernel<double><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,
+                                                             sig_coef, nsig, fvec, perm, (double*)ds, (double*)dz);
+  return cudaGetLastError();
+}
+
+}  // namespace mc

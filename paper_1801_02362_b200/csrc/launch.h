@@ -45,6 +45,10 @@ cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, c
 cudaError_t launch_msd_tf32_2sm(const float* fh, const float* fl, const float* lh, const float* ll, const double* gx,
                                 const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
                                 cudaStream_t stream);
+cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
+                                const double* lcen, const double* w, const double* wa, const int* sig_idx,
+                                const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
+                                void* ds, void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                  const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                  const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
