@@ -182,8 +182,16 @@ int mc_refine(const float* frames, const double* fcentroid, const float* landmar
   if (!Dex && !Dd) return MC_ERR_CONFIG;
   if ((Dex || Rex) && cap < 1) return MC_ERR_CONFIG;
   if (Dd && ldd < L) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_refine(frames, fcentroid, landmarks, lcentroid, w, gx, ga, T, L, n, perm, lo, cnt, cap,
-                                       Dex, Rex, Dd, ldd, flags, S_(stream)));
+  // fp64 tensor-core (DMMA) tiles by default; MC_REFINE_VECTOR=1 selects the CUDA-core kernel
+  static const bool vec = [] {
+    const char* e = getenv("MC_REFINE_VECTOR");
+    return e && e[0] == '1';
+  }();
+  if (vec)
+    return cuda_status(mc::launch_refine(frames, fcentroid, landmarks, lcentroid, w, gx, ga, T, L, n, perm, lo, cnt,
+                                         cap, Dex, Rex, Dd, ldd, flags, S_(stream)));
+  return cuda_status(mc::launch_refine_dmma(frames, fcentroid, landmarks, lcentroid, w, gx, ga, T, L, n, perm, lo, cnt,
+                                            cap, Dex, Rex, Dd, ldd, flags, S_(stream)));
 }
 
 int mc_pair_grad(int64_t P, int32_t n, int32_t npad, const double* xplanes, const double* aplanes, const int32_t* xi,

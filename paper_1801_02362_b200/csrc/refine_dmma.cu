@@ -1,0 +1,228 @@
+// Exact refinement tiles on the fp64 tensor cores (DMMA).
+//
+// Same contract as refine_kernel (refine.cu): for a group of 32 sorted frames
+// and each 32-landmark sub-tile of the group's window union, the exact fp64
+// covariances
+//   S[t,l][b][g] = sum_j (x_{t,j,b} - c_{t,b}) w_j (a_{l,j,g} - c_{l,g})
+// followed by the fused Newton + adjugate fit of the in-window pairs.  Here
+// the contraction is a [96 x n] . [n x 96] GEMM on mma.sync m8n8k4 f64
+// (rows (axis b, frame), columns (axis g, landmark), exact fp64 products and
+// sums), fed by a 6-stage cp.async ring of the raw fp32 rows (16 atoms per
+// stage, coalesced); each fragment is centred / weighted in registers when it
+// is read.  The accumulators are then staged through shared memory so one
+// thread owns whole 3x3 blocks for the fit epilogue.
+#include "mc_math.cuh"
+
+namespace mc {
+
+namespace {
+constexpr int QF = 32;                 // frames per group
+constexpr int QL = 32;                 // landmarks per sub-tile
+constexpr int QKC = 16;                // atoms per ring stage
+constexpr int QRS = 3 * QKC + 4;       // 52 floats per staged row: conflict-free fragment reads
+constexpr int QNST = 6;                // ring stages
+constexpr int QNT = 256;
+constexpr int QSTAGE = (QF + QL) * QRS;              // floats per stage
+constexpr int QCS = 3 * QL + 1;                      // staged accumulator row stride (doubles)
+constexpr int QRING = QNST * QSTAGE * (int)sizeof(float);
+constexpr int QCBYTES = 3 * QF * QCS * (int)sizeof(double);
+constexpr int QSMEM = (QRING > QCBYTES ? QRING : QCBYTES) + QNST * QKC * (int)sizeof(double);
+constexpr int QLPT = (QF + QL) * 3 * QKC / QNT;     // 12 raw floats per thread per stage
+
+__device__ __forceinline__ void cpa4(void* dst, const void* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(QNT, 2)
+refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const float* __restrict__ lr,
+                   const double* __restrict__ lc, const double* __restrict__ w, const double* __restrict__ gx,
+                   const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,
+                   const int* __restrict__ lo, const int* __restrict__ cnt, int cap, double* __restrict__ Dex,
+                   double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char qsm[];
+  float* ring = reinterpret_cast<float*>(qsm);                                     // [QNST][QF + QL][QRS]
+  double* sC = reinterpret_cast<double*>(qsm);                                      // [3 QF][QCS] (after the K loop)
+  double* sW = reinterpret_cast<double*>(qsm + (QRING > QCBYTES ? QRING : QCBYTES));  // [QNST][QKC]
+  __shared__ int s_t[QF], s_lo[QF], s_cnt[QF];
+  __shared__ double s_fc[QF][3];
+  __shared__ int s_wlo, s_whi;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;  // rows: m-tiles 6 wm .. +6; columns: n-tiles 3 wn .. +3
+  if (tid < QF) {
+    const int k = blockIdx.x * QF + tid;
+    int t = -1, a = 0, c = 0;
+    if (k < T) {
+      t = perm ? perm[k] : k;
+      a = lo ? lo[t] : 0;
+      c = lo ? cnt[t] : L;
+    }
+    s_t[tid] = t;
+    s_lo[tid] = a;
+    s_cnt[tid] = c;
+    for (int b = 0; b < 3; ++b) s_fc[tid][b] = t >= 0 ? fc[3 * t + b] : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int a = L, b = 0;
+    for (int i = 0; i < QF; ++i)
+      if (s_t[i] >= 0 && s_cnt[i] > 0) { a = min(a, s_lo[i]); b = max(b, s_lo[i] + s_cnt[i]); }
+    s_wlo = a;
+    s_whi = b;
+  }
+  __syncthreads();
+  const int wlo = s_wlo, whi = s_whi;
+  // per-thread fragment constants: frame centroid of each A row tile (axis b = mt / 4)
+  double fcA[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const int mt = wm * 6 + i;
+    fcA[i] = s_fc[(mt & 3) * 8 + gq][mt >> 2];
+  }
+  const int nch = (n + QKC - 1) / QKC;
+  for (int l0 = wlo; l0 < whi; l0 += QL) {
+    double lcB[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int nt = wn * 3 + i;
+      const int l = l0 + (nt & 3) * 8 + gq;
+      lcB[i] = l < L ? lc[3 * l + (nt >> 2)] : 0.0;
+    }
+    // ring stage ch: rows 0..31 frames, 32..63 landmarks, 48 floats each (atoms 16 ch ..)
+    auto issue = [&](int ch) {
+      float* dst = ring + (ch % QNST) * QSTAGE;
+      const int k0 = ch * QKC;
+#pragma unroll
+      for (int u = 0; u < QLPT; ++u) {
+        const int e = tid + u * QNT;  // [0, 64 * 48)
+        const int row = e / (3 * QKC), r = e - row * (3 * QKC);
+        const bool isf = row < QF;
+        const int s = isf ? s_t[row] : l0 + row - QF;
+        const bool ok = ch < nch && (isf ? s >= 0 : s < L) && k0 + r / 3 < n;
+        const float* src = (isf ? fr : lr) + ((int64_t)(ok ? s : 0) * n + (ok ? k0 : 0)) * 3 + (ok ? r : 0);
+        cpa4(dst + row * QRS + r, src, ok);
+      }
+      if (tid < QKC) {
+        const bool ok = ch < nch && k0 + tid < n;
+        cpa8(sW + (ch % QNST) * QKC + tid, w + (ok ? k0 + tid : 0), ok);
+      }
+      cpa_commit();
+    };
+    double c[6][3][2];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+#pragma unroll
+    for (int st = 0; st < QNST - 1; ++st) issue(st);
+    for (int ch = 0; ch < nch; ++ch) {
+      cpa_wait<QNST - 2>();
+      __syncthreads();
+      issue(ch + QNST - 1);
+      const float* sF = ring + (ch % QNST) * QSTAGE;
+      const float* sL = sF + QF * QRS;
+      const double* ww = sW + (ch % QNST) * QKC;
+#pragma unroll
+      for (int s = 0; s < QKC / 4; ++s) {
+        const int jj = 4 * s + tq;
+        const double wj = ww[jj];
+        double a[6], b[3];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const int mt = wm * 6 + i;
+          a[i] = (double)sF[((mt & 3) * 8 + gq) * QRS + 3 * jj + (mt >> 2)] - fcA[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int nt = wn * 3 + i;
+          b[i] = wj * ((double)sL[((nt & 3) * 8 + gq) * QRS + 3 * jj + (nt >> 2)] - lcB[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) dmma884(c[i][j], a[i], b[j]);
+      }
+    }
+    cpa_wait<0>();
+    __syncthreads();
+    // stage accumulators: row (b, f) = mt * 8 + gq, column (g, l) = nt * 8 + 2 tq + e
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int row = (wm * 6 + i) * 8 + gq, col = (wn * 3 + j) * 8 + 2 * tq;
+        sC[row * QCS + col] = c[i][j][0];
+        sC[row * QCS + col + 1] = c[i][j][1];
+      }
+    __syncthreads();
+    // fused fit of the in-window pairs (exact fp64)
+    for (int p = tid; p < QF * QL; p += QNT) {
+      const int f = p / QL, li = p - f * QL;
+      const int t = s_t[f];
+      const int l = l0 + li;
+      if (t < 0 || l >= L) continue;
+      const int slot = l - s_lo[f];
+      if (slot < 0 || slot >= s_cnt[f]) continue;
+      double S[9];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int g = 0; g < 3; ++g) S[b * 3 + g] = sC[(b * QF + f) * QCS + g * QL + li];
+      double q[4];
+      bool ill = false;
+      double msd = fit_fast(S, gx[t], ga[l], Rex ? q : nullptr, &ill);
+      uint8_t fl = 0;
+      if (ill) {
+        double k4[4][4], V[4][4], ev[4];
+        kearsley_from_S(S, gx[t], ga[l], k4);
+        if (!jacobi4(k4, ev, V)) fl |= kFlagNoConverge;
+        msd = ev[0];
+        q[0] = V[0][0]; q[1] = V[1][0]; q[2] = V[2][0]; q[3] = V[3][0];
+      }
+      if (Dex) Dex[(int64_t)t * cap + slot] = msd;
+      if (Dd) Dd[(int64_t)t * ldd + l] = (float)msd;
+      if (Rex) {
+        double r[9];
+        quat_to_rot(q, r);
+        double* o = Rex + ((int64_t)t * cap + slot) * 9;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) o[e] = r[e];
+      }
+      if (fl && flags) flags[t] |= fl;
+    }
+    __syncthreads();  // sC overlays the ring of the next sub-tile
+  }
+}
+
+cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc, const double* w,
+                               const double* gx, const double* ga, int T, int L, int n, const int* perm, const int* lo,
+                               const int* cnt, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,
+                               uint8_t* flags, cudaStream_t stream) {
+  if (T <= 0 || L <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(refine_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  refine_dmma_kernel<<<(T + QF - 1) / QF, QNT, QSMEM, stream>>>(fr, fc, lr, lc, w, gx, ga, T, L, n, perm, lo, cnt,
+                                                                 cap, Dex, Rex, Dd, ldd, flags);
+  return cudaGetLastError();
+}
+
+}  // namespace mc
