@@ -365,7 +365,8 @@ class ConfigTC:
         if name in ("mc_msd_tf32", "mc_msd_tf32_2sm"):
             return "tensor_flop", 3.0 * 18.0 * n * T * L
         if name in ("mc_msd_f16", "mc_msd_f16_2sm"):
-            return "tensor_flop_f16", 3.0 * 18.0 * n * T * L
+            terms = self.pcv.screen_terms if self.cfg == 4 else 3
+            return "tensor_flop_f16", terms * 18.0 * n * T * L
         if name == "mc_center_split16":
             return "bytes", T * n * 3 * 4 + 2 * T * 3 * (((n + 31) // 32) * 32) * 2
         if name == "mc_refine":
@@ -499,7 +500,8 @@ def run_ours(args, rank, world, local_rank):
                 "peak_src": f"bf16_tflops_sustained from {pk['src']} (kind::f16 runs at the bf16 rate; "
                             "kernel timed inside a long step)",
                 "peak_burst": pk["bf16"], "frac_of_burst": ach / pk["bf16"],
-                "flop_basis": "executed 3-term split-FP16 MMAs (3 x 18 n per pair)"}
+                "flop_basis": "executed FP16 MMAs: terms x 18 n per pair (config 4 screen: one-term hi x hi; "
+                              "split-precision estimate: 3 terms)"}
     else:
         ach = amount / (avg_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,

@@ -148,7 +148,9 @@ int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, 
  * mc_msd_tf32 (K2+K3, _kearsley_matrix + eigvals[0] of geometry.py:180-249): all-pairs
  *   3x3 covariance on tcgen05 (3xTF32, TMEM accumulators, TMA pipeline) with the
  *   fp64 Newton lambda_max in the epilogue -> MSD estimate D [T, ldd] fp32.  grid 0 = #SMs.
- * mc_candidates: per frame D_min and the landmark window {lam (D - D_min) <= thr}.
+ * mc_candidates: per frame D_min and the landmark window {lam (D - D_min) <= thr_t},
+ *   thr_t = thr + fcoef * fnorm[t] (fnorm nullable: thr_t = thr) -- the per-frame
+ *   estimate-error allowance of the one-term screen.
  * mc_sort_by_key: counting sort of frames by window start (workspace bins [nbins]).
  * mc_refine: exact fp64 covariance + fit of the in-window pairs (or, with lo = cnt =
  *   NULL, of all pairs: the dense exact MSD matrix into Dd). */
@@ -170,24 +172,29 @@ int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const 
                     const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                     void* stream);
 /* Same contraction with an FP16 operand format (kind::f16 tcgen05.mma, K = 16):
- * mc_center_split16 scales each structure by a power of two 2^e (max |value| < 2^14),
- *   splits into IEEE-half hi + lo (22 significant bits, like the TF32 pair) and writes
- *   them interleaved, hl [3, count, 2 kpad] (kpad % 32 == 0): per 32-atom block
- *   [hi x32 | lo x32], one 128 B line; scale_inv[count] = 2^-e.
+ * mc_center_split16 scales each structure by a power of two 2^e (max |value| < 2^14)
+ *   and writes IEEE halves: terms = 3 -> hi + lo (22 significant bits, like the TF32
+ *   pair) interleaved, hl [3, count, 2 kpad] (kpad % 32 == 0), per 32-atom block
+ *   [hi x32 | lo x32] = one 128 B line; terms = 1 -> hi only, hl [3, count, kpad]
+ *   (kpad % 64 == 0).  scale_inv[count] = 2^-e; opnorm[count] (nullable) = the fp64
+ *   2-norm of the (weighted, centred) operand, for the one-term error bound.
  * mc_msd_f16 / mc_msd_f16_2sm: as mc_msd_tf32 / _2sm on hl operands, S rescaled by
- *   fscale[t] * lscale[l] (exact) before the fp64 Newton epilogue.  Half the operand
- *   bytes and twice the tensor-core rate of the TF32 format per atom. */
+ *   fscale[t] * lscale[l] (exact) before the epilogue.  terms = 3: hi*hi + hi*lo +
+ *   lo*hi (split precision); terms = 1: hi*hi, a screening estimate with
+ *   |D_est - D| <= 4 (2^-10 + n 2^-27) opnorm_t opnorm_l (+ fp32 epilogue slack);
+ *   _2sm supports terms = 3 only. */
 int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
-                      const double* w_disp, int32_t weighted, void* hl, double* scale_inv, double* centroid,
-                      double* gnorm, double* wbar, double* mom, uint8_t* flags, void* stream);
+                      const double* w_disp, int32_t weighted, int32_t terms, void* hl, double* scale_inv,
+                      double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
+                      void* stream);
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
-               const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
-               void* stream);
+               const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, float* D, int64_t ldd,
+               int32_t grid, void* stream);
 int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
                    const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                    void* stream);
-int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
-                  int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
+int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
+                  double fcoef, int32_t cap, int32_t* lo, int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream);
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
               const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,

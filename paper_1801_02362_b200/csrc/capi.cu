@@ -160,11 +160,13 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
                                              fvec, perm, ds, dz, out_f32, S_(stream)));
 }
 
-int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, int32_t cap, int32_t* lo,
-                  int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
-  if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0)) return MC_ERR_CONFIG;
+int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
+                  double fcoef, int32_t cap, int32_t* lo, int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
+  if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0) || !(fcoef >= 0.0))
+    return MC_ERR_CONFIG;
   if (T > 0 && (!D || !lo || !cnt)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_candidates(D, T, L, ldd, lam, thr, cap, lo, cnt, dmin, flags, S_(stream)));
+  return cuda_status(
+      mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, cap, lo, cnt, dmin, flags, S_(stream)));
 }
 
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream) {
@@ -235,36 +237,41 @@ int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const floa
 }
 
 int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
-                      const double* w_disp, int32_t weighted, void* hl, double* scale_inv, double* centroid,
-                      double* gnorm, double* wbar, double* mom, uint8_t* flags, void* stream) {
+                      const double* w_disp, int32_t weighted, int32_t terms, void* hl, double* scale_inv,
+                      double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
+                      void* stream) {
   if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
   if (n < 2) return MC_ERR_INVALID_STRUCTURE;
-  if (count < 0 || kpad < n || kpad % 32 != 0) return MC_ERR_CONFIG;
+  if (terms != 1 && terms != 3) return MC_ERR_CONFIG;
+  if (count < 0 || kpad < n || kpad % (terms == 1 ? 64 : 32) != 0) return MC_ERR_CONFIG;
   if (count > 0 && (!coords || !w_align || !w_disp || !hl || !scale_inv || !gnorm)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_center_split16(coords, dtype, count, n, kpad, w_align, w_disp, weighted, hl, scale_inv,
-                                               centroid, gnorm, wbar, mom, flags, S_(stream)));
+  return cuda_status(mc::launch_center_split16(coords, dtype, count, n, kpad, w_align, w_disp, weighted, terms, hl,
+                                               scale_inv, opnorm, centroid, gnorm, wbar, mom, flags, S_(stream)));
 }
 
 static int msd_f16_args(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
-                        const double* ga, int32_t T, int32_t L, int32_t kpad, const float* D, int64_t ldd) {
-  if (T < 0 || L < 0 || kpad % 32 != 0 || kpad < 32 || ldd < L) return MC_ERR_CONFIG;
+                        const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const float* D,
+                        int64_t ldd) {
+  if (terms != 1 && terms != 3) return MC_ERR_CONFIG;
+  if (T < 0 || L < 0 || kpad % (terms == 1 ? 64 : 32) != 0 || kpad < 32 || ldd < L) return MC_ERR_CONFIG;
   if ((int64_t)T * L > 0 && (!fhl || !lhl || !fsc || !lsc || !gx || !ga || !D)) return MC_ERR_CONFIG;
   if (3LL * T > 0x7fffffffLL || 3LL * L > 0x7fffffffLL) return MC_ERR_CONFIG;
   return MC_OK;
 }
 
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
-               const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
-               void* stream) {
-  const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd);
+               const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, float* D, int64_t ldd,
+               int32_t grid, void* stream) {
+  const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, terms, D, ldd);
   if (st != MC_OK) return st;
-  return cuda_status(mc::launch_msd_f16(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
+  return cuda_status(
+      mc::launch_msd_f16(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, terms, D, ldd, grid, S_(stream)));
 }
 
 int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
                    const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                    void* stream) {
-  const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd);
+  const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, 3, D, ldd);
   if (st != MC_OK) return st;
   return cuda_status(mc::launch_msd_f16_2sm(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
 }

@@ -58,7 +58,8 @@ cudaError_t launch_cv_grad_block_planes(int T, int t0, int n, int npad, int cap,
                                         const double* sig_coef, const int* nsig, const double* fvec,
                                         const uint8_t* refresh, const int* ridx, const double* xyeig, void* ds,
                                         void* dz, int out_f32, cudaStream_t stream);
-cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, int cap, int* lo,
+cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
+                              double fcoef, int cap, int* lo,
                               int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc, const double* w,
@@ -83,10 +84,11 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
                             const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
                             cudaStream_t stream);
 cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
-                                  const double* w_disp, int weighted, void* hl, double* scale_inv, double* centroid,
-                                  double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream);
+                                  const double* w_disp, int weighted, int terms, void* hl, double* scale_inv,
+                                  double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom,
+                                  uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
-                           const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                           const double* ga, int T, int L, int kpad, int terms, float* D, int64_t ldd, int grid,
                            cudaStream_t stream);
 cudaError_t launch_msd_f16_2sm(const void* fhl, const void* lhl, const double* fsc, const double* lsc,
                                const double* gx, const double* ga, int T, int L, int kpad, float* D, int64_t ldd,

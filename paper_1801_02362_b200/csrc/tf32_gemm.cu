@@ -59,7 +59,8 @@ struct OpTF32 {
 struct OpF16 {
   using E = __half;
   // rows of 2 kpad halves: per 32-atom block [hi x32 | lo x32] = one 128 B
-  // line, so one SWIZZLE_128B TMA box row carries both parts of a k-block
+  // line, so one SWIZZLE_128B TMA box row carries both parts of a k-block.
+  // One-term mode (lo == nullptr on entry, see below): rows of kpad hi halves.
   static constexpr bool kInterleave = true;
   static __device__ __forceinline__ void split(double v, E& h, E& l) {
     h = __double2half(v);
@@ -73,7 +74,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
                     const double* __restrict__ w_disp, int weighted, typename OP::E* __restrict__ hi,
                     typename OP::E* __restrict__ lo, double* __restrict__ scale_inv, double* __restrict__ centroid,
                     double* __restrict__ gnorm, double* __restrict__ wbar, double* __restrict__ mom,
-                    uint8_t* __restrict__ flags) {
+                    uint8_t* __restrict__ flags, int one_term = 0, double* __restrict__ opnorm = nullptr) {
   __shared__ double scratch[NT / 32];
   const int64_t b = blockIdx.x;
   const T* x = coords + b * (int64_t)n * 3;
@@ -109,7 +110,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
     scale = ldexp(1.0, e);
     if (threadIdx.x == 0) scale_inv[b] = ldexp(1.0, -e);
   }
-  double g = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, m00 = 0, m01 = 0, m02 = 0, m11 = 0, m12 = 0, m22 = 0;
+  double g = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, m00 = 0, m01 = 0, m02 = 0, m11 = 0, m12 = 0, m22 = 0, on2 = 0.0;
   const int64_t plane = B * (int64_t)kpad;
   for (int j = threadIdx.x; j < kpad; j += NT) {
     double v[3] = {0.0, 0.0, 0.0};
@@ -127,10 +128,14 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
     m11 += wx1 * v[1]; m12 += wx1 * v[2]; m22 += wx2 * v[2];
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
-      const double val = (weighted ? w * v[p] : v[p]) * scale;
+      const double uv = weighted ? w * v[p] : v[p];
+      on2 += uv * uv;
+      const double val = uv * scale;
       typename OP::E h, l;
       OP::split(val, h, l);
-      if (OP::kInterleave) {
+      if (OP::kInterleave && one_term) {
+        hi[p * plane + b * kpad + j] = h;
+      } else if (OP::kInterleave) {
         const int64_t o = 2 * (p * plane + b * kpad) + (j >> 5) * 64 + (j & 31);
         hi[o] = h;
         hi[o + 32] = l;
@@ -141,6 +146,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
     }
   }
   g = block_sum<NT>(g, scratch);
+  if (opnorm) on2 = block_sum<NT>(on2, scratch);
   if (wbar) { b0 = block_sum<NT>(b0, scratch); b1 = block_sum<NT>(b1, scratch); b2 = block_sum<NT>(b2, scratch); }
   if (mom) {
     m00 = block_sum<NT>(m00, scratch); m01 = block_sum<NT>(m01, scratch); m02 = block_sum<NT>(m02, scratch);
@@ -155,6 +161,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
       mom[6 * b + 3] = m11; mom[6 * b + 4] = m12; mom[6 * b + 5] = m22;
     }
     if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
+    if (opnorm) opnorm[b] = sqrt(on2);
   }
 }
 
@@ -172,17 +179,19 @@ cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n,
 }
 
 cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
-                                  const double* w_disp, int weighted, void* hl, double* scale_inv, double* centroid,
-                                  double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream) {
+                                  const double* w_disp, int weighted, int terms, void* hl, double* scale_inv,
+                                  double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom,
+                                  uint8_t* flags, cudaStream_t stream) {
   if (B <= 0) return cudaSuccess;
+  const int one = terms == 1 ? 1 : 0;
   if (dtype == 0)
     center_split_kernel<float, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
         (const float*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
-        gnorm, wbar, mom, flags);
+        gnorm, wbar, mom, flags, one, opnorm);
   else
     center_split_kernel<double, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
         (const double*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
-        gnorm, wbar, mom, flags);
+        gnorm, wbar, mom, flags, one, opnorm);
   return cudaGetLastError();
 }
 
@@ -331,7 +340,7 @@ __device__ __forceinline__ void tile_coords(int tile, int ntm, int ntl, int& tm,
 }
 
 
-template <bool F16>
+template <bool F16, bool ONE = false>
 __global__ void __launch_bounds__(gemm::NT, 1)
 msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__ CUtensorMap mfl,
                 const __grid_constant__ CUtensorMap mlh, const __grid_constant__ CUtensorMap mll,
@@ -350,7 +359,8 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntm = (T + BM - 1) / BM, ntl = (L + BL - 1) / BL;
   const int ntiles = ntm * ntl;
-  const int nkb = kpad / KB;
+  // ONE (one-term F16 screen): 64 hi atoms per 128 B row and stage
+  const int nkb = ONE ? kpad / 64 : kpad / KB;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mfh)) : "memory");
@@ -474,6 +484,15 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
           if constexpr (F16) {
             // 128 B rows: hi atoms at byte 0..63, lo at 64..127; one MMA = 16 atoms = 32 B
             const uint32_t bb = st + 3 * A2_BYTES;
+            if constexpr (ONE) {
+              // one-term screen: hi x hi over 64 atoms (4 MMAs of K = 16 per 128 B row)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int p = 0; p < 3; ++p)
+                  umma<F16>(tmem_base + p * BN, umma_desc_sw128(st + p * A2_BYTES + k * 32),
+                            umma_desc_sw128(bb + k * 32), (kb | k) != 0 ? 1u : 0u);
+            } else
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const uint32_t koff = k * 32;
@@ -615,19 +634,19 @@ bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, i
   return r == CUDA_SUCCESS;
 }
 
-template <bool F16>
+template <bool F16, bool ONE = false>
 static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, const void* ll, const double* gx,
                                 const double* ga, const double* fsc, const double* lsc, int T, int L, int kpad,
                                 float* D, int64_t ldd, int grid, cudaStream_t stream) {
   using namespace gemm;
   if (T <= 0 || L <= 0) return cudaSuccess;
-  if (kpad % Fmt<F16>::KB) return cudaErrorInvalidValue;
+  if (kpad % (ONE ? 64 : Fmt<F16>::KB)) return cudaErrorInvalidValue;
   constexpr int esz = Fmt<F16>::ESZ;
   CUtensorMap mfh, mfl, mlh, mll;
   if (F16) {
-    // interleaved rows of 2 kpad halves; the lo maps are unused
-    if (!make_operand_map(&mfh, fh, esz, 3LL * T, 2LL * kpad, BM, true) ||
-        !make_operand_map(&mlh, lh, esz, 3LL * L, 2LL * kpad, BL, true))
+    // interleaved rows of 2 kpad halves (one-term: kpad hi halves); the lo maps are unused
+    const int64_t re = ONE ? kpad : 2LL * kpad;
+    if (!make_operand_map(&mfh, fh, esz, 3LL * T, re, BM, true) || !make_operand_map(&mlh, lh, esz, 3LL * L, re, BL, true))
       return cudaErrorInvalidValue;
     mfl = mfh;
     mll = mlh;
@@ -639,7 +658,8 @@ static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, 
   }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(msd_tf32_kernel<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e =
+        cudaFuncSetAttribute(msd_tf32_kernel<F16, ONE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -648,7 +668,7 @@ static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int g = grid > 0 ? grid : (ntiles < nsm ? ntiles : nsm);
-  msd_tf32_kernel<F16><<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, fsc, lsc, T, L, kpad, D, ldd);
+  msd_tf32_kernel<F16, ONE><<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, fsc, lsc, T, L, kpad, D, ldd);
   return cudaGetLastError();
 }
 
@@ -659,8 +679,10 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
 }
 
 cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
-                           const double* ga, int T, int L, int kpad, float* D, int64_t ldd, int grid,
+                           const double* ga, int T, int L, int kpad, int terms, float* D, int64_t ldd, int grid,
                            cudaStream_t stream) {
+  if (terms == 1)
+    return launch_gemm1<true, true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
   return launch_gemm1<true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
 }
 

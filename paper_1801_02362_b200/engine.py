@@ -24,6 +24,8 @@ from .errors import ConfigError, DegenerateFitError, EmptyActiveSetError, Invali
 # its weight is < e^-25 = 1.4e-11 of the leading term, so even L = 8192 dropped
 # landmarks change Z by < 1.1e-7 relative.
 DEFAULT_CUTOFF = 25.0
+# window-selection estimate of PathCVTC.evaluate (env MC_SCREEN: "f16x1" | "split")
+SCREEN = __import__("os").environ.get("MC_SCREEN", "f16x1")
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 
 
@@ -220,12 +222,22 @@ class PathCVTC:
     msd_matrix(exact=True): the dense exact matrix (every pair refit in fp64;
     the 3xTF32 estimate error, ~1e-7..1e-5 absolute, cannot certify the
     1e-6 relative tolerance); exact=False returns the estimate.
+
+    screen: the estimate evaluate() selects windows with.  "f16x1" (default
+    with the f16 operand format): one-term FP16 (hi x hi) with the rigorous
+    per-pair bound |D_est - D| <= c(n) ||x_t|| ||w a_l|| folded into each
+    frame's window threshold; "split": the
+    split-precision estimate (3 terms) with the measured margin.  Outputs are
+    the exact refits either way.
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None):
+                 operand_fmt=None, screen=None):
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
+        self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
+        if self.screen not in ("f16x1", "split") or (self.screen == "f16x1" and self.fmt != "f16"):
+            raise ConfigError(f"screen {self.screen!r} with operand format {self.fmt!r}")
         lm = _as_cuda(landmarks, device).float().contiguous()
         if lm.ndim != 3 or lm.shape[-1] != 3:
             raise InvalidStructureError("landmarks must be [L, n, 3]")
@@ -247,7 +259,9 @@ class PathCVTC:
             raise ConfigError("q must have one value per landmark")
         self.q = torch.from_numpy(qq).to(self.device)
         self.lraw = lm
-        self.ls = K.center_split(lm, self.wa, self.w, weighted=True, moments=True, fmt=self.fmt)
+        self._ls = {}
+        self.screen_terms = 1 if self.screen == "f16x1" else 3
+        self.ls = self._lsplit(self.screen_terms)
         if _or_flags(self.ls.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("landmark coordinates contain non-finite values")
         # estimate error margin (in units of lam * D): the split (22 significant bits,
@@ -255,35 +269,57 @@ class PathCVTC:
         # max 6.4e-6 (n=1000) and 6.4e-5 (n=10000)
         self.est_err = 2e-8 * self.n
         self.margin = 2.0 + self.lam * self.est_err
+        if self.screen == "f16x1":
+            # rigorous one-term bound per pair: |D_est - D| <= 4 ||dS||_F, ||dS||_F <=
+            # (2u + u^2 + n 2^-27) ||x_t|| ||w a_l|| (u = 2^-11 rounding of both operands,
+            # Cauchy-Schwarz per entry; n 2^-27: fp32 tensor-core accumulation), x1.25
+            # safety, + fp32-eigenvector Rayleigh slack.  The window threshold of frame t
+            # grows by 2 lam c ||x_t|| max_l ||w a_l|| (pair error + D_min error).
+            u = 2.0 ** -11
+            c_unit = 4.0 * (2 * u + u * u + self.n * 2.0 ** -27) * 1.25 + 1e-6
+            self.na_max = float(self.ls.opnorm.max().item())
+            self.fcoef = 2.0 * self.lam * c_unit * self.na_max
+            self.margin = 2.0
 
-    def _frames(self, frames):
+    def _lsplit(self, terms):
+        """Landmark operand split for `terms` (cached; the scalar fields agree)."""
+        if terms not in self._ls:
+            self._ls[terms] = K.center_split(self.lraw, self.wa, self.w, weighted=True, moments=True, fmt=self.fmt,
+                                             terms=terms if self.fmt == "f16" else 3)
+        return self._ls[terms]
+
+    def _frames(self, frames, terms=3):
         fr = _as_cuda(frames, self.device)
         if fr.dtype != torch.float32:
             fr = fr.float()
         _check_shapes(fr, self.lraw)
-        fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False, fmt=self.fmt)
+        fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False, fmt=self.fmt,
+                            terms=terms if self.fmt == "f16" else 3)
         if _or_flags(fs.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("frame coordinates contain non-finite values")
         return fr.contiguous(), fs
 
-    def estimate(self, frames):
-        fr, fs = self._frames(frames)
-        return K.msd_estimate(fs, self.ls), fr, fs
+    def estimate(self, frames, terms=3):
+        """Split-precision (terms=3) or one-term (f16, terms=1) MSD estimate of every pair."""
+        fr, fs = self._frames(frames, terms)
+        return K.msd_estimate(fs, self._lsplit(terms if self.fmt == "f16" else 3)), fr, fs
 
     def msd_matrix(self, frames, exact=True):
         fr, fs = self._frames(frames)
         D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
         if not exact:
-            return K.msd_estimate(fs, self.ls, D)
+            return K.msd_estimate(fs, self._lsplit(3), D)
         _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D)
         _raise_flags(flags, "msd_matrix")
         return D
 
     def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False):
-        Dest, fr, fs = self.estimate(frames)
+        Dest, fr, fs = self.estimate(frames, self.screen_terms)
         cap = self.window_cap
+        one = self.screen == "f16x1"
         while True:
-            lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap)
+            lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
+                                              fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0)
             if (_or_flags(cflags) & FLAG_SIG_OVERFLOW) and cap < self.L:
                 cap = min(self.L, 4 * cap)
                 continue

@@ -212,8 +212,9 @@ def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ou
     return ds, dz
 
 
-def candidates(D, lam, thr, cap, L=None):
-    """Per-frame D_min and the window of landmarks with lam (D - D_min) <= thr."""
+def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0):
+    """Per-frame D_min and the window of landmarks with lam (D - D_min) <= thr_t,
+    thr_t = thr + fcoef * fnorm[t] (fnorm: optional per-frame fp64 tensor)."""
     T = D.shape[0]
     L = D.shape[1] if L is None else L
     dev = D.device
@@ -221,8 +222,8 @@ def candidates(D, lam, thr, cap, L=None):
     cnt = torch.empty((T,), dtype=I32, device=dev)
     dmin = torch.empty((T,), dtype=torch.float32, device=dev)
     flags = torch.empty((T,), dtype=U8, device=dev)
-    call("mc_candidates", ptr(D), T, L, D.stride(0), float(lam), float(thr), cap, ptr(lo), ptr(cnt), ptr(dmin),
-         ptr(flags), stream_ptr())
+    call("mc_candidates", ptr(D), T, L, D.stride(0), float(lam), float(thr), ptr(fnorm), float(fcoef), cap, ptr(lo),
+         ptr(cnt), ptr(dmin), ptr(flags), stream_ptr())
     return lo, cnt, dmin, flags
 
 
@@ -250,8 +251,8 @@ def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, c
 
 # ---------------------------------------------------------------- fp32 / tensor-core path
 
-def kpad_for(n, fmt="tf32"):
-    q = 32 if fmt == "f16" else 16
+def kpad_for(n, fmt="tf32", terms=3):
+    q = (64 if terms == 1 else 32) if fmt == "f16" else 16
     return ((int(n) + q - 1) // q) * q
 
 
@@ -263,30 +264,36 @@ class Split:
     interleaved tensor hi [3, B, 2 kpad] of scaled IEEE halves (lo None) with
     scale = 2^-e per structure; + per-structure scalars."""
 
-    __slots__ = ("hi", "lo", "scale", "fmt", "centroid", "g", "wbar", "mom", "flags", "n", "kpad", "count")
+    __slots__ = ("hi", "lo", "scale", "fmt", "terms", "opnorm", "centroid", "g", "wbar", "mom", "flags", "n", "kpad",
+                 "count")
 
-    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale=None, fmt="tf32"):
+    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale=None, fmt="tf32", terms=3, opnorm=None):
         self.hi, self.lo, self.centroid, self.g, self.wbar, self.mom, self.flags = hi, lo, centroid, g, wbar, mom, flags
-        self.scale, self.fmt = scale, fmt
+        self.scale, self.fmt, self.terms, self.opnorm = scale, fmt, terms, opnorm
         self.n, self.kpad, self.count = n, kpad, hi.shape[1]
 
 
-def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None):
+def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, terms=3):
     """K1s: centre, optionally fold w into the operand, split into hi/lo planes
     (fmt "f16": power-of-two scaled IEEE halves, "tf32": TF32 words; default
-    env MC_OPERAND_FMT, f16)."""
+    env MC_OPERAND_FMT, f16).  terms=1 (f16 only): hi halves only, for the
+    one-term screening estimate; the operand 2-norms are returned in .opnorm."""
     require_cuda(coords)
     fmt = fmt or OPERAND_FMT
     if fmt not in ("f16", "tf32"):
         raise ValueError(f"operand format {fmt!r}")
+    if terms not in (1, 3) or (terms == 1 and fmt != "f16"):
+        raise ValueError(f"terms={terms} with format {fmt!r}")
     coords = coords.contiguous()
     b, n, _ = coords.shape
-    kpad = kpad_for(n, fmt)
+    kpad = kpad_for(n, fmt, terms)
     dev = coords.device
     dt = _lib.MC_F64 if coords.dtype == torch.float64 else _lib.MC_F32
-    if fmt == "f16":  # interleaved [hi x32 | lo x32] rows
-        hi = torch.empty((3, b, 2 * kpad), dtype=torch.float16, device=dev)
+    opnorm = None
+    if fmt == "f16":  # interleaved [hi x32 | lo x32] rows (one-term: hi rows)
+        hi = torch.empty((3, b, kpad if terms == 1 else 2 * kpad), dtype=torch.float16, device=dev)
         lo = None
+        opnorm = torch.empty((b,), dtype=F64, device=dev)
     else:
         hi = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
         lo = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
@@ -298,11 +305,12 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None):
     flags = torch.empty((b,), dtype=U8, device=dev)
     if fmt == "f16":
         call("mc_center_split16", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
-             ptr(hi), ptr(scale), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
+             terms, ptr(hi), ptr(scale), ptr(opnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags),
+             stream_ptr())
     else:
         call("mc_center_split", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
              ptr(hi), ptr(lo), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
-    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt)
+    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt, terms, opnorm)
 
 
 TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "0") == "1"
@@ -312,15 +320,18 @@ def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
     """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L]),
     in the operand format of the splits.  two_sm (default: env MC_TF32_2SM, on)
     selects the CTA-pair kernel."""
-    if fr.fmt != lm.fmt or fr.kpad != lm.kpad:
-        raise ValueError("frame and landmark splits differ in format / padding")
+    if fr.fmt != lm.fmt or fr.kpad != lm.kpad or fr.terms != lm.terms:
+        raise ValueError("frame and landmark splits differ in format / terms / padding")
     T, L = fr.count, lm.count
     if D is None:
         D = torch.empty((T, L), dtype=torch.float32, device=fr.hi.device)
     pair = TF32_2SM if two_sm is None else two_sm
-    if fr.fmt == "f16":
-        call("mc_msd_f16_2sm" if pair else "mc_msd_f16", ptr(fr.hi), ptr(lm.hi), ptr(fr.scale), ptr(lm.scale),
-             ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())
+    if fr.fmt == "f16" and (fr.terms == 1 or not pair):
+        call("mc_msd_f16", ptr(fr.hi), ptr(lm.hi), ptr(fr.scale), ptr(lm.scale), ptr(fr.g), ptr(lm.g), T, L, fr.kpad,
+             fr.terms, ptr(D), D.stride(0), grid, stream_ptr())
+    elif fr.fmt == "f16":
+        call("mc_msd_f16_2sm", ptr(fr.hi), ptr(lm.hi), ptr(fr.scale), ptr(lm.scale), ptr(fr.g), ptr(lm.g), T, L,
+             fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())
     else:
         call("mc_msd_tf32_2sm" if pair else "mc_msd_tf32", ptr(fr.hi), ptr(fr.lo), ptr(lm.hi), ptr(lm.lo),
              ptr(fr.g), ptr(lm.g), T, L, fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())

@@ -107,3 +107,46 @@ def test_tf32_weighted(cuda_device):
     est = _estimate(wl.frames, wl.landmarks, w, wa)
     ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), w=w, w_align=wa)
     assert np.abs(est - ref).max() < 5e-6
+
+
+@pytest.mark.parametrize("T,L,n", [(128, 48, 16), (300, 100, 100), (257, 97, 1000), (64, 64, 4000)])
+def test_one_term_screen_within_rigorous_bound(T, L, n, cuda_device):
+    """One-term FP16 estimate: |D_est - D| <= c(n) ||x_t|| ||w a_l|| for every pair
+    (the bound PathCVTC folds into each frame's window threshold)."""
+    dev = torch.device("cuda:0")
+    wl = synth.config2(seed=11, T=T, L=L, N=n)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam, screen="f16x1")
+    est, _, fs = pcv.estimate(wl.frames, terms=1)
+    est = est.cpu().numpy().astype(np.float64)
+    ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64))
+    nx = fs.opnorm.cpu().numpy()
+    na = pcv.ls.opnorm.cpu().numpy()
+    c_unit = pcv.fcoef / (2.0 * pcv.lam * pcv.na_max)
+    bound = c_unit * nx[:, None] * na[None, :]
+    err = np.abs(est - ref)
+    print(f"n={n}: max err {err.max():.3e}, max err/bound {np.max(err / bound):.3f}")
+    assert (err <= bound).all()
+    assert dev.type == "cuda"
+
+
+def test_one_term_and_split_screens_agree(cuda_device):
+    """Both screens select windows containing every significant landmark: s, z and the
+    gradients agree to the north-star tolerances (and with the fp64 oracle)."""
+    wl = synth.config4(T=40, L=512, N=600)
+    outs = {}
+    for screen in ("f16x1", "split"):
+        pcv = engine.PathCVTC(wl.landmarks, wl.lam, screen=screen)
+        outs[screen] = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    a, b = outs["f16x1"], outs["split"]
+    np.testing.assert_allclose(a["s"].cpu().numpy(), b["s"].cpu().numpy(), rtol=1e-9)
+    np.testing.assert_allclose(a["z"].cpu().numpy(), b["z"].cpu().numpy(), rtol=1e-9)
+    for key in ("ds", "dz"):  # extra (negligible, < e^-25) landmarks only: per-frame scale
+        x, y = a[key].cpu().numpy(), b[key].cpu().numpy()
+        scale = np.abs(y).reshape(y.shape[0], -1).max(axis=1)
+        assert np.all(np.abs(x - y).reshape(y.shape[0], -1).max(axis=1) <= 1e-9 * scale)
+    # the one-term windows (wider error allowance) contain the split-screen windows
+    alo, acnt = a["window_lo"].cpu().numpy(), a["window_cnt"].cpu().numpy()
+    blo, bcnt = b["window_lo"].cpu().numpy(), b["window_cnt"].cpu().numpy()
+    assert (alo <= blo).all() and (alo + acnt >= blo + bcnt).all()
+    ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    np.testing.assert_allclose(a["s"].cpu().numpy(), ref["s"], rtol=1e-6)
