@@ -86,6 +86,21 @@ def _or_flags(flags):
     return int(np.bitwise_or.reduce(flags.flatten().cpu().numpy())) if flags.numel() else 0
 
 
+_FLAG_BITS = (1, 2, 4, 8, 16)
+
+
+def _flag_bits_dev(flags):
+    """Bitwise OR of a uint8 flag array as a device bool[5] (no host sync)."""
+    bits = torch.tensor(_FLAG_BITS, dtype=torch.int32, device=flags.device)
+    if flags.numel() == 0:
+        return torch.zeros(len(_FLAG_BITS), dtype=torch.bool, device=flags.device)
+    return ((flags.flatten().to(torch.int32)[:, None] & bits) != 0).any(0)
+
+
+def _bits_value(row):
+    return sum(b for b, on in zip(_FLAG_BITS, row) if on)
+
+
 class PathCV:
     """Resident landmark set + evaluator for s, z and their atom gradients.
 
@@ -288,20 +303,20 @@ class PathCVTC:
                                              terms=terms if self.fmt == "f16" else 3)
         return self._ls[terms]
 
-    def _frames(self, frames, terms=3):
+    def _frames(self, frames, terms=3, check=True):
         fr = _as_cuda(frames, self.device)
         if fr.dtype != torch.float32:
             fr = fr.float()
         _check_shapes(fr, self.lraw)
         fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False, fmt=self.fmt,
                             terms=terms if self.fmt == "f16" else 3)
-        if _or_flags(fs.flags) & FLAG_NON_FINITE:
+        if check and _or_flags(fs.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("frame coordinates contain non-finite values")
         return fr.contiguous(), fs
 
-    def estimate(self, frames, terms=3):
+    def estimate(self, frames, terms=3, check=True):
         """Split-precision (terms=3) or one-term (f16, terms=1) MSD estimate of every pair."""
-        fr, fs = self._frames(frames, terms)
+        fr, fs = self._frames(frames, terms, check)
         return K.msd_estimate(fs, self._lsplit(terms if self.fmt == "f16" else 3)), fr, fs
 
     def msd_matrix(self, frames, exact=True):
@@ -314,28 +329,38 @@ class PathCVTC:
         return D
 
     def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False):
-        Dest, fr, fs = self.estimate(frames, self.screen_terms)
-        cap = self.window_cap
+        Dest, fr, fs = self.estimate(frames, self.screen_terms, check=False)
         one = self.screen == "f16x1"
+        cap = self.window_cap
         while True:
+            # the whole pipeline is enqueued without host round trips; the status
+            # flags of every stage are reduced on the device and read once at the end
             lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
                                               fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0)
-            if (_or_flags(cflags) & FLAG_SIG_OVERFLOW) and cap < self.L:
+            perm = K.sort_by_key(lo, self.L)
+            Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap)
+            wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
+                                    rowcnt=cnt)
+            out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
+                   "nsig": wres["nsig"]}
+            if grad:
+                out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap,
+                                                           perm, out_dtype)
+            status = torch.stack([_flag_bits_dev(fs.flags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
+                                  _flag_bits_dev(wres["flags"])])
+            ff, cf, rf, wf = (_bits_value(r) for r in status.cpu().tolist())
+            if ff & FLAG_NON_FINITE:
+                raise InvalidStructureError("frame coordinates contain non-finite values")
+            if (cf & FLAG_SIG_OVERFLOW) and cap < self.L:  # rare: a window wider than cap
                 cap = min(self.L, 4 * cap)
                 continue
             break
-        perm = K.sort_by_key(lo, self.L)
-        Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap)
-        _raise_flags(rflags, "path_cv refine")
-        wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
-                                rowcnt=cnt)
-        if _or_flags(wres["flags"]) & FLAG_NON_FINITE:
+        if rf & FLAG_NON_FINITE:
+            raise InvalidStructureError("path_cv refine: non-finite coordinates or distances")
+        if rf & FLAG_NO_CONVERGE:
+            raise MetadynError("path_cv refine: Jacobi diagonalisation did not converge")
+        if wf & FLAG_NON_FINITE:
             raise InvalidStructureError("non-finite distances in the path-CV reduction")
-        out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
-               "nsig": wres["nsig"]}
-        if grad:
-            out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap,
-                                                       perm, out_dtype)
         if return_estimate:
             out["D_est"] = Dest
         return out
