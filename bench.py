@@ -402,6 +402,18 @@ class ConfigTC:
         return d
 
 
+def measured_traffic(kernel, cfg, T):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full capture of
+    this workload (profiles/traffic.json), else None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            tab = json.load(f)
+        v = tab.get(kernel, {}).get(f"config{cfg}:T{T}")
+        return v
+    except (OSError, ValueError):
+        return None
+
+
 def tf32_peak_measure(device):
     """cuBLAS TF32 GEMM rate on this box (cross-check of the derived peak)."""
     import torch
@@ -521,7 +533,10 @@ def run_ours(args, rank, world, local_rank):
         ach = amount / (avg_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,
                 "peak_src": "nominal B200 FP64 37 TF/s (not measured)"}
-    roof.update({"kernel": name, "share_of_step": tms / total, "avg_launch_ms": avg_ms, "traffic": None})
+    traffic = measured_traffic(name, cfg, runner.T)
+    roof.update({"kernel": name, "share_of_step": tms / total, "avg_launch_ms": avg_ms, "traffic": traffic,
+                 "traffic_unit": "bytes per launch (dram read + write)",
+                 "traffic_src": "profiles/traffic.json (ncu --set full, same workload)" if traffic else None})
     kernels = {k: {"launches": c, "ms_per_step": t / nprof, "share": t / total}
                for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     units = runner.units() * world if runner.scaling == "weak" else runner.units()
