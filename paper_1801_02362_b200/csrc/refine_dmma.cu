@@ -7,9 +7,9 @@
 // followed by the fused Newton + adjugate fit of the in-window pairs.  Here
 // the contraction is a [96 x n] . [n x 96] GEMM on mma.sync m8n8k4 f64
 // (rows (axis b, frame), columns (axis g, landmark), exact fp64 products and
-// sums), fed by a 6-stage cp.async ring of the raw fp32 rows (16 atoms per
-// stage, coalesced); each fragment is centred / weighted in registers when it
-// is read.  The accumulators are then staged through shared memory so one
+// sums), fed by a 4-stage cp.async ring of the raw fp32 rows (32 atoms per
+// stage, 16-byte copies when N % 4 == 0); each fragment is centred / weighted
+// in registers when it is read.  The accumulators are then staged through shared memory so one
 // thread owns whole 3x3 blocks for the fit epilogue.
 #include "mc_math.cuh"
 
@@ -18,16 +18,18 @@ namespace mc {
 namespace {
 constexpr int QF = 32;                 // frames per group
 constexpr int QL = 32;                 // landmarks per sub-tile
-constexpr int QKC = 16;                // atoms per ring stage
-constexpr int QRS = 3 * QKC + 4;       // 52 floats per staged row: conflict-free fragment reads
-constexpr int QNST = 6;                // ring stages
+constexpr int QKC = 32;                // atoms per ring stage
+constexpr int QRS = 3 * QKC + 4;       // 100 floats per staged row: conflict-free fragment reads, 16 B aligned
+constexpr int QNST = 4;                // ring stages
 constexpr int QNT = 256;
 constexpr int QSTAGE = (QF + QL) * QRS;              // floats per stage
 constexpr int QCS = 3 * QL + 1;                      // staged accumulator row stride (doubles)
 constexpr int QRING = QNST * QSTAGE * (int)sizeof(float);
 constexpr int QCBYTES = 3 * QF * QCS * (int)sizeof(double);
 constexpr int QSMEM = (QRING > QCBYTES ? QRING : QCBYTES) + QNST * QKC * (int)sizeof(double);
-constexpr int QLPT = (QF + QL) * 3 * QKC / QNT;     // 12 raw floats per thread per stage
+constexpr int QLPT = (QF + QL) * 3 * QKC / QNT;     // 24 raw floats per thread per stage (scalar copies)
+constexpr int QV4 = 3 * QKC / 4;                     // 24 float4 per staged row
+constexpr int QVPT = (QF + QL) * QV4 / QNT;          // 6 float4 per thread per stage
 
 __device__ __forceinline__ void cpa4(void* dst, const void* src, bool ok) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -36,6 +38,10 @@ __device__ __forceinline__ void cpa4(void* dst, const void* src, bool ok) {
 __device__ __forceinline__ void cpa8(void* dst, const void* src, bool ok) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa16(void* dst, const void* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -48,6 +54,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 }  // namespace
 
+template <bool VEC>
 __global__ void __launch_bounds__(QNT, 2)
 refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const float* __restrict__ lr,
                    const double* __restrict__ lc, const double* __restrict__ w, const double* __restrict__ gx,
@@ -103,23 +110,38 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
       const int l = l0 + (nt & 3) * 8 + gq;
       lcB[i] = l < L ? lc[3 * l + (nt >> 2)] : 0.0;
     }
-    // ring stage ch: rows 0..31 frames, 32..63 landmarks, 48 floats each (atoms 16 ch ..)
-    auto issue = [&](int ch) {
-      float* dst = ring + (ch % QNST) * QSTAGE;
+    // ring stage ch: rows 0..31 frames, 32..63 landmarks, 3 QKC floats each (atoms QKC ch ..)
+    auto issue = [&](int ch, int slot) {
+      float* dst = ring + slot * QSTAGE;
       const int k0 = ch * QKC;
+      if (VEC) {
+        // N % 4 == 0: every row chunk starts 16-byte aligned and the atom tail is a
+        // whole number of float4 (3 (N - k0) floats, a multiple of 12)
 #pragma unroll
-      for (int u = 0; u < QLPT; ++u) {
-        const int e = tid + u * QNT;  // [0, 64 * 48)
-        const int row = e / (3 * QKC), r = e - row * (3 * QKC);
-        const bool isf = row < QF;
-        const int s = isf ? s_t[row] : l0 + row - QF;
-        const bool ok = ch < nch && (isf ? s >= 0 : s < L) && k0 + r / 3 < n;
-        const float* src = (isf ? fr : lr) + ((int64_t)(ok ? s : 0) * n + (ok ? k0 : 0)) * 3 + (ok ? r : 0);
-        cpa4(dst + row * QRS + r, src, ok);
+        for (int u = 0; u < QVPT; ++u) {
+          const int e = tid + u * QNT;
+          const int row = e / QV4, c4 = e - row * QV4;
+          const bool isf = row < QF;
+          const int s = isf ? s_t[row] : l0 + row - QF;
+          const bool ok = ch < nch && (isf ? s >= 0 : s < L) && 3 * k0 + 4 * c4 + 4 <= 3 * n;
+          const float* src = (isf ? fr : lr) + (ok ? ((int64_t)s * n + k0) * 3 + 4 * c4 : 0);
+          cpa16(dst + row * QRS + 4 * c4, src, ok);
+        }
+      } else {
+#pragma unroll 4
+        for (int u = 0; u < QLPT; ++u) {
+          const int e = tid + u * QNT;  // [0, 64 * 3 QKC)
+          const int row = e / (3 * QKC), r = e - row * (3 * QKC);
+          const bool isf = row < QF;
+          const int s = isf ? s_t[row] : l0 + row - QF;
+          const bool ok = ch < nch && (isf ? s >= 0 : s < L) && k0 + r / 3 < n;
+          const float* src = (isf ? fr : lr) + (ok ? ((int64_t)s * n + k0) * 3 + r : 0);
+          cpa4(dst + row * QRS + r, src, ok);
+        }
       }
       if (tid < QKC) {
         const bool ok = ch < nch && k0 + tid < n;
-        cpa8(sW + (ch % QNST) * QKC + tid, w + (ok ? k0 + tid : 0), ok);
+        cpa8(sW + slot * QKC + tid, w + (ok ? k0 + tid : 0), ok);
       }
       cpa_commit();
     };
@@ -129,34 +151,41 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 #pragma unroll
       for (int j = 0; j < 3; ++j) c[i][j][0] = c[i][j][1] = 0.0;
 #pragma unroll
-    for (int st = 0; st < QNST - 1; ++st) issue(st);
+    for (int st = 0; st < QNST - 1; ++st) issue(st, st);
+    // per-thread fragment offsets inside a stage (loop invariant)
+    int offA[6], offB[3];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const int mt = wm * 6 + i;
+      offA[i] = ((mt & 3) * 8 + gq) * QRS + 3 * tq + (mt >> 2);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int nt = wn * 3 + i;
+      offB[i] = (QF + (nt & 3) * 8 + gq) * QRS + 3 * tq + (nt >> 2);
+    }
+    int slot = 0, fill = QNST - 1;
     for (int ch = 0; ch < nch; ++ch) {
       cpa_wait<QNST - 2>();
       __syncthreads();
-      issue(ch + QNST - 1);
-      const float* sF = ring + (ch % QNST) * QSTAGE;
-      const float* sL = sF + QF * QRS;
-      const double* ww = sW + (ch % QNST) * QKC;
+      issue(ch + QNST - 1, fill);
+      fill = fill + 1 == QNST ? 0 : fill + 1;
+      const float* sg = ring + slot * QSTAGE;
+      const double* ww = sW + slot * QKC + tq;
 #pragma unroll
       for (int s = 0; s < QKC / 4; ++s) {
-        const int jj = 4 * s + tq;
-        const double wj = ww[jj];
+        const double wj = ww[4 * s];
         double a[6], b[3];
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const int mt = wm * 6 + i;
-          a[i] = (double)sF[((mt & 3) * 8 + gq) * QRS + 3 * jj + (mt >> 2)] - fcA[i];
-        }
+        for (int i = 0; i < 6; ++i) a[i] = (double)sg[offA[i] + 12 * s] - fcA[i];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          const int nt = wn * 3 + i;
-          b[i] = wj * ((double)sL[((nt & 3) * 8 + gq) * QRS + 3 * jj + (nt >> 2)] - lcB[i]);
-        }
+        for (int i = 0; i < 3; ++i) b[i] = wj * ((double)sg[offB[i] + 12 * s] - lcB[i]);
 #pragma unroll
         for (int i = 0; i < 6; ++i)
 #pragma unroll
           for (int j = 0; j < 3; ++j) dmma884(c[i][j], a[i], b[j]);
       }
+      slot = slot + 1 == QNST ? 0 : slot + 1;
     }
     cpa_wait<0>();
     __syncthreads();
@@ -216,12 +245,19 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
   if (T <= 0 || L <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(refine_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
+    cudaError_t e = cudaFuncSetAttribute(refine_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(refine_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  refine_dmma_kernel<<<(T + QF - 1) / QF, QNT, QSMEM, stream>>>(fr, fc, lr, lc, w, gx, ga, T, L, n, perm, lo, cnt,
-                                                                 cap, Dex, Rex, Dd, ldd, flags);
+  const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(fr) & 15) == 0 && (reinterpret_cast<uintptr_t>(lr) & 15) == 0;
+  if (vec)
+    refine_dmma_kernel<true><<<(T + QF - 1) / QF, QNT, QSMEM, stream>>>(fr, fc, lr, lc, w, gx, ga, T, L, n, perm, lo,
+                                                                       cnt, cap, Dex, Rex, Dd, ldd, flags);
+  else
+    refine_dmma_kernel<false><<<(T + QF - 1) / QF, QNT, QSMEM, stream>>>(fr, fc, lr, lc, w, gx, ga, T, L, n, perm, lo,
+                                                                        cnt, cap, Dex, Rex, Dd, ldd, flags);
   return cudaGetLastError();
 }
 
