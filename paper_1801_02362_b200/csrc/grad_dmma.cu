@@ -52,7 +52,14 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 }  // namespace
 
-template <typename OT>
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, bool ok) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+// VEC: N % 4 == 0 and 16-byte aligned inputs -> 16-byte copies of whole float4
+// (3 * (atoms) floats per row chunk is then a multiple of 4 at every boundary)
+template <typename OT, bool VEC>
 __global__ void __launch_bounds__(DNT, 1)
 cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const double* __restrict__ fcen,
                     const float* __restrict__ lraw, const double* __restrict__ lcen, const double* __restrict__ w,
@@ -103,13 +110,24 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   for (int a0 = katom0; a0 < katom1; a0 += DNA) {
     // the epilogue's frame coordinates: one cp.async group issued now, long
     // complete by the time the contraction below has finished
+    if (VEC) {
 #pragma unroll
-    for (int u = 0; u < XPT; ++u) {
-      const int e = tid + u * DNT;  // [0, DG * 3 DNA)
-      const int f = e / (3 * DNA), r = e - f * (3 * DNA);
-      const int t = s_t[f];
-      const bool ok = t >= 0 && a0 + r / 3 < n;
-      cp_async4(sX + e, fraw + ((int64_t)(ok ? t : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+      for (int u = 0; u < XPT / 4; ++u) {
+        const int e4 = tid + u * DNT;  // [0, DG * 3 DNA / 4)
+        const int f = e4 / (3 * DNA / 4), r = 4 * (e4 - f * (3 * DNA / 4));
+        const int t = s_t[f];
+        const bool ok = t >= 0 && 3 * a0 + r + 4 <= 3 * n;
+        cp_async16(sX + f * 3 * DNA + r, fraw + (ok ? ((int64_t)t * n + a0) * 3 + r : 0), ok);
+      }
+    } else {
+#pragma unroll 4
+      for (int u = 0; u < XPT; ++u) {
+        const int e = tid + u * DNT;  // [0, DG * 3 DNA)
+        const int f = e / (3 * DNA), r = e - f * (3 * DNA);
+        const int t = s_t[f];
+        const bool ok = t >= 0 && a0 + r / 3 < n;
+        cp_async4(sX + e, fraw + ((int64_t)(ok ? t : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+      }
     }
     cp_commit();
     double c[6][4][2];
@@ -143,43 +161,64 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         __syncthreads();
       }
       const int nch = (3 * wn + DKC - 1) / DKC;
-      // stage chunk ch (landmarks w0 + CHL ch .., atoms a0 .. a0 + DNA) into ring slot ch % NST;
+      // stage chunk ch (landmarks w0 + CHL ch .., atoms a0 .. a0 + DNA) into ring slot `slot`;
       // out-of-range elements are zero-filled (their coefficients are zero too)
-      auto issue = [&](int ch) {
-        float* dst = sR + (ch % NST) * CHL * LROW;
+      auto issue = [&](int ch, int slot) {
+        float* dst = sR + slot * CHL * LROW;
+        if (VEC) {
 #pragma unroll
-        for (int u = 0; u < LPT; ++u) {
-          const int e = tid + u * DNT;  // [0, CHL * 3 DNA)
-          const int q = e / (3 * DNA), r = e - q * (3 * DNA);
-          const int li = w0 + ch * CHL + q;
-          const bool ok = ch < nch && li < w0 + wn && a0 + r / 3 < n;
-          cp_async4(dst + q * LROW + r, lraw + ((int64_t)(ok ? li : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+          for (int u = 0; u < LPT / 4; ++u) {
+            const int e4 = tid + u * DNT;  // [0, CHL * 3 DNA / 4)
+            const int q = e4 / (3 * DNA / 4), r = 4 * (e4 - q * (3 * DNA / 4));
+            const int li = w0 + ch * CHL + q;
+            const bool ok = ch < nch && li < w0 + wn && 3 * a0 + r + 4 <= 3 * n;
+            cp_async16(dst + q * LROW + r, lraw + (ok ? ((int64_t)li * n + a0) * 3 + r : 0), ok);
+          }
+        } else {
+#pragma unroll 4
+          for (int u = 0; u < LPT; ++u) {
+            const int e = tid + u * DNT;  // [0, CHL * 3 DNA)
+            const int q = e / (3 * DNA), r = e - q * (3 * DNA);
+            const int li = w0 + ch * CHL + q;
+            const bool ok = ch < nch && li < w0 + wn && a0 + r / 3 < n;
+            cp_async4(dst + q * LROW + r, lraw + ((int64_t)(ok ? li : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+          }
         }
         cp_commit();
       };
 #pragma unroll
-      for (int st = 0; st < NST - 1; ++st) issue(st);
+      for (int st = 0; st < NST - 1; ++st) issue(st, st);
+      // loop-invariant fragment offsets: B element (kk = 4 s + tq -> landmark q, axis g)
+      int offB[DKC / 4];
+#pragma unroll
+      for (int s = 0; s < DKC / 4; ++s) {
+        const int kc = s * 4 + tq;
+        offB[s] = (kc / 3) * LROW + (warp * 32 + gq) * 3 + kc % 3;
+      }
+      const double* aRow = sA + gq * AST + tq;
+      int slot = 0, fill = NST - 1;
       for (int ch = 0; ch < nch; ++ch) {
         cp_wait<NST - 2>();
         __syncthreads();
-        issue(ch + NST - 1);
-        const float* rb = sR + (ch % NST) * CHL * LROW + (warp * 32 + gq) * 3;
+        issue(ch + NST - 1, fill);
+        fill = fill + 1 == NST ? 0 : fill + 1;
+        const float* rb = sR + slot * CHL * LROW;
+        const double* ak = aRow + ch * DKC;
+        const double* lk = sLc + ch * DKC + tq;
 #pragma unroll
         for (int s = 0; s < DKC / 4; ++s) {
-          const int kc = s * 4 + tq;            // kk within the chunk
-          const int q = kc / 3, g = kc - q * 3;
-          const int kk = ch * DKC + kc;
-          const double lcg = sLc[kk];
+          const double lcg = lk[4 * s];
           double a[6], b[4];
 #pragma unroll
-          for (int m = 0; m < 6; ++m) a[m] = sA[(m * 8 + gq) * AST + kk];
+          for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = (double)rb[q * LROW + j * 24 + g] - lcg;
+          for (int j = 0; j < 4; ++j) b[j] = (double)rb[offB[s] + j * 24] - lcg;
 #pragma unroll
           for (int m = 0; m < 6; ++m)
 #pragma unroll
             for (int j = 0; j < 4; ++j) dmma(c[m][j], a[m], b[j]);
         }
+        slot = slot + 1 == NST ? 0 : slot + 1;
       }
       cp_wait<0>();
       __syncthreads();
@@ -229,18 +268,24 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
   dim3 grid((T + DG - 1) / DG, (n + DATOMS - 1) / DATOMS);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(cv_grad_dmma_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(cv_grad_dmma_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
-    if (e != cudaSuccess) return e;
+    for (const void* fn : {(const void*)cv_grad_dmma_kernel<float, true>, (const void*)cv_grad_dmma_kernel<float, false>,
+                           (const void*)cv_grad_dmma_kernel<double, true>, (const void*)cv_grad_dmma_kernel<double, false>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
-  if (out_f32)
-    cv_grad_dmma_kernel<float><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,
-                                                            sig_coef, nsig, fvec, perm, (float*)ds, (float*)dz);
-  else
-    cv_grad_dmma_kernel<double><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,
-                                                             sig_coef, nsig, fvec, perm, (double*)ds, (double*)dz);
+  const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(fraw) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(lraw) & 15) == 0;
+#define MC_GD_LAUNCH(OTT, V)                                                                                         \
+  cv_grad_dmma_kernel<OTT, V><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,     \
+                                                            sig_coef, nsig, fvec, perm, (OTT*)ds, (OTT*)dz)
+  if (out_f32) {
+    if (vec) MC_GD_LAUNCH(float, true); else MC_GD_LAUNCH(float, false);
+  } else {
+    if (vec) MC_GD_LAUNCH(double, true); else MC_GD_LAUNCH(double, false);
+  }
+#undef MC_GD_LAUNCH
   return cudaGetLastError();
 }
 
