@@ -135,6 +135,23 @@ int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutof
                       const double* rxy, const double* xyeig, const double* gx, const double* ga, const double* lmom,
                       double* s, double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec,
                       uint8_t* flags, void* stream);
+/* Neighbour-list variant of mc_pathcv_weights on dense rows (SPEC neighbourlist +
+ * colvar active set): row t sums over the nb_m landmarks
+ * nb_idx[nb_row[t] * nb_m ..] only.  dmode 1 writes the row distances (Eq. 5 on
+ * non-refresh rows) into D and returns; dmode 2 takes D as already filled. */
+int mc_pathcv_weights_nl(int32_t T, int32_t t0, int32_t L, double lam, double cutoff, int32_t cap,
+                         const int32_t* nb_idx, const int32_t* nb_row, int32_t nb_m, int32_t dmode, double* D,
+                         const double* q, const double* R, const double* fwbar, const double* lwbar,
+                         const uint8_t* refresh, const int32_t* ridx, const double* S, const double* rxy,
+                         const double* xyeig, const double* gx, const double* ga, const double* lmom, double* s,
+                         double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec, uint8_t* flags,
+                         void* stream);
+/* mc_neighbour_topm (SPEC neighbourlist.maybe_update): for each of nrows rows
+ * (rows[k], nullable = 0..nrows-1) of D [*, ldd] (fp32/fp64), the indices of the M
+ * smallest distances, ties by lower index, ascending, into idx [nrows, M].
+ * M > L -> MC_ERR_CONFIG. */
+int mc_neighbour_topm(const void* D, int dtype, int32_t nrows, int32_t L, int64_t ldd, const int32_t* rows, int32_t M,
+                      int32_t* idx, void* stream);
 int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,

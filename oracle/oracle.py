@@ -354,15 +354,32 @@ def path_cv_exact(frames, landmarks, lam, q=None, w=None, w_align=None, grad=Tru
     return out
 
 
+def neighbour_update(distances, m):
+    """SPEC neighbourlist maybe_update (SPEC.md: [MODULE] neighbourlist, OP
+    maybe_update): indices of the m smallest distances, ties broken by the lower
+    index, sorted ascending.  m > N -> configuration error."""
+    d = np.asarray(distances, dtype=float)
+    if not 1 <= m <= d.shape[-1]:
+        raise ValueError("neighbour list size must satisfy 1 <= M <= N")
+    order = np.lexsort((np.arange(d.shape[-1]), d))  # primary: distance, secondary: index
+    return np.sort(order[:m])
+
+
 def close_structure_replay(frames, landmarks, lam, eps, q=None, w=None, w_align=None,
-                           grad=True):
-    """Alg. 2, no neighbour list.
+                           grad=True, neighbours=None, nl_stride=1):
+    """Alg. 2 (PAPER.md:168-194; SPEC.md:133-141,157-162).
 
     Per frame: centre x; always one exact fit x<->y with derivatives (first
     frame: y := x, D(x,y) := 0); refresh if first frame or D(x,y) > eps
     (strict).  On refresh y <- x_c, the saved rotations R_{a_i y} are refit
     exactly and the exact distances are returned; otherwise the Eq. 5/6
     approximations are returned for every landmark.
+
+    neighbours = M (optional): SPEC neighbourlist in close-structure mode -- at
+    frames 0, nl_stride, 2 nl_stride, ... the list is updated from that frame's
+    distances to ALL landmarks (approximated on non-refresh frames, exact on
+    refresh frames); s, z and their gradients sum over the active set only
+    (SPEC colvar "active set").
     """
     frames = np.asarray(frames, dtype=float)
     landmarks = np.asarray(landmarks, dtype=float)
@@ -381,6 +398,7 @@ def close_structure_replay(frames, landmarks, lam, eps, q=None, w=None, w_align=
         out["dz"] = np.zeros((t_count, n, 3))
     y = None
     saved = None
+    active = None
     counters = {"step_count": 0, "reassign_count": 0, "expensive_count": 0, "cheap_count": 0}
     for t in range(t_count):
         xc = center(frames[t], wa)
@@ -417,8 +435,16 @@ def close_structure_replay(frames, landmarks, lam, eps, q=None, w=None, w_align=
                 if grad:
                     grads[i] = g
         out["D"][t] = dist
-        out["s"][t], ds = property_map(dist, grads, q, lam)
-        out["z"][t], dz = path_z(dist, grads, lam)
+        if neighbours is not None:
+            if t % nl_stride == 0:
+                active = neighbour_update(dist, neighbours)
+            out.setdefault("active", np.zeros((t_count, neighbours), dtype=np.int64))[t] = active
+            da, ga_ = dist[active], (grads[active] if grad else None)
+            out["s"][t], ds = property_map(da, ga_, q[active], lam)
+            out["z"][t], dz = path_z(da, ga_, lam)
+        else:
+            out["s"][t], ds = property_map(dist, grads, q, lam)
+            out["z"][t], dz = path_z(dist, grads, lam)
         if grad:
             out["ds"][t], out["dz"][t] = ds, dz
     out["counters"] = counters

@@ -52,6 +52,9 @@ _SIGS = {
     "mc_xy_eig": [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P],
     "mc_pathcv_weights": [_I32, _I32, _I32, _D, _D, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "mc_pathcv_weights_nl": [_I32, _I32, _I32, _D, _D, _I32, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                             _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "mc_neighbour_topm": [_P, ctypes.c_int, _I32, _I32, _I64, _P, _I32, _P, _P],
     "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
     "mc_center_split": [_P, ctypes.c_int, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -110,6 +110,34 @@ int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutof
                                            flags, S_(stream)));
 }
 
+int mc_pathcv_weights_nl(int32_t T, int32_t t0, int32_t L, double lam, double cutoff, int32_t cap,
+                         const int32_t* nb_idx, const int32_t* nb_row, int32_t nb_m, int32_t dmode, double* D,
+                         const double* q, const double* R, const double* fwbar, const double* lwbar,
+                         const uint8_t* refresh, const int32_t* ridx, const double* S, const double* rxy,
+                         const double* xyeig, const double* gx, const double* ga, const double* lmom, double* s,
+                         double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec, uint8_t* flags,
+                         void* stream) {
+  if (T < 0 || t0 < 0 || dmode < 0 || dmode > 2) return MC_ERR_CONFIG;
+  if (T > 0 && L < 1) return MC_ERR_EMPTY_ACTIVE_SET;
+  if (!(lam > 0.0) || !(cutoff > 0.0) || cap < 1) return MC_ERR_CONFIG;
+  if ((nb_idx == nullptr) != (nb_row == nullptr)) return MC_ERR_CONFIG;
+  if (nb_idx && (nb_m < 1 || nb_m > L || L > 16384)) return MC_ERR_CONFIG;
+  if (T > 0 && (!D || !R || !fwbar || !lwbar)) return MC_ERR_CONFIG;
+  if (T > 0 && dmode != 1 && (!q || !s || !z || !sig_idx || !sig_coef || !nsig || !fvec)) return MC_ERR_CONFIG;
+  if (refresh && (!ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cv_weights(T, t0, L, lam, cutoff, cap, L, nullptr, nullptr, D, q, R, fwbar, lwbar,
+                                           refresh, ridx, S, rxy, xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig,
+                                           fvec, flags, S_(stream), nb_idx, nb_row, nb_m, dmode));
+}
+
+int mc_neighbour_topm(const void* D, int dtype, int32_t nrows, int32_t L, int64_t ldd, const int32_t* rows, int32_t M,
+                      int32_t* idx, void* stream) {
+  if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
+  if (nrows < 0 || L < 1 || ldd < L || M < 1 || M > L) return MC_ERR_CONFIG;  // SPEC: M > N -> configuration error
+  if (nrows > 0 && (!D || !idx)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_topm(D, dtype, nrows, L, ldd, rows, M, idx, S_(stream)));
+}
+
 int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, const double* fplanes, const double* lplanes,
                    const double* w, const double* w_align, const int32_t* sig_idx, const double* sig_coef,
                    const int32_t* nsig, const double* fvec, const uint8_t* refresh, const int32_t* ridx,

@@ -36,7 +36,10 @@ cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, i
                               const int* ridx, const double* S, const double* rxy, const double* xyeig,
                               const double* gx, const double* ga, const double* lmom, double* s, double* z,
                               int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
-                              cudaStream_t stream);
+                              cudaStream_t stream, const int* nb_idx = nullptr, const int* nb_row = nullptr,
+                              int nb_m = 0, int dmode = 0);
+cudaError_t launch_topm(const void* D, int dtype, int nrows, int L, int64_t ldd, const int* rows, int M, int* idx,
+                        cudaStream_t stream);
 cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
                            const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,

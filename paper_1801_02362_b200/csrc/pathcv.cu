@@ -34,8 +34,20 @@ __device__ __forceinline__ void mat3_mul(const double* a, const double* b, doubl
     for (int j = 0; j < 3; ++j) c[i * 3 + j] = a[i * 3] * b[j] + a[i * 3 + 1] * b[3 + j] + a[i * 3 + 2] * b[6 + j];
 }
 
+// Neighbour-list restriction (SPEC neighbourlist / colvar "active set"): row t
+// sums over the landmarks listed in nb_idx[nb_row[t] * nb_m ..] only (dense
+// rows); dmode 1 = write the row distances (Eq. 5 on non-refresh rows) and stop,
+// dmode 2 = distances already in D (no recomputation).
+struct NbArgs {
+  const int* idx;
+  const int* row;
+  int m;
+  int dmode;
+};
+constexpr int kNbMaxL = 16384;  // bitmap capacity (landmarks) for the active set
+
 __global__ void __launch_bounds__(WNT)
-cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* __restrict__ rowlo,
+cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int ld, NbArgs nb, const int* __restrict__ rowlo,
                   const int* __restrict__ rowcnt, double* __restrict__ D,
                   const double* __restrict__ q, const double* __restrict__ R, const double* __restrict__ fwbar,
                   const double* __restrict__ lwbar, const uint8_t* __restrict__ refresh,
@@ -46,10 +58,20 @@ cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int 
                   double* __restrict__ fvec, uint8_t* __restrict__ flags) {
   __shared__ double scratch[WNT / 32];
   __shared__ int wcount[WNT / 32];
+  __shared__ uint32_t act[kNbMaxL / 32];
   // frame t (global index; rows of D/S/R and the per-frame inputs) and its
   // chunk-local slot tl (the significant-list outputs of this launch)
   const int t = t0 + blockIdx.x, tl = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool masked = nb.idx != nullptr && nb.dmode != 1;
+  if (masked) {
+    for (int wv = tid; wv < (L + 31) / 32; wv += WNT) act[wv] = 0u;
+    __syncthreads();
+    const int* lst = nb.idx + (int64_t)nb.row[t] * nb.m;
+    for (int k = tid; k < nb.m; k += WNT) atomicOr(&act[lst[k] >> 5], 1u << (lst[k] & 31));
+    __syncthreads();
+  }
+  auto active = [&](int i) { return !masked || ((act[i >> 5] >> (i & 31)) & 1u); };
   const bool approx = refresh && !refresh[t];
   const int r = approx ? ridx[t] : t;
   double Rxy[9];
@@ -67,7 +89,7 @@ cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int 
   bool finite = true;
   for (int i = tid; i < nrow; i += WNT) {
     double d;
-    if (approx) {
+    if (approx && nb.dmode != 2) {
       const double* Ri = R + ((int64_t)r * ld + i) * 9;
       const double* Si = S + ((int64_t)t * ld + i) * 9;
       double Rr[9], Rh[9];
@@ -82,14 +104,17 @@ cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int 
     } else {
       d = Dt[i];
     }
+    if (!active(i)) continue;
     finite = finite && isfinite(d);
     dmin = fmin(dmin, d);
   }
+  if (nb.dmode == 1) return;  // distances only (block-uniform)
   dmin = block_min<WNT>(dmin, scratch);
   const int nonfinite = __syncthreads_or(!finite);
   // pass 2: partition function
   double zs = 0.0, qs = 0.0;
   for (int i = tid; i < nrow; i += WNT) {
+    if (!active(i)) continue;
     const double e = exp(-lam * (Dt[i] - dmin));
     zs += e;
     qs += q[off + i] * e;
@@ -107,7 +132,7 @@ cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int 
     const int i = b0 + tid;
     double di = 0.0;
     bool sig = false;
-    if (i < nrow) {
+    if (i < nrow && active(i)) {
       di = Dt[i];
       sig = lam * (di - dmin) <= cutoff;
     }
@@ -241,9 +266,10 @@ cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, i
                               const int* ridx, const double* S, const double* rxy, const double* xyeig,
                               const double* gx, const double* ga, const double* lmom, double* s, double* z,
                               int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, const int* nb_idx, const int* nb_row, int nb_m, int dmode) {
   if (T <= 0) return cudaSuccess;
-  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, t0, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
+  cv_weights_kernel<<<T, WNT, 0, stream>>>(T, t0, L, lam, cutoff, cap, ld, NbArgs{nb_idx, nb_row, nb_m, dmode}, rowlo,
+                                           rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
                                            xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
   return cudaGetLastError();
 }

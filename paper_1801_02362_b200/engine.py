@@ -163,10 +163,20 @@ class PathCV:
         _raise_flags(flags, "path_cv")
         return self._finish(raw, fr, D, R, S, None, grad, cap, out_dtype)
 
-    def close_replay(self, frames, eps, walkers=1, grad=True, window=DEFAULT_WINDOW, cap=None, out_dtype=None):
-        """Alg. 2 replay: frames [T, n, 3] (walkers == 1) or [W, S, n, 3]."""
+    def close_replay(self, frames, eps, walkers=1, grad=True, window=DEFAULT_WINDOW, cap=None, out_dtype=None,
+                     neighbours=None, nl_stride=1):
+        """Alg. 2 replay: frames [T, n, 3] (walkers == 1) or [W, S, n, 3].
+
+        neighbours = M: SPEC neighbourlist in close-structure mode -- each walker's
+        list is updated at steps 0, nl_stride, 2 nl_stride, ... from that step's
+        distances to all landmarks (approximated or exact, as the step has them;
+        `mc_neighbour_topm`), and s, z and gradients sum over the active set only."""
         if eps is None or not (eps >= 0):
             raise ConfigError("eps must be >= 0")
+        if neighbours is not None and not (1 <= int(neighbours) <= self.L):
+            raise ConfigError("neighbour list size must satisfy 1 <= M <= L")
+        if int(nl_stride) < 1:
+            raise ConfigError("neighbour list stride must be >= 1")
         fr_in = _as_cuda(frames, self.device)
         if fr_in.ndim == 4:
             walkers, steps = int(fr_in.shape[0]), int(fr_in.shape[1])
@@ -178,7 +188,21 @@ class PathCV:
         S = K.cov_dense(fr, self.lm)
         D, R, _, flags = K.fit_dense(S, fr.g, self.lm.g, rowmask=close["refresh"], want_rot=True)
         _raise_flags(flags, "close_structure_replay")
-        out = self._finish(raw, fr, D, R, S, close, grad, cap, out_dtype)
+        nb = None
+        if neighbours is not None:
+            # distances of every step (Eq. 5 rows filled in), then the lists at the update steps
+            K.pathcv_weights(D, self.q, self.lam, R, fr, self.lm, 1, self.cutoff, close=close, S=S, dmode=1)
+            stride = int(nl_stride)
+            nupd = (steps + stride - 1) // stride
+            k = torch.arange(steps, device=self.device, dtype=torch.int32)
+            w_ = torch.arange(walkers, device=self.device, dtype=torch.int32)
+            upd_rows = (w_[:, None] * steps + torch.arange(0, steps, stride, device=self.device,
+                                                           dtype=torch.int32)[None, :]).reshape(-1)
+            nb = {"idx": K.neighbour_topm(D, int(neighbours), rows=upd_rows),
+                  "row": (w_[:, None] * nupd + (k // stride)[None, :]).reshape(-1).contiguous()}
+        out = self._finish(raw, fr, D, R, S, close, grad, cap, out_dtype, nb=nb)
+        if nb is not None:
+            out["active"] = nb["idx"][nb["row"].long()]
         if grad and _or_flags(close["xyflags"]) & FLAG_DEGENERATE:
             raise DegenerateFitError("close-structure fit x<->y has a degenerate spectrum")
         out.update(refresh=close["refresh"].bool(), dxy=close["dxy"], ridx=close["ridx"], onthefly=close["onthefly"])
@@ -187,7 +211,7 @@ class PathCV:
     # significant-list buffers per chunk are bounded to ~this many bytes
     CHUNK_BYTES = 4 << 30
 
-    def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype):
+    def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype, nb=None):
         T = D.shape[0]
         cap0 = self._cap(cap)
         dev = D.device
@@ -205,7 +229,7 @@ class PathCV:
             chunk = min(T - t0, max(8, self.CHUNK_BYTES // (cap * 160)))
             while True:
                 wres = K.pathcv_weights(D, self.q, self.lam, R, fr, self.lm, cap, self.cutoff, close=close, S=S,
-                                        t0=t0, count=chunk, s=s, z=z)
+                                        t0=t0, count=chunk, s=s, z=z, nb=nb, dmode=2 if nb is not None else 0)
                 f = _or_flags(wres["flags"])
                 if f & FLAG_SIG_OVERFLOW and cap < self.L:
                     cap = self.L
@@ -377,5 +401,7 @@ def path_cv(frames, landmarks, lam, q=None, w=None, w_align=None, grad=True):
     return PathCV(landmarks, lam, q, w, w_align).evaluate(frames, grad=grad)
 
 
-def close_structure_replay(frames, landmarks, lam, eps, q=None, w=None, w_align=None, grad=True, walkers=1):
-    return PathCV(landmarks, lam, q, w, w_align).close_replay(frames, eps, walkers=walkers, grad=grad)
+def close_structure_replay(frames, landmarks, lam, eps, q=None, w=None, w_align=None, grad=True, walkers=1,
+                           neighbours=None, nl_stride=1):
+    return PathCV(landmarks, lam, q, w, w_align).close_replay(frames, eps, walkers=walkers, grad=grad,
+                                                              neighbours=neighbours, nl_stride=nl_stride)

@@ -80,7 +80,7 @@ class Structure:
 
     def _centred_device(self):
         dev = _device()
-        x = torch.from_numpy(self.coords)[None].to(dev)
+        x = torch.from_numpy(np.array(self.coords))[None].to(dev)
         n = self.n_atoms
         return K.center(x, _wdev(self.align_weights, n, dev), _wdev(self.disp_weights, n, dev))
 

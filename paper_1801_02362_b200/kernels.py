@@ -151,10 +151,30 @@ def close_decisions(fr: Centred, w, eps, walkers, steps, window=8):
             "onthefly": fly}
 
 
+def neighbour_topm(D, M, rows=None):
+    """Neighbour-list update on the device (SPEC neighbourlist.maybe_update): for each
+    row of D [*, L] (fp32/fp64; the listed ``rows`` or all), the indices of the M
+    smallest distances, ties by lower index, ascending -> int32 [nrows, M]."""
+    require_cuda(D)
+    if D.ndim != 2 or D.stride(1) != 1:
+        raise ValueError("D must be a row-major [rows, L] tensor")
+    L = D.shape[1]
+    rows_t = None if rows is None else rows.to(device=D.device, dtype=I32).contiguous()
+    nrows = D.shape[0] if rows_t is None else rows_t.numel()
+    idx = torch.empty((nrows, M), dtype=I32, device=D.device)
+    dt = _lib.MC_F64 if D.dtype == torch.float64 else _lib.MC_F32
+    call("mc_neighbour_topm", ptr(D), dt, nrows, L, D.stride(0), ptr(rows_t), int(M), ptr(idx), stream_ptr())
+    return idx
+
+
 def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L=None, rowlo=None, rowcnt=None,
-                   t0=0, count=None, s=None, z=None):
+                   t0=0, count=None, s=None, z=None, nb=None, dmode=0):
     """K4 weights for frames t0 .. t0+count-1.  D/R rows are dense [T, L] or sparse
-    windows [T, ld] (rowlo/rowcnt); the significant-list outputs are chunk-local."""
+    windows [T, ld] (rowlo/rowcnt); the significant-list outputs are chunk-local.
+    nb = {"idx": [U, M] int32, "row": [T] int32} restricts each row to its active
+    neighbour set (dense rows); dmode 1 = fill D only, 2 = D already filled."""
+    if nb is not None or dmode:
+        return _pathcv_weights_nl(D, q, lam, R, fr, lm, cap, cutoff, close, S, t0, count, s, z, nb, dmode)
     Ttot, ld = D.shape
     T = Ttot - t0 if count is None else count
     L = ld if L is None else L
@@ -172,6 +192,33 @@ def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L
          ptr(c.get("refresh")), ptr(c.get("ridx")), ptr(S if close else None), ptr(c.get("rxy")), ptr(c.get("xyeig")),
          ptr(fr.g if close else None), ptr(lm.g if close else None), ptr(lm.mom if close else None),
          ptr(s), ptr(z), ptr(sig_idx), ptr(sig_coef), ptr(nsig), ptr(fvec), ptr(flags), stream_ptr())
+    return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags,
+            "t0": t0, "count": T}
+
+
+def _pathcv_weights_nl(D, q, lam, R, fr, lm, cap, cutoff, close, S, t0, count, s, z, nb, dmode):
+    Ttot, L = D.shape
+    T = Ttot - t0 if count is None else count
+    dev = D.device
+    s = torch.empty((Ttot,), dtype=F64, device=dev) if s is None else s
+    z = torch.empty((Ttot,), dtype=F64, device=dev) if z is None else z
+    outs = dmode != 1
+    sig_idx = torch.empty((T, cap), dtype=I32, device=dev) if outs else None
+    sig_coef = torch.empty((T, cap, 18), dtype=F64, device=dev) if outs else None
+    nsig = torch.empty((T,), dtype=I32, device=dev) if outs else None
+    fvec = torch.empty((T, 16), dtype=F64, device=dev) if outs else None
+    flags = torch.empty((T,), dtype=U8, device=dev) if outs else None
+    c = close or {}
+    nbi = nb["idx"] if nb is not None else None
+    nbr = nb["row"] if nb is not None else None
+    call("mc_pathcv_weights_nl", T, t0, L, float(lam), float(cutoff), cap, ptr(nbi), ptr(nbr),
+         int(nbi.shape[1]) if nbi is not None else 0, int(dmode), ptr(D), ptr(q), ptr(R), ptr(fr.wbar), ptr(lm.wbar),
+         ptr(c.get("refresh")), ptr(c.get("ridx")), ptr(S if close else None), ptr(c.get("rxy")), ptr(c.get("xyeig")),
+         ptr(fr.g if close else None), ptr(lm.g if close else None), ptr(lm.mom if close else None),
+         ptr(s if outs else None), ptr(z if outs else None), ptr(sig_idx), ptr(sig_coef), ptr(nsig), ptr(fvec),
+         ptr(flags), stream_ptr())
+    if not outs:
+        return None
     return {"s": s, "z": z, "sig_idx": sig_idx, "sig_coef": sig_coef, "nsig": nsig, "fvec": fvec, "flags": flags,
             "t0": t0, "count": T}
 
