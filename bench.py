@@ -204,12 +204,14 @@ class Config3:
         from paper_1801_02362_b200 import dist as D
         from paper_1801_02362_b200 import engine, synth
 
+        # weak scaling: every rank replays its own W walkers (disjoint seeds of one
+        # global walker set), no data-path collective
         W = walkers_override or 256
         self.steps, self.n, self.L = 1000, 2500, 2048
-        off, cnt = D.shard_range(W, rank, world)
-        self.wl = synth.walkers_device(3, W, self.steps, self.n, self.L, device, off, cnt)
+        off, cnt = rank * W, W
+        self.wl = synth.walkers_device(3, world * W, self.steps, self.n, self.L, device, off, cnt)
         self.device = device
-        self.W_all, self.Wloc = W, cnt
+        self.W_all, self.Wloc = world * W, cnt
         self.T = cnt * self.steps
         import torch
 
@@ -220,7 +222,7 @@ class Config3:
         except RuntimeError:
             self.frames_host = self.frames_dev.cpu()
         self.parallelism = f"walker-sharded dp{world}" if world > 1 else "single"
-        self.scaling = "strong"
+        self.scaling = "weak"
         self.last = None
 
     def _step(self, frames):
@@ -272,10 +274,10 @@ class ConfigTC:
         shp = dict(CONFIG_SHAPES[cfg])
         if frames_override:
             shp["T"] = frames_override
-        T_all = shp["T"]
-        per = (T_all + world - 1) // world
-        off = rank * per
-        cnt = max(0, min(per, T_all - off))
+        # weak scaling: every rank evaluates its own full-size frame set (disjoint
+        # slices of one global set), landmarks replicated, no data-path collective
+        T_all = world * shp["T"]
+        off, cnt = rank * shp["T"], shp["T"]
         self.wl = synth.interp_config_device(shp["seed"], T_all, shp["L"], shp["N"], shp["n_endpoints"], device,
                                              frame_offset=off, frame_count=cnt)
         self.T_all, self.T = T_all, cnt
@@ -290,7 +292,7 @@ class ConfigTC:
             self.frames_host = self.frames_dev.cpu()
             self.host_kind = "pageable (pinning failed)"
         self.parallelism = f"frame-sharded dp{world}" if world > 1 else "single"
-        self.scaling = "strong"
+        self.scaling = "weak"
         self.last = None
         if cfg == 2:
             self.metric, self.unit = "aligned-MSD pairs/s", "pairs/s"
