@@ -40,6 +40,7 @@ extern "C" {
 #define MC_ERR_INVALID_STRUCTURE (-1) /* InvalidStructureError  errors.py:8  */
 #define MC_ERR_DEGENERATE_FIT (-2)    /* DegenerateFitError     errors.py:12 */
 #define MC_ERR_CONFIG (-3)            /* ConfigError            errors.py:16 */
+#define MC_ERR_OUT_OF_GRID (-4)       /* OutOfGridError         errors.py:20 */
 #define MC_ERR_EMPTY_ACTIVE_SET (-5)  /* EmptyActiveSetError    errors.py:24 */
 #define MC_ERR_CUDA_BASE (-100)       /* -100 - cudaError_t                  */
 
@@ -49,6 +50,7 @@ extern "C" {
 #define MC_FLAG_NON_FINITE 4u   /* non-finite coordinates or results (geometry.py:41) */
 #define MC_FLAG_ADJ_FALLBACK 8u /* informational: Jacobi used instead of adjugate      */
 #define MC_FLAG_SIG_OVERFLOW 16u /* significant-landmark list exceeded its capacity     */
+#define MC_FLAG_OUT_OF_GRID 32u /* CV value / hill centre outside the bias grid (SPEC metadynamics) */
 
 /* dtypes */
 #define MC_F32 0
@@ -235,6 +237,28 @@ int mc_pair_grad(int64_t P, int32_t n, int32_t npad, const double* xplanes, cons
  * out[0] = s, out[1] = z; ds, dz [n,3] when grads != NULL. */
 int mc_property_map(int32_t L, int32_t n, const double* D, const double* grads, const double* q, double lam,
                     double* out, double* ds, double* dz, void* stream);
+
+/* ---- metadynamics bias and force (SPEC [MODULE] metadynamics, PAPER Eq. 1) ----
+ * mc_mtd_bias_direct: V[t] = sum_h heights[h] prod_i exp(-(cv[t,i] - centers[h,i])^2 / (2 sigmas[h,i]^2))
+ *   and dV[t, i] = dV/dS_i (analytic); d <= 3 CVs, device arrays.
+ * mc_mtd_grid_deposit / mc_mtd_grid_eval: uniform grid per CV (d = 1 or 2; lo, hi, bins are HOST
+ *   arrays of d values; nodes lo + k h, k = 0..bins, row-major [bins0+1][bins1+1]); val, dgrid
+ *   [d][nodes] and (d = 2) the cross derivative dxy store the cubic Hermite data.  deposit adds
+ *   one hill (device center/sigma [d]) to every node within `cutoff` sigmas (SPEC: 6);
+ *   *flag = MC_FLAG_OUT_OF_GRID for a centre off the grid.  eval interpolates V, dV per frame;
+ *   flags[t] = MC_FLAG_OUT_OF_GRID (V = dV = 0) for a CV off the grid.
+ * mc_mtd_force: F[t,k,c] = -sum_i dV[t,i] G_i[t,k,c] (physical sign, SPEC design decision),
+ *   G_i = g0, g1, g2 the CV gradients [T, n, 3] (dtype f32/f64, F likewise). */
+int mc_mtd_bias_direct(const double* cv, int32_t T, int32_t d, const double* centers, const double* sigmas,
+                       const double* heights, int32_t H, double* V, double* dV, void* stream);
+int mc_mtd_grid_deposit(double* val, double* dgrid, double* dxy, int32_t d, const double* lo, const double* hi,
+                        const int32_t* bins, const double* center, const double* sigma, double height, double cutoff,
+                        uint8_t* flag, void* stream);
+int mc_mtd_grid_eval(const double* val, const double* dgrid, const double* dxy, int32_t d, const double* lo,
+                     const double* hi, const int32_t* bins, const double* cv, int32_t T, double* V, double* dV,
+                     uint8_t* flags, void* stream);
+int mc_mtd_force(const double* dV, int32_t T, int32_t d, const void* g0, const void* g1, const void* g2, int dtype,
+                 int32_t n, void* F, void* stream);
 
 #ifdef __cplusplus
 }

@@ -562,3 +562,117 @@ def batch_path_cv_exact(frames, landmarks, lam, q=None, w=None, w_align=None, gr
         if grad:
             out["ds"][t], out["dz"][t] = ds, dz
     return out
+
+
+# --------------------------------------------------------------------------
+# Metadynamics bias and force (SPEC [MODULE] metadynamics; PAPER Eq. 1;
+# SURVEY §8(f) 2).  Test infrastructure only, like everything in oracle/.
+# --------------------------------------------------------------------------
+
+def mtd_bias_direct(cv, centers, sigmas, heights):
+    """V(S) = sum_h w_h prod_i exp(-(S_i - c_hi)^2 / (2 sigma_hi^2)) and dV/dS_i
+    (analytic hill derivative; SPEC metadynamics bias_and_force, direct mode).
+    cv [T, d]; centers, sigmas [H, d]; heights [H] -> V [T], dV [T, d]."""
+    cv = np.atleast_2d(np.asarray(cv, dtype=float))
+    centers = np.asarray(centers, dtype=float).reshape(-1, cv.shape[1])
+    sigmas = np.asarray(sigmas, dtype=float).reshape(-1, cv.shape[1])
+    heights = np.asarray(heights, dtype=float).reshape(-1)
+    if centers.shape[0] == 0:
+        return np.zeros(cv.shape[0]), np.zeros_like(cv)
+    u = (cv[:, None, :] - centers[None]) / sigmas[None]          # [T, H, d]
+    g = heights[None] * np.exp(-0.5 * np.sum(u * u, axis=-1))     # [T, H]
+    V = g.sum(axis=1)
+    dV = np.einsum("th,thd->td", g, -u / sigmas[None])
+    return V, dV
+
+
+def mtd_grid_new(lo, hi, bins):
+    """Uniform grid per CV dimension (SPEC HillStore.grid): nodes lo + k h, k = 0..bins.
+    Stores values, first derivatives per dimension and (d = 2) the cross derivative,
+    the data of a tensor-product cubic Hermite interpolant."""
+    lo, hi = np.atleast_1d(np.asarray(lo, float)), np.atleast_1d(np.asarray(hi, float))
+    bins = np.atleast_1d(np.asarray(bins, int))
+    d = lo.shape[0]
+    if d not in (1, 2) or hi.shape != lo.shape or bins.shape != lo.shape or np.any(hi <= lo) or np.any(bins < 1):
+        raise ValueError("grid: 1 or 2 dimensions with lo < hi and bins >= 1")
+    shape = tuple(int(b) + 1 for b in bins)
+    return {"lo": lo, "hi": hi, "bins": bins, "h": (hi - lo) / bins, "val": np.zeros(shape),
+            "d": [np.zeros(shape) for _ in range(d)], "dxy": np.zeros(shape) if d == 2 else None}
+
+
+def mtd_grid_deposit(grid, center, sigma, height, cutoff=6.0):
+    """Add one hill to every grid node within `cutoff` sigmas per dimension (SPEC:
+    truncation radius 6 sigma, error <= w e^-18).  Out-of-grid centre -> error."""
+    c, s = np.atleast_1d(np.asarray(center, float)), np.atleast_1d(np.asarray(sigma, float))
+    if np.any(c < grid["lo"]) or np.any(c > grid["hi"]):
+        raise ValueError("hill centre outside the grid")
+    axes = [grid["lo"][i] + grid["h"][i] * np.arange(grid["bins"][i] + 1) for i in range(c.shape[0])]
+    masks = [np.abs(ax - c[i]) <= cutoff * s[i] for i, ax in enumerate(axes)]
+    u = [np.where(m, (ax - c[i]) / s[i], 0.0) for i, (ax, m) in enumerate(zip(axes, masks))]
+    e = [np.where(m, np.exp(-0.5 * ui * ui), 0.0) for ui, m in zip(u, masks)]
+    if c.shape[0] == 1:
+        g = height * e[0]
+        grid["val"] += g
+        grid["d"][0] += g * (-u[0] / s[0])
+    else:
+        g = height * np.outer(e[0], e[1])
+        a0, a1 = (-u[0] / s[0])[:, None], (-u[1] / s[1])[None, :]
+        grid["val"] += g
+        grid["d"][0] += g * a0
+        grid["d"][1] += g * a1
+        grid["dxy"] += g * a0 * a1
+    return grid
+
+
+def _hermite(t):
+    t2, t3 = t * t, t * t * t
+    return (2 * t3 - 3 * t2 + 1, -2 * t3 + 3 * t2, t3 - 2 * t2 + t, t3 - t2,
+            6 * t2 - 6 * t, -6 * t2 + 6 * t, 3 * t2 - 4 * t + 1, 3 * t2 - 2 * t)
+
+
+def mtd_grid_eval(grid, cv):
+    """Cubic Hermite interpolation (per dimension; tensor product for d = 2) of the
+    grid values -> V [T], dV [T, d].  A CV outside the grid raises ValueError (SPEC:
+    out-of-grid error)."""
+    cv = np.atleast_2d(np.asarray(cv, dtype=float))
+    d = cv.shape[1]
+    if np.any(cv < grid["lo"]) or np.any(cv > grid["hi"]):
+        raise ValueError("collective variable outside the bias grid")
+    idx, tt = [], []
+    for i in range(d):
+        x = (cv[:, i] - grid["lo"][i]) / grid["h"][i]
+        k = np.minimum(np.floor(x).astype(int), grid["bins"][i] - 1)
+        idx.append(k)
+        tt.append(x - k)
+    V = np.zeros(cv.shape[0])
+    dV = np.zeros_like(cv)
+    if d == 1:
+        k, t, h = idx[0], tt[0], grid["h"][0]
+        h00, h01, h10, h11, d00, d01, d10, d11 = _hermite(t)
+        f0, f1 = grid["val"][k], grid["val"][k + 1]
+        g0, g1 = grid["d"][0][k] * h, grid["d"][0][k + 1] * h
+        V = h00 * f0 + h01 * f1 + h10 * g0 + h11 * g1
+        dV[:, 0] = (d00 * f0 + d01 * f1 + d10 * g0 + d11 * g1) / h
+        return V, dV
+    kx, ky, tx, ty = idx[0], idx[1], tt[0], tt[1]
+    hx, hy = grid["h"]
+    bx, by = _hermite(tx), _hermite(ty)
+    for a in (0, 1):
+        for b in (0, 1):
+            f = grid["val"][kx + a, ky + b]
+            fx = grid["d"][0][kx + a, ky + b] * hx
+            fy = grid["d"][1][kx + a, ky + b] * hy
+            fxy = grid["dxy"][kx + a, ky + b] * hx * hy
+            H0x, H1x, D0x, D1x = bx[a], bx[2 + a], bx[4 + a], bx[6 + a]
+            H0y, H1y, D0y, D1y = by[b], by[2 + b], by[4 + b], by[6 + b]
+            V += f * H0x * H0y + fx * H1x * H0y + fy * H0x * H1y + fxy * H1x * H1y
+            dV[:, 0] += (f * D0x * H0y + fx * D1x * H0y + fy * D0x * H1y + fxy * D1x * H1y) / hx
+            dV[:, 1] += (f * H0x * D0y + fx * H1x * D0y + fy * H0x * D1y + fxy * H1x * D1y) / hy
+    return V, dV
+
+
+def mtd_force(dV, grads):
+    """Bias force on the atoms (SPEC: F = -dV/dx, the physical sign; Eq. 1 prints +):
+    F_k = -sum_i (dV/dS_i) (dS_i/dx_k).  dV [T, d]; grads: d arrays [T, N, 3]."""
+    dV = np.asarray(dV, dtype=float)
+    return -sum(dV[:, i, None, None] * np.asarray(g, dtype=float) for i, g in enumerate(grads))

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 from .errors import (ConfigError, DegenerateFitError, DeviceError, EmptyActiveSetError,
-                     InvalidStructureError)
+                     InvalidStructureError, OutOfGridError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MCB200_LIB") or os.path.join(_HERE, "libmcb200.so")
@@ -20,6 +20,7 @@ MC_OK = 0
 MC_ERR_INVALID_STRUCTURE = -1
 MC_ERR_DEGENERATE_FIT = -2
 MC_ERR_CONFIG = -3
+MC_ERR_OUT_OF_GRID = -4
 MC_ERR_EMPTY_ACTIVE_SET = -5
 MC_ERR_CUDA_BASE = -100
 
@@ -28,6 +29,7 @@ FLAG_NO_CONVERGE = 2
 FLAG_NON_FINITE = 4
 FLAG_ADJ_FALLBACK = 8
 FLAG_SIG_OVERFLOW = 16
+FLAG_OUT_OF_GRID = 32
 
 MC_F32 = 0
 MC_F64 = 1
@@ -55,6 +57,10 @@ _SIGS = {
     "mc_pathcv_weights_nl": [_I32, _I32, _I32, _D, _D, _I32, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                              _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "mc_neighbour_topm": [_P, ctypes.c_int, _I32, _I32, _I64, _P, _I32, _P, _P],
+    "mc_mtd_bias_direct": [_P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P],
+    "mc_mtd_grid_deposit": [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _D, _D, _P, _P],
+    "mc_mtd_grid_eval": [_P, _P, _P, _I32, _P, _P, _P, _P, _I32, _P, _P, _P, _P],
+    "mc_mtd_force": [_P, _I32, _I32, _P, _P, _P, ctypes.c_int, _I32, _P, _P],
     "mc_pathcv_grad": [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
     "mc_center_split": [_P, ctypes.c_int, _I64, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -117,6 +123,8 @@ def check(status, what=""):
         raise DegenerateFitError(f"{what}: degenerate fit")
     if status == MC_ERR_CONFIG:
         raise ConfigError(f"{what}: invalid configuration / arguments")
+    if status == MC_ERR_OUT_OF_GRID:
+        raise OutOfGridError(f"{what}: collective variable outside the bias grid")
     if status == MC_ERR_EMPTY_ACTIVE_SET:
         raise EmptyActiveSetError(f"{what}: empty active set")
     if status <= MC_ERR_CUDA_BASE:

@@ -304,4 +304,43 @@ int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const
   return cuda_status(mc::launch_msd_f16_2sm(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, D, ldd, grid, S_(stream)));
 }
 
+static bool bad_grid(int32_t d, const double* lo, const double* hi, const int32_t* bins) {
+  if (d < 1 || d > 2 || !lo || !hi || !bins) return true;
+  for (int i = 0; i < d; ++i)
+    if (!(hi[i] > lo[i]) || bins[i] < 1) return true;
+  return false;
+}
+
+int mc_mtd_bias_direct(const double* cv, int32_t T, int32_t d, const double* centers, const double* sigmas,
+                       const double* heights, int32_t H, double* V, double* dV, void* stream) {
+  if (T < 0 || d < 1 || d > 3 || H < 0) return MC_ERR_CONFIG;
+  if (T > 0 && (!cv || !V || !dV || (H > 0 && (!centers || !sigmas || !heights)))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_mtd_bias(cv, T, d, centers, sigmas, heights, H, V, dV, S_(stream)));
+}
+
+int mc_mtd_grid_deposit(double* val, double* dgrid, double* dxy, int32_t d, const double* lo, const double* hi,
+                        const int32_t* bins, const double* center, const double* sigma, double height, double cutoff,
+                        uint8_t* flag, void* stream) {
+  if (bad_grid(d, lo, hi, bins) || !val || !dgrid || (d == 2 && !dxy) || !center || !sigma) return MC_ERR_CONFIG;
+  if (!(height >= 0.0) || !(cutoff > 0.0)) return MC_ERR_CONFIG;
+  return cuda_status(
+      mc::launch_mtd_deposit(val, dgrid, dxy, d, lo, hi, bins, center, sigma, height, cutoff, flag, S_(stream)));
+}
+
+int mc_mtd_grid_eval(const double* val, const double* dgrid, const double* dxy, int32_t d, const double* lo,
+                     const double* hi, const int32_t* bins, const double* cv, int32_t T, double* V, double* dV,
+                     uint8_t* flags, void* stream) {
+  if (bad_grid(d, lo, hi, bins) || T < 0) return MC_ERR_CONFIG;
+  if (T > 0 && (!val || !dgrid || (d == 2 && !dxy) || !cv || !V || !dV)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_mtd_eval(val, dgrid, dxy, d, lo, hi, bins, cv, T, V, dV, flags, S_(stream)));
+}
+
+int mc_mtd_force(const double* dV, int32_t T, int32_t d, const void* g0, const void* g1, const void* g2, int dtype,
+                 int32_t n, void* F, void* stream) {
+  if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
+  if (T < 0 || n < 1 || d < 1 || d > 3) return MC_ERR_CONFIG;
+  if (T > 0 && (!dV || !g0 || !F || (d > 1 && !g1) || (d > 2 && !g2))) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_mtd_force(dV, T, d, g0, g1, g2, dtype, n, F, S_(stream)));
+}
+
 }  // extern "C"

@@ -38,6 +38,16 @@ cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, i
                               int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
                               cudaStream_t stream, const int* nb_idx = nullptr, const int* nb_row = nullptr,
                               int nb_m = 0, int dmode = 0);
+cudaError_t launch_mtd_bias(const double* cv, int T, int d, const double* centers, const double* sigmas,
+                            const double* heights, int H, double* V, double* dV, cudaStream_t stream);
+cudaError_t launch_mtd_deposit(double* val, double* dgrid, double* dxy, int d, const double* lo, const double* hi,
+                               const int* bins, const double* center, const double* sigma, double height,
+                               double cutoff, uint8_t* flag, cudaStream_t stream);
+cudaError_t launch_mtd_eval(const double* val, const double* dgrid, const double* dxy, int d, const double* lo,
+                            const double* hi, const int* bins, const double* cv, int T, double* V, double* dV,
+                            uint8_t* flags, cudaStream_t stream);
+cudaError_t launch_mtd_force(const double* dV, int T, int d, const void* g0, const void* g1, const void* g2,
+                             int dtype, int n, void* F, cudaStream_t stream);
 cudaError_t launch_topm(const void* D, int dtype, int nrows, int L, int64_t ldd, const int* rows, int M, int* idx,
                         cudaStream_t stream);
 cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
