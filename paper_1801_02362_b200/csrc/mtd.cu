@@ -9,6 +9,8 @@
 //                      derivatives, cross derivative) within 6 sigma
 //   mtd_eval_kernel    cubic Hermite interpolation (tensor product for d = 2)
 //   mtd_force_kernel   F = -sum_i dV/dS_i dS_i/dx, streaming (HBM-bound)
+#include <type_traits>
+
 #include "mc_math.cuh"
 
 namespace mc {
@@ -168,18 +170,56 @@ mtd_eval_kernel(const double* __restrict__ val, const double* __restrict__ dgrid
   dV[(int64_t)t * 2 + 1] = vy / hy;
 }
 
-// F[t, k, c] = -sum_i dV[t, i] G_i[t, k, c]; grid-stride over the flattened [T, 3N] (HBM-bound)
-template <typename E>
+// F[t, k, c] = -sum_i dV[t, i] G_i[t, k, c] (HBM-bound stream).  One CTA row per
+// frame slice: blockIdx.y = frame, dV loaded once, 16-byte vectors when the
+// frame's 3N elements are 16-byte aligned (VEC), scalar otherwise.
+template <typename E, bool VEC>
 __global__ void __launch_bounds__(MNT)
 mtd_force_kernel(const double* __restrict__ dV, int d, const E* __restrict__ g0, const E* __restrict__ g1,
-                 const E* __restrict__ g2, int64_t per_frame, int64_t total, E* __restrict__ F) {
-  const int64_t stride = (int64_t)gridDim.x * MNT;
-  for (int64_t e = (int64_t)blockIdx.x * MNT + threadIdx.x; e < total; e += stride) {
-    const int64_t t = e / per_frame;
-    double f = -dV[t * d] * (double)g0[e];
-    if (d > 1) f -= dV[t * d + 1] * (double)g1[e];
-    if (d > 2) f -= dV[t * d + 2] * (double)g2[e];
-    F[e] = (E)f;
+                 const E* __restrict__ g2, int64_t per_frame, int T, E* __restrict__ F) {
+  for (int64_t t = blockIdx.y; t < T; t += gridDim.y) {
+  const double a0 = -dV[t * d], a1 = d > 1 ? -dV[t * d + 1] : 0.0, a2 = d > 2 ? -dV[t * d + 2] : 0.0;
+  const int64_t base = t * per_frame;
+  constexpr int W = 16 / sizeof(E);
+  using V = typename std::conditional<sizeof(E) == 4, float4, double2>::type;
+  if (VEC) {
+    const int64_t nv = per_frame / W;
+    const V* p0 = reinterpret_cast<const V*>(g0 + base);
+    const V* p1 = reinterpret_cast<const V*>(g1 + base);
+    const V* p2 = reinterpret_cast<const V*>(g2 + base);
+    V* out = reinterpret_cast<V*>(F + base);
+    for (int64_t v = (int64_t)blockIdx.x * MNT + threadIdx.x; v < nv; v += (int64_t)gridDim.x * MNT) {
+      const V x0 = p0[v];
+      const E* x0e = reinterpret_cast<const E*>(&x0);
+      double acc[W];
+#pragma unroll
+      for (int c = 0; c < W; ++c) acc[c] = a0 * (double)x0e[c];
+      if (d > 1) {
+        const V x1 = p1[v];
+        const E* x1e = reinterpret_cast<const E*>(&x1);
+#pragma unroll
+        for (int c = 0; c < W; ++c) acc[c] += a1 * (double)x1e[c];
+      }
+      if (d > 2) {
+        const V x2 = p2[v];
+        const E* x2e = reinterpret_cast<const E*>(&x2);
+#pragma unroll
+        for (int c = 0; c < W; ++c) acc[c] += a2 * (double)x2e[c];
+      }
+      V r;
+      E* re = reinterpret_cast<E*>(&r);
+#pragma unroll
+      for (int c = 0; c < W; ++c) re[c] = (E)acc[c];
+      out[v] = r;
+    }
+    continue;
+  }
+  for (int64_t e = (int64_t)blockIdx.x * MNT + threadIdx.x; e < per_frame; e += (int64_t)gridDim.x * MNT) {
+    double f = a0 * (double)g0[base + e];
+    if (d > 1) f += a1 * (double)g1[base + e];
+    if (d > 2) f += a2 * (double)g2[base + e];
+    F[base + e] = (E)f;
+  }
   }
 }
 
@@ -217,19 +257,29 @@ cudaError_t launch_mtd_eval(const double* val, const double* dgrid, const double
 
 cudaError_t launch_mtd_force(const double* dV, int T, int d, const void* g0, const void* g1, const void* g2,
                              int dtype, int n, void* F, cudaStream_t stream) {
-  const int64_t per = 3LL * n, total = per * T;
-  if (total <= 0) return cudaSuccess;
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (total + MNT - 1) / MNT;
-  const unsigned grid = (unsigned)(want < (int64_t)nsm * 16 ? want : (int64_t)nsm * 16);
-  if (dtype == 0)
-    mtd_force_kernel<float><<<grid, MNT, 0, stream>>>(dV, d, (const float*)g0, (const float*)g1, (const float*)g2,
-                                                      per, total, (float*)F);
-  else
-    mtd_force_kernel<double><<<grid, MNT, 0, stream>>>(dV, d, (const double*)g0, (const double*)g1,
-                                                       (const double*)g2, per, total, (double*)F);
+  const int64_t per = 3LL * n;
+  if (T <= 0 || per <= 0) return cudaSuccess;
+  const int esz = dtype == 0 ? 4 : 8;
+  auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = (per * esz) % 16 == 0 && al(g0) && al(g1) && al(g2) && al(F);
+  const int64_t units = vec ? per * esz / 16 : per;
+  const unsigned bx = (unsigned)((units + MNT * 4 - 1) / (MNT * 4));  // ~4 vectors per thread per frame
+  const dim3 grid(bx, (unsigned)(T < 65535 ? T : 65535));
+  if (dtype == 0) {
+    if (vec)
+      mtd_force_kernel<float, true><<<grid, MNT, 0, stream>>>(dV, d, (const float*)g0, (const float*)g1,
+                                                              (const float*)g2, per, T, (float*)F);
+    else
+      mtd_force_kernel<float, false><<<grid, MNT, 0, stream>>>(dV, d, (const float*)g0, (const float*)g1,
+                                                               (const float*)g2, per, T, (float*)F);
+  } else {
+    if (vec)
+      mtd_force_kernel<double, true><<<grid, MNT, 0, stream>>>(dV, d, (const double*)g0, (const double*)g1,
+                                                               (const double*)g2, per, T, (double*)F);
+    else
+      mtd_force_kernel<double, false><<<grid, MNT, 0, stream>>>(dV, d, (const double*)g0, (const double*)g1,
+                                                                (const double*)g2, per, T, (double*)F);
+  }
   return cudaGetLastError();
 }
 
