@@ -172,7 +172,9 @@ int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, 
  *   estimate-error allowance of the one-term screen.
  * mc_sort_by_key: counting sort of frames by window start (workspace bins [nbins]).
  * mc_refine: exact fp64 covariance + fit of the in-window pairs (or, with lo = cnt =
- *   NULL, of all pairs: the dense exact MSD matrix into Dd). */
+ *   NULL, of all pairs: the dense exact MSD matrix into Dd).  lwbar [L, 3] (nullable)
+ *   = sum_j w_j (a_lj - c_l) (mc_center_split's wbar of the landmarks): frames then
+ *   enter the fp64 contraction uncentred, S = S_half - c_x lwbar^T. */
 int mc_center_split(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
                     const double* w_disp, int32_t weighted, float* hi, float* lo, double* centroid, double* gnorm,
                     double* wbar, double* mom, uint8_t* flags, void* stream);
@@ -216,7 +218,7 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
                   double fcoef, int32_t cap, int32_t* lo, int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream);
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
-              const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
+              const double* lwbar, const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
               const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
               float* Dd, int64_t ldd, uint8_t* flags, void* stream);
 

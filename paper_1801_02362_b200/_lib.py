@@ -73,7 +73,7 @@ _SIGS = {
     "mc_pathcv_grad_block": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
     "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _I32, _P, _P, _P, _P, _P],
     "mc_sort_by_key": [_P, _I32, _I32, _P, _P, _P],
-    "mc_refine": [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P],
+    "mc_refine": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P],
     "mc_pair_grad": [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],

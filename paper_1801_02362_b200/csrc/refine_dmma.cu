@@ -54,10 +54,16 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 }  // namespace
 
-template <bool VEC>
+// UNC (lwbar given): frames enter the contraction uncentred -- A = x, B = w (a - c_l) --
+// and S = S_half - c_x lwbar^T with lwbar_l = sum_j w_j (a_lj - c_l) (zero in exact
+// arithmetic when the displacement and alignment weights coincide), which saves the
+// per-fragment frame centring (6 DADD and 12 registers per k-step); no cancellation,
+// since S_half - S = c_x lwbar^T is itself ~0.
+template <bool VEC, bool UNC>
 __global__ void __launch_bounds__(QNT, 2)
 refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const float* __restrict__ lr,
-                   const double* __restrict__ lc, const double* __restrict__ w, const double* __restrict__ gx,
+                   const double* __restrict__ lc, const double* __restrict__ lwbar, const double* __restrict__ w,
+                   const double* __restrict__ gx,
                    const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,
                    const int* __restrict__ lo, const int* __restrict__ cnt, int cap, double* __restrict__ Dex,
                    double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
@@ -99,7 +105,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const int mt = wm * 6 + i;
-    fcA[i] = s_fc[(mt & 3) * 8 + gq][mt >> 2];
+    fcA[i] = UNC ? 0.0 : s_fc[(mt & 3) * 8 + gq][mt >> 2];
   }
   const int nch = (n + QKC - 1) / QKC;
   for (int l0 = wlo; l0 < whi; l0 += QL) {
@@ -177,7 +183,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
         const double wj = ww[4 * s];
         double a[6], b[3];
 #pragma unroll
-        for (int i = 0; i < 6; ++i) a[i] = (double)sg[offA[i] + 12 * s] - fcA[i];
+        for (int i = 0; i < 6; ++i) a[i] = UNC ? (double)sg[offA[i] + 12 * s] : (double)sg[offA[i] + 12 * s] - fcA[i];
 #pragma unroll
         for (int i = 0; i < 3; ++i) b[i] = wj * ((double)sg[offB[i] + 12 * s] - lcB[i]);
 #pragma unroll
@@ -211,7 +217,10 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 #pragma unroll
       for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int g = 0; g < 3; ++g) S[b * 3 + g] = sC[(b * QF + f) * QCS + g * QL + li];
+        for (int g = 0; g < 3; ++g) {
+          S[b * 3 + g] = sC[(b * QF + f) * QCS + g * QL + li];
+          if (UNC) S[b * 3 + g] -= s_fc[f][b] * lwbar[3 * l + g];
+        }
       double q[4];
       bool ill = false;
       double msd = fit_fast(S, gx[t], ga[l], Rex ? q : nullptr, &ill);
@@ -238,26 +247,31 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
   }
 }
 
-cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc, const double* w,
-                               const double* gx, const double* ga, int T, int L, int n, const int* perm, const int* lo,
-                               const int* cnt, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,
-                               uint8_t* flags, cudaStream_t stream) {
+cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
+                               const double* lwbar, const double* w, const double* gx, const double* ga, int T, int L,
+                               int n, const int* perm, const int* lo, const int* cnt, int cap, double* Dex,
+                               double* Rex, float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream) {
   if (T <= 0 || L <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(refine_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(refine_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
-    if (e != cudaSuccess) return e;
+    for (const void* fn : {(const void*)refine_dmma_kernel<true, true>, (const void*)refine_dmma_kernel<false, true>,
+                           (const void*)refine_dmma_kernel<true, false>, (const void*)refine_dmma_kernel<false, false>}) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(fr) & 15) == 0 && (reinterpret_cast<uintptr_t>(lr) & 15) == 0;
-  if (vec)
-    refine_dmma_kernel<true><<<(T + QF - 1) / QF, QNT, QSMEM, stream>>>(fr, fc, lr, lc, w, gx, ga, T, L, n, perm, lo,
-                                                                       cnt, cap, Dex, Rex, Dd, ldd, flags);
-  else
-    refine_dmma_kernel<false><<<(T + QF - 1) / QF, QNT, QSMEM, stream>>>(fr, fc, lr, lc, w, gx, ga, T, L, n, perm, lo,
-                                                                        cnt, cap, Dex, Rex, Dd, ldd, flags);
+  const dim3 grid((T + QF - 1) / QF);
+#define MC_RD_LAUNCH(V, U)                                                                                          \
+  refine_dmma_kernel<V, U><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, ga, T, L, n, perm, lo, cnt, \
+                                                         cap, Dex, Rex, Dd, ldd, flags)
+  if (lwbar) {
+    if (vec) MC_RD_LAUNCH(true, true); else MC_RD_LAUNCH(false, true);
+  } else {
+    if (vec) MC_RD_LAUNCH(true, false); else MC_RD_LAUNCH(false, false);
+  }
+#undef MC_RD_LAUNCH
   return cudaGetLastError();
 }
 

@@ -102,6 +102,13 @@ __device__ __forceinline__ void msd8_estimate(const float (&v)[9][8], double gx,
                           sf[0] - sf[4] - sf[8],  sf[1] + sf[3],  sf[2] + sf[6],  -sf[0] + sf[4] - sf[8],
                           sf[5] + sf[7],          -sf[0] - sf[4] + sf[8]};
     float qf[4];
+#ifdef MC_DIAG_EPI_KABSCH_ONLY
+    // diagnostic build only: the fp32 Kabsch value as the estimate (timing)
+    { out[i] = ok ? (float)(gx + ga[l] - 2.0 * (double)lmax_kabsch_f32(sf)) : 0.0f; continue; }
+#endif
+#ifdef MC_DIAG_EPI_NONE
+    { out[i] = ok ? (float)(gx + ga[l] - 2.0 * (double)(nf[0] + nf[4])) : 0.0f; continue; }
+#endif
     adj_eigvec_f32(nf, lmax_kabsch_f32(sf), qf);
     // fp64 Rayleigh quotient with N(S) in fp64
     double S[9];

@@ -290,7 +290,8 @@ def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, c
     Dex = torch.empty((T, cap), dtype=F64, device=dev) if cap else None
     Rex = torch.empty((T, cap, 9), dtype=F64, device=dev) if (cap and want_rot) else None
     flags = torch.zeros((T,), dtype=U8, device=dev)
-    call("mc_refine", ptr(frames), ptr(fsplit.centroid), ptr(landmarks), ptr(lsplit.centroid), ptr(w), ptr(fsplit.g),
+    call("mc_refine", ptr(frames), ptr(fsplit.centroid), ptr(landmarks), ptr(lsplit.centroid), ptr(lsplit.wbar),
+         ptr(w), ptr(fsplit.g),
          ptr(lsplit.g), T, L, n, ptr(perm), ptr(lo), ptr(cnt), cap, ptr(Dex), ptr(Rex), ptr(Dd),
          Dd.stride(0) if Dd is not None else 0, ptr(flags), stream_ptr())
     return Dex, Rex, flags
