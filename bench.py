@@ -383,11 +383,22 @@ class ConfigTC:
             return "tensor_flop", 3.0 * 18.0 * n * T * L
         if name in ("mc_msd_f16", "mc_msd_f16_2sm"):
             terms = self.pcv.screen_terms if self.cfg == 4 else 3
-            return "tensor_flop_f16", terms * 18.0 * n * T * L
+            pairs = T * L
+            if self.cfg == 4 and self.last is not None and "screen_tiles" in self.last:
+                tiles = int(self.last["screen_tiles"].item())
+                pairs = T * self.pcv.coarse.numel() + tiles * 128 * 48  # coarse + banded
+            return "tensor_flop_f16", terms * 18.0 * n * pairs
+        if name == "mc_pathcv_grad_block" and self.last is not None:
+            # useful fp64 work: 18 FMA (U^s, U^z: 2 CVs x 3 x 3) per significant pair and atom
+            return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_center_split16":
             return "bytes", T * n * 3 * 4 + 2 * T * 3 * (((n + 31) // 32) * 32) * 2
         if name == "mc_refine":
-            return "fp64_flop", 18.0 * n * T * L if self.cfg == 2 else 0.0
+            if self.cfg == 2:
+                return "fp64_tensor_flop", 18.0 * n * T * L
+            if self.last is not None:  # exact refits of the window pairs: 9 FMA per pair and atom
+                return "fp64_tensor_flop", 18.0 * n * float(self.last["window_cnt"].double().sum().item())
+            return "fp64_tensor_flop", 0.0
         if name == "mc_center_split":
             return "bytes", T * n * 3 * 4 + 2 * T * 3 * (((n + 15) // 16) * 16) * 4
         if name == "mc_pathcv_grad":
@@ -401,7 +412,15 @@ class ConfigTC:
         if self.cfg == 4 and self.last is not None:
             d["mean_window"] = float(self.last["window_cnt"].float().mean().item())
             d["mean_significant"] = float(self.last["nsig"].float().mean().item())
+            if "screen_tiles" in self.last:
+                ntl = (self.L + 47) // 48
+                full = ((self.T + 127) // 128) * ntl
+                d["screen_tiles_computed_frac"] = int(self.last["screen_tiles"].item()) / full
+                d["screen"] = "one-term FP16, metric-pruned (coarse stride %d)" % (self.L // self.pcv.coarse.numel())
         return d
+
+
+DMMA_PEAK_TF = 36.8  # measured mma.sync f64 rate on this pool's B200 (tools/_diag/dmma_probe.cu)
 
 
 def measured_traffic(kernel, cfg, T):
@@ -505,14 +524,15 @@ def run_ours(args, rank, world, local_rank):
     total = sum(t for _, t in prof.values()) or 1.0
     name, (cnt, tms) = max(prof.items(), key=lambda kv: kv[1][1])
     avg_ms = tms / cnt
+    step_ms = tms / nprof  # the kernel's time per step (all its launches)
     kind, amount = runner.kernel_work(name)
     tf32_cublas = tf32_peak_measure(device) if kind == "tensor_flop" and rank == 0 else None
     if kind == "bytes":
-        ach = amount / (avg_ms * 1e-3) / 1e9
+        ach = amount / (step_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm"], "unit": "GB/s", "frac": ach / pk["hbm"],
                 "peak_src": pk["src"]}
     elif kind == "tensor_flop":
-        ach = amount / (avg_ms * 1e-3) / 1e12
+        ach = amount / (step_ms * 1e-3) / 1e12
         # the kernel runs for ~1 s inside a multi-second step: the sustained
         # (power-capped) figure is the right denominator; burst reported beside it
         sustained = pk.get("bf16_sustained") or pk["bf16"]
@@ -523,7 +543,7 @@ def run_ours(args, rank, world, local_rank):
                 "peak_burst": pk["bf16"] / 2.0, "frac_of_burst": ach / (pk["bf16"] / 2.0),
                 "cublas_tf32_measured": tf32_cublas, "flop_basis": "executed 3xTF32 (3 x 18 n per pair)"}
     elif kind == "tensor_flop_f16":
-        ach = amount / (avg_ms * 1e-3) / 1e12
+        ach = amount / (step_ms * 1e-3) / 1e12
         sustained = pk.get("bf16_sustained") or pk["bf16"]
         roof = {"bound": "tensor", "achieved": ach, "peak": sustained, "unit": "TFLOP/s", "frac": ach / sustained,
                 "peak_src": f"bf16_tflops_sustained from {pk['src']} (kind::f16 runs at the bf16 rate; "
@@ -531,8 +551,14 @@ def run_ours(args, rank, world, local_rank):
                 "peak_burst": pk["bf16"], "frac_of_burst": ach / pk["bf16"],
                 "flop_basis": "executed FP16 MMAs: terms x 18 n per pair (config 4 screen: one-term hi x hi; "
                               "split-precision estimate: 3 terms)"}
+    elif kind == "fp64_tensor_flop":
+        ach = amount / (step_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TF, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TF,
+                "peak_src": "fp64 tensor cores (DMMA.8x8x4) measured on this pool's B200: 36.8 TF/s "
+                            "(tools/_diag/dmma_probe.cu; MEASURED_PEAKS.json has no fp64 figure)",
+                "flop_basis": "useful fp64 flops (significant / window pairs); executed includes window-union padding"}
     else:
-        ach = amount / (avg_ms * 1e-3) / 1e12
+        ach = amount / (step_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,
                 "peak_src": "nominal B200 FP64 37 TF/s (not measured)"}
     traffic = measured_traffic(name, cfg, runner.T)

@@ -186,7 +186,7 @@ int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const floa
 int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const float* lraw,
                          const double* lcen, const double* w, const double* w_align, const int32_t* sig_idx,
                          const double* sig_coef, const int32_t* nsig, const double* fvec, const int32_t* perm,
-                         void* ds, void* dz, int32_t out_f32, void* stream);
+                         const int32_t* out_map, void* ds, void* dz, int32_t out_f32, void* stream);
 /* mc_msd_tf32 on CTA pairs (tcgen05.mma.cta_group::2, M = 256 frames per pair):
  * same inputs/outputs; each SM stages half of the landmark operand. */
 int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const float* llo, const double* gx,
@@ -209,13 +209,33 @@ int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, i
                       double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
                       void* stream);
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
-               const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, float* D, int64_t ldd,
-               int32_t grid, void* stream);
+               const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const int32_t* tlist,
+               const int32_t* nlist, float* D, int64_t ldd, int32_t grid, void* stream);
 int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
                    const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                    void* stream);
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
-                  double fcoef, int32_t cap, int32_t* lo, int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
+                  double fcoef, const int32_t* rlo, const int32_t* rhi, int32_t cap, int32_t* lo, int32_t* cnt,
+                  float* dmin, uint8_t* flags, void* stream);
+/* Metric pruning of the screen (csrc/prune.cu):
+ * mc_prune_plan: from the one-term estimate Dc [T, C] against a coarse landmark subset,
+ *   its error bound c_unit * fnorm[t] * cnorm[c], and mind [C, ntl] = min over each
+ *   48-landmark tile of the exact RMSD coarse->landmark, the hull [hull_lo, hull_hi) of
+ *   landmark tiles that can hold a landmark within cutoff of D_min (thr = cutoff / lam,
+ *   D units; knear <= 8 nearest coarse landmarks; C <= 1024) and a sort key (0: hull
+ *   >= `wide` tiles, else 1 + hull_lo).
+ * mc_band_tiles: for the key-sorted order perm, the union hull of each 128-frame band,
+ *   the (band, landmark tile) list tlist [*, 2] with its length *nlist (device), and each
+ *   sorted row's landmark range [row_lo, row_hi) for mc_candidates(rlo, rhi).
+ * mc_gather_rows: dst[r] = src[idx[r]] for rows of rowlen elements of esz bytes. */
+int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
+                  double c_unit, const float* mind, int32_t ntl, double thr, int32_t knear, int32_t wide,
+                  int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream);
+int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,
+                  int32_t BL, int32_t L, int32_t* tlist, int32_t* nlist, int32_t* row_lo, int32_t* row_hi,
+                  void* stream);
+int mc_gather_rows(const void* src, int32_t esz, int64_t rowlen, const int32_t* idx, int32_t rows, void* dst,
+                   void* stream);
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream);
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
               const double* lwbar, const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,

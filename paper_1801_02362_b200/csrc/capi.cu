@@ -170,7 +170,7 @@ int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const 
 int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const float* lraw,
                          const double* lcen, const double* w, const double* w_align, const int32_t* sig_idx,
                          const double* sig_coef, const int32_t* nsig, const double* fvec, const int32_t* perm,
-                         void* ds, void* dz, int32_t out_f32, void* stream) {
+                         const int32_t* out_map, void* ds, void* dz, int32_t out_f32, void* stream) {
   if (T < 0 || n < 2 || cap < 1) return MC_ERR_CONFIG;
   if (T > 0 && (!fraw || !fcen || !lraw || !lcen || !w || !w_align || !sig_idx || !sig_coef || !nsig || !fvec ||
                 !ds || !dz))
@@ -181,20 +181,51 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
     const char* e = getenv("MC_GRAD_VECTOR");
     return e && e[0] == '1';
   }();
-  if (vec)
+  if (vec) {
+    if (out_map) return MC_ERR_CONFIG;  // the CUDA-core comparison kernel writes rows in place
     return cuda_status(mc::launch_cv_grad_block(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, sig_idx, sig_coef,
                                                 nsig, fvec, perm, ds, dz, out_f32, S_(stream)));
+  }
   return cuda_status(mc::launch_cv_grad_dmma(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, sig_idx, sig_coef, nsig,
-                                             fvec, perm, ds, dz, out_f32, S_(stream)));
+                                             fvec, perm, out_map, ds, dz, out_f32, S_(stream)));
 }
 
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
-                  double fcoef, int32_t cap, int32_t* lo, int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
+                  double fcoef, const int32_t* rlo, const int32_t* rhi, int32_t cap, int32_t* lo, int32_t* cnt,
+                  float* dmin, uint8_t* flags, void* stream) {
   if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0) || !(fcoef >= 0.0))
     return MC_ERR_CONFIG;
   if (T > 0 && (!D || !lo || !cnt)) return MC_ERR_CONFIG;
+  if ((rlo == nullptr) != (rhi == nullptr)) return MC_ERR_CONFIG;
   return cuda_status(
-      mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, cap, lo, cnt, dmin, flags, S_(stream)));
+      mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, cap, lo, cnt, dmin, flags, S_(stream)));
+}
+
+int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
+                  double c_unit, const float* mind, int32_t ntl, double thr, int32_t knear, int32_t wide,
+                  int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream) {
+  if (T < 0 || C < 1 || C > 1024 || lddc < C || ntl < 1 || knear < 1 || knear > 8 || !(c_unit >= 0.0) ||
+      !(thr >= 0.0))
+    return MC_ERR_CONFIG;
+  if (T > 0 && (!Dc || !fnorm || !cnorm || !mind || !hull_lo || !hull_hi || !key)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, c_unit, mind, ntl, thr, knear, wide, hull_lo,
+                                           hull_hi, key, S_(stream)));
+}
+
+int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,
+                  int32_t BL, int32_t L, int32_t* tlist, int32_t* nlist, int32_t* row_lo, int32_t* row_hi,
+                  void* stream) {
+  if (T < 0 || BM < 1 || BL < 1 || L < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!perm || !hull_lo || !hull_hi || !tlist || !nlist || !row_lo || !row_hi)) return MC_ERR_CONFIG;
+  return cuda_status(
+      mc::launch_band_tiles(perm, T, hull_lo, hull_hi, BM, BL, L, tlist, nlist, row_lo, row_hi, S_(stream)));
+}
+
+int mc_gather_rows(const void* src, int32_t esz, int64_t rowlen, const int32_t* idx, int32_t rows, void* dst,
+                   void* stream) {
+  if ((esz != 4 && esz != 8) || rowlen < 0 || rows < 0) return MC_ERR_CONFIG;
+  if (rows > 0 && rowlen > 0 && (!src || !idx || !dst)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_gather_rows(src, esz, rowlen, idx, rows, dst, S_(stream)));
 }
 
 int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, int32_t* perm, void* stream) {
@@ -288,12 +319,13 @@ static int msd_f16_args(const void* fhl, const void* lhl, const double* fsc, con
 }
 
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
-               const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, float* D, int64_t ldd,
-               int32_t grid, void* stream) {
+               const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const int32_t* tlist,
+               const int32_t* nlist, float* D, int64_t ldd, int32_t grid, void* stream) {
   const int st = msd_f16_args(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, terms, D, ldd);
   if (st != MC_OK) return st;
-  return cuda_status(
-      mc::launch_msd_f16(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, terms, D, ldd, grid, S_(stream)));
+  if ((tlist == nullptr) != (nlist == nullptr)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_msd_f16(fhl, lhl, fscale, lscale, gx, ga, T, L, kpad, terms, D, ldd, grid, S_(stream),
+                                        tlist, nlist));
 }
 
 int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,

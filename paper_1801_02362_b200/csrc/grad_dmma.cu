@@ -65,8 +65,8 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
                     const float* __restrict__ lraw, const double* __restrict__ lcen, const double* __restrict__ w,
                     const double* __restrict__ wa, const int* __restrict__ sig_idx,
                     const double* __restrict__ sig_coef, const int* __restrict__ nsig,
-                    const double* __restrict__ fvec, const int* __restrict__ perm, OT* __restrict__ ds,
-                    OT* __restrict__ dz) {
+                    const double* __restrict__ fvec, const int* __restrict__ perm, const int* __restrict__ out_map,
+                    OT* __restrict__ ds, OT* __restrict__ dz) {
   extern __shared__ __align__(16) double dsm[];
   double* sA = dsm;                                       // [DR][AST] coefficients
   double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
@@ -244,6 +244,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       if (t < 0) continue;
       const double cx = s_fc[f][b], sc = s_fv[f][sz], corr = s_fv[f][2 + sz * 3 + b];
       OT* __restrict__ out = sz ? dz : ds;
+      const int tout = out_map ? out_map[t] : t;
       const float* xs = sX + f * 3 * DNA + b;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -253,7 +254,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
           const int k = a0 + al;
           if (k >= n) continue;
           const double x = (double)xs[3 * al] - cx;
-          out[((int64_t)t * n + k) * 3 + b] = (OT)(2.0 * wk[j][e] * (sc * x - c[m][j][e]) - wak[j][e] * corr);
+          out[((int64_t)tout * n + k) * 3 + b] = (OT)(2.0 * wk[j][e] * (sc * x - c[m][j][e]) - wak[j][e] * corr);
         }
     }
     __syncthreads();  // sX is refilled by the next sub-tile
@@ -263,7 +264,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
 cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                 const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
-                                void* ds, void* dz, int out_f32, cudaStream_t stream) {
+                                const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   dim3 grid((T + DG - 1) / DG, (n + DATOMS - 1) / DATOMS);
   static bool attr = false;
@@ -279,7 +280,8 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
                    (reinterpret_cast<uintptr_t>(lraw) & 15) == 0;
 #define MC_GD_LAUNCH(OTT, V)                                                                                         \
   cv_grad_dmma_kernel<OTT, V><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,     \
-                                                            sig_coef, nsig, fvec, perm, (OTT*)ds, (OTT*)dz)
+                                                            sig_coef, nsig, fvec, perm, out_map, (OTT*)ds,     \
+                                                            (OTT*)dz)
   if (out_f32) {
     if (vec) MC_GD_LAUNCH(float, true); else MC_GD_LAUNCH(float, false);
   } else {

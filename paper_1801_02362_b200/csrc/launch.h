@@ -61,7 +61,7 @@ cudaError_t launch_msd_tf32_2sm(const float* fh, const float* fl, const float* l
 cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                 const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
-                                void* ds, void* dz, int out_f32, cudaStream_t stream);
+                                const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                  const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                  const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
@@ -72,7 +72,7 @@ cudaError_t launch_cv_grad_block_planes(int T, int t0, int n, int npad, int cap,
                                         const uint8_t* refresh, const int* ridx, const double* xyeig, void* ds,
                                         void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
-                              double fcoef, int cap, int* lo,
+                              double fcoef, const int* rlo, const int* rhi, int cap, int* lo,
                               int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
@@ -102,7 +102,14 @@ cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int 
                                   uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
                            const double* ga, int T, int L, int kpad, int terms, float* D, int64_t ldd, int grid,
-                           cudaStream_t stream);
+                           cudaStream_t stream, const int* tlist = nullptr, const int* nlist = nullptr);
+cudaError_t launch_prune_plan(const float* Dc, int T, int C, int64_t lddc, const double* fnorm, const double* cnorm,
+                              double c_unit, const float* mind, int ntl, double thr, int knear, int wide,
+                              int* hull_lo, int* hull_hi, int* key, cudaStream_t stream);
+cudaError_t launch_band_tiles(const int* perm, int T, const int* hull_lo, const int* hull_hi, int BM, int BL, int L,
+                              int* tlist, int* nlist, int* row_lo, int* row_hi, cudaStream_t stream);
+cudaError_t launch_gather_rows(const void* src, int esz, int64_t rowlen, const int* idx, int rows, void* dst,
+                               cudaStream_t stream);
 cudaError_t launch_msd_f16_2sm(const void* fhl, const void* lhl, const double* fsc, const double* lsc,
                                const double* gx, const double* ga, int T, int L, int kpad, float* D, int64_t ldd,
                                int grid, cudaStream_t stream);

@@ -25,18 +25,21 @@ constexpr int CNT = 256;
 
 __global__ void __launch_bounds__(CNT)
 cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, double thr0,
-            const double* __restrict__ fnorm, double fcoef, int cap, int* __restrict__ lo, int* __restrict__ cnt,
-            float* __restrict__ dmin_out, uint8_t* __restrict__ flags) {
+            const double* __restrict__ fnorm, double fcoef, const int* __restrict__ rlo, const int* __restrict__ rhi,
+            int cap, int* __restrict__ lo, int* __restrict__ cnt, float* __restrict__ dmin_out,
+            uint8_t* __restrict__ flags) {
   __shared__ double scratch[CNT / 32];
   __shared__ int imin[CNT / 32], imax[CNT / 32];
   const int t = blockIdx.x;
   const double thr = fnorm ? thr0 + fcoef * fnorm[t] : thr0;
   const float* row = D + (int64_t)t * ldd;
+  // scan range: the whole row, or the banded range the pruned screen computed
+  const int i0 = rlo ? rlo[t] : 0, i1 = rhi ? rhi[t] : L;
   double m = INFINITY;
-  for (int i = threadIdx.x; i < L; i += CNT) m = fmin(m, (double)row[i]);
+  for (int i = i0 + threadIdx.x; i < i1; i += CNT) m = fmin(m, (double)row[i]);
   m = block_min<CNT>(m, scratch);
   int a = L, b = -1;
-  for (int i = threadIdx.x; i < L; i += CNT) {
+  for (int i = i0 + threadIdx.x; i < i1; i += CNT) {
     if (lam * ((double)row[i] - m) <= thr) { a = min(a, i); b = max(b, i); }
   }
 #pragma unroll
@@ -62,10 +65,10 @@ cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, 
 }
 
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
-                              double fcoef, int cap, int* lo, int* cnt, float* dmin, uint8_t* flags,
-                              cudaStream_t stream) {
+                              double fcoef, const int* rlo, const int* rhi, int cap, int* lo, int* cnt, float* dmin,
+                              uint8_t* flags, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  cand_kernel<<<T, CNT, 0, stream>>>(D, T, L, ldd, lam, thr, fnorm, fcoef, cap, lo, cnt, dmin, flags);
+  cand_kernel<<<T, CNT, 0, stream>>>(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, cap, lo, cnt, dmin, flags);
   return cudaGetLastError();
 }
 

@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(gemm::NT, 1)
 msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__ CUtensorMap mfl,
                 const __grid_constant__ CUtensorMap mlh, const __grid_constant__ CUtensorMap mll,
                 const double* __restrict__ gx, const double* __restrict__ ga, const double* __restrict__ fsc,
-                const double* __restrict__ lsc, int T, int L, int kpad, float* __restrict__ D, int64_t ldd) {
+                const double* __restrict__ lsc, int T, int L, int kpad, float* __restrict__ D, int64_t ldd,
+                const int* __restrict__ tlist, const int* __restrict__ nlist) {
   using namespace gemm;
   constexpr int KB = Fmt<F16>::KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -358,7 +359,11 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntm = (T + BM - 1) / BM, ntl = (L + BL - 1) / BL;
-  const int ntiles = ntm * ntl;
+  // tile list (pruned / banded work, pairs (tm, tl)) or the full grouped raster
+  const int ntiles = tlist ? *nlist : ntm * ntl;
+  auto coords = [&](int tile, int& tm, int& tl) {
+    if (tlist) { tm = tlist[2 * tile]; tl = tlist[2 * tile + 1]; } else { tile_coords(tile, ntm, ntl, tm, tl); }
+  };
   // ONE (one-term F16 screen): 64 hi atoms per 128 B row and stage
   const int nkb = ONE ? kpad / 64 : kpad / KB;
 
@@ -391,7 +396,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int tm, tl;
-        tile_coords(tile, ntm, ntl, tm, tl);
+        coords(tile, tm, tl);
         const int t0 = tm * BM, l0 = tl * BL;
         for (int kb = 0; kb < nkb; ++kb) {
 #ifdef MC_DIAG_TRACE
@@ -542,7 +547,7 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       int tm, tl;
-      tile_coords(tile, ntm, ntl, tm, tl);
+      coords(tile, tm, tl);
       const int t = tm * BM + row;
       const int l0 = tl * BL;
       mbar_wait(tfull, it & 1);
@@ -637,7 +642,8 @@ bool make_operand_map(CUtensorMap* m, const void* base, int esz, int64_t rows, i
 template <bool F16, bool ONE = false>
 static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, const void* ll, const double* gx,
                                 const double* ga, const double* fsc, const double* lsc, int T, int L, int kpad,
-                                float* D, int64_t ldd, int grid, cudaStream_t stream) {
+                                float* D, int64_t ldd, int grid, cudaStream_t stream, const int* tlist = nullptr,
+                                const int* nlist = nullptr) {
   using namespace gemm;
   if (T <= 0 || L <= 0) return cudaSuccess;
   if (kpad % (ONE ? 64 : Fmt<F16>::KB)) return cudaErrorInvalidValue;
@@ -663,12 +669,14 @@ static cudaError_t launch_gemm1(const void* fh, const void* fl, const void* lh, 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int ntiles = ((T + BM - 1) / BM) * ((L + BL - 1) / BL);
+  // with a device-side tile list the count is only known on the device: one CTA per SM
+  const int ntiles = tlist ? 1 << 30 : ((T + BM - 1) / BM) * ((L + BL - 1) / BL);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int g = grid > 0 ? grid : (ntiles < nsm ? ntiles : nsm);
-  msd_tf32_kernel<F16, ONE><<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, fsc, lsc, T, L, kpad, D, ldd);
+  msd_tf32_kernel<F16, ONE><<<g, NT, SMEM_BYTES, stream>>>(mfh, mfl, mlh, mll, gx, ga, fsc, lsc, T, L, kpad, D, ldd,
+                                                           tlist, nlist);
   return cudaGetLastError();
 }
 
@@ -680,10 +688,12 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
 
 cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
                            const double* ga, int T, int L, int kpad, int terms, float* D, int64_t ldd, int grid,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const int* tlist, const int* nlist) {
   if (terms == 1)
-    return launch_gemm1<true, true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
-  return launch_gemm1<true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream);
+    return launch_gemm1<true, true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream,
+                                    tlist, nlist);
+  return launch_gemm1<true>(fhl, nullptr, lhl, nullptr, gx, ga, fsc, lsc, T, L, kpad, D, ldd, grid, stream, tlist,
+                            nlist);
 }
 
 }  // namespace mc

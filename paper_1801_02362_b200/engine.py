@@ -26,6 +26,8 @@ from .errors import ConfigError, DegenerateFitError, EmptyActiveSetError, Invali
 DEFAULT_CUTOFF = 25.0
 # window-selection estimate of PathCVTC.evaluate (env MC_SCREEN: "f16x1" | "split")
 SCREEN = __import__("os").environ.get("MC_SCREEN", "f16x1")
+# metric pruning of the one-term screen (env MC_PRUNE=0 disables)
+PRUNE = __import__("os").environ.get("MC_PRUNE", "1") == "1"
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 
 
@@ -271,7 +273,7 @@ class PathCVTC:
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None, screen=None):
+                 operand_fmt=None, screen=None, prune=None, coarse_stride=16, knear=4):
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
         self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
@@ -318,7 +320,32 @@ class PathCVTC:
             c_unit = 4.0 * (2 * u + u * u + self.n * 2.0 ** -27) * 1.25 + 1e-6
             self.na_max = float(self.ls.opnorm.max().item())
             self.fcoef = 2.0 * self.lam * c_unit * self.na_max
+            self.c_unit = c_unit
             self.margin = 2.0
+        # metric pruning of the screen: one-term screen only,
+        # worthwhile when there are many landmark tiles
+        ntl = (self.L + 47) // 48
+        self.prune = (PRUNE if prune is None else bool(prune)) and self.screen == "f16x1" and ntl >= 16
+        if self.prune:
+            self._init_prune(int(coarse_stride), int(knear))
+
+    def _init_prune(self, stride, knear):
+        """Coarse landmark subset (every `stride`-th, <= 1024), its one-term split, and
+        mind [C, ntl] = a lower bound of min over each 48-landmark tile of the exact
+        RMSD coarse -> landmark (exact fp64 refits, stored fp32, shrunk by 1e-6)."""
+        stride = max(stride, (self.L + 1023) // 1024)
+        self.coarse = torch.arange(0, self.L, stride, device=self.device)
+        lc = self.lraw[self.coarse].contiguous()
+        self.ls_coarse = K.center_split(lc, self.wa, self.w, weighted=True, moments=False, fmt=self.fmt, terms=1)
+        dcl = torch.empty((lc.shape[0], self.L), dtype=torch.float32, device=self.device)
+        fsc = K.center_split(lc, self.wa, self.w, weighted=False, fmt=self.fmt)
+        _, _, flags = K.refine(lc, fsc, self.lraw, self.ls, self.w, Dd=dcl)
+        _raise_flags(flags, "metric pruning: landmark distances")
+        ntl = (self.L + 47) // 48
+        rm = dcl.double().clamp_min(0.0).mul_(1.0 - 1e-6).sqrt_()
+        rm = torch.nn.functional.pad(rm, (0, ntl * 48 - self.L), value=float("inf"))
+        self.mind = rm.view(rm.shape[0], ntl, 48).amin(2).float().contiguous()
+        self.knear = max(1, min(8, knear))
 
     def _lsplit(self, terms):
         """Landmark operand split for `terms` (cached; the scalar fields agree)."""
@@ -352,15 +379,39 @@ class PathCVTC:
         _raise_flags(flags, "msd_matrix")
         return D
 
+    def _pruned_estimate(self, frames):
+        """Metric-pruned one-term screen: coarse screen -> per-frame admissible tile hulls
+        -> frames sorted by hull (perm0) -> banded tensor-core estimate of the sorted
+        frames.  Returns the sorted raw frames / split, the estimate, the row ranges
+        and perm0 (sorted position -> original frame)."""
+        fr0, fs0 = self._frames(frames, 1, check=False)
+        Dc = K.msd_estimate(fs0, self.ls_coarse)
+        hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.c_unit, self.mind,
+                                     (self.cutoff + 2.0) / self.lam, self.knear)
+        ntl = self.mind.shape[1]
+        perm0 = K.sort_by_key(key, ntl + 1)
+        frs = K.gather_rows(fr0, perm0)
+        _, fss = self._frames(frs, 1, check=False)
+        tlist, nlist, rlo, rhi = K.band_tiles(perm0, hlo, hhi, 128, 48, self.L, ntl)
+        Dest = torch.empty((frs.shape[0], self.L), dtype=torch.float32, device=self.device)
+        K.msd_estimate(fss, self.ls, Dest, tlist=tlist, nlist=nlist)
+        self._last_tiles = nlist
+        return Dest, frs, fss, fs0, rlo, rhi, perm0
+
     def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False):
-        Dest, fr, fs = self.estimate(frames, self.screen_terms, check=False)
+        rlo = rhi = perm0 = fs0 = None
+        if self.prune:
+            Dest, fr, fs, fs0, rlo, rhi, perm0 = self._pruned_estimate(frames)
+        else:
+            Dest, fr, fs = self.estimate(frames, self.screen_terms, check=False)
         one = self.screen == "f16x1"
         cap = self.window_cap
         while True:
             # the whole pipeline is enqueued without host round trips; the status
             # flags of every stage are reduced on the device and read once at the end
             lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
-                                              fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0)
+                                              fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0,
+                                              rlo=rlo, rhi=rhi)
             perm = K.sort_by_key(lo, self.L)
             Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap)
             wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
@@ -369,8 +420,9 @@ class PathCVTC:
                    "nsig": wres["nsig"]}
             if grad:
                 out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap,
-                                                           perm, out_dtype)
-            status = torch.stack([_flag_bits_dev(fs.flags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
+                                                           perm, out_dtype, out_map=perm0)
+            fflags = fs.flags if fs0 is None else torch.cat([fs.flags, fs0.flags])
+            status = torch.stack([_flag_bits_dev(fflags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
                                   _flag_bits_dev(wres["flags"])])
             ff, cf, rf, wf = (_bits_value(r) for r in status.cpu().tolist())
             if ff & FLAG_NON_FINITE:
@@ -385,8 +437,22 @@ class PathCVTC:
             raise MetadynError("path_cv refine: Jacobi diagonalisation did not converge")
         if wf & FLAG_NON_FINITE:
             raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        if perm0 is not None:
+            out["screen_tiles"] = self._last_tiles  # (band, landmark tile) pairs the pruned screen computed
+            # per-frame outputs back to the caller's frame order (the gradients were
+            # written in place through out_map); the windows refer to the same rows
+            p = perm0.long()
+            for key_ in ("s", "z", "window_lo", "window_cnt", "D_window", "nsig"):
+                v = out[key_]
+                back = torch.empty_like(v)
+                back[p] = v
+                out[key_] = back
+            if return_estimate:
+                back = torch.empty_like(Dest)
+                back[p] = Dest
+                Dest = back
         if return_estimate:
-            out["D_est"] = Dest
+            out["D_est"] = Dest  # pruned: entries outside each band are not computed
         return out
 
 

@@ -247,19 +247,59 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
     return ds, dz
 
 
-def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32):
-    """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames."""
+def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32,
+                      out_map=None):
+    """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames.
+    out_map (optional, int32 [T]): output row of frame t (gradients written in place)."""
     T, n = frames.shape[0], frames.shape[1]
     dev = frames.device
     ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
     dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
     call("mc_pathcv_grad_block", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(perm),
-         ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0, stream_ptr())
+         ptr(out_map), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0, stream_ptr())
     return ds, dz
 
 
-def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0):
+def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None):
+    """Per-frame admissible landmark-tile hulls of the metric-pruned screen (csrc/prune.cu)."""
+    T, C = Dc.shape
+    ntl = mind.shape[1]
+    dev = Dc.device
+    hlo = torch.empty((T,), dtype=I32, device=dev)
+    hhi = torch.empty((T,), dtype=I32, device=dev)
+    key = torch.empty((T,), dtype=I32, device=dev)
+    wide = max(1, (3 * ntl) // 4) if wide is None else int(wide)
+    call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), float(c_unit), ptr(mind), ntl,
+         float(thr), int(knear), wide, ptr(hlo), ptr(hhi), ptr(key), stream_ptr())
+    return hlo, hhi, key
+
+
+def band_tiles(perm, hull_lo, hull_hi, BM, BL, L, ntl):
+    """(band, landmark tile) work list of the pruned screen + per-row landmark ranges."""
+    T = perm.numel()
+    dev = perm.device
+    ntm = (T + BM - 1) // BM
+    tlist = torch.empty((ntm * ntl, 2), dtype=I32, device=dev)
+    nlist = torch.empty((1,), dtype=I32, device=dev)
+    rlo = torch.empty((T,), dtype=I32, device=dev)
+    rhi = torch.empty((T,), dtype=I32, device=dev)
+    call("mc_band_tiles", ptr(perm), T, ptr(hull_lo), ptr(hull_hi), BM, BL, L, ptr(tlist), ptr(nlist), ptr(rlo),
+         ptr(rhi), stream_ptr())
+    return tlist, nlist, rlo, rhi
+
+
+def gather_rows(src, idx):
+    """dst[r] = src[idx[r]] for a contiguous [rows, ...] fp32/fp64 tensor."""
+    src = src.contiguous()
+    rows = idx.numel()
+    dst = torch.empty((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    rowlen = int(src[0].numel()) if src.shape[0] else 0
+    call("mc_gather_rows", ptr(src), src.element_size(), rowlen, ptr(idx), rows, ptr(dst), stream_ptr())
+    return dst
+
+
+def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0, rlo=None, rhi=None):
     """Per-frame D_min and the window of landmarks with lam (D - D_min) <= thr_t,
     thr_t = thr + fcoef * fnorm[t] (fnorm: optional per-frame fp64 tensor)."""
     T = D.shape[0]
@@ -269,8 +309,8 @@ def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0):
     cnt = torch.empty((T,), dtype=I32, device=dev)
     dmin = torch.empty((T,), dtype=torch.float32, device=dev)
     flags = torch.empty((T,), dtype=U8, device=dev)
-    call("mc_candidates", ptr(D), T, L, D.stride(0), float(lam), float(thr), ptr(fnorm), float(fcoef), cap, ptr(lo),
-         ptr(cnt), ptr(dmin), ptr(flags), stream_ptr())
+    call("mc_candidates", ptr(D), T, L, D.stride(0), float(lam), float(thr), ptr(fnorm), float(fcoef), ptr(rlo),
+         ptr(rhi), cap, ptr(lo), ptr(cnt), ptr(dmin), ptr(flags), stream_ptr())
     return lo, cnt, dmin, flags
 
 
@@ -364,7 +404,7 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, ter
 TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "0") == "1"
 
 
-def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
+def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None, tlist=None, nlist=None):
     """K2+K3: MSD estimate of every (frame, landmark) pair on tcgen05 (fp32 [T, L]),
     in the operand format of the splits.  two_sm (default: env MC_TF32_2SM, on)
     selects the CTA-pair kernel."""
@@ -374,9 +414,9 @@ def msd_estimate(fr: Split, lm: Split, D=None, grid=0, two_sm=None):
     if D is None:
         D = torch.empty((T, L), dtype=torch.float32, device=fr.hi.device)
     pair = TF32_2SM if two_sm is None else two_sm
-    if fr.fmt == "f16" and (fr.terms == 1 or not pair):
+    if fr.fmt == "f16" and (fr.terms == 1 or not pair or tlist is not None):
         call("mc_msd_f16", ptr(fr.hi), ptr(lm.hi), ptr(fr.scale), ptr(lm.scale), ptr(fr.g), ptr(lm.g), T, L, fr.kpad,
-             fr.terms, ptr(D), D.stride(0), grid, stream_ptr())
+             fr.terms, ptr(tlist), ptr(nlist), ptr(D), D.stride(0), grid, stream_ptr())
     elif fr.fmt == "f16":
         call("mc_msd_f16_2sm", ptr(fr.hi), ptr(lm.hi), ptr(fr.scale), ptr(lm.scale), ptr(fr.g), ptr(lm.g), T, L,
              fr.kpad, ptr(D), D.stride(0), grid, stream_ptr())

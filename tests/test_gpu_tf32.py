@@ -150,3 +150,29 @@ def test_one_term_and_split_screens_agree(cuda_device):
     assert (alo <= blo).all() and (alo + acnt >= blo + bcnt).all()
     ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
     np.testing.assert_allclose(a["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+
+
+def test_metric_pruned_screen_matches_unpruned_and_oracle(cuda_device):
+    """Triangle-inequality pruning of the screen: same s, z
+    and gradients as the unpruned screen (and the oracle), with fewer tensor-core tiles."""
+    wl = synth.config4(T=300, L=1536, N=240)
+    a = engine.PathCVTC(wl.landmarks, wl.lam, prune=True)
+    b = engine.PathCVTC(wl.landmarks, wl.lam, prune=False)
+    assert a.prune and not b.prune
+    oa = a.evaluate(wl.frames, out_dtype=torch.float64)
+    ob = b.evaluate(wl.frames, out_dtype=torch.float64)
+    np.testing.assert_allclose(oa["s"].cpu().numpy(), ob["s"].cpu().numpy(), rtol=1e-9)
+    np.testing.assert_allclose(oa["z"].cpu().numpy(), ob["z"].cpu().numpy(), rtol=1e-9)
+    for key in ("ds", "dz"):
+        x, y = oa[key].cpu().numpy(), ob[key].cpu().numpy()
+        scale = np.abs(y).reshape(y.shape[0], -1).max(axis=1)
+        assert np.all(np.abs(x - y).reshape(y.shape[0], -1).max(axis=1) <= 1e-9 * scale)
+    # the pruned plan computes a strict subset of the tiles
+    _, _, _, _, rlo, rhi, perm0 = a._pruned_estimate(wl.frames)
+    covered = (rhi - rlo).double().mean().item()
+    print(f"mean banded landmark range {covered:.0f} of {wl.landmarks.shape[0]}")
+    assert covered < wl.landmarks.shape[0]
+    assert sorted(perm0.cpu().tolist()) == list(range(300))
+    ref = O.batch_path_cv_exact(wl.frames[:40].astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    np.testing.assert_allclose(oa["s"].cpu().numpy()[:40], ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(oa["z"].cpu().numpy()[:40], ref["z"], rtol=1e-6, atol=1e-9)
