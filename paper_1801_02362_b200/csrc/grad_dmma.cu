@@ -29,11 +29,16 @@ constexpr int DNA = 256;           // atoms per sub-tile (8 warps x 32)
 constexpr int DKC = 24;            // kk rows per B chunk (8 landmarks)
 constexpr int LROW = 3 * DNA + 8;  // raw floats per staged landmark row (+8: bank shift between landmarks)
 constexpr int NST = 3;             // cp.async ring stages
-constexpr int DNT = 256;
+#ifndef MC_GD_WAT
+#define MC_GD_WAT 16
+#endif
+constexpr int WAT = MC_GD_WAT;     // atoms per warp (n-tiles of 8)
+constexpr int NJ = WAT / 8;
+constexpr int DNT = 32 * (DNA / WAT);  // 16 warps: more warps in flight to hide the fragment-load latency
 constexpr int DATOMS = 2048;       // atoms per CTA
 constexpr int CHL = DKC / 3;       // landmarks per chunk
-constexpr int LPT = CHL * DNA * 3 / DNT;  // 24 raw floats per thread per chunk
-constexpr int XPT = DG * DNA * 3 / DNT;  // 24 frame floats per thread per sub-tile
+constexpr int LPT = CHL * DNA * 3 / DNT;  // raw floats per thread per chunk
+constexpr int XPT = DG * DNA * 3 / DNT;  // frame floats per thread per sub-tile
 constexpr int DSMEM = DR * AST * (int)sizeof(double) + DKMAX * (int)sizeof(double) +
                       NST * CHL * LROW * (int)sizeof(float) + DG * 3 * DNA * (int)sizeof(float);
 
@@ -130,11 +135,11 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       }
     }
     cp_commit();
-    double c[6][4][2];
+    double c[6][NJ][2];
 #pragma unroll
     for (int m = 0; m < 6; ++m)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) c[m][j][0] = c[m][j][1] = 0.0;
+      for (int j = 0; j < NJ; ++j) c[m][j][0] = c[m][j][1] = 0.0;
     for (int w0 = wlo; w0 < whi; w0 += DWMAX) {
       const int wn = min(DWMAX, whi - w0);
       if (restage || !staged) {  // block-uniform
@@ -193,7 +198,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
 #pragma unroll
       for (int s = 0; s < DKC / 4; ++s) {
         const int kc = s * 4 + tq;
-        offB[s] = (kc / 3) * LROW + (warp * 32 + gq) * 3 + kc % 3;
+        offB[s] = (kc / 3) * LROW + (warp * WAT + gq) * 3 + kc % 3;
       }
       const double* aRow = sA + gq * AST + tq;
       int slot = 0, fill = NST - 1;
@@ -208,15 +213,15 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
 #pragma unroll
         for (int s = 0; s < DKC / 4; ++s) {
           const double lcg = lk[4 * s];
-          double a[6], b[4];
+          double a[6], b[NJ];
 #pragma unroll
           for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = (double)rb[offB[s] + j * 24] - lcg;
+          for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24] - lcg;
 #pragma unroll
           for (int m = 0; m < 6; ++m)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dmma(c[m][j], a[m], b[j]);
+            for (int j = 0; j < NJ; ++j) dmma(c[m][j], a[m], b[j]);
         }
         slot = slot + 1 == NST ? 0 : slot + 1;
       }
@@ -225,12 +230,12 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     }
     // epilogue: each accumulator element is one (frame, s|z, axis, atom) output.
     // Loads of a half (3 row tiles x 8 atoms) are batched ahead of its stores.
-    double wk[4][2], wak[4][2];
+    double wk[NJ][2], wak[NJ][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int k = a0 + warp * 32 + j * 8 + 2 * tq + e;
+        const int k = a0 + warp * WAT + j * 8 + 2 * tq + e;
         wk[j][e] = k < n ? w[k] : 0.0;
         wak[j][e] = k < n ? wa[k] : 0.0;
       }
@@ -247,10 +252,10 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       const int tout = out_map ? out_map[t] : t;
       const float* xs = sX + f * 3 * DNA + b;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int al = warp * 32 + j * 8 + 2 * tq + e;
+          const int al = warp * WAT + j * 8 + 2 * tq + e;
           const int k = a0 + al;
           if (k >= n) continue;
           const double x = (double)xs[3 * al] - cx;
