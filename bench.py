@@ -284,7 +284,7 @@ class ConfigTC:
         self.n, self.L = shp["N"], shp["L"]
         self.pcv = engine.PathCVTC(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q)
         self.frames_dev = self.wl.frames
-        self.chunk = 32768
+        self.chunk = 24576
         try:
             self.frames_host = self.frames_dev.cpu().pin_memory()
             self.host_kind = "pinned"
@@ -319,17 +319,24 @@ class ConfigTC:
         return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
 
     def e2e_chunks(self):
-        """Chunk boundaries of the streamed step: sizes ramp up geometrically
-        (chunk/8, chunk/4, chunk/2, then chunk) so only a small first copy is
-        exposed, while each chunk's compute (~3.9 us/frame on config 4) covers
-        the next chunk's copy (~2.2 us/frame at 55 GB/s); large steady chunks
-        keep the window-sorted frame groups of the refine/gradient kernels tight."""
-        out, c0, size = [], 0, max(1, self.chunk // 8)
+        """Chunk boundaries of the streamed step: sizes ramp up geometrically (x1.5
+        from chunk/6 to chunk) so only a small first copy is exposed, while each
+        chunk's compute (~2.7 us/frame on config 4) covers the next chunk's copy
+        (~2.2 us/frame at 55 GB/s); large steady chunks keep the pruning bands and
+        the window-sorted frame groups of the refine/gradient kernels tight
+        (schedule sweep: tools/_diag/e2e_sched.py)."""
+        env = os.environ.get("MC_E2E_CHUNKS")  # "first,steady[,growth]" (measurement knob)
+        first, steady, growth = self.chunk // 6, self.chunk, 1.5
+        if env:
+            parts = [float(x) for x in env.split(",")]
+            first, steady = int(parts[0]), int(parts[1])
+            growth = parts[2] if len(parts) > 2 else 2.0
+        out, c0, size = [], 0, max(1, first)
         while c0 < self.T:
-            n = min(size, self.T - c0)
+            n = min(int(size), self.T - c0)
             out.append((c0, n))
             c0 += n
-            size = min(self.chunk, 2 * size)
+            size = min(steady, max(size + 1, int(size * growth)))
         return out
 
     def step_e2e(self):
