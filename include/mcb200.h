@@ -174,7 +174,8 @@ int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, 
  * mc_refine: exact fp64 covariance + fit of the in-window pairs (or, with lo = cnt =
  *   NULL, of all pairs: the dense exact MSD matrix into Dd).  lwbar [L, 3] (nullable)
  *   = sum_j w_j (a_lj - c_l) (mc_center_split's wbar of the landmarks): frames then
- *   enter the fp64 contraction uncentred, S = S_half - c_x lwbar^T. */
+ *   enter the fp64 contraction uncentred, S = S_half - c_x lwbar^T.  fmap [T] (nullable):
+ *   frame t's row in `frames` (the per-frame scalars stay indexed by t). */
 int mc_center_split(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
                     const double* w_disp, int32_t weighted, float* hi, float* lo, double* centroid, double* gnorm,
                     double* wbar, double* mom, uint8_t* flags, void* stream);
@@ -182,7 +183,9 @@ int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const floa
                 const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                 void* stream);
 /* Gradient pass of the fp32 path blocked over groups of 8 frames in candidate-sort
- * order (perm): each landmark coordinate feeds 8 frames; exact-refresh rows only. */
+ * order (perm): each landmark coordinate feeds 8 frames; exact-refresh rows only.
+ * out_map [T] (nullable): frame t's row in fraw and in ds/dz (the other per-frame
+ * inputs stay indexed by t) -- the pruned screen's sorted order back to the caller's. */
 int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const float* lraw,
                          const double* lcen, const double* w, const double* w_align, const int32_t* sig_idx,
                          const double* sig_coef, const int32_t* nsig, const double* fvec, const int32_t* perm,
@@ -240,7 +243,7 @@ int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, 
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
               const double* lwbar, const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
               const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
-              float* Dd, int64_t ldd, uint8_t* flags, void* stream);
+              float* Dd, int64_t ldd, const int32_t* fmap, uint8_t* flags, void* stream);
 
 /* Per-pair DistanceResult gradients of the reference-facing API:
  * exact_distance (Eq. 3/4) and approx_distance (Eq. 5/6,

@@ -77,7 +77,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
   float* sR = reinterpret_cast<float*>(sLc + DKMAX);      // [NST][CHL][LROW] raw landmark floats
   float* sX = sR + NST * CHL * LROW;                      // [DG][3 DNA] raw frame floats of the sub-tile
-  __shared__ int s_t[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
+  __shared__ int s_t[DG], s_raw[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
   __shared__ double s_fc[DG][3], s_fv[DG][8];
   __shared__ int s_wlo, s_whi;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -90,6 +90,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       ns = nsig[t];
     }
     s_t[tid] = t;
+    s_raw[tid] = (t >= 0 && out_map) ? out_map[t] : t;  // caller's row: raw coordinates and gradients
     s_ns[tid] = ns;
     s_flo[tid] = (t >= 0 && ns > 0) ? sig_idx[(int64_t)t * cap] : 0x7fffffff;
     s_fhi[tid] = (t >= 0 && ns > 0) ? sig_idx[(int64_t)t * cap + ns - 1] + 1 : -1;
@@ -120,7 +121,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       for (int u = 0; u < XPT / 4; ++u) {
         const int e4 = tid + u * DNT;  // [0, DG * 3 DNA / 4)
         const int f = e4 / (3 * DNA / 4), r = 4 * (e4 - f * (3 * DNA / 4));
-        const int t = s_t[f];
+        const int t = s_raw[f];
         const bool ok = t >= 0 && 3 * a0 + r + 4 <= 3 * n;
         cp_async16(sX + f * 3 * DNA + r, fraw + (ok ? ((int64_t)t * n + a0) * 3 + r : 0), ok);
       }
@@ -129,7 +130,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       for (int u = 0; u < XPT; ++u) {
         const int e = tid + u * DNT;  // [0, DG * 3 DNA)
         const int f = e / (3 * DNA), r = e - f * (3 * DNA);
-        const int t = s_t[f];
+        const int t = s_raw[f];
         const bool ok = t >= 0 && a0 + r / 3 < n;
         cp_async4(sX + e, fraw + ((int64_t)(ok ? t : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
       }
@@ -249,7 +250,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       if (t < 0) continue;
       const double cx = s_fc[f][b], sc = s_fv[f][sz], corr = s_fv[f][2 + sz * 3 + b];
       OT* __restrict__ out = sz ? dz : ds;
-      const int tout = out_map ? out_map[t] : t;
+      const int tout = s_raw[f];
       const float* xs = sX + f * 3 * DNA + b;
 #pragma unroll
       for (int j = 0; j < NJ; ++j)

@@ -63,7 +63,7 @@ template <bool VEC, bool UNC>
 __global__ void __launch_bounds__(QNT, 2)
 refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const float* __restrict__ lr,
                    const double* __restrict__ lc, const double* __restrict__ lwbar, const double* __restrict__ w,
-                   const double* __restrict__ gx,
+                   const double* __restrict__ gx, const int* __restrict__ fmap,
                    const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,
                    const int* __restrict__ lo, const int* __restrict__ cnt, int cap, double* __restrict__ Dex,
                    double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
@@ -71,7 +71,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
   float* ring = reinterpret_cast<float*>(qsm);                                     // [QNST][QF + QL][QRS]
   double* sC = reinterpret_cast<double*>(qsm);                                      // [3 QF][QCS] (after the K loop)
   double* sW = reinterpret_cast<double*>(qsm + (QRING > QCBYTES ? QRING : QCBYTES));  // [QNST][QKC]
-  __shared__ int s_t[QF], s_lo[QF], s_cnt[QF];
+  __shared__ int s_t[QF], s_raw[QF], s_lo[QF], s_cnt[QF];
   __shared__ double s_fc[QF][3];
   __shared__ int s_wlo, s_whi;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -86,6 +86,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
       c = lo ? cnt[t] : L;
     }
     s_t[tid] = t;
+    s_raw[tid] = (t >= 0 && fmap) ? fmap[t] : t;  // row of frame t in the raw coordinate array
     s_lo[tid] = a;
     s_cnt[tid] = c;
     for (int b = 0; b < 3; ++b) s_fc[tid][b] = t >= 0 ? fc[3 * t + b] : 0.0;
@@ -128,7 +129,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
           const int e = tid + u * QNT;
           const int row = e / QV4, c4 = e - row * QV4;
           const bool isf = row < QF;
-          const int s = isf ? s_t[row] : l0 + row - QF;
+          const int s = isf ? s_raw[row] : l0 + row - QF;
           const bool ok = ch < nch && (isf ? s >= 0 : s < L) && 3 * k0 + 4 * c4 + 4 <= 3 * n;
           const float* src = (isf ? fr : lr) + (ok ? ((int64_t)s * n + k0) * 3 + 4 * c4 : 0);
           cpa16(dst + row * QRS + 4 * c4, src, ok);
@@ -139,7 +140,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
           const int e = tid + u * QNT;  // [0, 64 * 3 QKC)
           const int row = e / (3 * QKC), r = e - row * (3 * QKC);
           const bool isf = row < QF;
-          const int s = isf ? s_t[row] : l0 + row - QF;
+          const int s = isf ? s_raw[row] : l0 + row - QF;
           const bool ok = ch < nch && (isf ? s >= 0 : s < L) && k0 + r / 3 < n;
           const float* src = (isf ? fr : lr) + (ok ? ((int64_t)s * n + k0) * 3 + r : 0);
           cpa4(dst + row * QRS + r, src, ok);
@@ -248,9 +249,10 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 }
 
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
-                               const double* lwbar, const double* w, const double* gx, const double* ga, int T, int L,
-                               int n, const int* perm, const int* lo, const int* cnt, int cap, double* Dex,
-                               double* Rex, float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream) {
+                               const double* lwbar, const double* w, const double* gx, const int* fmap,
+                               const double* ga, int T, int L, int n, const int* perm, const int* lo, const int* cnt,
+                               int cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
+                               cudaStream_t stream) {
   if (T <= 0 || L <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -264,8 +266,8 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
   const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(fr) & 15) == 0 && (reinterpret_cast<uintptr_t>(lr) & 15) == 0;
   const dim3 grid((T + QF - 1) / QF);
 #define MC_RD_LAUNCH(V, U)                                                                                          \
-  refine_dmma_kernel<V, U><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, ga, T, L, n, perm, lo, cnt, \
-                                                         cap, Dex, Rex, Dd, ldd, flags)
+  refine_dmma_kernel<V, U><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, fmap, ga, T, L, n, perm,  \
+                                                         lo, cnt, cap, Dex, Rex, Dd, ldd, flags)
   if (lwbar) {
     if (vec) MC_RD_LAUNCH(true, true); else MC_RD_LAUNCH(false, true);
   } else {

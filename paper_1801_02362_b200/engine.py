@@ -382,21 +382,22 @@ class PathCVTC:
     def _pruned_estimate(self, frames):
         """Metric-pruned one-term screen: coarse screen -> per-frame admissible tile hulls
         -> frames sorted by hull (perm0) -> banded tensor-core estimate of the sorted
-        frames.  Returns the sorted raw frames / split, the estimate, the row ranges
-        and perm0 (sorted position -> original frame)."""
+        frames.  Returns the estimate (sorted rows), the caller's raw frames, the sorted
+        split, the unsorted split, the row ranges and perm0 (sorted position -> frame)."""
         fr0, fs0 = self._frames(frames, 1, check=False)
         Dc = K.msd_estimate(fs0, self.ls_coarse)
         hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.c_unit, self.mind,
                                      (self.cutoff + 2.0) / self.lam, self.knear)
         ntl = self.mind.shape[1]
         perm0 = K.sort_by_key(key, ntl + 1)
-        frs = K.gather_rows(fr0, perm0)
-        _, fss = self._frames(frs, 1, check=False)
+        # sorted view of the split (operand rows + scalars gathered, no second split); the
+        # raw frames stay in place and are read through perm0 (refine fmap / grad out_map)
+        fss = K.gather_split(fs0, perm0)
         tlist, nlist, rlo, rhi = K.band_tiles(perm0, hlo, hhi, 128, 48, self.L, ntl)
-        Dest = torch.empty((frs.shape[0], self.L), dtype=torch.float32, device=self.device)
+        Dest = torch.empty((fr0.shape[0], self.L), dtype=torch.float32, device=self.device)
         K.msd_estimate(fss, self.ls, Dest, tlist=tlist, nlist=nlist)
         self._last_tiles = nlist
-        return Dest, frs, fss, fs0, rlo, rhi, perm0
+        return Dest, fr0, fss, fs0, rlo, rhi, perm0
 
     def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False):
         rlo = rhi = perm0 = fs0 = None
@@ -413,7 +414,8 @@ class PathCVTC:
                                               fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0,
                                               rlo=rlo, rhi=rhi)
             perm = K.sort_by_key(lo, self.L)
-            Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap)
+            Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
+                                        fmap=perm0)
             wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
                                     rowcnt=cnt)
             out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,

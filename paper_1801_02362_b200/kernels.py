@@ -250,7 +250,8 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
 def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32,
                       out_map=None):
     """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames.
-    out_map (optional, int32 [T]): output row of frame t (gradients written in place)."""
+    out_map (optional, int32 [T]): the caller's row of frame t -- its raw coordinates
+    are read from and its gradients written to that row."""
     T, n = frames.shape[0], frames.shape[1]
     dev = frames.device
     ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
@@ -289,6 +290,24 @@ def band_tiles(perm, hull_lo, hull_hi, BM, BL, L, ntl):
     return tlist, nlist, rlo, rhi
 
 
+def gather_split(sp, idx):
+    """The Split of frames idx[0], idx[1], ... (rows of every operand plane and of the
+    per-structure scalars gathered on the device; flags are kept as they are)."""
+    rows = idx.numel()
+    hi = torch.empty((sp.hi.shape[0], rows, sp.hi.shape[2]), dtype=sp.hi.dtype, device=sp.hi.device)
+    for p in range(sp.hi.shape[0]):
+        call("mc_gather_rows", ptr(sp.hi[p]), 4, sp.hi.shape[2] * sp.hi.element_size() // 4, ptr(idx), rows,
+             ptr(hi[p]), stream_ptr())
+    lo = None
+    if sp.lo is not None:
+        lo = torch.empty((sp.lo.shape[0], rows, sp.lo.shape[2]), dtype=sp.lo.dtype, device=sp.lo.device)
+        for p in range(sp.lo.shape[0]):
+            call("mc_gather_rows", ptr(sp.lo[p]), 4, sp.lo.shape[2], ptr(idx), rows, ptr(lo[p]), stream_ptr())
+    g = lambda x: None if x is None else gather_rows(x, idx)  # noqa: E731
+    return Split(hi, lo, g(sp.centroid), g(sp.g), g(sp.wbar), g(sp.mom), sp.flags, sp.n, sp.kpad, g(sp.scale),
+                 sp.fmt, sp.terms, g(sp.opnorm))
+
+
 def gather_rows(src, idx):
     """dst[r] = src[idx[r]] for a contiguous [rows, ...] fp32/fp64 tensor."""
     src = src.contiguous()
@@ -322,8 +341,10 @@ def sort_by_key(key, nbins):
     return perm
 
 
-def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None):
-    """Exact fp64 fits of the in-window pairs (sparse) or of all pairs (dense, into Dd)."""
+def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None,
+           fmap=None):
+    """Exact fp64 fits of the in-window pairs (sparse) or of all pairs (dense, into Dd).
+    fmap (optional int32 [T]): frame t's row in `frames` (per-frame scalars indexed by t)."""
     T, n = frames.shape[0], frames.shape[1]
     L = landmarks.shape[0]
     dev = frames.device
@@ -333,7 +354,7 @@ def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, c
     call("mc_refine", ptr(frames), ptr(fsplit.centroid), ptr(landmarks), ptr(lsplit.centroid), ptr(lsplit.wbar),
          ptr(w), ptr(fsplit.g),
          ptr(lsplit.g), T, L, n, ptr(perm), ptr(lo), ptr(cnt), cap, ptr(Dex), ptr(Rex), ptr(Dd),
-         Dd.stride(0) if Dd is not None else 0, ptr(flags), stream_ptr())
+         Dd.stride(0) if Dd is not None else 0, ptr(fmap), ptr(flags), stream_ptr())
     return Dex, Rex, flags
 
 
