@@ -175,7 +175,9 @@ int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, 
  *   NULL, of all pairs: the dense exact MSD matrix into Dd).  lwbar [L, 3] (nullable)
  *   = sum_j w_j (a_lj - c_l) (mc_center_split's wbar of the landmarks): frames then
  *   enter the fp64 contraction uncentred, S = S_half - c_x lwbar^T.  fmap [T] (nullable):
- *   frame t's row in `frames` (the per-frame scalars stay indexed by t). */
+ *   frame t's row in `frames` (the per-frame scalars stay indexed by t).  wuni > 0 (all
+ *   displacement weights equal to wuni) with fwbar [T, 3] (frames' wbar) and lwbar: both
+ *   operands enter raw, S = wuni S_raw - fwbar c_l^T - c_x lwbar^T - n wuni c_x c_l^T. */
 int mc_center_split(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
                     const double* w_disp, int32_t weighted, float* hi, float* lo, double* centroid, double* gnorm,
                     double* wbar, double* mom, uint8_t* flags, void* stream);
@@ -243,7 +245,8 @@ int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, 
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
               const double* lwbar, const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
               const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
-              float* Dd, int64_t ldd, const int32_t* fmap, uint8_t* flags, void* stream);
+              float* Dd, int64_t ldd, const int32_t* fmap, const double* fwbar, double wuni,
+              uint8_t* flags, void* stream);
 
 /* Per-pair DistanceResult gradients of the reference-facing API:
  * exact_distance (Eq. 3/4) and approx_distance (Eq. 5/6,

@@ -76,7 +76,8 @@ _SIGS = {
     "mc_band_tiles": [_P, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
     "mc_gather_rows": [_P, _I32, _I64, _P, _I32, _P, _P],
     "mc_sort_by_key": [_P, _I32, _I32, _P, _P, _P],
-    "mc_refine": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P, _P],
+    "mc_refine": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P, _D, _P,
+                  _P],
     "mc_pair_grad": [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],

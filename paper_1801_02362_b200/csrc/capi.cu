@@ -236,7 +236,8 @@ int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, 
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
               const double* lwbar, const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
               const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
-              float* Dd, int64_t ldd, const int32_t* fmap, uint8_t* flags, void* stream) {
+              float* Dd, int64_t ldd, const int32_t* fmap, const double* fwbar, double wuni, uint8_t* flags,
+              void* stream) {
   if (T < 0 || L < 1 || n < 2) return MC_ERR_CONFIG;
   if ((lo == nullptr) != (cnt == nullptr)) return MC_ERR_CONFIG;
   if (T > 0 && (!frames || !fcentroid || !landmarks || !lcentroid || !w || !gx || !ga)) return MC_ERR_CONFIG;
@@ -253,8 +254,8 @@ int mc_refine(const float* frames, const double* fcentroid, const float* landmar
     return cuda_status(mc::launch_refine(frames, fcentroid, landmarks, lcentroid, w, gx, ga, T, L, n, perm, lo, cnt,
                                          cap, Dex, Rex, Dd, ldd, flags, S_(stream)));
   }
-  return cuda_status(mc::launch_refine_dmma(frames, fcentroid, landmarks, lcentroid, lwbar, w, gx, fmap, ga, T, L, n,
-                                            perm, lo, cnt, cap, Dex, Rex, Dd, ldd, flags, S_(stream)));
+  return cuda_status(mc::launch_refine_dmma(frames, fcentroid, landmarks, lcentroid, lwbar, w, gx, fmap, fwbar, wuni,
+                                            ga, T, L, n, perm, lo, cnt, cap, Dex, Rex, Dd, ldd, flags, S_(stream)));
 }
 
 int mc_pair_grad(int64_t P, int32_t n, int32_t npad, const double* xplanes, const double* aplanes, const int32_t* xi,

@@ -77,9 +77,9 @@ cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double 
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
                                const double* lwbar, const double* w, const double* gx, const int* fmap,
-                               const double* ga, int T, int L, int n, const int* perm, const int* lo, const int* cnt,
-                               int cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
-                               cudaStream_t stream);
+                               const double* fwbar, double wuni, const double* ga, int T, int L, int n,
+                               const int* perm, const int* lo, const int* cnt, int cap, double* Dex, double* Rex,
+                               float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_refine(const float* fr, const double* fc, const float* lr, const double* lc, const double* w,
                           const double* gx, const double* ga, int T, int L, int n, const int* perm, const int* lo,
                           const int* cnt, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,

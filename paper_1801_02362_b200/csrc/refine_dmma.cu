@@ -59,11 +59,18 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // arithmetic when the displacement and alignment weights coincide), which saves the
 // per-fragment frame centring (6 DADD and 12 registers per k-step); no cancellation,
 // since S_half - S = c_x lwbar^T is itself ~0.
-template <bool VEC, bool UNC>
+// RAW (uniform weights wuni, fwbar and lwbar given): both operands enter uncentred and
+// unweighted -- A = x, B = a, fragments are plain fp32 -> fp64 conversions with no
+// fp64 ALU work in the K loop (DADD/DMUL compete with DMMA for issue: 9 per 18 DMMA
+// cost 14% of the DMMA rate, tools/_diag/dmma_probe2.cu) -- and the epilogue forms
+//   S = wuni S_raw - fwbar c_l^T - c_x lwbar^T - W c_x c_l^T   (W = n wuni),
+// whose cancellation costs ~1e-16 |c_x||c_l| / spread^2 relative (~1e-15 on config 4).
+template <bool VEC, bool UNC, bool RAW = false>
 __global__ void __launch_bounds__(QNT, 2)
 refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, const float* __restrict__ lr,
                    const double* __restrict__ lc, const double* __restrict__ lwbar, const double* __restrict__ w,
-                   const double* __restrict__ gx, const int* __restrict__ fmap,
+                   const double* __restrict__ gx, const int* __restrict__ fmap, const double* __restrict__ fwbar,
+                   double wuni,
                    const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,
                    const int* __restrict__ lo, const int* __restrict__ cnt, int cap, double* __restrict__ Dex,
                    double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
@@ -115,7 +122,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
     for (int i = 0; i < 3; ++i) {
       const int nt = wn * 3 + i;
       const int l = l0 + (nt & 3) * 8 + gq;
-      lcB[i] = l < L ? lc[3 * l + (nt >> 2)] : 0.0;
+      lcB[i] = (!RAW && l < L) ? lc[3 * l + (nt >> 2)] : 0.0;
     }
     // ring stage ch: rows 0..31 frames, 32..63 landmarks, 3 QKC floats each (atoms QKC ch ..)
     auto issue = [&](int ch, int slot) {
@@ -181,12 +188,14 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
       const double* ww = sW + slot * QKC + tq;
 #pragma unroll
       for (int s = 0; s < QKC / 4; ++s) {
-        const double wj = ww[4 * s];
+        const double wj = RAW ? 1.0 : ww[4 * s];
         double a[6], b[3];
 #pragma unroll
-        for (int i = 0; i < 6; ++i) a[i] = UNC ? (double)sg[offA[i] + 12 * s] : (double)sg[offA[i] + 12 * s] - fcA[i];
+        for (int i = 0; i < 6; ++i)
+          a[i] = (UNC || RAW) ? (double)sg[offA[i] + 12 * s] : (double)sg[offA[i] + 12 * s] - fcA[i];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) b[i] = wj * ((double)sg[offB[i] + 12 * s] - lcB[i]);
+        for (int i = 0; i < 3; ++i)
+          b[i] = RAW ? (double)sg[offB[i] + 12 * s] : wj * ((double)sg[offB[i] + 12 * s] - lcB[i]);
 #pragma unroll
         for (int i = 0; i < 6; ++i)
 #pragma unroll
@@ -220,7 +229,13 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 #pragma unroll
         for (int g = 0; g < 3; ++g) {
           S[b * 3 + g] = sC[(b * QF + f) * QCS + g * QL + li];
-          if (UNC) S[b * 3 + g] -= s_fc[f][b] * lwbar[3 * l + g];
+          if (RAW) {
+            const double cxb = s_fc[f][b], clg = lc[3 * l + g];
+            S[b * 3 + g] = wuni * S[b * 3 + g] - fwbar[3 * t + b] * clg - cxb * lwbar[3 * l + g] -
+                           wuni * n * cxb * clg;
+          } else if (UNC) {
+            S[b * 3 + g] -= s_fc[f][b] * lwbar[3 * l + g];
+          }
         }
       double q[4];
       bool ill = false;
@@ -250,14 +265,16 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
                                const double* lwbar, const double* w, const double* gx, const int* fmap,
-                               const double* ga, int T, int L, int n, const int* perm, const int* lo, const int* cnt,
-                               int cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
-                               cudaStream_t stream) {
+                               const double* fwbar, double wuni, const double* ga, int T, int L, int n,
+                               const int* perm, const int* lo, const int* cnt, int cap, double* Dex, double* Rex,
+                               float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream) {
   if (T <= 0 || L <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
     for (const void* fn : {(const void*)refine_dmma_kernel<true, true>, (const void*)refine_dmma_kernel<false, true>,
-                           (const void*)refine_dmma_kernel<true, false>, (const void*)refine_dmma_kernel<false, false>}) {
+                           (const void*)refine_dmma_kernel<true, false>, (const void*)refine_dmma_kernel<false, false>,
+                           (const void*)refine_dmma_kernel<true, false, true>,
+                           (const void*)refine_dmma_kernel<false, false, true>}) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
       if (e != cudaSuccess) return e;
     }
@@ -265,13 +282,15 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
   }
   const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(fr) & 15) == 0 && (reinterpret_cast<uintptr_t>(lr) & 15) == 0;
   const dim3 grid((T + QF - 1) / QF);
-#define MC_RD_LAUNCH(V, U)                                                                                          \
-  refine_dmma_kernel<V, U><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, fmap, ga, T, L, n, perm,  \
-                                                         lo, cnt, cap, Dex, Rex, Dd, ldd, flags)
-  if (lwbar) {
-    if (vec) MC_RD_LAUNCH(true, true); else MC_RD_LAUNCH(false, true);
+#define MC_RD_LAUNCH(V, U, R)                                                                                 \
+  refine_dmma_kernel<V, U, R><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, fmap, fwbar, wuni, ga, T, \
+                                                            L, n, perm, lo, cnt, cap, Dex, Rex, Dd, ldd, flags)
+  if (lwbar && fwbar && wuni > 0.0) {
+    if (vec) MC_RD_LAUNCH(true, false, true); else MC_RD_LAUNCH(false, false, true);
+  } else if (lwbar) {
+    if (vec) MC_RD_LAUNCH(true, true, false); else MC_RD_LAUNCH(false, true, false);
   } else {
-    if (vec) MC_RD_LAUNCH(true, false); else MC_RD_LAUNCH(false, false);
+    if (vec) MC_RD_LAUNCH(true, false, false); else MC_RD_LAUNCH(false, false, false);
   }
 #undef MC_RD_LAUNCH
   return cudaGetLastError();

@@ -300,6 +300,9 @@ class PathCVTC:
             raise ConfigError("q must have one value per landmark")
         self.q = torch.from_numpy(qq).to(self.device)
         self.lraw = lm
+        # uniform displacement weights (the configs' default): the exact refits run on raw,
+        # unweighted fp32 operands (refine_dmma RAW mode)
+        self.wuni = float(self.w[0].item()) if bool((self.w == self.w[0]).all()) else 0.0
         self._ls = {}
         self.screen_terms = 1 if self.screen == "f16x1" else 3
         self.ls = self._lsplit(self.screen_terms)
@@ -375,7 +378,7 @@ class PathCVTC:
         D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
         if not exact:
             return K.msd_estimate(fs, self._lsplit(3), D)
-        _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D)
+        _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D, wuni=self.wuni)
         _raise_flags(flags, "msd_matrix")
         return D
 
@@ -415,7 +418,7 @@ class PathCVTC:
                                               rlo=rlo, rhi=rhi)
             perm = K.sort_by_key(lo, self.L)
             Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
-                                        fmap=perm0)
+                                        fmap=perm0, wuni=self.wuni)
             wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
                                     rowcnt=cnt)
             out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,

@@ -342,7 +342,7 @@ def sort_by_key(key, nbins):
 
 
 def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None,
-           fmap=None):
+           fmap=None, wuni=0.0):
     """Exact fp64 fits of the in-window pairs (sparse) or of all pairs (dense, into Dd).
     fmap (optional int32 [T]): frame t's row in `frames` (per-frame scalars indexed by t)."""
     T, n = frames.shape[0], frames.shape[1]
@@ -354,7 +354,8 @@ def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, c
     call("mc_refine", ptr(frames), ptr(fsplit.centroid), ptr(landmarks), ptr(lsplit.centroid), ptr(lsplit.wbar),
          ptr(w), ptr(fsplit.g),
          ptr(lsplit.g), T, L, n, ptr(perm), ptr(lo), ptr(cnt), cap, ptr(Dex), ptr(Rex), ptr(Dd),
-         Dd.stride(0) if Dd is not None else 0, ptr(fmap), ptr(flags), stream_ptr())
+         Dd.stride(0) if Dd is not None else 0, ptr(fmap), ptr(fsplit.wbar if wuni > 0 else None), float(wuni),
+         ptr(flags), stream_ptr())
     return Dex, Rex, flags
 
 
