@@ -40,7 +40,8 @@ constexpr int CHL = DKC / 3;       // landmarks per chunk
 constexpr int LPT = CHL * DNA * 3 / DNT;  // raw floats per thread per chunk
 constexpr int XPT = DG * DNA * 3 / DNT;  // frame floats per thread per sub-tile
 constexpr int DSMEM = DR * AST * (int)sizeof(double) + DKMAX * (int)sizeof(double) +
-                      NST * CHL * LROW * (int)sizeof(float) + DG * 3 * DNA * (int)sizeof(float);
+                      NST * CHL * LROW * (int)sizeof(float) + DG * 3 * DNA * (int)sizeof(float) +
+                      (2 * NST + 1) * (int)sizeof(uint64_t);
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -49,6 +50,33 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok)
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+          smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared completing on an mbarrier (TMA engine)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -77,6 +105,11 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
   float* sR = reinterpret_cast<float*>(sLc + DKMAX);      // [NST][CHL][LROW] raw landmark floats
   float* sX = sR + NST * CHL * LROW;                      // [DG][3 DNA] raw frame floats of the sub-tile
+  // VEC: warp-decoupled ring -- thread 0 issues 1-D TMA bulk copies completing on
+  // full[slot]; each warp releases a slot on empty[slot]; no CTA barrier per chunk
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + DG * 3 * DNA);
+  uint64_t* empty = full + NST;
+  uint64_t* xfull = empty + NST;
   __shared__ int s_t[DG], s_raw[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
   __shared__ double s_fc[DG][3], s_fv[DG][8];
   __shared__ int s_wlo, s_whi;
@@ -107,23 +140,34 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     s_wlo = a;
     s_whi = b;
   }
+  if (VEC) {
+    if (tid == 0) {
+      for (int i = 0; i < NST; ++i) { mb_init(&full[i], 1); mb_init(&empty[i], DNT / 32); }
+      mb_init(xfull, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // stale ring rows are multiplied by zero coefficients: make them finite once
+    for (int e = tid; e < NST * CHL * LROW; e += DNT) sR[e] = 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   __syncthreads();
   const int wlo = s_wlo, whi = s_whi;
   const bool restage = whi - wlo > DWMAX;
+  uint32_t gch = 0, xphase = 0;  // VEC: chunks consumed by this CTA (ring position / parity)
   bool staged = false;
   const int katom0 = blockIdx.y * DATOMS;
   const int katom1 = min(n, katom0 + DATOMS);
   for (int a0 = katom0; a0 < katom1; a0 += DNA) {
     // the epilogue's frame coordinates: one cp.async group issued now, long
     // complete by the time the contraction below has finished
+    const int nat = min(DNA, n - a0);  // valid atoms of this sub-tile
     if (VEC) {
-#pragma unroll
-      for (int u = 0; u < XPT / 4; ++u) {
-        const int e4 = tid + u * DNT;  // [0, DG * 3 DNA / 4)
-        const int f = e4 / (3 * DNA / 4), r = 4 * (e4 - f * (3 * DNA / 4));
-        const int t = s_raw[f];
-        const bool ok = t >= 0 && 3 * a0 + r + 4 <= 3 * n;
-        cp_async16(sX + f * 3 * DNA + r, fraw + (ok ? ((int64_t)t * n + a0) * 3 + r : 0), ok);
+      if (tid == 0) {
+        int rows = 0;
+        for (int f = 0; f < DG; ++f) rows += s_raw[f] >= 0;
+        mb_expect(xfull, (uint32_t)(rows * 12 * nat));
+        for (int f = 0; f < DG; ++f)
+          if (s_raw[f] >= 0) bulk_g2s(sX + f * 3 * DNA, fraw + ((int64_t)s_raw[f] * n + a0) * 3, 12 * nat, xfull);
       }
     } else {
 #pragma unroll 4
@@ -135,7 +179,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         cp_async4(sX + e, fraw + ((int64_t)(ok ? t : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
       }
     }
-    cp_commit();
+    if (!VEC) cp_commit();
     double c[6][NJ][2];
 #pragma unroll
     for (int m = 0; m < 6; ++m)
@@ -167,33 +211,6 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         __syncthreads();
       }
       const int nch = (3 * wn + DKC - 1) / DKC;
-      // stage chunk ch (landmarks w0 + CHL ch .., atoms a0 .. a0 + DNA) into ring slot `slot`;
-      // out-of-range elements are zero-filled (their coefficients are zero too)
-      auto issue = [&](int ch, int slot) {
-        float* dst = sR + slot * CHL * LROW;
-        if (VEC) {
-#pragma unroll
-          for (int u = 0; u < LPT / 4; ++u) {
-            const int e4 = tid + u * DNT;  // [0, CHL * 3 DNA / 4)
-            const int q = e4 / (3 * DNA / 4), r = 4 * (e4 - q * (3 * DNA / 4));
-            const int li = w0 + ch * CHL + q;
-            const bool ok = ch < nch && li < w0 + wn && 3 * a0 + r + 4 <= 3 * n;
-            cp_async16(dst + q * LROW + r, lraw + (ok ? ((int64_t)li * n + a0) * 3 + r : 0), ok);
-          }
-        } else {
-#pragma unroll 4
-          for (int u = 0; u < LPT; ++u) {
-            const int e = tid + u * DNT;  // [0, CHL * 3 DNA)
-            const int q = e / (3 * DNA), r = e - q * (3 * DNA);
-            const int li = w0 + ch * CHL + q;
-            const bool ok = ch < nch && li < w0 + wn && a0 + r / 3 < n;
-            cp_async4(dst + q * LROW + r, lraw + ((int64_t)(ok ? li : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
-          }
-        }
-        cp_commit();
-      };
-#pragma unroll
-      for (int st = 0; st < NST - 1; ++st) issue(st, st);
       // loop-invariant fragment offsets: B element (kk = 4 s + tq -> landmark q, axis g)
       int offB[DKC / 4];
 #pragma unroll
@@ -202,6 +219,64 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         offB[s] = (kc / 3) * LROW + (warp * WAT + gq) * 3 + kc % 3;
       }
       const double* aRow = sA + gq * AST + tq;
+      if constexpr (VEC) {
+        // producer (thread 0): chunk ch -> ring slot (gch + ch) % NST once every warp released it
+        auto produce = [&](int ch) {
+          const uint32_t g = gch + (uint32_t)ch;
+          const int slot = (int)(g % NST);
+          if (g >= (uint32_t)NST) mb_wait(&empty[slot], ((g / NST) - 1) & 1u);
+          const int q1 = min(CHL, wn - ch * CHL);
+          mb_expect(&full[slot], (uint32_t)(q1 * 12 * nat));
+          float* dst = sR + slot * CHL * LROW;
+          for (int q = 0; q < q1; ++q)
+            bulk_g2s(dst + q * LROW, lraw + ((int64_t)(w0 + ch * CHL + q) * n + a0) * 3, 12 * nat, &full[slot]);
+        };
+        if (tid == 0)
+          for (int ch = 0; ch < min(nch, NST - 1); ++ch) produce(ch);
+        for (int ch = 0; ch < nch; ++ch) {
+          if (tid == 0 && ch + NST - 1 < nch) produce(ch + NST - 1);
+          const uint32_t g = gch + (uint32_t)ch;
+          const int slot = (int)(g % NST);
+          mb_wait(&full[slot], (g / NST) & 1u);
+          const float* rb = sR + slot * CHL * LROW;
+          const double* ak = aRow + ch * DKC;
+          const double* lk = sLc + ch * DKC + tq;
+#pragma unroll
+          for (int s = 0; s < DKC / 4; ++s) {
+            const double lcg = lk[4 * s];
+            double a[6], b[NJ];
+#pragma unroll
+            for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24] - lcg;
+#pragma unroll
+            for (int m = 0; m < 6; ++m)
+#pragma unroll
+              for (int j = 0; j < NJ; ++j) dmma(c[m][j], a[m], b[j]);
+          }
+          __syncwarp();
+          if (lane == 0) mb_arrive(&empty[slot]);
+        }
+        gch += (uint32_t)nch;
+        __syncthreads();  // sA may be restaged for the next window chunk
+        continue;
+      }
+      // stage chunk ch (landmarks w0 + CHL ch .., atoms a0 .. a0 + DNA) into ring slot `slot`;
+      // out-of-range elements are zero-filled (their coefficients are zero too)
+      auto issue = [&](int ch, int slot) {
+        float* dst = sR + slot * CHL * LROW;
+#pragma unroll 4
+        for (int u = 0; u < LPT; ++u) {
+          const int e = tid + u * DNT;  // [0, CHL * 3 DNA)
+          const int q = e / (3 * DNA), r = e - q * (3 * DNA);
+          const int li = w0 + ch * CHL + q;
+          const bool ok = ch < nch && li < w0 + wn && a0 + r / 3 < n;
+          cp_async4(dst + q * LROW + r, lraw + ((int64_t)(ok ? li : 0) * n + (ok ? a0 : 0)) * 3 + (ok ? r : 0), ok);
+        }
+        cp_commit();
+      };
+#pragma unroll
+      for (int st = 0; st < NST - 1; ++st) issue(st, st);
       int slot = 0, fill = NST - 1;
       for (int ch = 0; ch < nch; ++ch) {
         cp_wait<NST - 2>();
@@ -240,8 +315,13 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         wk[j][e] = k < n ? w[k] : 0.0;
         wak[j][e] = k < n ? wa[k] : 0.0;
       }
-    cp_wait<0>();
-    __syncthreads();
+    if (VEC) {
+      mb_wait(xfull, xphase);
+      xphase ^= 1u;
+    } else {
+      cp_wait<0>();
+      __syncthreads();
+    }
 #pragma unroll
     for (int m = 0; m < 6; ++m) {
       const int r = m * 8 + gq;
