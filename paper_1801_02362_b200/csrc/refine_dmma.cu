@@ -26,7 +26,8 @@ constexpr int QSTAGE = (QF + QL) * QRS;              // floats per stage
 constexpr int QCS = 3 * QL + 1;                      // staged accumulator row stride (doubles)
 constexpr int QRING = QNST * QSTAGE * (int)sizeof(float);
 constexpr int QCBYTES = 3 * QF * QCS * (int)sizeof(double);
-constexpr int QSMEM = (QRING > QCBYTES ? QRING : QCBYTES) + QNST * QKC * (int)sizeof(double);
+constexpr int QSMEM = (QRING > QCBYTES ? QRING : QCBYTES) + QNST * QKC * (int)sizeof(double) +
+                      2 * QNST * (int)sizeof(uint64_t);
 constexpr int QLPT = (QF + QL) * 3 * QKC / QNT;     // 24 raw floats per thread per stage (scalar copies)
 constexpr int QV4 = 3 * QKC / 4;                     // 24 float4 per staged row
 constexpr int QVPT = (QF + QL) * QV4 / QNT;          // 6 float4 per thread per stage
@@ -46,6 +47,25 @@ __device__ __forceinline__ void cpa16(void* dst, const void* src, bool ok) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+// arrive on b once every cp.async this thread issued so far has landed
+__device__ __forceinline__ void mb_cp_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+          saddr(b)),
+      "r"(parity)
+      : "memory");
+}
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -78,6 +98,12 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
   float* ring = reinterpret_cast<float*>(qsm);                                     // [QNST][QF + QL][QRS]
   double* sC = reinterpret_cast<double*>(qsm);                                      // [3 QF][QCS] (after the K loop)
   double* sW = reinterpret_cast<double*>(qsm + (QRING > QCBYTES ? QRING : QCBYTES));  // [QNST][QKC]
+  // split-barrier ring: every thread's cp.async of a stage arrives on full[slot]
+  // (cp.async.mbarrier.arrive), each warp releases the slot on empty[slot]; a thread
+  // refills a slot once every warp has released it -- warps drift by up to QNST-2
+  // stages instead of meeting at a CTA barrier every stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(sW + QNST * QKC);
+  uint64_t* empty = full + QNST;
   __shared__ int s_t[QF], s_raw[QF], s_lo[QF], s_cnt[QF];
   __shared__ double s_fc[QF][3];
   __shared__ int s_wlo, s_whi;
@@ -116,6 +142,12 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
     fcA[i] = UNC ? 0.0 : s_fc[(mt & 3) * 8 + gq][mt >> 2];
   }
   const int nch = (n + QKC - 1) / QKC;
+  if (tid == 0) {
+    for (int i = 0; i < QNST; ++i) { mb_init(&full[i], QNT); mb_init(&empty[i], QNT / 32); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t gch = 0;  // stages issued by this CTA (ring position / parity)
   for (int l0 = wlo; l0 < whi; l0 += QL) {
     double lcB[3];
 #pragma unroll
@@ -126,6 +158,8 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
     }
     // ring stage ch: rows 0..31 frames, 32..63 landmarks, 3 QKC floats each (atoms QKC ch ..)
     auto issue = [&](int ch, int slot) {
+      const uint32_t g = gch + (uint32_t)ch;
+      if (g >= (uint32_t)QNST) mb_wait(&empty[slot], ((g / QNST) - 1) & 1u);
       float* dst = ring + slot * QSTAGE;
       const int k0 = ch * QKC;
       if (VEC) {
@@ -157,7 +191,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
         const bool ok = ch < nch && k0 + tid < n;
         cpa8(sW + slot * QKC + tid, w + (ok ? k0 + tid : 0), ok);
       }
-      cpa_commit();
+      mb_cp_arrive(&full[slot]);
     };
     double c[6][3][2];
 #pragma unroll
@@ -165,7 +199,8 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 #pragma unroll
       for (int j = 0; j < 3; ++j) c[i][j][0] = c[i][j][1] = 0.0;
 #pragma unroll
-    for (int st = 0; st < QNST - 1; ++st) issue(st, st);
+    for (int st = 0; st < QNST - 1; ++st)
+      if (st < nch) issue(st, (int)((gch + st) % QNST));
     // per-thread fragment offsets inside a stage (loop invariant)
     int offA[6], offB[3];
 #pragma unroll
@@ -178,12 +213,11 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
       const int nt = wn * 3 + i;
       offB[i] = (QF + (nt & 3) * 8 + gq) * QRS + 3 * tq + (nt >> 2);
     }
-    int slot = 0, fill = QNST - 1;
     for (int ch = 0; ch < nch; ++ch) {
-      cpa_wait<QNST - 2>();
-      __syncthreads();
-      issue(ch + QNST - 1, fill);
-      fill = fill + 1 == QNST ? 0 : fill + 1;
+      const uint32_t g = gch + (uint32_t)ch;
+      const int slot = (int)(g % QNST);
+      if (ch + QNST - 1 < nch) issue(ch + QNST - 1, (int)((g + QNST - 1) % QNST));
+      mb_wait(&full[slot], (g / QNST) & 1u);
       const float* sg = ring + slot * QSTAGE;
       const double* ww = sW + slot * QKC + tq;
 #pragma unroll
@@ -201,10 +235,11 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
 #pragma unroll
           for (int j = 0; j < 3; ++j) dmma884(c[i][j], a[i], b[j]);
       }
-      slot = slot + 1 == QNST ? 0 : slot + 1;
+      __syncwarp();
+      if (lane == 0) mb_arrive(&empty[slot]);
     }
-    cpa_wait<0>();
-    __syncthreads();
+    gch += (uint32_t)nch;
+    __syncthreads();  // every stage consumed: the accumulator staging below overlays the ring
     // stage accumulators: row (b, f) = mt * 8 + gq, column (g, l) = nt * 8 + 2 tq + e
 #pragma unroll
     for (int i = 0; i < 6; ++i)
