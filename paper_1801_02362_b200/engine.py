@@ -424,8 +424,10 @@ class PathCVTC:
             out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
                    "nsig": wres["nsig"]}
             if grad:
+                # gradient groups by significant span (the refine groups are by window start)
+                gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
                 out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap,
-                                                           perm, out_dtype, out_map=perm0)
+                                                           gperm, out_dtype, out_map=perm0)
             fflags = fs.flags if fs0 is None else torch.cat([fs.flags, fs0.flags])
             status = torch.stack([_flag_bits_dev(fflags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
                                   _flag_bits_dev(wres["flags"])])

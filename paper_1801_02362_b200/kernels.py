@@ -262,6 +262,16 @@ def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ou
     return ds, dz
 
 
+def sig_span_key(wres, L):
+    """Gradient grouping key of each frame: first + last significant landmark (frames
+    with similar significant spans land in the same 8-frame group, so the group's
+    landmark union -- the K extent of the gradient GEMM -- stays close to one span)."""
+    idx, ns = wres["sig_idx"], wres["nsig"].long()
+    first = idx[:, 0]
+    last = idx.gather(1, (ns - 1).clamp_min(0)[:, None])[:, 0]
+    return torch.where(ns > 0, first + last, torch.full_like(first, 2 * L)).contiguous()
+
+
 def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None):
     """Per-frame admissible landmark-tile hulls of the metric-pruned screen (csrc/prune.cu)."""
     T, C = Dc.shape
