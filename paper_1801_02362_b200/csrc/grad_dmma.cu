@@ -11,10 +11,14 @@
 // The vector kernel re-reads all 18 coefficients of a (frame, landmark) from
 // shared memory for every atom; here one A fragment (1 double per lane) feeds
 // 4 DMMAs and one B fragment 6, so the fp64 pipe rather than shared memory
-// sets the pace.  Coefficients are staged once per CTA (2048 atoms); the raw
-// fp32 landmark coordinates stream through a 6-stage cp.async ring (4
-// landmarks x 256 atoms per stage, coalesced) and are converted / centred
-// when a B fragment is read (once per 6 DMMAs).
+// sets the pace.  Coefficients are staged once per CTA (all atoms of a group when
+// there are enough groups); the raw fp32 landmark coordinates stream through a
+// 3-stage ring of 1-D TMA bulk copies (8 landmarks x 256 atoms per stage) and are
+// converted when a B fragment is read (once per 6 DMMAs).  B holds raw, not
+// centred, coordinates: the centroid term sum_kk A[r, kk] lc[kk] is one scalar
+// per GEMM row, subtracted in the epilogue (no fp64 add beside the DMMAs).
+#include <algorithm>
+
 #include "mc_math.cuh"
 
 namespace mc {
@@ -35,7 +39,6 @@ constexpr int NST = 3;             // cp.async ring stages
 constexpr int WAT = MC_GD_WAT;     // atoms per warp (n-tiles of 8)
 constexpr int NJ = WAT / 8;
 constexpr int DNT = 32 * (DNA / WAT);  // 16 warps: more warps in flight to hide the fragment-load latency
-constexpr int DATOMS = 2048;       // atoms per CTA
 constexpr int CHL = DKC / 3;       // landmarks per chunk
 constexpr int LPT = CHL * DNA * 3 / DNT;  // raw floats per thread per chunk
 constexpr int XPT = DG * DNA * 3 / DNT;  // frame floats per thread per sub-tile
@@ -99,7 +102,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
                     const double* __restrict__ wa, const int* __restrict__ sig_idx,
                     const double* __restrict__ sig_coef, const int* __restrict__ nsig,
                     const double* __restrict__ fvec, const int* __restrict__ perm, const int* __restrict__ out_map,
-                    OT* __restrict__ ds, OT* __restrict__ dz) {
+                    OT* __restrict__ ds, OT* __restrict__ dz, int apb) {
   extern __shared__ __align__(16) double dsm[];
   double* sA = dsm;                                       // [DR][AST] coefficients
   double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
@@ -113,6 +116,8 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   __shared__ int s_t[DG], s_raw[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
   __shared__ double s_fc[DG][3], s_fv[DG][8];
   __shared__ int s_wlo, s_whi;
+  __shared__ double s_bias[DR];
+  __shared__ int s_cum[DG + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;  // mma groupID / threadID_in_group
   if (tid < DG) {
@@ -139,6 +144,12 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     for (int f = 0; f < DG; ++f) { a = min(a, s_flo[f]); b = max(b, s_fhi[f]); }
     s_wlo = a;
     s_whi = b;
+    int tot = 0;
+    for (int f = 0; f < DG; ++f) {
+      s_cum[f] = tot;
+      tot += s_t[f] >= 0 ? s_ns[f] * 18 : 0;
+    }
+    s_cum[DG] = tot;
   }
   if (VEC) {
     if (tid == 0) {
@@ -155,11 +166,36 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   const bool restage = whi - wlo > DWMAX;
   uint32_t gch = 0, xphase = 0;  // VEC: chunks consumed by this CTA (ring position / parity)
   bool staged = false;
-  const int katom0 = blockIdx.y * DATOMS;
-  const int katom1 = min(n, katom0 + DATOMS);
+  const int katom0 = blockIdx.y * apb;
+  const int katom1 = min(n, katom0 + apb);
+  // VEC producer (thread 0).  Without restaging every sub-tile walks the same
+  // landmark window, so the chunk sequence runs on across sub-tiles: the next
+  // sub-tile's first chunks are in flight during this one's epilogue.
+  int pa0 = katom0, pch = 0, pw0 = wlo, pwn = min(DWMAX, whi - wlo);
+  uint32_t gprod = 0, plimit = 0;
+  auto produce_next = [&]() {
+    const uint32_t g = gprod++;
+    const int slot = (int)(g % NST);
+    if (g >= (uint32_t)NST) mb_wait(&empty[slot], ((g / NST) - 1) & 1u);
+    const int natp = min(DNA, n - pa0);
+    const int q1 = min(CHL, pwn - pch * CHL);
+    mb_expect(&full[slot], (uint32_t)(q1 * 12 * natp));
+    float* dst = sR + slot * CHL * LROW;
+    for (int q = 0; q < q1; ++q)
+      bulk_g2s(dst + q * LROW, lraw + ((int64_t)(pw0 + pch * CHL + q) * n + pa0) * 3, 12 * natp, &full[slot]);
+    if (++pch * CHL >= pwn) {
+      pch = 0;
+      pa0 += DNA;
+    }
+  };
+  if (VEC && !restage && tid == 0 && whi > wlo) {
+    const int nchw = (3 * pwn + DKC - 1) / DKC;
+    plimit = (uint32_t)(((katom1 - katom0 + DNA - 1) / DNA) * nchw);
+    while (gprod < plimit && gprod < (uint32_t)(NST - 1)) produce_next();
+  }
   for (int a0 = katom0; a0 < katom1; a0 += DNA) {
-    // the epilogue's frame coordinates: one cp.async group issued now, long
-    // complete by the time the contraction below has finished
+    // the epilogue's frame coordinates: issued now, long complete by the time
+    // the contraction below has finished
     const int nat = min(DNA, n - a0);  // valid atoms of this sub-tile
     if (VEC) {
       if (tid == 0) {
@@ -187,30 +223,45 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       for (int j = 0; j < NJ; ++j) c[m][j][0] = c[m][j][1] = 0.0;
     for (int w0 = wlo; w0 < whi; w0 += DWMAX) {
       const int wn = min(DWMAX, whi - w0);
+      const int nch = (3 * wn + DKC - 1) / DKC;
+      if (VEC && restage && tid == 0) {  // the producer covers this (a0, w0) block only
+        pa0 = a0, pch = 0, pw0 = w0, pwn = wn;
+        plimit = gch + (uint32_t)nch;
+        while (gprod < plimit && gprod < gch + (uint32_t)(NST - 1)) produce_next();
+      }
       if (restage || !staged) {  // block-uniform
         staged = true;
         __syncthreads();
         for (int e = tid; e < DR * AST; e += DNT) sA[e] = 0.0;
         for (int e = tid; e < DKMAX; e += DNT) sLc[e] = e < 3 * wn ? lcen[3 * w0 + e] : 0.0;
         __syncthreads();
-        for (int f = 0; f < DG; ++f) {
-          const int t = s_t[f];
-          if (t < 0) continue;
-          const int ns = s_ns[f];
-          const int* idx = sig_idx + (int64_t)t * cap;
-          const double* co = sig_coef + (int64_t)t * cap * 18;
-          for (int e = tid; e < ns * 18; e += DNT) {
-            const int s = e / 18, e18 = e - s * 18;
-            const int l = idx[s] - w0;
-            if (l >= 0 && l < wn) {
-              const int sz = e18 / 9, b = (e18 % 9) / 3, g = e18 % 3;
-              sA[(f * 6 + sz * 3 + b) * AST + l * 3 + g] = co[e];
-            }
+        // coefficient scatter, all frames at once (independent loads in flight)
+        const int tot = s_cum[DG];
+#pragma unroll 4
+        for (int e = tid; e < tot; e += DNT) {
+          int f = 0;
+#pragma unroll
+          for (int q = 1; q < DG; ++q) f += e >= s_cum[q];
+          const int t = s_t[f], el = e - s_cum[f];
+          const int s = el / 18, e18 = el - s * 18;
+          const int l = sig_idx[(int64_t)t * cap + s] - w0;
+          const double v = sig_coef[((int64_t)t * cap + s) * 18 + e18];
+          if (l >= 0 && l < wn) {
+            const int sz = e18 / 9, b = (e18 % 9) / 3, g = e18 % 3;
+            sA[(f * 6 + sz * 3 + b) * AST + l * 3 + g] = v;
           }
         }
         __syncthreads();
+        // centroid term of the contraction (B holds raw coordinates):
+        // bias_r = sum_kk A[r, kk] lc[kk], subtracted in the epilogue
+        for (int r = warp; r < DR; r += DNT / 32) {
+          double acc = 0.0;
+          for (int kk = lane; kk < 3 * wn; kk += 32) acc += sA[r * AST + kk] * sLc[kk];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) s_bias[r] = (w0 == wlo ? 0.0 : s_bias[r]) + acc;
+        }
       }
-      const int nch = (3 * wn + DKC - 1) / DKC;
       // loop-invariant fragment offsets: B element (kk = 4 s + tq -> landmark q, axis g)
       int offB[DKC / 4];
 #pragma unroll
@@ -220,35 +271,21 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       }
       const double* aRow = sA + gq * AST + tq;
       if constexpr (VEC) {
-        // producer (thread 0): chunk ch -> ring slot (gch + ch) % NST once every warp released it
-        auto produce = [&](int ch) {
-          const uint32_t g = gch + (uint32_t)ch;
-          const int slot = (int)(g % NST);
-          if (g >= (uint32_t)NST) mb_wait(&empty[slot], ((g / NST) - 1) & 1u);
-          const int q1 = min(CHL, wn - ch * CHL);
-          mb_expect(&full[slot], (uint32_t)(q1 * 12 * nat));
-          float* dst = sR + slot * CHL * LROW;
-          for (int q = 0; q < q1; ++q)
-            bulk_g2s(dst + q * LROW, lraw + ((int64_t)(w0 + ch * CHL + q) * n + a0) * 3, 12 * nat, &full[slot]);
-        };
-        if (tid == 0)
-          for (int ch = 0; ch < min(nch, NST - 1); ++ch) produce(ch);
         for (int ch = 0; ch < nch; ++ch) {
-          if (tid == 0 && ch + NST - 1 < nch) produce(ch + NST - 1);
           const uint32_t g = gch + (uint32_t)ch;
+          if (tid == 0)
+            while (gprod < plimit && gprod < g + (uint32_t)NST) produce_next();
           const int slot = (int)(g % NST);
           mb_wait(&full[slot], (g / NST) & 1u);
           const float* rb = sR + slot * CHL * LROW;
           const double* ak = aRow + ch * DKC;
-          const double* lk = sLc + ch * DKC + tq;
 #pragma unroll
           for (int s = 0; s < DKC / 4; ++s) {
-            const double lcg = lk[4 * s];
             double a[6], b[NJ];
 #pragma unroll
             for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24] - lcg;
+            for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24];
 #pragma unroll
             for (int m = 0; m < 6; ++m)
 #pragma unroll
@@ -285,15 +322,13 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         fill = fill + 1 == NST ? 0 : fill + 1;
         const float* rb = sR + slot * CHL * LROW;
         const double* ak = aRow + ch * DKC;
-        const double* lk = sLc + ch * DKC + tq;
 #pragma unroll
         for (int s = 0; s < DKC / 4; ++s) {
-          const double lcg = lk[4 * s];
           double a[6], b[NJ];
 #pragma unroll
           for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24] - lcg;
+          for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24];
 #pragma unroll
           for (int m = 0; m < 6; ++m)
 #pragma unroll
@@ -329,6 +364,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       const int t = s_t[f];
       if (t < 0) continue;
       const double cx = s_fc[f][b], sc = s_fv[f][sz], corr = s_fv[f][2 + sz * 3 + b];
+      const double bias = s_bias[r];
       OT* __restrict__ out = sz ? dz : ds;
       const int tout = s_raw[f];
       const float* xs = sX + f * 3 * DNA + b;
@@ -340,7 +376,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
           const int k = a0 + al;
           if (k >= n) continue;
           const double x = (double)xs[3 * al] - cx;
-          out[((int64_t)tout * n + k) * 3 + b] = (OT)(2.0 * wk[j][e] * (sc * x - c[m][j][e]) - wak[j][e] * corr);
+          out[((int64_t)tout * n + k) * 3 + b] = (OT)(2.0 * wk[j][e] * (sc * x - (c[m][j][e] - bias)) - wak[j][e] * corr);
         }
     }
     __syncthreads();  // sX is refilled by the next sub-tile
@@ -352,7 +388,21 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
                                 const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream) {
   if (T <= 0 || n <= 0) return cudaSuccess;
-  dim3 grid((T + DG - 1) / DG, (n + DATOMS - 1) / DATOMS);
+  // atoms per CTA: all of them when there are enough frame groups to fill the
+  // machine (the coefficient staging is then paid once per group), else split
+  // the atoms over grid.y until ~4 CTAs per SM exist
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int groups = (T + DG - 1) / DG;
+  const int tiles = (n + DNA - 1) / DNA;
+  const int nyb = std::max(1, std::min(tiles, (4 * sms + groups - 1) / groups));
+  const int apb = ((tiles + nyb - 1) / nyb) * DNA;
+  dim3 grid(groups, (n + apb - 1) / apb);
   static bool attr = false;
   if (!attr) {
     for (const void* fn : {(const void*)cv_grad_dmma_kernel<float, true>, (const void*)cv_grad_dmma_kernel<float, false>,
@@ -367,7 +417,7 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
 #define MC_GD_LAUNCH(OTT, V)                                                                                         \
   cv_grad_dmma_kernel<OTT, V><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,     \
                                                             sig_coef, nsig, fvec, perm, out_map, (OTT*)ds,     \
-                                                            (OTT*)dz)
+                                                            (OTT*)dz, apb)
   if (out_f32) {
     if (vec) MC_GD_LAUNCH(float, true); else MC_GD_LAUNCH(float, false);
   } else {
