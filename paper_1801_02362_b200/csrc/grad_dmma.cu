@@ -18,6 +18,7 @@
 // centred, coordinates: the centroid term sum_kk A[r, kk] lc[kk] is one scalar
 // per GEMM row, subtracted in the epilogue (no fp64 add beside the DMMAs).
 #include <algorithm>
+#include <type_traits>
 
 #include "mc_math.cuh"
 
@@ -271,6 +272,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       }
       const double* aRow = sA + gq * AST + tq;
       if constexpr (VEC) {
+        const bool wact = a0 + warp * WAT < n;
         for (int ch = 0; ch < nch; ++ch) {
           const uint32_t g = gch + (uint32_t)ch;
           if (tid == 0)
@@ -279,17 +281,34 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
           mb_wait(&full[slot], (g / NST) & 1u);
           const float* rb = sR + slot * CHL * LROW;
           const double* ak = aRow + ch * DKC;
+          // KS k-steps of 4 kk; full chunks take the KS = 6 path, a partial last
+          // chunk only the k-steps that hold window landmarks
+          auto contract = [&](auto ks) {
+            constexpr int KS = decltype(ks)::value;
 #pragma unroll
-          for (int s = 0; s < DKC / 4; ++s) {
-            double a[6], b[NJ];
+            for (int s = 0; s < KS; ++s) {
+              double a[6], b[NJ];
 #pragma unroll
-            for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
+              for (int m = 0; m < 6; ++m) a[m] = ak[m * 8 * AST + 4 * s];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24];
+              for (int j = 0; j < NJ; ++j) b[j] = (double)rb[offB[s] + j * 24];
 #pragma unroll
-            for (int m = 0; m < 6; ++m)
+              for (int m = 0; m < 6; ++m)
 #pragma unroll
-              for (int j = 0; j < NJ; ++j) dmma(c[m][j], a[m], b[j]);
+                for (int j = 0; j < NJ; ++j) dmma(c[m][j], a[m], b[j]);
+            }
+          };
+          // warps whose atoms all lie past n skip the contraction
+          const int ksteps = wact ? (3 * min(CHL, wn - ch * CHL) + 3) / 4 : 0;
+          static_assert(DKC / 4 == 6, "k-step dispatch below assumes 6 k-steps per chunk");
+          switch (ksteps) {
+            case 6: contract(std::integral_constant<int, 6>{}); break;
+            case 5: contract(std::integral_constant<int, 5>{}); break;
+            case 4: contract(std::integral_constant<int, 4>{}); break;
+            case 3: contract(std::integral_constant<int, 3>{}); break;
+            case 2: contract(std::integral_constant<int, 2>{}); break;
+            case 1: contract(std::integral_constant<int, 1>{}); break;
+            default: break;
           }
           __syncwarp();
           if (lane == 0) mb_arrive(&empty[slot]);
