@@ -109,7 +109,9 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
   __shared__ int s_wlo, s_whi;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;  // rows: m-tiles 6 wm .. +6; columns: n-tiles 3 wn .. +3
+  // rows: m-tiles 6 wm .. +6; columns: landmarks 8 wn .. +8, all three axes (n-tile j = axis j),
+  // so a partial last sub-tile idles whole warps (their DMMA share goes to the co-resident CTA)
+  const int wm = warp & 1, wn = warp >> 1;
   if (tid < QF) {
     const int k = blockIdx.x * QF + tid;
     int t = -1, a = 0, c = 0;
@@ -152,10 +154,10 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
     double lcB[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const int nt = wn * 3 + i;
-      const int l = l0 + (nt & 3) * 8 + gq;
-      lcB[i] = (!RAW && l < L) ? lc[3 * l + (nt >> 2)] : 0.0;
+      const int l = l0 + wn * 8 + gq;
+      lcB[i] = (!RAW && l < L) ? lc[3 * l + i] : 0.0;
     }
+    const bool wact = l0 + wn * 8 < whi;  // this warp's landmarks intersect the window union
     // ring stage ch: rows 0..31 frames, 32..63 landmarks, 3 QKC floats each (atoms QKC ch ..)
     auto issue = [&](int ch, int slot) {
       const uint32_t g = gch + (uint32_t)ch;
@@ -209,10 +211,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
       offA[i] = ((mt & 3) * 8 + gq) * QRS + 3 * tq + (mt >> 2);
     }
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const int nt = wn * 3 + i;
-      offB[i] = (QF + (nt & 3) * 8 + gq) * QRS + 3 * tq + (nt >> 2);
-    }
+    for (int i = 0; i < 3; ++i) offB[i] = (QF + wn * 8 + gq) * QRS + 3 * tq + i;
     for (int ch = 0; ch < nch; ++ch) {
       const uint32_t g = gch + (uint32_t)ch;
       const int slot = (int)(g % QNST);
@@ -221,7 +220,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
       const float* sg = ring + slot * QSTAGE;
       const double* ww = sW + slot * QKC + tq;
 #pragma unroll
-      for (int s = 0; s < QKC / 4; ++s) {
+      for (int s = 0; s < (wact ? QKC / 4 : 0); ++s) {
         const double wj = RAW ? 1.0 : ww[4 * s];
         double a[6], b[3];
 #pragma unroll
@@ -240,12 +239,12 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
     }
     gch += (uint32_t)nch;
     __syncthreads();  // every stage consumed: the accumulator staging below overlays the ring
-    // stage accumulators: row (b, f) = mt * 8 + gq, column (g, l) = nt * 8 + 2 tq + e
+    // stage accumulators: row (b, f) = mt * 8 + gq, column (g, l) = g QL + 8 wn + 2 tq + e
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        const int row = (wm * 6 + i) * 8 + gq, col = (wn * 3 + j) * 8 + 2 * tq;
+        const int row = (wm * 6 + i) * 8 + gq, col = j * QL + wn * 8 + 2 * tq;
         sC[row * QCS + col] = c[i][j][0];
         sC[row * QCS + col + 1] = c[i][j][1];
       }

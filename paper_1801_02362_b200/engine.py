@@ -416,7 +416,8 @@ class PathCVTC:
             lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
                                               fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0,
                                               rlo=rlo, rhi=rhi)
-            perm = K.sort_by_key(lo, self.L)
+            # refine groups: frames sorted by window centre (32-frame unions stay tight)
+            perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
             Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
                                         fmap=perm0, wuni=self.wuni)
             wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,

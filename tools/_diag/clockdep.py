@@ -10,7 +10,7 @@ pcv = engine.PathCVTC(torch.from_numpy(wl.landmarks).to(dev), wl.lam, wl.q)
 Dest, fr, fs, fs0, rlo, rhi, perm0 = pcv._pruned_estimate(wl.frames)
 cap = pcv.window_cap
 lo, cnt, _, _ = K.candidates(Dest, pcv.lam, pcv.cutoff + pcv.margin, cap, fnorm=fs.opnorm, fcoef=pcv.fcoef, rlo=rlo, rhi=rhi)
-perm = K.sort_by_key(lo, pcv.L)
+perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * pcv.L + 1)
 def rf():
     return K.refine(fr, fs, pcv.lraw, pcv.ls, pcv.w, perm=perm, lo=lo, cnt=cnt, cap=cap, fmap=perm0, wuni=pcv.wuni)
 Dex, Rex, _ = rf()
