@@ -13,6 +13,8 @@ norms, moments) across calls, the way a metadynamics run reuses it every step.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -25,9 +27,13 @@ from .errors import ConfigError, DegenerateFitError, EmptyActiveSetError, Invali
 # landmarks change Z by < 1.1e-7 relative.
 DEFAULT_CUTOFF = 25.0
 # window-selection estimate of PathCVTC.evaluate (env MC_SCREEN: "f16x1" | "split")
-SCREEN = __import__("os").environ.get("MC_SCREEN", "f16x1")
+SCREEN = os.environ.get("MC_SCREEN", "f16x1")
 # metric pruning of the one-term screen (env MC_PRUNE=0 disables)
-PRUNE = __import__("os").environ.get("MC_PRUNE", "1") == "1"
+PRUNE = os.environ.get("MC_PRUNE", "1") == "1"
+# CTAs of the screening GEMM (0: one per SM).  Fewer CTAs draw less power: the
+# tensor-core screen otherwise trips the board's power cap, and the clock
+# recovery after it slows the fp64 kernels that follow.
+K2_GRID = int(os.environ.get("MC_K2_GRID", "0"))
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 
 
@@ -388,7 +394,7 @@ class PathCVTC:
         frames.  Returns the estimate (sorted rows), the caller's raw frames, the sorted
         split, the unsorted split, the row ranges and perm0 (sorted position -> frame)."""
         fr0, fs0 = self._frames(frames, 1, check=False)
-        Dc = K.msd_estimate(fs0, self.ls_coarse)
+        Dc = K.msd_estimate(fs0, self.ls_coarse, grid=K2_GRID)
         hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.c_unit, self.mind,
                                      (self.cutoff + 2.0) / self.lam, self.knear)
         ntl = self.mind.shape[1]
@@ -398,7 +404,7 @@ class PathCVTC:
         fss = K.gather_split(fs0, perm0)
         tlist, nlist, rlo, rhi = K.band_tiles(perm0, hlo, hhi, 128, 48, self.L, ntl)
         Dest = torch.empty((fr0.shape[0], self.L), dtype=torch.float32, device=self.device)
-        K.msd_estimate(fss, self.ls, Dest, tlist=tlist, nlist=nlist)
+        K.msd_estimate(fss, self.ls, Dest, grid=K2_GRID, tlist=tlist, nlist=nlist)
         self._last_tiles = nlist
         return Dest, fr0, fss, fs0, rlo, rhi, perm0
 

@@ -40,5 +40,23 @@ for name, fn in (("refine", rf), ("grad", gr), ("k2", k2)):
     for _ in range(8): fn()
     b.record(); torch.cuda.synchronize()
     res[name + "_b2b_avg"] = a.elapsed_time(b) / 8
+# pipeline order: K2 -> refine -> grad, each timed on the stream
+time.sleep(2.0)
+seq = []
+for _ in range(6):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(); k2(); ev[1].record(); rf(); ev[2].record(); gr(); ev[3].record()
+    seq.append(ev)
+torch.cuda.synchronize()
+res["pipe_k2"] = [e[0].elapsed_time(e[1]) for e in seq]
+res["pipe_refine"] = [e[1].elapsed_time(e[2]) for e in seq]
+res["pipe_grad"] = [e[2].elapsed_time(e[3]) for e in seq]
+# refine after an idle gap following K2
+seq = []
+for _ in range(4):
+    k2(); torch.cuda.synchronize(); time.sleep(0.5)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); rf(); b.record(); torch.cuda.synchronize(); seq.append(a.elapsed_time(b))
+res["refine_after_k2_gap"] = seq
 smi.terminate()
 print(json.dumps({k: (np.round(v, 1).tolist() if isinstance(v, list) else round(v, 1)) for k, v in res.items()}))
