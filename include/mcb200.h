@@ -223,19 +223,22 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
                   double fcoef, const int32_t* rlo, const int32_t* rhi, int32_t cap, int32_t* lo, int32_t* cnt,
                   float* dmin, uint8_t* flags, void* stream);
 /* Metric pruning of the screen (csrc/prune.cu):
- * mc_prune_plan: from the one-term estimate Dc [T, C] against a coarse landmark subset,
- *   its error bound c_unit * fnorm[t] * cnorm[c], and mind [C, ntl] = min over each
- *   48-landmark tile of the exact RMSD coarse->landmark, the hull [hull_lo, hull_hi) of
- *   landmark tiles that can hold a landmark within cutoff of D_min (thr = cutoff / lam,
- *   D units; knear <= 8 nearest coarse landmarks; C <= 1024) and a sort key (0: hull
- *   >= `wide` tiles, else 1 + hull_lo).
+ * mc_prune_plan: from the one-term estimate Dc [T, C] against a coarse landmark subset
+ *   (coarse landmark c = landmark c * cstride), its error bound c_unit * fnorm[t] * cnorm[c],
+ *   and mind / maxd [C, ntl] = min / max over each 48-landmark tile of the exact RMSD
+ *   coarse->landmark, the hull [hull_lo, hull_hi) of landmark tiles that can hold a
+ *   landmark within cutoff of D_min (thr = cutoff / lam, D units; knear <= 8 nearest
+ *   coarse landmarks; C <= 1024) and a sort key (0: hull >= `wide` tiles, else
+ *   1 + hull_lo).  Both triangle bounds d(t,l) >= d(c,l) - d(t,c) (knear nearest c) and
+ *   d(t,l) >= d(t,c) - d(c,l) (c within one tile of the landmark tile; maxd nullable =
+ *   first bound only) are applied; requires equal alignment / displacement weights.
  * mc_band_tiles: for the key-sorted order perm, the union hull of each 128-frame band,
  *   the (band, landmark tile) list tlist [*, 2] with its length *nlist (device), and each
  *   sorted row's landmark range [row_lo, row_hi) for mc_candidates(rlo, rhi).
  * mc_gather_rows: dst[r] = src[idx[r]] for rows of rowlen elements of esz bytes. */
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
-                  double c_unit, const float* mind, int32_t ntl, double thr, int32_t knear, int32_t wide,
-                  int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream);
+                  double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
+                  int32_t knear, int32_t wide, int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream);
 int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,
                   int32_t BL, int32_t L, int32_t* tlist, int32_t* nlist, int32_t* row_lo, int32_t* row_hi,
                   void* stream);

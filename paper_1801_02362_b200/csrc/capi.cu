@@ -202,14 +202,14 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
 }
 
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
-                  double c_unit, const float* mind, int32_t ntl, double thr, int32_t knear, int32_t wide,
-                  int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream) {
+                  double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
+                  int32_t knear, int32_t wide, int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream) {
   if (T < 0 || C < 1 || C > 1024 || lddc < C || ntl < 1 || knear < 1 || knear > 8 || !(c_unit >= 0.0) ||
-      !(thr >= 0.0))
+      !(thr >= 0.0) || (maxd && cstride < 1))
     return MC_ERR_CONFIG;
   if (T > 0 && (!Dc || !fnorm || !cnorm || !mind || !hull_lo || !hull_hi || !key)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, c_unit, mind, ntl, thr, knear, wide, hull_lo,
-                                           hull_hi, key, S_(stream)));
+  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, c_unit, mind, maxd, cstride, ntl, thr, knear,
+                                           wide, hull_lo, hull_hi, key, S_(stream)));
 }
 
 int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,

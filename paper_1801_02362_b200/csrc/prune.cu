@@ -12,7 +12,13 @@
 // and Dmin_ub(t) = min_c (Dc + e_tc) >= min_l D(t, l).  A tile with
 // LB > Dmin_ub + cutoff / lambda holds no landmark of weight >= e^-cutoff, so
 // it is dropped: identical significant sets, truncated mass below the existing
-// window bound.  prune_plan_kernel emits each frame's admissible tile hull
+// window bound.  The other side of the triangle, d(t, l) >= d(t, c) - d(c, l),
+// with dlo = sqrt(max(0, Dc - e_tc)) and maxd[c, tau] = max_{l in tau} d(c, l)
+// over the coarse landmarks within one tile of tau, gives
+//     LB2(t, tau) = max_c max(0, dlo(t, c) - maxd[c, tau])^2,
+// which prunes the far side of the path for every frame (a frame far from the
+// coarse landmarks around a tile is far from the whole tile); config 4: mean
+// hull 34.7 -> 3.7 tiles, screened tiles 25% -> 5.7% (tools/_diag/prune2.py).  prune_plan_kernel emits each frame's admissible tile hull
 // [lo, hi); frames are then sorted by hull start (wide hulls first), banded
 // into 128-frame tiles, and band_tiles_kernel lists the (frame tile, landmark
 // tile) pairs the tensor-core kernel computes.
@@ -27,8 +33,9 @@ constexpr int KNEAR_MAX = 8;
 
 __global__ void __launch_bounds__(PNT)
 prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, const double* __restrict__ fnorm,
-                  const double* __restrict__ cnorm, double c_unit, const float* __restrict__ mind, int ntl, double thr,
-                  int knear, int wide, int* __restrict__ hull_lo, int* __restrict__ hull_hi, int* __restrict__ key) {
+                  const double* __restrict__ cnorm, double c_unit, const float* __restrict__ mind,
+                  const float* __restrict__ maxd, int cstride, int ntl, double thr, int knear, int wide,
+                  int* __restrict__ hull_lo, int* __restrict__ hull_hi, int* __restrict__ key) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (PNT / 32) + (threadIdx.x >> 5);
   if (t >= T) return;
@@ -70,6 +77,17 @@ prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, cons
       if (near[k] >= C) continue;
       const double g = fmax(0.0, (double)mind[(int64_t)near[k] * ntl + tau] - dhi[k]);
       lb = fmax(lb, g * g);
+    }
+    if (maxd) {
+      // far side: d(t,l) >= d_lo(t,c) - maxd[c,tau] for the coarse landmarks within one
+      // tile of tau (a frame far from them is far from the whole tile)
+      const int c0 = max(0, (tau * 48 - 48 + cstride - 1) / cstride);
+      const int c1 = min(C - 1, (tau * 48 + 95) / cstride);
+      for (int c = c0; c <= c1; ++c) {
+        const double dlo = sqrt(fmax(0.0, (double)row[c] - ef * cnorm[c]));
+        const double g = fmax(0.0, dlo - (double)maxd[(int64_t)c * ntl + tau]);
+        lb = fmax(lb, g * g);
+      }
     }
     if (lb <= lim) { lo = min(lo, tau); hi = max(hi, tau); }
   }
@@ -157,12 +175,12 @@ __global__ void gather_rows_kernel(const E* __restrict__ src, int64_t rowlen, co
 }
 
 cudaError_t launch_prune_plan(const float* Dc, int T, int C, int64_t lddc, const double* fnorm, const double* cnorm,
-                              double c_unit, const float* mind, int ntl, double thr, int knear, int wide,
-                              int* hull_lo, int* hull_hi, int* key, cudaStream_t stream) {
+                              double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
+                              int knear, int wide, int* hull_lo, int* hull_hi, int* key, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
   if (knear > KNEAR_MAX) knear = KNEAR_MAX;
-  prune_plan_kernel<<<(T + PNT / 32 - 1) / (PNT / 32), PNT, 0, stream>>>(Dc, T, C, lddc, fnorm, cnorm, c_unit, mind,
-                                                                         ntl, thr, knear, wide, hull_lo, hull_hi, key);
+  prune_plan_kernel<<<(T + PNT / 32 - 1) / (PNT / 32), PNT, 0, stream>>>(
+      Dc, T, C, lddc, fnorm, cnorm, c_unit, mind, maxd, cstride, ntl, thr, knear, wide, hull_lo, hull_hi, key);
   return cudaGetLastError();
 }
 

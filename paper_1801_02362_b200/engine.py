@@ -279,7 +279,7 @@ class PathCVTC:
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None, screen=None, prune=None, coarse_stride=16, knear=4):
+                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4):
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
         self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
@@ -334,7 +334,9 @@ class PathCVTC:
         # metric pruning of the screen: one-term screen only,
         # worthwhile when there are many landmark tiles
         ntl = (self.L + 47) // 48
-        self.prune = (PRUNE if prune is None else bool(prune)) and self.screen == "f16x1" and ntl >= 16
+        # (RMSD is a pseudometric only when one weight vector both aligns and measures)
+        self.prune = ((PRUNE if prune is None else bool(prune)) and self.screen == "f16x1" and ntl >= 16
+                      and bool(torch.equal(self.w, self.wa)))
         if self.prune:
             self._init_prune(int(coarse_stride), int(knear))
 
@@ -351,9 +353,16 @@ class PathCVTC:
         _, _, flags = K.refine(lc, fsc, self.lraw, self.ls, self.w, Dd=dcl)
         _raise_flags(flags, "metric pruning: landmark distances")
         ntl = (self.L + 47) // 48
-        rm = dcl.double().clamp_min(0.0).mul_(1.0 - 1e-6).sqrt_()
-        rm = torch.nn.functional.pad(rm, (0, ntl * 48 - self.L), value=float("inf"))
-        self.mind = rm.view(rm.shape[0], ntl, 48).amin(2).float().contiguous()
+        # exact RMSDs, widened for the fp32 storage of D and the fp64 cancellation near 0
+        rm = dcl.double().clamp_min(0.0).sqrt_()
+        lo_ = (rm * (1.0 - 1e-6) - 1e-6).clamp_min_(0.0)
+        hi_ = rm * (1.0 + 1e-6) + 1e-6
+        pad = ntl * 48 - self.L
+        lo_ = torch.nn.functional.pad(lo_, (0, pad), value=float("inf"))
+        hi_ = torch.nn.functional.pad(hi_, (0, pad), value=0.0)
+        self.mind = lo_.view(lo_.shape[0], ntl, 48).amin(2).float().contiguous()
+        self.maxd = hi_.view(hi_.shape[0], ntl, 48).amax(2).float().contiguous()
+        self.cstride = stride
         self.knear = max(1, min(8, knear))
 
     def _lsplit(self, terms):
@@ -396,7 +405,7 @@ class PathCVTC:
         fr0, fs0 = self._frames(frames, 1, check=False)
         Dc = K.msd_estimate(fs0, self.ls_coarse, grid=K2_GRID)
         hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.c_unit, self.mind,
-                                     (self.cutoff + 2.0) / self.lam, self.knear)
+                                     (self.cutoff + 2.0) / self.lam, self.knear, maxd=self.maxd, cstride=self.cstride)
         ntl = self.mind.shape[1]
         perm0 = K.sort_by_key(key, ntl + 1)
         # sorted view of the split (operand rows + scalars gathered, no second split); the

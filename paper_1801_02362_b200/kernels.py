@@ -272,7 +272,7 @@ def sig_span_key(wres, L):
     return torch.where(ns > 0, first + last, torch.full_like(first, 2 * L)).contiguous()
 
 
-def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None):
+def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None, maxd=None, cstride=0):
     """Per-frame admissible landmark-tile hulls of the metric-pruned screen (csrc/prune.cu)."""
     T, C = Dc.shape
     ntl = mind.shape[1]
@@ -281,8 +281,8 @@ def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None):
     hhi = torch.empty((T,), dtype=I32, device=dev)
     key = torch.empty((T,), dtype=I32, device=dev)
     wide = max(1, (3 * ntl) // 4) if wide is None else int(wide)
-    call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), float(c_unit), ptr(mind), ntl,
-         float(thr), int(knear), wide, ptr(hlo), ptr(hhi), ptr(key), stream_ptr())
+    call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), float(c_unit), ptr(mind), ptr(maxd),
+         int(cstride), ntl, float(thr), int(knear), wide, ptr(hlo), ptr(hhi), ptr(key), stream_ptr())
     return hlo, hhi, key
 
 
