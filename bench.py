@@ -319,24 +319,67 @@ class ConfigTC:
         return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
 
     def e2e_chunks(self):
-        """Chunk boundaries of the streamed step: sizes ramp up geometrically (x1.5
-        from chunk/6 to chunk) so only a small first copy is exposed, while each
-        chunk's compute (~2.7 us/frame on config 4) covers the next chunk's copy
-        (~2.2 us/frame at 55 GB/s); large steady chunks keep the pruning bands and
-        the window-sorted frame groups of the refine/gradient kernels tight
-        (schedule sweep: tools/_diag/e2e_sched.py)."""
-        env = os.environ.get("MC_E2E_CHUNKS")  # "first,steady[,growth]" (measurement knob)
-        first, steady, growth = self.chunk // 6, self.chunk, 1.5
+        """Chunk boundaries of the streamed step.  The H2D copy (2.16 us/frame at
+        55.6 GB/s) is slower than the compute (~2.5 ms + 1.72 us/frame per chunk on
+        config 4), so the step is copy-bound and ends one chunk-compute after the
+        last copy: chunk sizes shrink geometrically (x0.87) towards a last chunk of
+        T/16, so each chunk's compute finishes under the next chunk's copy and only
+        a small compute is exposed at the end, while chunks stay large enough for
+        the pruning bands and frame groups to stay tight (sweeps:
+        tools/_diag/e2e_sched.py, tools/_diag/e2e_timeline.py)."""
+        env = os.environ.get("MC_E2E_CHUNKS")  # "first,steady[,growth[,taper]]" | "list:n1,n2,..." (knob)
+        if not env:
+            tail = [max(1024, (self.T // 16) // 32 * 32)]
+            while sum(tail) < self.T:
+                nxt = int(tail[-1] / 0.87) // 32 * 32
+                tail.append(min(nxt, self.T - sum(tail)))
+            out, c0 = [], 0
+            for n in reversed(tail):
+                out.append((c0, n))
+                c0 += n
+            return out
+        first, steady, growth, taper = self.chunk // 6, self.chunk, 1.5, True
+        if env and env.startswith("list:"):
+            sizes = [int(x) for x in env[5:].split(",")]
+            out, c0 = [], 0
+            for n in sizes:
+                n = min(n, self.T - c0)
+                if n <= 0:
+                    break
+                out.append((c0, n))
+                c0 += n
+            if c0 < self.T:
+                out.append((c0, self.T - c0))
+            return out
         if env:
             parts = [float(x) for x in env.split(",")]
             first, steady = int(parts[0]), int(parts[1])
             growth = parts[2] if len(parts) > 2 else 2.0
-        out, c0, size = [], 0, max(1, first)
-        while c0 < self.T:
-            n = min(int(size), self.T - c0)
+            taper = bool(int(parts[3])) if len(parts) > 3 else True
+        ramp, size = [], max(1, first)
+        while size < steady:
+            ramp.append(int(size))
+            size = max(size + 1, int(size * growth))
+        head, tail = list(ramp), (list(reversed(ramp)) if taper else [])
+        sizes, left = [], self.T
+        while left > 0:
+            if head:
+                n = head.pop(0)
+            elif left > sum(tail) + steady:
+                n = steady
+            elif tail and left > sum(tail):
+                n = left - sum(tail)
+            elif tail:
+                n = tail.pop(0)
+            else:
+                n = steady
+            n = min(n, left)
+            sizes.append(n)
+            left -= n
+        out, c0 = [], 0
+        for n in sizes:
             out.append((c0, n))
             c0 += n
-            size = min(steady, max(size + 1, int(size * growth)))
         return out
 
     def step_e2e(self):

@@ -11,6 +11,8 @@
 // stage, 16-byte copies when N % 4 == 0); each fragment is centred / weighted
 // in registers when it is read.  The accumulators are then staged through shared memory so one
 // thread owns whole 3x3 blocks for the fit epilogue.
+#include <algorithm>
+
 #include "mc_math.cuh"
 
 namespace mc {
@@ -93,7 +95,8 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
                    double wuni,
                    const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,
                    const int* __restrict__ lo, const int* __restrict__ cnt, int cap, double* __restrict__ Dex,
-                   double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
+                   double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags,
+                   int gbase) {
   extern __shared__ __align__(16) unsigned char qsm[];
   float* ring = reinterpret_cast<float*>(qsm);                                     // [QNST][QF + QL][QRS]
   double* sC = reinterpret_cast<double*>(qsm);                                      // [3 QF][QCS] (after the K loop)
@@ -113,7 +116,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
   // so a partial last sub-tile idles whole warps (their DMMA share goes to the co-resident CTA)
   const int wm = warp & 1, wn = warp >> 1;
   if (tid < QF) {
-    const int k = blockIdx.x * QF + tid;
+    const int k = (gbase + (int)blockIdx.y) * QF + tid;
     int t = -1, a = 0, c = 0;
     if (k < T) {
       t = perm ? perm[k] : k;
@@ -150,7 +153,9 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
   }
   __syncthreads();
   uint32_t gch = 0;  // stages issued by this CTA (ring position / parity)
-  for (int l0 = wlo; l0 < whi; l0 += QL) {
+  // CTA x of a group takes sub-tiles x, x + gridDim.x, ... of the group's union: the
+  // work unit is one 32 x 32 sub-tile (~1/3 of a group), so the last wave is short
+  for (int l0 = wlo + (int)blockIdx.x * QL; l0 < whi; l0 += (int)gridDim.x * QL) {
     double lcB[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -315,10 +320,19 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
     attr = true;
   }
   const bool vec = n % 4 == 0 && (reinterpret_cast<uintptr_t>(fr) & 15) == 0 && (reinterpret_cast<uintptr_t>(lr) & 15) == 0;
-  const dim3 grid((T + QF - 1) / QF);
-#define MC_RD_LAUNCH(V, U, R)                                                                                 \
-  refine_dmma_kernel<V, U, R><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, fmap, fwbar, wuni, ga, T, \
-                                                            L, n, perm, lo, cnt, cap, Dex, Rex, Dd, ldd, flags)
+  // x: sub-tile slots per group (typical window unions span 3-4 sub-tiles; wider
+  // unions loop), y: frame groups (launch order keeps a group's sub-tiles adjacent)
+  const int ngroups = (T + QF - 1) / QF;
+  const int lsub = (L + QL - 1) / QL;
+#define MC_RD_LAUNCH(V, U, R)                                                                                  \
+  do {                                                                                                         \
+  for (int g0 = 0; g0 < ngroups; g0 += 65535) {                                                                \
+    const dim3 grid((unsigned)std::min(lo ? 4 : 8, lsub), (unsigned)std::min(65535, ngroups - g0));           \
+    refine_dmma_kernel<V, U, R><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, fmap, fwbar, wuni, ga, \
+                                                              T, L, n, perm, lo, cnt, cap, Dex, Rex, Dd, ldd,   \
+                                                              flags, g0);                                       \
+  }                                                                                                            \
+  } while (0)
   if (lwbar && fwbar && wuni > 0.0) {
     if (vec) MC_RD_LAUNCH(true, false, true); else MC_RD_LAUNCH(false, false, true);
   } else if (lwbar) {

@@ -8,7 +8,7 @@ r.step_device(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); r.step_device(); e1.record(); torch.cuda.synchronize()
 print(json.dumps({"device_ms": e0.elapsed_time(e1)}))
-for sched in ["4096,32768,2", "8192,16384,2", "16384,16384,1", "8192,32768,1.25", "4096,24576,1.5", "12288,24576,2"]:
+for sched in os.environ.get("SCHEDS", "4096,24576,1.5,0;4096,24576,1.5,1;2048,24576,1.5,1;4096,16384,1.5,1;4096,32768,1.5,1;2048,12288,1.5,1").split(";"):
     os.environ["MC_E2E_CHUNKS"] = sched
     r.step_e2e(); torch.cuda.synchronize()
     ts = []
