@@ -250,6 +250,20 @@ int mc_refine(const float* frames, const double* fcentroid, const float* landmar
               const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,
               float* Dd, int64_t ldd, const int32_t* fmap, const double* fwbar, double wuni,
               uint8_t* flags, void* stream);
+/* Close-structure path on the fp64 tensor cores (fp32 coordinates, uniform weights):
+ * mc_cov_dmma: dense S [T, L, 9] = sum_j w (x_tj - c_t)(a_lj - c_l)^T (the mc_cov_f64
+ *   contract on raw fp32 frames / landmarks with their fp64 centroids and w-sums
+ *   wbar = sum_j w (x_j - c); wuni = the common weight), exact fp64 products and sums.
+ * mc_close_grad_fix: adds the Eq. 6 dR_xy term (the dk_contract closed form used by
+ *   mc_pathcv_grad) to ds / dz rows t0 .. t0+T-1 of the non-refresh frames, after the
+ *   contraction part came from mc_pathcv_grad_block; fvec = the chunk's K4 per-frame
+ *   vectors, ridx / refresh / xyeig global by frame, frames raw fp32 [*, n, 3]. */
+int mc_cov_dmma(const float* frames, const double* fcentroid, const double* fwbar, const float* landmarks,
+                const double* lcentroid, const double* lwbar, const double* w, double wuni, int32_t T, int32_t L,
+                int32_t n, double* S, void* stream);
+int mc_close_grad_fix(int32_t T, int32_t t0, int32_t n, const uint8_t* refresh, const int32_t* ridx,
+                      const double* xyeig, const double* fvec, const double* w, const float* frames,
+                      const double* fcentroid, void* ds, void* dz, int32_t out_f32, void* stream);
 
 /* Per-pair DistanceResult gradients of the reference-facing API:
  * exact_distance (Eq. 3/4) and approx_distance (Eq. 5/6,

@@ -78,6 +78,8 @@ _SIGS = {
     "mc_sort_by_key": [_P, _I32, _I32, _P, _P, _P],
     "mc_refine": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P, _D, _P,
                   _P],
+    "mc_cov_dmma": [_P, _P, _P, _P, _P, _P, _P, _D, _I32, _I32, _I32, _P, _P],
+    "mc_close_grad_fix": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
     "mc_pair_grad": [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],

@@ -233,6 +233,27 @@ int mc_sort_by_key(const int32_t* key, int32_t T, int32_t nbins, int32_t* bins, 
   return cuda_status(mc::launch_sort_by_key(key, T, nbins, bins, perm, S_(stream)));
 }
 
+int mc_cov_dmma(const float* frames, const double* fcentroid, const double* fwbar, const float* landmarks,
+                const double* lcentroid, const double* lwbar, const double* w, double wuni, int32_t T, int32_t L,
+                int32_t n, double* S, void* stream) {
+  if (T < 0 || L < 1 || n < 2 || !(wuni > 0.0)) return MC_ERR_CONFIG;
+  if (T > 0 && (!frames || !fcentroid || !fwbar || !landmarks || !lcentroid || !lwbar || !w || !S))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_refine_dmma(frames, fcentroid, landmarks, lcentroid, lwbar, w, nullptr, nullptr, fwbar,
+                                            wuni, nullptr, T, L, n, nullptr, nullptr, nullptr, 0, nullptr, nullptr,
+                                            nullptr, 0, nullptr, S_(stream), S));
+}
+
+int mc_close_grad_fix(int32_t T, int32_t t0, int32_t n, const uint8_t* refresh, const int32_t* ridx,
+                      const double* xyeig, const double* fvec, const double* w, const float* frames,
+                      const double* fcentroid, void* ds, void* dz, int32_t out_f32, void* stream) {
+  if (T < 0 || t0 < 0 || n < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!refresh || !ridx || !xyeig || !fvec || !w || !frames || !fcentroid || !ds || !dz))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_close_grad_fix(T, t0, n, refresh, ridx, xyeig, fvec, w, frames, fcentroid, ds, dz,
+                                               out_f32, S_(stream)));
+}
+
 int mc_refine(const float* frames, const double* fcentroid, const float* landmarks, const double* lcentroid,
               const double* lwbar, const double* w, const double* gx, const double* ga, int32_t T, int32_t L, int32_t n,
               const int32_t* perm, const int32_t* lo, const int32_t* cnt, int32_t cap, double* Dex, double* Rex,

@@ -169,9 +169,10 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   bool staged = false;
   const int katom0 = blockIdx.y * apb;
   const int katom1 = min(n, katom0 + apb);
-  // VEC producer (thread 0).  Without restaging every sub-tile walks the same
-  // landmark window, so the chunk sequence runs on across sub-tiles: the next
-  // sub-tile's first chunks are in flight during this one's epilogue.
+  // VEC producer (thread 0): walks the chunk sequence (atom sub-tile a0, window
+  // chunk w0, landmark chunk ch) in consumption order, up to NST - 1 chunks ahead,
+  // across w0 and a0 boundaries -- the next block's first chunks are in flight
+  // during this block's epilogue or coefficient restaging.
   int pa0 = katom0, pch = 0, pw0 = wlo, pwn = min(DWMAX, whi - wlo);
   uint32_t gprod = 0, plimit = 0;
   auto produce_next = [&]() {
@@ -186,12 +187,18 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       bulk_g2s(dst + q * LROW, lraw + ((int64_t)(pw0 + pch * CHL + q) * n + pa0) * 3, 12 * natp, &full[slot]);
     if (++pch * CHL >= pwn) {
       pch = 0;
-      pa0 += DNA;
+      pw0 += DWMAX;
+      if (pw0 >= whi) {
+        pw0 = wlo;
+        pa0 += DNA;
+      }
+      pwn = min(DWMAX, whi - pw0);
     }
   };
-  if (VEC && !restage && tid == 0 && whi > wlo) {
-    const int nchw = (3 * pwn + DKC - 1) / DKC;
-    plimit = (uint32_t)(((katom1 - katom0 + DNA - 1) / DNA) * nchw);
+  if (VEC && tid == 0 && whi > wlo) {
+    uint32_t per_a0 = 0;
+    for (int w0 = wlo; w0 < whi; w0 += DWMAX) per_a0 += (uint32_t)((3 * min(DWMAX, whi - w0) + DKC - 1) / DKC);
+    plimit = (uint32_t)((katom1 - katom0 + DNA - 1) / DNA) * per_a0;
     while (gprod < plimit && gprod < (uint32_t)(NST - 1)) produce_next();
   }
   for (int a0 = katom0; a0 < katom1; a0 += DNA) {
@@ -225,11 +232,6 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     for (int w0 = wlo; w0 < whi; w0 += DWMAX) {
       const int wn = min(DWMAX, whi - w0);
       const int nch = (3 * wn + DKC - 1) / DKC;
-      if (VEC && restage && tid == 0) {  // the producer covers this (a0, w0) block only
-        pa0 = a0, pch = 0, pw0 = w0, pwn = wn;
-        plimit = gch + (uint32_t)nch;
-        while (gprod < plimit && gprod < gch + (uint32_t)(NST - 1)) produce_next();
-      }
       if (restage || !staged) {  // block-uniform
         staged = true;
         __syncthreads();

@@ -50,6 +50,9 @@ cudaError_t launch_mtd_force(const double* dV, int T, int d, const void* g0, con
                              int dtype, int n, void* F, cudaStream_t stream);
 cudaError_t launch_topm(const void* D, int dtype, int nrows, int L, int64_t ldd, const int* rows, int M, int* idx,
                         cudaStream_t stream);
+cudaError_t launch_close_grad_fix(int T, int t0, int n, const uint8_t* refresh, const int* ridx, const double* xyeig,
+                                  const double* fvec, const double* w, const float* fraw, const double* fcen, void* ds,
+                                  void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, const double* lpl, const double* w,
                            const double* wa, const int* sig_idx, const double* sig_coef, const int* nsig,
                            const double* fvec, const uint8_t* refresh, const int* ridx, const double* xyeig,
@@ -79,7 +82,7 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
                                const double* lwbar, const double* w, const double* gx, const int* fmap,
                                const double* fwbar, double wuni, const double* ga, int T, int L, int n,
                                const int* perm, const int* lo, const int* cnt, int cap, double* Dex, double* Rex,
-                               float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream);
+                               float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream, double* Sout = nullptr);
 cudaError_t launch_refine(const float* fr, const double* fc, const float* lr, const double* lc, const double* w,
                           const double* gx, const double* ga, int T, int L, int n, const int* perm, const int* lo,
                           const int* cnt, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,

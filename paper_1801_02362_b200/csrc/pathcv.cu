@@ -18,6 +18,8 @@
 //   dR-term_k = v^T (dK/dx_k) q_0                     (closed form, mc_math)
 // Landmarks with lam (D_i - D_min) > cutoff (default 50) contribute
 // < e^-50 relative to the leading term and are skipped.
+#include <algorithm>
+
 #include "mc_math.cuh"
 
 namespace mc {
@@ -396,6 +398,72 @@ cudaError_t launch_cv_grad(int T, int n, int npad, int cap, const double* fpl, c
     cv_grad_kernel<double><<<grid, GNT, 0, stream>>>(n, npad, cap, fpl, lpl, w, wa, sig_idx, sig_coef, nsig, fvec,
                                                      refresh, ridx, xyeig, (double*)ds, (double*)dz, fraw, fcen, lraw,
                                                      lcen, perm);
+  return cudaGetLastError();
+}
+
+// Eq. 6 dR_xy term of the non-refresh frames, added after the contraction part of
+// the gradient came from the DMMA kernel (cv_grad_dmma_kernel).  Same closed form as
+// the approx branch of cv_grad_kernel, on raw fp32 coordinates recentred with the
+// fp64 centroids: x = frame t0 + t, y = its close structure ridx[t0 + t].
+template <typename OT>
+__global__ void __launch_bounds__(256)
+close_grad_fix_kernel(int t0, int n, const uint8_t* __restrict__ refresh, const int* __restrict__ ridx,
+                      const double* __restrict__ xyeig, const double* __restrict__ fvec, const double* __restrict__ w,
+                      const float* __restrict__ fraw, const double* __restrict__ fcen, OT* __restrict__ ds,
+                      OT* __restrict__ dz) {
+  const int tl = blockIdx.y;
+  const int t = t0 + tl;
+  if (refresh[t]) return;
+  const int r = ridx[t];
+  const double* e = xyeig + (int64_t)t * 20;
+  double q0[4];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) q0[rr] = e[4 + rr * 4];
+  const double* fv = fvec + (int64_t)tl * FVEC;
+  const double vs[4] = {fv[8], fv[9], fv[10], fv[11]};
+  const double vz[4] = {fv[12], fv[13], fv[14], fv[15]};
+  const double cx[3] = {fcen[3 * t], fcen[3 * t + 1], fcen[3 * t + 2]};
+  const double cy[3] = {fcen[3 * r], fcen[3 * r + 1], fcen[3 * r + 2]};
+  const float* xr = fraw + (int64_t)t * n * 3;
+  const float* yr = fraw + (int64_t)r * n * 3;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double xk[3], yk[3], d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      xk[a] = (double)xr[3 * k + a] - cx[a];
+      yk[a] = (double)yr[3 * k + a] - cy[a];
+    }
+    const double wk = w[k];
+    OT* os = ds + ((int64_t)t * n + k) * 3;
+    OT* oz = dz + ((int64_t)t * n + k) * 3;
+    dk_contract(vs, q0, wk, xk, yk, d);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) os[a] = (OT)((double)os[a] + d[a]);
+    dk_contract(vz, q0, wk, xk, yk, d);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) oz[a] = (OT)((double)oz[a] + d[a]);
+  }
+}
+
+cudaError_t launch_close_grad_fix(int T, int t0, int n, const uint8_t* refresh, const int* ridx, const double* xyeig,
+                                  const double* fvec, const double* w, const float* fraw, const double* fcen, void* ds,
+                                  void* dz, int out_f32, cudaStream_t stream) {
+  if (T <= 0 || n <= 0) return cudaSuccess;
+  if (T > 65535) {
+    for (int c = 0; c < T; c += 65535) {
+      cudaError_t e = launch_close_grad_fix(std::min(65535, T - c), t0 + c, n, refresh, ridx, xyeig,
+                                            fvec + (int64_t)c * FVEC, w, fraw, fcen, ds, dz, out_f32, stream);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  const dim3 grid((unsigned)std::min(8, (n + 255) / 256), (unsigned)T);
+  if (out_f32)
+    close_grad_fix_kernel<float><<<grid, 256, 0, stream>>>(t0, n, refresh, ridx, xyeig, fvec, w, fraw, fcen,
+                                                            (float*)ds, (float*)dz);
+  else
+    close_grad_fix_kernel<double><<<grid, 256, 0, stream>>>(t0, n, refresh, ridx, xyeig, fvec, w, fraw, fcen,
+                                                             (double*)ds, (double*)dz);
   return cudaGetLastError();
 }
 

@@ -96,7 +96,7 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
                    const double* __restrict__ ga, int T, int L, int n, const int* __restrict__ perm,
                    const int* __restrict__ lo, const int* __restrict__ cnt, int cap, double* __restrict__ Dex,
                    double* __restrict__ Rex, float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags,
-                   int gbase) {
+                   int gbase, double* __restrict__ Sout) {
   extern __shared__ __align__(16) unsigned char qsm[];
   float* ring = reinterpret_cast<float*>(qsm);                                     // [QNST][QF + QL][QRS]
   double* sC = reinterpret_cast<double*>(qsm);                                      // [3 QF][QCS] (after the K loop)
@@ -276,6 +276,12 @@ refine_dmma_kernel(const float* __restrict__ fr, const double* __restrict__ fc, 
             S[b * 3 + g] -= s_fc[f][b] * lwbar[3 * l + g];
           }
         }
+      if (Sout) {  // covariance output only (dense; the close-structure path fits a subset later)
+        double* o = Sout + ((int64_t)t * L + l) * 9;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) o[e] = S[e];
+        continue;
+      }
       double q[4];
       bool ill = false;
       double msd = fit_fast(S, gx[t], ga[l], Rex ? q : nullptr, &ill);
@@ -306,7 +312,7 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
                                const double* lwbar, const double* w, const double* gx, const int* fmap,
                                const double* fwbar, double wuni, const double* ga, int T, int L, int n,
                                const int* perm, const int* lo, const int* cnt, int cap, double* Dex, double* Rex,
-                               float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream) {
+                               float* Dd, int64_t ldd, uint8_t* flags, cudaStream_t stream, double* Sout) {
   if (T <= 0 || L <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -330,7 +336,7 @@ cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* l
     const dim3 grid((unsigned)std::min(lo ? 4 : 8, lsub), (unsigned)std::min(65535, ngroups - g0));           \
     refine_dmma_kernel<V, U, R><<<grid, QNT, QSMEM, stream>>>(fr, fc, lr, lc, lwbar, w, gx, fmap, fwbar, wuni, ga, \
                                                               T, L, n, perm, lo, cnt, cap, Dex, Rex, Dd, ldd,   \
-                                                              flags, g0);                                       \
+                                                              flags, g0, Sout);                                 \
   }                                                                                                            \
   } while (0)
   if (lwbar && fwbar && wuni > 0.0) {

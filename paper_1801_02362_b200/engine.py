@@ -34,6 +34,9 @@ PRUNE = os.environ.get("MC_PRUNE", "1") == "1"
 # tensor-core screen otherwise trips the board's power cap, and the clock
 # recovery after it slows the fp64 kernels that follow.
 K2_GRID = int(os.environ.get("MC_K2_GRID", "0"))
+# fp32 inputs of the fp64 PathCV engine on the fp64 tensor cores (env MC_CLOSE_DMMA=0:
+# the fp64-plane CUDA-core kernels)
+CLOSE_DMMA = os.environ.get("MC_CLOSE_DMMA", "1") == "1"
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 
 
@@ -109,6 +112,15 @@ def _bits_value(row):
     return sum(b for b, on in zip(_FLAG_BITS, row) if on)
 
 
+class _Cen:
+    """Centroid view of a frame chunk (what the blocked gradient pass reads)."""
+
+    __slots__ = ("centroid",)
+
+    def __init__(self, centroid):
+        self.centroid = centroid.contiguous()
+
+
 class PathCV:
     """Resident landmark set + evaluator for s, z and their atom gradients.
 
@@ -142,6 +154,12 @@ class PathCV:
         self.lm = K.center(lm, self.wa, self.w, weighted=True, moments=True)
         if _or_flags(self.lm.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("landmark coordinates contain non-finite values")
+        # fp32 coordinates with a uniform displacement weight: the covariances and the
+        # gradient contraction run on the fp64 tensor cores from the raw fp32 rows
+        # (DESIGN.md "Close structure on DMMA"); fp64 inputs keep the fp64 planes path
+        self.wuni = float(self.w[0].item()) if bool((self.w[:self.n] == self.w[0]).all()) else 0.0
+        self.lraw = lm.contiguous() if (lm.dtype == torch.float32 and CLOSE_DMMA and self.n % 4 == 0
+                                        and self.wuni > 0.0) else None
 
     # ------------------------------------------------------------------
     def _frames(self, frames):
@@ -152,10 +170,18 @@ class PathCV:
             raise InvalidStructureError("frame coordinates contain non-finite values")
         return fr, c
 
+    def _dmma(self, raw):
+        return self.lraw is not None and raw.dtype == torch.float32
+
+    def _cov(self, raw, fr):
+        if self._dmma(raw):
+            return K.cov_dmma(raw.contiguous(), fr, self.lraw, self.lm, self.w, self.wuni)
+        return K.cov_dense(fr, self.lm)
+
     def msd_matrix(self, frames, want_rot=False):
         """Exact aligned MSD of every (frame, landmark) pair: D [T, L] fp64."""
-        _, fr = self._frames(frames)
-        S = K.cov_dense(fr, self.lm)
+        raw, fr = self._frames(frames)
+        S = self._cov(raw, fr)
         D, rot, _, flags = K.fit_dense(S, fr.g, self.lm.g, want_rot=want_rot)
         _raise_flags(flags, "msd_matrix")
         return (D, rot) if want_rot else D
@@ -166,7 +192,7 @@ class PathCV:
     def evaluate(self, frames, grad=True, cap=None, out_dtype=None):
         """Alg. 1 without neighbour list: exact D_i for every landmark."""
         raw, fr = self._frames(frames)
-        S = K.cov_dense(fr, self.lm)
+        S = self._cov(raw, fr)
         D, R, _, flags = K.fit_dense(S, fr.g, self.lm.g, want_rot=True)
         _raise_flags(flags, "path_cv")
         return self._finish(raw, fr, D, R, S, None, grad, cap, out_dtype)
@@ -193,7 +219,7 @@ class PathCV:
             steps = int(fr_in.shape[0]) // walkers
         raw, fr = self._frames(fr_in)
         close = K.close_decisions(fr, self.w, eps, walkers, steps, window)
-        S = K.cov_dense(fr, self.lm)
+        S = self._cov(raw, fr)
         D, R, _, flags = K.fit_dense(S, fr.g, self.lm.g, rowmask=close["refresh"], want_rot=True)
         _raise_flags(flags, "close_structure_replay")
         nb = None
@@ -221,6 +247,7 @@ class PathCV:
 
     def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype, nb=None):
         T = D.shape[0]
+        raw = raw.contiguous()
         cap0 = self._cap(cap)
         dev = D.device
         s = torch.empty((T,), dtype=torch.float64, device=dev)
@@ -247,7 +274,16 @@ class PathCV:
             if f & FLAG_NON_FINITE:
                 raise InvalidStructureError("non-finite distances in the path-CV reduction")
             nsig[t0:t0 + chunk] = wres["nsig"]
-            if grad:
+            if grad and self._dmma(raw):
+                # contraction on DMMA (frame groups by significant span), then the
+                # close-structure dR_xy term of the non-refresh rows
+                sl = slice(t0, t0 + chunk)
+                gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
+                K.pathcv_grad_block(wres, _Cen(fr.centroid[sl]), self.lm, raw[sl], self.lraw, self.w, self.wa, cap,
+                                    gperm, ds=ds[sl], dz=dz[sl])
+                if close is not None:
+                    K.close_grad_fix(wres, close, self.w, raw, fr.centroid, ds, dz)
+            elif grad:
                 K.pathcv_grad(wres, fr, self.lm, self.w, self.wa, cap, odt, close=close, ds=ds, dz=dz)
             t0 += chunk
         out = {"s": s, "z": z, "D": D, "nsig": nsig}
@@ -308,7 +344,7 @@ class PathCVTC:
         self.lraw = lm
         # uniform displacement weights (the configs' default): the exact refits run on raw,
         # unweighted fp32 operands (refine_dmma RAW mode)
-        self.wuni = float(self.w[0].item()) if bool((self.w == self.w[0]).all()) else 0.0
+        self.wuni = float(self.w[0].item()) if bool((self.w[:self.n] == self.w[0]).all()) else 0.0
         self._ls = {}
         self.screen_terms = 1 if self.screen == "f16x1" else 3
         self.ls = self._lsplit(self.screen_terms)

@@ -70,6 +70,27 @@ def cov_dense(fr: Centred, lm: Centred):
     return S
 
 
+def cov_dmma(frames, fr: Centred, lraw, lm: Centred, w, wuni):
+    """S [T, L, 9] fp64 (the cov_dense contract) on the fp64 tensor cores from raw
+    fp32 frames / landmarks and the centroids / w-sums of their Centred objects
+    (uniform displacement weight wuni)."""
+    T, n = frames.shape[0], frames.shape[1]
+    L = lraw.shape[0]
+    S = torch.empty((T, L, 9), dtype=F64, device=frames.device)
+    call("mc_cov_dmma", ptr(frames), ptr(fr.centroid), ptr(fr.wbar), ptr(lraw), ptr(lm.centroid), ptr(lm.wbar), ptr(w),
+         float(wuni), T, L, n, ptr(S), stream_ptr())
+    return S
+
+
+def close_grad_fix(wres, close, w, frames, fcentroid, ds, dz):
+    """Adds the Eq. 6 dR_xy term of the non-refresh frames of wres's chunk to ds / dz
+    (full [T, n, 3] arrays) after pathcv_grad_block wrote the contraction part."""
+    T, t0 = wres["count"], wres["t0"]
+    call("mc_close_grad_fix", T, t0, frames.shape[1], ptr(close["refresh"]), ptr(close["ridx"]), ptr(close["xyeig"]),
+         ptr(wres["fvec"]), ptr(w), ptr(frames), ptr(fcentroid), ptr(ds), ptr(dz),
+         1 if ds.dtype == torch.float32 else 0, stream_ptr())
+
+
 def cov_pairs(xplanes, aplanes, xi, ai, npad, w):
     P = int(xi.shape[0]) if xi is not None else int(xplanes.shape[0])
     S = torch.empty((P, 9), dtype=F64, device=xplanes.device)
@@ -248,17 +269,17 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
 
 
 def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32,
-                      out_map=None):
+                      out_map=None, ds=None, dz=None):
     """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames.
     out_map (optional, int32 [T]): the caller's row of frame t -- its raw coordinates
-    are read from and its gradients written to that row."""
+    are read from and its gradients written to that row.  ds / dz: optional outputs."""
     T, n = frames.shape[0], frames.shape[1]
     dev = frames.device
-    ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
-    dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev)
+    ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev) if ds is None else ds
+    dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev) if dz is None else dz
     call("mc_pathcv_grad_block", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(perm),
-         ptr(out_map), ptr(ds), ptr(dz), 1 if out_dtype == torch.float32 else 0, stream_ptr())
+         ptr(out_map), ptr(ds), ptr(dz), 1 if ds.dtype == torch.float32 else 0, stream_ptr())
     return ds, dz
 
 
