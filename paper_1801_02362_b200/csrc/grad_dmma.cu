@@ -34,6 +34,7 @@ constexpr int DNA = 256;           // atoms per sub-tile (8 warps x 32)
 constexpr int DKC = 24;            // kk rows per B chunk (8 landmarks)
 constexpr int LROW = 3 * DNA + 8;  // raw floats per staged landmark row (+8: bank shift between landmarks)
 constexpr int NST = 3;             // cp.async ring stages
+constexpr int MAXWC = 127;         // window chunks with per-chunk list ranges (union <= 12192 landmarks)
 #ifndef MC_GD_WAT
 #define MC_GD_WAT 16
 #endif
@@ -119,6 +120,9 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   __shared__ int s_wlo, s_whi;
   __shared__ double s_bias[DR];
   __shared__ int s_cum[DG + 1];
+  // s_beg[f][c]: first position of frame f's (ascending) significant list inside
+  // window chunk c = [wlo + c DWMAX, ..); a restage reads only its chunk's entries
+  __shared__ int s_beg[DG][MAXWC + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;  // mma groupID / threadID_in_group
   if (tid < DG) {
@@ -145,12 +149,6 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     for (int f = 0; f < DG; ++f) { a = min(a, s_flo[f]); b = max(b, s_fhi[f]); }
     s_wlo = a;
     s_whi = b;
-    int tot = 0;
-    for (int f = 0; f < DG; ++f) {
-      s_cum[f] = tot;
-      tot += s_t[f] >= 0 ? s_ns[f] * 18 : 0;
-    }
-    s_cum[DG] = tot;
   }
   if (VEC) {
     if (tid == 0) {
@@ -165,6 +163,25 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   __syncthreads();
   const int wlo = s_wlo, whi = s_whi;
   const bool restage = whi - wlo > DWMAX;
+  const int nwc = whi > wlo ? (whi - wlo + DWMAX - 1) / DWMAX : 0;
+  const bool ranged = nwc <= MAXWC;  // else: each restage filters the whole list
+  if (ranged) {
+    for (int i = tid; i < DG * (MAXWC + 1); i += DNT) (&s_beg[0][0])[i] = 0;
+    __syncthreads();
+    for (int f = 0; f < DG; ++f) {
+      const int t = s_t[f], ns = s_ns[f];
+      if (t < 0 || ns <= 0) continue;  // block-uniform
+      const int* idx = sig_idx + (int64_t)t * cap;
+      for (int e = tid; e < ns; e += DNT) {
+        const int c = (idx[e] - wlo) / DWMAX;
+        const int cprev = e == 0 ? -1 : (idx[e - 1] - wlo) / DWMAX;
+        for (int q = cprev + 1; q <= c; ++q) s_beg[f][q] = e;
+        if (e == ns - 1)
+          for (int q = c + 1; q <= nwc; ++q) s_beg[f][q] = ns;
+      }
+    }
+    __syncthreads();
+  }
   uint32_t gch = 0, xphase = 0;  // VEC: chunks consumed by this CTA (ring position / parity)
   bool staged = false;
   const int katom0 = blockIdx.y * apb;
@@ -238,7 +255,18 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
         for (int e = tid; e < DR * AST; e += DNT) sA[e] = 0.0;
         for (int e = tid; e < DKMAX; e += DNT) sLc[e] = e < 3 * wn ? lcen[3 * w0 + e] : 0.0;
         __syncthreads();
-        // coefficient scatter, all frames at once (independent loads in flight)
+        // coefficient scatter of this window chunk, all frames at once (independent
+        // loads in flight); entries of the chunk only when the list ranges are known
+        const int wc = (w0 - wlo) / DWMAX;
+        if (tid == 0) {
+          int tot = 0;
+          for (int f = 0; f < DG; ++f) {
+            s_cum[f] = tot;
+            if (s_t[f] >= 0) tot += 18 * (ranged ? s_beg[f][wc + 1] - s_beg[f][wc] : s_ns[f]);
+          }
+          s_cum[DG] = tot;
+        }
+        __syncthreads();
         const int tot = s_cum[DG];
 #pragma unroll 4
         for (int e = tid; e < tot; e += DNT) {
@@ -246,7 +274,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
 #pragma unroll
           for (int q = 1; q < DG; ++q) f += e >= s_cum[q];
           const int t = s_t[f], el = e - s_cum[f];
-          const int s = el / 18, e18 = el - s * 18;
+          const int s = el / 18 + (ranged ? s_beg[f][wc] : 0), e18 = el % 18;
           const int l = sig_idx[(int64_t)t * cap + s] - w0;
           const double v = sig_coef[((int64_t)t * cap + s) * 18 + e18];
           if (l >= 0 && l < wn) {
