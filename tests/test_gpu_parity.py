@@ -213,3 +213,47 @@ def test_config3_walkers_slice_vs_oracle(cuda_device):
         assert_grad(out["ds"].cpu().numpy()[sl], ref["ds"])
         assert_grad(out["dz"].cpu().numpy()[sl], ref["dz"])
     assert 0 < out["refresh"].sum() < 120
+
+
+def test_cov_dmma_matches_cov_f64(cuda_device):
+    """Dense covariances on the fp64 tensor cores (raw fp32 operands, RAW epilogue)
+    = the fp64-plane CUDA-core contraction, to fp64 rounding."""
+    from paper_1801_02362_b200 import synth as S
+
+    wl = S.walkers_device(4, 8, 6, 64, 40, cuda_device)
+    fr = wl.frames.reshape(-1, 64, 3).contiguous()
+    pcv = engine.PathCV(torch.from_numpy(wl.landmarks).to(cuda_device), wl.lam, wl.q)
+    assert pcv.lraw is not None
+    c = K.center(fr, pcv.wa, pcv.w)
+    s_tc = K.cov_dmma(fr, c, pcv.lraw, pcv.lm, pcv.w, pcv.wuni).cpu().numpy()
+    s_ref = K.cov_dense(c, pcv.lm).cpu().numpy()
+    scale = np.abs(s_ref).max()
+    assert np.abs(s_tc - s_ref).max() <= 1e-13 * scale
+
+
+def test_close_replay_dmma_path_equals_fp64_path(cuda_device):
+    """Config-3 shapes (fp32, N % 4 == 0): the DMMA close-structure path (dense S on
+    DMMA, gradient contraction on DMMA + the Eq. 6 correction) against the
+    fp64-plane CUDA-core path: identical refresh log, s/z to 1e-10 (fp64 summation
+    order; the weights amplify it by lam * |dD|), gradients to fp32 output rounding."""
+    from paper_1801_02362_b200 import synth as S
+
+    wl = S.walkers_device(5, 64, 60, 96, 120, cuda_device, walker_offset=3, walker_count=4)
+    lm = torch.from_numpy(wl.landmarks).to(cuda_device)
+    a = engine.PathCV(lm, wl.lam, wl.q)
+    assert a.lraw is not None
+    saved = engine.CLOSE_DMMA
+    try:
+        engine.CLOSE_DMMA = False
+        b = engine.PathCV(lm, wl.lam, wl.q)
+    finally:
+        engine.CLOSE_DMMA = saved
+    assert b.lraw is None
+    oa = a.close_replay(wl.frames, wl.eps, grad=True)
+    ob = b.close_replay(wl.frames, wl.eps, grad=True)
+    np.testing.assert_array_equal(oa["refresh"].cpu().numpy(), ob["refresh"].cpu().numpy())
+    assert 0 < int(oa["refresh"].sum()) < oa["refresh"].numel()
+    np.testing.assert_allclose(oa["s"].cpu().numpy(), ob["s"].cpu().numpy(), rtol=1e-10)
+    np.testing.assert_allclose(oa["z"].cpu().numpy(), ob["z"].cpu().numpy(), rtol=1e-10, atol=1e-15)
+    for key in ("ds", "dz"):
+        assert_grad(oa[key].cpu().numpy(), ob[key].cpu().numpy(), rtol=1e-6)
