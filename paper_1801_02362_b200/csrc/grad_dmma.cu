@@ -46,7 +46,7 @@ constexpr int LPT = CHL * DNA * 3 / DNT;  // raw floats per thread per chunk
 constexpr int XPT = DG * DNA * 3 / DNT;  // frame floats per thread per sub-tile
 constexpr int DSMEM = DR * AST * (int)sizeof(double) + DKMAX * (int)sizeof(double) +
                       NST * CHL * LROW * (int)sizeof(float) + DG * 3 * DNA * (int)sizeof(float) +
-                      (2 * NST + 1) * (int)sizeof(uint64_t);
+                      2 * DNA * (int)sizeof(double) + (2 * NST + 1) * (int)sizeof(uint64_t);
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -112,13 +112,17 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   float* sX = sR + NST * CHL * LROW;                      // [DG][3 DNA] raw frame floats of the sub-tile
   // VEC: warp-decoupled ring -- thread 0 issues 1-D TMA bulk copies completing on
   // full[slot]; each warp releases a slot on empty[slot]; no CTA barrier per chunk
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + DG * 3 * DNA);
+  double* sWW = reinterpret_cast<double*>(sX + DG * 3 * DNA);  // VEC: [2][DNA] w, w_align of the sub-tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(sWW + 2 * DNA);
   uint64_t* empty = full + NST;
   uint64_t* xfull = empty + NST;
   __shared__ int s_t[DG], s_raw[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
   __shared__ double s_fc[DG][3], s_fv[DG][8];
   __shared__ int s_wlo, s_whi;
   __shared__ double s_bias[DR];
+  __shared__ double s_rcx[DR], s_rsc[DR], s_rcorr[DR];
+  __shared__ unsigned long long s_rptr[DR];
+  __shared__ int s_rx[DR];
   __shared__ int s_cum[DG + 1];
   // s_beg[f][c]: first position of frame f's (ascending) significant list inside
   // window chunk c = [wlo + c DWMAX, ..); a restage reads only its chunk's entries
@@ -144,6 +148,16 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     }
   }
   __syncthreads();
+  if (tid < DR) {  // epilogue row table: r = (frame f, s|z, axis b)
+    const int f = tid / 6, sz = (tid % 6) / 3, b = tid % 3;
+    const int t = s_t[f];
+    s_rptr[tid] = t < 0 ? 0ull
+                        : reinterpret_cast<unsigned long long>((sz ? dz : ds) + (int64_t)s_raw[f] * n * 3 + b);
+    s_rcx[tid] = t < 0 ? 0.0 : s_fc[f][b];
+    s_rsc[tid] = t < 0 ? 0.0 : s_fv[f][sz];
+    s_rcorr[tid] = t < 0 ? 0.0 : s_fv[f][2 + sz * 3 + b];
+    s_rx[tid] = f * 3 * DNA + b;
+  }
   if (tid == 0) {
     int a = 0x7fffffff, b = -1;
     for (int f = 0; f < DG; ++f) { a = min(a, s_flo[f]); b = max(b, s_fhi[f]); }
@@ -226,9 +240,12 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
       if (tid == 0) {
         int rows = 0;
         for (int f = 0; f < DG; ++f) rows += s_raw[f] >= 0;
-        mb_expect(xfull, (uint32_t)(rows * 12 * nat));
+        mb_expect(xfull, (uint32_t)(rows * 12 * nat + 16 * nat));
         for (int f = 0; f < DG; ++f)
           if (s_raw[f] >= 0) bulk_g2s(sX + f * 3 * DNA, fraw + ((int64_t)s_raw[f] * n + a0) * 3, 12 * nat, xfull);
+        // the epilogue's atom weights ride on the same barrier (no global loads there)
+        bulk_g2s(sWW, w + a0, 8 * nat, xfull);
+        bulk_g2s(sWW + DNA, wa + a0, 8 * nat, xfull);
       }
     } else {
 #pragma unroll 4
@@ -391,41 +408,47 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     // epilogue: each accumulator element is one (frame, s|z, axis, atom) output.
     // Loads of a half (3 row tiles x 8 atoms) are batched ahead of its stores.
     double wk[NJ][2], wak[NJ][2];
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int k = a0 + warp * WAT + j * 8 + 2 * tq + e;
-        wk[j][e] = k < n ? w[k] : 0.0;
-        wak[j][e] = k < n ? wa[k] : 0.0;
-      }
     if (VEC) {
       mb_wait(xfull, xphase);
       xphase ^= 1u;
-    } else {
-      cp_wait<0>();
-      __syncthreads();
-    }
-#pragma unroll
-    for (int m = 0; m < 6; ++m) {
-      const int r = m * 8 + gq;
-      const int f = r / 6, sz = (r % 6) / 3, b = r % 3;
-      const int t = s_t[f];
-      if (t < 0) continue;
-      const double cx = s_fc[f][b], sc = s_fv[f][sz], corr = s_fv[f][2 + sz * 3 + b];
-      const double bias = s_bias[r];
-      OT* __restrict__ out = sz ? dz : ds;
-      const int tout = s_raw[f];
-      const float* xs = sX + f * 3 * DNA + b;
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int al = warp * WAT + j * 8 + 2 * tq + e;
-          const int k = a0 + al;
-          if (k >= n) continue;
+          wk[j][e] = a0 + al < n ? sWW[al] : 0.0;
+          wak[j][e] = a0 + al < n ? sWW[DNA + al] : 0.0;
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = a0 + warp * WAT + j * 8 + 2 * tq + e;
+          wk[j][e] = k < n ? w[k] : 0.0;
+          wak[j][e] = k < n ? wa[k] : 0.0;
+        }
+      cp_wait<0>();
+      __syncthreads();
+    }
+    // per GEMM row r: output row pointer (ds or dz of frame f, axis b; null for an
+    // absent frame), centroid, sums and the sX offset, tabulated once per CTA
+    const bool full = a0 + DNA <= n;  // block-uniform: no per-atom bound checks
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      const int r = m * 8 + gq;
+      OT* __restrict__ rp = reinterpret_cast<OT*>(s_rptr[r]);
+      if (!rp) continue;
+      const double cx = s_rcx[r], sc = s_rsc[r], corr = s_rcorr[r], bias = s_bias[r];
+      const float* xs = sX + s_rx[r];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int al = warp * WAT + j * 8 + 2 * tq + e;
+          if (!full && a0 + al >= n) continue;
           const double x = (double)xs[3 * al] - cx;
-          out[((int64_t)tout * n + k) * 3 + b] = (OT)(2.0 * wk[j][e] * (sc * x - (c[m][j][e] - bias)) - wak[j][e] * corr);
+          rp[(int64_t)(a0 + al) * 3] = (OT)(2.0 * wk[j][e] * (sc * x - (c[m][j][e] - bias)) - wak[j][e] * corr);
         }
     }
     __syncthreads();  // sX is refilled by the next sub-tile
