@@ -165,6 +165,110 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
   }
 }
 
+// Fast K1s for the one-term F16 frame operand (fp32 input, unweighted operand,
+// N % 4 == 0): 4-atom groups move as float4 triples (the second pass re-reads the
+// structure from L2), the scaled halves go out as 8-byte rows of 4 atoms per
+// axis, and the sums of each pass are reduced in one shared-memory round.  Same
+// values as center_split_kernel<float, OpF16> (fp64 centring and scaling, rn halves).
+constexpr int CSF_NT = 512;
+
+template <int NT, int K>
+__device__ __forceinline__ void block_sum_n(double (&v)[K], double* scratch) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) scratch[k * (NT / 32) + warp] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) r += scratch[k * (NT / 32) + i];
+    v[k] = r;
+  }
+}
+
+__global__ void __launch_bounds__(CSF_NT, 2)
+center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, int kpad,
+                          const double* __restrict__ w_align, const double* __restrict__ w_disp,
+                          __half* __restrict__ hi, double* __restrict__ scale_inv, double* __restrict__ centroid,
+                          double* __restrict__ gnorm, double* __restrict__ wbar, uint8_t* __restrict__ flags,
+                          double* __restrict__ opnorm) {
+  __shared__ double scratch[5 * (CSF_NT / 32)];
+  const int64_t b = blockIdx.x;
+  const float4* x4 = reinterpret_cast<const float4*>(coords + b * (int64_t)n * 3);
+  const int G = n / 4;
+  double c[3] = {0.0, 0.0, 0.0};
+  double xmax = 0.0;
+  bool finite = true;
+#pragma unroll 2
+  for (int gi = threadIdx.x; gi < G; gi += CSF_NT) {
+    const float4 q0 = x4[3 * gi], q1 = x4[3 * gi + 1], q2 = x4[3 * gi + 2];
+    const float f[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double wa = w_align[4 * gi + a];
+      const double x0 = f[3 * a], x1 = f[3 * a + 1], x2 = f[3 * a + 2];
+      finite = finite && isfinite(x0) && isfinite(x1) && isfinite(x2);
+      c[0] += wa * x0; c[1] += wa * x1; c[2] += wa * x2;
+      xmax = fmax(xmax, fmax(fabs(x0), fmax(fabs(x1), fabs(x2))));
+    }
+  }
+  xmax = -block_min<CSF_NT>(-xmax, scratch);
+  block_sum_n<CSF_NT, 3>(c, scratch);
+  const int nonfinite = __syncthreads_or(!finite);
+  const double bound = 2.0 * xmax;  // |x_j - c| <= 2 max|x|
+  int e = 0;
+  if (bound > 0.0 && isfinite(bound)) {
+    frexp(bound, &e);
+    e = 14 - e;
+  }
+  e = max(-1000, min(1000, e));
+  const double scale = ldexp(1.0, e);
+  const int64_t plane = B * (int64_t)kpad;
+  __half* h0 = hi + b * kpad;
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // g, wbar (3), |operand|^2
+#pragma unroll 2
+  for (int gi = threadIdx.x; gi < kpad / 4; gi += CSF_NT) {
+    uint2 o[3] = {make_uint2(0u, 0u), make_uint2(0u, 0u), make_uint2(0u, 0u)};
+    if (gi < G) {
+      const float4 q0 = x4[3 * gi], q1 = x4[3 * gi + 1], q2 = x4[3 * gi + 2];
+      const float f[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+      __half h[3][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double wd = w_disp[4 * gi + a];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          const double v = (double)f[3 * a + p] - c[p];
+          acc[0] += wd * v * v;
+          acc[1 + p] += wd * v;
+          acc[4] += v * v;
+          h[p][a] = __double2half(v * scale);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 3; ++p) o[p] = *reinterpret_cast<const uint2*>(h[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(h0 + p * plane + 4 * gi) = o[p];
+  }
+  block_sum_n<CSF_NT, 5>(acc, scratch);
+  if (threadIdx.x == 0) {
+    if (centroid) { centroid[3 * b] = c[0]; centroid[3 * b + 1] = c[1]; centroid[3 * b + 2] = c[2]; }
+    gnorm[b] = acc[0];
+    if (wbar) { wbar[3 * b] = acc[1]; wbar[3 * b + 1] = acc[2]; wbar[3 * b + 2] = acc[3]; }
+    if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
+    if (opnorm) opnorm[b] = sqrt(acc[4]);
+    scale_inv[b] = ldexp(1.0, -e);
+  }
+}
+
 cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
                                 const double* w_disp, int weighted, float* hi, float* lo, double* centroid,
                                 double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream) {
@@ -184,6 +288,13 @@ cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int 
                                   uint8_t* flags, cudaStream_t stream) {
   if (B <= 0) return cudaSuccess;
   const int one = terms == 1 ? 1 : 0;
+  if (dtype == 0 && one && !weighted && !mom && n % 4 == 0 && kpad % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(coords) & 15) == 0 && B <= 0x7fffffffLL) {
+    center_split_f16x1_kernel<<<(unsigned)B, CSF_NT, 0, stream>>>((const float*)coords, B, n, kpad, w_align, w_disp,
+                                                                  (__half*)hl, scale_inv, centroid, gnorm, wbar,
+                                                                  flags, opnorm);
+    return cudaGetLastError();
+  }
   if (dtype == 0)
     center_split_kernel<float, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
         (const float*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
