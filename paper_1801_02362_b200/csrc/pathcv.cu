@@ -262,6 +262,110 @@ cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int 
   }
 }
 
+// One warp per frame for the exact sparse-window rows of the fp32 path (no close
+// structure, no neighbour list): the ~80-entry windows fill a warp, so the
+// reductions are shuffles and the significant-list compaction is one ballot per
+// 32 entries -- no CTA barriers.  Same outputs as cv_weights_kernel.
+constexpr int WWPB = 8;  // frames (warps) per CTA
+
+__global__ void __launch_bounds__(WWPB * 32)
+cv_weights_warp_kernel(int T, int t0, double lam, double cutoff, int cap, int ld, const int* __restrict__ rowlo,
+                       const int* __restrict__ rowcnt, const double* __restrict__ D, const double* __restrict__ q,
+                       const double* __restrict__ R, const double* __restrict__ fwbar,
+                       const double* __restrict__ lwbar, double* __restrict__ s_out, double* __restrict__ z_out,
+                       int* __restrict__ sig_idx, double* __restrict__ sig_coef, int* __restrict__ nsig,
+                       double* __restrict__ fvec, uint8_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int tl = blockIdx.x * WWPB + (threadIdx.x >> 5);
+  if (tl >= T) return;
+  const int t = t0 + tl;
+  const int nrow = rowcnt[t], off = rowlo[t];
+  const double* Dt = D + (int64_t)t * ld;
+  double dmin = INFINITY;
+  bool finite = true;
+  for (int i = lane; i < nrow; i += 32) {
+    const double d = Dt[i];
+    finite = finite && isfinite(d);
+    dmin = fmin(dmin, d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+  const bool nonfinite = __any_sync(0xffffffffu, !finite);
+  double zs = 0.0, qs = 0.0;
+  for (int i = lane; i < nrow; i += 32) {
+    const double e = exp(-lam * (Dt[i] - dmin));
+    zs += e;
+    qs += q[off + i] * e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    zs += __shfl_xor_sync(0xffffffffu, zs, o);
+    qs += __shfl_xor_sync(0xffffffffu, qs, o);
+  }
+  const double sval = qs / zs;
+  const double zval = dmin - log(zs) / lam;
+  double acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+  int total = 0;
+  for (int b0 = 0; b0 < nrow; b0 += 32) {
+    const int i = b0 + lane;
+    const double di = i < nrow ? Dt[i] : 0.0;
+    const bool sig = i < nrow && lam * (di - dmin) <= cutoff;
+    const unsigned bal = __ballot_sync(0xffffffffu, sig);
+    if (sig) {
+      const int pos = total + __popc(bal & ((1u << lane) - 1u));
+      const double p = exp(-lam * (di - dmin)) / zs;
+      const int li = off + i;
+      const double cs = -lam * p * (q[li] - sval);
+      const double cz = p;
+      double Rh[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) Rh[e] = R[((int64_t)t * ld + i) * 9 + e];
+      if (pos < cap) {
+        sig_idx[(int64_t)tl * cap + pos] = li;
+        double* co = sig_coef + ((int64_t)tl * cap + pos) * 18;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) { co[e] = cs * Rh[e]; co[9 + e] = cz * Rh[e]; }
+      }
+      acc[0] += cs;
+      acc[1] += cz;
+      const double wb0 = lwbar[3 * li], wb1 = lwbar[3 * li + 1], wb2 = lwbar[3 * li + 2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double rw = Rh[a * 3] * wb0 + Rh[a * 3 + 1] * wb1 + Rh[a * 3 + 2] * wb2;
+        acc[2 + a] += cs * rw;
+        acc[5 + a] += cz * rw;
+      }
+    }
+    total += __popc(bal);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  if (lane != 0) return;
+  s_out[t] = sval;
+  z_out[t] = zval;
+  nsig[tl] = min(total, cap);
+  double* fv = fvec + (int64_t)tl * FVEC;
+  fv[0] = acc[0];
+  fv[1] = acc[1];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    fv[2 + a] = 2.0 * (acc[0] * fwbar[3 * t + a] - acc[2 + a]);
+    fv[5 + a] = 2.0 * (acc[1] * fwbar[3 * t + a] - acc[5 + a]);
+  }
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr) fv[8 + rr] = 0.0;
+  if (flags) {
+    uint8_t f = 0;
+    if (total > cap) f |= kFlagSigOverflow;
+    if (nonfinite || !isfinite(sval) || !isfinite(zval)) f |= kFlagNonFinite;
+    flags[tl] = f;
+  }
+}
+
 cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
                               const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
@@ -270,6 +374,11 @@ cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, i
                               int* sig_idx, double* sig_coef, int* nsig, double* fvec, uint8_t* flags,
                               cudaStream_t stream, const int* nb_idx, const int* nb_row, int nb_m, int dmode) {
   if (T <= 0) return cudaSuccess;
+  if (!refresh && !nb_idx && dmode == 0 && rowlo && rowcnt) {
+    cv_weights_warp_kernel<<<(T + WWPB - 1) / WWPB, WWPB * 32, 0, stream>>>(
+        T, t0, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, s, z, sig_idx, sig_coef, nsig, fvec, flags);
+    return cudaGetLastError();
+  }
   cv_weights_kernel<<<T, WNT, 0, stream>>>(T, t0, L, lam, cutoff, cap, ld, NbArgs{nb_idx, nb_row, nb_m, dmode}, rowlo,
                                            rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
                                            xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
