@@ -203,16 +203,19 @@ int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const 
  *   pair) interleaved, hl [3, count, 2 kpad] (kpad % 32 == 0), per 32-atom block
  *   [hi x32 | lo x32] = one 128 B line; terms = 1 -> hi only, hl [3, count, kpad]
  *   (kpad % 64 == 0).  scale_inv[count] = 2^-e; opnorm[count] (nullable) = the fp64
- *   2-norm of the (weighted, centred) operand, for the one-term error bound.
+ *   2-norm of the (weighted, centred) operand and rnorm[count] (nullable, terms = 1)
+ *   the 2-norm of its half-precision rounding residual, for the one-term error bound.
  * mc_msd_f16 / mc_msd_f16_2sm: as mc_msd_tf32 / _2sm on hl operands, S rescaled by
  *   fscale[t] * lscale[l] (exact) before the epilogue.  terms = 3: hi*hi + hi*lo +
  *   lo*hi (split precision); terms = 1: hi*hi, a screening estimate with
- *   |D_est - D| <= 4 (2^-10 + n 2^-27) opnorm_t opnorm_l (+ fp32 epilogue slack);
+ *   |D_est - D| <= 4 ||dS||_F, ||dS||_F <= rn_t op_l + op_t rn_l + rn_t rn_l
+ *   + n 2^-27 (op_t + rn_t)(op_l + rn_l) (op = opnorm, rn = rnorm; rn <= 2^-11 op)
+ *   (+ fp32 epilogue slack);
  *   _2sm supports terms = 3 only. */
 int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
                       const double* w_disp, int32_t weighted, int32_t terms, void* hl, double* scale_inv,
-                      double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
-                      void* stream);
+                      double* opnorm, double* rnorm, double* centroid, double* gnorm, double* wbar, double* mom,
+                      uint8_t* flags, void* stream);
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
                const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const int32_t* tlist,
                const int32_t* nlist, float* D, int64_t ldd, int32_t grid, void* stream);
@@ -224,7 +227,10 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
                   float* dmin, uint8_t* flags, void* stream);
 /* Metric pruning of the screen (csrc/prune.cu):
  * mc_prune_plan: from the one-term estimate Dc [T, C] against a coarse landmark subset
- *   (coarse landmark c = landmark c * cstride), its error bound c_unit * fnorm[t] * cnorm[c],
+ *   (coarse landmark c = landmark c * cstride), its error bound c_unit * fnorm[t] * cnorm[c]
+ *   (or, with the rounding-residual norms frnorm / crnorm of mc_center_split16, the
+ *   per-pair bound 5 (r_t o_c + o_t r_c + r_t r_c) + c_unit (o_t + r_t)(o_c + r_c)
+ *   + 1e-6 o_t o_c, c_unit = 5 n 2^-27),
  *   and mind / maxd [C, ntl] = min / max over each 48-landmark tile of the exact RMSD
  *   coarse->landmark, the hull [hull_lo, hull_hi) of landmark tiles that can hold a
  *   landmark within cutoff of D_min (thr = cutoff / lam, D units; knear <= 8 nearest
@@ -237,7 +243,7 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
  *   sorted row's landmark range [row_lo, row_hi) for mc_candidates(rlo, rhi).
  * mc_gather_rows: dst[r] = src[idx[r]] for rows of rowlen elements of esz bytes. */
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
-                  double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
+                  const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
                   int32_t knear, int32_t wide, int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream);
 int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,
                   int32_t BL, int32_t L, int32_t* tlist, int32_t* nlist, int32_t* row_lo, int32_t* row_hi,

@@ -202,13 +202,13 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
 }
 
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
-                  double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
+                  const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
                   int32_t knear, int32_t wide, int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream) {
   if (T < 0 || C < 1 || C > 1024 || lddc < C || ntl < 1 || knear < 1 || knear > 8 || !(c_unit >= 0.0) ||
-      !(thr >= 0.0) || (maxd && cstride < 1))
+      !(thr >= 0.0) || (maxd && cstride < 1) || ((frnorm == nullptr) != (crnorm == nullptr)))
     return MC_ERR_CONFIG;
   if (T > 0 && (!Dc || !fnorm || !cnorm || !mind || !hull_lo || !hull_hi || !key)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, c_unit, mind, maxd, cstride, ntl, thr, knear,
+  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, frnorm, crnorm, c_unit, mind, maxd, cstride, ntl, thr, knear,
                                            wide, hull_lo, hull_hi, key, S_(stream)));
 }
 
@@ -321,15 +321,16 @@ int mc_msd_tf32(const float* fhi, const float* flo, const float* lhi, const floa
 
 int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, int32_t kpad, const double* w_align,
                       const double* w_disp, int32_t weighted, int32_t terms, void* hl, double* scale_inv,
-                      double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom, uint8_t* flags,
-                      void* stream) {
+                      double* opnorm, double* rnorm, double* centroid, double* gnorm, double* wbar, double* mom,
+                      uint8_t* flags, void* stream) {
   if (dtype != MC_F32 && dtype != MC_F64) return MC_ERR_CONFIG;
   if (n < 2) return MC_ERR_INVALID_STRUCTURE;
   if (terms != 1 && terms != 3) return MC_ERR_CONFIG;
   if (count < 0 || kpad < n || kpad % (terms == 1 ? 64 : 32) != 0) return MC_ERR_CONFIG;
   if (count > 0 && (!coords || !w_align || !w_disp || !hl || !scale_inv || !gnorm)) return MC_ERR_CONFIG;
   return cuda_status(mc::launch_center_split16(coords, dtype, count, n, kpad, w_align, w_disp, weighted, terms, hl,
-                                               scale_inv, opnorm, centroid, gnorm, wbar, mom, flags, S_(stream)));
+                                               scale_inv, opnorm, rnorm, centroid, gnorm, wbar, mom, flags,
+                                               S_(stream)));
 }
 
 static int msd_f16_args(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,

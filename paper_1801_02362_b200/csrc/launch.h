@@ -102,13 +102,13 @@ cudaError_t launch_msd_tf32(const float* fh, const float* fl, const float* lh, c
                             cudaStream_t stream);
 cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
                                   const double* w_disp, int weighted, int terms, void* hl, double* scale_inv,
-                                  double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom,
-                                  uint8_t* flags, cudaStream_t stream);
+                                  double* opnorm, double* rnorm, double* centroid, double* gnorm, double* wbar,
+                                  double* mom, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
                            const double* ga, int T, int L, int kpad, int terms, float* D, int64_t ldd, int grid,
                            cudaStream_t stream, const int* tlist = nullptr, const int* nlist = nullptr);
 cudaError_t launch_prune_plan(const float* Dc, int T, int C, int64_t lddc, const double* fnorm, const double* cnorm,
-                              double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
+                              const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
                               int knear, int wide, int* hull_lo, int* hull_hi, int* key, cudaStream_t stream);
 cudaError_t launch_band_tiles(const int* perm, int T, const int* hull_lo, const int* hull_hi, int BM, int BL, int L,
                               int* tlist, int* nlist, int* row_lo, int* row_hi, cudaStream_t stream);

@@ -33,17 +33,26 @@ constexpr int KNEAR_MAX = 8;
 
 __global__ void __launch_bounds__(PNT)
 prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, const double* __restrict__ fnorm,
-                  const double* __restrict__ cnorm, double c_unit, const float* __restrict__ mind,
+                  const double* __restrict__ cnorm, const double* __restrict__ frnorm,
+                  const double* __restrict__ crnorm, double c_unit, const float* __restrict__ mind,
                   const float* __restrict__ maxd, int cstride, int ntl, double thr, int knear, int wide,
                   int* __restrict__ hull_lo, int* __restrict__ hull_hi, int* __restrict__ key) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (PNT / 32) + (threadIdx.x >> 5);
   if (t >= T) return;
   const float* row = Dc + (int64_t)t * lddc;
-  const double ef = c_unit * fnorm[t];
+  // rigorous one-term error of the pair (t, c): legacy c_unit ||x|| ||c||, or with the
+  // rounding-residual norms 5 (r_t |c| + |x| r_c + r_t r_c) + c_unit (|x| + r_t)(|c| + r_c)
+  // + 1e-6 |x| |c|  (c_unit = 5 n 2^-27: the fp32 accumulation term)
+  const double p1 = fnorm[t], p2 = frnorm ? frnorm[t] : 0.0;
+  auto ebound = [&](int c) -> double {
+    if (!frnorm) return c_unit * p1 * cnorm[c];
+    const double q1 = cnorm[c], q2 = crnorm[c];
+    return 5.0 * (p2 * q1 + p1 * q2 + p2 * q2) + c_unit * (p1 + p2) * (q1 + q2) + 1e-6 * p1 * q1;
+  };
   // D_min upper bound over all landmarks (the coarse ones are a subset)
   double dub = INFINITY;
-  for (int c = lane; c < C; c += 32) dub = fmin(dub, (double)row[c] + ef * cnorm[c]);
+  for (int c = lane; c < C; c += 32) dub = fmin(dub, (double)row[c] + ebound(c));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dub = fmin(dub, __shfl_xor_sync(0xffffffffu, dub, o));
   // the knear nearest coarse landmarks (by estimate), with their distance upper bounds
@@ -65,7 +74,7 @@ prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, cons
       if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
     }
     near[k] = bc;
-    dhi[k] = bc < C ? sqrt(fmax(0.0, (double)row[bc] + ef * cnorm[bc])) : INFINITY;
+    dhi[k] = bc < C ? sqrt(fmax(0.0, (double)row[bc] + ebound(bc))) : INFINITY;
     if (bc < C && (bc & 31) == lane && (bc >> 5) < 32) taken_lo |= 1u << (bc >> 5);
   }
   // admissible hull of landmark tiles
@@ -84,7 +93,7 @@ prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, cons
       const int c0 = max(0, (tau * 48 - 48 + cstride - 1) / cstride);
       const int c1 = min(C - 1, (tau * 48 + 95) / cstride);
       for (int c = c0; c <= c1; ++c) {
-        const double dlo = sqrt(fmax(0.0, (double)row[c] - ef * cnorm[c]));
+        const double dlo = sqrt(fmax(0.0, (double)row[c] - ebound(c)));
         const double g = fmax(0.0, dlo - (double)maxd[(int64_t)c * ntl + tau]);
         lb = fmax(lb, g * g);
       }
@@ -175,12 +184,13 @@ __global__ void gather_rows_kernel(const E* __restrict__ src, int64_t rowlen, co
 }
 
 cudaError_t launch_prune_plan(const float* Dc, int T, int C, int64_t lddc, const double* fnorm, const double* cnorm,
-                              double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
+                              const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
                               int knear, int wide, int* hull_lo, int* hull_hi, int* key, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
   if (knear > KNEAR_MAX) knear = KNEAR_MAX;
   prune_plan_kernel<<<(T + PNT / 32 - 1) / (PNT / 32), PNT, 0, stream>>>(
-      Dc, T, C, lddc, fnorm, cnorm, c_unit, mind, maxd, cstride, ntl, thr, knear, wide, hull_lo, hull_hi, key);
+      Dc, T, C, lddc, fnorm, cnorm, frnorm, crnorm, c_unit, mind, maxd, cstride, ntl, thr, knear, wide, hull_lo,
+      hull_hi, key);
   return cudaGetLastError();
 }
 

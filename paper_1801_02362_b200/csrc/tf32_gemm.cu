@@ -51,6 +51,7 @@ __device__ __forceinline__ float tf32_rna(float v) {
 struct OpTF32 {
   using E = float;
   static constexpr bool kInterleave = false;
+  static __device__ __forceinline__ double value(E h) { return (double)h; }
   static __device__ __forceinline__ void split(double v, E& h, E& l) {
     h = tf32_rna((float)v);
     l = tf32_rna((float)(v - (double)h));
@@ -58,6 +59,7 @@ struct OpTF32 {
 };
 struct OpF16 {
   using E = __half;
+  static __device__ __forceinline__ double value(E h) { return (double)__half2float(h); }
   // rows of 2 kpad halves: per 32-atom block [hi x32 | lo x32] = one 128 B
   // line, so one SWIZZLE_128B TMA box row carries both parts of a k-block.
   // One-term mode (lo == nullptr on entry, see below): rows of kpad hi halves.
@@ -74,7 +76,8 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
                     const double* __restrict__ w_disp, int weighted, typename OP::E* __restrict__ hi,
                     typename OP::E* __restrict__ lo, double* __restrict__ scale_inv, double* __restrict__ centroid,
                     double* __restrict__ gnorm, double* __restrict__ wbar, double* __restrict__ mom,
-                    uint8_t* __restrict__ flags, int one_term = 0, double* __restrict__ opnorm = nullptr) {
+                    uint8_t* __restrict__ flags, int one_term = 0, double* __restrict__ opnorm = nullptr,
+                    double* __restrict__ rnorm = nullptr) {
   __shared__ double scratch[NT / 32];
   const int64_t b = blockIdx.x;
   const T* x = coords + b * (int64_t)n * 3;
@@ -111,6 +114,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
     if (threadIdx.x == 0) scale_inv[b] = ldexp(1.0, -e);
   }
   double g = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, m00 = 0, m01 = 0, m02 = 0, m11 = 0, m12 = 0, m22 = 0, on2 = 0.0;
+  double rn2 = 0.0;  // one-term: squared 2-norm of the operand's rounding residual
   const int64_t plane = B * (int64_t)kpad;
   for (int j = threadIdx.x; j < kpad; j += NT) {
     double v[3] = {0.0, 0.0, 0.0};
@@ -135,6 +139,8 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
       OP::split(val, h, l);
       if (OP::kInterleave && one_term) {
         hi[p * plane + b * kpad + j] = h;
+        const double rd = OP::value(h) / scale - uv;
+        rn2 += rd * rd;
       } else if (OP::kInterleave) {
         const int64_t o = 2 * (p * plane + b * kpad) + (j >> 5) * 64 + (j & 31);
         hi[o] = h;
@@ -147,6 +153,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
   }
   g = block_sum<NT>(g, scratch);
   if (opnorm) on2 = block_sum<NT>(on2, scratch);
+  if (rnorm) rn2 = block_sum<NT>(rn2, scratch);
   if (wbar) { b0 = block_sum<NT>(b0, scratch); b1 = block_sum<NT>(b1, scratch); b2 = block_sum<NT>(b2, scratch); }
   if (mom) {
     m00 = block_sum<NT>(m00, scratch); m01 = block_sum<NT>(m01, scratch); m02 = block_sum<NT>(m02, scratch);
@@ -162,6 +169,7 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
     }
     if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
     if (opnorm) opnorm[b] = sqrt(on2);
+    if (rnorm) rnorm[b] = sqrt(rn2);
   }
 }
 
@@ -198,8 +206,8 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
                           const double* __restrict__ w_align, const double* __restrict__ w_disp,
                           __half* __restrict__ hi, double* __restrict__ scale_inv, double* __restrict__ centroid,
                           double* __restrict__ gnorm, double* __restrict__ wbar, uint8_t* __restrict__ flags,
-                          double* __restrict__ opnorm) {
-  __shared__ double scratch[5 * (CSF_NT / 32)];
+                          double* __restrict__ opnorm, double* __restrict__ rnorm) {
+  __shared__ double scratch[6 * (CSF_NT / 32)];
   const int64_t b = blockIdx.x;
   const float4* x4 = reinterpret_cast<const float4*>(coords + b * (int64_t)n * 3);
   const int G = n / 4;
@@ -232,7 +240,8 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
   const double scale = ldexp(1.0, e);
   const int64_t plane = B * (int64_t)kpad;
   __half* h0 = hi + b * kpad;
-  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // g, wbar (3), |operand|^2
+  double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // g, wbar (3), |operand|^2, |rounding residual|^2
+  const double sinv = ldexp(1.0, -e);
 #pragma unroll 2
   for (int gi = threadIdx.x; gi < kpad / 4; gi += CSF_NT) {
     uint2 o[3] = {make_uint2(0u, 0u), make_uint2(0u, 0u), make_uint2(0u, 0u)};
@@ -250,6 +259,8 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
           acc[1 + p] += wd * v;
           acc[4] += v * v;
           h[p][a] = __double2half(v * scale);
+          const double rd = (double)__half2float(h[p][a]) * sinv - v;
+          acc[5] += rd * rd;
         }
       }
 #pragma unroll
@@ -258,13 +269,14 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
 #pragma unroll
     for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(h0 + p * plane + 4 * gi) = o[p];
   }
-  block_sum_n<CSF_NT, 5>(acc, scratch);
+  block_sum_n<CSF_NT, 6>(acc, scratch);
   if (threadIdx.x == 0) {
     if (centroid) { centroid[3 * b] = c[0]; centroid[3 * b + 1] = c[1]; centroid[3 * b + 2] = c[2]; }
     gnorm[b] = acc[0];
     if (wbar) { wbar[3 * b] = acc[1]; wbar[3 * b + 1] = acc[2]; wbar[3 * b + 2] = acc[3]; }
     if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
     if (opnorm) opnorm[b] = sqrt(acc[4]);
+    if (rnorm) rnorm[b] = sqrt(acc[5]);
     scale_inv[b] = ldexp(1.0, -e);
   }
 }
@@ -284,25 +296,25 @@ cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n,
 
 cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
                                   const double* w_disp, int weighted, int terms, void* hl, double* scale_inv,
-                                  double* opnorm, double* centroid, double* gnorm, double* wbar, double* mom,
-                                  uint8_t* flags, cudaStream_t stream) {
+                                  double* opnorm, double* rnorm, double* centroid, double* gnorm, double* wbar,
+                                  double* mom, uint8_t* flags, cudaStream_t stream) {
   if (B <= 0) return cudaSuccess;
   const int one = terms == 1 ? 1 : 0;
   if (dtype == 0 && one && !weighted && !mom && n % 4 == 0 && kpad % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(coords) & 15) == 0 && B <= 0x7fffffffLL) {
     center_split_f16x1_kernel<<<(unsigned)B, CSF_NT, 0, stream>>>((const float*)coords, B, n, kpad, w_align, w_disp,
                                                                   (__half*)hl, scale_inv, centroid, gnorm, wbar,
-                                                                  flags, opnorm);
+                                                                  flags, opnorm, rnorm);
     return cudaGetLastError();
   }
   if (dtype == 0)
     center_split_kernel<float, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
         (const float*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
-        gnorm, wbar, mom, flags, one, opnorm);
+        gnorm, wbar, mom, flags, one, opnorm, rnorm);
   else
     center_split_kernel<double, OpF16, 256><<<(unsigned)B, 256, 0, stream>>>(
         (const double*)coords, B, n, kpad, w_align, w_disp, weighted, (__half*)hl, nullptr, scale_inv, centroid,
-        gnorm, wbar, mom, flags, one, opnorm);
+        gnorm, wbar, mom, flags, one, opnorm, rnorm);
   return cudaGetLastError();
 }
 

@@ -361,11 +361,18 @@ class PathCVTC:
             # Cauchy-Schwarz per entry; n 2^-27: fp32 tensor-core accumulation), x1.25
             # safety, + fp32-eigenvector Rayleigh slack.  The window threshold of frame t
             # grows by 2 lam c ||x_t|| max_l ||w a_l|| (pair error + D_min error).
+            # With the measured rounding residuals r = ||fl16(v) - v|| of both operands
+            # (typically ~0.4 u ||v||) the same argument gives, per pair,
+            #   ||dS||_F <= r_t o_l + o_t r_l + r_t r_l + n 2^-27 (o_t + r_t)(o_l + r_l)
+            # (o = operand 2-norm), i.e. |D_est - D| <= e_tl = 5 (r_t o_l + o_t r_l + r_t r_l)
+            # + kacc (o_t + r_t)(o_l + r_l) + 1e-6 o_t o_l with kacc = 5 n 2^-27 -- about
+            # half the u-based bound; frame t's window allowance is 2 lam max_l e_tl.
             u = 2.0 ** -11
             c_unit = 4.0 * (2 * u + u * u + self.n * 2.0 ** -27) * 1.25 + 1e-6
             self.na_max = float(self.ls.opnorm.max().item())
-            self.fcoef = 2.0 * self.lam * c_unit * self.na_max
-            self.c_unit = c_unit
+            self.nr_max = float(self.ls.rnorm.max().item())
+            self.kacc = 5.0 * self.n * 2.0 ** -27
+            self.c_unit = c_unit  # the u-based bound (reported by the tests beside e_tl)
             self.margin = 2.0
         # metric pruning of the screen: one-term screen only,
         # worthwhile when there are many landmark tiles
@@ -375,6 +382,13 @@ class PathCVTC:
                       and bool(torch.equal(self.w, self.wa)))
         if self.prune:
             self._init_prune(int(coarse_stride), int(knear))
+
+    def frame_bound(self, fs):
+        """max_l e_tl: the one-term estimate error bound of frame t against any landmark
+        (the per-pair bound with the landmark norms at their maxima)."""
+        o, r = fs.opnorm, fs.rnorm
+        A, dA = self.na_max, self.nr_max
+        return (5.0 * (r * (A + dA) + o * dA) + self.kacc * (o + r) * (A + dA) + 1e-6 * o * A).contiguous()
 
     def _init_prune(self, stride, knear):
         """Coarse landmark subset (every `stride`-th, <= 1024), its one-term split, and
@@ -440,8 +454,9 @@ class PathCVTC:
         split, the unsorted split, the row ranges and perm0 (sorted position -> frame)."""
         fr0, fs0 = self._frames(frames, 1, check=False)
         Dc = K.msd_estimate(fs0, self.ls_coarse, grid=K2_GRID)
-        hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.c_unit, self.mind,
-                                     (self.cutoff + 2.0) / self.lam, self.knear, maxd=self.maxd, cstride=self.cstride)
+        hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.kacc, self.mind,
+                                     (self.cutoff + 2.0) / self.lam, self.knear, maxd=self.maxd, cstride=self.cstride,
+                                     frnorm=fs0.rnorm, crnorm=self.ls_coarse.rnorm)
         ntl = self.mind.shape[1]
         perm0 = K.sort_by_key(key, ntl + 1)
         # sorted view of the split (operand rows + scalars gathered, no second split); the
@@ -465,7 +480,8 @@ class PathCVTC:
             # the whole pipeline is enqueued without host round trips; the status
             # flags of every stage are reduced on the device and read once at the end
             lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
-                                              fnorm=fs.opnorm if one else None, fcoef=self.fcoef if one else 0.0,
+                                              fnorm=self.frame_bound(fs) if one else None,
+                                              fcoef=2.0 * self.lam if one else 0.0,
                                               rlo=rlo, rhi=rhi)
             # refine groups: frames sorted by window centre (32-frame unions stay tight)
             perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)

@@ -293,7 +293,8 @@ def sig_span_key(wres, L):
     return torch.where(ns > 0, first + last, torch.full_like(first, 2 * L)).contiguous()
 
 
-def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None, maxd=None, cstride=0):
+def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None, maxd=None, cstride=0, frnorm=None,
+               crnorm=None):
     """Per-frame admissible landmark-tile hulls of the metric-pruned screen (csrc/prune.cu)."""
     T, C = Dc.shape
     ntl = mind.shape[1]
@@ -302,8 +303,9 @@ def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None, maxd=Non
     hhi = torch.empty((T,), dtype=I32, device=dev)
     key = torch.empty((T,), dtype=I32, device=dev)
     wide = max(1, (3 * ntl) // 4) if wide is None else int(wide)
-    call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), float(c_unit), ptr(mind), ptr(maxd),
-         int(cstride), ntl, float(thr), int(knear), wide, ptr(hlo), ptr(hhi), ptr(key), stream_ptr())
+    call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), ptr(frnorm), ptr(crnorm),
+         float(c_unit), ptr(mind), ptr(maxd), int(cstride), ntl, float(thr), int(knear), wide, ptr(hlo), ptr(hhi),
+         ptr(key), stream_ptr())
     return hlo, hhi, key
 
 
@@ -336,7 +338,7 @@ def gather_split(sp, idx):
             call("mc_gather_rows", ptr(sp.lo[p]), 4, sp.lo.shape[2], ptr(idx), rows, ptr(lo[p]), stream_ptr())
     g = lambda x: None if x is None else gather_rows(x, idx)  # noqa: E731
     return Split(hi, lo, g(sp.centroid), g(sp.g), g(sp.wbar), g(sp.mom), sp.flags, sp.n, sp.kpad, g(sp.scale),
-                 sp.fmt, sp.terms, g(sp.opnorm))
+                 sp.fmt, sp.terms, g(sp.opnorm), g(sp.rnorm))
 
 
 def gather_rows(src, idx):
@@ -405,12 +407,13 @@ class Split:
     interleaved tensor hi [3, B, 2 kpad] of scaled IEEE halves (lo None) with
     scale = 2^-e per structure; + per-structure scalars."""
 
-    __slots__ = ("hi", "lo", "scale", "fmt", "terms", "opnorm", "centroid", "g", "wbar", "mom", "flags", "n", "kpad",
-                 "count")
+    __slots__ = ("hi", "lo", "scale", "fmt", "terms", "opnorm", "rnorm", "centroid", "g", "wbar", "mom", "flags", "n",
+                 "kpad", "count")
 
-    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale=None, fmt="tf32", terms=3, opnorm=None):
+    def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale=None, fmt="tf32", terms=3, opnorm=None,
+                 rnorm=None):
         self.hi, self.lo, self.centroid, self.g, self.wbar, self.mom, self.flags = hi, lo, centroid, g, wbar, mom, flags
-        self.scale, self.fmt, self.terms, self.opnorm = scale, fmt, terms, opnorm
+        self.scale, self.fmt, self.terms, self.opnorm, self.rnorm = scale, fmt, terms, opnorm, rnorm
         self.n, self.kpad, self.count = n, kpad, hi.shape[1]
 
 
@@ -430,11 +433,12 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, ter
     kpad = kpad_for(n, fmt, terms)
     dev = coords.device
     dt = _lib.MC_F64 if coords.dtype == torch.float64 else _lib.MC_F32
-    opnorm = None
+    opnorm = rnorm = None
     if fmt == "f16":  # interleaved [hi x32 | lo x32] rows (one-term: hi rows)
         hi = torch.empty((3, b, kpad if terms == 1 else 2 * kpad), dtype=torch.float16, device=dev)
         lo = None
         opnorm = torch.empty((b,), dtype=F64, device=dev)
+        rnorm = torch.empty((b,), dtype=F64, device=dev) if terms == 1 else None
     else:
         hi = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
         lo = torch.empty((3, b, kpad), dtype=torch.float32, device=dev)
@@ -446,12 +450,12 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, ter
     flags = torch.empty((b,), dtype=U8, device=dev)
     if fmt == "f16":
         call("mc_center_split16", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
-             terms, ptr(hi), ptr(scale), ptr(opnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags),
-             stream_ptr())
+             terms, ptr(hi), ptr(scale), ptr(opnorm), ptr(rnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(mom),
+             ptr(flags), stream_ptr())
     else:
         call("mc_center_split", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
              ptr(hi), ptr(lo), ptr(centroid), ptr(g), ptr(wbar), ptr(mom), ptr(flags), stream_ptr())
-    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt, terms, opnorm)
+    return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt, terms, opnorm, rnorm)
 
 
 TF32_2SM = __import__("os").environ.get("MC_TF32_2SM", "0") == "1"

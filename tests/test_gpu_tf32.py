@@ -119,13 +119,21 @@ def test_one_term_screen_within_rigorous_bound(T, L, n, cuda_device):
     est, _, fs = pcv.estimate(wl.frames, terms=1)
     est = est.cpu().numpy().astype(np.float64)
     ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64))
-    nx = fs.opnorm.cpu().numpy()
-    na = pcv.ls.opnorm.cpu().numpy()
-    c_unit = pcv.fcoef / (2.0 * pcv.lam * pcv.na_max)
-    bound = c_unit * nx[:, None] * na[None, :]
+    nx, rx = fs.opnorm.cpu().numpy(), fs.rnorm.cpu().numpy()
+    na, ra = pcv.ls.opnorm.cpu().numpy(), pcv.ls.rnorm.cpu().numpy()
+    # the residual norms are at most u = 2^-11 of the operand norms
+    assert (rx <= 2.0 ** -11 * nx * (1 + 1e-12)).all() and (ra <= 2.0 ** -11 * na * (1 + 1e-12)).all()
+    o_t, r_t, o_l, r_l = nx[:, None], rx[:, None], na[None, :], ra[None, :]
+    bound = 5.0 * (r_t * o_l + o_t * r_l + r_t * r_l) + pcv.kacc * (o_t + r_t) * (o_l + r_l) + 1e-6 * o_t * o_l
+    ubound = pcv.c_unit * o_t * o_l
     err = np.abs(est - ref)
-    print(f"n={n}: max err {err.max():.3e}, max err/bound {np.max(err / bound):.3f}")
+    print(f"n={n}: max err {err.max():.3e}, max err/bound {np.max(err / bound):.3f}, "
+          f"bound/u-bound {np.median(bound / ubound):.3f}")
     assert (err <= bound).all()
+    assert np.median(bound / ubound) < 0.9  # the measured residuals tighten the u-based bound
+    # the per-frame allowance PathCVTC uses covers every pair of the frame
+    fb = pcv.frame_bound(fs).cpu().numpy()
+    assert (bound <= fb[:, None] * (1 + 1e-12)).all()
     assert dev.type == "cuda"
 
 
