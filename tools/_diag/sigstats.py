@@ -9,7 +9,7 @@ wl = synth.interp_config_device(4, T, 8192, 10000, 32, dev)
 pcv = engine.PathCVTC(torch.from_numpy(wl.landmarks).to(dev), wl.lam, wl.q)
 Dest, fr, fs, fs0, rlo, rhi, perm0 = pcv._pruned_estimate(wl.frames)
 cap = pcv.window_cap
-lo, cnt, _, _ = K.candidates(Dest, pcv.lam, pcv.cutoff + pcv.margin, cap, fnorm=fs.opnorm, fcoef=pcv.fcoef, rlo=rlo, rhi=rhi)
+lo, cnt, _, _ = K.candidates(Dest, pcv.lam, pcv.cutoff + pcv.margin, cap, fnorm=pcv.frame_bound(fs), fcoef=2.0 * pcv.lam, rlo=rlo, rhi=rhi)
 perm = K.sort_by_key(lo, pcv.L)
 Dex, Rex, _ = K.refine(fr, fs, pcv.lraw, pcv.ls, pcv.w, perm=perm, lo=lo, cnt=cnt, cap=cap, fmap=perm0, wuni=pcv.wuni)
 wres = K.pathcv_weights(Dex, pcv.q, pcv.lam, Rex, fs, pcv.ls, cap, pcv.cutoff, L=pcv.L, rowlo=lo, rowcnt=cnt)

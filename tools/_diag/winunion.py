@@ -9,7 +9,7 @@ wl = synth.interp_config_device(4, T, 8192, 10000, 32, dev)
 pcv = engine.PathCVTC(torch.from_numpy(wl.landmarks).to(dev), wl.lam, wl.q)
 Dest, fr, fs, fs0, rlo, rhi, perm0 = pcv._pruned_estimate(wl.frames)
 cap = pcv.window_cap
-lo, cnt, _, _ = K.candidates(Dest, pcv.lam, pcv.cutoff + pcv.margin, cap, fnorm=fs.opnorm, fcoef=pcv.fcoef, rlo=rlo, rhi=rhi)
+lo, cnt, _, _ = K.candidates(Dest, pcv.lam, pcv.cutoff + pcv.margin, cap, fnorm=pcv.frame_bound(fs), fcoef=2.0 * pcv.lam, rlo=rlo, rhi=rhi)
 lo = lo.cpu().numpy().astype(np.int64); cnt = cnt.cpu().numpy().astype(np.int64); hi = lo + cnt
 def pad(p, G=32, QL=32):
     a = lo[p].reshape(-1, G).min(1); b = hi[p].reshape(-1, G).max(1)
