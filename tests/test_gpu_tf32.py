@@ -184,3 +184,31 @@ def test_metric_pruned_screen_matches_unpruned_and_oracle(cuda_device):
     ref = O.batch_path_cv_exact(wl.frames[:40].astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
     np.testing.assert_allclose(oa["s"].cpu().numpy()[:40], ref["s"], rtol=1e-6)
     np.testing.assert_allclose(oa["z"].cpu().numpy()[:40], ref["z"], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("n,weights", [(333, "uniform"), (332, "equal"), (330, "split")])
+def test_pathcv_tc_ragged_atoms_and_weights(n, weights, cuda_device):
+    """The non-vector copy paths (N % 4 != 0), the centred-operand refine mode
+    (non-uniform weights) and the unpruned screen (alignment != displacement
+    weights) against the fp64 oracle: s, z 1e-6, gradients 1e-5."""
+    wl = synth.config4(T=36, L=768, N=n)
+    rng = np.random.default_rng(n)
+    w = wa = None
+    if weights == "equal":
+        w = wa = rng.uniform(0.5, 1.5, size=n)
+    elif weights == "split":
+        w = rng.uniform(0.5, 1.5, size=n)
+        wa = rng.uniform(0.5, 1.5, size=n)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam, w=w, w_align=wa)
+    assert pcv.prune == (weights != "split")
+    assert (pcv.wuni > 0) == (weights == "uniform")
+    out = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam, w=w,
+                                w_align=wa)
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    for key in ("ds", "dz"):
+        got, r = out[key].cpu().numpy(), ref[key]
+        scale = np.abs(r).reshape(r.shape[0], -1).max(axis=1)
+        err = np.abs(got - r).reshape(r.shape[0], -1).max(axis=1)
+        assert np.all(err <= 1e-5 * scale), f"{key}: worst rel {np.max(err / scale):.3e}"
