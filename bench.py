@@ -265,7 +265,7 @@ class ConfigTC:
     """Configs 2/4: fp32 path on tcgen05 (3xTF32 estimate) + exact fp64 refinement.
     Frames are sharded across ranks; landmarks are replicated (no collective)."""
 
-    def __init__(self, cfg, device, rank, world, frames_override=None):
+    def __init__(self, cfg, device, rank, world, frames_override=None, shard="frames"):
         import torch
 
         from paper_1801_02362_b200 import engine, synth
@@ -274,15 +274,30 @@ class ConfigTC:
         shp = dict(CONFIG_SHAPES[cfg])
         if frames_override:
             shp["T"] = frames_override
-        # weak scaling: every rank evaluates its own full-size frame set (disjoint
-        # slices of one global set), landmarks replicated, no data-path collective
-        T_all = world * shp["T"]
-        off, cnt = rank * shp["T"], shp["T"]
+        self.shard = shard
+        if shard == "landmarks":
+            # the north_star's variant: every rank holds all T
+            # frames and its landmark shard; per-frame minima / partials / straddling
+            # gradient rows are exchanged over NCCL; strong scaling (total work fixed)
+            if cfg != 4:
+                raise SystemExit("--shard landmarks applies to config 4 (path-CV)")
+            T_all, off, cnt = shp["T"], 0, shp["T"]
+        else:
+            # weak scaling: every rank evaluates its own full-size frame set (disjoint
+            # slices of one global set), landmarks replicated, no data-path collective
+            T_all = world * shp["T"]
+            off, cnt = rank * shp["T"], shp["T"]
         self.wl = synth.interp_config_device(shp["seed"], T_all, shp["L"], shp["N"], shp["n_endpoints"], device,
                                              frame_offset=off, frame_count=cnt)
         self.T_all, self.T = T_all, cnt
         self.n, self.L = shp["N"], shp["L"]
-        self.pcv = engine.PathCVTC(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q)
+        self.pcv = engine.PathCVTC(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q,
+                                   shard=(rank, world) if shard == "landmarks" else None)
+        if shard == "landmarks":
+            from paper_1801_02362_b200 import dist as Dd
+
+            self._comm = Dd.DistComm() if world > 1 else None
+            self.L_local = self.pcv.L
         self.frames_dev = self.wl.frames
         self.chunk = 24576
         try:
@@ -291,8 +306,13 @@ class ConfigTC:
         except RuntimeError:
             self.frames_host = self.frames_dev.cpu()
             self.host_kind = "pageable (pinning failed)"
-        self.parallelism = f"frame-sharded dp{world}" if world > 1 else "single"
-        self.scaling = "weak"
+        if shard == "landmarks":
+            self.parallelism = f"landmark-sharded x{world} (NCCL: per-frame min/partials + straddling rows)"
+            self.scaling = "strong"
+            self.replicated_units = True  # every rank evaluates the same T frames
+        else:
+            self.parallelism = f"frame-sharded dp{world}" if world > 1 else "single"
+            self.scaling = "weak"
         self.last = None
         if cfg == 2:
             self.metric, self.unit = "aligned-MSD pairs/s", "pairs/s"
@@ -304,6 +324,11 @@ class ConfigTC:
     def _step(self, frames, D=None):
         if self.cfg == 2:
             self.last = self.pcv.msd_matrix(frames) if D is None else self._msd_into(frames, D)
+        elif self.shard == "landmarks":
+            from paper_1801_02362_b200 import dist as Dd
+
+            steps = self.pcv.sharded_steps(frames, grad=True)
+            self.last = Dd.drive(steps, self._comm) if self._comm else Dd.drive_lockstep([steps])[0]
         else:
             self.last = self.pcv.evaluate(frames, grad=True)
         return self.last
@@ -459,6 +484,8 @@ class ConfigTC:
 
     def extra(self):
         d = {"pairs_per_step": self.T * self.L, "host_buffers": self.host_kind}
+        if self.shard == "landmarks":
+            d["landmarks_per_rank"] = self.pcv.L
         if self.cfg == 4 and self.last is not None:
             d["mean_window"] = float(self.last["window_cnt"].float().mean().item())
             d["mean_significant"] = float(self.last["nsig"].float().mean().item())
@@ -530,7 +557,7 @@ def run_ours(args, rank, world, local_rank):
     elif cfg == 3:
         runner = Config3(device, rank, world, args.walkers)
     else:
-        runner = ConfigTC(cfg, device, rank, world, args.frames)
+        runner = ConfigTC(cfg, device, rank, world, args.frames, args.shard)
     for _ in range(args.warmup):
         runner.step_device()
     torch.cuda.synchronize()
@@ -618,7 +645,7 @@ def run_ours(args, rank, world, local_rank):
     kernels = {k: {"launches": c, "ms_per_step": t / nprof, "share": t / total}
                for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     units = runner.units() * world if runner.scaling == "weak" else runner.units()
-    if dist and runner.scaling == "strong":
+    if dist and runner.scaling == "strong" and not getattr(runner, "replicated_units", False):
         t = torch.tensor([float(units)], device=device, dtype=torch.float64)
         dist.all_reduce(t)
         units = float(t.item())
@@ -759,6 +786,8 @@ def main():
     ap.add_argument("--frames", type=int, default=0, help="override T (configs 2/4) for quick runs")
     ap.add_argument("--walkers", type=int, default=0, help="override W (config 3) for quick runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
+    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks"],
+                    help="multi-GPU split of config 4: frames (weak, no collective) or landmarks (strong, NCCL)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

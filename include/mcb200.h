@@ -137,6 +137,16 @@ int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutof
                       const double* rxy, const double* xyeig, const double* gx, const double* ga, const double* lmom,
                       double* s, double* z, int32_t* sig_idx, double* sig_coef, int32_t* nsig, double* fvec,
                       uint8_t* flags, void* stream);
+/* Landmark-sharded evaluation (north_star "landmarks sharded ...
+ * all-reduce of the per-frame exp-weighted partial sums"): after the host merged every
+ * shard's (s_g, z_g) into s, z, it rescales this shard's K4 coefficients to the global
+ * softmax, cs' = alpha (cs + beta cz), cz' = alpha cz with alpha[t] = Z_g / Z and
+ * beta[t] = -lam (s_g - s) -- sig_coef [T, cap, 18] (first nsig[t] entries) and fvec
+ * [T, 16] in place -- so mc_pathcv_grad_block then writes this shard's share of the
+ * global gradients (replaces the SPEC property_map gradient, for the
+ * shard's landmarks). */
+int mc_shard_rescale(int32_t T, int32_t cap, const int32_t* nsig, const double* alpha, const double* beta,
+                     double* sig_coef, double* fvec, void* stream);
 /* Neighbour-list variant of mc_pathcv_weights on dense rows (SPEC neighbourlist +
  * colvar active set): row t sums over the nb_m landmarks
  * nb_idx[nb_row[t] * nb_m ..] only.  dmode 1 writes the row distances (Eq. 5 on
@@ -169,7 +179,9 @@ int mc_pathcv_grad(int32_t T, int32_t t0, int32_t n, int32_t npad, int32_t cap, 
  *   fp64 Newton lambda_max in the epilogue -> MSD estimate D [T, ldd] fp32.  grid 0 = #SMs.
  * mc_candidates: per frame D_min and the landmark window {lam (D - D_min) <= thr_t},
  *   thr_t = thr + fcoef * fnorm[t] (fnorm nullable: thr_t = thr) -- the per-frame
- *   estimate-error allowance of the one-term screen.
+ *   estimate-error allowance of the one-term screen.  dref [T] (nullable): landmark-
+ *   sharded evaluation -- D_min = min(row minimum, dref[t]) with dref the minimum over
+ *   every shard's estimate; a shard holding no window landmark returns cnt = 0.
  * mc_sort_by_key: counting sort of frames by window start (workspace bins [nbins]).
  * mc_refine: exact fp64 covariance + fit of the in-window pairs (or, with lo = cnt =
  *   NULL, of all pairs: the dense exact MSD matrix into Dd).  lwbar [L, 3] (nullable)
@@ -223,8 +235,8 @@ int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const
                    const double* ga, int32_t T, int32_t L, int32_t kpad, float* D, int64_t ldd, int32_t grid,
                    void* stream);
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
-                  double fcoef, const int32_t* rlo, const int32_t* rhi, int32_t cap, int32_t* lo, int32_t* cnt,
-                  float* dmin, uint8_t* flags, void* stream);
+                  double fcoef, const int32_t* rlo, const int32_t* rhi, const float* dref, int32_t cap, int32_t* lo,
+                  int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
 /* Metric pruning of the screen (csrc/prune.cu):
  * mc_prune_plan: from the one-term estimate Dc [T, C] against a coarse landmark subset
  *   (coarse landmark c = landmark c * cstride), its error bound c_unit * fnorm[t] * cnorm[c]
@@ -238,13 +250,18 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
  *   1 + hull_lo).  Both triangle bounds d(t,l) >= d(c,l) - d(t,c) (knear nearest c) and
  *   d(t,l) >= d(t,c) - d(c,l) (c within one tile of the landmark tile; maxd nullable =
  *   first bound only) are applied; requires equal alignment / displacement weights.
+ *   Landmark-sharded evaluation: a first call with dub_out [T] and NULL hull outputs
+ *   writes this shard's D_min upper bound; the caller all-reduces the minimum over the
+ *   shards and passes it as dub_in [T] to the second call, where a frame with no
+ *   admissible tile in this shard gets the empty hull [ntl, 0) (key ntl).
  * mc_band_tiles: for the key-sorted order perm, the union hull of each 128-frame band,
  *   the (band, landmark tile) list tlist [*, 2] with its length *nlist (device), and each
  *   sorted row's landmark range [row_lo, row_hi) for mc_candidates(rlo, rhi).
  * mc_gather_rows: dst[r] = src[idx[r]] for rows of rowlen elements of esz bytes. */
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
                   const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
-                  int32_t knear, int32_t wide, int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream);
+                  int32_t knear, int32_t wide, const double* dub_in, double* dub_out, int32_t* hull_lo,
+                  int32_t* hull_hi, int32_t* key, void* stream);
 int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,
                   int32_t BL, int32_t L, int32_t* tlist, int32_t* nlist, int32_t* row_lo, int32_t* row_hi,
                   void* stream);

@@ -71,8 +71,10 @@ _SIGS = {
     "mc_msd_f16": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _I64, _I32, _P],
     "mc_msd_f16_2sm": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P],
     "mc_pathcv_grad_block": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
-    "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _P, _I32, _P, _P, _P, _P, _P],
-    "mc_prune_plan": [_P, _I32, _I32, _I64, _P, _P, _P, _P, _D, _P, _P, _I32, _I32, _D, _I32, _I32, _P, _P, _P, _P],
+    "mc_shard_rescale": [_I32, _I32, _P, _P, _P, _P, _P, _P],
+    "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
+    "mc_prune_plan": [_P, _I32, _I32, _I64, _P, _P, _P, _P, _D, _P, _P, _I32, _I32, _D, _I32, _I32, _P, _P, _P, _P, _P,
+                      _P],
     "mc_band_tiles": [_P, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
     "mc_gather_rows": [_P, _I32, _I64, _P, _I32, _P, _P],
     "mc_sort_by_key": [_P, _I32, _I32, _P, _P, _P],

@@ -91,6 +91,13 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
   return cuda_status(mc::launch_xy_eig(fplanes, gx, T, npad, w, refresh, ridx, xyeig, rxy, flags, S_(stream)));
 }
 
+int mc_shard_rescale(int32_t T, int32_t cap, const int32_t* nsig, const double* alpha, const double* beta,
+                     double* sig_coef, double* fvec, void* stream) {
+  if (T < 0 || cap < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!nsig || !alpha || !beta || !sig_coef || !fvec)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_shard_rescale(T, cap, nsig, alpha, beta, sig_coef, fvec, S_(stream)));
+}
+
 int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutoff, int32_t cap, int32_t ld, const int32_t* rowlo,
                       const int32_t* rowcnt, double* D, const double* q, const double* R, const double* fwbar,
                       const double* lwbar, const uint8_t* refresh, const int32_t* ridx, const double* S,
@@ -191,25 +198,32 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
 }
 
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
-                  double fcoef, const int32_t* rlo, const int32_t* rhi, int32_t cap, int32_t* lo, int32_t* cnt,
-                  float* dmin, uint8_t* flags, void* stream) {
+                  double fcoef, const int32_t* rlo, const int32_t* rhi, const float* dref, int32_t cap, int32_t* lo,
+                  int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
   if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0) || !(fcoef >= 0.0))
     return MC_ERR_CONFIG;
   if (T > 0 && (!D || !lo || !cnt)) return MC_ERR_CONFIG;
   if ((rlo == nullptr) != (rhi == nullptr)) return MC_ERR_CONFIG;
   return cuda_status(
-      mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, cap, lo, cnt, dmin, flags, S_(stream)));
+      mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, dref, cap, lo, cnt, dmin, flags,
+                                              S_(stream)));
 }
 
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,
                   const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int32_t cstride, int32_t ntl, double thr,
-                  int32_t knear, int32_t wide, int32_t* hull_lo, int32_t* hull_hi, int32_t* key, void* stream) {
+                  int32_t knear, int32_t wide, const double* dub_in, double* dub_out, int32_t* hull_lo,
+                  int32_t* hull_hi, int32_t* key, void* stream) {
   if (T < 0 || C < 1 || C > 1024 || lddc < C || ntl < 1 || knear < 1 || knear > 8 || !(c_unit >= 0.0) ||
       !(thr >= 0.0) || (maxd && cstride < 1) || ((frnorm == nullptr) != (crnorm == nullptr)))
     return MC_ERR_CONFIG;
-  if (T > 0 && (!Dc || !fnorm || !cnorm || !mind || !hull_lo || !hull_hi || !key)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, frnorm, crnorm, c_unit, mind, maxd, cstride, ntl, thr, knear,
-                                           wide, hull_lo, hull_hi, key, S_(stream)));
+  // bound-only pass: dub_out set, no hull outputs
+  const bool hulls = hull_lo || hull_hi || key;
+  if (T > 0 && (!Dc || !fnorm || !cnorm)) return MC_ERR_CONFIG;
+  if (T > 0 && hulls && (!mind || !hull_lo || !hull_hi || !key)) return MC_ERR_CONFIG;
+  if (T > 0 && !hulls && !dub_out) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_prune_plan(Dc, T, C, lddc, fnorm, cnorm, frnorm, crnorm, c_unit, mind, maxd, cstride,
+                                           ntl, thr, knear, wide, dub_in, dub_out, hull_lo, hull_hi, key,
+                                           S_(stream)));
 }
 
 int mc_band_tiles(const int32_t* perm, int32_t T, const int32_t* hull_lo, const int32_t* hull_hi, int32_t BM,

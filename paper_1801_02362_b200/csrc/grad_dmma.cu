@@ -157,6 +157,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     s_rsc[tid] = t < 0 ? 0.0 : s_fv[f][sz];
     s_rcorr[tid] = t < 0 ? 0.0 : s_fv[f][2 + sz * 3 + b];
     s_rx[tid] = f * 3 * DNA + b;
+    s_bias[tid] = 0.0;  // stays 0 when the group has no significant landmark (sharded: empty windows)
   }
   if (tid == 0) {
     int a = 0x7fffffff, b = -1;

@@ -30,6 +30,8 @@ cudaError_t launch_close_scan(const double* fpl, const double* gx, int walkers, 
 cudaError_t launch_xy_eig(const double* fpl, const double* gx, int64_t T, int npad, const double* w,
                           const uint8_t* refresh, const int* ridx, double* xyeig, double* rxy, uint8_t* flags,
                           cudaStream_t stream);
+cudaError_t launch_shard_rescale(int T, int cap, const int* nsig, const double* alpha, const double* beta,
+                                 double* sig_coef, double* fvec, cudaStream_t stream);
 cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
                               const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
@@ -75,7 +77,7 @@ cudaError_t launch_cv_grad_block_planes(int T, int t0, int n, int npad, int cap,
                                         const uint8_t* refresh, const int* ridx, const double* xyeig, void* ds,
                                         void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
-                              double fcoef, const int* rlo, const int* rhi, int cap, int* lo,
+                              double fcoef, const int* rlo, const int* rhi, const float* dref, int cap, int* lo,
                               int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
@@ -109,7 +111,8 @@ cudaError_t launch_msd_f16(const void* fhl, const void* lhl, const double* fsc, 
                            cudaStream_t stream, const int* tlist = nullptr, const int* nlist = nullptr);
 cudaError_t launch_prune_plan(const float* Dc, int T, int C, int64_t lddc, const double* fnorm, const double* cnorm,
                               const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
-                              int knear, int wide, int* hull_lo, int* hull_hi, int* key, cudaStream_t stream);
+                              int knear, int wide, const double* dub_in, double* dub_out, int* hull_lo, int* hull_hi,
+                              int* key, cudaStream_t stream);
 cudaError_t launch_band_tiles(const int* perm, int T, const int* hull_lo, const int* hull_hi, int BM, int BL, int L,
                               int* tlist, int* nlist, int* row_lo, int* row_hi, cudaStream_t stream);
 cudaError_t launch_gather_rows(const void* src, int esz, int64_t rowlen, const int* idx, int rows, void* dst,

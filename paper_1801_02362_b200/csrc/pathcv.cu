@@ -280,6 +280,18 @@ cv_weights_warp_kernel(int T, int t0, double lam, double cutoff, int cap, int ld
   if (tl >= T) return;
   const int t = t0 + tl;
   const int nrow = rowcnt[t], off = rowlo[t];
+  if (nrow == 0) {
+    // empty window: only in landmark-sharded evaluation (this shard holds no landmark
+    // near the frame): Z_g = 0, i.e. z_g = +inf, and no significant entries
+    if (lane < FVEC) fvec[(int64_t)tl * FVEC + lane] = 0.0;
+    if (lane == 0) {
+      s_out[t] = 0.0;
+      z_out[t] = INFINITY;
+      nsig[tl] = 0;
+      if (flags) flags[tl] = 0;
+    }
+    return;
+  }
   const double* Dt = D + (int64_t)t * ld;
   double dmin = INFINITY;
   bool finite = true;
@@ -382,6 +394,45 @@ cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, i
   cv_weights_kernel<<<T, WNT, 0, stream>>>(T, t0, L, lam, cutoff, cap, ld, NbArgs{nb_idx, nb_row, nb_m, dmode}, rowlo,
                                            rowcnt, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy,
                                            xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
+  return cudaGetLastError();
+}
+
+// Landmark-sharded evaluation: shard g computed s_g, z_g and
+// its coefficients cs, cz against its own landmarks.  With the merged s and
+// w_g = Z_g / Z, the global coefficients of its landmarks are
+//   cs' = w_g (cs - lam (s_g - s) cz) = alpha (cs + beta cz),   cz' = alpha cz,
+// and every per-entry / per-frame quantity of the gradient pass is linear in
+// (cs, cz): sig_coef [.., 0:9 | 9:18], fvec [0 | 1], [2:5 | 5:8], [8:12 | 12:16].
+__global__ void __launch_bounds__(256)
+shard_rescale_kernel(int T, int cap, const int* __restrict__ nsig, const double* __restrict__ alpha,
+                     const double* __restrict__ beta, double* __restrict__ sig_coef, double* __restrict__ fvec) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const double a = alpha[t], b = beta[t];
+  const int ns = nsig[t];
+  double* co = sig_coef + (int64_t)t * cap * 18;
+  for (int e = lane; e < ns * 9; e += 32) {
+    const int i = e / 9, k = e - 9 * i;
+    const double cs = co[i * 18 + k], cz = co[i * 18 + 9 + k];
+    co[i * 18 + k] = a * (cs + b * cz);
+    co[i * 18 + 9 + k] = a * cz;
+  }
+  if (lane < 8) {
+    // (s, z) pairs of fvec: (0, 1), (2..4, 5..7), (8..11, 12..15)
+    double* fv = fvec + (int64_t)t * FVEC;
+    const int is = lane == 0 ? 0 : (lane < 4 ? 1 + lane : 4 + lane);
+    const int iz = lane == 0 ? 1 : (lane < 4 ? 4 + lane : 8 + lane);
+    const double cs = fv[is], cz = fv[iz];
+    fv[is] = a * (cs + b * cz);
+    fv[iz] = a * cz;
+  }
+}
+
+cudaError_t launch_shard_rescale(int T, int cap, const int* nsig, const double* alpha, const double* beta,
+                                 double* sig_coef, double* fvec, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  shard_rescale_kernel<<<(T + 7) / 8, 256, 0, stream>>>(T, cap, nsig, alpha, beta, sig_coef, fvec);
   return cudaGetLastError();
 }
 

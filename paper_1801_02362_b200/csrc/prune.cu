@@ -36,7 +36,8 @@ prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, cons
                   const double* __restrict__ cnorm, const double* __restrict__ frnorm,
                   const double* __restrict__ crnorm, double c_unit, const float* __restrict__ mind,
                   const float* __restrict__ maxd, int cstride, int ntl, double thr, int knear, int wide,
-                  int* __restrict__ hull_lo, int* __restrict__ hull_hi, int* __restrict__ key) {
+                  const double* __restrict__ dub_in, double* __restrict__ dub_out, int* __restrict__ hull_lo,
+                  int* __restrict__ hull_hi, int* __restrict__ key) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (PNT / 32) + (threadIdx.x >> 5);
   if (t >= T) return;
@@ -55,6 +56,12 @@ prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, cons
   for (int c = lane; c < C; c += 32) dub = fmin(dub, (double)row[c] + ebound(c));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dub = fmin(dub, __shfl_xor_sync(0xffffffffu, dub, o));
+  // landmark-sharded evaluation: pass 1 writes this shard's bound (dub_out, no hulls),
+  // the host all-reduces the minimum, pass 2 prunes against it (dub_in) -- a shard
+  // far from the frame then admits no tile at all
+  if (dub_out && lane == 0) dub_out[t] = dub;
+  if (!hull_lo) return;
+  if (dub_in) dub = fmin(dub, dub_in[t]);
   // the knear nearest coarse landmarks (by estimate), with their distance upper bounds
   int near[KNEAR_MAX];
   double dhi[KNEAR_MAX];
@@ -106,7 +113,18 @@ prune_plan_kernel(const float* __restrict__ Dc, int T, int C, int64_t lddc, cons
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
   if (lane == 0) {
-    if (hi < lo) { lo = 0; hi = ntl - 1; }  // cannot happen (the nearest coarse tile is admissible); stay safe
+    if (hi < lo) {
+      if (dub_in) {
+        // sharded: no tile of this shard can hold a significant landmark; the empty
+        // hull [ntl, 0) neither widens a band's union nor its row range, and sorts last
+        hull_lo[t] = ntl;
+        hull_hi[t] = 0;
+        key[t] = ntl;
+        return;
+      }
+      lo = 0;  // cannot happen unsharded (the nearest coarse tile is admissible); stay safe
+      hi = ntl - 1;
+    }
     hull_lo[t] = lo;
     hull_hi[t] = hi + 1;
     // sort key: frames whose hull covers >= `wide` tiles first (they need almost
@@ -185,12 +203,13 @@ __global__ void gather_rows_kernel(const E* __restrict__ src, int64_t rowlen, co
 
 cudaError_t launch_prune_plan(const float* Dc, int T, int C, int64_t lddc, const double* fnorm, const double* cnorm,
                               const double* frnorm, const double* crnorm, double c_unit, const float* mind, const float* maxd, int cstride, int ntl, double thr,
-                              int knear, int wide, int* hull_lo, int* hull_hi, int* key, cudaStream_t stream) {
+                              int knear, int wide, const double* dub_in, double* dub_out, int* hull_lo, int* hull_hi,
+                              int* key, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
   if (knear > KNEAR_MAX) knear = KNEAR_MAX;
   prune_plan_kernel<<<(T + PNT / 32 - 1) / (PNT / 32), PNT, 0, stream>>>(
-      Dc, T, C, lddc, fnorm, cnorm, frnorm, crnorm, c_unit, mind, maxd, cstride, ntl, thr, knear, wide, hull_lo,
-      hull_hi, key);
+      Dc, T, C, lddc, fnorm, cnorm, frnorm, crnorm, c_unit, mind, maxd, cstride, ntl, thr, knear, wide, dub_in,
+      dub_out, hull_lo, hull_hi, key);
   return cudaGetLastError();
 }
 

@@ -26,8 +26,8 @@ constexpr int CNT = 256;
 __global__ void __launch_bounds__(CNT)
 cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, double thr0,
             const double* __restrict__ fnorm, double fcoef, const int* __restrict__ rlo, const int* __restrict__ rhi,
-            int cap, int* __restrict__ lo, int* __restrict__ cnt, float* __restrict__ dmin_out,
-            uint8_t* __restrict__ flags) {
+            const float* __restrict__ dref, int cap, int* __restrict__ lo, int* __restrict__ cnt,
+            float* __restrict__ dmin_out, uint8_t* __restrict__ flags) {
   __shared__ double scratch[CNT / 32];
   __shared__ int imin[CNT / 32], imax[CNT / 32];
   const int t = blockIdx.x;
@@ -38,6 +38,10 @@ cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, 
   double m = INFINITY;
   for (int i = i0 + threadIdx.x; i < i1; i += CNT) m = fmin(m, (double)row[i]);
   m = block_min<CNT>(m, scratch);
+  // landmark-sharded evaluation: the window is taken against the minimum over every
+  // shard's estimate (an all-reduce of the per-frame minima), so a shard that holds
+  // none of the frame's window returns an empty one
+  if (dref) m = fmin(m, (double)dref[t]);
   int a = L, b = -1;
   for (int i = i0 + threadIdx.x; i < i1; i += CNT) {
     if (lam * ((double)row[i] - m) <= thr) { a = min(a, i); b = max(b, i); }
@@ -54,6 +58,7 @@ cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, 
     a = min(imin[0], a);
     b = max(imax[0], b);
     int c = b - a + 1;
+    if (c <= 0) { a = 0; c = 0; }
     uint8_t f = 0;
     if (!isfinite(m)) f |= kFlagNonFinite;
     if (c > cap) { f |= kFlagSigOverflow; c = cap; }
@@ -65,10 +70,10 @@ cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, 
 }
 
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
-                              double fcoef, const int* rlo, const int* rhi, int cap, int* lo, int* cnt, float* dmin,
-                              uint8_t* flags, cudaStream_t stream) {
+                              double fcoef, const int* rlo, const int* rhi, const float* dref, int cap, int* lo,
+                              int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  cand_kernel<<<T, CNT, 0, stream>>>(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, cap, lo, cnt, dmin, flags);
+  cand_kernel<<<T, CNT, 0, stream>>>(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, dref, cap, lo, cnt, dmin, flags);
   return cudaGetLastError();
 }
 

@@ -6,21 +6,31 @@ each rank takes a contiguous slice (``shard_range``) and needs no data-path
 collective; results stay on their rank (``gather_frames`` is only for callers
 that want them on rank 0).
 
-Landmark sharding (the north_star's variant, ``--shard landmarks``): rank g
-owns landmarks [gL/G, (g+1)L/G) and computes, for every frame, the path-CV of
-its own shard: s_g, z_g and their gradients.  Because
-  Z_g = sum_{i in g} e^{-lam D_i} = e^{-lam z_g}  and  s_g = sum q_i e^{..} / Z_g,
-the global values follow from the per-frame pairs (s_g, z_g) alone:
-  w_g = Z_g / Z,   s = sum_g w_g s_g,   z = -(1/lam) ln sum_g e^{-lam z_g},
-  dz = sum_g w_g dz_g,   ds = sum_g w_g [ds_g - lam (s_g - s) dz_g].
-``merge_landmark_shards`` all-gathers the [T, 2] partials (16 B per frame per
-rank) and merges them in fixed rank order (bitwise independent of timing);
-the gradient combination is an all-reduce of the weighted per-rank
-gradients (the one large exchange of this variant).
+Landmark sharding (the north_star's variant, ``bench.py --shard landmarks``,
+``PathCVTC(..., shard=(rank, world))``): rank g owns landmarks
+[gL/G, (g+1)L/G) and every frame.  Per-frame exchanges, all O(T):
+  1. all-reduce MIN of the coarse screen's D_min upper bound (pruning) and of the
+     screen estimate's minimum -- every shard takes its windows against the global
+     minimum, so a shard far from a frame computes nothing for it;
+  2. all-gather of the per-frame partials (s_g, z_g) of each shard's exact window
+     (16 B per frame per rank).  Because
+       Z_g = sum_{i in g} e^{-lam D_i} = e^{-lam z_g}  and  s_g = sum q_i e^{..} / Z_g,
+     the global values follow from them alone (``merge_partials``, fixed rank order,
+     bitwise independent of timing):
+       w_g = Z_g / Z,   s = sum_g w_g s_g,   z = -(1/lam) ln sum_g e^{-lam z_g},
+       dz = sum_g w_g dz_g,   ds = sum_g w_g [ds_g - lam (s_g - s) dz_g];
+     each shard rescales its coefficients by (alpha, beta) = (w_g, -lam (s_g - s))
+     on the device (mc_shard_rescale) before its gradient pass;
+  3. the gradient rows: frame t is owned by the shard with the largest Z_g (its
+     nearest landmark); shards whose window of t is non-empty but that do not own
+     it send their rows to the owner (one all-to-all of the straddling rows only,
+     ``exchange_owned_rows``).  The dense alternative, an all-reduce of T x n x 3
+     per CV (``merge_landmark_shards``), moves 31 GB per step at config 4.
 """
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -34,9 +44,11 @@ def shard_range(total, rank, world):
 
 
 def merge_partials(s_parts, z_parts, lam):
-    """Merge per-shard (s_g, z_g) [G, T] into global (s, z, w [G, T]); fixed order."""
+    """Merge per-shard (s_g, z_g) [G, T] into global (s, z, w [G, T]); fixed order.
+    A shard with an empty window for frame t reports z_g = +inf (w_g = 0)."""
     zmin = torch.min(z_parts, dim=0).values
     e = torch.exp(-lam * (z_parts - zmin[None, :]))
+    e = torch.where(torch.isinf(z_parts), torch.zeros_like(e), e)
     tot = e.sum(dim=0)
     w = e / tot[None, :]
     s = (w * s_parts).sum(dim=0)
@@ -74,3 +86,152 @@ def gather_frames(x, total, group=None):
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
     return torch.cat([p[:c] for p, c in zip(parts, sizes)])
+
+
+# ---------------------------------------------------------------- landmark-sharded exchanges
+
+def shard_coefficients(s_parts, z_parts, lam, rank):
+    """Global (s, z) and this shard's coefficient rescaling (alpha, beta) [T]:
+    cs' = alpha (cs + beta cz), cz' = alpha cz."""
+    s, z, w = merge_partials(s_parts, z_parts, lam)
+    alpha = w[rank].contiguous()
+    beta = (-lam * (s_parts[rank] - s)).contiguous()
+    return s, z, alpha, beta
+
+
+def gradient_owners(z_parts):
+    """Owner shard of every frame: the largest Z_g (smallest z_g; ties to the lower rank)."""
+    return torch.argmin(z_parts, dim=0)
+
+
+def exchange_plan(z_parts, rank):
+    """Rows this rank sends to / receives from every other rank: frame t goes from every
+    shard with a non-empty window (finite z_g) to its owner."""
+    world = z_parts.shape[0]
+    owner = gradient_owners(z_parts)
+    active = torch.isfinite(z_parts)
+    send = [torch.nonzero(active[rank] & (owner == h)).flatten() if h != rank else None for h in range(world)]
+    recv = [torch.nonzero(active[g] & (owner == rank)).flatten() if g != rank else None for g in range(world)]
+    return owner, send, recv
+
+
+def _alltoall_rows(bufs_send, recv_counts, row_shape, dtype, device, group=None):
+    """Variable-size all-to-all of row blocks (one all_to_all_single on packed buffers)."""
+    world = len(bufs_send)
+    rowlen = int(np.prod(row_shape)) if row_shape else 1
+    send_counts = [0 if b is None else int(b.shape[0]) for b in bufs_send]
+    flat = [b.reshape(-1) for b in bufs_send if b is not None and b.shape[0]]
+    sendbuf = torch.cat(flat) if flat else torch.empty((0,), dtype=dtype, device=device)
+    recvbuf = torch.empty((sum(recv_counts) * rowlen,), dtype=dtype, device=device)
+    dist.all_to_all_single(recvbuf, sendbuf, [c * rowlen for c in recv_counts], [c * rowlen for c in send_counts],
+                           group=group)
+    out, off = [], 0
+    for g in range(world):
+        c = recv_counts[g]
+        out.append(recvbuf[off * rowlen:(off + c) * rowlen].view((c,) + tuple(row_shape)))
+        off += c
+    return out
+
+
+def exchange_owned_rows(ds, dz, z_parts, group=None):
+    """Complete the gradient rows this rank owns: add the straddling rows of the other
+    shards (in fixed rank order).  ds, dz: [T, n, 3] partial sums of this shard.
+    Returns owner [T]; rows with owner != rank stay partial and must be ignored."""
+    rank = dist.get_rank(group)
+    owner, send, recv = exchange_plan(z_parts, rank)
+    if len(send) == 1:
+        return owner
+    row_shape = (2,) + tuple(ds.shape[1:])
+    bufs = [None if idx is None else torch.stack([ds[idx], dz[idx]], dim=1) for idx in send]
+    counts = [0 if idx is None else int(idx.numel()) for idx in recv]
+    got = _alltoall_rows(bufs, counts, row_shape, ds.dtype, ds.device, group)
+    for g, idx in enumerate(recv):
+        if idx is None or idx.numel() == 0:
+            continue
+        ds.index_add_(0, idx.to(ds.device), got[g][:, 0])
+        dz.index_add_(0, idx.to(dz.device), got[g][:, 1])
+    return owner
+
+
+class DistComm:
+    """Collectives of the landmark-sharded evaluation over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def min(self, t):
+        t = t.clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return t
+
+    def gather(self, t):
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t.contiguous(), group=self.group)
+        return torch.stack(parts)
+
+    def exchange(self, ds, dz, z_parts):
+        return exchange_owned_rows(ds, dz, z_parts, self.group)
+
+
+def drive(steps, comm):
+    """Run a landmark-sharded evaluation generator (PathCVTC.sharded_steps) against
+    ``comm``: every yielded (op, *args) is one collective; returns its final value."""
+    try:
+        req = next(steps)
+        while True:
+            op, args = req[0], req[1:]
+            req = steps.send(getattr(comm, op)(*args))
+    except StopIteration as e:
+        return e.value
+
+
+def drive_lockstep(steps_list, lam=None):
+    """Run G shard generators in one process, in lock step, with the collectives
+    computed locally (the same merge arithmetic as DistComm; one device, no
+    inter-rank waits).  Used by the single-GPU tests of the sharded path."""
+    G = len(steps_list)
+    reqs = [next(g) for g in steps_list]
+    results = [None] * G
+    while True:
+        ops = {r[0] for r in reqs}
+        if len(ops) != 1:
+            raise RuntimeError(f"shards out of step: {ops}")
+        op = ops.pop()
+        if op == "min":
+            v = torch.stack([r[1] for r in reqs]).amin(0)
+            outs = [v.clone() for _ in range(G)]
+        elif op == "gather":
+            v = torch.stack([r[1] for r in reqs])
+            outs = [v for _ in range(G)]
+        elif op == "exchange":
+            # every shard's rows, owner-summed in rank order
+            z_parts = reqs[0][3]
+            owner, _, _ = exchange_plan(z_parts, 0)
+            active = torch.isfinite(z_parts)
+            for h in range(G):
+                ds_h, dz_h = reqs[h][1], reqs[h][2]
+                for g in range(G):
+                    if g == h:
+                        continue
+                    idx = torch.nonzero(active[g] & (owner == h)).flatten()
+                    if idx.numel():
+                        ds_h.index_add_(0, idx, reqs[g][1][idx])
+                        dz_h.index_add_(0, idx, reqs[g][2][idx])
+            outs = [owner for _ in range(G)]
+        else:
+            raise RuntimeError(f"unknown collective {op!r}")
+        done = 0
+        for i, g in enumerate(steps_list):
+            if results[i] is not None:
+                continue
+            try:
+                reqs[i] = g.send(outs[i])
+            except StopIteration as e:
+                results[i] = e.value
+                done += 1
+        if all(r is not None for r in results):
+            return results
+        if done:
+            raise RuntimeError("shards finished out of step")

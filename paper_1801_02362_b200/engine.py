@@ -315,7 +315,12 @@ class PathCVTC:
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4):
+                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None):
+        """shard = (rank, world): landmark-sharded evaluation.
+        ``landmarks`` (and q) are the FULL set; this engine keeps landmarks
+        shard_range(L, rank, world) with their global q, and the landmark-norm maxima of
+        the one-term error bound over the full set (identical windows on every shard
+        count).  Evaluate with ``evaluate_sharded`` / ``sharded_steps``."""
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
         self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
@@ -340,6 +345,26 @@ class PathCVTC:
             q.detach().cpu().numpy() if torch.is_tensor(q) else q, dtype=float)
         if qq.shape != (self.L,):
             raise ConfigError("q must have one value per landmark")
+        self.shard = None
+        if shard is not None:
+            from .dist import shard_range
+            rank, world = int(shard[0]), int(shard[1])
+            if not (0 <= rank < world):
+                raise ConfigError(f"shard {shard!r}")
+            off, cnt = shard_range(self.L, rank, world)
+            if cnt < 1:
+                raise EmptyActiveSetError(f"landmark shard {rank} of {world} is empty (L = {self.L})")
+            if self.screen == "f16x1":
+                full = K.center_split(lm, self.wa, self.w, weighted=True, moments=False, fmt=self.fmt, terms=1)
+                self._na_max_full = float(full.opnorm.max().item())
+                self._nr_max_full = float(full.rnorm.max().item())
+                del full
+            lm = lm[off:off + cnt].contiguous()
+            qq = qq[off:off + cnt]
+            self.shard = (rank, world, off, cnt)
+            self.L_total = self.L
+            self.L = cnt
+            self.window_cap = int(min(window_cap, self.L))
         self.q = torch.from_numpy(qq).to(self.device)
         self.lraw = lm
         # uniform displacement weights (the configs' default): the exact refits run on raw,
@@ -371,6 +396,8 @@ class PathCVTC:
             c_unit = 4.0 * (2 * u + u * u + self.n * 2.0 ** -27) * 1.25 + 1e-6
             self.na_max = float(self.ls.opnorm.max().item())
             self.nr_max = float(self.ls.rnorm.max().item())
+            if self.shard is not None:  # the D_min error term ranges over every shard's landmarks
+                self.na_max, self.nr_max = self._na_max_full, self._nr_max_full
             self.kacc = 5.0 * self.n * 2.0 ** -27
             self.c_unit = c_unit  # the u-based bound (reported by the tests beside e_tl)
             self.margin = 2.0
@@ -528,6 +555,109 @@ class PathCVTC:
                 Dest = back
         if return_estimate:
             out["D_est"] = Dest  # pruned: entries outside each band are not computed
+        return out
+
+
+    # ------------------------------------------------------------ landmark sharding
+
+    def evaluate_sharded(self, frames, grad=True, out_dtype=torch.float32, comm=None):
+        """Landmark-sharded evaluate over a torch.distributed group (comm: dist.DistComm,
+        default the world group).  Returns s, z [T] (global, every rank) and, with grad,
+        ds, dz [T, n, 3] whose rows with owner == rank are complete (the others hold
+        this shard's partial sums), plus owner [T]."""
+        from . import dist as Dd
+        return Dd.drive(self.sharded_steps(frames, grad, out_dtype), comm or Dd.DistComm())
+
+    def sharded_steps(self, frames, grad=True, out_dtype=torch.float32):
+        """Generator of the landmark-sharded evaluation: yields ("min", t), ("gather", t)
+        and ("exchange", ds, dz, z_parts) collectives (dist.drive / drive_lockstep run
+        them) and returns the result dict.  Same windows, refits and truncation as
+        evaluate() on the full landmark set."""
+        from . import dist as Dd
+        if self.shard is None:
+            raise ConfigError("sharded_steps needs PathCVTC(..., shard=(rank, world))")
+        rank, world = self.shard[0], self.shard[1]
+        one = self.screen == "f16x1"
+        rlo = rhi = perm0 = None
+        if self.prune:
+            fr, fs0 = self._frames(frames, 1, check=False)
+            Dc = K.msd_estimate(fs0, self.ls_coarse, grid=K2_GRID)
+            dub = K.screen_bound(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.kacc, fs0.rnorm, self.ls_coarse.rnorm)
+            dub = yield ("min", dub)
+            hlo, hhi, key = K.prune_plan(Dc, fs0.opnorm, self.ls_coarse.opnorm, self.kacc, self.mind,
+                                         (self.cutoff + 2.0) / self.lam, self.knear, maxd=self.maxd,
+                                         cstride=self.cstride, frnorm=fs0.rnorm, crnorm=self.ls_coarse.rnorm,
+                                         dub_in=dub)
+            ntl = self.mind.shape[1]
+            perm0 = K.sort_by_key(key, ntl + 1)
+            fs = K.gather_split(fs0, perm0)
+            tlist, nlist, rlo, rhi = K.band_tiles(perm0, hlo, hhi, 128, 48, self.L, ntl)
+            Dest = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
+            K.msd_estimate(fs, self.ls, Dest, grid=K2_GRID, tlist=tlist, nlist=nlist)
+        else:
+            fs0 = None
+            Dest, fr, fs = self.estimate(frames, self.screen_terms, check=False)
+        T = fr.shape[0]
+        p = perm0.long() if perm0 is not None else None
+        fnorm = self.frame_bound(fs) if one else None
+        fcoef = 2.0 * self.lam if one else 0.0
+        # the estimate minimum over every shard (in the caller's frame order)
+        _, _, dmin, _ = K.candidates(Dest, self.lam, self.cutoff + self.margin, 1, fnorm=fnorm, fcoef=fcoef,
+                                     rlo=rlo, rhi=rhi)
+        if p is not None:
+            dm = torch.empty_like(dmin)
+            dm[p] = dmin
+            dmin = dm
+        dref = yield ("min", dmin)
+        if p is not None:
+            dref = dref[p].contiguous()
+        cap = self.window_cap
+        while True:
+            lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap, fnorm=fnorm,
+                                              fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
+            perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
+            Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
+                                        fmap=perm0, wuni=self.wuni)
+            wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
+                                    rowcnt=cnt)
+            sl, zl = wres["s"], wres["z"]
+            if p is not None:
+                sl, zl = torch.empty_like(sl), torch.empty_like(zl)
+                sl[p], zl[p] = wres["s"], wres["z"]
+            fflags = fs.flags if fs0 is None else torch.cat([fs.flags, fs0.flags])
+            status = torch.stack([_flag_bits_dev(fflags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
+                                  _flag_bits_dev(wres["flags"])]).to(torch.float64).flatten()
+            # one gather: the partials and every shard's status bits (so all shards take
+            # the same retry / error decision)
+            parts = yield ("gather", torch.cat([sl, zl, status]))
+            bits = parts[:, 2 * T:].reshape(world, 4, -1) > 0
+            ff, cf, rf, wf = (_bits_value(b.tolist()) for b in bits.any(0).cpu())
+            if ff & FLAG_NON_FINITE:
+                raise InvalidStructureError("frame coordinates contain non-finite values")
+            if (cf & FLAG_SIG_OVERFLOW) and cap < self.L:
+                cap = min(self.L, 4 * cap)
+                continue
+            break
+        if rf & FLAG_NON_FINITE:
+            raise InvalidStructureError("path_cv refine: non-finite coordinates or distances")
+        if rf & FLAG_NO_CONVERGE:
+            raise MetadynError("path_cv refine: Jacobi diagonalisation did not converge")
+        if wf & FLAG_NON_FINITE:
+            raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        s_parts, z_parts = parts[:, :T], parts[:, T:2 * T]
+        s, z, alpha, beta = Dd.shard_coefficients(s_parts, z_parts, self.lam, rank)
+        out = {"s": s, "z": z, "z_parts": z_parts, "window_cnt": cnt if p is None else cnt[torch.argsort(p)],
+               "nsig": wres["nsig"]}
+        if grad:
+            if p is not None:
+                alpha, beta = alpha[p].contiguous(), beta[p].contiguous()
+            K.shard_rescale(wres, alpha, beta, cap)
+            gperm = K.sig_span_key(wres, self.L)
+            gperm = K.sort_by_key(gperm, 2 * self.L + 1)
+            ds, dz = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, out_dtype,
+                                         out_map=perm0)
+            owner = yield ("exchange", ds, dz, z_parts)
+            out.update(ds=ds, dz=dz, owner=owner)
         return out
 
 

@@ -217,6 +217,14 @@ def pathcv_weights(D, q, lam, R, fr, lm, cap, cutoff=50.0, close=None, S=None, L
             "t0": t0, "count": T}
 
 
+def shard_rescale(wres, alpha, beta, cap):
+    """Rescale a landmark shard's K4 coefficients (wres, in place) to the merged softmax:
+    cs' = alpha (cs + beta cz), cz' = alpha cz (alpha, beta: fp64 [T] in wres' row order)."""
+    call("mc_shard_rescale", int(wres["count"]), int(cap), ptr(wres["nsig"]), ptr(alpha), ptr(beta),
+         ptr(wres["sig_coef"]), ptr(wres["fvec"]), stream_ptr())
+    return wres
+
+
 def _pathcv_weights_nl(D, q, lam, R, fr, lm, cap, cutoff, close, S, t0, count, s, z, nb, dmode):
     Ttot, L = D.shape
     T = Ttot - t0 if count is None else count
@@ -294,8 +302,9 @@ def sig_span_key(wres, L):
 
 
 def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None, maxd=None, cstride=0, frnorm=None,
-               crnorm=None):
-    """Per-frame admissible landmark-tile hulls of the metric-pruned screen (csrc/prune.cu)."""
+               crnorm=None, dub_in=None):
+    """Per-frame admissible landmark-tile hulls of the metric-pruned screen (csrc/prune.cu).
+    dub_in (fp64 [T], landmark-sharded): the D_min upper bound over every shard."""
     T, C = Dc.shape
     ntl = mind.shape[1]
     dev = Dc.device
@@ -304,9 +313,19 @@ def prune_plan(Dc, fnorm, cnorm, c_unit, mind, thr, knear=4, wide=None, maxd=Non
     key = torch.empty((T,), dtype=I32, device=dev)
     wide = max(1, (3 * ntl) // 4) if wide is None else int(wide)
     call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), ptr(frnorm), ptr(crnorm),
-         float(c_unit), ptr(mind), ptr(maxd), int(cstride), ntl, float(thr), int(knear), wide, ptr(hlo), ptr(hhi),
-         ptr(key), stream_ptr())
+         float(c_unit), ptr(mind), ptr(maxd), int(cstride), ntl, float(thr), int(knear), wide, ptr(dub_in), None,
+         ptr(hlo), ptr(hhi), ptr(key), stream_ptr())
     return hlo, hhi, key
+
+
+def screen_bound(Dc, fnorm, cnorm, c_unit, frnorm=None, crnorm=None):
+    """Per-frame D_min upper bound min_c (Dc + e_tc) of a coarse one-term screen
+    (mc_prune_plan's bound-only pass; landmark-sharded evaluation all-reduces it)."""
+    T, C = Dc.shape
+    dub = torch.empty((T,), dtype=F64, device=Dc.device)
+    call("mc_prune_plan", ptr(Dc), T, C, Dc.stride(0), ptr(fnorm), ptr(cnorm), ptr(frnorm), ptr(crnorm),
+         float(c_unit), None, None, 0, 1, 0.0, 1, 1, None, ptr(dub), None, None, None, stream_ptr())
+    return dub
 
 
 def band_tiles(perm, hull_lo, hull_hi, BM, BL, L, ntl):
@@ -351,9 +370,10 @@ def gather_rows(src, idx):
     return dst
 
 
-def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0, rlo=None, rhi=None):
+def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0, rlo=None, rhi=None, dref=None):
     """Per-frame D_min and the window of landmarks with lam (D - D_min) <= thr_t,
-    thr_t = thr + fcoef * fnorm[t] (fnorm: optional per-frame fp64 tensor)."""
+    thr_t = thr + fcoef * fnorm[t] (fnorm: optional per-frame fp64 tensor).
+    dref (fp32 [T], landmark-sharded): the estimate minimum over every shard."""
     T = D.shape[0]
     L = D.shape[1] if L is None else L
     dev = D.device
@@ -362,7 +382,7 @@ def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0, rlo=None, rhi=No
     dmin = torch.empty((T,), dtype=torch.float32, device=dev)
     flags = torch.empty((T,), dtype=U8, device=dev)
     call("mc_candidates", ptr(D), T, L, D.stride(0), float(lam), float(thr), ptr(fnorm), float(fcoef), ptr(rlo),
-         ptr(rhi), cap, ptr(lo), ptr(cnt), ptr(dmin), ptr(flags), stream_ptr())
+         ptr(rhi), ptr(dref), cap, ptr(lo), ptr(cnt), ptr(dmin), ptr(flags), stream_ptr())
     return lo, cnt, dmin, flags
 
 

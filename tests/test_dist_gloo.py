@@ -107,3 +107,108 @@ def test_merge_partials_single_shard_identity():
     z = torch.tensor([[0.3, 0.1]], dtype=torch.float64)
     ms, mz, w = D.merge_partials(s, z, 7.0)
     assert torch.equal(ms, s[0]) and torch.allclose(mz, z[0]) and torch.all(w == 1)
+
+
+# ---------------------------------------------------------------- landmark-sharded exchanges
+#
+# The same collective sequence as PathCVTC.sharded_steps (min -> gather -> exchange),
+# with the oracle's exact distances and gradients standing in for the device
+# kernels: per-shard windows against the global minimum, local (s_g, z_g), the
+# (alpha, beta) coefficient rescaling and the owner all-to-all of the gradient rows.
+
+_CUT = 6.0  # small, so that the toy path's windows split between the shards
+
+
+def _toy_problem():
+    wl = synth.config0(seed=5, T=40, L=16, N=7)  # frames near landmarks 7..14: both shards
+    n = wl.frames.shape[1]
+    w = O.normalise_weights(None, n)
+    lc = np.stack([O.center(a, w) for a in wl.landmarks])
+    D_ = np.zeros((wl.frames.shape[0], wl.landmarks.shape[0]))
+    G_ = np.zeros(D_.shape + (n, 3))
+    for t, x in enumerate(wl.frames):
+        xc = O.center(x, w)
+        for i in range(lc.shape[0]):
+            D_[t, i], G_[t, i], _ = O.exact_distance(xc, lc[i], w, w, with_rot_term=False)
+    return wl, D_, G_
+
+
+def _toy_steps(rank, world, wl, D_, G_, cut=_CUT):
+    """Generator mirroring PathCVTC.sharded_steps on precomputed D / dD."""
+    T, L = D_.shape
+    off, cnt = D.shard_range(L, rank, world)
+    Dl = torch.from_numpy(D_[:, off:off + cnt].copy())
+    Gl = torch.from_numpy(G_[:, off:off + cnt].copy())
+    q = torch.arange(off, off + cnt, dtype=torch.float64)
+    lam = wl.lam
+    dref = yield ("min", Dl.min(1).values)
+    win = lam * (Dl - dref[:, None]) <= cut
+    sl = torch.zeros(T, dtype=torch.float64)
+    zl = torch.full((T,), float("inf"), dtype=torch.float64)
+    cs = torch.zeros((T, cnt), dtype=torch.float64)
+    cz = torch.zeros((T, cnt), dtype=torch.float64)
+    for t in range(T):
+        if not win[t].any():
+            continue
+        d = Dl[t][win[t]]
+        e = torch.exp(-lam * (d - d.min()))
+        p = e / e.sum()
+        sl[t] = (p * q[win[t]]).sum()
+        zl[t] = d.min() - torch.log(e.sum()) / lam
+        cs[t, win[t]] = -lam * p * (q[win[t]] - sl[t])
+        cz[t, win[t]] = p
+    parts = yield ("gather", torch.cat([sl, zl]))
+    s_parts, z_parts = parts[:, :T], parts[:, T:]
+    s, z, alpha, beta = D.shard_coefficients(s_parts, z_parts, lam, rank)
+    cs2 = alpha[:, None] * (cs + beta[:, None] * cz)
+    cz2 = alpha[:, None] * cz
+    ds = torch.einsum("ti,tika->tka", cs2, Gl)
+    dz = torch.einsum("ti,tika->tka", cz2, Gl)
+    owner = yield ("exchange", ds, dz, z_parts)
+    return {"s": s, "z": z, "ds": ds, "dz": dz, "owner": owner, "z_parts": z_parts}
+
+
+def _sharded_exchange(rank, world):
+    wl, D_, G_ = _toy_problem()
+    out = D.drive(_toy_steps(rank, world, wl, D_, G_), D.DistComm())
+    return {k: v.numpy() for k, v in out.items()}
+
+
+def test_landmark_sharded_exchange_matches_full():
+    out = _spawn(_sharded_exchange)
+    wl, D_, G_ = _toy_problem()
+    # one shard with the same truncation is the reference; untruncated it is the oracle
+    ref = {k: v.numpy() for k, v in D.drive_lockstep([_toy_steps(0, 1, wl, D_, G_)])[0].items()}
+    full = D.drive_lockstep([_toy_steps(0, 1, wl, D_, G_, cut=1e9)])[0]
+    orc = O.batch_path_cv_exact(wl.frames, wl.landmarks, wl.lam)
+    np.testing.assert_allclose(full["s"].numpy(), orc["s"], rtol=1e-12)
+    np.testing.assert_allclose(full["ds"].numpy(), orc["ds"], atol=1e-10 * np.abs(orc["ds"]).max())
+    owner = out[0]["owner"]
+    assert np.array_equal(owner, out[1]["owner"])
+    zp = out[0]["z_parts"]
+    # the windows really are split: some frames are empty on one shard, some straddle
+    assert (~np.isfinite(zp)).any() and np.isfinite(zp).all(0).any()
+    for rank in (0, 1):
+        o = out[rank]
+        np.testing.assert_allclose(o["s"], ref["s"], rtol=1e-12)
+        np.testing.assert_allclose(o["z"], ref["z"], rtol=1e-12, atol=1e-15)
+        mine = owner == rank
+        for key in ("ds", "dz"):
+            np.testing.assert_allclose(o[key][mine], ref[key][mine], atol=1e-10 * np.abs(ref[key]).max())
+    # the lock-step single-process driver (used by the one-GPU tests) gives the same bits
+    loc = D.drive_lockstep([_toy_steps(r, 2, wl, D_, G_) for r in range(2)])
+    for rank in (0, 1):
+        for key in ("s", "z", "owner"):
+            assert np.array_equal(loc[rank][key].numpy(), out[rank][key])
+        mine = owner == rank
+        for key in ("ds", "dz"):
+            assert np.array_equal(loc[rank][key].numpy()[mine], out[rank][key][mine])
+
+
+def test_merge_partials_empty_shard():
+    s = torch.tensor([[1.5, 0.0], [2.5, 3.0]], dtype=torch.float64)
+    z = torch.tensor([[0.3, float("inf")], [0.3, 0.1]], dtype=torch.float64)
+    ms, mz, w = D.merge_partials(s, z, 7.0)
+    assert w[0, 1] == 0 and w[1, 1] == 1 and ms[1] == 3.0 and mz[1] == 0.1
+    np.testing.assert_allclose(w[:, 0].numpy(), [0.5, 0.5])
+    assert D.gradient_owners(z).tolist() == [0, 1]

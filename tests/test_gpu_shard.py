@@ -1,0 +1,122 @@
+"""GPU tests of the landmark-sharded evaluation.
+
+G shard engines run in one process on one GPU, driven in lock step by
+``dist.drive_lockstep`` (the collectives computed locally with the same merge
+arithmetic as ``dist.DistComm``; no rank waits on another's kernels).  The
+merged s, z and the owner rows of ds, dz must equal the unsharded evaluate() on
+the full landmark set, and that one the oracle.  A real one-rank NCCL group runs
+the same generator through ``evaluate_sharded``.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+from oracle import oracle as O
+from paper_1801_02362_b200 import dist as D
+from paper_1801_02362_b200 import engine, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _rows_close(x, y, rel):
+    """Per-frame max-norm comparison (the gradient tolerance of the north_star)."""
+    x = x.reshape(x.shape[0], -1)
+    y = y.reshape(y.shape[0], -1)
+    scale = np.abs(y).max(axis=1)
+    err = np.abs(x - y).max(axis=1)
+    assert np.all(err <= rel * scale + 1e-300), float((err / scale).max())
+
+
+def _sharded(wl, G, **kw):
+    engs = [engine.PathCVTC(wl.landmarks, wl.lam, shard=(g, G), **kw) for g in range(G)]
+    outs = D.drive_lockstep([e.sharded_steps(wl.frames, out_dtype=torch.float64) for e in engs])
+    return engs, outs
+
+
+@pytest.mark.parametrize("G,L", [(1, 1536), (2, 1536), (3, 1536), (4, 384)])
+def test_landmark_sharded_matches_unsharded(G, L, cuda_device):
+    wl = synth.config4(T=260, L=L, N=240)
+    full = engine.PathCVTC(wl.landmarks, wl.lam)
+    ref = full.evaluate(wl.frames, out_dtype=torch.float64)
+    engs, outs = _sharded(wl, G)
+    # pruning is on whenever a shard has >= 16 landmark tiles
+    assert [e.prune for e in engs] == [(e.L + 47) // 48 >= 16 for e in engs]
+    s_ref, z_ref = ref["s"].cpu().numpy(), ref["z"].cpu().numpy()
+    owner = outs[0]["owner"].cpu().numpy()
+    for g, o in enumerate(outs):
+        # every shard holds the merged s, z (bitwise the same on all shards)
+        np.testing.assert_array_equal(o["s"].cpu().numpy(), outs[0]["s"].cpu().numpy())
+        np.testing.assert_allclose(o["s"].cpu().numpy(), s_ref, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(o["z"].cpu().numpy(), z_ref, rtol=1e-9, atol=1e-12)
+        mine = owner == g
+        if mine.any():
+            # a shard's significant set is taken against its own window minimum (>= the
+            # global one): a superset of the unsharded set, the extra landmarks below
+            # e^-cutoff weight (amplified ~1e3 by the cancellation in ds)
+            for key in ("ds", "dz"):
+                _rows_close(o[key].cpu().numpy()[mine], ref[key].cpu().numpy()[mine], 1e-7)
+    # every frame has exactly one owner, and with G > 1 the windows are split: most
+    # frames have an empty window on some shard (the global-minimum exchange)
+    assert set(np.unique(owner)) <= set(range(G))
+    if G > 1:
+        active = torch.isfinite(outs[0]["z_parts"]).sum(0).cpu().numpy()
+        assert active.min() >= 1 and (active < G).mean() > 0.5
+        # the same windows split over the shards (up to the hull gaps at shard boundaries
+        # and the unscanned margins of the banded screen)
+        tot = sum(int(o["window_cnt"].sum().item()) for o in outs)
+        rtot = int(ref["window_cnt"].sum().item())
+        assert abs(tot - rtot) <= 0.05 * rtot, (tot, rtot)
+
+
+def test_landmark_sharded_vs_oracle(cuda_device):
+    wl = synth.config4(T=40, L=1536, N=240)
+    _, outs = _sharded(wl, 2)
+    ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    owner = outs[0]["owner"].cpu().numpy()
+    for g, o in enumerate(outs):
+        np.testing.assert_allclose(o["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+        np.testing.assert_allclose(o["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+        mine = owner == g
+        for key in ("ds", "dz"):
+            _rows_close(o[key].cpu().numpy()[mine], ref[key][mine], 1e-5)
+
+
+def test_landmark_shard_window_overflow_retry(cuda_device):
+    """A window wider than the capacity on any shard makes every shard retry."""
+    wl = synth.config4(T=24, L=256, N=200)
+    ref = engine.PathCVTC(wl.landmarks, wl.lam).evaluate(wl.frames, out_dtype=torch.float64)
+    _, outs = _sharded(wl, 2, window_cap=4)
+    np.testing.assert_allclose(outs[1]["s"].cpu().numpy(), ref["s"].cpu().numpy(), rtol=1e-9)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_landmark_sharded_through_nccl_one_rank(cuda_device):
+    """evaluate_sharded over a real NCCL process group (world size 1 on one GPU)."""
+    wl = synth.config4(T=64, L=1536, N=240)
+    init = not dist.is_initialized()
+    if init:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=cuda_device)
+    try:
+        eng = engine.PathCVTC(wl.landmarks, wl.lam, shard=(0, 1))
+        out = eng.evaluate_sharded(wl.frames, out_dtype=torch.float64)
+        torch.cuda.synchronize()
+    finally:
+        if init:
+            dist.destroy_process_group()
+    ref = engine.PathCVTC(wl.landmarks, wl.lam).evaluate(wl.frames, out_dtype=torch.float64)
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"].cpu().numpy(), rtol=1e-12)
+    assert bool((out["owner"] == 0).all())
+    _rows_close(out["ds"].cpu().numpy(), ref["ds"].cpu().numpy(), 1e-12)
