@@ -25,6 +25,8 @@
 // the landmark operand stays L2-resident while a frame tile is in use):
 //   warp 0: TMA producer   warp 1: MMA issuer (one elected lane)
 //   warp 2: TMEM allocator warps 4-7: epilogue (TMEM lane quarter = warp%4)
+#include <algorithm>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -177,8 +179,9 @@ center_split_kernel(const T* __restrict__ coords, int64_t B, int n, int kpad, co
 // N % 4 == 0): 4-atom groups move as float4 triples (the second pass re-reads the
 // structure from L2), the scaled halves go out as 8-byte rows of 4 atoms per
 // axis, and the sums of each pass are reduced in one shared-memory round.  Same
-// values as center_split_kernel<float, OpF16> (fp64 centring and scaling, rn halves).
-constexpr int CSF_NT = 512;
+// centroid / G / wbar / opnorm as center_split_kernel<float, OpF16> (fp64 centring);
+// the halves are rn16(fl32(v) 2^e) and rnorm a rigorous upper bound of the exact
+// residual norm (see below).
 
 template <int NT, int K>
 __device__ __forceinline__ void block_sum_n(double (&v)[K], double* scratch) {
@@ -201,7 +204,8 @@ __device__ __forceinline__ void block_sum_n(double (&v)[K], double* scratch) {
   }
 }
 
-__global__ void __launch_bounds__(CSF_NT, 2)
+template <int CSF_NT>
+__global__ void __launch_bounds__(CSF_NT, 1024 / CSF_NT)
 center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, int kpad,
                           const double* __restrict__ w_align, const double* __restrict__ w_disp,
                           __half* __restrict__ hi, double* __restrict__ scale_inv, double* __restrict__ centroid,
@@ -212,7 +216,7 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
   const float4* x4 = reinterpret_cast<const float4*>(coords + b * (int64_t)n * 3);
   const int G = n / 4;
   double c[3] = {0.0, 0.0, 0.0};
-  double xmax = 0.0;
+  float xmax = 0.0f;
   bool finite = true;
 #pragma unroll 2
   for (int gi = threadIdx.x; gi < G; gi += CSF_NT) {
@@ -221,22 +225,32 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const double wa = w_align[4 * gi + a];
-      const double x0 = f[3 * a], x1 = f[3 * a + 1], x2 = f[3 * a + 2];
-      finite = finite && isfinite(x0) && isfinite(x1) && isfinite(x2);
-      c[0] += wa * x0; c[1] += wa * x1; c[2] += wa * x2;
-      xmax = fmax(xmax, fmax(fabs(x0), fmax(fabs(x1), fabs(x2))));
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const float x = f[3 * a + p];
+        finite = finite && isfinite(x);
+        xmax = fmaxf(xmax, fabsf(x));
+        c[p] = fma(wa, (double)x, c[p]);
+      }
     }
   }
-  xmax = -block_min<CSF_NT>(-xmax, scratch);
+  const double xm = -block_min<CSF_NT>(-(double)xmax, scratch);
   block_sum_n<CSF_NT, 3>(c, scratch);
   const int nonfinite = __syncthreads_or(!finite);
-  const double bound = 2.0 * xmax;  // |x_j - c| <= 2 max|x|
+  const double bound = 2.0 * xm;  // |x_j - c| <= 2 max|x|
   int e = 0;
   if (bound > 0.0 && isfinite(bound)) {
     frexp(bound, &e);
     e = 14 - e;
   }
   e = max(-1000, min(1000, e));
+  // fp32 scaling and residuals (exact while 2^e and 2^-e are normal floats): the
+  // rounding residual of each half is measured against vf = fl32(v), exactly (Sterbenz:
+  // h 2^-e and vf are within a factor 2), and rnorm is returned as the rigorous upper
+  // bound ||h 2^-e - vf|| (1 + 1e-5) + 2^-24 ||v|| of ||h 2^-e - v|| -- half the fp64
+  // work per coordinate of the exact residual (the kernel is issue-bound, not HBM-bound)
+  const bool f32s = e >= -126 && e <= 126;
+  const float scf = f32s ? ldexpf(1.0f, e) : 0.0f, sif = f32s ? ldexpf(1.0f, -e) : 0.0f;
   const double scale = ldexp(1.0, e);
   const int64_t plane = B * (int64_t)kpad;
   __half* h0 = hi + b * kpad;
@@ -249,20 +263,30 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
       const float4 q0 = x4[3 * gi], q1 = x4[3 * gi + 1], q2 = x4[3 * gi + 2];
       const float f[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
       __half h[3][4];
+      float r2 = 0.0f;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const double wd = w_disp[4 * gi + a];
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
           const double v = (double)f[3 * a + p] - c[p];
-          acc[0] += wd * v * v;
-          acc[1 + p] += wd * v;
-          acc[4] += v * v;
-          h[p][a] = __double2half(v * scale);
-          const double rd = (double)__half2float(h[p][a]) * sinv - v;
-          acc[5] += rd * rd;
+          const double tv = wd * v;
+          acc[0] = fma(tv, v, acc[0]);
+          acc[1 + p] += tv;
+          acc[4] = fma(v, v, acc[4]);
+          if (f32s) {
+            const float vf = (float)v;
+            h[p][a] = __float2half_rn(vf * scf);
+            const float r = fmaf(__half2float(h[p][a]), sif, -vf);
+            r2 = fmaf(r, r, r2);
+          } else {
+            h[p][a] = __double2half(v * scale);
+            const double rd = (double)__half2float(h[p][a]) * sinv - v;
+            acc[5] = fma(rd, rd, acc[5]);
+          }
         }
       }
+      acc[5] += (double)r2;
 #pragma unroll
       for (int p = 0; p < 3; ++p) o[p] = *reinterpret_cast<const uint2*>(h[p]);
     }
@@ -275,9 +299,12 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
     gnorm[b] = acc[0];
     if (wbar) { wbar[3 * b] = acc[1]; wbar[3 * b + 1] = acc[2]; wbar[3 * b + 2] = acc[3]; }
     if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
-    if (opnorm) opnorm[b] = sqrt(acc[4]);
-    if (rnorm) rnorm[b] = sqrt(acc[5]);
-    scale_inv[b] = ldexp(1.0, -e);
+    const double on = sqrt(acc[4]);
+    if (opnorm) opnorm[b] = on;
+    // ||h 2^-e - v|| <= ||h 2^-e - vf|| + ||vf - v||, |vf - v| <= 2^-24 |v|; 1e-5 covers the
+    // fp32 accumulation of the <= 12 (kpad / 4 / CSF_NT + 1) squares per thread
+    if (rnorm) rnorm[b] = f32s ? sqrt(acc[5]) * (1.0 + 1e-5) + ldexp(on, -24) : sqrt(acc[5]);
+    scale_inv[b] = sinv;
   }
 }
 
@@ -302,9 +329,13 @@ cudaError_t launch_center_split16(const void* coords, int dtype, int64_t B, int 
   const int one = terms == 1 ? 1 : 0;
   if (dtype == 0 && one && !weighted && !mom && n % 4 == 0 && kpad % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(coords) & 15) == 0 && B <= 0x7fffffffLL) {
-    center_split_f16x1_kernel<<<(unsigned)B, CSF_NT, 0, stream>>>((const float*)coords, B, n, kpad, w_align, w_disp,
-                                                                  (__half*)hl, scale_inv, centroid, gnorm, wbar,
-                                                                  flags, opnorm, rnorm);
+    // 256 threads x 4 CTAs per SM: 1.25x the 512 x 2 rate (tools/_diag/k1_sweep.sh)
+    static const int nt = getenv("MC_K1_NT") ? atoi(getenv("MC_K1_NT")) : 256;
+    auto k = nt == 256 ? center_split_f16x1_kernel<256>
+                       : (nt == 128 ? center_split_f16x1_kernel<128> : center_split_f16x1_kernel<512>);
+    k<<<(unsigned)B, nt == 256 ? 256 : (nt == 128 ? 128 : 512), 0, stream>>>(
+        (const float*)coords, B, n, kpad, w_align, w_disp, (__half*)hl, scale_inv, centroid, gnorm, wbar, flags,
+        opnorm, rnorm);
     return cudaGetLastError();
   }
   if (dtype == 0)

@@ -212,3 +212,34 @@ def test_pathcv_tc_ragged_atoms_and_weights(n, weights, cuda_device):
         scale = np.abs(r).reshape(r.shape[0], -1).max(axis=1)
         err = np.abs(got - r).reshape(r.shape[0], -1).max(axis=1)
         assert np.all(err <= 1e-5 * scale), f"{key}: worst rel {np.max(err / scale):.3e}"
+
+
+@pytest.mark.parametrize("n,T", [(600, 700), (10000, 64), (1000, 1500)])
+def test_fast_one_term_split_vs_fp64(n, T, cuda_device):
+    """Fast K1s (one-term F16 frame operand, n % 4 == 0): centroid / G / wbar / operand
+    norm equal the fp64 values, every half is the scaled centred coordinate to half
+    precision, and rnorm bounds the true rounding residual tightly.  Same scalars as the
+    generic per-structure kernel (forced here by requesting the second moments)."""
+    rng = np.random.default_rng(n + T)
+    x = (rng.normal(0.0, 0.7, size=(T, n, 3)) + rng.uniform(-2, 2, size=(T, 1, 3))).astype(np.float32)
+    x[3] *= 1e-3  # a structure with a very different scale
+    xt = torch.from_numpy(x).to(cuda_device)
+    w = torch.full((n,), 1.0 / n, dtype=torch.float64, device=cuda_device)
+    sp = K.center_split(xt, w, w, weighted=False, fmt="f16", terms=1)
+    xd = x.astype(np.float64)
+    c = xd.mean(axis=1)
+    v = xd - c[:, None, :]
+    np.testing.assert_allclose(sp.centroid.cpu().numpy(), c, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(sp.g.cpu().numpy(), (v * v).sum(axis=(1, 2)) / n, rtol=1e-12)
+    np.testing.assert_allclose(sp.opnorm.cpu().numpy(), np.sqrt((v * v).sum(axis=(1, 2))), rtol=1e-12)
+    assert np.abs(sp.wbar.cpu().numpy()).max() < 1e-12
+    sinv = sp.scale.cpu().numpy()
+    h = sp.hi.float().cpu().numpy()[:, :, :n].transpose(1, 2, 0).astype(np.float64) * sinv[:, None, None]
+    res = np.sqrt(((h - v) ** 2).sum(axis=(1, 2)))
+    rn = sp.rnorm.cpu().numpy()
+    assert np.all(res <= rn) and np.all(rn <= res * (1 + 2e-5) + 2 ** -23 * sp.opnorm.cpu().numpy())
+    assert np.all(np.abs(h - v) <= 2 ** -11 * np.abs(v) + 2 ** -24 * sinv[:, None, None] + 1e-300)
+    ref = K.center_split(xt, w, w, weighted=False, moments=True, fmt="f16", terms=1)
+    for a, b in ((sp.centroid, ref.centroid), (sp.scale, ref.scale), (sp.g, ref.g), (sp.opnorm, ref.opnorm)):
+        np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(sp.rnorm.cpu().numpy(), ref.rnorm.cpu().numpy(), rtol=1e-3)
