@@ -328,6 +328,33 @@ int mc_mtd_grid_eval(const double* val, const double* dgrid, const double* dxy, 
 int mc_mtd_force(const double* dV, int32_t T, int32_t d, const void* g0, const void* g1, const void* g2, int dtype,
                  int32_t n, void* F, void* stream);
 
+/* ---- toy MD driver (SPEC [MODULE] toysim run) ----
+ * mc_toysim_run: W independent walkers (one CTA each) advance `steps` overdamped Langevin
+ *   steps (Euler-Maruyama, x += mob F + noise xi, xi ~ N(0,1) from Philox4x32-10 keyed by
+ *   `seed`, counter (bead, step, walker)) of an n-bead chain (harmonic bonds bond_k, bond_r0;
+ *   harmonic angles angle_k, theta0; n <= 64) in ONE launch.  mode 0: free dynamics (the
+ *   reference-set pre-run); 1: original method (Alg. 1, exact fits to all L <= 128
+ *   references every step); 2: close structure (Alg. 2, threshold eps, strict '>').
+ *   Per step: path CV s, z (lambda = lam) of the centred frame, metadynamics hills on s
+ *   (height hill_h, width hill_sigma, deposited at the step's s when step % tau_g == 0,
+ *   after the step's force; capacity max_hills), bias force -dV/ds ds/dx.
+ *   refs [L, n, 3] centred, refg [L] = sum w |a|^2, refmom [L, 6] = sum w a a^T (xx, xy,
+ *   xz, yy, yz, zz), q [L], w / wa [n] displacement / alignment weights.  State in/out:
+ *   x, y [W, n, 3], rays [W, L, 9] (saved R_{a_i y}), hasy [W], hills [W, max_hills],
+ *   nhills [W], counters [W, 3] (+= expensive, cheap, reassign; SPEC msd-engine rules).
+ *   Out: cv [W, steps, 4] = (s, z, V_bias, D(x, y)), rlog [W, steps] (1 = reassigned),
+ *   traj [W, ceil(steps / traj_stride), n, 3] positions at the start of steps
+ *   step0 + k traj_stride (traj_stride 0: none; step0 % traj_stride == 0), flags [W]
+ *   (|= NoConverge / NonFinite / SigOverflow = hill capacity exceeded).  Continuing a run:
+ *   call again with step0 += steps and the same state arrays. */
+int mc_toysim_run(int32_t W, int32_t n, int32_t L, int32_t steps, int64_t step0, int32_t mode, int32_t tau_g,
+                  int32_t max_hills, int32_t traj_stride, double bond_k, double bond_r0, double angle_k,
+                  double theta0, double mob, double noise, double lam, double eps, double hill_h, double hill_sigma,
+                  uint64_t seed, const double* refs, const double* refg, const double* refmom, const double* q,
+                  const double* w, const double* wa, double* x, double* y, double* rays, int32_t* hasy,
+                  double* hills, int32_t* nhills, int64_t* counters, double* cv, uint8_t* rlog, double* traj,
+                  uint8_t* flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

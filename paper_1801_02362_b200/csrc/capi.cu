@@ -414,4 +414,29 @@ int mc_mtd_force(const double* dV, int32_t T, int32_t d, const void* g0, const v
   return cuda_status(mc::launch_mtd_force(dV, T, d, g0, g1, g2, dtype, n, F, S_(stream)));
 }
 
+int mc_toysim_run(int32_t W, int32_t n, int32_t L, int32_t steps, int64_t step0, int32_t mode, int32_t tau_g,
+                  int32_t max_hills, int32_t traj_stride, double bond_k, double bond_r0, double angle_k,
+                  double theta0, double mob, double noise, double lam, double eps, double hill_h, double hill_sigma,
+                  uint64_t seed, const double* refs, const double* refg, const double* refmom, const double* q,
+                  const double* w, const double* wa, double* x, double* y, double* rays, int32_t* hasy,
+                  double* hills, int32_t* nhills, int64_t* counters, double* cv, uint8_t* rlog, double* traj,
+                  uint8_t* flags, void* stream) {
+  if (W < 0 || n < 3 || n > 64 || steps < 0 || step0 < 0 || mode < 0 || mode > 2 || tau_g < 0 || max_hills < 0 ||
+      traj_stride < 0 || !(mob > 0.0) || !(noise >= 0.0) || !(bond_r0 > 0.0))
+    return MC_ERR_CONFIG;
+  if (mode != 0 && (L < 1 || L > 128 || !(lam > 0.0) || !(eps >= 0.0) || !(hill_sigma > 0.0) || !(hill_h >= 0.0)))
+    return MC_ERR_CONFIG;
+  if (traj_stride > 0 && step0 % traj_stride != 0) return MC_ERR_CONFIG;
+  if (W > 0 && steps > 0) {
+    if (!x || !y || !w || !wa || !hasy || !nhills || !counters || (traj_stride > 0 && !traj)) return MC_ERR_CONFIG;
+    if (mode != 0 && (!refs || !refg || !refmom || !q || !cv || !rlog || (max_hills > 0 && !hills)))
+      return MC_ERR_CONFIG;
+    if (mode == 2 && !rays) return MC_ERR_CONFIG;
+  }
+  mc::ToyParams P{n, L, steps, mode, tau_g, max_hills, traj_stride, (long long)step0, bond_k, bond_r0, angle_k,
+                  theta0, mob, noise, lam, eps, hill_h, hill_sigma, (unsigned long long)seed};
+  return cuda_status(mc::launch_toysim(P, W, refs, refg, refmom, q, w, wa, x, y, rays, hasy, hills, nhills,
+                                       reinterpret_cast<long long*>(counters), cv, rlog, traj, flags, S_(stream)));
+}
+
 }  // extern "C"

@@ -120,4 +120,14 @@ cudaError_t launch_gather_rows(const void* src, int esz, int64_t rowlen, const i
 cudaError_t launch_msd_f16_2sm(const void* fhl, const void* lhl, const double* fsc, const double* lsc,
                                const double* gx, const double* ga, int T, int L, int kpad, float* D, int64_t ldd,
                                int grid, cudaStream_t stream);
+struct ToyParams {  // csrc/toysim.cu
+  int n, L, steps, mode, tau_g, max_hills, traj_stride;
+  long long step0;
+  double bond_k, bond_r0, angle_k, theta0, mob, noise, lam, eps, hill_h, hill_sigma;
+  unsigned long long seed;
+};
+cudaError_t launch_toysim(const ToyParams& P, int W, const double* refs, const double* refg, const double* refmom,
+                          const double* q, const double* w, const double* wa, double* xs, double* ys, double* rays,
+                          int* hasy, double* hills, int* nhills, long long* counters, double* cv, uint8_t* rlog,
+                          double* traj, uint8_t* flags, cudaStream_t stream);
 }  // namespace mc

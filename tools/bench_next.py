@@ -5,7 +5,10 @@
 * metadynamics bias force (`mc_mtd_force`) on the path-CV gradients
   [T, N, 3] fp32 (ds, dz) — HBM-bound: 2 x 12 T N read + 12 T N written;
 * direct hill sum (`mc_mtd_bias_direct`) for T frames x H hills — one exp per
-  (frame, hill): reported as Gexp/s.
+  (frame, hill): reported as Gexp/s;
+* the toy MD driver (`mc_toysim_run`, SPEC toysim, 8(f) 3): W walkers x S steps
+  of an 8-bead chain against 16 references in the close-structure and original
+  modes, one launch — walker-steps/s, beside the numpy oracle's rate (1 core).
 
 CUDA events, after warm-up; prints one JSON line per kernel with the roofline
 fraction against MEASURED_PEAKS.json hbm_gbs.
@@ -44,6 +47,8 @@ def main():
     ap.add_argument("--N", type=int, default=10000)
     ap.add_argument("--M", type=int, default=64)
     ap.add_argument("--H", type=int, default=4096)
+    ap.add_argument("--W", type=int, default=4096, help="toy MD walkers")
+    ap.add_argument("--S", type=int, default=2000, help="toy MD steps per launch")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "MEASURED_PEAKS.json")) as f:
@@ -79,6 +84,38 @@ def main():
     ms = timed(lambda: st.bias(cv, use_grid=False))
     print(json.dumps({"kernel": "mc_mtd_bias_direct", "frames": a.T, "hills": a.H, "ms": ms,
                       "Gexp_per_s": a.T * a.H / ms / 1e6}))
+    del ds, dz, F
+    toysim_rows(a)
+
+
+def toysim_rows(a):
+    import time
+
+    import numpy as np
+
+    from oracle import toysim as OT
+    from paper_1801_02362_b200.toysim import MtdConfig, ToySim, ToySystem, make_references
+
+    sysm = ToySystem(rng_seed=1)
+    refs = make_references(sysm, n_refs=16, stride=300)
+    for mode in ("close", "original"):
+        sim = ToySim(sysm, refs, mode=mode, eps=0.01, mtd=MtdConfig(), walkers=a.W, max_hills=(50 + 3 * a.S) // 50 + 2)
+        sim.run(50)
+        torch.cuda.synchronize()
+        ms = timed(lambda: sim.run(a.S), iters=2)
+        sim.check()
+        reas = sim.counters[:, 2].double().sum().item()
+        steps_done = a.W * (50 + 3 * a.S)
+        p = {"bond_k": sysm.bond_k, "bond_r0": sysm.bond_r0, "angle_k": sysm.angle_k, "theta0": sysm.theta0,
+             "mob": sysm.mobility, "noise": sysm.noise, "seed": 1, "tau_g": 50, "lam": 100.0, "eps": 0.01,
+             "hill_h": 0.5, "hill_sigma": 0.5}
+        t0 = time.perf_counter()
+        OT.run(p, refs, np.arange(16.0), sysm.initial_chain(), 100, mode=2 if mode == "close" else 1)
+        cpu = 100 / (time.perf_counter() - t0)
+        print(json.dumps({"kernel": "mc_toysim_run", "mode": mode, "walkers": a.W, "steps": a.S, "beads": 8,
+                          "references": 16, "ms": ms, "walker_steps_per_s": a.W * a.S / ms * 1e3,
+                          "mean_K": steps_done / max(reas, 1) if mode == "close" else None,
+                          "cpu_oracle_steps_per_s_1core": cpu}))
 
 
 if __name__ == "__main__":
