@@ -177,6 +177,10 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   }
   __syncthreads();
   const int wlo = s_wlo, whi = s_whi;
+  // no significant landmark in the whole group (landmark-sharded evaluation: frames whose
+  // window lies on other shards): nothing to contract and nothing to write -- those rows
+  // belong to (and are completed by) other ranks
+  if (whi < 0) return;
   const bool restage = whi - wlo > DWMAX;
   const int nwc = whi > wlo ? (whi - wlo + DWMAX - 1) / DWMAX : 0;
   const bool ranged = nwc <= MAXWC;  // else: each restage filters the whole list

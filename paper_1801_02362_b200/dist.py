@@ -43,6 +43,25 @@ def shard_range(total, rank, world):
     return offset, count
 
 
+def balanced_bounds(load, world, floor=1.0):
+    """Contiguous landmark shards with equal work: cut the cumulative per-landmark load
+    (``PathCVTC.landmark_load`` on a frame sample, plus ``floor`` per landmark for the
+    per-landmark fixed costs) at its G quantiles.  Returns G + 1 offsets 0 = b_0 < ... <
+    b_G = L (every shard keeps >= 1 landmark)."""
+    load = torch.as_tensor(load, dtype=torch.float64).cpu() + float(floor)
+    L = int(load.numel())
+    if not 1 <= world <= L:
+        raise ValueError("1 <= world <= number of landmarks")
+    cum = torch.cumsum(load, 0)
+    tot = float(cum[-1])
+    b = [0]
+    for g in range(1, world):
+        cut = int(torch.searchsorted(cum, torch.tensor(tot * g / world, dtype=torch.float64)).item()) + 1
+        b.append(min(max(cut, b[-1] + 1), L - (world - g)))
+    b.append(L)
+    return b
+
+
 def merge_partials(s_parts, z_parts, lam):
     """Merge per-shard (s_g, z_g) [G, T] into global (s, z, w [G, T]); fixed order.
     A shard with an empty window for frame t reports z_g = +inf (w_g = 0)."""

@@ -316,11 +316,13 @@ class PathCVTC:
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
                  operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None):
-        """shard = (rank, world): landmark-sharded evaluation.
-        ``landmarks`` (and q) are the FULL set; this engine keeps landmarks
-        shard_range(L, rank, world) with their global q, and the landmark-norm maxima of
-        the one-term error bound over the full set (identical windows on every shard
-        count).  Evaluate with ``evaluate_sharded`` / ``sharded_steps``."""
+        """shard = (rank, world[, bounds]): landmark-sharded evaluation.
+        ``landmarks`` (and q) are the FULL set; this engine keeps the contiguous landmarks
+        [bounds[rank], bounds[rank + 1]) -- default shard_range(L, rank, world); work-
+        balanced bounds from ``landmark_load`` + ``dist.balanced_bounds`` -- with their
+        global q, and the landmark-norm maxima of the one-term error bound over the full
+        set (identical windows on every shard count).  Evaluate with
+        ``evaluate_sharded`` / ``sharded_steps``."""
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
         self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
@@ -351,7 +353,13 @@ class PathCVTC:
             rank, world = int(shard[0]), int(shard[1])
             if not (0 <= rank < world):
                 raise ConfigError(f"shard {shard!r}")
-            off, cnt = shard_range(self.L, rank, world)
+            if len(shard) > 2 and shard[2] is not None:
+                b = [int(v) for v in shard[2]]
+                if len(b) != world + 1 or b[0] != 0 or b[-1] != self.L or any(x > y for x, y in zip(b, b[1:])):
+                    raise ConfigError("shard bounds must be 0 = b_0 <= ... <= b_G = L")
+                off, cnt = b[rank], b[rank + 1] - b[rank]
+            else:
+                off, cnt = shard_range(self.L, rank, world)
             if cnt < 1:
                 raise EmptyActiveSetError(f"landmark shard {rank} of {world} is empty (L = {self.L})")
             if self.screen == "f16x1":
@@ -560,11 +568,24 @@ class PathCVTC:
 
     # ------------------------------------------------------------ landmark sharding
 
+    def landmark_load(self, frames):
+        """Per-landmark work of an evaluation of ``frames`` (unsharded engine): how many
+        frames' exact windows cover each landmark (refits and gradient rows scale with
+        it).  Input to ``dist.balanced_bounds`` for work-balanced landmark shards."""
+        out = self.evaluate(frames, grad=False)
+        lo, cnt = out["window_lo"].long(), out["window_cnt"].long()
+        diff = torch.zeros(self.L + 1, dtype=torch.int64, device=self.device)
+        diff.index_add_(0, lo, torch.ones_like(lo))
+        diff.index_add_(0, lo + cnt, -torch.ones_like(lo))
+        return torch.cumsum(diff[:-1], 0)
+
+
     def evaluate_sharded(self, frames, grad=True, out_dtype=torch.float32, comm=None):
         """Landmark-sharded evaluate over a torch.distributed group (comm: dist.DistComm,
         default the world group).  Returns s, z [T] (global, every rank) and, with grad,
         ds, dz [T, n, 3] whose rows with owner == rank are complete (the others hold
-        this shard's partial sums), plus owner [T]."""
+        this shard's partial sums, or are left unwritten where this shard has no
+        window), plus owner [T]."""
         from . import dist as Dd
         return Dd.drive(self.sharded_steps(frames, grad, out_dtype), comm or Dd.DistComm())
 

@@ -212,3 +212,14 @@ def test_merge_partials_empty_shard():
     assert w[0, 1] == 0 and w[1, 1] == 1 and ms[1] == 3.0 and mz[1] == 0.1
     np.testing.assert_allclose(w[:, 0].numpy(), [0.5, 0.5])
     assert D.gradient_owners(z).tolist() == [0, 1]
+
+
+def test_balanced_bounds():
+    b = D.balanced_bounds(torch.ones(10), 3)
+    assert b == [0, 4, 7, 10]
+    load = torch.zeros(64)
+    load[10:14] = 1000.0  # one hot region
+    b = D.balanced_bounds(load, 4)
+    assert b[0] == 0 and b[-1] == 64 and all(x < y for x, y in zip(b, b[1:]))
+    assert sum(1 for x in b[1:-1] if 10 <= x <= 14) >= 2  # the hot region is split
+    assert D.balanced_bounds(torch.zeros(4), 4) == [0, 1, 2, 3, 4]

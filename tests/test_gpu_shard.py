@@ -32,8 +32,8 @@ def _rows_close(x, y, rel):
     assert np.all(err <= rel * scale + 1e-300), float((err / scale).max())
 
 
-def _sharded(wl, G, **kw):
-    engs = [engine.PathCVTC(wl.landmarks, wl.lam, shard=(g, G), **kw) for g in range(G)]
+def _sharded(wl, G, bounds=None, **kw):
+    engs = [engine.PathCVTC(wl.landmarks, wl.lam, shard=(g, G, bounds), **kw) for g in range(G)]
     outs = D.drive_lockstep([e.sharded_steps(wl.frames, out_dtype=torch.float64) for e in engs])
     return engs, outs
 
@@ -84,6 +84,25 @@ def test_landmark_sharded_vs_oracle(cuda_device):
         mine = owner == g
         for key in ("ds", "dz"):
             _rows_close(o[key].cpu().numpy()[mine], ref[key][mine], 1e-5)
+
+
+def test_work_balanced_landmark_shards(cuda_device):
+    """Contiguous shards cut at equal window load (landmark_load + balanced_bounds): the
+    same results as the unsharded evaluate, with uneven shard sizes."""
+    wl = synth.config4(T=260, L=1536, N=240)
+    full = engine.PathCVTC(wl.landmarks, wl.lam)
+    load = full.landmark_load(wl.frames[:128])
+    assert int(load.sum().item()) == int(full.evaluate(wl.frames[:128], grad=False)["window_cnt"].sum().item())
+    b = D.balanced_bounds(load, 3)
+    ref = full.evaluate(wl.frames, out_dtype=torch.float64)
+    engs, outs = _sharded(wl, 3, bounds=b)
+    assert [e.L for e in engs] == [b[1] - b[0], b[2] - b[1], b[3] - b[2]]
+    owner = outs[0]["owner"].cpu().numpy()
+    for g, o in enumerate(outs):
+        np.testing.assert_allclose(o["s"].cpu().numpy(), ref["s"].cpu().numpy(), rtol=1e-9, atol=1e-12)
+        mine = owner == g
+        for key in ("ds", "dz"):
+            _rows_close(o[key].cpu().numpy()[mine], ref[key].cpu().numpy()[mine], 1e-7)
 
 
 def test_landmark_shard_window_overflow_retry(cuda_device):
