@@ -60,3 +60,64 @@ def test_config4_fullsize_properties_and_spot_checks(cuda_device):
         r = ref[key]
         scale = np.abs(r).reshape(3, -1).max(axis=1)
         assert np.all(np.abs(got - r).reshape(3, -1).max(axis=1) <= 1e-5 * scale)
+
+
+def _rigid(x, rng):
+    """Random rotation (uniform quaternion) + translation of every structure in x [B, n, 3]."""
+    q = rng.normal(size=(x.shape[0], 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    a, b, c, d = q.T
+    R = np.stack([np.stack([a * a + b * b - c * c - d * d, 2 * (b * c - a * d), 2 * (b * d + a * c)], -1),
+                  np.stack([2 * (b * c + a * d), a * a - b * b + c * c - d * d, 2 * (c * d - a * b)], -1),
+                  np.stack([2 * (b * d - a * c), 2 * (c * d + a * b), a * a - b * b - c * c + d * d], -1)], 1)
+    return np.einsum("bij,bnj->bni", R, x) + rng.uniform(-1, 1, size=(x.shape[0], 1, 3))
+
+
+def test_config2_fullsize_matrix_properties_and_spot_checks(cuda_device):
+    """Config 2 at full size (65536 x 4096 x 1000, every pair refit exactly): finite and
+    non-negative; four full rows against the C restatement of the reference (1e-6 relative
+    or 1e-9 absolute); rigid-motion invariance of 256 rows; near-identical pairs (a
+    landmark under a rigid motion as a frame) give D ~ 0 within 1e-9 absolute."""
+    wl = synth.interp_config_device(2, 65536, 4096, 1000, 16, cuda_device)
+    lms = torch.from_numpy(wl.landmarks).to(cuda_device)
+    pcv = engine.PathCVTC(lms, wl.lam, wl.q)
+    D = pcv.msd_matrix(wl.frames)
+    assert D.shape == (65536, 4096)
+    assert bool(torch.isfinite(D).all()) and float(D.min()) > -1e-9
+    idx = [0, 12345, 40000, 65535]
+    ref, _ = C.msd_matrix(wl.frames[idx].double().cpu().numpy(), wl.landmarks.astype(np.float64))
+    got = D[idx].double().cpu().numpy()
+    assert np.all(np.abs(got - ref) <= np.maximum(1e-6 * np.abs(ref), 1e-9 + 6e-8 * np.abs(ref)))
+    rng = np.random.default_rng(7)
+    rows = rng.choice(65536, 256, replace=False)
+    moved = torch.from_numpy(_rigid(wl.frames[rows].double().cpu().numpy(), rng)).float().to(cuda_device)
+    # fp32 storage of the moved coordinates changes them by ~1e-7 relative
+    np.testing.assert_allclose(pcv.msd_matrix(moved).cpu().numpy(), D[rows].cpu().numpy(), rtol=2e-5, atol=1e-7)
+    same = torch.from_numpy(_rigid(wl.landmarks[:64].astype(np.float64), rng)).float().to(cuda_device)
+    d0 = pcv.msd_matrix(same).double().cpu().numpy()[np.arange(64), np.arange(64)]
+    ref0 = C.msd_matrix(same.double().cpu().numpy(), wl.landmarks[:64].astype(np.float64))[0][np.arange(64), np.arange(64)]
+    assert np.all(np.abs(d0 - ref0) <= 1e-9), np.abs(d0 - ref0).max()
+
+
+def test_config3_fullsize_two_walkers_vs_c_oracle(cuda_device):
+    """Config 3 at full size per walker (1000 steps, N = 2500, L = 2048, fp32): two of the
+    256 walkers replayed on the device (close structure on DMMA) against the C restatement:
+    identical refresh logs, s and z within 1e-6, D(x, y) within 1e-6 relative; gradients
+    of the first 40 steps within 1e-5 of the per-frame maximum."""
+    wl = synth.walkers_device(3, 256, 1000, 2500, 2048, cuda_device, walker_offset=17, walker_count=2)
+    out = engine.close_structure_replay(wl.frames, wl.landmarks, wl.lam, wl.eps)
+    fr = wl.frames.double().cpu().numpy()
+    lm = wl.landmarks.astype(np.float64)
+    for k in range(2):
+        sl = slice(k * 1000, (k + 1) * 1000)
+        ref = C.close_replay(fr[k], lm, wl.lam, wl.eps, grad=False)
+        np.testing.assert_array_equal(out["refresh"].cpu().numpy()[sl], ref["refresh"])
+        np.testing.assert_allclose(out["s"].cpu().numpy()[sl], ref["s"], rtol=1e-6)
+        np.testing.assert_allclose(out["z"].cpu().numpy()[sl], ref["z"], rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(out["dxy"].cpu().numpy()[sl][1:], ref["dxy"][1:], rtol=1e-6, atol=1e-9)
+        assert 0 < ref["refresh"].sum() < 1000
+    sub = C.close_replay(fr[0][:40], lm, wl.lam, wl.eps)
+    for key in ("ds", "dz"):
+        got, r = out[key][:40].double().cpu().numpy(), sub[key]
+        scale = np.abs(r).reshape(40, -1).max(axis=1)
+        assert np.all(np.abs(got - r).reshape(40, -1).max(axis=1) <= 1e-5 * scale)
