@@ -93,6 +93,13 @@ def _raise_flags(flags, what):
         raise MetadynError(f"{what}: Jacobi diagonalisation did not converge")
 
 
+def _raise_bits(f, what):
+    if f & FLAG_NON_FINITE:
+        raise InvalidStructureError(f"{what}: non-finite coordinates or distances")
+    if f & FLAG_NO_CONVERGE:
+        raise MetadynError(f"{what}: Jacobi diagonalisation did not converge")
+
+
 def _or_flags(flags):
     return int(np.bitwise_or.reduce(flags.flatten().cpu().numpy())) if flags.numel() else 0
 
@@ -100,9 +107,15 @@ def _or_flags(flags):
 _FLAG_BITS = (1, 2, 4, 8, 16)
 
 
+_BITS = {}
+
+
 def _flag_bits_dev(flags):
-    """Bitwise OR of a uint8 flag array as a device bool[5] (no host sync)."""
-    bits = torch.tensor(_FLAG_BITS, dtype=torch.int32, device=flags.device)
+    """Bitwise OR of a uint8 flag array as a device bool[5] (no host sync; the bit
+    table is cached per device, so the call is CUDA-graph capturable after one use)."""
+    bits = _BITS.get(flags.device)
+    if bits is None:
+        bits = _BITS[flags.device] = torch.tensor(_FLAG_BITS, dtype=torch.int32, device=flags.device)
     if flags.numel() == 0:
         return torch.zeros(len(_FLAG_BITS), dtype=torch.bool, device=flags.device)
     return ((flags.flatten().to(torch.int32)[:, None] & bits) != 0).any(0)
@@ -188,6 +201,10 @@ class PathCV:
 
     def _cap(self, cap):
         return int(min(self.L, 512) if cap is None else min(cap, self.L))
+
+    def graph(self, T, grad=True, dtype=torch.float64, out_dtype=None):
+        """A CUDA-graph replay of evaluate() for T frames of ``dtype`` (PathCVGraph)."""
+        return PathCVGraph(self, T, grad=grad, dtype=dtype, out_dtype=out_dtype)
 
     def evaluate(self, frames, grad=True, cap=None, out_dtype=None):
         """Alg. 1 without neighbour list: exact D_i for every landmark."""
@@ -290,6 +307,83 @@ class PathCV:
         if grad:
             out["ds"], out["dz"] = ds, dz
         return out
+
+
+class PathCVGraph:
+    """CUDA-graph replay of ``PathCV.evaluate`` for a fixed frame count (the small,
+    launch-bound configurations: config 0 is ~0.12 ms of kernels behind ~0.23 ms of
+    launches and host checks).  The whole pipeline -- centring, covariances, fits,
+    K4 weights over every landmark (capacity L: no overflow retry), gradients -- is
+    captured once on static buffers; ``evaluate(frames)`` copies the frames in,
+    replays the graph and returns the static output tensors (overwritten by the next
+    call).  No host synchronisation inside: the status bits of every stage are
+    OR-ed on the device and raised by ``check()`` (call it whenever convenient)."""
+
+    def __init__(self, pcv: "PathCV", T, grad=True, dtype=torch.float64, out_dtype=None):
+        if int(T) < 1:
+            raise ConfigError("graph frame count must be >= 1")
+        if int(T) * pcv.L * 160 > 2 ** 31:
+            raise ConfigError("graph mode keeps every landmark's coefficients: T * L too large")
+        self.pcv, self.T, self.grad = pcv, int(T), bool(grad)
+        self.x = torch.zeros((self.T, pcv.n, 3), dtype=dtype, device=pcv.device)
+        self.out_dtype = out_dtype
+        side = torch.cuda.Stream(device=pcv.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up: one-time attributes, allocator pools
+            self._pipeline()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize(pcv.device)
+        self.graph = torch.cuda.CUDAGraph()
+        from . import _lib
+
+        n0 = _lib.COUNTERS["launches"]
+        with torch.cuda.graph(self.graph):
+            self.out = self._pipeline()
+        self.launches = _lib.COUNTERS["launches"] - n0  # library kernels per replay
+
+    def _pipeline(self):
+        p = self.pcv
+        fr = K.center(self.x, p.wa, p.w)
+        S = p._cov(self.x, fr)
+        D, R, _, fflags = K.fit_dense(S, fr.g, p.lm.g, want_rot=True)
+        T = self.T
+        s = torch.empty((T,), dtype=torch.float64, device=p.device)
+        z = torch.empty((T,), dtype=torch.float64, device=p.device)
+        wres = K.pathcv_weights(D, p.q, p.lam, R, fr, p.lm, p.L, p.cutoff, s=s, z=z)
+        out = {"s": s, "z": z, "D": D, "nsig": wres["nsig"]}
+        if self.grad:
+            raw = self.x
+            odt = self.out_dtype or (torch.float64 if raw.dtype == torch.float64 else torch.float32)
+            ds = torch.empty((T, p.n, 3), dtype=odt, device=p.device)
+            dz = torch.empty((T, p.n, 3), dtype=odt, device=p.device)
+            if p._dmma(raw):
+                gperm = K.sort_by_key(K.sig_span_key(wres, p.L), 2 * p.L + 1)
+                K.pathcv_grad_block(wres, fr, p.lm, raw, p.lraw, p.w, p.wa, p.L, gperm, ds=ds, dz=dz)
+            else:
+                K.pathcv_grad(wres, fr, p.lm, p.w, p.wa, p.L, odt, ds=ds, dz=dz)
+            out["ds"], out["dz"] = ds, dz
+        out["status"] = torch.stack([_flag_bits_dev(fr.flags), _flag_bits_dev(fflags), _flag_bits_dev(wres["flags"])])
+        return out
+
+    def evaluate(self, frames):
+        """Copy ``frames`` [T, n, 3] (host or device) in, replay; returns the static outputs."""
+        if tuple(frames.shape) != (self.T, self.pcv.n, 3):
+            raise InvalidStructureError(f"graph captured for frames [{self.T}, {self.pcv.n}, 3]")
+        from . import _lib
+
+        self.x.copy_(frames, non_blocking=True)
+        self.graph.replay()
+        _lib.COUNTERS["launches"] += self.launches
+        return self.out
+
+    def check(self):
+        """Raise the errors evaluate() would have raised for the last replay (one host read)."""
+        ff, fit, wf = (_bits_value(r) for r in self.out["status"].cpu().tolist())
+        if ff & FLAG_NON_FINITE:
+            raise InvalidStructureError("frame coordinates contain non-finite values")
+        _raise_bits(fit, "path_cv")
+        if wf & FLAG_NON_FINITE:
+            raise InvalidStructureError("non-finite distances in the path-CV reduction")
 
 
 class PathCVTC:

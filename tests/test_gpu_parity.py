@@ -12,6 +12,7 @@ import torch
 
 from oracle import oracle as O
 from paper_1801_02362_b200 import engine, kernels as K, synth
+from paper_1801_02362_b200.errors import InvalidStructureError
 
 pytestmark = pytest.mark.gpu
 
@@ -257,3 +258,23 @@ def test_close_replay_dmma_path_equals_fp64_path(cuda_device):
     np.testing.assert_allclose(oa["z"].cpu().numpy(), ob["z"].cpu().numpy(), rtol=1e-10, atol=1e-15)
     for key in ("ds", "dz"):
         assert_grad(oa[key].cpu().numpy(), ob[key].cpu().numpy(), rtol=1e-6)
+
+
+def test_cuda_graph_replay_equals_eager(cuda_device):
+    """PathCVGraph (config-0 shape): the replayed pipeline gives the eager evaluate()'s
+    s, z and gradients bit for bit, for several inputs; errors surface through check()."""
+    wl = synth.config0()
+    pcv = engine.PathCV(torch.from_numpy(wl.landmarks).to(cuda_device), wl.lam, wl.q)
+    g = pcv.graph(wl.frames.shape[0])
+    for k in range(3):
+        fr = torch.from_numpy(wl.frames + 0.01 * k).to(cuda_device)
+        out = g.evaluate(fr)
+        g.check()
+        ref = pcv.evaluate(fr, grad=True, cap=pcv.L)
+        for key in ("s", "z", "ds", "dz"):
+            assert torch.equal(out[key], ref[key]), key
+    bad = torch.from_numpy(wl.frames.copy()).to(cuda_device)
+    bad[5, 3, 1] = float("nan")
+    g.evaluate(bad)
+    with pytest.raises(InvalidStructureError):
+        g.check()
