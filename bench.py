@@ -290,12 +290,20 @@ class ConfigTC:
         if frames_override:
             shp["T"] = frames_override
         self.shard = shard
+        if shard.startswith("landmarks") and cfg != 4:
+            raise SystemExit("--shard landmarks applies to config 4 (path-CV)")
         if shard == "landmarks":
-            # the north_star's variant: every rank holds all T
-            # frames and its landmark shard; per-frame minima / partials / straddling
-            # gradient rows are exchanged over NCCL; strong scaling (total work fixed)
-            if cfg != 4:
-                raise SystemExit("--shard landmarks applies to config 4 (path-CV)")
+            # the north_star's variant, frame-routed: rank g holds a
+            # landmark shard (48-landmark tile bounds) and its T/G home frames; frames are
+            # routed to the shards their admissible tiles live on, gradient rows come back
+            # home; strong scaling (total work fixed), each rank copies only its home frames
+            from paper_1801_02362_b200 import dist as Dd
+
+            T_all = shp["T"]
+            off, cnt = Dd.shard_range(T_all, rank, world)
+        elif shard == "landmarks-replicated":
+            # every rank holds all T frames and its landmark shard; per-frame minima /
+            # partials / straddling gradient rows are exchanged over NCCL
             T_all, off, cnt = shp["T"], 0, shp["T"]
         else:
             # weak scaling: every rank evaluates its own full-size frame set (disjoint
@@ -306,9 +314,15 @@ class ConfigTC:
                                              frame_offset=off, frame_count=cnt)
         self.T_all, self.T = T_all, cnt
         self.n, self.L = shp["N"], shp["L"]
-        self.pcv = engine.PathCVTC(torch.from_numpy(self.wl.landmarks).to(device), self.wl.lam, self.wl.q,
-                                   shard=(rank, world) if shard == "landmarks" else None)
+        self._off, self._c0 = off, 0
+        lms = torch.from_numpy(self.wl.landmarks).to(device)
         if shard == "landmarks":
+            self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q, shard=(rank, world, Dd.tile_bounds(self.L, world)),
+                                       route=True)
+        else:
+            self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q,
+                                       shard=(rank, world) if shard == "landmarks-replicated" else None)
+        if shard.startswith("landmarks"):
             from paper_1801_02362_b200 import dist as Dd
 
             self._comm = Dd.DistComm() if world > 1 else None
@@ -322,6 +336,11 @@ class ConfigTC:
             self.frames_host = self.frames_dev.cpu()
             self.host_kind = "pageable (pinning failed)"
         if shard == "landmarks":
+            self.parallelism = (f"landmark-sharded x{world}, frame-routed (NCCL: frames to their shards, "
+                                "per-frame min/partials, gradient rows home)")
+            self.scaling = "strong"
+            self.replicated_units = True  # value = the T global frames / the slowest rank's time
+        elif shard == "landmarks-replicated":
             self.parallelism = f"landmark-sharded x{world} (NCCL: per-frame min/partials + straddling rows)"
             self.scaling = "strong"
             self.replicated_units = True  # every rank evaluates the same T frames
@@ -339,10 +358,13 @@ class ConfigTC:
     def _step(self, frames, D=None):
         if self.cfg == 2:
             self.last = self.pcv.msd_matrix(frames) if D is None else self._msd_into(frames, D)
-        elif self.shard == "landmarks":
+        elif self.shard.startswith("landmarks"):
             from paper_1801_02362_b200 import dist as Dd
 
-            steps = self.pcv.sharded_steps(frames, grad=True)
+            if self.shard == "landmarks":
+                steps = self.pcv.routed_steps(frames, self._off + self._c0, self.T_all, grad=True)
+            else:
+                steps = self.pcv.sharded_steps(frames, grad=True)
             self.last = Dd.drive(steps, self._comm) if self._comm else Dd.drive_lockstep([steps])[0]
         else:
             self.last = self.pcv.evaluate(frames, grad=True)
@@ -454,9 +476,11 @@ class ConfigTC:
                 D = self._step(fr)
                 outs.append(D.to("cpu", non_blocking=True))
             else:
+                self._c0 = chunks[i][0]  # home offset of this chunk (frame-routed landmark shards)
                 o = self._step(fr)
                 outs.append(o["s"].to("cpu", non_blocking=True))
                 outs.append(o["z"].to("cpu", non_blocking=True))
+        self._c0 = 0
         comp.synchronize()
         return outs
 
@@ -500,7 +524,7 @@ class ConfigTC:
 
     def extra(self):
         d = {"pairs_per_step": self.T * self.L, "host_buffers": self.host_kind}
-        if self.shard == "landmarks":
+        if self.shard.startswith("landmarks"):
             d["landmarks_per_rank"] = self.pcv.L
         if self.cfg == 4 and self.last is not None:
             d["mean_window"] = float(self.last["window_cnt"].float().mean().item())
@@ -802,8 +826,9 @@ def main():
     ap.add_argument("--frames", type=int, default=0, help="override T (configs 2/4) for quick runs")
     ap.add_argument("--walkers", type=int, default=0, help="override W (config 3) for quick runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
-    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks"],
-                    help="multi-GPU split of config 4: frames (weak, no collective) or landmarks (strong, NCCL)")
+    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks", "landmarks-replicated"],
+                    help="multi-GPU split of config 4: frames (weak, no collective) or landmarks (strong, NCCL; "
+                         "frame-routed, or with every frame replicated on every rank)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

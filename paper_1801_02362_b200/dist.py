@@ -62,6 +62,22 @@ def balanced_bounds(load, world, floor=1.0):
     return b
 
 
+def tile_bounds(L, world, load=None, tile=48):
+    """Contiguous landmark shards cut at multiples of the screen's 48-landmark tile (the
+    frame-routed variant routes frames by tile hulls): balanced by ``load`` (per-landmark
+    work, ``PathCVTC.landmark_load``) when given, else by landmark count."""
+    ntl = (int(L) + tile - 1) // tile
+    if not 1 <= world <= ntl:
+        raise ValueError("1 <= world <= number of landmark tiles")
+    if load is None:
+        tl = torch.ones(ntl, dtype=torch.float64)
+    else:
+        ld = torch.as_tensor(load, dtype=torch.float64).cpu() + 1.0
+        tl = torch.nn.functional.pad(ld, (0, ntl * tile - int(L))).view(ntl, tile).sum(1)
+    b = balanced_bounds(tl, world, floor=0.0)
+    return [min(int(L), x * tile) for x in b]
+
+
 def merge_partials(s_parts, z_parts, lam):
     """Merge per-shard (s_g, z_g) [G, T] into global (s, z, w [G, T]); fixed order.
     A shard with an empty window for frame t reports z_g = +inf (w_g = 0)."""
@@ -193,6 +209,22 @@ class DistComm:
     def exchange(self, ds, dz, z_parts):
         return exchange_owned_rows(ds, dz, z_parts, self.group)
 
+    def alltoallv(self, fields):
+        """fields: list of per-destination row blocks (same row counts across fields).
+        Returns, per field, the list of blocks received from every source rank."""
+        if self.world == 1:
+            return [list(blocks) for blocks in fields]
+        counts = torch.tensor([int(b.shape[0]) for b in fields[0]], dtype=torch.int64, device=fields[0][0].device)
+        rcounts = torch.empty_like(counts)
+        dist.all_to_all_single(rcounts, counts, group=self.group)
+        rc = rcounts.cpu().tolist()
+        out = []
+        for blocks in fields:
+            shape = tuple(blocks[0].shape[1:])
+            out.append(_alltoall_rows([b.contiguous() for b in blocks], rc, shape, blocks[0].dtype,
+                                      blocks[0].device, self.group))
+        return out
+
 
 def drive(steps, comm):
     """Run a landmark-sharded evaluation generator (PathCVTC.sharded_steps) against
@@ -224,6 +256,9 @@ def drive_lockstep(steps_list, lam=None):
         elif op == "gather":
             v = torch.stack([r[1] for r in reqs])
             outs = [v for _ in range(G)]
+        elif op == "alltoallv":
+            nf = len(reqs[0][1])
+            outs = [[[reqs[g][1][f][h] for g in range(G)] for f in range(nf)] for h in range(G)]
         elif op == "exchange":
             # every shard's rows, owner-summed in rank order
             z_parts = reqs[0][3]

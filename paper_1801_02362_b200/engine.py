@@ -409,14 +409,18 @@ class PathCVTC:
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None):
+                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None, route=False):
         """shard = (rank, world[, bounds]): landmark-sharded evaluation.
         ``landmarks`` (and q) are the FULL set; this engine keeps the contiguous landmarks
         [bounds[rank], bounds[rank + 1]) -- default shard_range(L, rank, world); work-
         balanced bounds from ``landmark_load`` + ``dist.balanced_bounds`` -- with their
         global q, and the landmark-norm maxima of the one-term error bound over the full
         set (identical windows on every shard count).  Evaluate with
-        ``evaluate_sharded`` / ``sharded_steps``."""
+        ``evaluate_sharded`` / ``sharded_steps``.  route=True (frame-routed variant,
+        DESIGN.md section 7): bounds at multiples of the 48-landmark tile; the engine also
+        keeps the GLOBAL coarse screen (coarse landmarks, tile tables) so each rank screens
+        only its home frames and routes every frame to the shards its admissible tiles
+        live on; evaluate with ``evaluate_routed`` / ``routed_steps``."""
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
         self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
@@ -442,6 +446,15 @@ class PathCVTC:
         if qq.shape != (self.L,):
             raise ConfigError("q must have one value per landmark")
         self.shard = None
+        self._gprune = None
+        if shard is not None and route:
+            g = PathCVTC(lm, lam, q, w, w_align, cutoff, window_cap, device, operand_fmt, screen, True,
+                         coarse_stride, knear)
+            if not g.prune:
+                raise ConfigError("frame routing needs the metric-pruned screen (>= 16 tiles, equal weights)")
+            self._gprune = {"ls_coarse": g.ls_coarse, "mind": g.mind, "maxd": g.maxd, "cstride": g.cstride,
+                            "knear": g.knear, "ntl": int(g.mind.shape[1])}
+            del g
         if shard is not None:
             from .dist import shard_range
             rank, world = int(shard[0]), int(shard[1])
@@ -453,7 +466,12 @@ class PathCVTC:
                     raise ConfigError("shard bounds must be 0 = b_0 <= ... <= b_G = L")
                 off, cnt = b[rank], b[rank + 1] - b[rank]
             else:
+                b = None
                 off, cnt = shard_range(self.L, rank, world)
+            if route:
+                if b is None or any(x % 48 for x in b[:-1]):
+                    raise ConfigError("frame routing needs shard bounds at multiples of 48 (dist.tile_bounds)")
+                self._tile_bounds = [x // 48 for x in b[:-1]] + [(self.L + 47) // 48]
             if cnt < 1:
                 raise EmptyActiveSetError(f"landmark shard {rank} of {world} is empty (L = {self.L})")
             if self.screen == "f16x1":
@@ -773,6 +791,160 @@ class PathCVTC:
                                          out_map=perm0)
             owner = yield ("exchange", ds, dz, z_parts)
             out.update(ds=ds, dz=dz, owner=owner)
+        return out
+
+
+    # ------------------------------------------------------------ frame-routed landmark sharding
+
+    def evaluate_routed(self, frames, home_offset, t_total, grad=True, out_dtype=torch.float32, comm=None):
+        """Frame-routed landmark-sharded evaluate over a torch.distributed group: this
+        rank passes its HOME frames (global rows [home_offset, home_offset + len)) and
+        gets back their s, z and complete ds, dz (frame-sharded outputs)."""
+        from . import dist as Dd
+        return Dd.drive(self.routed_steps(frames, home_offset, t_total, grad, out_dtype), comm or Dd.DistComm())
+
+    def routed_steps(self, frames, home_offset, t_total, grad=True, out_dtype=torch.float32):
+        """Generator ("frame routing"): home phase -- one-term split of
+        the home frames and the coarse screen against the GLOBAL coarse landmarks, giving
+        each frame's admissible tile hull; ("alltoallv") every frame goes to the shards
+        whose tiles its hull meets; shard phase -- banded screen of the received frames
+        against the local landmarks, ("min") the global estimate minimum of every frame,
+        exact refits, K4 partials, ("gather") the per-frame partials of every shard, the
+        coefficient rescale and the gradient pass; ("alltoallv") each shard's rows of the
+        frames it holds a window of go back to their home rank, which sums them."""
+        from . import dist as Dd
+        if self._gprune is None:
+            raise ConfigError("routed_steps needs PathCVTC(..., shard=(rank, world, bounds), route=True)")
+        rank, world = self.shard[0], self.shard[1]
+        gp, dev, n = self._gprune, self.device, self.n
+        frh, fsh = self._frames(frames, 1, check=False)
+        Th = frh.shape[0]
+        # home phase: global coarse screen -> admissible global tile hulls
+        Dc = K.msd_estimate(fsh, gp["ls_coarse"], grid=K2_GRID)
+        hlo, hhi, _ = K.prune_plan(Dc, fsh.opnorm, gp["ls_coarse"].opnorm, self.kacc, gp["mind"],
+                                   (self.cutoff + 2.0) / self.lam, gp["knear"], maxd=gp["maxd"],
+                                   cstride=gp["cstride"], frnorm=fsh.rnorm, crnorm=gp["ls_coarse"].rnorm)
+        del Dc
+        tb = torch.tensor(self._tile_bounds, dtype=torch.int32, device=dev)
+        dest = (hlo[:, None] < tb[None, 1:]) & (hhi[:, None] > tb[None, :-1])  # [Th, G]
+        sends = [torch.nonzero(dest[:, r]).flatten() for r in range(world)]
+        gids = torch.arange(home_offset, home_offset + Th, dtype=torch.int64, device=dev)
+        if world == 1:  # nothing to route: the home frames are the received frames (no copies)
+            src_counts, gid, fr, hull = [Th], gids, frh, torch.stack([hlo, hhi], 1)
+        else:
+            got = yield ("alltoallv", [[gids[i] for i in sends], [frh[i] for i in sends],
+                                       [torch.stack([hlo[i], hhi[i]], 1) for i in sends]])
+            src_counts = [int(x.shape[0]) for x in got[0]]
+            gid = torch.cat(got[0])
+            fr = torch.cat(got[1]).contiguous()
+            hull = torch.cat(got[2])
+            del got
+        R = int(gid.numel())
+        t0, t1 = self._tile_bounds[rank], self._tile_bounds[rank + 1]
+        ntl = t1 - t0
+        one = self.screen == "f16x1"
+        big = torch.full((t_total,), float("inf"), dtype=torch.float32, device=dev)
+        if R:
+            if world == 1:
+                fr, fs0 = frh, fsh  # the home split is the received split
+            else:
+                fr, fs0 = self._frames(fr, 1, check=False)
+            lo = (hull[:, 0].clamp(min=t0) - t0).to(torch.int32)
+            hi = (hull[:, 1].clamp(max=t1) - t0).to(torch.int32)
+            wide = max(1, (3 * ntl) // 4)
+            key = torch.where(hi - lo >= wide, torch.zeros_like(lo), 1 + lo).to(torch.int32).contiguous()
+            perm0 = K.sort_by_key(key, ntl + 1)
+            p = perm0.long()
+            fs = K.gather_split(fs0, perm0)
+            tlist, nlist, rlo, rhi = K.band_tiles(perm0, lo.contiguous(), hi.contiguous(), 128, 48, self.L, ntl)
+            Dest = torch.empty((R, self.L), dtype=torch.float32, device=dev)
+            K.msd_estimate(fs, self.ls, Dest, grid=K2_GRID, tlist=tlist, nlist=nlist)
+            fnorm = self.frame_bound(fs) if one else None
+            fcoef = 2.0 * self.lam if one else 0.0
+            _, _, dmin, _ = K.candidates(Dest, self.lam, self.cutoff + self.margin, 1, fnorm=fnorm, fcoef=fcoef,
+                                         rlo=rlo, rhi=rhi)
+            big[gid[p]] = dmin
+        dglob = yield ("min", big)
+        s_loc = torch.zeros((t_total,), dtype=torch.float64, device=dev)
+        z_loc = torch.full((t_total,), float("inf"), dtype=torch.float64, device=dev)
+        cap = self.window_cap
+        while True:
+            status = torch.zeros(20, dtype=torch.float64, device=dev)
+            if R:
+                dref = dglob[gid[p]].contiguous()
+                lo_w, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap, fnorm=fnorm,
+                                                    fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
+                perm = K.sort_by_key((2 * lo_w + cnt).to(torch.int32), 2 * self.L + 1)
+                Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo_w, cnt=cnt, cap=cap,
+                                            fmap=perm0, wuni=self.wuni)
+                wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L,
+                                        rowlo=lo_w, rowcnt=cnt)
+                s_loc[gid[p]] = wres["s"]
+                z_loc[gid[p]] = wres["z"]
+                fflags = torch.cat([fs.flags, fs0.flags])
+                status = torch.stack([_flag_bits_dev(fflags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
+                                      _flag_bits_dev(wres["flags"])]).to(torch.float64).flatten()
+            parts = yield ("gather", torch.cat([s_loc, z_loc, status]))
+            bits = parts[:, 2 * t_total:].reshape(world, 4, -1) > 0
+            ff, cf, rf, wf = (_bits_value(b.tolist()) for b in bits.any(0).cpu())
+            if ff & FLAG_NON_FINITE:
+                raise InvalidStructureError("frame coordinates contain non-finite values")
+            if (cf & FLAG_SIG_OVERFLOW) and cap < self.L:
+                cap = min(self.L, 4 * cap)
+                continue
+            break
+        if rf & FLAG_NON_FINITE:
+            raise InvalidStructureError("path_cv refine: non-finite coordinates or distances")
+        if rf & FLAG_NO_CONVERGE:
+            raise MetadynError("path_cv refine: Jacobi diagonalisation did not converge")
+        if wf & FLAG_NON_FINITE:
+            raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        s_parts, z_parts = parts[:, :t_total], parts[:, t_total:2 * t_total]
+        s, z, alpha, beta = Dd.shard_coefficients(s_parts, z_parts, self.lam, rank)
+        sl = slice(home_offset, home_offset + Th)
+        out = {"s": s[sl].contiguous(), "z": z[sl].contiguous(), "received": R,
+               "window_cnt": cnt if R else torch.zeros(0, dtype=torch.int32, device=dev),
+               "nsig": wres["nsig"] if R else torch.zeros(0, dtype=torch.int32, device=dev)}
+        if not grad:
+            return out
+        odt = out_dtype
+        rows_s = rows_z = None
+        act_parts = [[] for _ in range(world)]
+        if R:
+            K.shard_rescale(wres, alpha[gid[p]].contiguous(), beta[gid[p]].contiguous(), cap)
+            gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
+            if world == 1:  # every home frame's rows are complete here: write the outputs directly
+                del Dest, Dex, Rex
+                ds, dz = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, odt,
+                                             out_map=perm0)
+                out.update(ds=ds, dz=dz)
+                return out
+            rows_s, rows_z = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, odt,
+                                                 out_map=perm0)
+            # rows of received frames with a window here, per source rank (position in its list)
+            cnt_recv = torch.empty_like(cnt)
+            cnt_recv[p] = cnt
+            act = cnt_recv > 0
+            o = 0
+            for r in range(world):
+                c = src_counts[r]
+                act_parts[r] = torch.nonzero(act[o:o + c]).flatten() + o
+                o += c
+        empty_rows = torch.empty((0, n, 3), dtype=odt, device=dev)
+        back = yield ("alltoallv", [
+            [(idx - sum(src_counts[:r])) for r, idx in enumerate(act_parts)] if R else
+            [torch.empty(0, dtype=torch.int64, device=dev)] * world,
+            [rows_s[idx] for idx in act_parts] if R else [empty_rows] * world,
+            [rows_z[idx] for idx in act_parts] if R else [empty_rows] * world])
+        ds = torch.zeros((Th, n, 3), dtype=odt, device=dev)
+        dz = torch.zeros((Th, n, 3), dtype=odt, device=dev)
+        for r in range(world):  # fixed source order: bitwise-reproducible sums
+            pos = back[0][r]
+            if pos.numel():
+                home_rows = sends[r][pos]
+                ds.index_add_(0, home_rows, back[1][r])
+                dz.index_add_(0, home_rows, back[2][r])
+        out.update(ds=ds, dz=dz)
         return out
 
 

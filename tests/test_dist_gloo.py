@@ -223,3 +223,39 @@ def test_balanced_bounds():
     assert b[0] == 0 and b[-1] == 64 and all(x < y for x, y in zip(b, b[1:]))
     assert sum(1 for x in b[1:-1] if 10 <= x <= 14) >= 2  # the hot region is split
     assert D.balanced_bounds(torch.zeros(4), 4) == [0, 1, 2, 3, 4]
+
+
+def _toy_alltoallv(rank, world):
+    """Variable-size all-to-all of two fields (int64 ids, float rows)."""
+    def steps(r):
+        ids = [torch.arange(r * 10 + d, r * 10 + d + d + r, dtype=torch.int64) for d in range(world)]
+        rows = [torch.full((int(i.numel()), 2, 3), float(r * 100 + d)) for d, i in enumerate(ids)]
+        got = yield ("alltoallv", [ids, rows])
+        return {"ids": torch.cat(got[0]), "rows": torch.cat(got[1])}
+    out = D.drive(steps(rank), D.DistComm())
+    return {k: v.numpy() for k, v in out.items()}
+
+
+def test_alltoallv_dist_equals_lockstep():
+    out = _spawn(_toy_alltoallv)
+
+    def steps(r, world=2):
+        ids = [torch.arange(r * 10 + d, r * 10 + d + d + r, dtype=torch.int64) for d in range(world)]
+        rows = [torch.full((int(i.numel()), 2, 3), float(r * 100 + d)) for d, i in enumerate(ids)]
+        got = yield ("alltoallv", [ids, rows])
+        return {"ids": torch.cat(got[0]), "rows": torch.cat(got[1])}
+
+    loc = D.drive_lockstep([steps(0), steps(1)])
+    for r in (0, 1):
+        assert np.array_equal(loc[r]["ids"].numpy(), out[r]["ids"])
+        assert np.array_equal(loc[r]["rows"].numpy(), out[r]["rows"])
+    # rank 1 receives rank 0's block for destination 1 ([1]) then its own ([11, 12])
+    assert out[1]["ids"].tolist() == [1, 11, 12]
+
+
+def test_tile_bounds():
+    assert D.tile_bounds(1536, 1) == [0, 1536]
+    b = D.tile_bounds(1536, 3)
+    assert b == [0, 528, 1056, 1536] or all(x % 48 == 0 for x in b[:-1])
+    b = D.tile_bounds(1000, 4)
+    assert b[0] == 0 and b[-1] == 1000 and all(x % 48 == 0 for x in b[:-1])

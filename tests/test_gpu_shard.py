@@ -139,3 +139,36 @@ def test_landmark_sharded_through_nccl_one_rank(cuda_device):
     np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"].cpu().numpy(), rtol=1e-12)
     assert bool((out["owner"] == 0).all())
     _rows_close(out["ds"].cpu().numpy(), ref["ds"].cpu().numpy(), 1e-12)
+
+
+def _routed(wl, G, bounds, **kw):
+    T = wl.frames.shape[0]
+    engs = [engine.PathCVTC(wl.landmarks, wl.lam, shard=(g, G, bounds), route=True, **kw) for g in range(G)]
+    gens = []
+    for g, e in enumerate(engs):
+        off, cnt = D.shard_range(T, g, G)
+        gens.append(e.routed_steps(wl.frames[off:off + cnt], off, T, out_dtype=torch.float64))
+    return engs, D.drive_lockstep(gens)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_frame_routed_landmark_shards_match_unsharded(G, cuda_device):
+    """Frame-routed landmark sharding: every rank screens only its home frames against the
+    global coarse landmarks, frames travel to the shards their admissible tiles live on,
+    gradient rows come back home.  The concatenated home outputs equal the unsharded
+    evaluate (s, z to 1e-9; ds, dz to 1e-7 of the per-frame maximum)."""
+    wl = synth.config4(T=260, L=1536, N=240)
+    ref = engine.PathCVTC(wl.landmarks, wl.lam).evaluate(wl.frames, out_dtype=torch.float64)
+    b = D.tile_bounds(1536, G)
+    assert all(x % 48 == 0 for x in b[:-1])
+    engs, outs = _routed(wl, G, b)
+    s = torch.cat([o["s"] for o in outs]).cpu().numpy()
+    z = torch.cat([o["z"] for o in outs]).cpu().numpy()
+    np.testing.assert_allclose(s, ref["s"].cpu().numpy(), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(z, ref["z"].cpu().numpy(), rtol=1e-9, atol=1e-12)
+    for key in ("ds", "dz"):
+        got = torch.cat([o[key] for o in outs]).cpu().numpy()
+        _rows_close(got, ref[key].cpu().numpy(), 1e-7)
+    received = [o["received"] for o in outs]
+    if G > 1:  # frames travel only where their hulls are: far fewer than G x T copies
+        assert sum(received) < 1.6 * 260, received
