@@ -265,6 +265,10 @@ class Config3:
         T, n, L = self.T, self.n, self.L
         if name == "mc_cov_f64":
             return "fp64_flop", 18.0 * n * T * L
+        if name == "mc_cov_dmma":  # dense S [T, L, 9]: 9 fp64 FMA per atom and pair on DMMA
+            return "fp64_tensor_flop", 18.0 * n * T * L
+        if name == "mc_pathcv_grad_block" and self.last is not None:
+            return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_fit_dense":
             return "bytes", T * L * (72 + 8 + 72 + 1)
         return "bytes", 0.0
