@@ -908,8 +908,9 @@ class PathCVTC:
         if not grad:
             return out
         odt = out_dtype
-        rows_s = rows_z = None
-        act_parts = [[] for _ in range(world)]
+        i64 = torch.empty(0, dtype=torch.int64, device=dev)
+        pos_back = [i64] * world  # per source rank: positions (in its list) of frames with a window here
+        rows_back = [[torch.empty((0, n, 3), dtype=odt, device=dev)] * world for _ in range(2)]
         if R:
             K.shard_rescale(wres, alpha[gid[p]].contiguous(), beta[gid[p]].contiguous(), cap)
             gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
@@ -921,21 +922,16 @@ class PathCVTC:
                 return out
             rows_s, rows_z = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, odt,
                                                  out_map=perm0)
-            # rows of received frames with a window here, per source rank (position in its list)
             cnt_recv = torch.empty_like(cnt)
-            cnt_recv[p] = cnt
-            act = cnt_recv > 0
+            cnt_recv[p] = cnt  # window count of every received frame, in received order
             o = 0
             for r in range(world):
                 c = src_counts[r]
-                act_parts[r] = torch.nonzero(act[o:o + c]).flatten() + o
+                pos = torch.nonzero(cnt_recv[o:o + c] > 0).flatten()
+                pos_back[r] = pos
+                rows_back[0][r], rows_back[1][r] = rows_s[o + pos], rows_z[o + pos]
                 o += c
-        empty_rows = torch.empty((0, n, 3), dtype=odt, device=dev)
-        back = yield ("alltoallv", [
-            [(idx - sum(src_counts[:r])) for r, idx in enumerate(act_parts)] if R else
-            [torch.empty(0, dtype=torch.int64, device=dev)] * world,
-            [rows_s[idx] for idx in act_parts] if R else [empty_rows] * world,
-            [rows_z[idx] for idx in act_parts] if R else [empty_rows] * world])
+        back = yield ("alltoallv", [pos_back, rows_back[0], rows_back[1]])
         ds = torch.zeros((Th, n, 3), dtype=odt, device=dev)
         dz = torch.zeros((Th, n, 3), dtype=odt, device=dev)
         for r in range(world):  # fixed source order: bitwise-reproducible sums
