@@ -82,6 +82,9 @@ def test_counter_identities_and_eps_zero(refs, cuda_device):
     assert rep.expensive_count == steps + rep.reassign_count * L
     assert rep.cheap_count == (steps - rep.reassign_count) * L
     assert 1 < rep.reassign_count < steps and rep.measured_K == steps / rep.reassign_count
+    from paper_1801_02362_b200 import perf
+
+    assert perf.measured_vs_model(rep, N=L)["difference"] == 0.0
     r0 = run(sysm, refs, mode="close", n_steps=steps, eps=0.0)
     ro = run(sysm, refs, mode="original", n_steps=steps)
     assert r0.reassign_count == steps and ro.expensive_count == steps * L
