@@ -189,8 +189,8 @@ class Config01:
     def kernel_work(self, name):
         T, n, L = self.T, self.n, self.L
         npad = ((n + 31) // 32) * 32
-        if name == "mc_cov_f64":
-            return "fp64_flop", 18.0 * n * T * L
+        if name == "mc_cov_f64":  # on DMMA (cov_dmma_f64_kernel) unless MC_COV_F64=1
+            return ("fp64_flop" if os.environ.get("MC_COV_F64") == "1" else "fp64_tensor_flop"), 18.0 * n * T * L
         if name == "mc_fit_dense":
             return "bytes", T * L * (72 + 8 + 72 + 1)
         if name == "mc_pathcv_weights":

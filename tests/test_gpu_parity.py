@@ -278,3 +278,22 @@ def test_cuda_graph_replay_equals_eager(cuda_device):
     g.evaluate(bad)
     with pytest.raises(InvalidStructureError):
         g.check()
+
+
+@pytest.mark.parametrize("T,L,n", [(70, 45, 50), (33, 97, 304), (5, 3, 22)])
+def test_cov_f64_dmma_vs_numpy(T, L, n, cuda_device):
+    """fp64-plane covariance on the fp64 tensor cores (cov_dmma_f64_kernel, the default for
+    fp64 inputs) = the fp64 numpy contraction of the same planes, to fp64 rounding; ragged
+    T, L (not multiples of the 32 x 32 tile) and padded atom counts."""
+    rng = np.random.default_rng(T + L + n)
+    x = torch.from_numpy(rng.normal(0, 0.5, size=(T, n, 3))).to(cuda_device)
+    a = torch.from_numpy(rng.normal(0, 0.5, size=(L, n, 3))).to(cuda_device)
+    w = torch.from_numpy(rng.uniform(0.5, 1.5, size=n) / n).to(cuda_device)
+    wp = torch.zeros(K.npad_for(n), dtype=torch.float64, device=cuda_device)
+    wp[:n] = w
+    fx = K.center(x, wp, wp)
+    fa = K.center(a, wp, wp, weighted=True)
+    S = K.cov_dense(fx, fa).cpu().numpy()
+    xp, ap = fx.planes.cpu().numpy(), fa.wplanes.cpu().numpy()
+    ref = np.einsum("tbj,lgj->tlbg", xp, ap).reshape(T, L, 9)
+    assert np.abs(S - ref).max() <= 1e-13 * np.abs(ref).max()
