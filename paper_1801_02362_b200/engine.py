@@ -530,6 +530,23 @@ class PathCVTC:
         if self.prune:
             self._init_prune(int(coarse_stride), int(knear))
 
+    def _exact_windows(self, Dest, fr, fs, cap, rlo=None, rhi=None, perm0=None, dref=None):
+        """Screen estimate -> per-frame windows (mc_candidates, against dref when sharded)
+        -> frames sorted by window centre (32-frame refit unions stay tight) -> exact fp64
+        refits of the window pairs (DMMA) -> K4 weights.  Shared by evaluate() and the
+        two landmark-sharded generators.  Returns (lo, cnt, wres, cflags, rflags)."""
+        one = self.screen == "f16x1"
+        lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
+                                          fnorm=self.frame_bound(fs) if one else None,
+                                          fcoef=2.0 * self.lam if one else 0.0, rlo=rlo, rhi=rhi, dref=dref)
+        perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
+        Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
+                                    fmap=perm0, wuni=self.wuni)
+        wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
+                                rowcnt=cnt)
+        wres["D_window"] = Dex
+        return lo, cnt, wres, cflags, rflags
+
     def frame_bound(self, fs):
         """max_l e_tl: the one-term estimate error bound of frame t against any landmark
         (the per-pair bound with the landmark norms at their maxima)."""
@@ -621,21 +638,12 @@ class PathCVTC:
             Dest, fr, fs, fs0, rlo, rhi, perm0 = self._pruned_estimate(frames)
         else:
             Dest, fr, fs = self.estimate(frames, self.screen_terms, check=False)
-        one = self.screen == "f16x1"
         cap = self.window_cap
         while True:
             # the whole pipeline is enqueued without host round trips; the status
             # flags of every stage are reduced on the device and read once at the end
-            lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap,
-                                              fnorm=self.frame_bound(fs) if one else None,
-                                              fcoef=2.0 * self.lam if one else 0.0,
-                                              rlo=rlo, rhi=rhi)
-            # refine groups: frames sorted by window centre (32-frame unions stay tight)
-            perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
-            Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
-                                        fmap=perm0, wuni=self.wuni)
-            wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
-                                    rowcnt=cnt)
+            lo, cnt, wres, cflags, rflags = self._exact_windows(Dest, fr, fs, cap, rlo, rhi, perm0)
+            Dex = wres["D_window"]
             out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
                    "nsig": wres["nsig"]}
             if grad:
@@ -746,13 +754,7 @@ class PathCVTC:
             dref = dref[p].contiguous()
         cap = self.window_cap
         while True:
-            lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap, fnorm=fnorm,
-                                              fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
-            perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
-            Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
-                                        fmap=perm0, wuni=self.wuni)
-            wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
-                                    rowcnt=cnt)
+            _, cnt, wres, cflags, rflags = self._exact_windows(Dest, fr, fs, cap, rlo, rhi, perm0, dref)
             sl, zl = wres["s"], wres["z"]
             if p is not None:
                 sl, zl = torch.empty_like(sl), torch.empty_like(zl)
@@ -872,13 +874,7 @@ class PathCVTC:
             status = torch.zeros(20, dtype=torch.float64, device=dev)
             if R:
                 dref = dglob[gid[p]].contiguous()
-                lo_w, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, cap, fnorm=fnorm,
-                                                    fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
-                perm = K.sort_by_key((2 * lo_w + cnt).to(torch.int32), 2 * self.L + 1)
-                Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo_w, cnt=cnt, cap=cap,
-                                            fmap=perm0, wuni=self.wuni)
-                wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L,
-                                        rowlo=lo_w, rowcnt=cnt)
+                _, cnt, wres, cflags, rflags = self._exact_windows(Dest, fr, fs, cap, rlo, rhi, perm0, dref)
                 s_loc[gid[p]] = wres["s"]
                 z_loc[gid[p]] = wres["z"]
                 fflags = torch.cat([fs.flags, fs0.flags])
@@ -915,7 +911,8 @@ class PathCVTC:
             K.shard_rescale(wres, alpha[gid[p]].contiguous(), beta[gid[p]].contiguous(), cap)
             gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
             if world == 1:  # every home frame's rows are complete here: write the outputs directly
-                del Dest, Dex, Rex
+                del Dest
+                wres.pop("D_window", None)  # free the window refits before the gradient outputs
                 ds, dz = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, odt,
                                              out_map=perm0)
                 out.update(ds=ds, dz=dz)
