@@ -5,12 +5,21 @@
 // refresh), so the device work is split into:
 //   1. a speculative window: D(x_s, x_{s-k}) for k = 1..K for every frame
 //      in parallel (cov_pairs + Newton; fp64, so |dD| ~ 1e-16),
-//   2. this scan kernel: one CTA per walker walks its frames in order,
-//      reading the window from shared memory; only when the close structure
-//      is older than K frames does the whole CTA compute the fit on the fly,
+//   2. this scan kernel, one CTA per walker.  First a parallel pass: the next
+//      refresh after a refresh at r is next(r) = the first s in (r, r + K] with
+//      D(x_s, x_r) > eps (from the window), so the refresh chain 0 -> next(0) ->
+//      ... is a linked list; pointer doubling in shared memory marks every node
+//      of the chain from frame 0 in log2(steps) rounds, and a prefix-max scan
+//      gives every frame its close structure.  Only if the chain reaches a
+//      refresh whose successor lies beyond the window (or the walker is too long
+//      for shared memory) does the CTA fall back to walking its frames in order,
+//      computing the fit on the fly when the close structure is older than K,
 //   3. xy_eig_kernel: the full x<->y spectrum (reference Jacobi) of every
 //      non-refresh frame, which Eq. 6's dR_xy/dx term needs.
 // Strict '>' and first-frame refresh follow SPEC.md:159,162.
+#include <algorithm>
+#include <cstdlib>
+
 #include "mc_math.cuh"
 
 namespace mc {
@@ -25,12 +34,73 @@ __global__ void __launch_bounds__(SCAN_NT)
 close_scan_kernel(const double* __restrict__ fpl, const double* __restrict__ gx, int steps, int npad,
                   const double* __restrict__ w, const double* __restrict__ dwin, int K, double eps,
                   uint8_t* __restrict__ refresh, int* __restrict__ ridx, double* __restrict__ dxy,
-                  int* __restrict__ n_onthefly) {
-  extern __shared__ double sw[];  // [SCAN_CHUNK * K]
+                  int* __restrict__ n_onthefly, int par) {
+  extern __shared__ double sw[];  // [SCAN_CHUNK * K] (serial) or the chain arrays (parallel)
   __shared__ double scratch[SCAN_NT / 32];
   __shared__ int s_r, s_pos, s_miss;
+  __shared__ int s_seg[SCAN_NT];
   const int walker = blockIdx.x;
   const int64_t base = (int64_t)walker * steps;
+  const int tid = threadIdx.x;
+  if (par) {
+    // ---- parallel pass: J = next-refresh pointers, M = chain marks (shared memory)
+    int* J = reinterpret_cast<int*>(sw);
+    int* J2 = J + steps;
+    uint8_t* M = reinterpret_cast<uint8_t*>(J2 + steps);
+    constexpr int END = 0x7fffffff, UNK = -1;
+    auto next_of = [&](int r) {
+      for (int k = 1; k <= K; ++k) {
+        const int s = r + k;
+        if (s >= steps) return END;
+        if (dwin[(base + s) * K + (k - 1)] > eps) return s;
+      }
+      return r + K + 1 >= steps ? END : UNK;
+    };
+    for (int r = tid; r < steps; r += SCAN_NT) {
+      J[r] = next_of(r);
+      M[r] = r == 0;
+    }
+    __syncthreads();
+    for (int span = 1; span < steps; span <<= 1) {
+      for (int r = tid; r < steps; r += SCAN_NT) {
+        const int j = J[r];
+        if (M[r] && j >= 0 && j != END) M[j] = 1;
+      }
+      __syncthreads();
+      for (int r = tid; r < steps; r += SCAN_NT) {
+        const int j = J[r];
+        J2[r] = (j >= 0 && j != END) ? J[j] : j;
+      }
+      __syncthreads();
+      int* t = J;
+      J = J2;
+      J2 = t;
+    }
+    // a marked refresh whose successor is beyond the window: the chain is unresolved
+    int miss = 0;
+    for (int r = tid; r < steps; r += SCAN_NT) miss |= (M[r] && next_of(r) == UNK);
+    if (!__syncthreads_or(miss)) {
+      // prefix max of the marked positions: each frame's close structure
+      const int per = (steps + SCAN_NT - 1) / SCAN_NT, s0 = tid * per, s1 = min(steps, s0 + per);
+      int m = -1;
+      for (int t = s0; t < s1; ++t) if (M[t]) m = t;
+      s_seg[tid] = m;
+      __syncthreads();
+      int run = -1;
+      for (int i = 0; i < tid; ++i) run = max(run, s_seg[i]);
+      for (int t = s0; t < s1; ++t) {
+        const int prev = run;  // last refresh before t
+        if (M[t]) run = t;
+        refresh[base + t] = M[t];
+        ridx[base + t] = (int)(base + run);
+        // D(x_t, y) with y the close structure t was tested against (0 for frame 0)
+        dxy[base + t] = t == 0 ? 0.0 : dwin[(base + t) * K + (t - prev - 1)];
+      }
+      if (tid == 0 && n_onthefly) n_onthefly[walker] = 0;
+      return;
+    }
+    __syncthreads();  // fall through to the serial walk (its staging reuses sw)
+  }
   if (threadIdx.x == 0) { s_r = -1; s_pos = 0; }
   int fly = 0;
   for (int c0 = 0; c0 < steps; c0 += SCAN_CHUNK) {
@@ -104,13 +174,16 @@ cudaError_t launch_close_scan(const double* fpl, const double* gx, int walkers, 
                               const double* w, const double* dwin, int K, double eps, uint8_t* refresh,
                               int* ridx, double* dxy, int* n_onthefly, cudaStream_t stream) {
   if (walkers <= 0 || steps <= 0) return cudaSuccess;
-  const size_t smem = (size_t)SCAN_CHUNK * K * sizeof(double);
+  const size_t serial = (size_t)SCAN_CHUNK * K * sizeof(double);
+  const size_t chain = (size_t)steps * 9;  // two int pointer arrays + the marks
+  const bool par = chain <= 200 * 1024 && getenv("MC_CLOSE_SCAN_SERIAL") == nullptr;
+  const size_t smem = std::max(serial, par ? (chain + 15) / 16 * 16 : (size_t)0);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(close_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   close_scan_kernel<<<walkers, SCAN_NT, smem, stream>>>(fpl, gx, steps, npad, w, dwin, K, eps, refresh, ridx, dxy,
-                                                        n_onthefly);
+                                                        n_onthefly, par ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -297,3 +297,34 @@ def test_cov_f64_dmma_vs_numpy(T, L, n, cuda_device):
     xp, ap = fx.planes.cpu().numpy(), fa.wplanes.cpu().numpy()
     ref = np.einsum("tbj,lgj->tlbg", xp, ap).reshape(T, L, 9)
     assert np.abs(S - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("factor", [0.5, 4.0, 30.0])
+def test_close_scan_parallel_chain_equals_serial_walk(factor, cuda_device):
+    """The pointer-doubling refresh chain (parallel pass of close_scan_kernel) gives the
+    serial walk's refresh log, close-structure indices and D(x, y) exactly -- frequent
+    refreshes (chain resolved in parallel) and rare ones (successor beyond the window:
+    serial fallback with on-the-fly fits)."""
+    import os
+
+    rng = np.random.default_rng(int(factor * 10))
+    wl = synth.config0(seed=9, T=4, L=12, N=16)
+    steps = 300
+    x = np.cumsum(rng.normal(0, 0.002, size=(steps, 16, 3)), axis=0) + wl.landmarks[3][None]
+    frames = torch.from_numpy(x).to(cuda_device)
+    pcv = engine.PathCV(torch.from_numpy(wl.landmarks).to(cuda_device), wl.lam)
+    # eps = factor x the one-step MSD: refreshes every frame (0.5), every few frames (4,
+    # inside the 8-frame window: resolved in parallel), or rarely (30: successors beyond
+    # the window -> serial walk with on-the-fly fits)
+    eps = factor * float(np.mean(np.sum((x[1:] - x[:-1]) ** 2, axis=(1, 2)) / 16))
+    par = pcv.close_replay(frames, eps, grad=False)
+    os.environ["MC_CLOSE_SCAN_SERIAL"] = "1"
+    try:
+        ser = pcv.close_replay(frames, eps, grad=False)
+    finally:
+        del os.environ["MC_CLOSE_SCAN_SERIAL"]
+    for key in ("refresh", "dxy", "s", "z"):
+        assert torch.equal(par[key], ser[key]), key
+    n = int(par["refresh"].sum())
+    print(f"eps = {factor} x step MSD: {n} refreshes in {steps}")
+    assert (n > 0.9 * steps) if factor < 1 else (1 < n < steps)
