@@ -378,7 +378,7 @@ class ConfigTC:
         from paper_1801_02362_b200 import kernels as K
 
         fr, fs = self.pcv._frames(frames)
-        K.refine(fr, fs, self.pcv.lraw, self.pcv.ls, self.pcv.w, Dd=D)
+        K.refine(fr, fs, self.pcv.lraw, self.pcv.ls, self.pcv.w, Dd=D, wuni=self.pcv.wuni)
         return D
 
     def step_device(self):
@@ -394,6 +394,17 @@ class ConfigTC:
         the pruning bands and frame groups to stay tight (sweeps:
         tools/_diag/e2e_sched.py, tools/_diag/e2e_timeline.py)."""
         env = os.environ.get("MC_E2E_CHUNKS")  # "first,steady[,growth[,taper]]" | "list:n1,n2,..." (knob)
+        if not env and self.cfg == 2:
+            # config 2 is compute-bound (12 KB in, 16 KB out per frame): few large chunks,
+            # small first / last ones (tools/_diag/e2e_c2.sh: 188.8 -> 182.4 ms)
+            e = max(32, (self.T // 32) // 32 * 32)
+            mid = (self.T - 2 * e) // 2
+            sizes = [e, mid, self.T - 2 * e - mid, e] if self.T > 4 * e else [self.T]
+            out, c0 = [], 0
+            for n in sizes:
+                out.append((c0, n))
+                c0 += n
+            return out
         if not env:
             div = int(os.environ.get("MC_E2E_TAIL", "16"))  # last chunk = T / div (sweep knob)
             tail = [max(1024, (self.T // div) // 32 * 32)]
@@ -477,8 +488,22 @@ class ConfigTC:
             comp.wait_event(ev)
             fr.record_stream(comp)
             if self.cfg == 2:
+                # the [n, L] result goes back on its own stream into pinned memory, so the
+                # D2H of chunk i overlaps the compute of chunk i + 1 (full-duplex PCIe)
+                if not hasattr(self, "_d2h_stream"):
+                    self._d2h_stream = torch.cuda.Stream(device=self.device)
+                    self._d_host = torch.empty((self.T, self.L), dtype=torch.float32).pin_memory()
                 D = self._step(fr)
-                outs.append(D.to("cpu", non_blocking=True))
+                done = torch.cuda.Event()
+                done.record(comp)
+                c0, n = chunks[i]
+                with torch.cuda.stream(self._d2h_stream):
+                    self._d2h_stream.wait_event(done)
+                    D.record_stream(self._d2h_stream)
+                    self._d_host[c0:c0 + n].copy_(D, non_blocking=True)
+                if i + 1 == len(chunks):
+                    comp.wait_stream(self._d2h_stream)
+                    outs.append(self._d_host)
             else:
                 self._c0 = chunks[i][0]  # home offset of this chunk (frame-routed landmark shards)
                 o = self._step(fr)
