@@ -19,6 +19,7 @@
 // Landmarks with lam (D_i - D_min) > cutoff (default 50) contribute
 // < e^-50 relative to the leading term and are skipped.
 #include <algorithm>
+#include <cstdlib>
 
 #include "mc_math.cuh"
 
@@ -378,6 +379,208 @@ cv_weights_warp_kernel(int T, int t0, double lam, double cutoff, int cap, int ld
   }
 }
 
+// Warp-per-frame form of cv_weights_kernel for close-structure rows (refresh != NULL,
+// no neighbour list): the same three passes (Eq. 5 distances of non-refresh rows and
+// their minimum, the partition function, the ordered significant list with the
+// per-frame sums and the Eq. 6 M-matrix terms), with warp shuffles instead of block
+// reductions -- one frame per warp, 8 frames per CTA.  Same values as the block kernel
+// up to the summation order.
+__global__ void __launch_bounds__(WWPB * 32)
+cv_weights_close_warp_kernel(int T, int t0, double lam, double cutoff, int cap, int ld,
+                             const int* __restrict__ rowlo, const int* __restrict__ rowcnt, int L,
+                             double* __restrict__ D, const double* __restrict__ q, const double* __restrict__ R,
+                             const double* __restrict__ fwbar, const double* __restrict__ lwbar,
+                             const uint8_t* __restrict__ refresh, const int* __restrict__ ridx,
+                             const double* __restrict__ S, const double* __restrict__ rxy,
+                             const double* __restrict__ xyeig, const double* __restrict__ gx,
+                             const double* __restrict__ ga, const double* __restrict__ lmom,
+                             double* __restrict__ s_out, double* __restrict__ z_out, int* __restrict__ sig_idx,
+                             double* __restrict__ sig_coef, int* __restrict__ nsig, double* __restrict__ fvec,
+                             uint8_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int tl = blockIdx.x * WWPB + (threadIdx.x >> 5);
+  if (tl >= T) return;
+  const int t = t0 + tl;
+  const bool approx = !refresh[t];
+  const int r = approx ? ridx[t] : t;
+  double Rxy[9];
+  if (approx) {
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Rxy[e] = rxy[(int64_t)t * 9 + e];
+  }
+  double* Dt = D + (int64_t)t * ld;
+  const int nrow = rowcnt ? rowcnt[t] : L;
+  const int off = rowlo ? rowlo[t] : 0;
+  double dmin = INFINITY;
+  bool finite = true;
+  for (int i = lane; i < nrow; i += 32) {
+    double d;
+    if (approx) {
+      const double* Ri = R + ((int64_t)r * ld + i) * 9;
+      const double* Si = S + ((int64_t)t * ld + i) * 9;
+      double Rr[9], Rh[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) Rr[e] = Ri[e];
+      mat3_mul(Rxy, Rr, Rh);
+      double dot = 0.0;
+#pragma unroll
+      for (int e = 0; e < 9; ++e) dot = fma(Rh[e], Si[e], dot);
+      d = gx[t] + ga[i] - 2.0 * dot;
+      Dt[i] = d;
+    } else {
+      d = Dt[i];
+    }
+    finite = finite && isfinite(d);
+    dmin = fmin(dmin, d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+  const bool nonfinite = __any_sync(0xffffffffu, !finite);
+  double zs = 0.0, qs = 0.0;
+  for (int i = lane; i < nrow; i += 32) {
+    const double e = exp(-lam * (Dt[i] - dmin));
+    zs += e;
+    qs += q[off + i] * e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    zs += __shfl_xor_sync(0xffffffffu, zs, o);
+    qs += __shfl_xor_sync(0xffffffffu, qs, o);
+  }
+  const double sval = qs / zs;
+  const double zval = dmin - log(zs) / lam;
+  double acc[44];
+#pragma unroll
+  for (int e = 0; e < 44; ++e) acc[e] = 0.0;
+  int total = 0;
+  for (int b0 = 0; b0 < nrow; b0 += 32) {
+    const int i = b0 + lane;
+    const double di = i < nrow ? Dt[i] : 0.0;
+    const bool sig = i < nrow && lam * (di - dmin) <= cutoff;
+    const unsigned bal = __ballot_sync(0xffffffffu, sig);
+    if (sig) {
+      const int pos = total + __popc(bal & ((1u << lane) - 1u));
+      const double p = exp(-lam * (di - dmin)) / zs;
+      const int li = off + i;
+      const double cs = -lam * p * (q[li] - sval);
+      const double cz = p;
+      double Rh[9], Rr[9];
+      if (approx) {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Rr[e] = R[((int64_t)r * ld + i) * 9 + e];
+        mat3_mul(Rxy, Rr, Rh);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Rh[e] = R[((int64_t)t * ld + i) * 9 + e];
+      }
+      if (pos < cap) {
+        sig_idx[(int64_t)tl * cap + pos] = li;
+        double* co = sig_coef + ((int64_t)tl * cap + pos) * 18;
+#pragma unroll
+        for (int e = 0; e < 9; ++e) { co[e] = cs * Rh[e]; co[9 + e] = cz * Rh[e]; }
+      }
+      acc[0] += cs;
+      acc[1] += cz;
+      const double wb0 = lwbar[3 * li], wb1 = lwbar[3 * li + 1], wb2 = lwbar[3 * li + 2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double rw = Rh[a * 3] * wb0 + Rh[a * 3 + 1] * wb1 + Rh[a * 3 + 2] * wb2;
+        acc[2 + a] += cs * rw;
+        acc[5 + a] += cz * rw;
+      }
+      if (approx) {
+        const double* Si = S + ((int64_t)t * ld + i) * 9;
+        const double* m = lmom + 6 * (int64_t)li;
+        const double A[9] = {m[0], m[1], m[2], m[1], m[3], m[4], m[2], m[4], m[5]};
+        double SRt[9], RA[9], RAR[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            SRt[a * 3 + b] = Si[a * 3] * Rr[b * 3] + Si[a * 3 + 1] * Rr[b * 3 + 1] + Si[a * 3 + 2] * Rr[b * 3 + 2];
+        mat3_mul(Rr, A, RA);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            RAR[a * 3 + b] = RA[a * 3] * Rr[b * 3] + RA[a * 3 + 1] * Rr[b * 3 + 1] + RA[a * 3 + 2] * Rr[b * 3 + 2];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          acc[8 + e] += cs * SRt[e];
+          acc[17 + e] += cz * SRt[e];
+          acc[26 + e] += cs * RAR[e];
+          acc[35 + e] += cz * RAR[e];
+        }
+      }
+    }
+    total += __popc(bal);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  if (approx) {  // warp-uniform
+#pragma unroll
+    for (int e = 8; e < 44; ++e)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  }
+  if (lane != 0) return;
+  s_out[t] = sval;
+  z_out[t] = zval;
+  nsig[tl] = min(total, cap);
+  double* fv = fvec + (int64_t)tl * FVEC;
+  const double fw[3] = {fwbar[3 * t], fwbar[3 * t + 1], fwbar[3 * t + 2]};
+  double corr[2][3], vv[2][4];
+  for (int c = 0; c < 2; ++c) {
+    const double sumc = acc[c];
+    for (int a = 0; a < 3; ++a) corr[c][a] = 2.0 * (sumc * fw[a] - acc[2 + 3 * c + a]);
+    vv[c][0] = vv[c][1] = vv[c][2] = vv[c][3] = 0.0;
+  }
+  if (approx) {
+    const double* e = xyeig + (int64_t)t * 20;
+    double q0[4], qm[3][4], inv[3];
+    for (int rr = 0; rr < 4; ++rr) q0[rr] = e[4 + rr * 4];
+    for (int m = 0; m < 3; ++m) {
+      for (int rr = 0; rr < 4; ++rr) qm[m][rr] = e[4 + rr * 4 + m + 1];
+      inv[m] = 1.0 / (e[0] - e[m + 1]);
+    }
+    double J[4][9];
+    rot_quat_jacobian(q0, J);
+    const double yw[3] = {fwbar[3 * r], fwbar[3 * r + 1], fwbar[3 * r + 2]};
+    for (int c = 0; c < 2; ++c) {
+      const double* SR = acc + 8 + 9 * c;
+      const double* RAR = acc + 26 + 9 * c;
+      double XR[9], M[9];
+      mat3_mul(Rxy, RAR, XR);
+      for (int k = 0; k < 9; ++k) M[k] = -2.0 * (SR[k] - XR[k]);
+      double g[4];
+      for (int cc = 0; cc < 4; ++cc) {
+        double sacc = 0.0;
+        for (int k = 0; k < 9; ++k) sacc += M[k] * J[cc][k];
+        g[cc] = sacc;
+      }
+      for (int m = 0; m < 3; ++m) {
+        const double h = (qm[m][0] * g[0] + qm[m][1] * g[1] + qm[m][2] * g[2] + qm[m][3] * g[3]) * inv[m];
+        for (int rr = 0; rr < 4; ++rr) vv[c][rr] += h * qm[m][rr];
+      }
+      double dsum[3];
+      dk_contract(vv[c], q0, 1.0, fw, yw, dsum);
+      for (int a = 0; a < 3; ++a) corr[c][a] += dsum[a];
+    }
+  }
+  fv[0] = acc[0];
+  fv[1] = acc[1];
+  for (int a = 0; a < 3; ++a) { fv[2 + a] = corr[0][a]; fv[5 + a] = corr[1][a]; }
+  for (int rr = 0; rr < 4; ++rr) { fv[8 + rr] = vv[0][rr]; fv[12 + rr] = vv[1][rr]; }
+  if (flags) {
+    uint8_t f = 0;
+    if (total > cap) f |= kFlagSigOverflow;
+    if (nonfinite || !isfinite(sval) || !isfinite(zval)) f |= kFlagNonFinite;
+    flags[tl] = f;
+  }
+}
+
 cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, int cap, int ld, const int* rowlo,
                               const int* rowcnt, double* D, const double* q,
                               const double* R, const double* fwbar, const double* lwbar, const uint8_t* refresh,
@@ -389,6 +592,12 @@ cudaError_t launch_cv_weights(int T, int t0, int L, double lam, double cutoff, i
   if (!refresh && !nb_idx && dmode == 0 && rowlo && rowcnt) {
     cv_weights_warp_kernel<<<(T + WWPB - 1) / WWPB, WWPB * 32, 0, stream>>>(
         T, t0, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, s, z, sig_idx, sig_coef, nsig, fvec, flags);
+    return cudaGetLastError();
+  }
+  if (refresh && !nb_idx && dmode == 0 && getenv("MC_WEIGHTS_BLOCK") == nullptr) {
+    cv_weights_close_warp_kernel<<<(T + WWPB - 1) / WWPB, WWPB * 32, 0, stream>>>(
+        T, t0, lam, cutoff, cap, ld, rowlo, rowcnt, L, D, q, R, fwbar, lwbar, refresh, ridx, S, rxy, xyeig, gx, ga,
+        lmom, s, z, sig_idx, sig_coef, nsig, fvec, flags);
     return cudaGetLastError();
   }
   cv_weights_kernel<<<T, WNT, 0, stream>>>(T, t0, L, lam, cutoff, cap, ld, NbArgs{nb_idx, nb_row, nb_m, dmode}, rowlo,
