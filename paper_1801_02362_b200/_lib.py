@@ -87,6 +87,9 @@ _SIGS = {
     "mc_pair_grad": [_I64, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],
+    "mc_ldig_prep": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "mc_pathcv_grad_i8": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P,
+                          _P, _P, _I32, _I32, _P, _P],
 }
 
 # optional entry points (none at present)

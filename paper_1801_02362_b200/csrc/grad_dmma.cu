@@ -104,7 +104,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
                     const double* __restrict__ wa, const int* __restrict__ sig_idx,
                     const double* __restrict__ sig_coef, const int* __restrict__ nsig,
                     const double* __restrict__ fvec, const int* __restrict__ perm, const int* __restrict__ out_map,
-                    OT* __restrict__ ds, OT* __restrict__ dz, int apb) {
+                    OT* __restrict__ ds, OT* __restrict__ dz, int apb, int min_width) {
   extern __shared__ __align__(16) double dsm[];
   double* sA = dsm;                                       // [DR][AST] coefficients
   double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
@@ -181,6 +181,9 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   // window lies on other shards): nothing to contract and nothing to write -- those rows
   // belong to (and are completed by) other ranks
   if (whi < 0) return;
+  // min_width >= 0: only groups whose union is wider than min_width landmarks (the
+  // int8 tensor-core kernel, grad_i8.cu, has done the others)
+  if (min_width >= 0 && whi - wlo <= min_width) return;
   const bool restage = whi - wlo > DWMAX;
   const int nwc = whi > wlo ? (whi - wlo + DWMAX - 1) / DWMAX : 0;
   const bool ranged = nwc <= MAXWC;  // else: each restage filters the whole list
@@ -463,7 +466,8 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
 cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                 const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
-                                const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream) {
+                                const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream,
+                                int min_width) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   // atoms per CTA: all of them when there are enough frame groups to fill the
   // machine (the coefficient staging is then paid once per group), else split
@@ -494,7 +498,7 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
 #define MC_GD_LAUNCH(OTT, V)                                                                                         \
   cv_grad_dmma_kernel<OTT, V><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,     \
                                                             sig_coef, nsig, fvec, perm, out_map, (OTT*)ds,     \
-                                                            (OTT*)dz, apb)
+                                                            (OTT*)dz, apb, min_width)
   if (out_f32) {
     if (vec) MC_GD_LAUNCH(float, true); else MC_GD_LAUNCH(float, false);
   } else {

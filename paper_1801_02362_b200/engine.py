@@ -37,6 +37,9 @@ K2_GRID = int(os.environ.get("MC_K2_GRID", "0"))
 # fp32 inputs of the fp64 PathCV engine on the fp64 tensor cores (env MC_CLOSE_DMMA=0:
 # the fp64-plane CUDA-core kernels)
 CLOSE_DMMA = os.environ.get("MC_CLOSE_DMMA", "1") == "1"
+# gradient contraction on the int8 tensor cores (exact int8 digits, csrc/grad_i8.cu);
+# env MC_GRAD_I8=0 keeps the fp64 DMMA kernel for every group
+GRAD_I8 = os.environ.get("MC_GRAD_I8", "1") == "1"
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 
 
@@ -173,6 +176,7 @@ class PathCV:
         self.wuni = float(self.w[0].item()) if bool((self.w[:self.n] == self.w[0]).all()) else 0.0
         self.lraw = lm.contiguous() if (lm.dtype == torch.float32 and CLOSE_DMMA and self.n % 4 == 0
                                         and self.wuni > 0.0) else None
+        self.ldig = K.ldig_prep(self.lraw, self.lm.centroid) if (self.lraw is not None and GRAD_I8) else None
 
     # ------------------------------------------------------------------
     def _frames(self, frames):
@@ -297,7 +301,7 @@ class PathCV:
                 sl = slice(t0, t0 + chunk)
                 gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
                 K.pathcv_grad_block(wres, _Cen(fr.centroid[sl]), self.lm, raw[sl], self.lraw, self.w, self.wa, cap,
-                                    gperm, ds=ds[sl], dz=dz[sl])
+                                    gperm, ds=ds[sl], dz=dz[sl], ldig=self.ldig)
                 if close is not None:
                     K.close_grad_fix(wres, close, self.w, raw, fr.centroid, ds, dz)
             elif grad:
@@ -358,7 +362,7 @@ class PathCVGraph:
             dz = torch.empty((T, p.n, 3), dtype=odt, device=p.device)
             if p._dmma(raw):
                 gperm = K.sort_by_key(K.sig_span_key(wres, p.L), 2 * p.L + 1)
-                K.pathcv_grad_block(wres, fr, p.lm, raw, p.lraw, p.w, p.wa, p.L, gperm, ds=ds, dz=dz)
+                K.pathcv_grad_block(wres, fr, p.lm, raw, p.lraw, p.w, p.wa, p.L, gperm, ds=ds, dz=dz, ldig=p.ldig)
             else:
                 K.pathcv_grad(wres, fr, p.lm, p.w, p.wa, p.L, odt, ds=ds, dz=dz)
             out["ds"], out["dz"] = ds, dz
@@ -495,6 +499,8 @@ class PathCVTC:
         self.ls = self._lsplit(self.screen_terms)
         if _or_flags(self.ls.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("landmark coordinates contain non-finite values")
+        # int8 digits of the centred landmarks for the tensor-core gradient contraction
+        self.ldig = K.ldig_prep(self.lraw, self.ls.centroid) if (GRAD_I8 and self.n % 4 == 0) else None
         # estimate error margin (in units of lam * D): the split (22 significant bits,
         # TF32 or scaled-F16 pair) + fp32-accumulation error grows ~ sqrt(n); measured
         # max 6.4e-6 (n=1000) and 6.4e-5 (n=10000)
@@ -632,7 +638,19 @@ class PathCVTC:
         self._last_tiles = nlist
         return Dest, fr0, fss, fs0, rlo, rhi, perm0
 
-    def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False):
+    def evaluate(self, frames, grad=True, out_dtype=torch.float32, return_estimate=False, bias=None, dV=None):
+        """s, z (and with grad the atom gradients ds, dz) of every frame.
+
+        bias (metadynamics.HillStore over (s, z)) or dV ([T, 2] dV/ds, dV/dz per frame, the
+        caller's frame order): also the metadynamics bias force F = -(dV/ds ds + dV/dz dz)
+        [T, n, 3] (SPEC bias_and_force, Eq. 1) as out["force"] -- computed by ONE fused
+        tensor-core contraction over the K4 coefficients (csrc/grad_i8.cu, ncv = 1), so
+        grad=False with a bias returns s, z, V and F without materialising ds, dz."""
+        if bias is not None and dV is not None:
+            raise ConfigError("pass either a HillStore (bias) or dV, not both")
+        want_force = bias is not None or dV is not None
+        if want_force and bias is not None and getattr(bias, "d", 2) != 2:
+            raise ConfigError("the fused force needs a bias over the two path CVs (s, z)")
         rlo = rhi = perm0 = fs0 = None
         if self.prune:
             Dest, fr, fs, fs0, rlo, rhi, perm0 = self._pruned_estimate(frames)
@@ -646,15 +664,36 @@ class PathCVTC:
             Dex = wres["D_window"]
             out = {"s": wres["s"], "z": wres["z"], "window_lo": lo, "window_cnt": cnt, "D_window": Dex,
                    "nsig": wres["nsig"]}
-            if grad:
+            gperm = None
+            if grad or want_force:
                 # gradient groups by significant span (the refine groups are by window start)
                 gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
+            if grad:
                 out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap,
-                                                           gperm, out_dtype, out_map=perm0)
+                                                           gperm, out_dtype, out_map=perm0, ldig=self.ldig)
+            wide = None
+            if want_force:
+                if bias is not None:
+                    V, dVs = bias.bias(torch.stack([wres["s"], wres["z"]], 1))  # coefficient-row order
+                    out["V"] = V
+                else:
+                    dVs = torch.as_tensor(dV, dtype=torch.float64).to(self.device).reshape(-1, 2)
+                    if dVs.shape[0] != fr.shape[0]:
+                        raise ConfigError("dV must be [T, 2]")
+                    if perm0 is not None:
+                        dVs = dVs[perm0.long()]
+                dVs = dVs.contiguous()
+                out["_dVs"] = dVs
+                if self.ldig is not None:
+                    wide = torch.zeros((1,), dtype=torch.int32, device=self.device)
+                    out["force"] = K.pathcv_force_i8(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm,
+                                                     self.ldig, dVs, out_dtype, out_map=perm0, wide=wide)
             fflags = fs.flags if fs0 is None else torch.cat([fs.flags, fs0.flags])
             status = torch.stack([_flag_bits_dev(fflags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
-                                  _flag_bits_dev(wres["flags"])])
-            ff, cf, rf, wf = (_bits_value(r) for r in status.cpu().tolist())
+                                  _flag_bits_dev(wres["flags"]),
+                                  (wide if wide is not None else torch.zeros(1, dtype=torch.int32, device=self.device)
+                                   ).bool().expand(len(_FLAG_BITS))])
+            ff, cf, rf, wf, wd = (_bits_value(r) for r in status.cpu().tolist())
             if ff & FLAG_NON_FINITE:
                 raise InvalidStructureError("frame coordinates contain non-finite values")
             if (cf & FLAG_SIG_OVERFLOW) and cap < self.L:  # rare: a window wider than cap
@@ -667,12 +706,36 @@ class PathCVTC:
             raise MetadynError("path_cv refine: Jacobi diagonalisation did not converge")
         if wf & FLAG_NON_FINITE:
             raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        if want_force and (self.ldig is None or wd):
+            # a 16-frame group wider than the tensor-core kernel's K extent (or no int8
+            # operand): the force from the two gradients (mc_mtd_force, streaming)
+            from . import _lib
+            from ._lib import call, ptr, stream_ptr
+            if "ds" in out:
+                ds, dz = out["ds"], out["dz"]
+            else:
+                ds, dz = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, out_dtype,
+                                             out_map=perm0, ldig=self.ldig)
+            # ds, dz rows are in the caller's order (out_map); dV is in coefficient-row order
+            dVc = out["_dVs"]
+            if perm0 is not None:
+                back = torch.empty_like(dVc)
+                back[perm0.long()] = dVc
+                dVc = back
+            F = torch.empty_like(ds)
+            n = ds.shape[1]
+            call("mc_mtd_force", ptr(dVc.contiguous()), ds.shape[0], 2, ptr(ds), ptr(dz), None,
+                 _lib.MC_F64 if ds.dtype == torch.float64 else _lib.MC_F32, n, ptr(F), stream_ptr())
+            out["force"] = F
+        out.pop("_dVs", None)
         if perm0 is not None:
             out["screen_tiles"] = self._last_tiles  # (band, landmark tile) pairs the pruned screen computed
             # per-frame outputs back to the caller's frame order (the gradients were
             # written in place through out_map); the windows refer to the same rows
             p = perm0.long()
-            for key_ in ("s", "z", "window_lo", "window_cnt", "D_window", "nsig"):
+            for key_ in ("s", "z", "window_lo", "window_cnt", "D_window", "nsig", "V"):
+                if key_ not in out:
+                    continue
                 v = out[key_]
                 back = torch.empty_like(v)
                 back[p] = v
@@ -790,7 +853,7 @@ class PathCVTC:
             gperm = K.sig_span_key(wres, self.L)
             gperm = K.sort_by_key(gperm, 2 * self.L + 1)
             ds, dz = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, out_dtype,
-                                         out_map=perm0)
+                                         out_map=perm0, ldig=self.ldig)
             owner = yield ("exchange", ds, dz, z_parts)
             out.update(ds=ds, dz=dz, owner=owner)
         return out
@@ -914,11 +977,11 @@ class PathCVTC:
                 del Dest
                 wres.pop("D_window", None)  # free the window refits before the gradient outputs
                 ds, dz = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, odt,
-                                             out_map=perm0)
+                                             out_map=perm0, ldig=self.ldig)
                 out.update(ds=ds, dz=dz)
                 return out
             rows_s, rows_z = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm, odt,
-                                                 out_map=perm0)
+                                                 out_map=perm0, ldig=self.ldig)
             cnt_recv = torch.empty_like(cnt)
             cnt_recv[p] = cnt  # window count of every received frame, in received order
             o = 0

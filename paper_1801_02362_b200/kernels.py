@@ -276,19 +276,66 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
     return ds, dz
 
 
+class LandmarkDigits:
+    """int8 digit planes of a landmark set for the tensor-core gradient (mc_ldig_prep):
+    dig [4, npad, kpad] int8, eB [npad] int32 (per-atom power-of-two scale)."""
+
+    __slots__ = ("dig", "eB", "npad", "kpad", "L", "n")
+
+    def __init__(self, dig, eB, npad, kpad, L, n):
+        self.dig, self.eB, self.npad, self.kpad, self.L, self.n = dig, eB, npad, kpad, L, n
+
+
+def ldig_prep(landmarks, lcen):
+    """landmarks [L, n, 3] fp32 raw, lcen [L, 3] fp64 centroids -> LandmarkDigits."""
+    L, n = landmarks.shape[0], landmarks.shape[1]
+    npad = ((n + 127) // 128) * 128
+    kpad = ((3 * L + 15) // 16) * 16
+    dev = landmarks.device
+    dig = torch.empty((4, npad, kpad), dtype=torch.int8, device=dev)
+    eB = torch.empty((npad,), dtype=I32, device=dev)
+    call("mc_ldig_prep", ptr(landmarks.contiguous()), ptr(lcen.contiguous()), L, n, npad, kpad, ptr(eB), ptr(dig),
+         stream_ptr())
+    return LandmarkDigits(dig, eB, npad, kpad, L, n)
+
+
 def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32,
-                      out_map=None, ds=None, dz=None):
+                      out_map=None, ds=None, dz=None, ldig=None):
     """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames.
     out_map (optional, int32 [T]): the caller's row of frame t -- its raw coordinates
-    are read from and its gradients written to that row.  ds / dz: optional outputs."""
+    are read from and its gradients written to that row.  ds / dz: optional outputs.
+    ldig (LandmarkDigits): the contraction runs on the int8 tensor cores
+    (mc_pathcv_grad_i8; wide groups on DMMA in the same call), else on DMMA."""
     T, n = frames.shape[0], frames.shape[1]
     dev = frames.device
     ds = torch.empty((T, n, 3), dtype=out_dtype, device=dev) if ds is None else ds
     dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev) if dz is None else dz
+    f32 = 1 if ds.dtype == torch.float32 else 0
+    if ldig is not None:
+        call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
+             ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
+             ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), None, ptr(perm), ptr(out_map), ptr(ds),
+             ptr(dz), f32, 2, None, stream_ptr())
+        return ds, dz
     call("mc_pathcv_grad_block", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(perm),
-         ptr(out_map), ptr(ds), ptr(dz), 1 if ds.dtype == torch.float32 else 0, stream_ptr())
+         ptr(out_map), ptr(ds), ptr(dz), f32, stream_ptr())
     return ds, dz
+
+
+def pathcv_force_i8(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ldig, dV, out_dtype=torch.float32,
+                    out_map=None, F=None, wide=None):
+    """Fused metadynamics bias force F = -(dV/ds ds + dV/dz dz) [T, n, 3] from the K4
+    coefficients (one tensor-core contraction instead of ds, dz + mc_mtd_force).
+    dV [T, 2] fp64 (indexed like the coefficient rows).  Groups of 16 frames wider than
+    80 landmarks are skipped and set wide[0] = 1 (int32 device flag, caller-zeroed)."""
+    T, n = frames.shape[0], frames.shape[1]
+    F = torch.empty((T, n, 3), dtype=out_dtype, device=frames.device) if F is None else F
+    call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
+         ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
+         ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(dV.contiguous()), ptr(perm), ptr(out_map),
+         ptr(F), None, 1 if F.dtype == torch.float32 else 0, 1, ptr(wide), stream_ptr())
+    return F
 
 
 def sig_span_key(wres, L):

@@ -154,6 +154,10 @@ def step_close_structure(x: Structure, state: CloseStructureState, ref: Referenc
         D, R, g = _exact_batch(x, ref, all_idx)
         state.y = x.center()
         state.saved_rots = R
+        # the state now describes x against its own close structure: R_xy = I with
+        # x's spectrum, so approx_distance right after a reassignment equals the
+        # exact distance instead of reusing the fit to the old y
+        state.fit_xy, state._xy_eig, _ = _fit_xy(x, state.y)
         state.reassign_count += 1
         state.expensive_count += ref.n
         return state, [DistanceResult(float(D[i]), g[i], True) for i in all_idx]

@@ -147,6 +147,24 @@ def test_approx_distance_equals_exact_after_reassignment(cuda_device):
     assert abs(r.value - exact[2].value) < 1e-12
 
 
+def test_approx_distance_right_after_a_single_reassigning_step(cuda_device):
+    """after a refresh the state's x<->y fit is x against its own close
+    structure (R_xy = I), so approx_distance equals the exact distance at once --
+    on the first step and on a later refresh (where a stale fit to the old y
+    would otherwise be combined with the new saved rotations)."""
+    wl = synth.config0(seed=13, T=3, L=5, N=12)
+    ref = colvar.ReferenceSet([G.Structure(a).center() for a in wl.landmarks], lam=wl.lam)
+    state = msd.CloseStructureState(epsilon=1e-12)  # every distinct frame reassigns
+    for t in range(3):
+        x = G.Structure(wl.frames[t])
+        state, exact = msd.step_close_structure(x, state, ref)
+        assert all(r.exact for r in exact) and state.reassign_count == t + 1
+        for i in (0, 3):
+            r = msd.approx_distance(x, i, state, ref)
+            assert abs(r.value - exact[i].value) < 1e-12
+            np.testing.assert_allclose(r.grad, exact[i].grad, atol=1e-9 * max(1.0, np.abs(exact[i].grad).max()))
+
+
 def test_property_map_kats(cuda_device):
     a = G.Structure(np.random.default_rng(0).normal(size=(4, 3)))
     ref1 = colvar.ReferenceSet([a], lam=3.0, properties=[7.0])

@@ -1,0 +1,100 @@
+"""GPU tests of the int8 tensor-core (tcgen05 kind::i8, Ozaki digits) gradient
+contraction (csrc/grad_i8.cu) against the fp64 DMMA kernel and the fp64 oracle,
+and of the fused metadynamics bias force on the same kernel.
+
+Tolerances (BASELINE.json north_star): gradients within 1e-5 of the per-frame
+maximum vs the oracle; the int8 and DMMA contractions agree to 1e-6 of the
+per-frame maximum (both are exact to ~1e-8 of the contraction's magnitude).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1801_02362_b200 import engine, kernels as K, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel_rows(got, ref):
+    got = got.reshape(got.shape[0], -1).astype(np.float64)
+    ref = ref.reshape(ref.shape[0], -1).astype(np.float64)
+    scale = np.abs(ref).max(axis=1)
+    err = np.abs(got - ref).max(axis=1)
+    return err / np.maximum(scale, 1e-300)
+
+
+def test_landmark_digits_reconstruct_centred_coordinates(cuda_device):
+    """mc_ldig_prep: sum_q d_q 2^(24-8q) 2^(eB-31) equals ac = lraw - lcen within 2^(eB-32)."""
+    wl = synth.config4(seed=11, T=4, L=77, N=300)
+    lm = torch.from_numpy(wl.landmarks).cuda()
+    lcen = lm.double().mean(dim=1)
+    ld = K.ldig_prep(lm, lcen)
+    dig = ld.dig.cpu().numpy().astype(np.int64)
+    eB = ld.eB.cpu().numpy()[:300]
+    L, n = 77, 300
+    X = dig[0] * 2 ** 24 + dig[1] * 2 ** 16 + dig[2] * 2 ** 8 + dig[3]  # [npad, kpad]
+    rec = X[:n, :3 * L].astype(np.float64) * np.ldexp(1.0, eB - 31)[:, None]
+    ac = (wl.landmarks.astype(np.float64) - lcen.cpu().numpy()[:, None, :])  # [L, n, 3]
+    ref = ac.transpose(1, 0, 2).reshape(n, 3 * L)
+    err = np.abs(rec - ref)
+    assert np.all(err <= np.ldexp(1.0, eB - 32)[:, None] * (1 + 1e-12))
+    assert np.all(np.abs(dig[0]) <= 127) and np.all(dig[:, n:, :] == 0) and np.all(dig[:, :, 3 * L:] == 0)
+    # the leading digit of each atom's largest coordinate is near full scale
+    assert np.all(np.abs(dig[0, :n, :3 * L]).max(axis=1) >= 63)
+
+
+@pytest.mark.parametrize("T,L,N", [(96, 512, 600), (77, 300, 1000), (40, 2048, 2500)])
+def test_i8_gradient_matches_dmma_and_oracle(T, L, N, cuda_device):
+    """PathCVTC.evaluate with the int8 contraction == the fp64 DMMA contraction (1e-6 of the
+    per-frame max), and both == the fp64 oracle (1e-5); ragged T, n % 128 != 0."""
+    wl = synth.config4(seed=5, T=T, L=L, N=N)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam)
+    assert pcv.ldig is not None
+    out = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    ldig, pcv.ldig = pcv.ldig, None
+    dm = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    pcv.ldig = ldig
+    ref = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    for key in ("ds", "dz"):
+        a, b = out[key].cpu().numpy(), dm[key].cpu().numpy()
+        r_dm = _rel_rows(a, b)
+        r_or = _rel_rows(a, ref[key])
+        print(f"{key}: i8 vs dmma worst {r_dm.max():.2e}, i8 vs oracle worst {r_or.max():.2e}")
+        assert r_dm.max() <= 1e-6
+        assert r_or.max() <= 1e-5
+    np.testing.assert_array_equal(out["s"].cpu().numpy(), dm["s"].cpu().numpy())
+
+
+def test_i8_gradient_fp32_output_and_wide_groups(cuda_device):
+    """fp32 outputs; a small lambda widens the significant windows past 80 landmarks, so
+    part of the groups run on the DMMA fallback inside the same call: still == DMMA."""
+    wl = synth.config4(seed=6, T=64, L=1024, N=400)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam * 0.02, window_cap=1024)
+    out = pcv.evaluate(wl.frames)
+    nsig = out["nsig"].cpu().numpy()
+    assert nsig.max() > 80, "the case must exercise the wide-group fallback"
+    ldig, pcv.ldig = pcv.ldig, None
+    dm = pcv.evaluate(wl.frames)
+    pcv.ldig = ldig
+    for key in ("ds", "dz"):
+        r = _rel_rows(out[key].cpu().numpy(), dm[key].cpu().numpy())
+        assert r.max() <= 2e-6, f"{key}: {r.max():.2e}"
+
+
+def test_fused_bias_force_equals_contracted_gradients(cuda_device):
+    """F = -(V_s ds + V_z dz) from one tensor-core contraction == the same combination of
+    the separately computed gradients (1e-6 of the per-frame max)."""
+    wl = synth.config4(seed=8, T=50, L=512, N=800)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam)
+    rng = np.random.default_rng(3)
+    dV = torch.from_numpy(rng.normal(size=(50, 2))).cuda()
+    out = pcv.evaluate(wl.frames, out_dtype=torch.float64, dV=dV)
+    F = out["force"].cpu().numpy()
+    ref = -(dV[:, 0, None, None] * out["ds"] + dV[:, 1, None, None] * out["dz"]).cpu().numpy()
+    r = _rel_rows(F, ref)
+    assert r.max() <= 1e-6, f"{r.max():.2e}"
+    # zero net force (translation invariance): the int8 digits are exact to ~2^-31 per atom,
+    # so the atom sum vanishes to ~1e-7 of the largest component (the DMMA sum to ~1e-14)
+    assert np.abs(F.sum(axis=1)).max() <= 1e-6 * np.abs(F).max()
