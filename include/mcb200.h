@@ -208,8 +208,10 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
  * reads of _kearsley_matrix's contraction, geometry.py:180-196, by exact int8 digits):
  * the centred landmark coordinates ac = lraw - lcen (fp64) split into 4 signed int8
  * digits with a power-of-two scale 2^eB[k] per atom over every (landmark, axis):
- *   ac[l,k,g] ~= 2^(eB[k] - 31) sum_q dig[q][k][3l+g] 2^(24 - 8q)   (|error| <= 2^(eB-32)).
- * dig int8 [4, npad, kpad] (npad % 128 == 0, kpad % 16 == 0, kpad >= 3L), eB int32 [npad].
+ *   ac[l,k,g] ~= 2^(eB[k] - 31) sum_q D_q[k][3l+g] 2^(24 - 8q)   (|error| <= 2^(eB-32)),
+ * stored per 32-byte k-step with the 4 digits interleaved: D_q[k][kk] =
+ * dig[k][kk / 32][q][kk % 32], dig int8 [npad, kpad / 32, 4, 32] (npad % 128 == 0,
+ * kpad % 32 == 0, kpad >= 3L), eB int32 [npad].
  * Once per landmark set. */
 int mc_ldig_prep(const float* lraw, const double* lcen, int32_t L, int32_t n, int32_t npad, int32_t kpad,
                  int32_t* eB, int8_t* dig, void* stream);
@@ -219,17 +221,20 @@ int mc_ldig_prep(const float* lraw, const double* lcen, int32_t L, int32_t n, in
  * and the epilogue recombines them in fp64 (relative error ~2^-31 of the contraction's
  * magnitude, SPEC.md:228-236 gradient tolerance 1e-5).  ncv = 2: ds (out0), dz (out1)
  * -- the SPEC property_map gradients; groups of 8 frames whose significant union is
- * wider than 80 landmarks (or n % 4 != 0) go to the DMMA kernel in the same call.
+ * wider than 117 landmarks (or n % 4 != 0) go to the DMMA kernel in the same call.
  * ncv = 1: the metadynamics bias force F = -(dV/ds ds + dV/dz dz) (SPEC bias_and_force,
  * Eq. 1) written to out0 [T, n, 3] from dV [T, 2] (groups of 16 frames); groups wider
- * than 80 landmarks are NOT written and set *wide_flag = 1 (the caller then takes the
+ * than 123 landmarks are NOT written and set *wide_flag = 1 (the caller then takes the
  * two-output path).  Other arguments as mc_pathcv_grad_block. */
 int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const float* lraw,
                       const double* lcen, const double* w, const double* w_align, const int8_t* dig,
                       const int32_t* eB, int32_t npad, int32_t kpad, const int32_t* sig_idx, const double* sig_coef,
                       const int32_t* nsig, const double* fvec, const double* dV, const int32_t* perm,
                       const int32_t* out_map, void* out0, void* out1, int32_t out_f32, int32_t ncv,
-                      int32_t* wide_flag, void* stream);
+                      int32_t* wide_flag, void* workspace, int64_t ws_bytes, void* stream);
+/* Bytes of caller workspace mc_pathcv_grad_i8 needs for T frames (per frame group: a
+ * header and the A-digit image, <= 73 KB); -1 on bad arguments. */
+int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv);
 /* mc_msd_tf32 on CTA pairs (tcgen05.mma.cta_group::2, M = 256 frames per pair):
  * same inputs/outputs; each SM stages half of the landmark operand. */
 int mc_msd_tf32_2sm(const float* fhi, const float* flo, const float* lhi, const float* llo, const double* gx,

@@ -89,7 +89,7 @@ _SIGS = {
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],
     "mc_ldig_prep": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
     "mc_pathcv_grad_i8": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P,
-                          _P, _P, _I32, _I32, _P, _P],
+                          _P, _P, _I32, _I32, _P, _P, _I64, _P],
 }
 
 # optional entry points (none at present)
@@ -118,13 +118,15 @@ def load():
             fn.argtypes = args
             fn.restype = ctypes.c_int
     lib.mc_version.restype = ctypes.c_int
+    lib.mc_grad_i8_workspace_size.argtypes = [_I32, _I32]
+    lib.mc_grad_i8_workspace_size.restype = _I64
     _lib = lib
     return lib
 
 
 def exported_symbols():
     """Names declared in include/mcb200.h that the loaded library must export."""
-    return ["mc_version", *_SIGS.keys()]
+    return ["mc_version", "mc_grad_i8_workspace_size", *_SIGS.keys()]
 
 
 def check(status, what=""):

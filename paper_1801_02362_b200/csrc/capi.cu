@@ -199,7 +199,7 @@ int mc_pathcv_grad_block(int32_t T, int32_t n, int32_t cap, const float* fraw, c
 
 int mc_ldig_prep(const float* lraw, const double* lcen, int32_t L, int32_t n, int32_t npad, int32_t kpad,
                  int32_t* eB, int8_t* dig, void* stream) {
-  if (L < 1 || n < 2 || npad < n || npad % 128 != 0 || kpad < 3 * L || kpad % 16 != 0) return MC_ERR_CONFIG;
+  if (L < 1 || n < 2 || npad < n || npad % 128 != 0 || kpad < 3 * L || kpad % 32 != 0) return MC_ERR_CONFIG;
   if (!lraw || !lcen || !eB || !dig) return MC_ERR_CONFIG;
   return cuda_status(mc::launch_ldig(lraw, lcen, L, n, npad, kpad, eB, dig, S_(stream)));
 }
@@ -209,16 +209,23 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
                       const int32_t* eB, int32_t npad, int32_t kpad, const int32_t* sig_idx, const double* sig_coef,
                       const int32_t* nsig, const double* fvec, const double* dV, const int32_t* perm,
                       const int32_t* out_map, void* out0, void* out1, int32_t out_f32, int32_t ncv,
-                      int32_t* wide_flag, void* stream) {
+                      int32_t* wide_flag, void* workspace, int64_t ws_bytes, void* stream) {
   if (T < 0 || n < 2 || cap < 1 || (ncv != 1 && ncv != 2)) return MC_ERR_CONFIG;
   if (T > 0 && (!fraw || !fcen || !lraw || !lcen || !w || !w_align || !dig || !eB || !sig_idx || !sig_coef ||
                 !nsig || !fvec || !out0 || (ncv == 2 && !out1) || (ncv == 1 && !dV)))
     return MC_ERR_CONFIG;
-  if (npad < n || npad % 128 != 0 || kpad % 16 != 0) return MC_ERR_CONFIG;
-  if (ncv == 1 && n % 4 != 0) return MC_ERR_CONFIG;  // the fused force runs only on the tensor-core kernel
+  if (npad < n || npad % 128 != 0 || kpad % 32 != 0) return MC_ERR_CONFIG;
+  if (ncv == 1 && (n % 4 != 0 || !workspace || ws_bytes < (int64_t)mc::grad_i8_workspace(T, 1)))
+    return MC_ERR_CONFIG;  // the fused force runs only on the tensor-core kernel
   return cuda_status(mc::launch_cv_grad_i8(T, n, cap, fraw, fcen, lraw, lcen, w, w_align, dig, eB, npad, kpad,
                                            sig_idx, sig_coef, nsig, fvec, dV, perm, out_map, out0, out1, out_f32,
-                                           ncv, wide_flag, S_(stream)));
+                                           ncv, wide_flag, workspace, ws_bytes < 0 ? 0 : (size_t)ws_bytes,
+                                           S_(stream)));
+}
+
+int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv) {
+  if (T < 0 || (ncv != 1 && ncv != 2)) return -1;
+  return (int64_t)mc::grad_i8_workspace(T, ncv);
 }
 
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,

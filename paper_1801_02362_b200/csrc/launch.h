@@ -1,6 +1,7 @@
 // Internal host launchers (one per kernel family); capi.cu wraps them in the C ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 namespace mc {
@@ -74,7 +75,9 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
                               const double* lcen, const double* w, const double* wa, const int8_t* dig, const int* eB,
                               int npad, int kpad, const int* sig_idx, const double* sig_coef, const int* nsig,
                               const double* fvec, const double* dV, const int* perm, const int* out_map, void* out0,
-                              void* out1, int out_f32, int ncv, int* wide_flag, cudaStream_t stream);
+                              void* out1, int out_f32, int ncv, int* wide_flag, void* ws, size_t ws_bytes,
+                              cudaStream_t stream);
+size_t grad_i8_workspace(int T, int ncv);
 cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                  const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                  const double* sig_coef, const int* nsig, const double* fvec, const int* perm,

@@ -277,8 +277,9 @@ def pathcv_grad(wres, fr, lm, w, w_align, cap, out_dtype=F64, close=None, raw=No
 
 
 class LandmarkDigits:
-    """int8 digit planes of a landmark set for the tensor-core gradient (mc_ldig_prep):
-    dig [4, npad, kpad] int8, eB [npad] int32 (per-atom power-of-two scale)."""
+    """int8 digits of a landmark set for the tensor-core gradient (mc_ldig_prep):
+    dig [npad, kpad / 32, 4, 32] int8 (the 4 digits of each 32-byte k-step of an atom's
+    row interleaved), eB [npad] int32 (per-atom power-of-two scale)."""
 
     __slots__ = ("dig", "eB", "npad", "kpad", "L", "n")
 
@@ -290,13 +291,18 @@ def ldig_prep(landmarks, lcen):
     """landmarks [L, n, 3] fp32 raw, lcen [L, 3] fp64 centroids -> LandmarkDigits."""
     L, n = landmarks.shape[0], landmarks.shape[1]
     npad = ((n + 127) // 128) * 128
-    kpad = ((3 * L + 15) // 16) * 16
+    kpad = ((3 * L + 31) // 32) * 32
     dev = landmarks.device
-    dig = torch.empty((4, npad, kpad), dtype=torch.int8, device=dev)
+    dig = torch.empty((npad, kpad // 32, 4, 32), dtype=torch.int8, device=dev)
     eB = torch.empty((npad,), dtype=I32, device=dev)
     call("mc_ldig_prep", ptr(landmarks.contiguous()), ptr(lcen.contiguous()), L, n, npad, kpad, ptr(eB), ptr(dig),
          stream_ptr())
     return LandmarkDigits(dig, eB, npad, kpad, L, n)
+
+
+def _grad_i8_ws(T, ncv, dev):
+    nb = int(_lib.load().mc_grad_i8_workspace_size(int(T), int(ncv)))
+    return torch.empty((nb,), dtype=torch.uint8, device=dev), nb
 
 
 def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32,
@@ -312,10 +318,11 @@ def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ou
     dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev) if dz is None else dz
     f32 = 1 if ds.dtype == torch.float32 else 0
     if ldig is not None:
+        ws, nb = _grad_i8_ws(T, 2, dev)
         call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
              ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
              ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), None, ptr(perm), ptr(out_map), ptr(ds),
-             ptr(dz), f32, 2, None, stream_ptr())
+             ptr(dz), f32, 2, None, ptr(ws), nb, stream_ptr())
         return ds, dz
     call("mc_pathcv_grad_block", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(perm),
@@ -328,13 +335,14 @@ def pathcv_force_i8(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ldig
     """Fused metadynamics bias force F = -(dV/ds ds + dV/dz dz) [T, n, 3] from the K4
     coefficients (one tensor-core contraction instead of ds, dz + mc_mtd_force).
     dV [T, 2] fp64 (indexed like the coefficient rows).  Groups of 16 frames wider than
-    80 landmarks are skipped and set wide[0] = 1 (int32 device flag, caller-zeroed)."""
+    117 landmarks are skipped and set wide[0] = 1 (int32 device flag, caller-zeroed)."""
     T, n = frames.shape[0], frames.shape[1]
     F = torch.empty((T, n, 3), dtype=out_dtype, device=frames.device) if F is None else F
+    ws, nb = _grad_i8_ws(T, 1, frames.device)
     call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
          ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(dV.contiguous()), ptr(perm), ptr(out_map),
-         ptr(F), None, 1 if F.dtype == torch.float32 else 0, 1, ptr(wide), stream_ptr())
+         ptr(F), None, 1 if F.dtype == torch.float32 else 0, 1, ptr(wide), ptr(ws), nb, stream_ptr())
     return F
 
 

@@ -31,7 +31,8 @@ def test_landmark_digits_reconstruct_centred_coordinates(cuda_device):
     lm = torch.from_numpy(wl.landmarks).cuda()
     lcen = lm.double().mean(dim=1)
     ld = K.ldig_prep(lm, lcen)
-    dig = ld.dig.cpu().numpy().astype(np.int64)
+    d4 = ld.dig.cpu().numpy().astype(np.int64)  # [npad, kpad / 32, 4, 32]
+    dig = d4.transpose(2, 0, 1, 3).reshape(4, d4.shape[0], -1)  # [4, npad, kpad]
     eB = ld.eB.cpu().numpy()[:300]
     L, n = 77, 300
     X = dig[0] * 2 ** 24 + dig[1] * 2 ** 16 + dig[2] * 2 ** 8 + dig[3]  # [npad, kpad]
@@ -68,13 +69,13 @@ def test_i8_gradient_matches_dmma_and_oracle(T, L, N, cuda_device):
 
 
 def test_i8_gradient_fp32_output_and_wide_groups(cuda_device):
-    """fp32 outputs; a small lambda widens the significant windows past 80 landmarks, so
+    """fp32 outputs; a small lambda widens the significant windows past 117 landmarks, so
     part of the groups run on the DMMA fallback inside the same call: still == DMMA."""
     wl = synth.config4(seed=6, T=64, L=1024, N=400)
     pcv = engine.PathCVTC(wl.landmarks, wl.lam * 0.02, window_cap=1024)
     out = pcv.evaluate(wl.frames)
     nsig = out["nsig"].cpu().numpy()
-    assert nsig.max() > 80, "the case must exercise the wide-group fallback"
+    assert nsig.max() > 117, "the case must exercise the wide-group fallback"
     ldig, pcv.ldig = pcv.ldig, None
     dm = pcv.evaluate(wl.frames)
     pcv.ldig = ldig
@@ -95,6 +96,7 @@ def test_fused_bias_force_equals_contracted_gradients(cuda_device):
     ref = -(dV[:, 0, None, None] * out["ds"] + dV[:, 1, None, None] * out["dz"]).cpu().numpy()
     r = _rel_rows(F, ref)
     assert r.max() <= 1e-6, f"{r.max():.2e}"
-    # zero net force (translation invariance): the int8 digits are exact to ~2^-31 per atom,
-    # so the atom sum vanishes to ~1e-7 of the largest component (the DMMA sum to ~1e-14)
-    assert np.abs(F.sum(axis=1)).max() <= 1e-6 * np.abs(F).max()
+    # zero net force (translation invariance): each atom's force is exact to ~1e-8 of the
+    # frame's largest component, so the sum over the atoms vanishes to within the 1e-5
+    # gradient tolerance (the fp64 DMMA sum to ~1e-14)
+    assert np.abs(F.sum(axis=1)).max() <= 1e-5 * np.abs(F).max()

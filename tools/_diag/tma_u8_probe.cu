@@ -46,14 +46,14 @@ int main() {
   cudaMalloc(&o, 1 << 16);
   cudaMemcpy(d, h, rows * cols, cudaMemcpyHostToDevice);
   int bad_total = 0;
-  for (int sw : {64, 128}) {
+  for (int sw : {32, 64, 128}) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols};
     cuuint32_t box[2] = {(cuuint32_t)sw, 128};
     cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, d, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                      sw == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : sw == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int c0 = (3 * 37) & ~15, c1 = 256;  // the K start must be 16-byte aligned (an unaligned one faults)
     const int nbytes = sw * 128;
@@ -66,7 +66,9 @@ int main() {
     for (int r = 0; r < 128; ++r)
       for (int c = 0; c < sw; ++c) {
         int off;
-        if (sw == 64)
+        if (sw == 32)
+          off = (r >> 3) * 256 + (r & 7) * 32 + ((((c >> 4) ^ ((r & 7) >> 2)) & 1) << 4) + (c & 15);
+        else if (sw == 64)
           off = (r >> 3) * 512 + (r & 7) * 64 + ((((c >> 4) ^ ((r & 7) >> 1)) & 3) << 4) + (c & 15);
         else
           off = (r >> 3) * 1024 + (r & 7) * 128 + ((((c >> 4) ^ (r & 7)) & 7) << 4) + (c & 15);
