@@ -149,9 +149,12 @@ def test_one_term_and_split_screens_agree(cuda_device):
     np.testing.assert_allclose(a["s"].cpu().numpy(), b["s"].cpu().numpy(), rtol=1e-9)
     np.testing.assert_allclose(a["z"].cpu().numpy(), b["z"].cpu().numpy(), rtol=1e-9)
     for key in ("ds", "dz"):  # extra (negligible, < e^-25) landmarks only: per-frame scale
+        # (the int8 tensor-core contraction is exact to ~3e-8 of the per-frame maximum and
+        # scales each coefficient row by its own maximum, so two significant sets that differ
+        # by negligible landmarks round differently at that level)
         x, y = a[key].cpu().numpy(), b[key].cpu().numpy()
         scale = np.abs(y).reshape(y.shape[0], -1).max(axis=1)
-        assert np.all(np.abs(x - y).reshape(y.shape[0], -1).max(axis=1) <= 1e-9 * scale)
+        assert np.all(np.abs(x - y).reshape(y.shape[0], -1).max(axis=1) <= 1e-6 * scale)
     # the one-term windows (wider error allowance) contain the split-screen windows
     alo, acnt = a["window_lo"].cpu().numpy(), a["window_cnt"].cpu().numpy()
     blo, bcnt = b["window_lo"].cpu().numpy(), b["window_cnt"].cpu().numpy()
