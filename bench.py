@@ -267,6 +267,10 @@ class Config3:
             return "fp64_flop", 18.0 * n * T * L
         if name == "mc_cov_dmma":  # dense S [T, L, 9]: 9 fp64 FMA per atom and pair on DMMA
             return "fp64_tensor_flop", 18.0 * n * T * L
+        if name == "mc_pathcv_grad_i8" and self.last is not None:
+            # executed int8 MMA work: per (frame, significant landmark, atom) 18 multiply-adds
+            # (2 CVs x 3 x 3) x the 10 kept digit products (tcgen05.mma kind::i8)
+            return "int8_tensor_op", 2.0 * 10.0 * 18.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_pathcv_grad_block" and self.last is not None:
             return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_fit_dense":
@@ -310,10 +314,12 @@ class ConfigTC:
             # partials / straddling gradient rows are exchanged over NCCL
             T_all, off, cnt = shp["T"], 0, shp["T"]
         else:
-            # weak scaling: every rank evaluates its own full-size frame set (disjoint
-            # slices of one global set), landmarks replicated, no data-path collective
-            T_all = world * shp["T"]
-            off, cnt = rank * shp["T"], shp["T"]
+            # strong scaling: the config's fixed frame set (T frames) is split across the
+            # ranks, T / G frames each, landmarks replicated, no data-path collective
+            from paper_1801_02362_b200 import dist as Dd
+
+            T_all = shp["T"]
+            off, cnt = Dd.shard_range(T_all, rank, world)
         self.wl = synth.interp_config_device(shp["seed"], T_all, shp["L"], shp["N"], shp["n_endpoints"], device,
                                              frame_offset=off, frame_count=cnt)
         self.T_all, self.T = T_all, cnt
@@ -349,15 +355,29 @@ class ConfigTC:
             self.scaling = "strong"
             self.replicated_units = True  # every rank evaluates the same T frames
         else:
-            self.parallelism = f"frame-sharded dp{world}" if world > 1 else "single"
-            self.scaling = "weak"
+            self.parallelism = (f"frame-sharded x{world} (T/{world} frames per rank, landmarks replicated, "
+                                "no collective)") if world > 1 else "single"
+            self.scaling = "strong"
         self.last = None
         if cfg == 2:
             self.metric, self.unit = "aligned-MSD pairs/s", "pairs/s"
             self.D = torch.empty((self.T, self.L), dtype=torch.float32, device=device)
         else:
             self.metric, self.unit = "path-CV frames/s", "frames/s"
-        self.dtype = "f32 in / tf32x3 tensor + f64 exact"
+            # metadynamics bias over (s, z) for the fused-force end-to-end variant: 256 hills
+            # spread along the path (direct summation, SPEC bias_and_force)
+            from paper_1801_02362_b200.metadynamics import HillStore
+
+            self.hills = HillStore(2, 1, 1.0, [16.0, 0.005], device=device)
+            hr = np.random.default_rng(44)
+            for k, c in enumerate(zip(hr.uniform(0, self.L - 1, 256), hr.uniform(0.0, 0.02, 256))):
+                self.hills.deposit(torch.tensor(c, dtype=torch.float64), k)
+        if cfg == 2:
+            self.dtype = "f32 coordinates; exact fp64 refits of every pair on the fp64 tensor cores (DMMA)"
+        else:
+            self.dtype = ("f32 coordinates; one-term FP16 tcgen05 screen (rigorous bound) -> exact fp64 refits "
+                          "(DMMA) -> fp64 weights -> gradient contraction on tcgen05 kind::i8 with exact int8 "
+                          "digits (int32 accumulation, fp64 recombination)")
 
     def _step(self, frames, D=None):
         if self.cfg == 2:
@@ -460,9 +480,10 @@ class ConfigTC:
             c0 += n
         return out
 
-    def step_e2e(self):
+    def step_e2e(self, force=False):
         """Public API with host frames: chunked H2D on a copy stream, double-buffered
-        against the compute of the previous chunk, then D2H of the result."""
+        against the compute of the previous chunk, then D2H of the whole result (config 4:
+        ds, dz, s, z -- or with force=True the fused bias force F, s, z, V)."""
         import torch
 
         if not hasattr(self, "_copy_stream"):
@@ -506,16 +527,60 @@ class ConfigTC:
                     outs.append(self._d_host)
             else:
                 self._c0 = chunks[i][0]  # home offset of this chunk (frame-routed landmark shards)
-                o = self._step(fr)
-                outs.append(o["s"].to("cpu", non_blocking=True))
-                outs.append(o["z"].to("cpu", non_blocking=True))
+                if force:
+                    o = self.pcv.evaluate(fr, grad=False, bias=self.hills)
+                    res = [o["force"], o["s"], o["z"], o["V"]]
+                else:
+                    o = self._step(fr)
+                    res = [o["ds"], o["dz"], o["s"], o["z"]]
+                # the step's whole result back to the host, on its own stream (full-duplex
+                # PCIe: chunk i's D2H overlaps chunk i + 1's H2D and compute); pinned
+                # double-buffered host slots (stream order makes slot reuse safe)
+                done = torch.cuda.Event()
+                done.record(comp)
+                slot = self._host_slots(chunks, force)[i % 2]
+                n = chunks[i][1]
+                with torch.cuda.stream(self._d2h_stream):
+                    self._d2h_stream.wait_event(done)
+                    for r, h in zip(res, slot):
+                        r.record_stream(self._d2h_stream)
+                        h[:n].copy_(r, non_blocking=True)
+                if i + 1 == len(chunks):
+                    comp.wait_stream(self._d2h_stream)
+                    outs.append(slot)
         self._c0 = 0
         comp.synchronize()
         return outs
 
-    def e2e_bytes(self):
+    def _host_slots(self, chunks, force):
+        """Two pinned host slots for the chunk results (gradients or force + per-frame scalars)."""
+        import torch
+
+        key = "force" if force else "grad"
+        if not hasattr(self, "_slots"):
+            self._slots = {}
+            self._d2h_stream = torch.cuda.Stream(device=self.device)
+        if key not in self._slots:
+            m = max(n for _, n in chunks)
+            big = 1 if force else 2
+            self._slots[key] = [[torch.empty((m, self.n, 3), dtype=torch.float32).pin_memory() for _ in range(big)] +
+                                [torch.empty((m,), dtype=torch.float64).pin_memory() for _ in range(4 - big)]
+                                for _ in range(2)]
+        return self._slots[key]
+
+    def step_e2e_force(self):
+        """The metadynamics consumer's call: s, z, V and the fused bias force F [T, n, 3]
+        (one tensor-core contraction, no ds / dz) back to the host."""
+        return self.step_e2e(force=True)
+
+    def e2e_bytes(self, force=False):
         h2d = self.T * self.n * 3 * 4
-        d2h = self.T * self.L * 4 if self.cfg == 2 else self.T * 16
+        if self.cfg == 2:
+            d2h = self.T * self.L * 4
+        elif force:
+            d2h = self.T * self.n * 3 * 4 + self.T * 3 * 8  # F, s, z, V
+        else:
+            d2h = 2 * self.T * self.n * 3 * 4 + self.T * 2 * 8  # ds, dz, s, z
         return h2d, d2h
 
     def units(self):
@@ -532,6 +597,10 @@ class ConfigTC:
                 tiles = int(self.last["screen_tiles"].item())
                 pairs = T * self.pcv.coarse.numel() + tiles * 128 * 48  # coarse + banded
             return "tensor_flop_f16", terms * 18.0 * n * pairs
+        if name == "mc_pathcv_grad_i8" and self.last is not None:
+            # executed int8 MMA work: per (frame, significant landmark, atom) 18 multiply-adds
+            # (2 CVs x 3 x 3) x the 10 kept digit products (tcgen05.mma kind::i8)
+            return "int8_tensor_op", 2.0 * 10.0 * 18.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_pathcv_grad_block" and self.last is not None:
             # useful fp64 work: 18 FMA (U^s, U^z: 2 CVs x 3 x 3) per significant pair and atom
             return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
@@ -566,7 +635,21 @@ class ConfigTC:
         return d
 
 
-DMMA_PEAK_TF = 36.8  # measured mma.sync f64 rate on this pool's B200 (tools/_diag/dmma_probe.cu)
+DMMA_PEAK_TF = 36.2  # measured mma.sync f64 rate on this pool's B200 (profiles/r02_dmma_probe_b200.txt)
+
+
+def _int8_roof(amount, step_ms, pk):
+    """Roofline of an int8 tcgen05 kernel: executed int8 ops per second against twice the
+    measured bf16 GEMM rate (kind::i8 issues twice the multiply-adds of kind::f16 per cycle:
+    8192 vs 4096 per SM, tools/_diag/i8_probe.cu)."""
+    ach = amount / (step_ms * 1e-3) / 1e12
+    sustained = 2.0 * (pk.get("bf16_sustained") or pk["bf16"])
+    return {"bound": "tensor", "achieved": ach, "peak": sustained, "unit": "TOPS (int8)", "frac": ach / sustained,
+            "peak_src": f"2 x bf16_tflops_sustained from {pk['src']} (kind::i8 = 2x the kind::f16 MAC rate, "
+                        "measured by tools/_diag/i8_probe.cu)",
+            "peak_burst": 2.0 * pk["bf16"], "frac_of_burst": ach / (2.0 * pk["bf16"]),
+            "flop_basis": "executed int8 multiply-adds x 2: 10 digit products x 18 per (frame, significant "
+                          "landmark, atom)"}
 
 
 def measured_traffic(kernel, cfg, T):
@@ -660,6 +743,16 @@ def run_ours(args, rank, world, local_rank):
     runner.step_e2e()
     ms_e2e = timed(runner.step_e2e, args.steps)
     h2d, d2h = runner.e2e_bytes()
+    e2e_force = None
+    if hasattr(runner, "step_e2e_force") and cfg == 4 and runner.shard == "frames":
+        runner.step_e2e_force()
+        ms_f = timed(runner.step_e2e_force, args.steps)
+        h2f, d2f = runner.e2e_bytes(force=True)
+        e2e_force = {"value": None, "ms_per_step": ms_f, "h2d_bytes_per_step": h2f * (world if runner.scaling == "weak" else 1),
+                     "d2h_bytes_per_step": d2f * (world if runner.scaling == "weak" else 1),
+                     "what": "evaluate(frames, grad=False, bias=HillStore): s, z, V and the metadynamics bias force "
+                             "F = -(dV/ds ds + dV/dz dz) [T, n, 3] from one fused int8 tensor-core contraction "
+                             "(SPEC bias_and_force), all copied back to pinned host memory"}
     # live per-kernel timing: CUDA events around each launch on the launch stream
     nprof = max(1, min(args.steps, 2))
     _lib.start_profile()
@@ -700,9 +793,12 @@ def run_ours(args, rank, world, local_rank):
     elif kind == "fp64_tensor_flop":
         ach = amount / (step_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TF, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TF,
-                "peak_src": "fp64 tensor cores (DMMA.8x8x4) measured on this pool's B200: 36.8 TF/s "
-                            "(tools/_diag/dmma_probe.cu; MEASURED_PEAKS.json has no fp64 figure)",
+                "peak_src": "fp64 tensor cores (DMMA.8x8x4) measured on this pool's B200: 36.2 TF/s "
+                            "(profiles/r02_dmma_probe_b200.txt from tools/_diag/dmma_probe.cu; "
+                            "MEASURED_PEAKS.json has no fp64 figure)",
                 "flop_basis": "useful fp64 flops (significant / window pairs); executed includes window-union padding"}
+    elif kind == "int8_tensor_op":
+        roof = _int8_roof(amount, step_ms, pk)
     else:
         ach = amount / (step_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,
@@ -713,11 +809,26 @@ def run_ours(args, rank, world, local_rank):
                  "traffic_src": "profiles/traffic.json (ncu --set full, same workload)" if traffic else None})
     kernels = {k: {"launches": c, "ms_per_step": t / nprof, "share": t / total}
                for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    # the gradient contraction's own roofline (int8 tensor pipe) when it is not the top kernel
+    roof_grad = None
+    if name != "mc_pathcv_grad_i8" and "mc_pathcv_grad_i8" in prof:
+        gk, gamount = runner.kernel_work("mc_pathcv_grad_i8")
+        gc, gt = prof["mc_pathcv_grad_i8"]
+        if gk == "int8_tensor_op":
+            roof_grad = _int8_roof(gamount, gt / nprof, pk)
+            roof_grad.update({"kernel": "mc_pathcv_grad_i8", "share_of_step": gt / total, "avg_launch_ms": gt / gc})
     units = runner.units() * world if runner.scaling == "weak" else runner.units()
     if dist and runner.scaling == "strong" and not getattr(runner, "replicated_units", False):
         t = torch.tensor([float(units)], device=device, dtype=torch.float64)
         dist.all_reduce(t)
         units = float(t.item())
+    # bytes per step of the whole job: every rank copies its own frames and results
+    h2d_tot, d2h_tot = h2d * world, d2h * world
+    if e2e_force is not None:
+        e2e_force["value"] = units / (e2e_force["ms_per_step"] * 1e-3)
+        e2e_force["unit"] = runner.unit
+        e2e_force["h2d_bytes_per_step"] *= world
+        e2e_force["d2h_bytes_per_step"] *= world
     line = {
         "metric": runner.metric, "value": units / (ms * 1e-3), "unit": runner.unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -726,10 +837,17 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": CONFIG_NAMES[cfg], "frames_per_rank": runner.T, "landmarks": runner.L,
                    "atoms": runner.n, "parallelism": runner.parallelism,
                    "l2": "working set > L2 (126 MB): frames/operands re-read from HBM every step"},
-        "e2e": {"value": units / (ms_e2e * 1e-3), "unit": runner.unit, "h2d_bytes_per_step": h2d * world,
-                "d2h_bytes_per_step": d2h * world, "ms_per_step": ms_e2e},
+        "e2e": {"value": units / (ms_e2e * 1e-3), "unit": runner.unit,
+                "h2d_bytes_per_step": h2d_tot,
+                "d2h_bytes_per_step": d2h_tot, "ms_per_step": ms_e2e,
+                "what": "the public API with pinned host frames: chunked H2D, evaluate(), and the whole result "
+                        "(config 4: ds, dz, s, z; config 2: the MSD matrix) back to pinned host memory"},
         "gpu_launches": launches, "clocks": clocks, "roofline": roof, "kernels": kernels,
     }
+    if e2e_force is not None:
+        line["e2e_bias_force"] = e2e_force
+    if roof_grad is not None:
+        line["roofline_gradient"] = roof_grad
     line["config"].update(runner.extra())
     if cfg == 4 and getattr(runner, "last", None) is not None and "window_cnt" in runner.last:
         # the BASELINE metric's other half: aligned-MSD pairs/s of the same step -- every
@@ -737,9 +855,11 @@ def run_ours(args, rank, world, local_rank):
         # the window pairs are refit exactly in fp64
         exact = float(runner.last["window_cnt"].double().sum().item()) * (world if runner.scaling == "weak" else 1)
         line["aligned_msd_pairs_per_s"] = {
-            "covered": units * runner.L / (ms * 1e-3), "exact_fp64_refits": exact / (ms * 1e-3),
-            "note": "covered = T x L pairs per step (one-term tensor-core screen with a rigorous bound, metric "
-                    "pruning); exact = window pairs refit in fp64 (those that reach s, z and the gradients)"}
+            "value": exact / (ms * 1e-3), "unit": "pairs/s",
+            "what": "exact fp64 aligned MSDs per second: the window pairs refit in fp64 (those that reach s, z and "
+                    "the gradients); every other (frame, landmark) pair is excluded by the certified one-term "
+                    "screen bound or the metric pruning, not computed",
+            "screened_pairs_per_s": units * runner.L / (ms * 1e-3)}
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, runner, args)
     if rank == 0:
@@ -773,12 +893,14 @@ def cpu_baseline(cfg, runner, args, seconds=12.0):
     else:
         frames = wl.frames[:256].double().cpu().numpy()
     fn = _cpu_fn(cfg, wl)
-    k = min(frames.shape[0], 4 if cfg in (2, 4) else (16 if cfg == 3 else 64))
+    # a first small sample, then one sized to ~`seconds` of CPU work; oracle/c runs the
+    # (frame, landmark) fits in parallel over pairs, so every thread is busy either way
+    k = min(frames.shape[0], 2 if cfg in (2, 4) else (16 if cfg == 3 else 64))
     t0 = time.perf_counter()
     fn(frames[:k])
     dt = time.perf_counter() - t0
-    if cfg in (0, 1, 3):
-        k2 = int(min(frames.shape[0], max(k, k * seconds / max(dt, 1e-6))))
+    k2 = int(min(frames.shape[0], max(k, k * seconds / max(dt, 1e-6))))
+    if k2 > k:
         t0 = time.perf_counter()
         fn(frames[:k2])
         dt = time.perf_counter() - t0
@@ -813,7 +935,7 @@ def run_reference(args, rank, world):
         L, n = 2048, 2500
     else:
         shp = CONFIG_SHAPES[cfg]
-        rng_frames = 16 if cfg == 2 else 4
+        rng_frames = 16  # >= the host's cores worth of frames per step (fits run in parallel over pairs)
         wl = _host_sample(cfg, rng_frames)
         sample = wl.frames
         L, n = wl.landmarks.shape[0], shp["N"]

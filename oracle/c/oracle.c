@@ -151,22 +151,24 @@ static int set_threads(int nthreads) {
 
 int oc_max_threads(void) { return set_threads(0); }
 
-/* all-pairs MSD: frames [T,n,3], landmarks [L,n,3] (raw, fp64) -> D [T,L] */
+/* all-pairs MSD: frames [T,n,3], landmarks [L,n,3] (raw, fp64) -> D [T,L].
+ * Every structure is centred once, then the T x L fits run in parallel over PAIRS
+ * (not frames), so a small frame sample still keeps every host thread busy. */
 int oc_msd_matrix(const double* frames, const double* landmarks, int T, int L, int n, const double* w,
                   const double* wa, double* D, int nthreads) {
   const int used = set_threads(nthreads);
   double* lc = (double*)malloc(sizeof(double) * 3 * n * (size_t)L);
+  double* fc = (double*)malloc(sizeof(double) * 3 * n * (size_t)T);
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < L; ++i) center(landmarks + (size_t)i * 3 * n, n, wa, lc + (size_t)i * 3 * n);
-#pragma omp parallel
-  {
-    double* xc = (double*)malloc(sizeof(double) * 3 * n);
-#pragma omp for schedule(dynamic, 1)
-    for (int t = 0; t < T; ++t) {
-      center(frames + (size_t)t * 3 * n, n, wa, xc);
-      for (int i = 0; i < L; ++i) D[(size_t)t * L + i] = oc_fit(xc, lc + (size_t)i * 3 * n, w, n, NULL, NULL);
-    }
-    free(xc);
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < T; ++t) center(frames + (size_t)t * 3 * n, n, wa, fc + (size_t)t * 3 * n);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (long long e = 0; e < (long long)T * L; ++e) {
+    const int t = (int)(e / L), i = (int)(e % L);
+    D[e] = oc_fit(fc + (size_t)t * 3 * n, lc + (size_t)i * 3 * n, w, n, NULL, NULL);
   }
+  free(fc);
   free(lc);
   return used;
 }
@@ -323,68 +325,97 @@ int oc_close_replay(const double* frames, const double* landmarks, int T, int L,
   return used;
 }
 
-/* Alg. 1 path-CV: s, z [T]; ds, dz [T,n,3] (nullable) */
+/* Alg. 1 path-CV: s, z [T]; ds, dz [T,n,3] (nullable).
+ * Three parallel phases so every host thread is busy even for a handful of frames:
+ * (1) the T x L exact fits (geometry.py:227-249) in parallel over PAIRS, keeping D and R;
+ * (2) per frame the shifted softmax s, z (PAPER Eq. 2); (3) the
+ * gradients (Eq. 4 summed with the K4 coefficients) in parallel over (frame, atom block),
+ * each landmark's translation term sum_j 2 w_j d_j = 2 (Sx - R Sa) from per-structure sums. */
 int oc_path_cv_exact(const double* frames, const double* landmarks, int T, int L, int n, double lam, const double* q,
                      const double* w, const double* wa, double* s, double* z, double* ds, double* dz, int nthreads) {
   const int used = set_threads(nthreads);
   double* lc = (double*)malloc(sizeof(double) * 3 * n * (size_t)L);
-  for (int i = 0; i < L; ++i) center(landmarks + (size_t)i * 3 * n, n, wa, lc + (size_t)i * 3 * n);
-#pragma omp parallel
-  {
-    double* xc = (double*)malloc(sizeof(double) * 3 * n);
-    double* D = (double*)malloc(sizeof(double) * L);
-    double* R = (double*)malloc(sizeof(double) * 9 * (size_t)L);
-    double* gs = (double*)malloc(sizeof(double) * 3 * n);
-    double* gz = (double*)malloc(sizeof(double) * 3 * n);
-#pragma omp for schedule(dynamic, 1)
-    for (int t = 0; t < T; ++t) {
-      center(frames + (size_t)t * 3 * n, n, wa, xc);
-      double dmin = INFINITY;
-      for (int i = 0; i < L; ++i) {
-        D[i] = oc_fit(xc, lc + (size_t)i * 3 * n, w, n, R + 9 * (size_t)i, NULL);
-        if (D[i] < dmin) dmin = D[i];
-      }
-      double zs = 0, qs = 0;
-      for (int i = 0; i < L; ++i) {
-        const double e = exp(-lam * (D[i] - dmin));
-        zs += e;
-        qs += q[i] * e;
-      }
-      const double sv = qs / zs;
-      s[t] = sv;
-      z[t] = dmin - log(zs) / lam;
-      if (ds) {
-        memset(gs, 0, sizeof(double) * 3 * n);
-        memset(gz, 0, sizeof(double) * 3 * n);
-        for (int i = 0; i < L; ++i) {
-          const double p = exp(-lam * (D[i] - dmin)) / zs;
-          const double cs = -lam * p * (q[i] - sv), cz = p;
-          const double* a = lc + (size_t)i * 3 * n;
-          const double* r = R + 9 * (size_t)i;
-          double sum[3] = {0, 0, 0};
-          for (int j = 0; j < n; ++j) {
-            double d[3];
-            for (int b = 0; b < 3; ++b)
-              d[b] = xc[3 * j + b] - (r[3 * b] * a[3 * j] + r[3 * b + 1] * a[3 * j + 1] + r[3 * b + 2] * a[3 * j + 2]);
-            for (int b = 0; b < 3; ++b) {
-              const double g = 2.0 * w[j] * d[b];
-              sum[b] += g;
-              gs[3 * j + b] += cs * g;
-              gz[3 * j + b] += cz * g;
-            }
-          }
-          for (int j = 0; j < n; ++j)
-            for (int b = 0; b < 3; ++b) {
-              gs[3 * j + b] -= cs * wa[j] * sum[b];
-              gz[3 * j + b] -= cz * wa[j] * sum[b];
-            }
-        }
-        memcpy(ds + (size_t)t * 3 * n, gs, sizeof(double) * 3 * n);
-        memcpy(dz + (size_t)t * 3 * n, gz, sizeof(double) * 3 * n);
-      }
-    }
-    free(xc); free(D); free(R); free(gs); free(gz);
+  double* fc = (double*)malloc(sizeof(double) * 3 * n * (size_t)T);
+  double* D = (double*)malloc(sizeof(double) * (size_t)T * L);
+  double* R = (double*)malloc(sizeof(double) * 9 * (size_t)T * L);
+  double* Sa = (double*)malloc(sizeof(double) * 3 * (size_t)L);
+  double* Sx = (double*)malloc(sizeof(double) * 3 * (size_t)T);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < L; ++i) {
+    double* a = lc + (size_t)i * 3 * n;
+    center(landmarks + (size_t)i * 3 * n, n, wa, a);
+    double acc[3] = {0, 0, 0};
+    for (int j = 0; j < n; ++j)
+      for (int b = 0; b < 3; ++b) acc[b] += w[j] * a[3 * j + b];
+    for (int b = 0; b < 3; ++b) Sa[3 * i + b] = acc[b];
   }
-  free(lc);
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < T; ++t) {
+    double* x = fc + (size_t)t * 3 * n;
+    center(frames + (size_t)t * 3 * n, n, wa, x);
+    double acc[3] = {0, 0, 0};
+    for (int j = 0; j < n; ++j)
+      for (int b = 0; b < 3; ++b) acc[b] += w[j] * x[3 * j + b];
+    for (int b = 0; b < 3; ++b) Sx[3 * t + b] = acc[b];
+  }
+  /* (1) fits */
+#pragma omp parallel for schedule(dynamic, 16)
+  for (long long e = 0; e < (long long)T * L; ++e) {
+    const int t = (int)(e / L), i = (int)(e % L);
+    D[e] = oc_fit(fc + (size_t)t * 3 * n, lc + (size_t)i * 3 * n, w, n, R + 9 * (size_t)e, NULL);
+  }
+  /* (2) softmax weights -> s, z; D is overwritten with the coefficient p_i */
+  double* cs = (double*)malloc(sizeof(double) * (size_t)T * L);
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < T; ++t) {
+    double* Dt = D + (size_t)t * L;
+    double dmin = INFINITY;
+    for (int i = 0; i < L; ++i)
+      if (Dt[i] < dmin) dmin = Dt[i];
+    double zs = 0, qs = 0;
+    for (int i = 0; i < L; ++i) {
+      const double e = exp(-lam * (Dt[i] - dmin));
+      zs += e;
+      qs += q[i] * e;
+    }
+    const double sv = qs / zs;
+    s[t] = sv;
+    z[t] = dmin - log(zs) / lam;
+    for (int i = 0; i < L; ++i) {
+      const double p = exp(-lam * (Dt[i] - dmin)) / zs;
+      cs[(size_t)t * L + i] = -lam * p * (q[i] - sv);
+      Dt[i] = p;
+    }
+  }
+  /* (3) gradients over (frame, block of 64 atoms) */
+  if (ds) {
+    const int AB = 64, nb = (n + AB - 1) / AB;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long long e = 0; e < (long long)T * nb; ++e) {
+      const int t = (int)(e / nb), j0 = (int)(e % nb) * AB, j1 = j0 + AB < n ? j0 + AB : n;
+      const double* xc = fc + (size_t)t * 3 * n;
+      double gs[3 * 64], gz[3 * 64];
+      memset(gs, 0, sizeof(gs));
+      memset(gz, 0, sizeof(gz));
+      for (int i = 0; i < L; ++i) {
+        const double c_s = cs[(size_t)t * L + i], c_z = D[(size_t)t * L + i];
+        const double* a = lc + (size_t)i * 3 * n;
+        const double* r = R + 9 * ((size_t)t * L + i);
+        double sum[3];
+        for (int b = 0; b < 3; ++b)
+          sum[b] = 2.0 * (Sx[3 * t + b] - (r[3 * b] * Sa[3 * i] + r[3 * b + 1] * Sa[3 * i + 1] + r[3 * b + 2] * Sa[3 * i + 2]));
+        for (int j = j0; j < j1; ++j)
+          for (int b = 0; b < 3; ++b) {
+            const double d = xc[3 * j + b] - (r[3 * b] * a[3 * j] + r[3 * b + 1] * a[3 * j + 1] + r[3 * b + 2] * a[3 * j + 2]);
+            const double g = 2.0 * w[j] * d - wa[j] * sum[b];
+            gs[3 * (j - j0) + b] += c_s * g;
+            gz[3 * (j - j0) + b] += c_z * g;
+          }
+      }
+      memcpy(ds + ((size_t)t * n + j0) * 3, gs, sizeof(double) * 3 * (j1 - j0));
+      memcpy(dz + ((size_t)t * n + j0) * 3, gz, sizeof(double) * 3 * (j1 - j0));
+    }
+  }
+  free(cs); free(Sx); free(Sa); free(R); free(D); free(fc); free(lc);
   return used;
 }

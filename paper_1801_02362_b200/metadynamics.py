@@ -73,6 +73,11 @@ class HillStore:
             raise ConfigError("hills are deposited in nondecreasing step order")
         c = torch.as_tensor(cv_values, dtype=F64).to(self.device).reshape(1, self.d)
         if self.grid is not None:
+            # a rejected deposit must leave the grid untouched (grid and direct V agree for
+            # every deposition history): check the centre before the kernel adds anything
+            ch = c.cpu().numpy().reshape(self.d)
+            if not ((ch >= self._lo) & (ch <= self._hi)).all():
+                raise OutOfGridError("hill centre outside the bias grid")
             g = self.grid
             lo, hi, bins = self._geom()
             call("mc_mtd_grid_deposit", ptr(g["val"]), ptr(g["d"]), ptr(g["dxy"]), self.d, lo, hi, bins, ptr(c),

@@ -94,8 +94,11 @@ def test_device_grid_matches_oracle_grid_and_direct(d, cuda_device):
     assert float((V - Vd).abs().max()) < 1e-4
     with pytest.raises(OutOfGridError):
         st.bias(torch.tensor([[1.5] * d], device=cuda_device))
+    before = st.grid["val"].clone()
     with pytest.raises(OutOfGridError):
         st.deposit(torch.tensor([2.0] * d), 5 * 60)
+    # a rejected deposit leaves the grid and the hill list unchanged
+    assert torch.equal(st.grid["val"], before) and st.centers.shape[0] == 60
 
 
 @pytest.mark.gpu
