@@ -264,6 +264,7 @@ def interp_config_device(seed, T, L, N, n_endpoints, device, frame_offset=0, fra
     frame_count = T - frame_offset if frame_count is None else frame_count
     ends_t = torch.from_numpy(ends).to(device=device, dtype=torch.float32)
     frames = torch.empty((frame_count, N, 3), dtype=torch.float32, device=device)
+    sigma = torch.empty((frame_count,), dtype=torch.float64, device=device)  # per-frame noise level
     n_seg = n_endpoints - 1
     for c0 in range(frame_offset - frame_offset % chunk, frame_offset + frame_count, chunk):
         g = torch.Generator(device=device).manual_seed(seed * 1_000_003 + c0 // chunk)
@@ -290,6 +291,8 @@ def interp_config_device(seed, T, L, N, n_endpoints, device, frame_offset=0, fra
         b = min(c0 + cn, frame_offset + frame_count)
         if b > a:
             frames[a - frame_offset: b - frame_offset] = blk[a - c0: b - c0]
+            sigma[a - frame_offset: b - frame_offset] = sig[a - c0: b - c0]
     wl.frames = frames
+    wl.sigma = sigma
     wl.meta["generator"] = "device (torch, per-chunk seeded)"
     return wl

@@ -109,12 +109,26 @@ def test_tf32_weighted(cuda_device):
     assert np.abs(est - ref).max() < 5e-6
 
 
-@pytest.mark.parametrize("T,L,n", [(128, 48, 16), (300, 100, 100), (257, 97, 1000), (64, 64, 4000)])
-def test_one_term_screen_within_rigorous_bound(T, L, n, cuda_device):
+def _same_sign(T, L, n, seed=21):
+    """Adversarial structures for the accumulation term of the bound: every coordinate
+    positive (all products of the one-term contraction add with the same sign, so the fp32
+    accumulation errors cannot cancel), frames close to the landmarks."""
+    rng = np.random.default_rng(seed)
+    base = rng.uniform(0.5, 1.5, size=(n, 3))
+    lms = (base[None] + rng.normal(0.0, 0.02, size=(L, n, 3))).astype(np.float32)
+    frs = (base[None] + rng.normal(0.0, 0.02, size=(T, n, 3))).astype(np.float32)
+    return synth._finish("same-sign", frs, lms)
+
+
+@pytest.mark.parametrize("T,L,n,kind", [(128, 48, 16, "path"), (300, 100, 100, "path"), (257, 97, 1000, "path"),
+                                        (64, 64, 4000, "path"), (48, 40, 10000, "path"),
+                                        (48, 40, 10000, "same-sign")])
+def test_one_term_screen_within_rigorous_bound(T, L, n, kind, cuda_device):
     """One-term FP16 estimate: |D_est - D| <= c(n) ||x_t|| ||w a_l|| for every pair
-    (the bound PathCVTC folds into each frame's window threshold)."""
+    (the bound PathCVTC folds into each frame's window threshold), up to the headline
+    n = 10000 and for all-positive coordinates (no cancellation of accumulation errors)."""
     dev = torch.device("cuda:0")
-    wl = synth.config2(seed=11, T=T, L=L, N=n)
+    wl = synth.config2(seed=11, T=T, L=L, N=n) if kind == "path" else _same_sign(T, L, n)
     pcv = engine.PathCVTC(wl.landmarks, wl.lam, screen="f16x1")
     est, _, fs = pcv.estimate(wl.frames, terms=1)
     est = est.cpu().numpy().astype(np.float64)
