@@ -97,6 +97,12 @@ int mc_fit_full(const double* S, int64_t P, const int32_t* xi, const int32_t* ai
 int mc_rot_grad(const double* xplanes, const double* aplanes, const int32_t* xi, const int32_t* ai, int64_t P,
                 int32_t n, int32_t npad, const double* w, const double* eig, double* out, void* stream);
 
+/* jacobi_eigh (geometry.py:106-153) for general symmetric n x n matrices (1 <= n <= 48),
+ * mats [B, n, n] row-major, any tolerance / sweep limit: vals [B, n] ascending, vecs
+ * [B, n, n] (columns = eigenvectors, largest-|component| positive), flags [B]
+ * (MC_FLAG_NO_CONVERGE when max_sweeps were not enough: geometry.py:144-145). */
+int mc_jacobi_n(const double* mats, int64_t B, int32_t n, double tol, int32_t max_sweeps, double* vals, double* vecs,
+                uint8_t* flags, void* stream);
 /* jacobi_eigh (geometry.py:106-153) on B symmetric 4x4 matrices [B,16]:
  * vals [B,4] ascending, vecs [B,16] row-major. */
 int mc_jacobi4(const double* mats, int64_t B, double* vals, double* vecs, uint8_t* flags, void* stream);

@@ -49,6 +49,7 @@ _SIGS = {
     "mc_fit_full": [_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "mc_rot_grad": [_P, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _P],
     "mc_jacobi4": [_P, _I64, _P, _P, _P, _P],
+    "mc_jacobi_n": [_P, _I64, _I32, _D, _I32, _P, _P, _P, _P],
     "mc_window_pairs": [_I32, _I32, _I32, _P, _P, _P],
     "mc_close_scan": [_P, _P, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P, _P, _P],
     "mc_xy_eig": [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P],

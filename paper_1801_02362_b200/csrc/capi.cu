@@ -63,6 +63,13 @@ int mc_rot_grad(const double* xplanes, const double* aplanes, const int32_t* xi,
   return cuda_status(mc::launch_rot_grad(xplanes, aplanes, xi, ai, P, n, npad, w, eig, out, S_(stream)));
 }
 
+int mc_jacobi_n(const double* mats, int64_t B, int32_t n, double tol, int32_t max_sweeps, double* vals, double* vecs,
+                uint8_t* flags, void* stream) {
+  if (B < 0 || n < 1 || n > 48 || max_sweeps < 0 || !(tol >= 0.0)) return MC_ERR_CONFIG;
+  if (B > 0 && (!mats || !vals || !vecs)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_jacobi_n(mats, B, n, tol, max_sweeps, vals, vecs, flags, S_(stream)));
+}
+
 int mc_jacobi4(const double* mats, int64_t B, double* vals, double* vecs, uint8_t* flags, void* stream) {
   if (B < 0 || (B > 0 && (!mats || !vals || !vecs))) return MC_ERR_CONFIG;
   return cuda_status(mc::launch_jacobi4(mats, B, vals, vecs, flags, S_(stream)));

@@ -224,4 +224,112 @@ cudaError_t launch_jacobi4(const double* mats, int64_t B, double* vals, double* 
   return cudaGetLastError();
 }
 
+// jacobi_eigh (geometry.py:106-153) for a general symmetric n x n matrix, one
+// CTA per matrix (n <= 48): the same cyclic sweep order, rotation formula, tolerance floor
+// max(tol, 4e-16 ||A||_F), stable ascending sort and largest-|component|-positive sign
+// rule; each rotation updates the columns / rows / eigenvector columns with one thread per
+// element (c x - s y without FMA contraction, as the reference's numpy expressions).
+constexpr int kJnMax = 48;
+__global__ void __launch_bounds__(kJnMax)
+jacobi_n_kernel(const double* __restrict__ mats, int n, double tol, int max_sweeps, double* __restrict__ vals,
+                double* __restrict__ vecs, uint8_t* __restrict__ flags) {
+  __shared__ double a[kJnMax][kJnMax + 1], v[kJnMax][kJnMax + 1];
+  __shared__ double red[kJnMax];
+  __shared__ int s_done;
+  const int b = blockIdx.x, k = threadIdx.x;
+  const double* m = mats + (int64_t)b * n * n;
+  for (int i = 0; i < n; ++i)
+    if (k < n) {
+      a[i][k] = m[i * n + k];
+      v[i][k] = i == k ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  // Frobenius norm for the tolerance floor
+  double fr = 0.0;
+  if (k < n)
+    for (int i = 0; i < n; ++i) fr = __fma_rn(a[i][k], a[i][k], fr);
+  red[k] = fr;
+  __syncthreads();
+  if (k == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += red[i];
+    red[0] = fmax(tol, 4e-16 * sqrt(t));
+  }
+  __syncthreads();
+  const double tl = red[0];
+  __syncthreads();
+  int converged = 0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    double off = 0.0;
+    if (k < n)
+      for (int i = 0; i < n; ++i)
+        if (i != k) off = __fma_rn(a[i][k], a[i][k], off);
+    red[k] = off;
+    __syncthreads();
+    if (k == 0) {
+      double t = 0.0;
+      for (int i = 0; i < n; ++i) t += red[i];
+      s_done = sqrt(t) < tl;
+    }
+    __syncthreads();
+    if (s_done) { converged = 1; break; }
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a[p][q];
+        __syncthreads();
+        if (apq == 0.0) continue;  // uniform
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+        const double t = copysign(1.0, theta) / (fabs(theta) + hypot(theta, 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        if (k < n) {  // columns p, q
+          const double xp = a[k][p], xq = a[k][q];
+          a[k][p] = __dsub_rn(__dmul_rn(c, xp), __dmul_rn(sn, xq));
+          a[k][q] = __dadd_rn(__dmul_rn(sn, xp), __dmul_rn(c, xq));
+        }
+        __syncthreads();
+        if (k < n) {  // rows p, q
+          const double xp = a[p][k], xq = a[q][k];
+          a[p][k] = __dsub_rn(__dmul_rn(c, xp), __dmul_rn(sn, xq));
+          a[q][k] = __dadd_rn(__dmul_rn(sn, xp), __dmul_rn(c, xq));
+          const double vp = v[k][p], vq = v[k][q];
+          v[k][p] = __dsub_rn(__dmul_rn(c, vp), __dmul_rn(sn, vq));
+          v[k][q] = __dadd_rn(__dmul_rn(sn, vp), __dmul_rn(c, vq));
+        }
+        __syncthreads();
+        if (k == 0) a[p][q] = a[q][p] = 0.0;
+        __syncthreads();
+      }
+  }
+  __syncthreads();
+  if (k == 0) {
+    // stable ascending sort of the diagonal (insertion sort keeps equal keys in order)
+    int ord[kJnMax];
+    for (int i = 0; i < n; ++i) ord[i] = i;
+    for (int i = 1; i < n; ++i) {
+      const int o = ord[i];
+      int j = i - 1;
+      while (j >= 0 && a[ord[j]][ord[j]] > a[o][o]) { ord[j + 1] = ord[j]; --j; }
+      ord[j + 1] = o;
+    }
+    for (int j = 0; j < n; ++j) {
+      const int c = ord[j];
+      vals[(int64_t)b * n + j] = a[c][c];
+      int im = 0;
+      for (int i = 1; i < n; ++i)
+        if (fabs(v[i][c]) > fabs(v[im][c])) im = i;  // first maximum, like np.argmax
+      const double sg = v[im][c] < 0.0 ? -1.0 : 1.0;
+      for (int i = 0; i < n; ++i) vecs[((int64_t)b * n + i) * n + j] = sg * v[i][c];
+    }
+    if (flags) flags[b] = converged ? 0 : kFlagNoConverge;
+  }
+}
+
+cudaError_t launch_jacobi_n(const double* mats, int64_t B, int n, double tol, int max_sweeps, double* vals,
+                            double* vecs, uint8_t* flags, cudaStream_t stream) {
+  if (B <= 0) return cudaSuccess;
+  if (n < 1 || n > kJnMax) return cudaErrorInvalidValue;
+  jacobi_n_kernel<<<(unsigned)B, kJnMax, 0, stream>>>(mats, n, tol, max_sweeps, vals, vecs, flags);
+  return cudaGetLastError();
+}
+
 }  // namespace mc

@@ -22,6 +22,8 @@ cudaError_t launch_fit_full(const double* S, int64_t P, const int* xi, const int
                             cudaStream_t stream);
 cudaError_t launch_rot_grad(const double* xpl, const double* apl, const int* xi, const int* ai, int64_t P, int n,
                             int npad, const double* w, const double* eig, double* out, cudaStream_t stream);
+cudaError_t launch_jacobi_n(const double* mats, int64_t B, int n, double tol, int max_sweeps, double* vals,
+                            double* vecs, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_jacobi4(const double* mats, int64_t B, double* vals, double* vecs, uint8_t* flags,
                            cudaStream_t stream);
 cudaError_t launch_window_pairs(int walkers, int steps, int K, int* xi, int* ai, cudaStream_t stream);

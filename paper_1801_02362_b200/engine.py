@@ -41,6 +41,7 @@ CLOSE_DMMA = os.environ.get("MC_CLOSE_DMMA", "1") == "1"
 # env MC_GRAD_I8=0 keeps the fp64 DMMA kernel for every group
 GRAD_I8 = os.environ.get("MC_GRAD_I8", "1") == "1"
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
+NB_MAX_L = 16384        # neighbour-list active-set bitmap capacity (csrc/pathcv.cu kNbMaxL)
 
 
 def normalise_weights(w, n, kind, device):
@@ -230,6 +231,9 @@ class PathCV:
             raise ConfigError("eps must be >= 0")
         if neighbours is not None and not (1 <= int(neighbours) <= self.L):
             raise ConfigError("neighbour list size must satisfy 1 <= M <= L")
+        if neighbours is not None and self.L > NB_MAX_L:
+            raise ConfigError(f"neighbour lists support up to {NB_MAX_L} landmarks (the active set is a "
+                              f"shared-memory bitmap in the K4 weights kernel); this set has {self.L}")
         if int(nl_stride) < 1:
             raise ConfigError("neighbour list stride must be >= 1")
         fr_in = _as_cuda(frames, self.device)

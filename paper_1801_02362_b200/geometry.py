@@ -117,16 +117,21 @@ class RotationFit:
 
 
 def jacobi_eigh(mat, tol=1e-14, max_sweeps=60):
-    """Cyclic-Jacobi eigen-decomposition (geometry.py:106-153) of a symmetric
-    4x4 matrix on the device (the only size the fit uses).  Returns ascending
-    eigenvalues and sign-normalised eigenvector columns."""
+    """Cyclic-Jacobi eigen-decomposition (geometry.py:106-153) of a symmetric matrix on
+    the device: the batched 4x4 kernel for the Kearsley form at the reference tolerances,
+    a general n x n kernel (n <= 48, any tol / max_sweeps) otherwise.  Returns ascending
+    eigenvalues and sign-normalised eigenvector columns; ValueError for a non-symmetric
+    input and RuntimeError when the sweeps do not converge, as the reference."""
     a = np.array(mat, dtype=float)
     n = a.shape[0]
-    if a.shape != (n, n) or not np.allclose(a, a.T, atol=1e-12 * max(1.0, np.abs(a).max())):
+    if a.ndim != 2 or a.shape != (n, n) or not np.allclose(a, a.T, atol=1e-12 * max(1.0, np.abs(a).max())):
         raise ValueError("jacobi_eigh expects a symmetric square matrix")
-    if n != 4 or tol != 1e-14 or max_sweeps != 60:
-        raise ConfigError("device jacobi_eigh supports the 4x4 Kearsley form with the reference tolerances")
-    vals, vecs, flags = K.jacobi4(torch.from_numpy(a.reshape(1, 16)).to(_device()))
+    if n == 4 and tol == 1e-14 and max_sweeps == 60:
+        vals, vecs, flags = K.jacobi4(torch.from_numpy(a.reshape(1, 16)).to(_device()))
+    elif 1 <= n <= 48:
+        vals, vecs, flags = K.jacobi_n(torch.from_numpy(a.reshape(1, n, n)).to(_device()), tol, max_sweeps)
+    else:
+        raise ConfigError("device jacobi_eigh supports matrices up to 48 x 48")
     if int(flags.item()) & FLAG_NO_CONVERGE:
         raise RuntimeError("Jacobi diagonalisation did not converge")
     return vals[0].cpu().numpy(), vecs[0].cpu().numpy()

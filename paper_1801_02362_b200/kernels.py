@@ -137,6 +137,17 @@ def rot_grad(xplanes, aplanes, n, npad, w, eig, xi=None, ai=None):
     return out
 
 
+def jacobi_n(mats, tol=1e-14, max_sweeps=60):
+    """mats [B, n, n] fp64 symmetric (CUDA) -> (vals [B, n], vecs [B, n, n], flags [B])."""
+    B, n = mats.shape[0], mats.shape[1]
+    vals = torch.empty((B, n), dtype=F64, device=mats.device)
+    vecs = torch.empty((B, n, n), dtype=F64, device=mats.device)
+    flags = torch.empty((B,), dtype=U8, device=mats.device)
+    call("mc_jacobi_n", ptr(mats.contiguous()), B, n, float(tol), int(max_sweeps), ptr(vals), ptr(vecs), ptr(flags),
+         stream_ptr())
+    return vals, vecs, flags
+
+
 def jacobi4(mats):
     mats = mats.contiguous()
     B = int(mats.shape[0])

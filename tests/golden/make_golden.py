@@ -13,6 +13,9 @@ Contents
                     centring for seeded pairs: N in {2..12, 22, 304}, random
                     and uniform weights, x == a, x = Q a, near-identical pairs.
 * ``jacobi.npz``    jacobi_eigh on random symmetric 4x4 matrices.
+* ``jacobi_n.npz``  jacobi_eigh on symmetric n x n matrices (n = 1..40, several
+                    tolerances / sweep limits); entries with ``conv`` = 0 raised
+                    RuntimeError (not enough sweeps).
 * ``misc.npz``      rotation_derivative_check on an 8-atom pair, the degenerate
                     2-atom case (DegenerateFitError) and error cases.
 * ``pathcv0.npz``   a config-0-shaped slice (8 frames x 20 landmarks x 22
@@ -108,6 +111,31 @@ def make_jacobi(rng):
         vecs.append(v)
     np.savez_compressed(os.path.join(HERE, "jacobi.npz"), mats=np.array(mats),
                         vals=np.array(vals), vecs=np.array(vecs))
+
+
+def make_jacobi_n(rng):
+    """General-size cases for the device jacobi_eigh: one flat array per field."""
+    sizes, tols, sweeps, mats, vals, vecs, conv = [], [], [], [], [], [], []
+    cases = [(n, 1e-14, 60) for n in (1, 2, 3, 5, 6, 7, 9, 12, 16, 20, 33, 40)]
+    cases += [(4, 1e-8, 60), (6, 1e-6, 60), (8, 1e-14, 2), (10, 1e-14, 1), (5, 0.0, 60)]
+    for n, tol, ms in cases:
+        b = rng.normal(size=(n, n)) * (10.0 ** rng.uniform(-2, 2))
+        m = b + b.T
+        try:
+            w, v = ref.jacobi_eigh(m, tol=tol, max_sweeps=ms)
+            ok = 1
+        except RuntimeError:
+            w, v, ok = np.zeros(n), np.zeros((n, n)), 0
+        sizes.append(n)
+        tols.append(tol)
+        sweeps.append(ms)
+        mats.append(m.ravel())
+        vals.append(w.ravel())
+        vecs.append(v.ravel())
+        conv.append(ok)
+    np.savez_compressed(os.path.join(HERE, "jacobi_n.npz"), sizes=np.array(sizes), tols=np.array(tols),
+                        sweeps=np.array(sweeps), conv=np.array(conv), mats=np.concatenate(mats),
+                        vals=np.concatenate(vals), vecs=np.concatenate(vecs))
 
 
 def make_misc(rng):
@@ -209,6 +237,7 @@ def main():
     rng = np.random.default_rng(20180107)
     n = make_fits(rng)
     make_jacobi(rng)
+    make_jacobi_n(np.random.default_rng(1234))
     make_misc(rng)
     make_pathcv0()
     k = make_close()

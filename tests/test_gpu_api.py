@@ -88,6 +88,26 @@ def test_jacobi_eigh_matches_reference(golden, cuda_device):
         G.jacobi_eigh(np.array([[1.0, 2.0], [0.0, 1.0]]))
 
 
+def test_jacobi_eigh_general_n_matches_reference(golden, cuda_device):
+    """geometry.jacobi_eigh for n != 4 and custom tol / max_sweeps (the general-n device
+    kernel) against the reference's own outputs, RuntimeError where the reference raised."""
+    g = golden("jacobi_n.npz")
+    o1 = o2 = 0
+    for n, tol, ms, ok in zip(g["sizes"], g["tols"], g["sweeps"], g["conv"]):
+        n, tol, ms = int(n), float(tol), int(ms)
+        m = g["mats"][o2:o2 + n * n].reshape(n, n)
+        v, u = g["vals"][o1:o1 + n], g["vecs"][o2:o2 + n * n].reshape(n, n)
+        o1, o2 = o1 + n, o2 + n * n
+        if not ok:
+            with pytest.raises(RuntimeError):
+                G.jacobi_eigh(m, tol=tol, max_sweeps=ms)
+            continue
+        w, vec = G.jacobi_eigh(m, tol=tol, max_sweeps=ms)
+        scale = max(1.0, np.abs(m).max())
+        np.testing.assert_allclose(w / scale, v / scale, atol=1e-12)
+        np.testing.assert_allclose(vec, u, atol=1e-8)
+
+
 def test_exact_distance_vs_oracle(cuda_device):
     rng = np.random.default_rng(10)
     n = 6

@@ -55,6 +55,33 @@ def test_jacobi_matches_reference(golden):
         np.testing.assert_allclose(u, vec, atol=1e-9)
 
 
+def _jacobi_n_cases(g):
+    """Unpack tests/golden/jacobi_n.npz (flat per-field arrays) into per-case tuples."""
+    o1 = o2 = 0
+    for n, tol, ms, ok in zip(g["sizes"], g["tols"], g["sweeps"], g["conv"]):
+        n = int(n)
+        m = g["mats"][o2:o2 + n * n].reshape(n, n)
+        v = g["vals"][o1:o1 + n]
+        u = g["vecs"][o2:o2 + n * n].reshape(n, n)
+        o1 += n
+        o2 += n * n
+        yield m, float(tol), int(ms), bool(ok), v, u
+
+
+def test_jacobi_general_n_matches_reference(golden):
+    """The oracle's jacobi_eigh on the reference's general-size cases (n = 1..40, custom
+    tolerances, sweep limits that make the reference raise RuntimeError)."""
+    for m, tol, ms, ok, v, u in _jacobi_n_cases(golden("jacobi_n.npz")):
+        if not ok:
+            with pytest.raises(RuntimeError):
+                O.jacobi_eigh(m, tol=tol, max_sweeps=ms)
+            continue
+        w, vec = O.jacobi_eigh(m, tol=tol, max_sweeps=ms)
+        scale = max(1.0, np.abs(m).max())
+        np.testing.assert_allclose(w / scale, v / scale, atol=1e-12)
+        np.testing.assert_allclose(vec, u, atol=1e-8)
+
+
 def test_misc_reference_cases(golden):
     g = golden("misc.npz")
     w = np.full(8, 1 / 8)
