@@ -15,7 +15,7 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 def header_symbols():
     with open(os.path.join(ROOT, "include", "mcb200.h")) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^int\s+(mc_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t)\s+(mc_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_expected_entry_points():
