@@ -300,11 +300,14 @@ class ConfigTC:
         self.shard = shard
         if shard.startswith("landmarks") and cfg != 4:
             raise SystemExit("--shard landmarks applies to config 4 (path-CV)")
-        if shard == "landmarks":
-            # the north_star's variant, frame-routed: rank g holds a
-            # landmark shard (48-landmark tile bounds) and its T/G home frames; frames are
-            # routed to the shards their admissible tiles live on, gradient rows come back
-            # home; strong scaling (total work fixed), each rank copies only its home frames
+        if shard in ("landmarks", "landmarks-routed"):
+            # the north_star's variant.  "landmarks": the survey's
+            # two-phase plan -- rank g screens its landmark shard for every frame (one
+            # all-gather of the frames' screening operand, O(T) minima / windows), then refits
+            # and differentiates its T/G home frames against the replicated landmarks;
+            # "landmarks-routed": frames routed to the shards their admissible tiles live on,
+            # gradient rows come back home.  Strong scaling (total work fixed), each rank
+            # copies only its home frames.
             from paper_1801_02362_b200 import dist as Dd
 
             T_all = shp["T"]
@@ -327,6 +330,8 @@ class ConfigTC:
         self._off, self._c0 = off, 0
         lms = torch.from_numpy(self.wl.landmarks).to(device)
         if shard == "landmarks":
+            self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q, shard=(rank, world), two_phase=True)
+        elif shard == "landmarks-routed":
             self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q, shard=(rank, world, Dd.tile_bounds(self.L, world)),
                                        route=True)
         else:
@@ -346,6 +351,12 @@ class ConfigTC:
             self.frames_host = self.frames_dev.cpu()
             self.host_kind = "pageable (pinning failed)"
         if shard == "landmarks":
+            self.parallelism = (f"landmark-sharded x{world}, two-phase (NCCL: one all-gather of the frames' one-term "
+                                "screening operand, all-reduce MIN of per-frame bounds, all-gather of per-shard "
+                                "windows; refits and gradients frame-sharded against replicated landmarks)")
+            self.scaling = "strong"
+            self.replicated_units = False
+        elif shard == "landmarks-routed":
             self.parallelism = (f"landmark-sharded x{world}, frame-routed (NCCL: frames to their shards, "
                                 "per-frame min/partials, gradient rows home)")
             self.scaling = "strong"
@@ -386,6 +397,9 @@ class ConfigTC:
             from paper_1801_02362_b200 import dist as Dd
 
             if self.shard == "landmarks":
+                # home offsets / totals of chunked calls follow from the gathered counts
+                steps = self.pcv.two_phase_steps(frames, None, None, grad=True)
+            elif self.shard == "landmarks-routed":
                 steps = self.pcv.routed_steps(frames, self._off + self._c0, self.T_all, grad=True)
             else:
                 steps = self.pcv.sharded_steps(frames, grad=True)
@@ -986,9 +1000,10 @@ def main():
     ap.add_argument("--frames", type=int, default=0, help="override T (configs 2/4) for quick runs")
     ap.add_argument("--walkers", type=int, default=0, help="override W (config 3) for quick runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
-    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks", "landmarks-replicated"],
-                    help="multi-GPU split of config 4: frames (weak, no collective) or landmarks (strong, NCCL; "
-                         "frame-routed, or with every frame replicated on every rank)")
+    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks", "landmarks-routed",
+                                                          "landmarks-replicated"],
+                    help="multi-GPU split of config 4: frames (strong, no collective) or landmarks (strong, NCCL; "
+                         "two-phase (default), frame-routed, or with every frame replicated on every rank)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -209,6 +209,17 @@ class DistComm:
     def exchange(self, ds, dz, z_parts):
         return exchange_owned_rows(ds, dz, z_parts, self.group)
 
+    def allgather_split(self, sp):
+        """All-gather of a frame Split (the one-term screening operand + per-frame scalars)
+        over the ranks, concatenated in rank order (ragged frame counts); returns
+        (Split, per-rank frame counts)."""
+        from .kernels import Split
+
+        counts = torch.tensor([sp.count], dtype=torch.int64, device=sp.hi.device)
+        allc = self.gather(counts).flatten().cpu().tolist()
+        return (concat_splits([_gather_ragged(self, x, allc, dim) for x, dim in _split_fields(sp)], sp, allc, Split),
+                allc)
+
     def alltoallv(self, fields):
         """fields: list of per-destination row blocks (same row counts across fields).
         Returns, per field, the list of blocks received from every source rank."""
@@ -224,6 +235,33 @@ class DistComm:
             out.append(_alltoall_rows([b.contiguous() for b in blocks], rc, shape, blocks[0].dtype,
                                       blocks[0].device, self.group))
         return out
+
+
+def _split_fields(sp):
+    """(tensor, frame dim) of every per-frame field of a Split (None fields skipped later)."""
+    return [(sp.hi, 1), (sp.lo, 1), (sp.scale, 0), (sp.opnorm, 0), (sp.rnorm, 0), (sp.centroid, 0), (sp.g, 0),
+            (sp.wbar, 0), (sp.mom, 0)]
+
+
+def _gather_ragged(comm, x, counts, dim):
+    """All-gather of [.., count_r, ..] blocks along `dim` (padded to the largest count)."""
+    if x is None:
+        return None
+    mx = max(counts)
+    if x.shape[dim] < mx:
+        pad_shape = list(x.shape)
+        pad_shape[dim] = mx - x.shape[dim]
+        x = torch.cat([x, torch.zeros(pad_shape, dtype=x.dtype, device=x.device)], dim=dim)
+    parts = comm.gather(x.contiguous())  # [G, ...]
+    return torch.cat([parts[r].narrow(dim, 0, c) for r, c in enumerate(counts)], dim=dim)
+
+
+def concat_splits(fields, like, counts, cls):
+    """Assemble the gathered Split (the order of _split_fields)."""
+    hi, lo, scale, opnorm, rnorm, centroid, g, wbar, mom = fields
+    flags = torch.zeros((sum(counts),), dtype=torch.uint8, device=like.hi.device)
+    return cls(hi.contiguous(), None if lo is None else lo.contiguous(), centroid, g, wbar, mom, flags, like.n,
+               like.kpad, scale, like.fmt, like.terms, opnorm, rnorm)
 
 
 def drive(steps, comm):
@@ -256,6 +294,17 @@ def drive_lockstep(steps_list, lam=None):
         elif op == "gather":
             v = torch.stack([r[1] for r in reqs])
             outs = [v for _ in range(G)]
+        elif op == "allgather_split":
+            from .kernels import Split
+
+            sps = [r[1] for r in reqs]
+            counts = [sp.count for sp in sps]
+            fields = []
+            for k, (_, dim) in enumerate(_split_fields(sps[0])):
+                xs = [_split_fields(sp)[k][0] for sp in sps]
+                fields.append(None if xs[0] is None else torch.cat(xs, dim=dim))
+            v = concat_splits(fields, sps[0], counts, Split)
+            outs = [(v, counts) for _ in range(G)]
         elif op == "alltoallv":
             nf = len(reqs[0][1])
             outs = [[[reqs[g][1][f][h] for g in range(G)] for f in range(nf)] for h in range(G)]

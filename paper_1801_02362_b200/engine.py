@@ -417,7 +417,8 @@ class PathCVTC:
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None, route=False):
+                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None, route=False,
+                 two_phase=False):
         """shard = (rank, world[, bounds]): landmark-sharded evaluation.
         ``landmarks`` (and q) are the FULL set; this engine keeps the contiguous landmarks
         [bounds[rank], bounds[rank + 1]) -- default shard_range(L, rank, world); work-
@@ -428,7 +429,11 @@ class PathCVTC:
         DESIGN.md section 7): bounds at multiples of the 48-landmark tile; the engine also
         keeps the GLOBAL coarse screen (coarse landmarks, tile tables) so each rank screens
         only its home frames and routes every frame to the shards its admissible tiles
-        live on; evaluate with ``evaluate_routed`` / ``routed_steps``."""
+        live on; evaluate with ``evaluate_routed`` / ``routed_steps``.  two_phase=True (the
+        survey's two-phase plan): this engine screens its landmark shard
+        for every frame (phase 1) and also keeps the FULL landmark set (``self._full``,
+        unpruned) for the exact refits, weights and gradients of the rank's home frames
+        (phase 2); evaluate with ``evaluate_two_phase`` / ``two_phase_steps``."""
         K.require_cuda()
         self.fmt = operand_fmt or K.OPERAND_FMT
         self.screen = screen or (SCREEN if self.fmt == "f16" else "split")
@@ -455,6 +460,12 @@ class PathCVTC:
             raise ConfigError("q must have one value per landmark")
         self.shard = None
         self._gprune = None
+        self._full = None
+        if shard is not None and two_phase:
+            if route:
+                raise ConfigError("two_phase and route are alternative landmark-sharded schemes")
+            self._full = PathCVTC(lm, lam, q, w, w_align, cutoff, window_cap, device, operand_fmt, screen, False,
+                                  coarse_stride, knear)
         if shard is not None and route:
             g = PathCVTC(lm, lam, q, w, w_align, cutoff, window_cap, device, operand_fmt, screen, True,
                          coarse_stride, knear)
@@ -1005,6 +1016,125 @@ class PathCVTC:
                 ds.index_add_(0, home_rows, back[1][r])
                 dz.index_add_(0, home_rows, back[2][r])
         out.update(ds=ds, dz=dz)
+        return out
+
+
+    # ------------------------------------------------------------ two-phase landmark sharding
+
+    def evaluate_two_phase(self, frames, home_offset, t_total, grad=True, out_dtype=torch.float32, comm=None):
+        """Two-phase landmark-sharded evaluate over a torch.distributed group: this rank
+        passes its HOME frames (global rows [home_offset, home_offset + len); None: the
+        ranks' home frames concatenated in rank order) and gets back their s, z and complete
+        ds, dz (frame-sharded outputs)."""
+        from . import dist as Dd
+        return Dd.drive(self.two_phase_steps(frames, home_offset, t_total, grad, out_dtype), comm or Dd.DistComm())
+
+    def two_phase_steps(self, frames, home_offset, t_total, grad=True, out_dtype=torch.float32):
+        """Generator of the survey's two-phase plan.
+
+        Phase 1 -- landmark-sharded screen: ("allgather_split") the one-term split of every
+        rank's home frames (one all-gather: each rank then holds the screening operand of
+        all T frames); the metric-pruned one-term screen of all T frames against this
+        rank's landmark shard, with ("min") the global D_min upper bound for the pruning and
+        ("min") the global estimate minimum for the windows; each shard's window of every
+        frame (global landmark indices) goes to every rank in one ("gather").  The window
+        of a frame is the hull of its per-shard windows -- the unsharded window, since
+        every shard selects against the same global threshold.
+        Phase 2 -- frame-sharded exact work on the home frames against the replicated
+        landmark set: fp64 refits of the windows, the K4 softmax (complete: the window
+        holds every significant landmark), and the int8 tensor-core gradient contraction.
+        No further collective; the collectives move O(T) scalars plus the frames' screening
+        operand once."""
+        if self._full is None or self.shard is None:
+            raise ConfigError("two_phase_steps needs PathCVTC(..., shard=(rank, world[, bounds]), two_phase=True)")
+        rank, world, off, cnt_l = self.shard
+        full = self._full
+        dev = self.device
+        one = self.screen == "f16x1"
+        frh, fsh = self._frames(frames, 1, check=False)
+        Th = frh.shape[0]
+        # ---- phase 1: screen all frames against this landmark shard
+        fs_all, counts = yield ("allgather_split", fsh)
+        T = fs_all.count
+        if t_total is not None and T != int(t_total):
+            raise ConfigError(f"gathered {T} frames, expected {t_total}")
+        if home_offset is None:  # the ranks' home frames in rank order
+            home_offset = int(sum(counts[:rank]))
+        rlo = rhi = perm0 = None
+        if self.prune:
+            Dc = K.msd_estimate(fs_all, self.ls_coarse, grid=K2_GRID)
+            dub = K.screen_bound(Dc, fs_all.opnorm, self.ls_coarse.opnorm, self.kacc, fs_all.rnorm,
+                                 self.ls_coarse.rnorm)
+            dub = yield ("min", dub)
+            hlo, hhi, key = K.prune_plan(Dc, fs_all.opnorm, self.ls_coarse.opnorm, self.kacc, self.mind,
+                                         (self.cutoff + 2.0) / self.lam, self.knear, maxd=self.maxd,
+                                         cstride=self.cstride, frnorm=fs_all.rnorm, crnorm=self.ls_coarse.rnorm,
+                                         dub_in=dub)
+            del Dc
+            ntl = self.mind.shape[1]
+            perm0 = K.sort_by_key(key, ntl + 1)
+            fs = K.gather_split(fs_all, perm0)
+            tlist, nlist, rlo, rhi = K.band_tiles(perm0, hlo, hhi, 128, 48, self.L, ntl)
+            Dest = torch.empty((T, self.L), dtype=torch.float32, device=dev)
+            K.msd_estimate(fs, self.ls, Dest, grid=K2_GRID, tlist=tlist, nlist=nlist)
+        else:
+            fs = fs_all
+            Dest = K.msd_estimate(fs, self.ls)
+        fnorm = self.frame_bound(fs) if one else None
+        fcoef = 2.0 * self.lam if one else 0.0
+        _, _, dmin, _ = K.candidates(Dest, self.lam, self.cutoff + self.margin, 1, fnorm=fnorm, fcoef=fcoef,
+                                     rlo=rlo, rhi=rhi)
+        p = perm0.long() if perm0 is not None else None
+        if p is not None:
+            dm = torch.empty_like(dmin)
+            dm[p] = dmin
+            dmin = dm
+        dref = yield ("min", dmin)
+        if p is not None:
+            dref = dref[p].contiguous()
+        lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, self.L, fnorm=fnorm,
+                                          fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
+        del Dest
+        if p is not None:  # back to frame order
+            lo_f, cnt_f = torch.empty_like(lo), torch.empty_like(cnt)
+            lo_f[p], cnt_f[p] = lo, cnt
+            lo, cnt = lo_f, cnt_f
+        win = torch.stack([lo + off, cnt]).to(torch.int32)
+        parts = yield ("gather", win)  # [G, 2, T]: every shard's window of every frame
+        glo, gcnt = parts[:, 0].long(), parts[:, 1].long()
+        act = gcnt > 0
+        big = torch.iinfo(torch.int64).max
+        lo_t = torch.where(act, glo, torch.full_like(glo, big)).amin(0)
+        hi_t = torch.where(act, glo + gcnt, torch.full_like(glo, -1)).amax(0)
+        sl = slice(home_offset, home_offset + Th)
+        lo_h = lo_t[sl].clamp(max=full.L).to(torch.int32).contiguous()
+        cnt_h = (hi_t[sl] - lo_t[sl]).clamp(min=0).to(torch.int32).contiguous()
+        # ---- phase 2: exact refits, weights and gradients of the home frames, all landmarks
+        cap = int(max(1, min(full.L, int(cnt_h.max().item()) if Th else 1)))
+        perm = K.sort_by_key((2 * lo_h + cnt_h).to(torch.int32), 2 * full.L + 1)
+        Dex, Rex, rflags = K.refine(frh, fsh, full.lraw, full.ls, full.w, perm=perm, lo=lo_h, cnt=cnt_h, cap=cap,
+                                    wuni=full.wuni)
+        wres = K.pathcv_weights(Dex, full.q, full.lam, Rex, fsh, full.ls, cap, full.cutoff, L=full.L, rowlo=lo_h,
+                                rowcnt=cnt_h)
+        out = {"s": wres["s"], "z": wres["z"], "window_lo": lo_h, "window_cnt": cnt_h, "nsig": wres["nsig"],
+               "D_window": Dex}
+        if grad:
+            gperm = K.sort_by_key(K.sig_span_key(wres, full.L), 2 * full.L + 1)
+            out["ds"], out["dz"] = K.pathcv_grad_block(wres, fsh, full.ls, frh, full.lraw, full.w, full.wa, cap, gperm,
+                                                       out_dtype, ldig=full.ldig)
+        status = torch.stack([_flag_bits_dev(fsh.flags), _flag_bits_dev(cflags), _flag_bits_dev(rflags),
+                              _flag_bits_dev(wres["flags"])])
+        ff, cf, rf, wf = (_bits_value(r) for r in status.cpu().tolist())
+        if ff & FLAG_NON_FINITE:
+            raise InvalidStructureError("frame coordinates contain non-finite values")
+        if rf & FLAG_NON_FINITE:
+            raise InvalidStructureError("path_cv refine: non-finite coordinates or distances")
+        if rf & FLAG_NO_CONVERGE:
+            raise MetadynError("path_cv refine: Jacobi diagonalisation did not converge")
+        if wf & FLAG_NON_FINITE:
+            raise InvalidStructureError("non-finite distances in the path-CV reduction")
+        if Th and bool((cnt_h == 0).any()):
+            raise EmptyActiveSetError("a frame has no landmark in any shard's window")
         return out
 
 

@@ -259,3 +259,78 @@ def test_tile_bounds():
     assert b == [0, 528, 1056, 1536] or all(x % 48 == 0 for x in b[:-1])
     b = D.tile_bounds(1000, 4)
     assert b[0] == 0 and b[-1] == 1000 and all(x % 48 == 0 for x in b[:-1])
+
+
+def _two_phase(rank, world):
+    """The two-phase landmark-sharded protocol (PathCVTC.two_phase_steps) with the oracle's
+    exact distances standing in for the device screen: ragged all-gather of the frames'
+    screening operand (DistComm.allgather_split), all-reduce MIN of the per-frame minimum,
+    all-gather of every shard's windows, hull merge, phase-2 exact path CV of the home
+    frames over the merged windows."""
+    from paper_1801_02362_b200.kernels import Split
+
+    wl = synth.config0(seed=23, T=7, L=16, N=9)
+    T, L, n = wl.frames.shape[0], wl.landmarks.shape[0], wl.frames.shape[1]
+    comm = D.DistComm()
+    off, cnt = D.shard_range(T, rank, world)
+    b = D.balanced_bounds(torch.ones(L), world)
+    l0, l1 = b[rank], b[rank + 1]
+    # the home frames' "split": coordinates as halves in plane-major [3, count, n] + scalars
+    home = wl.frames[off:off + cnt]
+    hi = torch.from_numpy(np.ascontiguousarray(home.transpose(2, 0, 1))).half()
+    sc = torch.from_numpy(np.arange(off, off + cnt, dtype=np.float64))
+    sp = Split(hi, None, sc[:, None].repeat(1, 3), sc, sc[:, None].repeat(1, 3), None,
+               torch.zeros(cnt, dtype=torch.uint8), n, n, sc, "f16", 1, sc, sc)
+    allsp, counts = comm.allgather_split(sp)
+    assert counts == [D.shard_range(T, r, world)[1] for r in range(world)]
+    got_hi = allsp.hi.float().numpy().transpose(1, 2, 0)
+    assert allsp.count == T and np.array_equal(allsp.g.numpy(), np.arange(T, dtype=np.float64))
+    assert np.array_equal(got_hi, wl.frames.astype(np.float16).astype(np.float32))
+    # phase 1: every frame against this landmark shard
+    fc = O.batch_center(wl.frames, np.full(n, 1.0 / n))
+    lc = O.batch_center(wl.landmarks, np.full(n, 1.0 / n))
+    Dsh = O.batch_fit(fc[:, None], lc[None, l0:l1], np.full(n, 1.0 / n))[0][..., 0]  # [T, l1 - l0]
+    dmin = comm.min(torch.from_numpy(Dsh.min(axis=1)))
+    thr = 12.0
+    lo = np.zeros(T, dtype=np.int32)
+    cn = np.zeros(T, dtype=np.int32)
+    for t in range(T):
+        ok = np.nonzero(wl.lam * (Dsh[t] - dmin[t].item()) <= thr)[0]
+        if ok.size:
+            lo[t], cn[t] = l0 + ok[0], ok[-1] - ok[0] + 1
+    parts = comm.gather(torch.from_numpy(np.stack([lo, cn])))
+    glo, gcn = parts[:, 0].long(), parts[:, 1].long()
+    act = gcn > 0
+    lo_t = torch.where(act, glo, torch.full_like(glo, 1 << 40)).amin(0).numpy()
+    hi_t = torch.where(act, glo + gcn, torch.full_like(glo, -1)).amax(0).numpy()
+    # phase 2: the home frames over their merged windows
+    res = []
+    for t in range(off, off + cnt):
+        a, e = int(lo_t[t]), int(hi_t[t])
+        r = O.path_cv_exact(wl.frames[t:t + 1], wl.landmarks[a:e], wl.lam, q=wl.q[a:e])
+        res.append((a, e, r["s"][0], r["z"][0], r["ds"][0], r["dz"][0]))
+    return lo_t, hi_t, res
+
+
+def test_two_phase_landmark_sharding_protocol():
+    out = _spawn(_two_phase)
+    wl = synth.config0(seed=23, T=7, L=16, N=9)
+    T, n = wl.frames.shape[0], wl.frames.shape[1]
+    ref = O.path_cv_exact(wl.frames, wl.landmarks, wl.lam)
+    fc = O.batch_center(wl.frames, np.full(n, 1.0 / n))
+    lc = O.batch_center(wl.landmarks, np.full(n, 1.0 / n))
+    Dfull = O.batch_fit(fc[:, None], lc[None], np.full(n, 1.0 / n))[0][..., 0]
+    # the merged windows are the unsharded windows (hull of the same global threshold)
+    for t in range(T):
+        ok = np.nonzero(wl.lam * (Dfull[t] - Dfull[t].min()) <= 12.0)[0]
+        for r in (0, 1):
+            assert (out[r][0][t], out[r][1][t]) == (ok[0], ok[-1] + 1)
+    t = 0
+    for r in (0, 1):
+        for a, e, s, z, ds, dz in out[r][2]:
+            # landmarks outside the window weigh < e^-12 of the leading term
+            assert abs(s - ref["s"][t]) <= 1e-4 * max(1.0, abs(ref["s"][t]))
+            assert abs(z - ref["z"][t]) <= 1e-4 * abs(ref["z"][t]) + 1e-7
+            assert np.abs(ds - ref["ds"][t]).max() <= 1e-3 * np.abs(ref["ds"][t]).max()
+            t += 1
+    assert t == T

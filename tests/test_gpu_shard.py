@@ -178,3 +178,58 @@ def test_frame_routed_landmark_shards_match_unsharded(G, cuda_device):
     received = [o["received"] for o in outs]
     if G > 1:  # frames travel only where their hulls are: far fewer than G x T copies
         assert sum(received) < 1.6 * 260, received
+
+
+def _two_phase(wl, G, bounds=None, **kw):
+    T = wl.frames.shape[0]
+    engs = [engine.PathCVTC(wl.landmarks, wl.lam, shard=(g, G, bounds), two_phase=True, **kw) for g in range(G)]
+    gens = []
+    for g, e in enumerate(engs):
+        off, cnt = D.shard_range(T, g, G)
+        gens.append(e.two_phase_steps(wl.frames[off:off + cnt], off, T, out_dtype=torch.float64))
+    return engs, D.drive_lockstep(gens)
+
+
+@pytest.mark.parametrize("G,L", [(1, 1536), (2, 1536), (3, 1536), (4, 768)])
+def test_two_phase_landmark_shards_match_unsharded(G, L, cuda_device):
+    """The two-phase plan (landmark-sharded screen of every frame, one all-gather of the
+    screening operand, O(T) minima and windows; frame-sharded exact refits, weights and
+    gradients against the replicated landmarks): the concatenated home outputs equal the
+    unsharded evaluate -- same windows, s and z to 1e-9, ds and dz to SHARD_REL."""
+    wl = synth.config4(T=260, L=L, N=240)
+    ref = engine.PathCVTC(wl.landmarks, wl.lam).evaluate(wl.frames, out_dtype=torch.float64)
+    engs, outs = _two_phase(wl, G)
+    assert all(e.L < L for e in engs) or G == 1
+    s = torch.cat([o["s"] for o in outs]).cpu().numpy()
+    z = torch.cat([o["z"] for o in outs]).cpu().numpy()
+    np.testing.assert_allclose(s, ref["s"].cpu().numpy(), rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(z, ref["z"].cpu().numpy(), rtol=1e-9, atol=1e-12)
+    lo = torch.cat([o["window_lo"] for o in outs]).cpu().numpy()
+    cnt = torch.cat([o["window_cnt"] for o in outs]).cpu().numpy()
+    rlo, rcnt = ref["window_lo"].cpu().numpy(), ref["window_cnt"].cpu().numpy()
+    # the hull of the shards' windows covers the unsharded window (it can exceed it by the
+    # unscanned margins of the banded screens at shard boundaries)
+    assert (lo <= rlo).all() and (lo + cnt >= rlo + rcnt).all()
+    assert cnt.sum() <= 1.05 * rcnt.sum()
+    for key in ("ds", "dz"):
+        got = torch.cat([o[key] for o in outs]).cpu().numpy()
+        _rows_close(got, ref[key].cpu().numpy(), SHARD_REL)
+
+
+def test_two_phase_through_nccl_one_rank(cuda_device):
+    """evaluate_two_phase over a real NCCL process group (world size 1 on one GPU)."""
+    wl = synth.config4(T=64, L=1536, N=240)
+    init = not dist.is_initialized()
+    if init:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=cuda_device)
+    try:
+        eng = engine.PathCVTC(wl.landmarks, wl.lam, shard=(0, 1), two_phase=True)
+        out = eng.evaluate_two_phase(wl.frames, 0, 64, out_dtype=torch.float64)
+        torch.cuda.synchronize()
+    finally:
+        if init:
+            dist.destroy_process_group()
+    ref = engine.PathCVTC(wl.landmarks, wl.lam).evaluate(wl.frames, out_dtype=torch.float64)
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"].cpu().numpy(), rtol=1e-9)
+    _rows_close(out["ds"].cpu().numpy(), ref["ds"].cpu().numpy(), SHARD_REL)
