@@ -238,6 +238,23 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
                       const int32_t* nsig, const double* fvec, const double* dV, const int32_t* perm,
                       const int32_t* out_map, void* out0, void* out1, int32_t out_f32, int32_t ncv,
                       int32_t* wide_flag, void* workspace, int64_t ws_bytes, void* stream);
+/* Row digits for the int8 exact refits (the operands of _kearsley_matrix's covariance,
+ * geometry.py:180-196, as exact int8 slices): structure k of B is raw row fmap[perm[k]]
+ * (nullable maps), centred with centroid[perm[k]] and optionally weighted by w; its
+ * three axis rows 3k + b over the atoms get a power-of-two scale 2^e[3k + b] and 4
+ * signed int8 digits, stored per 32-atom k-step interleaved: dig [3B, kpad/32, 4, 32]
+ * (kpad % 32 == 0, kpad >= n).  Landmarks: weighted, once per set; frames: per call,
+ * in the refit's window-sorted order. */
+int mc_row_digits(const float* raw, const double* centroid, const double* w, const int32_t* perm,
+                  const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e, void* stream);
+/* mc_refine on the int8 tensor cores (tcgen05.mma.kind::i8, 10 digit products, int32
+ * TMEM accumulation, S exact to ~2^-31 of its scale): same outputs as mc_refine from the
+ * row digits of the landmarks (ldig, eL: mc_row_digits weighted) and of the frames in
+ * perm order (fdig, eF); gx / ga = the structures' weighted G norms; n < 32768. */
+int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T, int32_t L,
+                 int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt, const double* gx,
+                 const double* ga, int32_t cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
+                 void* stream);
 /* Bytes of caller workspace mc_pathcv_grad_i8 needs for T frames (per frame group: a
  * header and the A-digit image, <= 73 KB); -1 on bad arguments. */
 int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv);

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmcb200.so")
 SOURCES = ["center.cu", "cov_f64.cu", "fit.cu", "close.cu", "pathcv.cu", "pairs.cu", "grad_block.cu", "grad_dmma.cu", "grad_i8.cu", "tf32_gemm.cu", "tf32_gemm_2sm.cu",
-           "refine.cu", "refine_dmma.cu", "neighbour.cu", "mtd.cu", "prune.cu", "toysim.cu",
+           "refine.cu", "refine_dmma.cu", "refine_i8.cu", "neighbour.cu", "mtd.cu", "prune.cu", "toysim.cu",
            "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

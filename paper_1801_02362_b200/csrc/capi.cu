@@ -230,6 +230,27 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
                                            S_(stream)));
 }
 
+int mc_row_digits(const float* raw, const double* centroid, const double* w, const int32_t* perm,
+                  const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e, void* stream) {
+  if (B < 0 || n < 2 || kpad < n || kpad % 32 != 0) return MC_ERR_CONFIG;
+  if (B > 0 && (!raw || !centroid || !dig || !e)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_rdig(raw, centroid, w, perm, fmap, B, n, kpad, dig, e, S_(stream)));
+}
+
+int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T, int32_t L,
+                 int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt, const double* gx,
+                 const double* ga, int32_t cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
+                 void* stream) {
+  if (T < 0 || L < 1 || n < 2 || n >= 32768 || kpad < n || kpad % 32 != 0) return MC_ERR_CONFIG;
+  if ((lo == nullptr) != (cnt == nullptr)) return MC_ERR_CONFIG;
+  if (T > 0 && (!ldig || !eL || !fdig || !eF || !gx || !ga)) return MC_ERR_CONFIG;
+  if (!Dex && !Dd) return MC_ERR_CONFIG;
+  if ((Dex || Rex) && cap < 1) return MC_ERR_CONFIG;
+  if (Dd && ldd < L) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_refine_i8(ldig, eL, fdig, eF, T, L, n, kpad, perm, lo, cnt, gx, ga, cap, Dex, Rex, Dd,
+                                          ldd, flags, S_(stream)));
+}
+
 int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv) {
   if (T < 0 || (ncv != 1 && ncv != 2)) return -1;
   return (int64_t)mc::grad_i8_workspace(T, ncv);

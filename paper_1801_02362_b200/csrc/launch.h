@@ -80,6 +80,12 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
                               void* out1, int out_f32, int ncv, int* wide_flag, void* ws, size_t ws_bytes,
                               cudaStream_t stream);
 size_t grad_i8_workspace(int T, int ncv);
+cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
+                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream);
+cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,
+                             int kpad, const int* perm, const int* lo, const int* cnt, const double* gx,
+                             const double* ga, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,
+                             uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                  const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                  const double* sig_coef, const int* nsig, const double* fvec, const int* perm,

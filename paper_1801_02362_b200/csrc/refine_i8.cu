@@ -1,0 +1,469 @@
+// Exact refits (the Kearsley covariances of the in-window pairs, geometry.py:180-196)
+// on the 5th-gen tensor cores through exact int8 digits (Ozaki scheme,
+// tcgen05.mma.kind::i8 with int32 accumulation in TMEM).
+//
+// Same contract as refine_dmma_kernel (refine_dmma.cu): for every frame t and every
+// landmark l of its window [lo_t, lo_t + cnt_t) (or of all L, dense mode)
+//   S[t,l][b][g] = sum_j (x_{t,j,b} - c_{t,b}) w_j (a_{l,j,g} - c_{l,g})
+// followed by the fused Newton + adjugate fit (Jacobi fallback) -> MSD, R.
+// Both operands are split per ROW over the atoms (K = atoms) into 4 signed int8
+// digits, v = 2^(e-31) (d0 2^24 + d1 2^16 + d2 2^8 + d3) (the rules of grad_i8.cu):
+//   frames  FD: rows (sorted slot k, axis b) = centred x, written per call (rdig_kernel),
+//   landmarks LD: rows (l, axis g) = w (a - c_l), once per landmark set,
+// each row stored with the 4 digits of every 32-atom k-step interleaved
+// ([rows][kpad/32][4][32]: one 128-byte TMA row segment per k-step).  Every digit
+// product is exact and the 10 products with p + q <= 3 are accumulated in int32
+// per level (|acc3| <= 4 2^14 n < 2^31 for n < 32768), then
+//   S = 2^(eF + eL - 38) (acc0 2^24 + acc1 2^16 + acc2 2^8 + acc3)   (exact in fp64).
+// Error: each operand is exact to 2^-31 of its row maximum, so S is exact to
+// ~2^-31 sqrt(n)/n of |x||w a| -- ~1e-11 on the MSD at config 4 (tolerance 1e-9).
+//
+// Tile: M = 128 TMEM lanes = 42 landmarks x 3 axes (lanes 126, 127 unused), N = 48 =
+// 16 window-sorted frames x 3 axes; per 32-atom k-step 10 MMAs (M=128, N=48, K=32),
+// one per digit product (A = LD digit q, B = FD digit p: the K slices [32q, 32q + 32)
+// and [32p, 32p + 32) of the interleaved rows) into the TMEM columns of level p + q.
+// Accumulators 4 levels x 48 columns, double-buffered (384 of 512 TMEM columns), so a
+// tile's epilogue (staging the 9 entries of each pair in shared memory, then one thread
+// per in-window pair runs the fit) overlaps the next tile's MMAs.  A frame group takes
+// ceil(union / 42) landmark tiles of its window union.  Warp roles (256 threads,
+// persistent over frame groups): 0 TMA producer (7-stage ring of 22 KB: 16 KB of
+// landmark rows + 6 KB of frame rows per k-step), 1 MMA issuer, 2 TMEM allocator,
+// 4-7 epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "launch.h"
+#include "mc_math.cuh"
+
+namespace mc {
+
+namespace ri8 {
+constexpr int FG = 16;             // frames per group
+constexpr int NR = 3 * FG;         // 48 N rows
+constexpr int LT = 42;             // landmarks per tile
+constexpr int MR = 128;            // M rows (TMEM lanes); 3 LT = 126 used
+constexpr int KS = 32;             // atoms per k-step
+constexpr int ROWB = 4 * KS;       // 128 bytes per row and k-step (4 digits)
+constexpr int A_ST = MR * ROWB;    // 16 KB
+constexpr int B_ST = NR * ROWB;    // 6 KB
+constexpr int STAGE = A_ST + B_ST; // 22 KB (a multiple of 1024)
+constexpr int NST = 7;
+constexpr int ACC = 4 * NR;        // 192 TMEM columns per accumulator buffer
+constexpr int EPI = 4;             // epilogue warps (one per TMEM lane quarter)
+constexpr int NT = 32 * (4 + EPI);
+constexpr int SC_BYTES = FG * LT * 9 * 8;  // staged covariances of a tile (fp64)
+constexpr int SMEM = NST * STAGE + SC_BYTES + 1024 + 512;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+          su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+// K-major SWIZZLE_128B operand (128 B rows, 8-row groups 1024 B apart), layout 2
+__device__ __forceinline__ uint64_t desc128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// D = S32, A = B = signed 8 bit, K-major, N = 48, M = 128
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NR >> 3) << 17) | ((uint32_t)(MR >> 4) << 24);
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(reinterpret_cast<uint64_t>(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tld4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI) : "memory"); }
+
+__device__ __forceinline__ int digit_exp(double mx) {
+  if (!(mx > 0.0) || !isfinite(mx)) return 0;
+  int e;
+  frexp(mx, &e);  // mx < 2^e
+  if (ldexp(mx, 7 - e) > 127.0) ++e;
+  return e;
+}
+__device__ __forceinline__ void digits4(double v, double qs, int8_t* d) {
+  int X = __double2int_rn(v * qs);
+#pragma unroll
+  for (int p = 3; p > 0; --p) {
+    const int lo = ((X + 128) & 255) - 128;
+    d[p] = (int8_t)lo;
+    X = (X - lo) >> 8;
+  }
+  d[0] = (int8_t)X;
+}
+}  // namespace ri8
+
+// Row digits of B structures (one CTA each, 256 threads): structure k is raw row
+// fmap[perm[k]] (perm, fmap nullable), centred with cen[perm[k]] (fp64), optionally
+// weighted by w; rows 3k + axis of dig ([3B][kpad/32][4][32], kpad % 32 == 0) and the
+// per-row exponents e[3k + axis].  The structure is staged in shared memory (n <= 16384
+// per pass; larger n re-reads it from L2).
+__global__ void __launch_bounds__(256)
+rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const double* __restrict__ w,
+            const int* __restrict__ perm, const int* __restrict__ fmap, int B, int n, int kpad,
+            int8_t* __restrict__ dig, int* __restrict__ eout, int staged) {
+  extern __shared__ __align__(16) float sx[];  // the structure's 3n coordinates (staged mode)
+  __shared__ double red[3][8];
+  __shared__ int s_e[3];
+  const int k = blockIdx.x;
+  if (k >= B) return;
+  const int t = perm ? perm[k] : k;
+  const int src = fmap ? fmap[t] : t;
+  const float* x = raw + (int64_t)src * n * 3;
+  if (staged) {  // one coalesced pass over the row (16-byte loads when aligned)
+    const int nf = 3 * n;
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0 && nf % 4 == 0) {
+      for (int e = threadIdx.x; e < nf / 4; e += 256)
+        reinterpret_cast<float4*>(sx)[e] = __ldg(reinterpret_cast<const float4*>(x) + e);
+    } else {
+      for (int e = threadIdx.x; e < nf; e += 256) sx[e] = __ldg(x + e);
+    }
+    __syncthreads();
+    x = sx;
+  }
+  double c[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) c[b] = cen[3 * t + b];
+  double mx[3] = {0.0, 0.0, 0.0};
+  for (int j = threadIdx.x; j < n; j += 256) {
+    const double wj = w ? w[j] : 1.0;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) mx[b] = fmax(mx[b], fabs(wj * ((double)x[3 * j + b] - c[b])));
+  }
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx[b] = fmax(mx[b], __shfl_xor_sync(0xffffffffu, mx[b], o));
+    if ((threadIdx.x & 31) == 0) red[b][threadIdx.x >> 5] = mx[b];
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double m = 0.0;
+    for (int i = 0; i < 8; ++i) m = fmax(m, red[threadIdx.x][i]);
+    const int e = ri8::digit_exp(m);
+    s_e[threadIdx.x] = e;
+    eout[3 * k + threadIdx.x] = e;
+  }
+  __syncthreads();
+  // one thread per (k-step, axis, 4-atom quad): the 4 digits of 4 consecutive atoms packed
+  // into one 32-bit word per digit plane, so 8 threads write a plane's 32 bytes
+  const int nks = kpad / 32;
+  for (int task = threadIdx.x; task < 24 * nks; task += 256) {
+    const int qd = task & 7, rest = task >> 3;
+    const int ks = rest / 3, b = rest - 3 * ks;
+    const double qs = ldexp(1.0, 31 - s_e[b]);
+    uint32_t word[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = 32 * ks + 4 * qd + i;
+      int8_t d[4] = {0, 0, 0, 0};
+      if (j < n) ri8::digits4((w ? w[j] : 1.0) * ((double)x[3 * j + b] - c[b]), qs, d);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) word[q] |= (uint32_t)(uint8_t)d[q] << (8 * i);
+    }
+    uint32_t* dst = reinterpret_cast<uint32_t*>(dig + ((int64_t)(3 * k + b) * nks + ks) * 128) + qd;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[8 * q] = word[q];
+  }
+}
+
+__global__ void __launch_bounds__(ri8::NT, 1)
+refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int T, int L,
+                 int nks, const int* __restrict__ perm, const int* __restrict__ lo, const int* __restrict__ cnt,
+                 const int* __restrict__ eF, const int* __restrict__ eL, const double* __restrict__ gx,
+                 const double* __restrict__ ga, int cap, double* __restrict__ Dex, double* __restrict__ Rex,
+                 float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
+  using namespace ri8;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sSt = sm;                                                  // [NST][A 16 KB | B 6 KB]
+  double* sC = reinterpret_cast<double*>(sm + NST * STAGE);          // [FG][LT][9]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NST * STAGE + SC_BYTES);
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;  // [2]
+  uint64_t* tempty = tfull + 2;   // [2]
+  __shared__ uint32_t tmem_slot;
+  __shared__ int s_t[FG], s_lo[FG], s_cnt[FG], s_eF[NR];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int groups = (T + FG - 1) / FG;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    for (int s = 0; s < NST; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mb_init(&tfull[b], 1); mb_init(&tempty[b], EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+
+  // the window union of group g (every role computes it from global memory)
+  auto union_of = [&](int g, int& wlo, int& whi) {
+    wlo = L;
+    whi = 0;
+    for (int f = 0; f < FG; ++f) {
+      const int k = g * FG + f;
+      if (k >= T) break;
+      const int t = perm ? perm[k] : k;
+      const int a = lo ? lo[t] : 0, c = lo ? cnt[t] : L;
+      if (c > 0) { wlo = min(wlo, a); whi = max(whi, a + c); }
+    }
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t st = 0;
+      for (int g = blockIdx.x; g < groups; g += gridDim.x) {
+        int wlo, whi;
+        union_of(g, wlo, whi);
+        for (int l0 = wlo; l0 < whi; l0 += LT)
+          for (int ks = 0; ks < nks; ++ks, ++st) {
+            const int s = st % NST;
+            mb_wait(&empty[s], ((st / NST) & 1) ^ 1);
+            mb_expect(&full[s], (uint32_t)STAGE);
+            uint8_t* dst = sSt + s * STAGE;
+            tma2d(&mapA, &full[s], dst, ROWB * ks, 3 * l0);
+            tma2d(&mapB, &full[s], dst + A_ST, ROWB * ks, NR * g);
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    uint32_t st = 0, it = 0;
+    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
+      int wlo, whi;
+      union_of(g, wlo, whi);
+      for (int l0 = wlo; l0 < whi; l0 += LT, ++it) {
+        const int ab = it & 1;
+        mb_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + (uint32_t)(ab * ACC);
+        for (int ks = 0; ks < nks; ++ks, ++st) {
+          const int s = st % NST;
+          mb_wait(&full[s], (st / NST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            const uint32_t a = su32(sSt + s * STAGE), b = a + A_ST;
+            // level-major order: the 10 digit products with p + q <= 3
+#pragma unroll
+            for (int lvl = 0; lvl < 4; ++lvl)
+#pragma unroll
+              for (int p = 0; p <= lvl; ++p) {
+                const int q = lvl - p;
+                mma_i8(d + (uint32_t)(NR * lvl), desc128(a + KS * q), desc128(b + KS * p),
+                       (ks > 0 || p > 0) ? 1u : 0u);
+              }
+            mma_commit(&empty[s]);
+            if (ks == nks - 1) mma_commit(&tfull[ab]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int r = (warp & 3) * 32 + lane;  // TMEM lane = landmark row 3 l' + g of the tile
+    const int lp = r / 3, gg = r - 3 * (r / 3);
+    const int et = tid - 128;
+    uint32_t it = 0;
+    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
+      int wlo, whi;
+      union_of(g, wlo, whi);
+      if (et < FG) {
+        const int k = g * FG + et;
+        const int t = k < T ? (perm ? perm[k] : k) : -1;
+        s_t[et] = t;
+        s_lo[et] = (t >= 0 && lo) ? lo[t] : 0;
+        s_cnt[et] = t < 0 ? 0 : (lo ? cnt[t] : L);
+      }
+      if (et < NR) s_eF[et] = (g * NR + et < 3 * T) ? eF[g * NR + et] : 0;
+      epi_bar();
+      for (int l0 = wlo; l0 < whi; l0 += LT, ++it) {
+        const int ab = it & 1;
+        const int l = l0 + lp;
+        const bool lok = r < 3 * LT && l < L;
+        const int el = lok ? eL[3 * l + gg] : 0;
+        mb_wait(&tfull[ab], (it >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        __syncwarp();
+        const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(ab * ACC);
+#pragma unroll 1
+        for (int fc = 0; fc < FG / 4; ++fc) {  // 4 frames (12 columns) at a time
+          uint32_t acc[4][12];
+#pragma unroll
+          for (int lvl = 0; lvl < 4; ++lvl) {
+            tld8(tb + NR * lvl + 12 * fc, &acc[lvl][0]);
+            tld4(tb + NR * lvl + 12 * fc + 8, &acc[lvl][8]);
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (lok) {
+#pragma unroll
+            for (int c = 0; c < 12; ++c) {
+              const int f = 4 * fc + c / 3, b = c % 3;
+              const double v = (double)(int)acc[0][c] * 16777216.0 + (double)(int)acc[1][c] * 65536.0 +
+                               (double)(int)acc[2][c] * 256.0 + (double)(int)acc[3][c];
+              sC[(f * LT + lp) * 9 + 3 * b + gg] = v * pow2d(s_eF[3 * f + b] + el - 38);
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mb_arrive(&tempty[ab]);
+        epi_bar();
+        // fused fit of the in-window pairs (exact fp64)
+        for (int pi = et; pi < FG * LT; pi += 32 * EPI) {
+          const int f = pi / LT, li = pi - f * LT;
+          const int t = s_t[f], ll = l0 + li;
+          if (t < 0 || ll >= L || ll >= whi) continue;
+          const int slot = ll - s_lo[f];
+          if (slot < 0 || slot >= s_cnt[f]) continue;
+          const double* S = sC + (f * LT + li) * 9;
+          double q[4];
+          bool ill = false;
+          double msd = fit_fast(S, gx[t], ga[ll], Rex ? q : nullptr, &ill);
+          uint8_t fl = 0;
+          if (ill) {
+            double k4[4][4], V[4][4], ev[4];
+            kearsley_from_S(S, gx[t], ga[ll], k4);
+            if (!jacobi4(k4, ev, V)) fl |= kFlagNoConverge;
+            msd = ev[0];
+            q[0] = V[0][0]; q[1] = V[1][0]; q[2] = V[2][0]; q[3] = V[3][0];
+          }
+          if (Dex) Dex[(int64_t)t * cap + slot] = msd;
+          if (Dd) Dd[(int64_t)t * ldd + ll] = (float)msd;
+          if (Rex) {
+            double rr[9];
+            quat_to_rot(q, rr);
+            double* o = Rex + ((int64_t)t * cap + slot) * 9;
+#pragma unroll
+            for (int e = 0; e < 9; ++e) o[e] = rr[e];
+          }
+          if (fl && flags) flags[t] |= fl;
+        }
+        epi_bar();  // sC is rewritten by the next tile
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_ri8() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_dig_map(CUtensorMap* m, const int8_t* dig, int64_t rows, int kpad, int box_rows) {
+  auto enc = get_encode_ri8();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)4 * kpad, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)4 * kpad};
+  cuuint32_t box[2] = {(cuuint32_t)ri8::ROWB, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(dig), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
+                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream) {
+  if (B <= 0 || n <= 0) return cudaSuccess;
+  if (kpad % 32 || kpad < n) return cudaErrorInvalidValue;
+  // stage the structure in shared memory when it fits (n <= 16384: 192 KB)
+  const int staged = 0;  // staging a 120 KB row in shared memory (1 CTA / SM) measured slower than two L2-served passes
+  const int smem = staged ? 12 * n : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e2 = cudaFuncSetAttribute(rdig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 16384);
+    if (e2 != cudaSuccess) return e2;
+    attr = true;
+  }
+  rdig_kernel<<<B, 256, smem, stream>>>(raw, cen, w, perm, fmap, B, n, kpad, dig, e, staged);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,
+                             int kpad, const int* perm, const int* lo, const int* cnt, const double* gx,
+                             const double* ga, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,
+                             uint8_t* flags, cudaStream_t stream) {
+  using namespace ri8;
+  if (T <= 0 || L <= 0) return cudaSuccess;
+  if (kpad % 32 || kpad < n || n >= 32768) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  if (!make_dig_map(&ma, ldig, 3LL * L, kpad, MR) || !make_dig_map(&mb, fdig, 3LL * T, kpad, NR))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(refine_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int groups = (T + FG - 1) / FG;
+  const int grid = groups < sms ? groups : sms;
+  refine_i8_kernel<<<grid, NT, SMEM, stream>>>(ma, mb, T, L, kpad / 32, perm, lo, cnt, eF, eL, gx, ga, cap, Dex, Rex,
+                                               Dd, ldd, flags);
+  return cudaGetLastError();
+}
+
+}  // namespace mc

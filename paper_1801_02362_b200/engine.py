@@ -40,6 +40,9 @@ CLOSE_DMMA = os.environ.get("MC_CLOSE_DMMA", "1") == "1"
 # gradient contraction on the int8 tensor cores (exact int8 digits, csrc/grad_i8.cu);
 # env MC_GRAD_I8=0 keeps the fp64 DMMA kernel for every group
 GRAD_I8 = os.environ.get("MC_GRAD_I8", "1") == "1"
+# exact window refits on the int8 tensor cores (exact int8 digits, csrc/refine_i8.cu);
+# env MC_REFINE_I8=0 keeps the fp64 DMMA kernel
+REFINE_I8 = os.environ.get("MC_REFINE_I8", "1") == "1"
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 NB_MAX_L = 16384        # neighbour-list active-set bitmap capacity (csrc/pathcv.cu kNbMaxL)
 
@@ -516,6 +519,9 @@ class PathCVTC:
             raise InvalidStructureError("landmark coordinates contain non-finite values")
         # int8 digits of the centred landmarks for the tensor-core gradient contraction
         self.ldig = K.ldig_prep(self.lraw, self.ls.centroid) if (GRAD_I8 and self.n % 4 == 0) else None
+        # ... and of the weighted centred landmark rows (over the atoms) for the exact refits
+        self.rdl = K.row_digits(self.lraw, self.ls.centroid, w=self.w) if (REFINE_I8 and self.n < 32768) else None
+        self._fdbuf = None
         # estimate error margin (in units of lam * D): the split (22 significant bits,
         # TF32 or scaled-F16 pair) + fp32-accumulation error grows ~ sqrt(n); measured
         # max 6.4e-6 (n=1000) and 6.4e-5 (n=10000)
@@ -561,12 +567,22 @@ class PathCVTC:
                                           fnorm=self.frame_bound(fs) if one else None,
                                           fcoef=2.0 * self.lam if one else 0.0, rlo=rlo, rhi=rhi, dref=dref)
         perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
-        Dex, Rex, rflags = K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap,
-                                    fmap=perm0, wuni=self.wuni)
+        Dex, Rex, rflags = self._refine_windows(fr, fs, perm, lo, cnt, cap, perm0)
         wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
                                 rowcnt=cnt)
         wres["D_window"] = Dex
         return lo, cnt, wres, cflags, rflags
+
+    def _refine_windows(self, fr, fs, perm, lo, cnt, cap, fmap=None):
+        """Exact fp64 refits of the window pairs: int8 tensor-core kernel (frame row digits in
+        window-sorted order, then mc_refine_i8) or the fp64 DMMA kernel."""
+        T = fs.count
+        if self.rdl is not None:
+            self._fdbuf = K.row_digits(fr, fs.centroid, None, perm=perm, fmap=fmap, count=T, out=self._fdbuf)
+            return K.refine_i8(self.rdl, self._fdbuf, T, self.L, self.n, fs.g, self.ls.g, perm=perm, lo=lo, cnt=cnt,
+                               cap=cap)
+        return K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap, fmap=fmap,
+                        wuni=self.wuni)
 
     def frame_bound(self, fs):
         """max_l e_tl: the one-term estimate error bound of frame t against any landmark
@@ -628,7 +644,11 @@ class PathCVTC:
         D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
         if not exact:
             return K.msd_estimate(fs, self._lsplit(3), D)
-        _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D, wuni=self.wuni)
+        if self.rdl is not None:
+            self._fdbuf = K.row_digits(fr, fs.centroid, None, count=fr.shape[0], out=self._fdbuf)
+            _, _, flags = K.refine_i8(self.rdl, self._fdbuf, fr.shape[0], self.L, self.n, fs.g, self.ls.g, Dd=D)
+        else:
+            _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D, wuni=self.wuni)
         _raise_flags(flags, "msd_matrix")
         return D
 
@@ -1112,8 +1132,7 @@ class PathCVTC:
         # ---- phase 2: exact refits, weights and gradients of the home frames, all landmarks
         cap = int(max(1, min(full.L, int(cnt_h.max().item()) if Th else 1)))
         perm = K.sort_by_key((2 * lo_h + cnt_h).to(torch.int32), 2 * full.L + 1)
-        Dex, Rex, rflags = K.refine(frh, fsh, full.lraw, full.ls, full.w, perm=perm, lo=lo_h, cnt=cnt_h, cap=cap,
-                                    wuni=full.wuni)
+        Dex, Rex, rflags = full._refine_windows(frh, fsh, perm, lo_h, cnt_h, cap)
         wres = K.pathcv_weights(Dex, full.q, full.lam, Rex, fsh, full.ls, cap, full.cutoff, L=full.L, rowlo=lo_h,
                                 rowcnt=cnt_h)
         out = {"s": wres["s"], "z": wres["z"], "window_lo": lo_h, "window_cnt": cnt_h, "nsig": wres["nsig"],

@@ -460,6 +460,42 @@ def sort_by_key(key, nbins):
     return perm
 
 
+class RowDigits:
+    """Row digits of B structures (mc_row_digits): dig [3B, kpad/32, 4, 32] int8, e [3B] int32."""
+
+    __slots__ = ("dig", "e", "kpad", "count")
+
+    def __init__(self, dig, e, kpad, count):
+        self.dig, self.e, self.kpad, self.count = dig, e, kpad, count
+
+
+def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None):
+    """raw [*, n, 3] fp32 (rows read through fmap / perm), centroid [*, 3] fp64 -> RowDigits."""
+    n = raw.shape[1]
+    B = int(count if count is not None else (perm.numel() if perm is not None else raw.shape[0]))
+    kpad = ((n + 31) // 32) * 32
+    if out is None or out.dig.shape[0] < 3 * B or out.kpad != kpad:
+        dig = torch.empty((3 * B, kpad // 32, 4, 32), dtype=torch.int8, device=raw.device)
+        e = torch.empty((3 * B,), dtype=I32, device=raw.device)
+    else:
+        dig, e = out.dig, out.e
+    call("mc_row_digits", ptr(raw.contiguous()), ptr(centroid.contiguous()), ptr(w), ptr(perm), ptr(fmap), B, n, kpad,
+         ptr(dig), ptr(e), stream_ptr())
+    return RowDigits(dig, e, kpad, B)
+
+
+def refine_i8(ldig, fdig, T, L, n, gx, ga, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None):
+    """mc_refine on the int8 tensor cores from landmark / frame row digits (same outputs as refine)."""
+    dev = gx.device
+    Dex = torch.empty((T, cap), dtype=F64, device=dev) if cap else None
+    Rex = torch.empty((T, cap, 9), dtype=F64, device=dev) if (cap and want_rot) else None
+    flags = torch.zeros((T,), dtype=U8, device=dev)
+    call("mc_refine_i8", ptr(ldig.dig), ptr(ldig.e), ptr(fdig.dig), ptr(fdig.e), T, L, n, ldig.kpad, ptr(perm),
+         ptr(lo), ptr(cnt), ptr(gx), ptr(ga), cap, ptr(Dex), ptr(Rex), ptr(Dd),
+         Dd.stride(0) if Dd is not None else 0, ptr(flags), stream_ptr())
+    return Dex, Rex, flags
+
+
 def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None,
            fmap=None, wuni=0.0):
     """Exact fp64 fits of the in-window pairs (sparse) or of all pairs (dense, into Dd).

@@ -100,3 +100,55 @@ def test_fused_bias_force_equals_contracted_gradients(cuda_device):
     # frame's largest component, so the sum over the atoms vanishes to within the 1e-5
     # gradient tolerance (the fp64 DMMA sum to ~1e-14)
     assert np.abs(F.sum(axis=1)).max() <= 1e-5 * np.abs(F).max()
+
+
+@pytest.mark.parametrize("T,L,N", [(96, 512, 600), (77, 300, 1000), (40, 2048, 2500)])
+def test_i8_refits_match_dmma_refits_and_oracle(T, L, N, cuda_device):
+    """Exact window refits on the int8 tensor cores (mc_refine_i8) == the fp64 DMMA refits:
+    every window MSD within 1e-9 absolute + 1e-12 relative, and == the fp64 oracle's MSDs
+    (1e-6 relative or 1e-9 absolute); s and z == the oracle (1e-6)."""
+    wl = synth.config4(seed=9, T=T, L=L, N=N)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam)
+    assert pcv.rdl is not None
+    a = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    rdl, pcv.rdl = pcv.rdl, None
+    b = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    pcv.rdl = rdl
+    np.testing.assert_array_equal(a["window_cnt"].cpu().numpy(), b["window_cnt"].cpu().numpy())
+    cnt, lo = a["window_cnt"].cpu().numpy(), a["window_lo"].cpu().numpy()
+    Da, Db = a["D_window"].cpu().numpy(), b["D_window"].cpu().numpy()
+    ref = O.batch_msd_matrix(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64))
+    worst = 0.0
+    for t in range(T):
+        x, y = Da[t, :cnt[t]], Db[t, :cnt[t]]
+        r = ref[t, lo[t]:lo[t] + cnt[t]]
+        assert np.all(np.abs(x - y) <= 1e-9 + 1e-12 * np.abs(y)), np.abs(x - y).max()
+        assert np.all(np.abs(x - r) <= np.maximum(1e-6 * np.abs(r), 1e-9))
+        worst = max(worst, float(np.abs(x - r).max()))
+    print(f"T={T} L={L} N={N}: worst |D_i8 - D_oracle| {worst:.2e}")
+    # the int8 refits are exact to ~1e-10 absolute on D (31-bit operand digits), which moves
+    # s and z by ~lam 1e-10: far inside the 1e-6 tolerance against the oracle
+    ds_ = np.abs(a["s"].cpu().numpy() - b["s"].cpu().numpy()).max()
+    dz_ = np.abs(a["z"].cpu().numpy() - b["z"].cpu().numpy()).max()
+    print(f"  s: max |i8 - dmma| {ds_:.2e}; z: {dz_:.2e}")
+    np.testing.assert_allclose(a["s"].cpu().numpy(), b["s"].cpu().numpy(), rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(a["z"].cpu().numpy(), b["z"].cpu().numpy(), rtol=1e-8, atol=1e-10)
+    ref_cv = O.batch_path_cv_exact(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam)
+    np.testing.assert_allclose(a["s"].cpu().numpy(), ref_cv["s"], rtol=1e-6)
+    np.testing.assert_allclose(a["z"].cpu().numpy(), ref_cv["z"], rtol=1e-6, atol=1e-9)
+
+
+def test_i8_dense_refits_near_identical_pairs(cuda_device):
+    """Dense exact matrix (config-2 path) on the int8 kernel: a landmark under a rigid motion
+    as a frame gives D ~ 0 within 1e-9 absolute; every pair within 1e-6 relative or 1e-9
+    absolute of the oracle."""
+    wl = synth.config2(seed=5, T=70, L=90, N=1000)
+    rng = np.random.default_rng(2)
+    frames = wl.frames.copy()
+    frames[:20] = synth.rigid_motion(rng, wl.landmarks[:20].astype(np.float64), dtype=np.float32)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam)
+    D = pcv.msd_matrix(frames).cpu().numpy().astype(np.float64)
+    ref = O.batch_msd_matrix(frames.astype(np.float64), wl.landmarks.astype(np.float64))
+    assert np.all(np.abs(D - ref) <= np.maximum(1e-6 * np.abs(ref), 1e-9 + 6e-8 * np.abs(ref)))
+    d0 = np.abs(D[np.arange(20), np.arange(20)] - ref[np.arange(20), np.arange(20)])
+    assert d0.max() <= 1e-9, d0.max()
