@@ -213,7 +213,10 @@ class Config3:
     (fp32 coordinates, fp64 finalisation; exact fp64 path).  Walkers are sharded
     across ranks (independent objects, no collective)."""
 
-    metric, unit, dtype = "path-CV frames/s", "frames/s", "f32 in / f64 exact"
+    metric, unit = "path-CV frames/s", "frames/s"
+    dtype = ("f32 coordinates; one-term FP16 tcgen05 screen of the refresh frames -> close-structure lifetime "
+             "windows -> covariances and refresh fits on tcgen05 kind::i8 (exact int8 row digits) -> fp64 Eq. 5 / "
+             "weights -> gradient contraction (DMMA for windows wider than 117 landmarks)")
 
     def __init__(self, device, rank, world, walkers_override=None):
         from paper_1801_02362_b200 import dist as D
@@ -251,12 +254,16 @@ class Config3:
         import torch
 
         out = self._step(self.frames_host.to(self.device, non_blocking=True))
-        host = [out[k].to("cpu", non_blocking=True) for k in ("s", "z", "refresh", "dxy")]
+        if not hasattr(self, "_host"):
+            self._host = {k: torch.empty(out[k].shape, dtype=out[k].dtype).pin_memory()
+                          for k in ("ds", "dz", "s", "z", "refresh", "dxy")}
+        for k, h in self._host.items():  # the whole result: gradients, s, z, refresh log, D(x, y)
+            h.copy_(out[k], non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        return host
+        return self._host
 
     def e2e_bytes(self):
-        return self.T * self.n * 12, self.T * (8 + 8 + 1 + 8)
+        return self.T * self.n * 12, self.T * (2 * self.n * 3 * 4 + 8 + 8 + 1 + 8)
 
     def units(self):
         return self.T
@@ -275,12 +282,19 @@ class Config3:
             return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_fit_dense":
             return "bytes", T * L * (72 + 8 + 72 + 1)
+        if name == "mc_refine_i8" and self.last is not None and "window_cnt" in self.last:
+            # pruned replay: every frame's covariances over its close structure's window
+            # (9 multiply-adds per pair and atom x 10 digit products)
+            return "int8_tensor_op_refine", 2.0 * 10.0 * 9.0 * n * float(self.last["window_cnt"].double().sum().item())
         return "bytes", 0.0
 
     def extra(self):
         d = {"walkers": self.W_all, "walkers_per_rank": self.Wloc, "steps": self.steps}
         if self.last is not None:
             d["refresh_fraction"] = float(self.last["refresh"].float().mean().item())
+            if "window_cnt" in self.last:
+                d["mean_window"] = float(self.last["window_cnt"].float().mean().item())
+                d["mean_significant"] = float(self.last["nsig"].float().mean().item())
         return d
 
 
@@ -384,10 +398,12 @@ class ConfigTC:
             for k, c in enumerate(zip(hr.uniform(0, self.L - 1, 256), hr.uniform(0.0, 0.02, 256))):
                 self.hills.deposit(torch.tensor(c, dtype=torch.float64), k)
         if cfg == 2:
-            self.dtype = "f32 coordinates; exact fp64 refits of every pair on the fp64 tensor cores (DMMA)"
+            self.dtype = ("f32 coordinates; every pair's covariance on tcgen05 kind::i8 with exact int8 row digits "
+                          "(int32 accumulation, fp64 recombination) + fused fp64 fit")
         else:
             self.dtype = ("f32 coordinates; one-term FP16 tcgen05 screen (rigorous bound) -> exact fp64 refits "
-                          "(DMMA) -> fp64 weights -> gradient contraction on tcgen05 kind::i8 with exact int8 "
+                          "(tcgen05 kind::i8, exact int8 row digits) -> fp64 weights -> gradient contraction on "
+                          "tcgen05 kind::i8 with exact int8 "
                           "digits (int32 accumulation, fp64 recombination)")
 
     def _step(self, frames, D=None):
@@ -409,11 +425,7 @@ class ConfigTC:
         return self.last
 
     def _msd_into(self, frames, D):
-        from paper_1801_02362_b200 import kernels as K
-
-        fr, fs = self.pcv._frames(frames)
-        K.refine(fr, fs, self.pcv.lraw, self.pcv.ls, self.pcv.w, Dd=D, wuni=self.pcv.wuni)
-        return D
+        return self.pcv.msd_matrix(frames, out=D)
 
     def step_device(self):
         return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
@@ -618,6 +630,16 @@ class ConfigTC:
         if name == "mc_pathcv_grad_block" and self.last is not None:
             # useful fp64 work: 18 FMA (U^s, U^z: 2 CVs x 3 x 3) per significant pair and atom
             return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
+        if name == "mc_refine_i8":
+            # executed int8 MMA work: 9 multiply-adds (3 x 3) per (pair, atom) x the 10 kept digit
+            # products; pairs = every pair (config 2) or the window pairs (config 4)
+            if self.cfg == 2:
+                pairs = float(T * L)
+            elif self.last is not None:
+                pairs = float(self.last["window_cnt"].double().sum().item())
+            else:
+                pairs = 0.0
+            return "int8_tensor_op_refine", 2.0 * 10.0 * 9.0 * n * pairs
         if name == "mc_center_split16":
             return "bytes", T * n * 3 * 4 + 2 * T * 3 * (((n + 31) // 32) * 32) * 2
         if name == "mc_refine":
@@ -652,7 +674,7 @@ class ConfigTC:
 DMMA_PEAK_TF = 36.2  # measured mma.sync f64 rate on this pool's B200 (profiles/r02_dmma_probe_b200.txt)
 
 
-def _int8_roof(amount, step_ms, pk):
+def _int8_roof(amount, step_ms, pk, basis=None):
     """Roofline of an int8 tcgen05 kernel: executed int8 ops per second against twice the
     measured bf16 GEMM rate (kind::i8 issues twice the multiply-adds of kind::f16 per cycle:
     8192 vs 4096 per SM, tools/_diag/i8_probe.cu)."""
@@ -662,8 +684,8 @@ def _int8_roof(amount, step_ms, pk):
             "peak_src": f"2 x bf16_tflops_sustained from {pk['src']} (kind::i8 = 2x the kind::f16 MAC rate, "
                         "measured by tools/_diag/i8_probe.cu)",
             "peak_burst": 2.0 * pk["bf16"], "frac_of_burst": ach / (2.0 * pk["bf16"]),
-            "flop_basis": "executed int8 multiply-adds x 2: 10 digit products x 18 per (frame, significant "
-                          "landmark, atom)"}
+            "flop_basis": basis or ("executed int8 multiply-adds x 2: 10 digit products x 18 per (frame, "
+                                    "significant landmark, atom)")}
 
 
 def measured_traffic(kernel, cfg, T):
@@ -813,6 +835,9 @@ def run_ours(args, rank, world, local_rank):
                 "flop_basis": "useful fp64 flops (significant / window pairs); executed includes window-union padding"}
     elif kind == "int8_tensor_op":
         roof = _int8_roof(amount, step_ms, pk)
+    elif kind == "int8_tensor_op_refine":
+        roof = _int8_roof(amount, step_ms, pk, "executed int8 multiply-adds x 2: 10 digit products x 9 per "
+                                               "(refit pair, atom)")
     else:
         ach = amount / (step_ms * 1e-3) / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,
@@ -831,6 +856,14 @@ def run_ours(args, rank, world, local_rank):
         if gk == "int8_tensor_op":
             roof_grad = _int8_roof(gamount, gt / nprof, pk)
             roof_grad.update({"kernel": "mc_pathcv_grad_i8", "share_of_step": gt / total, "avg_launch_ms": gt / gc})
+    roof_refine = None
+    if name != "mc_refine_i8" and "mc_refine_i8" in prof and hasattr(runner, "pcv"):
+        rk, ramount = runner.kernel_work("mc_refine_i8")
+        rc, rt = prof["mc_refine_i8"]
+        if rk == "int8_tensor_op_refine":
+            roof_refine = _int8_roof(ramount, rt / nprof, pk, "executed int8 multiply-adds x 2: 10 digit products x 9 "
+                                                              "per (refit pair, atom)")
+            roof_refine.update({"kernel": "mc_refine_i8", "share_of_step": rt / total, "avg_launch_ms": rt / rc})
     units = runner.units() * world if runner.scaling == "weak" else runner.units()
     if dist and runner.scaling == "strong" and not getattr(runner, "replicated_units", False):
         t = torch.tensor([float(units)], device=device, dtype=torch.float64)
@@ -862,6 +895,8 @@ def run_ours(args, rank, world, local_rank):
         line["e2e_bias_force"] = e2e_force
     if roof_grad is not None:
         line["roofline_gradient"] = roof_grad
+    if roof_refine is not None:
+        line["roofline_refits"] = roof_refine
     line["config"].update(runner.extra())
     if cfg == 4 and getattr(runner, "last", None) is not None and "window_cnt" in runner.last:
         # the BASELINE metric's other half: aligned-MSD pairs/s of the same step -- every

@@ -132,7 +132,9 @@ int mc_xy_eig(const double* fplanes, const double* gx, int64_t T, int32_t npad, 
  *   Rows are dense (ld = L, rowlo = rowcnt = NULL) or sparse windows: row t of
  *   D/R (stride ld) holds landmarks rowlo[t] .. rowlo[t]+rowcnt[t]-1 (the
  *   refined candidates of the tensor-core path; landmarks outside a window
- *   have lam (D - D_min) > cutoff and weight < e^-cutoff).
+ *   have lam (D - D_min) > cutoff and weight < e^-cutoff).  With refresh and
+ *   windows (the pruned close replay) a non-refresh row t has the window of its
+ *   close structure ridx[t]: S row t and R row ridx[t] share the slot layout.
  * mc_pathcv_grad: one pass over atoms writing ds, dz [T, n, 3] (fp64, or fp32 if
  *   out_f32).  Coordinates from centred fp64 planes, or (fplanes/lplanes NULL)
  *   from raw fp32 AoS input + fp64 centroids.  perm (nullable): frame visiting order
@@ -255,6 +257,15 @@ int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, cons
                  int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt, const double* gx,
                  const double* ga, int32_t cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
                  void* stream);
+/* mc_refine_i8 for the pruned close-structure replay (PathCV.close_replay, fp32 frames;
+ * replaces the dense covariances of _kearsley_matrix, geometry.py:180-196, for the Eq. 5
+ * rows of SPEC.md:124-132): the exact covariances S of every window pair to Sex
+ * [T, cap, 9] and, on the rows with fitmask[t] != 0 (the refresh rows, Alg. 2 step 5),
+ * the fits (Dex [T, cap], Rex [T, cap, 9]); windows lo / cnt are required. */
+int mc_refine_i8_close(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T,
+                       int32_t L, int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt,
+                       const double* gx, const double* ga, int32_t cap, const uint8_t* fitmask, double* Sex,
+                       double* Dex, double* Rex, uint8_t* flags, void* stream);
 /* Bytes of caller workspace mc_pathcv_grad_i8 needs for T frames (per frame group: a
  * header and the A-digit image, <= 73 KB); -1 on bad arguments. */
 int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv);
@@ -291,6 +302,14 @@ int mc_msd_f16_2sm(const void* fhl, const void* lhl, const double* fscale, const
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
                   double fcoef, const int32_t* rlo, const int32_t* rhi, const float* dref, int32_t cap, int32_t* lo,
                   int32_t* cnt, float* dmin, uint8_t* flags, void* stream);
+/* mc_candidates with the close-structure lifetime window (DESIGN.md
+ * section 5): row t is a refresh frame y and dlife[t] >= 0 the largest D(x, y) of the
+ * frames x that keep y as their close structure; the window holds every landmark any of
+ * them can need, thr_t = thr + fcoef fnorm[t] + lam (2 d + 2 sqrt(d) (X + dmu)),
+ * dmu = sqrt(D_min + fnorm[t]), X^2 = (sqrt(d) + dmu)^2 + thr / lam. */
+int mc_candidates_life(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr,
+                       const double* fnorm, double fcoef, const double* dlife, int32_t cap, int32_t* lo, int32_t* cnt,
+                       float* dmin, uint8_t* flags, void* stream);
 /* Metric pruning of the screen (csrc/prune.cu):
  * mc_prune_plan: from the one-term estimate Dc [T, C] against a coarse landmark subset
  *   (coarse landmark c = landmark c * cstride), its error bound c_unit * fnorm[t] * cnorm[c]

@@ -76,6 +76,8 @@ _SIGS = {
     + [_P] * 18,
     "mc_shard_rescale": [_I32, _I32, _P, _P, _P, _P, _P, _P],
     "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
+    "mc_candidates_life": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _I32, _P, _P, _P, _P, _P],
+    "mc_refine_i8_close": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P],
     "mc_prune_plan": [_P, _I32, _I32, _I64, _P, _P, _P, _P, _D, _P, _P, _I32, _I32, _D, _I32, _I32, _P, _P, _P, _P, _P,
                       _P],
     "mc_band_tiles": [_P, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],

@@ -118,7 +118,7 @@ int mc_pathcv_weights(int32_t T, int32_t t0, int32_t L, double lam, double cutof
   if (!rowcnt && ld != L) return MC_ERR_CONFIG;
   if (T > 0 && (!D || !q || !R || !fwbar || !lwbar || !s || !z || !sig_idx || !sig_coef || !nsig || !fvec))
     return MC_ERR_CONFIG;
-  if (refresh && (rowcnt || !ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
+  if (refresh && (!ridx || !S || !rxy || !xyeig || !gx || !ga || !lmom)) return MC_ERR_CONFIG;
   return cuda_status(mc::launch_cv_weights(T, t0, L, lam, cutoff, cap, ld, rowlo, rowcnt, D, q, R, fwbar, lwbar, refresh,
                                            ridx, S, rxy, xyeig, gx, ga, lmom, s, z, sig_idx, sig_coef, nsig, fvec,
                                            flags, S_(stream)));
@@ -256,6 +256,17 @@ int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv) {
   return (int64_t)mc::grad_i8_workspace(T, ncv);
 }
 
+int mc_refine_i8_close(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T,
+                       int32_t L, int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt,
+                       const double* gx, const double* ga, int32_t cap, const uint8_t* fitmask, double* Sex,
+                       double* Dex, double* Rex, uint8_t* flags, void* stream) {
+  if (T < 0 || L < 1 || n < 2 || n >= 32768 || kpad < n || kpad % 32 != 0 || cap < 1) return MC_ERR_CONFIG;
+  if (T > 0 && (!ldig || !eL || !fdig || !eF || !gx || !ga || !lo || !cnt || !fitmask || !Sex || !Dex || !Rex))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_refine_i8(ldig, eL, fdig, eF, T, L, n, kpad, perm, lo, cnt, gx, ga, cap, Dex, Rex,
+                                          nullptr, 0, flags, S_(stream), Sex, fitmask));
+}
+
 int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr, const double* fnorm,
                   double fcoef, const int32_t* rlo, const int32_t* rhi, const float* dref, int32_t cap, int32_t* lo,
                   int32_t* cnt, float* dmin, uint8_t* flags, void* stream) {
@@ -266,6 +277,15 @@ int mc_candidates(const float* D, int32_t T, int32_t L, int64_t ldd, double lam,
   return cuda_status(
       mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, dref, cap, lo, cnt, dmin, flags,
                                               S_(stream)));
+}
+
+int mc_candidates_life(const float* D, int32_t T, int32_t L, int64_t ldd, double lam, double thr,
+                       const double* fnorm, double fcoef, const double* dlife, int32_t cap, int32_t* lo, int32_t* cnt,
+                       float* dmin, uint8_t* flags, void* stream) {
+  if (T < 0 || L < 1 || ldd < L || cap < 1 || !(lam > 0.0) || !(thr >= 0.0) || !(fcoef >= 0.0)) return MC_ERR_CONFIG;
+  if (T > 0 && (!D || !lo || !cnt || !dlife)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_candidates(D, T, L, ldd, lam, thr, fnorm, fcoef, nullptr, nullptr, nullptr, cap, lo, cnt,
+                                           dmin, flags, S_(stream), dlife));
 }
 
 int mc_prune_plan(const float* Dc, int32_t T, int32_t C, int64_t lddc, const double* fnorm, const double* cnorm,

@@ -85,7 +85,8 @@ cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, co
 cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,
                              int kpad, const int* perm, const int* lo, const int* cnt, const double* gx,
                              const double* ga, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,
-                             uint8_t* flags, cudaStream_t stream);
+                             uint8_t* flags, cudaStream_t stream, double* Sex = nullptr,
+                             const uint8_t* fitmask = nullptr);
 cudaError_t launch_cv_grad_block(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,
                                  const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                  const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
@@ -97,7 +98,8 @@ cudaError_t launch_cv_grad_block_planes(int T, int t0, int n, int npad, int cap,
                                         void* dz, int out_f32, cudaStream_t stream);
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
                               double fcoef, const int* rlo, const int* rhi, const float* dref, int cap, int* lo,
-                              int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream);
+                              int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream,
+                              const double* dlife = nullptr);
 cudaError_t launch_sort_by_key(const int* key, int T, int nbins, int* bins, int* perm, cudaStream_t stream);
 cudaError_t launch_refine_dmma(const float* fr, const double* fc, const float* lr, const double* lc,
                                const double* lwbar, const double* w, const double* gx, const int* fmap,

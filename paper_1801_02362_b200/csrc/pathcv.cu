@@ -102,7 +102,7 @@ cv_weights_kernel(int T, int t0, int L, double lam, double cutoff, int cap, int 
       double dot = 0.0;
 #pragma unroll
       for (int e = 0; e < 9; ++e) dot = fma(Rh[e], Si[e], dot);
-      d = gx[t] + ga[i] - 2.0 * dot;
+      d = gx[t] + ga[off + i] - 2.0 * dot;
       Dt[i] = d;
     } else {
       d = Dt[i];
@@ -425,7 +425,7 @@ cv_weights_close_warp_kernel(int T, int t0, double lam, double cutoff, int cap, 
       double dot = 0.0;
 #pragma unroll
       for (int e = 0; e < 9; ++e) dot = fma(Rh[e], Si[e], dot);
-      d = gx[t] + ga[i] - 2.0 * dot;
+      d = gx[t] + ga[off + i] - 2.0 * dot;
       Dt[i] = d;
     } else {
       d = Dt[i];

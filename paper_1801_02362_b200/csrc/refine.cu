@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(CNT)
 cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, double thr0,
             const double* __restrict__ fnorm, double fcoef, const int* __restrict__ rlo, const int* __restrict__ rhi,
             const float* __restrict__ dref, int cap, int* __restrict__ lo, int* __restrict__ cnt,
-            float* __restrict__ dmin_out, uint8_t* __restrict__ flags) {
+            float* __restrict__ dmin_out, uint8_t* __restrict__ flags, const double* __restrict__ dlife) {
   __shared__ double scratch[CNT / 32];
   __shared__ int imin[CNT / 32], imax[CNT / 32];
   const int t = blockIdx.x;
@@ -42,9 +42,22 @@ cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, 
   // shard's estimate (an all-reduce of the per-frame minima), so a shard that holds
   // none of the frame's window returns an empty one
   if (dref) m = fmin(m, (double)dref[t]);
+  // close-structure lifetime window (PathCV.close_replay): frame t is
+  // a refresh frame y whose later frames x lie within D(x, y) <= delta = dlife[t].  With the
+  // RMSD triangle inequality every landmark any of them needs (lam (D~_l(x) - min D~(x))
+  // <= thr) has d(y, a_l) <= sqrt(delta) + sqrt((sqrt(delta) + d_min(y))^2 + thr / lam), so
+  // the window grows by lam (2 delta + 2 sqrt(delta) (X + dmu)), X^2 = (sqrt(delta) + dmu)^2
+  // + thr / lam, dmu = sqrt(m + e_t) >= d_min(y) (e_t = fnorm[t] the estimate error bound)
+  double thr_t = thr;
+  if (dlife) {
+    const double dl = fmax(dlife[t], 0.0), sd = sqrt(dl);
+    const double dmu = sqrt(fmax(m + (fnorm ? fnorm[t] : 0.0), 0.0));
+    const double X = sqrt((sd + dmu) * (sd + dmu) + thr / lam);
+    thr_t = thr + lam * (2.0 * dl + 2.0 * sd * (X + dmu));
+  }
   int a = L, b = -1;
   for (int i = i0 + threadIdx.x; i < i1; i += CNT) {
-    if (lam * ((double)row[i] - m) <= thr) { a = min(a, i); b = max(b, i); }
+    if (lam * ((double)row[i] - m) <= thr_t) { a = min(a, i); b = max(b, i); }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -71,9 +84,10 @@ cand_kernel(const float* __restrict__ D, int T, int L, int64_t ldd, double lam, 
 
 cudaError_t launch_candidates(const float* D, int T, int L, int64_t ldd, double lam, double thr, const double* fnorm,
                               double fcoef, const int* rlo, const int* rhi, const float* dref, int cap, int* lo,
-                              int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream) {
+                              int* cnt, float* dmin, uint8_t* flags, cudaStream_t stream, const double* dlife) {
   if (T <= 0) return cudaSuccess;
-  cand_kernel<<<T, CNT, 0, stream>>>(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, dref, cap, lo, cnt, dmin, flags);
+  cand_kernel<<<T, CNT, 0, stream>>>(D, T, L, ldd, lam, thr, fnorm, fcoef, rlo, rhi, dref, cap, lo, cnt, dmin, flags,
+                                     dlife);
   return cudaGetLastError();
 }
 

@@ -206,7 +206,8 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                  int nks, const int* __restrict__ perm, const int* __restrict__ lo, const int* __restrict__ cnt,
                  const int* __restrict__ eF, const int* __restrict__ eL, const double* __restrict__ gx,
                  const double* __restrict__ ga, int cap, double* __restrict__ Dex, double* __restrict__ Rex,
-                 float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags) {
+                 float* __restrict__ Dd, int64_t ldd, uint8_t* __restrict__ flags, double* __restrict__ Sex,
+                 const uint8_t* __restrict__ fitmask) {
   using namespace ri8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
@@ -360,6 +361,12 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           const int slot = ll - s_lo[f];
           if (slot < 0 || slot >= s_cnt[f]) continue;
           const double* S = sC + (f * LT + li) * 9;
+          if (Sex) {  // close-structure replay: the covariances of every window pair (Eq. 5 rows)
+            double* so = Sex + ((int64_t)t * cap + slot) * 9;
+#pragma unroll
+            for (int e = 0; e < 9; ++e) so[e] = S[e];
+          }
+          if (fitmask && !fitmask[t]) continue;  // fits only on the refresh rows
           double q[4];
           bool ill = false;
           double msd = fit_fast(S, gx[t], ga[ll], Rex ? q : nullptr, &ill);
@@ -439,7 +446,7 @@ cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, co
 cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,
                              int kpad, const int* perm, const int* lo, const int* cnt, const double* gx,
                              const double* ga, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,
-                             uint8_t* flags, cudaStream_t stream) {
+                             uint8_t* flags, cudaStream_t stream, double* Sex, const uint8_t* fitmask) {
   using namespace ri8;
   if (T <= 0 || L <= 0) return cudaSuccess;
   if (kpad % 32 || kpad < n || n >= 32768) return cudaErrorInvalidValue;
@@ -462,7 +469,7 @@ cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fd
   const int groups = (T + FG - 1) / FG;
   const int grid = groups < sms ? groups : sms;
   refine_i8_kernel<<<grid, NT, SMEM, stream>>>(ma, mb, T, L, kpad / 32, perm, lo, cnt, eF, eL, gx, ga, cap, Dex, Rex,
-                                               Dd, ldd, flags);
+                                               Dd, ldd, flags, Sex, fitmask);
   return cudaGetLastError();
 }
 

@@ -43,6 +43,10 @@ GRAD_I8 = os.environ.get("MC_GRAD_I8", "1") == "1"
 # exact window refits on the int8 tensor cores (exact int8 digits, csrc/refine_i8.cu);
 # env MC_REFINE_I8=0 keeps the fp64 DMMA kernel
 REFINE_I8 = os.environ.get("MC_REFINE_I8", "1") == "1"
+# pruned close-structure replay (fp32 frames, w = w'): screened lifetime windows per
+# refresh frame instead of the dense covariances; env
+# MC_CLOSE_PRUNE=0 keeps the dense path
+CLOSE_PRUNE = os.environ.get("MC_CLOSE_PRUNE", "1") == "1"
 DEFAULT_WINDOW = 8      # speculative close-structure window (frames)
 NB_MAX_L = 16384        # neighbour-list active-set bitmap capacity (csrc/pathcv.cu kNbMaxL)
 
@@ -181,6 +185,7 @@ class PathCV:
         self.lraw = lm.contiguous() if (lm.dtype == torch.float32 and CLOSE_DMMA and self.n % 4 == 0
                                         and self.wuni > 0.0) else None
         self.ldig = K.ldig_prep(self.lraw, self.lm.centroid) if (self.lraw is not None and GRAD_I8) else None
+        self._tc = None  # one-term screen + int8 refit engine of the pruned close replay (lazy)
 
     # ------------------------------------------------------------------
     def _frames(self, frames):
@@ -247,6 +252,13 @@ class PathCV:
             steps = int(fr_in.shape[0]) // walkers
         raw, fr = self._frames(fr_in)
         close = K.close_decisions(fr, self.w, eps, walkers, steps, window)
+        if neighbours is None and self._close_prunable(raw):
+            out = self._close_replay_pruned(raw, fr, close, grad, cap, out_dtype)
+            if grad and _or_flags(close["xyflags"]) & FLAG_DEGENERATE:
+                raise DegenerateFitError("close-structure fit x<->y has a degenerate spectrum")
+            out.update(refresh=close["refresh"].bool(), dxy=close["dxy"], ridx=close["ridx"],
+                       onthefly=close["onthefly"])
+            return out
         S = self._cov(raw, fr)
         D, R, _, flags = K.fit_dense(S, fr.g, self.lm.g, rowmask=close["refresh"], want_rot=True)
         _raise_flags(flags, "close_structure_replay")
@@ -270,10 +282,60 @@ class PathCV:
         out.update(refresh=close["refresh"].bool(), dxy=close["dxy"], ridx=close["ridx"], onthefly=close["onthefly"])
         return out
 
+    def _close_prunable(self, raw):
+        return (CLOSE_PRUNE and REFINE_I8 and self._dmma(raw) and self.n < 32768
+                and bool(torch.equal(self.w, self.wa)))
+
+    def _close_replay_pruned(self, raw, fr, close, grad, cap, out_dtype):
+        """Alg. 2 replay with screened windows instead of the dense [T, L] covariances.
+
+        With one weight vector aligning and measuring, the optimally aligned RMSD d is a
+        metric, and for a frame x that keeps the close structure y (D(x, y) <= delta):
+        d~_l(x) >= d(x, a_l) >= d(y, a_l) - sqrt(delta) and min_l d~_l(x) <= sqrt(delta) +
+        d_min(y) (Eq. 5 with R_xy, R_{a y} optimal).  So every landmark x can need has
+        d(y, a_l) <= sqrt(delta) + sqrt((sqrt(delta) + d_min(y))^2 + thr / lam): a window
+        of y fixed for y's whole lifetime (delta = the largest D(x, y) of its frames).  Only
+        the refresh frames are screened (one-term FP16 tcgen05 estimate with its rigorous
+        bound); every frame's covariances with its close structure's window, and the
+        refresh frames' fits, come from one int8 tensor-core pass (mc_refine_i8_close);
+        the K4 weights evaluate Eq. 5 on the window slots."""
+        if self._tc is None:
+            self._tc = PathCVTC(self.lraw, self.lam, self.q, self.w[:self.n], self.wa[:self.n], cutoff=self.cutoff,
+                                prune=False, device=self.device)
+        tc = self._tc
+        T = raw.shape[0]
+        refresh, ridx = close["refresh"], close["ridx"]
+        rows = torch.nonzero(refresh).squeeze(1)
+        keep = refresh == 0
+        dlife = torch.zeros((T,), dtype=torch.float64, device=self.device)
+        dlife.scatter_reduce_(0, ridx[keep].long(), close["dxy"][keep], reduce="amax")
+        Dest, _, fsr = tc.estimate(raw[rows], terms=tc.screen_terms, check=False)
+        one = tc.screen == "f16x1"
+        lo_r, cnt_r, _, cflags = K.candidates_life(Dest, self.lam, tc.cutoff + tc.margin, self.L, dlife[rows],
+                                                   fnorm=tc.frame_bound(fsr) if one else None,
+                                                   fcoef=2.0 * self.lam if one else 0.0)
+        del Dest
+        src = (torch.cumsum(refresh.to(torch.int32), 0) - 1)[ridx.long()].long()
+        lo, cnt = lo_r[src].contiguous(), cnt_r[src].contiguous()
+        ld = max(1, int(cnt.max().item()))
+        perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
+        fdig = K.row_digits(raw, fr.centroid, None, perm=perm, count=T)
+        S, D, R, rflags = K.refine_i8_close(tc.rdl, fdig, T, self.L, self.n, fr.g, self.lm.g, perm, lo, cnt, ld,
+                                            refresh)
+        del fdig
+        f = _or_flags(cflags) | _or_flags(rflags)
+        if f & FLAG_NON_FINITE:
+            raise InvalidStructureError("close_structure_replay: non-finite coordinates or distances")
+        if f & FLAG_NO_CONVERGE:
+            raise MetadynError("close_structure_replay: Jacobi diagonalisation did not converge")
+        out = self._finish(raw, fr, D, R, S, close, grad, cap, out_dtype, rowlo=lo, rowcnt=cnt)
+        out["window_lo"], out["window_cnt"] = lo, cnt
+        return out
+
     # significant-list buffers per chunk are bounded to ~this many bytes
     CHUNK_BYTES = 4 << 30
 
-    def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype, nb=None):
+    def _finish(self, raw, fr, D, R, S, close, grad, cap, out_dtype, nb=None, rowlo=None, rowcnt=None):
         T = D.shape[0]
         raw = raw.contiguous()
         cap0 = self._cap(cap)
@@ -292,7 +354,8 @@ class PathCV:
             chunk = min(T - t0, max(8, self.CHUNK_BYTES // (cap * 160)))
             while True:
                 wres = K.pathcv_weights(D, self.q, self.lam, R, fr, self.lm, cap, self.cutoff, close=close, S=S,
-                                        t0=t0, count=chunk, s=s, z=z, nb=nb, dmode=2 if nb is not None else 0)
+                                        t0=t0, count=chunk, s=s, z=z, nb=nb, dmode=2 if nb is not None else 0,
+                                        L=self.L, rowlo=rowlo, rowcnt=rowcnt)
                 f = _or_flags(wres["flags"])
                 if f & FLAG_SIG_OVERFLOW and cap < self.L:
                     cap = self.L
@@ -639,9 +702,11 @@ class PathCVTC:
         fr, fs = self._frames(frames, terms, check)
         return K.msd_estimate(fs, self._lsplit(terms if self.fmt == "f16" else 3)), fr, fs
 
-    def msd_matrix(self, frames, exact=True):
+    def msd_matrix(self, frames, exact=True, out=None):
+        """[T, L] fp32 aligned MSDs: exact=True every pair refit exactly (int8 tensor cores,
+        or DMMA), exact=False the split-precision estimate.  out: optional [T, L] buffer."""
         fr, fs = self._frames(frames)
-        D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device)
+        D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device) if out is None else out
         if not exact:
             return K.msd_estimate(fs, self._lsplit(3), D)
         if self.rdl is not None:

@@ -452,6 +452,20 @@ def candidates(D, lam, thr, cap, L=None, fnorm=None, fcoef=0.0, rlo=None, rhi=No
     return lo, cnt, dmin, flags
 
 
+def candidates_life(D, lam, thr, cap, dlife, fnorm=None, fcoef=0.0):
+    """mc_candidates with the close-structure lifetime window: row t a refresh frame y,
+    dlife [T] fp64 the largest D(x, y) of the frames x that keep y."""
+    T, L = D.shape
+    dev = D.device
+    lo = torch.empty((T,), dtype=I32, device=dev)
+    cnt = torch.empty((T,), dtype=I32, device=dev)
+    dmin = torch.empty((T,), dtype=torch.float32, device=dev)
+    flags = torch.empty((T,), dtype=U8, device=dev)
+    call("mc_candidates_life", ptr(D), T, L, D.stride(0), float(lam), float(thr), ptr(fnorm), float(fcoef),
+         ptr(dlife.contiguous()), cap, ptr(lo), ptr(cnt), ptr(dmin), ptr(flags), stream_ptr())
+    return lo, cnt, dmin, flags
+
+
 def sort_by_key(key, nbins):
     T = key.shape[0]
     bins = torch.empty((nbins,), dtype=I32, device=key.device)
@@ -494,6 +508,19 @@ def refine_i8(ldig, fdig, T, L, n, gx, ga, perm=None, lo=None, cnt=None, cap=0, 
          ptr(lo), ptr(cnt), ptr(gx), ptr(ga), cap, ptr(Dex), ptr(Rex), ptr(Dd),
          Dd.stride(0) if Dd is not None else 0, ptr(flags), stream_ptr())
     return Dex, Rex, flags
+
+
+def refine_i8_close(ldig, fdig, T, L, n, gx, ga, perm, lo, cnt, cap, fitmask):
+    """Pruned close-structure replay: S [T, cap, 9] of every window pair, fits (D [T, cap],
+    R [T, cap, 9]) on the rows with fitmask (mc_refine_i8_close)."""
+    dev = gx.device
+    Sex = torch.empty((T, cap, 9), dtype=F64, device=dev)
+    Dex = torch.empty((T, cap), dtype=F64, device=dev)
+    Rex = torch.empty((T, cap, 9), dtype=F64, device=dev)
+    flags = torch.zeros((T,), dtype=U8, device=dev)
+    call("mc_refine_i8_close", ptr(ldig.dig), ptr(ldig.e), ptr(fdig.dig), ptr(fdig.e), T, L, n, ldig.kpad, ptr(perm),
+         ptr(lo), ptr(cnt), ptr(gx), ptr(ga), cap, ptr(fitmask), ptr(Sex), ptr(Dex), ptr(Rex), ptr(flags), stream_ptr())
+    return Sex, Dex, Rex, flags
 
 
 def refine(frames, fsplit, landmarks, lsplit, w, perm=None, lo=None, cnt=None, cap=0, want_rot=True, Dd=None,

@@ -243,14 +243,15 @@ def test_close_replay_dmma_path_equals_fp64_path(cuda_device):
     lm = torch.from_numpy(wl.landmarks).to(cuda_device)
     a = engine.PathCV(lm, wl.lam, wl.q)
     assert a.lraw is not None
-    saved = engine.CLOSE_DMMA
+    saved = engine.CLOSE_DMMA, engine.CLOSE_PRUNE
     try:
         engine.CLOSE_DMMA = False
         b = engine.PathCV(lm, wl.lam, wl.q)
+        engine.CLOSE_DMMA, engine.CLOSE_PRUNE = saved[0], False  # the dense DMMA path
+        oa = a.close_replay(wl.frames, wl.eps, grad=True)
     finally:
-        engine.CLOSE_DMMA = saved
+        engine.CLOSE_DMMA, engine.CLOSE_PRUNE = saved
     assert b.lraw is None
-    oa = a.close_replay(wl.frames, wl.eps, grad=True)
     ob = b.close_replay(wl.frames, wl.eps, grad=True)
     np.testing.assert_array_equal(oa["refresh"].cpu().numpy(), ob["refresh"].cpu().numpy())
     assert 0 < int(oa["refresh"].sum()) < oa["refresh"].numel()
@@ -258,6 +259,44 @@ def test_close_replay_dmma_path_equals_fp64_path(cuda_device):
     np.testing.assert_allclose(oa["z"].cpu().numpy(), ob["z"].cpu().numpy(), rtol=1e-10, atol=1e-15)
     for key in ("ds", "dz"):
         assert_grad(oa[key].cpu().numpy(), ob[key].cpu().numpy(), rtol=1e-6)
+
+
+@pytest.mark.parametrize("seed,W,steps,n,L", [(5, 4, 60, 96, 120), (7, 3, 80, 200, 400), (9, 2, 50, 64, 1000)])
+def test_close_replay_pruned_equals_dense(seed, W, steps, n, L, cuda_device):
+    """Pruned close-structure replay (screened lifetime windows of the refresh frames,
+    covariances and refresh fits on the int8 tensor cores) = the dense replay (every
+    landmark's covariance on DMMA): identical refresh log, s and z to 2e-7 relative / 1e-10
+    absolute (the int8 digits are exact to 2^-31 of each row's maximum: ~1e-10 on D, against
+    fp64 DMMA), gradients to 1e-6 of the per-frame maximum; every frame's significant
+    landmarks inside its window."""
+    from paper_1801_02362_b200 import synth as S
+
+    wl = S.walkers_device(seed, 64, steps, n, L, cuda_device, walker_offset=1, walker_count=W)
+    lm = torch.from_numpy(wl.landmarks).to(cuda_device)
+    pcv = engine.PathCV(lm, wl.lam, wl.q)
+    assert pcv._close_prunable(wl.frames.reshape(-1, n, 3))
+    op = pcv.close_replay(wl.frames, wl.eps, grad=True)
+    assert "window_cnt" in op
+    saved = engine.CLOSE_PRUNE
+    try:
+        engine.CLOSE_PRUNE = False
+        od = pcv.close_replay(wl.frames, wl.eps, grad=True)
+    finally:
+        engine.CLOSE_PRUNE = saved
+    assert "window_cnt" not in od
+    np.testing.assert_array_equal(op["refresh"].cpu().numpy(), od["refresh"].cpu().numpy())
+    assert 0 < int(op["refresh"].sum()) < op["refresh"].numel()
+    np.testing.assert_allclose(op["s"].cpu().numpy(), od["s"].cpu().numpy(), rtol=2e-7, atol=1e-10)
+    np.testing.assert_allclose(op["z"].cpu().numpy(), od["z"].cpu().numpy(), rtol=2e-7, atol=1e-10)
+    for key in ("ds", "dz"):
+        assert_grad(op[key].cpu().numpy(), od[key].cpu().numpy(), rtol=1e-6)
+    # the dense distances of every landmark within the cutoff lie in the window
+    D = od["D"].cpu().numpy()
+    lo, cnt = op["window_lo"].cpu().numpy(), op["window_cnt"].cpu().numpy()
+    sig = wl.lam * (D - D.min(axis=1, keepdims=True)) <= pcv.cutoff
+    idx = np.arange(D.shape[1])[None, :]
+    inside = (idx >= lo[:, None]) & (idx < (lo + cnt)[:, None])
+    assert np.all(inside[sig])
 
 
 def test_cuda_graph_replay_equals_eager(cuda_device):
