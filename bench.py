@@ -274,7 +274,7 @@ class Config3:
             return "fp64_flop", 18.0 * n * T * L
         if name == "mc_cov_dmma":  # dense S [T, L, 9]: 9 fp64 FMA per atom and pair on DMMA
             return "fp64_tensor_flop", 18.0 * n * T * L
-        if name == "mc_pathcv_grad_i8" and self.last is not None:
+        if name in ("mc_pathcv_grad_i8", "mc_pathcv_grad_i8_wide") and self.last is not None:
             # executed int8 MMA work: per (frame, significant landmark, atom) 18 multiply-adds
             # (2 CVs x 3 x 3) x the 10 kept digit products (tcgen05.mma kind::i8)
             return "int8_tensor_op", 2.0 * 10.0 * 18.0 * n * float(self.last["nsig"].double().sum().item())
@@ -623,7 +623,7 @@ class ConfigTC:
                 tiles = int(self.last["screen_tiles"].item())
                 pairs = T * self.pcv.coarse.numel() + tiles * 128 * 48  # coarse + banded
             return "tensor_flop_f16", terms * 18.0 * n * pairs
-        if name == "mc_pathcv_grad_i8" and self.last is not None:
+        if name in ("mc_pathcv_grad_i8", "mc_pathcv_grad_i8_wide") and self.last is not None:
             # executed int8 MMA work: per (frame, significant landmark, atom) 18 multiply-adds
             # (2 CVs x 3 x 3) x the 10 kept digit products (tcgen05.mma kind::i8)
             return "int8_tensor_op", 2.0 * 10.0 * 18.0 * n * float(self.last["nsig"].double().sum().item())

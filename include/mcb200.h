@@ -257,6 +257,25 @@ int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, cons
                  int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt, const double* gx,
                  const double* ga, int32_t cap, double* Dex, double* Rex, float* Dd, int64_t ldd, uint8_t* flags,
                  void* stream);
+/* Wide frame groups of mc_pathcv_grad_i8 (significant union wider than 117 landmarks, e.g.
+ * the close-structure replay of config 3 with ~430 significant landmarks per frame):
+ * mc_grad_i8_wide_plan writes per frame group (8 frames for ncv = 2, 16 for ncv = 1, in
+ * perm order) the bytes of its A-digit image if it is wide, else 0 (bytes [groups]);
+ * the caller lists the wide groups (wide_ids [nwide]), places their images (wide_off
+ * [nwide] byte offsets into wimg, 16-byte aligned; sum of bytes) and calls
+ * mc_pathcv_grad_i8 with a non-NULL wide_flag (the narrow groups; wide ones are left
+ * out) and mc_pathcv_grad_i8_wide (the listed groups: the A digits streamed with the B
+ * boxes instead of resident; hws = mc_grad_i8_wide_header_size bytes).  Same outputs
+ * and exactness as mc_pathcv_grad_i8. */
+int mc_grad_i8_wide_plan(int32_t T, int32_t cap, int32_t ncv, const int32_t* sig_idx, const int32_t* nsig,
+                         const int32_t* perm, int64_t* bytes, void* stream);
+int64_t mc_grad_i8_wide_header_size(int32_t nwide, int32_t ncv);
+int mc_pathcv_grad_i8_wide(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const double* w,
+                           const double* w_align, const int8_t* dig, const int32_t* eB, int32_t npad, int32_t kpad,
+                           const int32_t* sig_idx, const double* sig_coef, const int32_t* nsig, const double* fvec,
+                           const double* dV, const int32_t* perm, const int32_t* out_map, void* out0, void* out1,
+                           int32_t out_f32, int32_t ncv, const int32_t* wide_ids, int32_t nwide,
+                           const int64_t* wide_off, void* hws, int64_t hws_bytes, void* wimg, void* stream);
 /* mc_refine_i8 for the pruned close-structure replay (PathCV.close_replay, fp32 frames;
  * replaces the dense covariances of _kearsley_matrix, geometry.py:180-196, for the Eq. 5
  * rows of SPEC.md:124-132): the exact covariances S of every window pair to Sex

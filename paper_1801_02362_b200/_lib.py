@@ -76,6 +76,9 @@ _SIGS = {
     + [_P] * 18,
     "mc_shard_rescale": [_I32, _I32, _P, _P, _P, _P, _P, _P],
     "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
+    "mc_grad_i8_wide_plan": [_I32, _I32, _I32, _P, _P, _P, _P, _P],
+    "mc_pathcv_grad_i8_wide": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+                               _P, _I32, _I32, _P, _I32, _P, _P, _I64, _P, _P],
     "mc_candidates_life": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _I32, _P, _P, _P, _P, _P],
     "mc_refine_i8_close": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P],
     "mc_prune_plan": [_P, _I32, _I32, _I64, _P, _P, _P, _P, _D, _P, _P, _I32, _I32, _D, _I32, _I32, _P, _P, _P, _P, _P,
@@ -125,13 +128,15 @@ def load():
     lib.mc_version.restype = ctypes.c_int
     lib.mc_grad_i8_workspace_size.argtypes = [_I32, _I32]
     lib.mc_grad_i8_workspace_size.restype = _I64
+    lib.mc_grad_i8_wide_header_size.argtypes = [_I32, _I32]
+    lib.mc_grad_i8_wide_header_size.restype = _I64
     _lib = lib
     return lib
 
 
 def exported_symbols():
     """Names declared in include/mcb200.h that the loaded library must export."""
-    return ["mc_version", "mc_grad_i8_workspace_size", *_SIGS.keys()]
+    return ["mc_version", "mc_grad_i8_workspace_size", "mc_grad_i8_wide_header_size", *_SIGS.keys()]
 
 
 def check(status, what=""):

@@ -251,6 +251,38 @@ int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, cons
                                           ldd, flags, S_(stream)));
 }
 
+int mc_grad_i8_wide_plan(int32_t T, int32_t cap, int32_t ncv, const int32_t* sig_idx, const int32_t* nsig,
+                         const int32_t* perm, int64_t* bytes, void* stream) {
+  if (T < 0 || cap < 1 || (ncv != 1 && ncv != 2)) return MC_ERR_CONFIG;
+  if (T > 0 && (!sig_idx || !nsig || !bytes)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_grad_i8_plan(T, cap, ncv, sig_idx, nsig, perm, reinterpret_cast<long long*>(bytes),
+                                             S_(stream)));
+}
+
+int64_t mc_grad_i8_wide_header_size(int32_t nwide, int32_t ncv) {
+  if (nwide < 0 || (ncv != 1 && ncv != 2)) return -1;
+  return (int64_t)mc::grad_i8_wide_header_bytes(nwide, ncv);
+}
+
+int mc_pathcv_grad_i8_wide(int32_t T, int32_t n, int32_t cap, const float* fraw, const double* fcen, const double* w,
+                           const double* w_align, const int8_t* dig, const int32_t* eB, int32_t npad, int32_t kpad,
+                           const int32_t* sig_idx, const double* sig_coef, const int32_t* nsig, const double* fvec,
+                           const double* dV, const int32_t* perm, const int32_t* out_map, void* out0, void* out1,
+                           int32_t out_f32, int32_t ncv, const int32_t* wide_ids, int32_t nwide,
+                           const int64_t* wide_off, void* hws, int64_t hws_bytes, void* wimg, void* stream) {
+  if (T < 0 || n < 2 || cap < 1 || nwide < 0 || (ncv != 1 && ncv != 2)) return MC_ERR_CONFIG;
+  if (nwide == 0) return MC_OK;
+  if (!fraw || !fcen || !w || !w_align || !dig || !eB || !sig_idx || !sig_coef || !nsig || !fvec || !out0 ||
+      (ncv == 2 && !out1) || (ncv == 1 && !dV) || !wide_ids || !wide_off || !hws || !wimg)
+    return MC_ERR_CONFIG;
+  if (n % 4 != 0 || npad < n || npad % 128 != 0 || kpad % 32 != 0) return MC_ERR_CONFIG;
+  if (hws_bytes < (int64_t)mc::grad_i8_wide_header_bytes(nwide, ncv)) return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_cv_grad_i8_wide(T, n, cap, fraw, fcen, w, w_align, dig, eB, npad, kpad, sig_idx,
+                                                sig_coef, nsig, fvec, dV, perm, out_map, out0, out1, out_f32, ncv,
+                                                wide_ids, nwide, reinterpret_cast<const long long*>(wide_off), hws,
+                                                wimg, S_(stream)));
+}
+
 int64_t mc_grad_i8_workspace_size(int32_t T, int32_t ncv) {
   if (T < 0 || (ncv != 1 && ncv != 2)) return -1;
   return (int64_t)mc::grad_i8_workspace(T, ncv);

@@ -74,12 +74,14 @@ template <>
 struct Cfg<2> {
   static constexpr int DG = 8;
   static constexpr int NST = 7;
+  static constexpr int NST_W = 8;  // stages of the streamed-A (wide) kernel
   static constexpr int X_BUF = DG * BMA * 12;
 };
 template <>
 struct Cfg<1> {
   static constexpr int DG = 16;
   static constexpr int NST = 6;
+  static constexpr int NST_W = 7;
   static constexpr int X_BUF = DG * BMA * 12;
 };
 
@@ -93,13 +95,18 @@ template <int DG>
 struct __align__(16) GHdr {
   int t[DG], raw[DG];
   int wlo, koff, k0, nks, active, pad_[3];
+  long long img, pad2_;  // wide groups: byte offset of the group's image in the wide workspace
   double cx[DG][3];
   RowC rc[R];
 };
 
-template <int NCV>
+// wide groups (union wider than WMAX landmarks): the A digits are not resident; each
+// pipeline stage carries the B box and the group's A block of that k-step
+constexpr int W_STAGE = L_STAGE + C_KS;  // 22 KB
+template <int NCV, bool WIDE = false>
 constexpr int smem_bytes() {
-  return Cfg<NCV>::NST * L_STAGE + C_IMG + 2 * Cfg<NCV>::X_BUF + (int)sizeof(GHdr<Cfg<NCV>::DG>) + 32 * 8 + 1024;
+  return (WIDE ? Cfg<NCV>::NST_W * W_STAGE : Cfg<NCV>::NST * L_STAGE + C_IMG) + 2 * Cfg<NCV>::X_BUF +
+         (int)sizeof(GHdr<Cfg<NCV>::DG>) + 32 * 8 + 1024;
 }
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -219,6 +226,8 @@ __device__ __forceinline__ void digits4(double v, double qs, int8_t* d) {
   }
   d[0] = (int8_t)X;
 }
+static_assert(smem_bytes<1, true>() <= 227 * 1024 && smem_bytes<2, true>() <= 227 * 1024 &&
+              smem_bytes<1>() <= 227 * 1024 && smem_bytes<2>() <= 227 * 1024, "shared memory per CTA");
 }  // namespace gi8
 
 // B digits of a landmark set: per-atom exponent eB[k] over every (landmark, axis)
@@ -326,6 +335,7 @@ cstack_prep_kernel(int T, int cap, const double* __restrict__ fcen, const int* _
     h.k0 = b >= 0 ? 3 * a - h.koff : 0;
     h.nks = h.active ? (3 * width + h.koff + KS - 1) / KS : 0;
     h.pad_[0] = h.pad_[1] = h.pad_[2] = 0;
+    h.img = h.pad2_ = 0;
   }
   __syncthreads();
   const int nks = h.nks, wlo = h.wlo, koff = h.koff, tot = s_cum[DG];
@@ -393,7 +403,195 @@ cstack_prep_kernel(int T, int cap, const double* __restrict__ fcen, const int* _
   for (int e = tid; e < nks * C_KS / 16; e += 128) cd[e] = reinterpret_cast<const int4*>(img)[e];
 }
 
-template <typename OT, int NCV>
+// Wide-group plan (one thread per frame group): bytes of the group's A image when its
+// significant union is wider than WMAX landmarks (the narrow kernel skips those), else 0.
+template <int NCV>
+__global__ void grad_i8_plan_kernel(int T, int cap, const int* __restrict__ sig_idx, const int* __restrict__ nsig,
+                                    const int* __restrict__ perm, long long* __restrict__ bytes) {
+  using namespace gi8;
+  constexpr int DG = Cfg<NCV>::DG;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (T + DG - 1) / DG) return;
+  int a = 0x7fffffff, b = -1;
+  for (int f = 0; f < DG; ++f) {
+    const int k = g * DG + f;
+    if (k >= T) break;
+    const int t = perm ? perm[k] : k;
+    const int ns = nsig[t];
+    if (ns <= 0) continue;
+    a = min(a, sig_idx[(int64_t)t * cap]);
+    b = max(b, sig_idx[(int64_t)t * cap + ns - 1] + 1);
+  }
+  long long by = 0;
+  if (b >= 0 && b - a > WMAX) {
+    const int koff = (3 * a) & 31;
+    by = (long long)((3 * (b - a) + koff + KS - 1) / KS) * C_KS;
+  }
+  bytes[g] = by;
+}
+
+// A digits of one WIDE frame group (one CTA per listed group): as cstack_prep_kernel, but
+// the image (nks > NKS_MAX k-steps) is built NKS_MAX k-steps at a time in shared memory
+// and copied to the wide workspace at wide_off[i]; header hdrs[i] (compact order).
+template <int NCV>
+__global__ void __launch_bounds__(128)
+cstack_prep_wide_kernel(int T, int cap, const double* __restrict__ fcen, const int* __restrict__ sig_idx,
+                        const double* __restrict__ sig_coef, const int* __restrict__ nsig,
+                        const double* __restrict__ fvec, const double* __restrict__ dV, const int* __restrict__ perm,
+                        const int* __restrict__ out_map, const int* __restrict__ wide_ids,
+                        const long long* __restrict__ wide_off, gi8::GHdr<gi8::Cfg<NCV>::DG>* __restrict__ hdrs,
+                        uint8_t* __restrict__ wimg) {
+  using namespace gi8;
+  constexpr int DG = Cfg<NCV>::DG;
+  constexpr int EPR = 9 * NCV;
+  extern __shared__ __align__(16) uint8_t img[];  // [NKS_MAX][192 rows x 32 B]
+  __shared__ GHdr<DG> h;
+  __shared__ int s_ns[DG], s_cum[DG + 1], s_pa[DG], s_pb[DG], s_ccum[DG + 1];
+  __shared__ double s_fv[DG][8], s_dv[DG][2];
+  __shared__ unsigned long long s_rmax[R];
+  __shared__ double s_qs[R];
+  const int g = wide_ids[blockIdx.x], tid = threadIdx.x;
+  if (tid < DG) {
+    const int k = g * DG + tid;
+    int t = -1, ns = 0;
+    if (k < T) {
+      t = perm ? perm[k] : k;
+      ns = nsig[t];
+    }
+    h.t[tid] = t;
+    h.raw[tid] = t < 0 ? -1 : (out_map ? out_map[t] : t);
+    s_ns[tid] = t < 0 ? 0 : ns;
+    for (int a = 0; a < 3; ++a) h.cx[tid][a] = t < 0 ? 0.0 : fcen[3 * t + a];
+    for (int e = 0; e < 8; ++e) s_fv[tid][e] = t < 0 ? 0.0 : fvec[(int64_t)t * FVEC + e];
+    s_dv[tid][0] = (NCV == 1 && t >= 0) ? dV[2 * t] : 0.0;
+    s_dv[tid][1] = (NCV == 1 && t >= 0) ? dV[2 * t + 1] : 0.0;
+  }
+  if (tid < R) s_rmax[tid] = 0ull;
+  __syncthreads();
+  if (tid == 0) {
+    int a = 0x7fffffff, b = -1, tot = 0;
+    for (int f = 0; f < DG; ++f) {
+      if (s_ns[f] > 0) {
+        a = min(a, sig_idx[(int64_t)h.t[f] * cap]);
+        b = max(b, sig_idx[(int64_t)h.t[f] * cap + s_ns[f] - 1] + 1);
+      }
+      s_cum[f] = tot;
+      tot += s_ns[f] * EPR;
+    }
+    s_cum[DG] = tot;
+    h.active = 1;
+    h.wlo = a;
+    h.koff = (3 * a) & 31;
+    h.k0 = 3 * a - h.koff;
+    h.nks = (3 * (b - a) + h.koff + KS - 1) / KS;
+    h.pad_[0] = h.pad_[1] = h.pad_[2] = 0;
+    h.img = wide_off[blockIdx.x];
+    h.pad2_ = 0;
+  }
+  __syncthreads();
+  const int nks = h.nks, wlo = h.wlo, koff = h.koff;
+  // entry e of the frame-major list restricted to sig positions [pa_f, pb_f) (cum: prefix)
+  auto entry = [&](int e, const int* pa, const int* cum, int& row, int& kk) -> double {
+    int f = 0;
+#pragma unroll
+    for (int q = 1; q < DG; ++q) f += e >= cum[q];
+    const int el = e - cum[f];
+    const int s = pa[f] + el / EPR, j = el % EPR;
+    const int64_t base = (int64_t)h.t[f] * cap + s;
+    const int l = sig_idx[base];
+    double v;
+    if (NCV == 2) {
+      v = sig_coef[base * 18 + j];
+      row = f * 6 + (j / 9) * 3 + (j % 9) / 3;
+    } else {
+      v = -(s_dv[f][0] * sig_coef[base * 18 + j] + s_dv[f][1] * sig_coef[base * 18 + 9 + j]);
+      row = f * 3 + j / 3;
+    }
+    kk = 3 * (l - wlo) + j % 3 + koff;
+    return v;
+  };
+  if (tid < DG) s_pa[tid] = 0;
+  __syncthreads();
+  for (int e = tid; e < s_cum[DG]; e += 128) {
+    int row, kk;
+    const double v = entry(e, s_pa, s_cum, row, kk);
+    atomicMax(&s_rmax[row], (unsigned long long)__double_as_longlong(fabs(v)));
+  }
+  __syncthreads();
+  if (tid < R) s_qs[tid] = ldexp(1.0, 31 - digit_exp(__longlong_as_double((long long)s_rmax[tid])));
+  uint8_t* dst0 = wimg + h.img;
+  for (int c0 = 0; c0 < nks; c0 += NKS_MAX) {
+    const int nc = min(NKS_MAX, nks - c0);
+    const int k_lo = KS * c0, k_hi = KS * (c0 + nc);  // this chunk's K bytes
+    for (int e = tid; e < nc * C_KS / 16; e += 128) reinterpret_cast<int4*>(img)[e] = make_int4(0, 0, 0, 0);
+    if (tid < DG) {
+      // sig positions whose landmark touches [k_lo, k_hi): 3 (l - wlo) + koff + 2 >= k_lo and
+      // 3 (l - wlo) + koff < k_hi (the ascending list, binary searches)
+      const int64_t base = (int64_t)max(h.t[tid], 0) * cap;
+      const int ns = s_ns[tid];
+      const int lmin = wlo + max(0, (k_lo - koff - 2 + 2) / 3), lmax = wlo + (k_hi - koff + 2) / 3;  // [lmin, lmax)
+      int lo = 0, hi = ns;
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (sig_idx[base + m] < lmin) lo = m + 1; else hi = m;
+      }
+      const int pa = lo;
+      hi = ns;
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (sig_idx[base + m] < lmax) lo = m + 1; else hi = m;
+      }
+      s_pa[tid] = pa;
+      s_pb[tid] = lo;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int f = 0; f < DG; ++f) {
+        s_ccum[f] = tot;
+        tot += (s_pb[f] - s_pa[f]) * EPR;
+      }
+      s_ccum[DG] = tot;
+    }
+    __syncthreads();
+    for (int e = tid; e < s_ccum[DG]; e += 128) {
+      int row, kk;
+      const double v = entry(e, s_pa, s_ccum, row, kk);
+      if (kk < k_lo || kk >= k_hi) continue;
+      int8_t d[4];
+      digits4(v, s_qs[row], d);
+#pragma unroll
+      for (int p = 0; p < NDIG; ++p) img[swz32(p * R + row, kk - k_lo, C_KS)] = (uint8_t)d[p];
+    }
+    __syncthreads();
+    int4* cd = reinterpret_cast<int4*>(dst0 + (int64_t)c0 * C_KS);
+    for (int e = tid; e < nc * C_KS / 16; e += 128) cd[e] = reinterpret_cast<const int4*>(img)[e];
+    __syncthreads();
+  }
+  if (tid < R) {
+    const int f = NCV == 2 ? tid / 6 : tid / 3;
+    const int cv = NCV == 2 ? (tid % 6) / 3 : 0;
+    const int b = tid % 3;
+    const int e = digit_exp(__longlong_as_double((long long)s_rmax[tid]));
+    double sc, corr;
+    if (NCV == 2) {
+      sc = s_fv[f][cv];
+      corr = s_fv[f][2 + cv * 3 + b];
+    } else {
+      sc = -(s_dv[f][0] * s_fv[f][0] + s_dv[f][1] * s_fv[f][1]);
+      corr = -(s_dv[f][0] * s_fv[f][2 + b] + s_dv[f][1] * s_fv[f][5 + b]);
+    }
+    h.rc[tid].scp = ldexp(sc, -e);
+    h.rc[tid].P = ldexpf(1.0f, e);
+    h.rc[tid].corr = (float)corr;
+  }
+  __syncthreads();
+  const int4* hs = reinterpret_cast<const int4*>(&h);
+  int4* hd = reinterpret_cast<int4*>(hdrs + blockIdx.x);
+  for (int e = tid; e < (int)(sizeof(GHdr<DG>) / 16); e += 128) hd[e] = hs[e];
+}
+
+template <typename OT, int NCV, bool WIDE>
 __global__ void __launch_bounds__(gi8::NT, 1)
 cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int npad, const float* __restrict__ fraw,
                   const double* __restrict__ w, const double* __restrict__ wa, const int* __restrict__ eB,
@@ -401,14 +599,15 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
                   OT* __restrict__ out0, OT* __restrict__ out1) {
   using namespace gi8;
   constexpr int DG = Cfg<NCV>::DG;
-  constexpr int NST = Cfg<NCV>::NST;
+  constexpr int NST = WIDE ? Cfg<NCV>::NST_W : Cfg<NCV>::NST;
+  constexpr int STG = WIDE ? W_STAGE : L_STAGE;  // stage bytes (WIDE: B box + the k-step's A block)
   constexpr int X_BUF = Cfg<NCV>::X_BUF;
   using Hdr = GHdr<DG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sL = sm;                 // [NST][128 atoms][4 digits x 32 B] (SWIZZLE_128B)
-  uint8_t* sC = sL + NST * L_STAGE;  // [NKS_MAX][192 rows x 32 B]
-  uint8_t* sX = sC + C_IMG;          // [2][DG][128 atoms x 3] fp32
+  uint8_t* sL = sm;                  // [NST][128 atoms][4 digits x 32 B] (SWIZZLE_128B) [+ A block]
+  uint8_t* sC = sL + NST * STG;      // [NKS_MAX][192 rows x 32 B] (narrow groups only)
+  uint8_t* sX = sC + (WIDE ? 0 : C_IMG);  // [2][DG][128 atoms x 3] fp32
   Hdr* hdr = reinterpret_cast<Hdr*>(sX + 2 * X_BUF);
   uint64_t* lfull = reinterpret_cast<uint64_t*>(hdr + 1);
   uint64_t* lempty = lfull + NST;
@@ -421,7 +620,7 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
   __shared__ uint32_t tmem_slot;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int groups = (T + DG - 1) / DG;
+  const int groups = WIDE ? T : (T + DG - 1) / DG;  // WIDE: T = the number of listed groups
   const int ntile = (n + BMA - 1) / BMA;
 
   if (warp == 0 && lane == 0) {
@@ -457,17 +656,19 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
         const Hdr* hg = hdrs + g;
         const int active = hg->active, nks = hg->nks, k0 = hg->k0;
         mb_wait(cempty, (i & 1) ^ 1);  // the previous group's MMAs, frame rows and epilogue are done
-        mb_expect(cfull, (uint32_t)(sizeof(Hdr) + (active ? nks * C_KS : 0)));
+        mb_expect(cfull, (uint32_t)(sizeof(Hdr) + ((active && !WIDE) ? nks * C_KS : 0)));
         bulk_g2s(hdr, hg, (uint32_t)sizeof(Hdr), cfull);
-        if (active) bulk_g2s(sC, cimg + (int64_t)g * C_IMG, (uint32_t)(nks * C_KS), cfull);
+        if (active && !WIDE) bulk_g2s(sC, cimg + (int64_t)g * C_IMG, (uint32_t)(nks * C_KS), cfull);
         if (!active) continue;
+        const uint8_t* aimg = WIDE ? cimg + hg->img : nullptr;
         for (int tl = 0; tl < ntile; ++tl) {
           const int a0 = tl * BMA;
           for (int j = 0; j < nks; ++j, ++st) {
             const int s = st % NST;
             mb_wait(&lempty[s], ((st / NST) & 1) ^ 1);
-            mb_expect(&lfull[s], (uint32_t)L_STAGE);
-            tma2d(&mapB, &lfull[s], sL + s * L_STAGE, 4 * (k0 + KS * j), a0, keep);
+            mb_expect(&lfull[s], (uint32_t)STG);
+            tma2d(&mapB, &lfull[s], sL + s * STG, 4 * (k0 + KS * j), a0, keep);
+            if (WIDE) bulk_g2s(sL + s * STG + L_STAGE, aimg + (int64_t)j * C_KS, (uint32_t)C_KS, &lfull[s]);
           }
         }
       }
@@ -493,8 +694,8 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
             mb_wait(&lfull[s], (st / NST) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
-              const uint32_t lb = su32(sL + s * L_STAGE);
-              const uint64_t bdesc = desc32(cbase + (uint32_t)(j * C_KS));
+              const uint32_t lb = su32(sL + s * STG);
+              const uint64_t bdesc = desc32(WIDE ? lb + (uint32_t)L_STAGE : cbase + (uint32_t)(j * C_KS));
               mma_i8(d, desc128(lb), bdesc, ID0, j == 0 ? 0u : 1u);
               mma_i8(d + R, desc128(lb + KS), bdesc, ID1, 1u);
               mma_i8(d + 2 * R, desc128(lb + 2 * KS), bdesc, ID2, 1u);
@@ -630,6 +831,29 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_i8() {
   }
   return fn;
 }
+bool make_ldig_map(CUtensorMap* map, const int8_t* dig, int npad, int kpad) {
+  using namespace gi8;
+  auto enc = get_encode_i8();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)NDIG * kpad, (cuuint64_t)npad};
+  cuuint64_t strides[1] = {(cuuint64_t)NDIG * kpad};
+  cuuint32_t box[2] = {(cuuint32_t)(NDIG * KS), (cuuint32_t)BMA};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(dig), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count_i8() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
 }  // namespace
 
 cudaError_t launch_ldig(const float* lraw, const double* lcen, int L, int n, int npad, int kpad, int* eB,
@@ -676,24 +900,9 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
     const char* e = getenv("MC_GI8_DBG");
     return e ? atoi(e) : 0;
   }();
-  auto enc = get_encode_i8();
-  if (!enc) return cudaErrorInvalidValue;
   CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)NDIG * kpad, (cuuint64_t)npad};
-  cuuint64_t strides[1] = {(cuuint64_t)NDIG * kpad};
-  cuuint32_t box[2] = {(cuuint32_t)(NDIG * KS), (cuuint32_t)BMA};
-  cuuint32_t estr[2] = {1, 1};
-  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(dig), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  if (!make_ldig_map(&map, dig, npad, kpad)) return cudaErrorInvalidValue;
+  const int sms = sm_count_i8();
   const int DG = ncv == 2 ? Cfg<2>::DG : Cfg<1>::DG;
   const int groups = (T + DG - 1) / DG;
   const int grid = groups < sms ? groups : sms;
@@ -705,7 +914,7 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
     uint8_t* cimg = wsb + (size_t)groups * sizeof(H);                                                            \
     static bool attr = false;                                                                                    \
     if (!attr) {                                                                                                 \
-      cudaError_t e = cudaFuncSetAttribute(cv_grad_i8_kernel<OTT, NC>,                                           \
+      cudaError_t e = cudaFuncSetAttribute(cv_grad_i8_kernel<OTT, NC, false>,                                    \
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<NC>());       \
       if (e == cudaSuccess)                                                                                      \
         e = cudaFuncSetAttribute(cstack_prep_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C_IMG);    \
@@ -714,7 +923,8 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
     }                                                                                                            \
     cstack_prep_kernel<NC><<<groups, 128, C_IMG, stream>>>(T, cap, fcen, sig_idx, sig_coef, nsig, fvec, dV,      \
                                                            perm, out_map, hdrs, cimg, wide_flag);                \
-    cv_grad_i8_kernel<OTT, NC><<<grid, NT, smem_bytes<NC>(), stream>>>(map, T, n, npad, fraw, w, wa, eB, hdrs,   \
+    cv_grad_i8_kernel<OTT, NC, false><<<grid, NT, smem_bytes<NC>(), stream>>>(map, T, n, npad, fraw, w, wa, eB,  \
+                                                                              hdrs,                              \
                                                                        cimg, (OTT*)out0, (OTT*)out1);            \
   } while (0)
   if (ncv == 2) {
@@ -724,10 +934,77 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
   }
 #undef MC_GI8
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || ncv != 2 || (dbg & 16)) return e;
+  // ncv = 2 with wide_flag: the caller runs the wide groups on launch_cv_grad_i8_wide
+  if (e != cudaSuccess || ncv != 2 || (dbg & 16) || wide_flag) return e;
   // groups wider than WMAX landmarks: the DMMA kernel (every other group returns at once)
   return launch_cv_grad_dmma(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx, sig_coef, nsig, fvec, perm, out_map,
                              out0, out1, out_f32, stream, WMAX);
+}
+
+cudaError_t launch_grad_i8_plan(int T, int cap, int ncv, const int* sig_idx, const int* nsig, const int* perm,
+                                long long* bytes, cudaStream_t stream) {
+  using namespace gi8;
+  if (T <= 0) return cudaSuccess;
+  const int DG = ncv == 2 ? Cfg<2>::DG : Cfg<1>::DG;
+  const int groups = (T + DG - 1) / DG;
+  if (ncv == 2)
+    grad_i8_plan_kernel<2><<<(groups + 127) / 128, 128, 0, stream>>>(T, cap, sig_idx, nsig, perm, bytes);
+  else
+    grad_i8_plan_kernel<1><<<(groups + 127) / 128, 128, 0, stream>>>(T, cap, sig_idx, nsig, perm, bytes);
+  return cudaGetLastError();
+}
+
+size_t grad_i8_wide_header_bytes(int nwide, int ncv) {
+  using namespace gi8;
+  const size_t hb = ncv == 2 ? sizeof(GHdr<Cfg<2>::DG>) : sizeof(GHdr<Cfg<1>::DG>);
+  return (size_t)nwide * hb + 256;
+}
+
+// the wide groups (listed in wide_ids, their images at byte offsets wide_off of wimg):
+// A images built in chunks, then the streamed-A kernel over the listed groups
+cudaError_t launch_cv_grad_i8_wide(int T, int n, int cap, const float* fraw, const double* fcen, const double* w,
+                                   const double* wa, const int8_t* dig, const int* eB, int npad, int kpad,
+                                   const int* sig_idx, const double* sig_coef, const int* nsig, const double* fvec,
+                                   const double* dV, const int* perm, const int* out_map, void* out0, void* out1,
+                                   int out_f32, int ncv, const int* wide_ids, int nwide, const long long* wide_off,
+                                   void* hws, void* wimg, cudaStream_t stream) {
+  using namespace gi8;
+  if (T <= 0 || nwide <= 0) return cudaSuccess;
+  if ((ncv != 1 && ncv != 2) || n % 4 != 0 || (reinterpret_cast<uintptr_t>(fraw) & 15) || kpad % 32 ||
+      npad % BMA || !hws || !wimg)
+    return cudaErrorInvalidValue;
+  CUtensorMap map;
+  if (!make_ldig_map(&map, dig, npad, kpad)) return cudaErrorInvalidValue;
+  const int sms = sm_count_i8();
+  const int grid = nwide < sms ? nwide : sms;
+  uint8_t* hb = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(hws) + 255) & ~uintptr_t(255));
+#define MC_GI8W(OTT, NC)                                                                                         \
+  do {                                                                                                           \
+    using H = GHdr<Cfg<NC>::DG>;                                                                                 \
+    H* hdrs = reinterpret_cast<H*>(hb);                                                                          \
+    static bool attr = false;                                                                                    \
+    if (!attr) {                                                                                                 \
+      cudaError_t e = cudaFuncSetAttribute(cv_grad_i8_kernel<OTT, NC, true>,                                     \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<NC, true>()); \
+      if (e == cudaSuccess)                                                                                      \
+        e = cudaFuncSetAttribute(cstack_prep_wide_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                 C_IMG);                                                                         \
+      if (e != cudaSuccess) return e;                                                                            \
+      attr = true;                                                                                               \
+    }                                                                                                            \
+    cstack_prep_wide_kernel<NC><<<nwide, 128, C_IMG, stream>>>(T, cap, fcen, sig_idx, sig_coef, nsig, fvec, dV,  \
+                                                               perm, out_map, wide_ids, wide_off, hdrs,          \
+                                                               (uint8_t*)wimg);                                  \
+    cv_grad_i8_kernel<OTT, NC, true><<<grid, NT, smem_bytes<NC, true>(), stream>>>(                              \
+        map, nwide, n, npad, fraw, w, wa, eB, hdrs, (const uint8_t*)wimg, (OTT*)out0, (OTT*)out1);               \
+  } while (0)
+  if (ncv == 2) {
+    if (out_f32) MC_GI8W(float, 2); else MC_GI8W(double, 2);
+  } else {
+    if (out_f32) MC_GI8W(float, 1); else MC_GI8W(double, 1);
+  }
+#undef MC_GI8W
+  return cudaGetLastError();
 }
 
 }  // namespace mc

@@ -80,6 +80,15 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
                               void* out1, int out_f32, int ncv, int* wide_flag, void* ws, size_t ws_bytes,
                               cudaStream_t stream);
 size_t grad_i8_workspace(int T, int ncv);
+cudaError_t launch_grad_i8_plan(int T, int cap, int ncv, const int* sig_idx, const int* nsig, const int* perm,
+                                long long* bytes, cudaStream_t stream);
+size_t grad_i8_wide_header_bytes(int nwide, int ncv);
+cudaError_t launch_cv_grad_i8_wide(int T, int n, int cap, const float* fraw, const double* fcen, const double* w,
+                                   const double* wa, const int8_t* dig, const int* eB, int npad, int kpad,
+                                   const int* sig_idx, const double* sig_coef, const int* nsig, const double* fvec,
+                                   const double* dV, const int* perm, const int* out_map, void* out0, void* out1,
+                                   int out_f32, int ncv, const int* wide_ids, int nwide, const long long* wide_off,
+                                   void* hws, void* wimg, cudaStream_t stream);
 cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
                         int n, int kpad, int8_t* dig, int* e, cudaStream_t stream);
 cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,

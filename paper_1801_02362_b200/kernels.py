@@ -316,6 +316,53 @@ def _grad_i8_ws(T, ncv, dev):
     return torch.empty((nb,), dtype=torch.uint8, device=dev), nb
 
 
+# groups wider than the resident-image limit (117 landmarks) on the streamed-A int8 kernel
+# (env MC_GRAD_I8_WIDE=0: the DMMA kernel, as before)
+GRAD_I8_WIDE = __import__("os").environ.get("MC_GRAD_I8_WIDE", "1") == "1"
+
+
+def _grad_i8_wide(wres, cap, perm, ncv, dev, T):
+    """Plan the wide frame groups of a mc_pathcv_grad_i8 call: (wide_ids, nwide, wide_off,
+    header workspace, image workspace) or None when no group is wide (one host read)."""
+    DG = 8 if ncv == 2 else 16
+    groups = (T + DG - 1) // DG
+    by = torch.empty((groups,), dtype=torch.int64, device=dev)
+    call("mc_grad_i8_wide_plan", T, cap, ncv, ptr(wres["sig_idx"]), ptr(wres["nsig"]), ptr(perm), ptr(by),
+         stream_ptr())
+    ids = torch.nonzero(by).squeeze(1)
+    nwide = int(ids.numel())
+    if nwide == 0:
+        return None
+    sz = by[ids]
+    off = (torch.cumsum(sz, 0) - sz).contiguous()
+    total = int(sz.sum().item())
+    hb = int(_lib.load().mc_grad_i8_wide_header_size(nwide, ncv))
+    return (ids.to(I32).contiguous(), nwide, off, torch.empty((hb,), dtype=torch.uint8, device=dev), hb,
+            torch.empty((total + 256,), dtype=torch.uint8, device=dev))
+
+
+def _grad_i8_call(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_map, ldig, dV, out0, out1, f32, ncv,
+                  wide_flag, dev):
+    T, n = frames.shape[0], frames.shape[1]
+    ws, nb = _grad_i8_ws(T, ncv, dev)
+    plan = _grad_i8_wide(wres, cap, perm, ncv, dev, T) if GRAD_I8_WIDE and n % 4 == 0 else None
+    wf = wide_flag
+    if plan is not None and wf is None:
+        wf = torch.zeros((1,), dtype=I32, device=dev)  # narrow call: leave the wide groups out
+    call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
+         ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
+         ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(dV), ptr(perm), ptr(out_map), ptr(out0),
+         ptr(out1), f32, ncv, ptr(wf), ptr(ws), nb, stream_ptr())
+    if plan is not None:
+        ids, nwide, off, hws, hb, wimg = plan
+        call("mc_pathcv_grad_i8_wide", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(w), ptr(w_align), ptr(ldig.dig),
+             ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]),
+             ptr(wres["fvec"]), ptr(dV), ptr(perm), ptr(out_map), ptr(out0), ptr(out1), f32, ncv, ptr(ids), nwide,
+             ptr(off), ptr(hws), hb, ptr(wimg), stream_ptr())
+        if wide_flag is not None:
+            wide_flag.zero_()  # every wide group was written by the streamed-A kernel
+
+
 def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_dtype=torch.float32,
                       out_map=None, ds=None, dz=None, ldig=None):
     """Blocked gradient pass (fp32 path, exact rows): groups of 8 sorted frames.
@@ -329,11 +376,8 @@ def pathcv_grad_block(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ou
     dz = torch.empty((T, n, 3), dtype=out_dtype, device=dev) if dz is None else dz
     f32 = 1 if ds.dtype == torch.float32 else 0
     if ldig is not None:
-        ws, nb = _grad_i8_ws(T, 2, dev)
-        call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
-             ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
-             ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), None, ptr(perm), ptr(out_map), ptr(ds),
-             ptr(dz), f32, 2, None, ptr(ws), nb, stream_ptr())
+        _grad_i8_call(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_map, ldig, None, ds, dz, f32, 2,
+                      None, dev)
         return ds, dz
     call("mc_pathcv_grad_block", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(wres["sig_idx"]), ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(perm),
@@ -349,11 +393,8 @@ def pathcv_force_i8(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, ldig
     117 landmarks are skipped and set wide[0] = 1 (int32 device flag, caller-zeroed)."""
     T, n = frames.shape[0], frames.shape[1]
     F = torch.empty((T, n, 3), dtype=out_dtype, device=frames.device) if F is None else F
-    ws, nb = _grad_i8_ws(T, 1, frames.device)
-    call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
-         ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
-         ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(dV.contiguous()), ptr(perm), ptr(out_map),
-         ptr(F), None, 1 if F.dtype == torch.float32 else 0, 1, ptr(wide), ptr(ws), nb, stream_ptr())
+    _grad_i8_call(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_map, ldig, dV.contiguous(), F, None,
+                  1 if F.dtype == torch.float32 else 0, 1, wide, frames.device)
     return F
 
 

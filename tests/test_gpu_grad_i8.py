@@ -70,7 +70,8 @@ def test_i8_gradient_matches_dmma_and_oracle(T, L, N, cuda_device):
 
 def test_i8_gradient_fp32_output_and_wide_groups(cuda_device):
     """fp32 outputs; a small lambda widens the significant windows past 117 landmarks, so
-    part of the groups run on the DMMA fallback inside the same call: still == DMMA."""
+    part of the groups run on the streamed-A int8 kernel (mc_pathcv_grad_i8_wide) beside
+    the resident-image one: still == DMMA."""
     wl = synth.config4(seed=6, T=64, L=1024, N=400)
     pcv = engine.PathCVTC(wl.landmarks, wl.lam * 0.02, window_cap=1024)
     out = pcv.evaluate(wl.frames)
@@ -82,6 +83,33 @@ def test_i8_gradient_fp32_output_and_wide_groups(cuda_device):
     for key in ("ds", "dz"):
         r = _rel_rows(out[key].cpu().numpy(), dm[key].cpu().numpy())
         assert r.max() <= 2e-6, f"{key}: {r.max():.2e}"
+
+
+def test_i8_wide_groups_streamed_equal_dmma_fallback_and_force(cuda_device):
+    """Very wide significant unions (several hundred landmarks: the A image is built in
+    chunks of 12 k-steps and streamed with the B boxes): the streamed-A int8 gradient ==
+    the DMMA fallback (1e-6 of the per-frame max); the fused force of wide 16-frame
+    groups == -(V_s ds + V_z dz) without the two-output fallback."""
+    wl = synth.config4(seed=12, T=72, L=1024, N=512)
+    pcv = engine.PathCVTC(wl.landmarks, wl.lam * 0.004, window_cap=1024)
+    out = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    nsig = out["nsig"].cpu().numpy()
+    assert nsig.max() > 400, nsig.max()
+    saved = K.GRAD_I8_WIDE
+    try:
+        K.GRAD_I8_WIDE = False
+        fb = pcv.evaluate(wl.frames, out_dtype=torch.float64)
+    finally:
+        K.GRAD_I8_WIDE = saved
+    for key in ("ds", "dz"):
+        r = _rel_rows(out[key].cpu().numpy(), fb[key].cpu().numpy())
+        assert r.max() <= 1e-6, f"{key}: {r.max():.2e}"
+    rng = np.random.default_rng(5)
+    dV = torch.from_numpy(rng.normal(size=(72, 2))).cuda()
+    of = pcv.evaluate(wl.frames, grad=False, out_dtype=torch.float64, dV=dV)
+    ref = -(dV[:, 0, None, None] * out["ds"] + dV[:, 1, None, None] * out["dz"]).cpu().numpy()
+    r = _rel_rows(of["force"].cpu().numpy(), ref)
+    assert r.max() <= 1e-6, f"force: {r.max():.2e}"
 
 
 def test_fused_bias_force_equals_contracted_gradients(cuda_device):
