@@ -640,7 +640,7 @@ class ConfigTC:
             else:
                 pairs = 0.0
             return "int8_tensor_op_refine", 2.0 * 10.0 * 9.0 * n * pairs
-        if name == "mc_center_split16":
+        if name in ("mc_center_split16", "mc_center_split16_uniform"):
             return "bytes", T * n * 3 * 4 + 2 * T * 3 * (((n + 31) // 32) * 32) * 2
         if name == "mc_refine":
             if self.cfg == 2:

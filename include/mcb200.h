@@ -312,6 +312,14 @@ int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, i
                       const double* w_disp, int32_t weighted, int32_t terms, void* hl, double* scale_inv,
                       double* opnorm, double* rnorm, double* centroid, double* gnorm, double* wbar, double* mom,
                       uint8_t* flags, void* stream);
+/* mc_center_split16 for the one-term frame operand with uniform weights (w = w' = wuni on
+ * the n atoms, fp32 AoS input, n % 4 == 0, 16-byte aligned): the same outputs (halves,
+ * scale, opnorm, rigorous rnorm bound, centroid, G = wuni sum |x - c|^2, wbar = 0,
+ * flags) from one fp64 moment pass (shifted by the first atom) and one fp32 split pass
+ * (geometry.py:67-76 centring).  mom is not produced. */
+int mc_center_split16_uniform(const float* coords, int64_t count, int32_t n, int32_t kpad, double wuni, void* hl,
+                              double* scale_inv, double* opnorm, double* rnorm, double* centroid, double* gnorm,
+                              double* wbar, uint8_t* flags, void* stream);
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
                const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const int32_t* tlist,
                const int32_t* nlist, float* D, int64_t ldd, int32_t grid, void* stream);

@@ -458,6 +458,17 @@ int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, i
                                                S_(stream)));
 }
 
+int mc_center_split16_uniform(const float* coords, int64_t count, int32_t n, int32_t kpad, double wuni, void* hl,
+                              double* scale_inv, double* opnorm, double* rnorm, double* centroid, double* gnorm,
+                              double* wbar, uint8_t* flags, void* stream) {
+  if (n < 2) return MC_ERR_INVALID_STRUCTURE;
+  if (count < 0 || kpad < n || kpad % 64 != 0 || n % 4 != 0 || !(wuni > 0.0)) return MC_ERR_CONFIG;
+  if (count > 0 && (!coords || !hl || !scale_inv || !gnorm || (reinterpret_cast<uintptr_t>(coords) & 15)))
+    return MC_ERR_CONFIG;
+  return cuda_status(mc::launch_center_split16_uniform(coords, count, n, kpad, wuni, hl, scale_inv, opnorm, rnorm,
+                                                       centroid, gnorm, wbar, flags, S_(stream)));
+}
+
 static int msd_f16_args(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,
                         const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const float* D,
                         int64_t ldd) {

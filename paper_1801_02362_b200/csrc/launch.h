@@ -80,6 +80,9 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
                               void* out1, int out_f32, int ncv, int* wide_flag, void* ws, size_t ws_bytes,
                               cudaStream_t stream);
 size_t grad_i8_workspace(int T, int ncv);
+cudaError_t launch_center_split16_uniform(const float* coords, int64_t B, int n, int kpad, double wuni, void* hl,
+                                          double* scale_inv, double* opnorm, double* rnorm, double* centroid,
+                                          double* gnorm, double* wbar, uint8_t* flags, cudaStream_t stream);
 cudaError_t launch_grad_i8_plan(int T, int cap, int ncv, const int* sig_idx, const int* nsig, const int* perm,
                                 long long* bytes, cudaStream_t stream);
 size_t grad_i8_wide_header_bytes(int nwide, int ncv);

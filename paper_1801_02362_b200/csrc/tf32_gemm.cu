@@ -308,6 +308,125 @@ center_split_f16x1_kernel(const float* __restrict__ coords, int64_t B, int n, in
   }
 }
 
+// K1s for uniform weights (w = w' = wuni on the n atoms; the configs' case): every
+// per-structure sum comes out of the FIRST pass as moments shifted by the first atom p
+// (U1 = sum (x - p), U2 = sum (x - p)^2 per axis, fp64; no cancellation: |c - p| is of
+// the structure's size), so the second pass is pure fp32: vf = fl32(x - fl32(c)),
+// h = rn16(vf 2^e) and the residual |h 2^-e - vf|^2.  Per coordinate 5 instructions in
+// pass 1 (3 fp64) and 6 fp32 in pass 2, against ~20 with 5 fp64 in center_split_f16x1.
+//   c = p + U1 / n,  sum |x - c|^2 = sum_b (U2_b - U1_b^2 / n),  G = wuni * that,
+//   wbar = sum w (x - c) = 0,
+//   rnorm: ||h 2^-e - v|| <= ||h 2^-e - vf|| (1 + 1e-5) + ||vf - v||, and per coordinate
+//   |vf - v| <= 2^-24 |x - c32| + |c - c32| <= 2^-24 (|v| + 2 |c|), so
+//   ||vf - v|| <= 2^-24 (1 + 2^-20) (||v|| + 2 sqrt(n) |c|_2).
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT)
+center_split_f16x1_uni_kernel(const float* __restrict__ coords, int64_t B, int n, int kpad, double wuni,
+                              __half* __restrict__ hi, double* __restrict__ scale_inv, double* __restrict__ centroid,
+                              double* __restrict__ gnorm, double* __restrict__ wbar, uint8_t* __restrict__ flags,
+                              double* __restrict__ opnorm, double* __restrict__ rnorm) {
+  __shared__ double scratch[6 * (NT / 32)];
+  const int64_t b = blockIdx.x;
+  const float* xb = coords + b * (int64_t)n * 3;
+  const float4* x4 = reinterpret_cast<const float4*>(xb);
+  const int G = n / 4;
+  const double p0 = (double)__ldg(xb), p1 = (double)__ldg(xb + 1), p2 = (double)__ldg(xb + 2);
+  double u[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // U1 (3), U2 (3)
+  float xmax = 0.0f;
+#pragma unroll 2
+  for (int gi = threadIdx.x; gi < G; gi += NT) {
+    const float4 q0 = x4[3 * gi], q1 = x4[3 * gi + 1], q2 = x4[3 * gi + 2];
+    const float f[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const double y = (double)f[3 * a + p] - (p == 0 ? p0 : (p == 1 ? p1 : p2));
+        u[p] += y;
+        u[3 + p] = fma(y, y, u[3 + p]);
+        xmax = fmaxf(xmax, fabsf(f[3 * a + p]));
+      }
+    }
+  }
+  const double xm = -block_min<NT>(-(double)xmax, scratch);
+  block_sum_n<NT, 6>(u, scratch);
+  const double inv_n = 1.0 / (double)n;
+  const double c[3] = {p0 + u[0] * inv_n, p1 + u[1] * inv_n, p2 + u[2] * inv_n};
+  const double on2 = fmax(0.0, (u[3] - u[0] * u[0] * inv_n) + (u[4] - u[1] * u[1] * inv_n) +
+                                   (u[5] - u[2] * u[2] * inv_n));
+  const bool nonfinite = !isfinite(u[0] + u[1] + u[2] + u[3] + u[4] + u[5]) || !isfinite(xm);
+  const double bound = 2.0 * xm;  // |x_j - c| <= 2 max|x|
+  int e = 0;
+  if (bound > 0.0 && isfinite(bound)) {
+    frexp(bound, &e);
+    e = 14 - e;
+  }
+  e = max(-1000, min(1000, e));
+  const bool f32s = e >= -126 && e <= 126;
+  const float scf = f32s ? ldexpf(1.0f, e) : 0.0f, sif = f32s ? ldexpf(1.0f, -e) : 0.0f;
+  const double scale = ldexp(1.0, e), sinv = ldexp(1.0, -e);
+  const float c32[3] = {(float)c[0], (float)c[1], (float)c[2]};
+  const int64_t plane = B * (int64_t)kpad;
+  __half* h0 = hi + b * kpad;
+  double r2d = 0.0;
+#pragma unroll 2
+  for (int gi = threadIdx.x; gi < kpad / 4; gi += NT) {
+    uint2 o[3] = {make_uint2(0u, 0u), make_uint2(0u, 0u), make_uint2(0u, 0u)};
+    if (gi < G) {
+      const float4 q0 = x4[3 * gi], q1 = x4[3 * gi + 1], q2 = x4[3 * gi + 2];
+      const float f[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+      __half h[3][4];
+      float r2 = 0.0f;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          if (f32s) {
+            const float vf = f[3 * a + p] - c32[p];
+            h[p][a] = __float2half_rn(vf * scf);
+            const float r = fmaf(__half2float(h[p][a]), sif, -vf);
+            r2 = fmaf(r, r, r2);
+          } else {  // extreme scales: fp64 (rare)
+            const double v = (double)f[3 * a + p] - c[p];
+            h[p][a] = __double2half(v * scale);
+            const double rd = (double)__half2float(h[p][a]) * sinv - v;
+            r2d = fma(rd, rd, r2d);
+          }
+        }
+      }
+      r2d += (double)r2;
+#pragma unroll
+      for (int p = 0; p < 3; ++p) o[p] = *reinterpret_cast<const uint2*>(h[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < 3; ++p) *reinterpret_cast<uint2*>(h0 + p * plane + 4 * gi) = o[p];
+  }
+  r2d = block_sum<NT>(r2d, scratch);
+  if (threadIdx.x == 0) {
+    if (centroid) { centroid[3 * b] = c[0]; centroid[3 * b + 1] = c[1]; centroid[3 * b + 2] = c[2]; }
+    gnorm[b] = wuni * on2;
+    if (wbar) { wbar[3 * b] = 0.0; wbar[3 * b + 1] = 0.0; wbar[3 * b + 2] = 0.0; }
+    if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
+    const double on = sqrt(on2);
+    if (opnorm) opnorm[b] = on;
+    const double cn = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    if (rnorm)
+      rnorm[b] = f32s ? sqrt(r2d) * (1.0 + 1e-5) + ldexp(1.0 + ldexp(1.0, -20), -24) * (on + 2.0 * sqrt((double)n) * cn)
+                      : sqrt(r2d);
+    scale_inv[b] = sinv;
+  }
+}
+
+cudaError_t launch_center_split16_uniform(const float* coords, int64_t B, int n, int kpad, double wuni, void* hl,
+                                          double* scale_inv, double* opnorm, double* rnorm, double* centroid,
+                                          double* gnorm, double* wbar, uint8_t* flags, cudaStream_t stream) {
+  if (B <= 0) return cudaSuccess;
+  if (n % 4 || kpad % 4 || (reinterpret_cast<uintptr_t>(coords) & 15) || B > 0x7fffffffLL) return cudaErrorInvalidValue;
+  center_split_f16x1_uni_kernel<256><<<(unsigned)B, 256, 0, stream>>>(coords, B, n, kpad, wuni, (__half*)hl, scale_inv,
+                                                                      centroid, gnorm, wbar, flags, opnorm, rnorm);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_center_split(const void* coords, int dtype, int64_t B, int n, int kpad, const double* w_align,
                                 const double* w_disp, int weighted, float* hi, float* lo, double* centroid,
                                 double* gnorm, double* wbar, double* mom, uint8_t* flags, cudaStream_t stream) {

@@ -575,6 +575,8 @@ class PathCVTC:
         # uniform displacement weights (the configs' default): the exact refits run on raw,
         # unweighted fp32 operands (refine_dmma RAW mode)
         self.wuni = float(self.w[0].item()) if bool((self.w[:self.n] == self.w[0]).all()) else 0.0
+        # uniform w = w': the frame split takes the one-fp64-pass K1s (mc_center_split16_uniform)
+        self._k1_wuni = self.wuni if bool(torch.equal(self.w, self.wa)) else 0.0
         self._ls = {}
         self.screen_terms = 1 if self.screen == "f16x1" else 3
         self.ls = self._lsplit(self.screen_terms)
@@ -692,7 +694,7 @@ class PathCVTC:
             fr = fr.float()
         _check_shapes(fr, self.lraw)
         fs = K.center_split(fr.contiguous(), self.wa, self.w, weighted=False, fmt=self.fmt,
-                            terms=terms if self.fmt == "f16" else 3)
+                            terms=terms if self.fmt == "f16" else 3, wuni=self._k1_wuni)
         if check and _or_flags(fs.flags) & FLAG_NON_FINITE:
             raise InvalidStructureError("frame coordinates contain non-finite values")
         return fr.contiguous(), fs

@@ -607,7 +607,11 @@ class Split:
         self.n, self.kpad, self.count = n, kpad, hi.shape[1]
 
 
-def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, terms=3):
+# uniform-weight one-term K1s (mc_center_split16_uniform); env MC_K1_UNIFORM=0 disables
+K1_UNIFORM = __import__("os").environ.get("MC_K1_UNIFORM", "1") == "1"
+
+
+def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, terms=3, wuni=0.0):
     """K1s: centre, optionally fold w into the operand, split into hi/lo planes
     (fmt "f16": power-of-two scaled IEEE halves, "tf32": TF32 words; default
     env MC_OPERAND_FMT, f16).  terms=1 (f16 only): hi halves only, for the
@@ -638,7 +642,11 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, ter
     wbar = torch.empty((b, 3), dtype=F64, device=dev)
     mom = torch.empty((b, 6), dtype=F64, device=dev) if moments else None
     flags = torch.empty((b,), dtype=U8, device=dev)
-    if fmt == "f16":
+    if (fmt == "f16" and terms == 1 and wuni > 0.0 and K1_UNIFORM and not weighted and not moments
+            and dt == _lib.MC_F32 and n % 4 == 0 and coords.data_ptr() % 16 == 0):
+        call("mc_center_split16_uniform", ptr(coords), b, n, kpad, float(wuni), ptr(hi), ptr(scale), ptr(opnorm),
+             ptr(rnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(flags), stream_ptr())
+    elif fmt == "f16":
         call("mc_center_split16", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
              terms, ptr(hi), ptr(scale), ptr(opnorm), ptr(rnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(mom),
              ptr(flags), stream_ptr())

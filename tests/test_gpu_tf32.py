@@ -260,3 +260,46 @@ def test_fast_one_term_split_vs_fp64(n, T, cuda_device):
     for a, b in ((sp.centroid, ref.centroid), (sp.scale, ref.scale), (sp.g, ref.g), (sp.opnorm, ref.opnorm)):
         np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(sp.rnorm.cpu().numpy(), ref.rnorm.cpu().numpy(), rtol=1e-3)
+
+
+@pytest.mark.parametrize("n,T", [(600, 700), (10000, 64), (1000, 1500)])
+def test_uniform_one_term_split_vs_fp64(n, T, cuda_device):
+    """Uniform-weight K1s (mc_center_split16_uniform: one fp64 moment pass shifted by the
+    first atom, one fp32 split pass): centroid / G / operand norm equal the fp64 values,
+    wbar = 0, every half is the scaled centred coordinate to half precision, rnorm is a
+    rigorous and tight bound of the true residual ||h 2^-e - (x - c)||, and the scalars
+    agree with the generic kernel."""
+    rng = np.random.default_rng(n + 7 * T)
+    x = (rng.normal(0.0, 0.7, size=(T, n, 3)) + rng.uniform(-2, 2, size=(T, 1, 3))).astype(np.float32)
+    x[3] *= 1e-3  # a structure with a very different scale
+    x[5] += 40.0  # a large translation (|c| >> spread)
+    xt = torch.from_numpy(x).to(cuda_device)
+    w = torch.full((n,), 1.0 / n, dtype=torch.float64, device=cuda_device)
+    sp = K.center_split(xt, w, w, weighted=False, fmt="f16", terms=1, wuni=1.0 / n)
+    xd = x.astype(np.float64)
+    c = xd.mean(axis=1)
+    v = xd - c[:, None, :]
+    np.testing.assert_allclose(sp.centroid.cpu().numpy(), c, rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(sp.g.cpu().numpy(), (v * v).sum(axis=(1, 2)) / n, rtol=1e-12)
+    on = np.sqrt((v * v).sum(axis=(1, 2)))
+    np.testing.assert_allclose(sp.opnorm.cpu().numpy(), on, rtol=1e-12)
+    assert np.abs(sp.wbar.cpu().numpy()).max() == 0.0
+    sinv = sp.scale.cpu().numpy()
+    h = sp.hi.float().cpu().numpy()[:, :, :n].transpose(1, 2, 0).astype(np.float64) * sinv[:, None, None]
+    assert np.all(sp.hi.float().cpu().numpy()[:, :, n:] == 0)
+    res = np.sqrt(((h - v) ** 2).sum(axis=(1, 2)))
+    rn = sp.rnorm.cpu().numpy()
+    cn = np.sqrt((c * c).sum(axis=1))
+    assert np.all(res <= rn), "rnorm must bound the true residual"
+    assert np.all(rn <= res * (1 + 2e-5) + 2 ** -23 * (on + 2 * np.sqrt(n) * cn))
+    assert np.all(np.abs(h - v) <= 2 ** -11 * np.abs(v) + 2 ** -23 * (np.abs(v) + 2 * np.abs(c)[:, None, :])
+                  + 2 ** -24 * sinv[:, None, None])
+    ref = K.center_split(xt, w, w, weighted=False, fmt="f16", terms=1)
+    for a, b in ((sp.centroid, ref.centroid), (sp.scale, ref.scale), (sp.g, ref.g), (sp.opnorm, ref.opnorm)):
+        np.testing.assert_allclose(a.cpu().numpy(), b.cpu().numpy(), rtol=1e-12, atol=1e-15)
+    # the halves agree with the fp64-centring kernel except for rare one-ulp ties (the
+    # translated structure 5 centres in fp32 at |c| = 40: excluded)
+    keep = torch.ones(T, dtype=torch.bool, device=cuda_device)
+    keep[5] = False
+    same = (sp.hi[:, keep] == ref.hi[:, keep]).float().mean().item()
+    assert same > 0.999, same
