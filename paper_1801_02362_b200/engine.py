@@ -851,6 +851,96 @@ class PathCVTC:
         return out
 
 
+    def evaluate_nl(self, frames, neighbours, nl_stride=1, walkers=1, grad=True, out_dtype=torch.float32):
+        """SPEC neighbourlist (``maybe_update``) on the tensor-core path with
+        exact distances every frame (Alg. 1): frames [T, n, 3] (one trajectory, or
+        ``walkers`` consecutive trajectories) or [W, S, n, 3].  Each walker's list is the M
+        landmarks nearest (exact aligned MSD, ties by lower index) to its frames 0, nl_stride,
+        2 nl_stride, ...; s, z and the gradients of every frame sum over the active set of
+        its last update (SPEC colvar "active set"), like PathCV.close_replay(eps=0,
+        neighbours=M) and the oracle.
+
+        Certified top-M without a dense exact matrix: the one-term screen of the update
+        frames bounds every pair (|D_est - D| <= e_t); with k_t the M-th smallest estimate,
+        any landmark with D_est - e_t > k_t + e_t cannot be among the M nearest, so only the
+        candidates' hull is refit exactly (int8 tensor cores) and the exact top-M taken
+        among them (mc_neighbour_topm).  Every frame is then refit over the hull of its
+        active set; window slots outside the set are masked (D = 1e300, weight 0)."""
+        if self.shard is not None:
+            raise ConfigError("evaluate_nl runs on an unsharded engine")
+        M, stride = int(neighbours), int(nl_stride)
+        if not (1 <= M <= self.L):
+            raise ConfigError("neighbour list size must satisfy 1 <= M <= L")
+        if stride < 1:
+            raise ConfigError("neighbour list stride must be >= 1")
+        fr_in = _as_cuda(frames, self.device)
+        if fr_in.ndim == 4:
+            walkers = int(fr_in.shape[0])
+            fr_in = fr_in.reshape(-1, self.n, 3)
+        T = int(fr_in.shape[0])
+        if walkers < 1 or T % walkers:
+            raise ConfigError("frames must split into equal walker trajectories")
+        steps = T // walkers
+        fr, fs = self._frames(fr_in, self.screen_terms)
+        dev = self.device
+        nupd = (steps + stride - 1) // stride
+        w_ = torch.arange(walkers, device=dev, dtype=torch.int32)
+        upd = (w_[:, None] * steps + torch.arange(0, steps, stride, device=dev, dtype=torch.int32)[None, :])
+        upd = upd.reshape(-1).contiguous()
+        k = torch.arange(steps, device=dev, dtype=torch.int32)
+        row = (w_[:, None] * nupd + (k // stride)[None, :]).reshape(-1).contiguous()
+        # 1. certified candidates of the update frames' top-M
+        fsu = K.gather_split(fs, upd)
+        Dest = K.msd_estimate(fsu, self._lsplit(self.screen_terms), grid=K2_GRID)
+        one = self.screen == "f16x1"
+        e = self.frame_bound(fsu) if one else torch.full((upd.numel(),), self.est_err, dtype=torch.float64, device=dev)
+        kth = Dest.gather(1, K.neighbour_topm(Dest, M).long()).amax(1).double()
+        m = Dest.amin(1).double()
+        allow = self.lam * ((kth - m) * (1.0 + 1e-6) + 2.0 * e + 1e-6 * kth.abs() + 1e-12)
+        lo_u, cnt_u, _, cflags = K.candidates(Dest, self.lam, 0.0, self.L, fnorm=allow.contiguous(), fcoef=1.0)
+        del Dest
+        cap_u = max(1, int(cnt_u.max().item()))
+        perm_u = K.sort_by_key((2 * lo_u + cnt_u).to(torch.int32), 2 * self.L + 1)
+        Dex_u, _, rflags_u = self._refine_windows(fr, fsu, perm_u, lo_u, cnt_u, cap_u, fmap=upd)
+        # 2. exact top-M of every update frame among its candidates
+        U = upd.numel()
+        ri, si = torch.nonzero(torch.arange(cap_u, device=dev)[None, :] < cnt_u[:, None], as_tuple=True)
+        Dfull = torch.full((U, self.L), float("inf"), dtype=torch.float64, device=dev)
+        Dfull[ri, lo_u[ri].long() + si] = Dex_u[ri, si]
+        idx = K.neighbour_topm(Dfull, M)
+        del Dfull
+        # 3. every frame over the hull of its active set, slots outside the set masked
+        lst = idx[row.long()]
+        lo = lst.amin(1).contiguous()
+        cnt = (lst.amax(1) - lo + 1).contiguous()
+        cap = max(1, int(cnt.max().item()))
+        perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
+        Dex, Rex, rflags = self._refine_windows(fr, fs, perm, lo, cnt, cap)
+        mem = torch.zeros((U, self.L), dtype=torch.bool, device=dev)
+        mem.scatter_(1, idx.long(), True)
+        slot = torch.arange(cap, device=dev)
+        inw = slot[None, :] < cnt[:, None]
+        cols = (lo[:, None].long() + slot[None, :]).clamp_(max=self.L - 1)
+        member = mem[row.long()[:, None], cols] & inw
+        Dex.masked_fill_(inw & ~member, 1e300)
+        wres = K.pathcv_weights(Dex, self.q, self.lam, Rex, fs, self.ls, cap, self.cutoff, L=self.L, rowlo=lo,
+                                rowcnt=cnt)
+        out = {"s": wres["s"], "z": wres["z"], "nsig": wres["nsig"], "active": lst, "window_lo": lo,
+               "window_cnt": cnt, "D_window": Dex}
+        if grad:
+            gperm = K.sort_by_key(K.sig_span_key(wres, self.L), 2 * self.L + 1)
+            out["ds"], out["dz"] = K.pathcv_grad_block(wres, fs, self.ls, fr, self.lraw, self.w, self.wa, cap, gperm,
+                                                       out_dtype, ldig=self.ldig)
+        f = (_or_flags(fs.flags) | _or_flags(cflags) | _or_flags(rflags_u) | _or_flags(rflags)
+             | _or_flags(wres["flags"]))
+        if f & FLAG_NON_FINITE:
+            raise InvalidStructureError("evaluate_nl: non-finite coordinates or distances")
+        if f & FLAG_NO_CONVERGE:
+            raise MetadynError("evaluate_nl: Jacobi diagonalisation did not converge")
+        if f & FLAG_SIG_OVERFLOW:
+            raise ConfigError("evaluate_nl: more significant landmarks than the list capacity")
+        return out
+
     # ------------------------------------------------------------ landmark sharding
 
     def landmark_load(self, frames):

@@ -87,3 +87,64 @@ def test_replay_with_neighbour_list_matches_oracle(M, stride, cuda_device):
         scale = np.abs(r).reshape(r.shape[0], -1).max(axis=1) + 1e-300
         err = np.abs(got - r).reshape(r.shape[0], -1).max(axis=1)
         assert np.all(err <= 1e-5 * scale), f"{key}: worst rel {np.max(err / scale):.3e}"
+
+
+def _grad_close(got, r, rtol=1e-5):
+    scale = np.abs(r).reshape(r.shape[0], -1).max(axis=1) + 1e-300
+    err = np.abs(got - r).reshape(r.shape[0], -1).max(axis=1)
+    assert np.all(err <= rtol * scale), f"worst rel {np.max(err / scale):.3e}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,stride", [(5, 1), (12, 4)])
+def test_tensor_core_neighbour_list_matches_oracle(M, stride, cuda_device):
+    """PathCVTC.evaluate_nl (fp32 frames; certified top-M of the update frames from the
+    one-term screen + exact int8 refits of the candidates) == the oracle's exact-mode
+    replay with the same neighbour list (eps = 0: every frame exact): identical active
+    sets, s / z within 1e-6, gradients within 1e-5."""
+    from paper_1801_02362_b200 import engine, synth
+
+    wl = synth.config4(seed=21, T=12, L=60, N=40)
+    ref = O.close_structure_replay(wl.frames.astype(np.float64), wl.landmarks.astype(np.float64), wl.lam, 0.0,
+                                   neighbours=M, nl_stride=stride)
+    assert ref["refresh"].all()
+    out = engine.PathCVTC(wl.landmarks, wl.lam).evaluate_nl(wl.frames, M, nl_stride=stride, out_dtype=torch.float64)
+    np.testing.assert_array_equal(out["active"].cpu().numpy(), ref["active"])
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    for key in ("ds", "dz"):
+        _grad_close(out[key].cpu().numpy(), ref[key])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,stride,walkers", [(16, 1, 1), (40, 5, 2), (300, 1, 1)])
+def test_tensor_core_neighbour_list_matches_fp64_engine(M, stride, walkers, cuda_device):
+    """At larger shapes (L = 1024, N = 400, window-limited screen): evaluate_nl == the fp64
+    engine's exact-mode close replay with the neighbour list (close_replay(eps=0,
+    neighbours=M), itself pinned to the oracle above): identical active sets, s / z 1e-6,
+    gradients 1e-5; with M larger than the significant set the result equals the
+    list-free evaluate."""
+    from paper_1801_02362_b200 import engine, synth
+
+    wl = synth.config4(seed=22, T=48, L=1024, N=400)
+    fr = torch.from_numpy(wl.frames).to(cuda_device)
+    if walkers > 1:
+        fr = fr.reshape(walkers, -1, 400, 3)
+    tc = engine.PathCVTC(wl.landmarks, wl.lam)
+    out = tc.evaluate_nl(fr, M, nl_stride=stride, out_dtype=torch.float64)
+    saved = engine.CLOSE_PRUNE
+    try:
+        engine.CLOSE_PRUNE = False  # dense exact distances: the list from every landmark
+        ref = engine.PathCV(wl.landmarks, wl.lam).close_replay(fr.double(), 0.0, walkers=1, neighbours=M,
+                                                               nl_stride=stride)
+    finally:
+        engine.CLOSE_PRUNE = saved
+    assert bool(ref["refresh"].all())
+    np.testing.assert_array_equal(out["active"].cpu().numpy(), ref["active"].cpu().numpy())
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"].cpu().numpy(), rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"].cpu().numpy(), rtol=1e-6, atol=1e-9)
+    for key in ("ds", "dz"):
+        _grad_close(out[key].cpu().numpy(), ref[key].cpu().numpy())
+    if M == 300:
+        full = tc.evaluate(wl.frames, out_dtype=torch.float64)
+        np.testing.assert_allclose(out["s"].cpu().numpy(), full["s"].cpu().numpy(), rtol=1e-9)
