@@ -777,6 +777,7 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
           const double sxa = pow2d(14 - eb);
           const double q2w = valid ? 2.0 * w[a] * pow2d(eb - 14) : 0.0;
           const double wak = valid ? wa[a] : 0.0;
+          const float q2wf = (float)q2w, wakf = (float)wak;
           mb_wait(&xfull[ab], (it >> 1) & 1);
           const float* X = reinterpret_cast<const float*>(sX + ab * X_BUF);
 #pragma unroll
@@ -797,10 +798,19 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
                 const float lo = fmaf((float)(int)acc[3][rl], 5.9604644775390625e-8f,
                                       fmaf((float)(int)acc[2][rl], 1.52587890625e-5f,
                                            (float)(int)acc[1][rl] * 3.90625e-3f));
-                const double v = (double)(int)acc[0][rl] + (double)lo;
-                // t = sc' xc' - v in units of 2^(eA_r + eB_k - 14)
-                const double tt = fma(rc.scp, xc[b], -v);
-                if (valid) store_stream(dst + b, (OT)(tt * (double)rc.P * q2w - wak * (double)rc.corr));
+                if constexpr (sizeof(OT) == 4) {
+                  // fp32 outputs: only the cancelling step sc' xc' - acc0 in fp64 (3 fp64-pipe
+                  // ops per output instead of 9); t1 and lo are then both far below 2^31 units and
+                  // the rest is fp32 (relative error ~2^-23 of the result, the output's own rounding)
+                  const double t1 = fma(rc.scp, xc[b], -(double)(int)acc[0][rl]);
+                  const float tt = (float)t1 - lo;
+                  if (valid) store_stream(dst + b, (OT)fmaf(tt, rc.P * q2wf, -wakf * rc.corr));
+                } else {
+                  const double v = (double)(int)acc[0][rl] + (double)lo;
+                  // t = sc' xc' - v in units of 2^(eA_r + eB_k - 14)
+                  const double tt = fma(rc.scp, xc[b], -v);
+                  if (valid) store_stream(dst + b, (OT)(tt * (double)rc.P * q2w - wak * (double)rc.corr));
+                }
               }
             }
           }
