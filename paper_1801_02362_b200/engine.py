@@ -1249,11 +1249,19 @@ class PathCVTC:
                                          dub_in=dub)
             del Dc
             ntl = self.mind.shape[1]
-            perm0 = K.sort_by_key(key, ntl + 1)
+            # only the frames with an admissible tile in THIS shard are gathered and screened
+            # (empty hulls [ntl, 0) get their own last bin): ~T/G x (shards per hull) rows
+            # instead of all T
+            act = hhi > 0
+            perm0 = K.sort_by_key(torch.where(act, key, torch.full_like(key, ntl + 1)).contiguous(), ntl + 2)
+            nact = int(act.sum().item())
+            perm0 = perm0[:nact].contiguous()
             fs = K.gather_split(fs_all, perm0)
             tlist, nlist, rlo, rhi = K.band_tiles(perm0, hlo, hhi, 128, 48, self.L, ntl)
-            Dest = torch.empty((T, self.L), dtype=torch.float32, device=dev)
-            K.msd_estimate(fs, self.ls, Dest, grid=K2_GRID, tlist=tlist, nlist=nlist)
+            Dest = torch.empty((max(nact, 1), self.L), dtype=torch.float32, device=dev)
+            if nact:
+                K.msd_estimate(fs, self.ls, Dest[:nact], grid=K2_GRID, tlist=tlist, nlist=nlist)
+            Dest = Dest[:nact]
         else:
             fs = fs_all
             Dest = K.msd_estimate(fs, self.ls)
@@ -1262,8 +1270,8 @@ class PathCVTC:
         _, _, dmin, _ = K.candidates(Dest, self.lam, self.cutoff + self.margin, 1, fnorm=fnorm, fcoef=fcoef,
                                      rlo=rlo, rhi=rhi)
         p = perm0.long() if perm0 is not None else None
-        if p is not None:
-            dm = torch.empty_like(dmin)
+        if p is not None:  # frame order; frames screened on no tile of this shard: +inf
+            dm = torch.full((T,), float("inf"), dtype=dmin.dtype, device=dev)
             dm[p] = dmin
             dmin = dm
         dref = yield ("min", dmin)
@@ -1272,8 +1280,9 @@ class PathCVTC:
         lo, cnt, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, self.L, fnorm=fnorm,
                                           fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
         del Dest
-        if p is not None:  # back to frame order
-            lo_f, cnt_f = torch.empty_like(lo), torch.empty_like(cnt)
+        if p is not None:  # back to frame order (unscreened frames: empty window here)
+            lo_f = torch.zeros((T,), dtype=lo.dtype, device=dev)
+            cnt_f = torch.zeros((T,), dtype=cnt.dtype, device=dev)
             lo_f[p], cnt_f[p] = lo, cnt
             lo, cnt = lo_f, cnt_f
         win = torch.stack([lo + off, cnt]).to(torch.int32)
