@@ -246,9 +246,11 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
  * three axis rows 3k + b over the atoms get a power-of-two scale 2^e[3k + b] and 4
  * signed int8 digits, stored per 32-atom k-step interleaved: dig [3B, kpad/32, 4, 32]
  * (kpad % 32 == 0, kpad >= n).  Landmarks: weighted, once per set; frames: per call,
- * in the refit's window-sorted order. */
+ * in the refit's window-sorted order.  ein [*, 3] (nullable, unweighted rows only): the
+ * exponents of structure perm[k] precomputed by mc_center_split16_uniform (one pass). */
 int mc_row_digits(const float* raw, const double* centroid, const double* w, const int32_t* perm,
-                  const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e, void* stream);
+                  const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e,
+                  const int32_t* ein, void* stream);
 /* mc_refine on the int8 tensor cores (tcgen05.mma.kind::i8, 10 digit products, int32
  * TMEM accumulation, S exact to ~2^-31 of its scale): same outputs as mc_refine from the
  * row digits of the landmarks (ldig, eL: mc_row_digits weighted) and of the frames in
@@ -316,10 +318,12 @@ int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, i
  * the n atoms, fp32 AoS input, n % 4 == 0, 16-byte aligned): the same outputs (halves,
  * scale, opnorm, rigorous rnorm bound, centroid, G = wuni sum |x - c|^2, wbar = 0,
  * flags) from one fp64 moment pass (shifted by the first atom) and one fp32 split pass
- * (geometry.py:67-76 centring).  mom is not produced. */
+ * (geometry.py:67-76 centring).  mom is not produced.  dexp [count, 3] (nullable): the
+ * per-axis int8 row-digit exponents of the unweighted centred rows, from the per-axis
+ * coordinate extrema of the first pass (mc_row_digits' ein: one pass instead of two). */
 int mc_center_split16_uniform(const float* coords, int64_t count, int32_t n, int32_t kpad, double wuni, void* hl,
                               double* scale_inv, double* opnorm, double* rnorm, double* centroid, double* gnorm,
-                              double* wbar, uint8_t* flags, void* stream);
+                              double* wbar, uint8_t* flags, int32_t* dexp, void* stream);
 int mc_msd_f16(const void* fhl, const void* lhl, const double* fscale, const double* lscale, const double* gx,
                const double* ga, int32_t T, int32_t L, int32_t kpad, int32_t terms, const int32_t* tlist,
                const int32_t* nlist, float* D, int64_t ldd, int32_t grid, void* stream);

@@ -79,7 +79,7 @@ _SIGS = {
     "mc_grad_i8_wide_plan": [_I32, _I32, _I32, _P, _P, _P, _P, _P],
     "mc_pathcv_grad_i8_wide": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                                _P, _I32, _I32, _P, _I32, _P, _P, _I64, _P, _P],
-    "mc_center_split16_uniform": [_P, _I64, _I32, _I32, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "mc_center_split16_uniform": [_P, _I64, _I32, _I32, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "mc_candidates_life": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _I32, _P, _P, _P, _P, _P],
     "mc_refine_i8_close": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P, _P],
     "mc_prune_plan": [_P, _I32, _I32, _I64, _P, _P, _P, _P, _D, _P, _P, _I32, _I32, _D, _I32, _I32, _P, _P, _P, _P, _P,
@@ -95,7 +95,7 @@ _SIGS = {
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],
     "mc_ldig_prep": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
-    "mc_row_digits": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P],
+    "mc_row_digits": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
     "mc_refine_i8": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P],
     "mc_pathcv_grad_i8": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P, _I32, _I32, _P, _P, _I64, _P],

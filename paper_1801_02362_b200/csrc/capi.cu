@@ -231,10 +231,12 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
 }
 
 int mc_row_digits(const float* raw, const double* centroid, const double* w, const int32_t* perm,
-                  const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e, void* stream) {
+                  const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e,
+                  const int32_t* ein, void* stream) {
   if (B < 0 || n < 2 || kpad < n || kpad % 32 != 0) return MC_ERR_CONFIG;
   if (B > 0 && (!raw || !centroid || !dig || !e)) return MC_ERR_CONFIG;
-  return cuda_status(mc::launch_rdig(raw, centroid, w, perm, fmap, B, n, kpad, dig, e, S_(stream)));
+  if (ein && w) return MC_ERR_CONFIG;  // precomputed exponents are those of the unweighted rows
+  return cuda_status(mc::launch_rdig(raw, centroid, w, perm, fmap, B, n, kpad, dig, e, S_(stream), ein));
 }
 
 int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T, int32_t L,
@@ -460,13 +462,13 @@ int mc_center_split16(const void* coords, int dtype, int64_t count, int32_t n, i
 
 int mc_center_split16_uniform(const float* coords, int64_t count, int32_t n, int32_t kpad, double wuni, void* hl,
                               double* scale_inv, double* opnorm, double* rnorm, double* centroid, double* gnorm,
-                              double* wbar, uint8_t* flags, void* stream) {
+                              double* wbar, uint8_t* flags, int32_t* dexp, void* stream) {
   if (n < 2) return MC_ERR_INVALID_STRUCTURE;
   if (count < 0 || kpad < n || kpad % 64 != 0 || n % 4 != 0 || !(wuni > 0.0)) return MC_ERR_CONFIG;
   if (count > 0 && (!coords || !hl || !scale_inv || !gnorm || (reinterpret_cast<uintptr_t>(coords) & 15)))
     return MC_ERR_CONFIG;
   return cuda_status(mc::launch_center_split16_uniform(coords, count, n, kpad, wuni, hl, scale_inv, opnorm, rnorm,
-                                                       centroid, gnorm, wbar, flags, S_(stream)));
+                                                       centroid, gnorm, wbar, flags, dexp, S_(stream)));
 }
 
 static int msd_f16_args(const void* fhl, const void* lhl, const double* fsc, const double* lsc, const double* gx,

@@ -82,7 +82,8 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
 size_t grad_i8_workspace(int T, int ncv);
 cudaError_t launch_center_split16_uniform(const float* coords, int64_t B, int n, int kpad, double wuni, void* hl,
                                           double* scale_inv, double* opnorm, double* rnorm, double* centroid,
-                                          double* gnorm, double* wbar, uint8_t* flags, cudaStream_t stream);
+                                          double* gnorm, double* wbar, uint8_t* flags, int* dexp,
+                                          cudaStream_t stream);
 cudaError_t launch_grad_i8_plan(int T, int cap, int ncv, const int* sig_idx, const int* nsig, const int* perm,
                                 long long* bytes, cudaStream_t stream);
 size_t grad_i8_wide_header_bytes(int nwide, int ncv);
@@ -93,7 +94,7 @@ cudaError_t launch_cv_grad_i8_wide(int T, int n, int cap, const float* fraw, con
                                    int out_f32, int ncv, const int* wide_ids, int nwide, const long long* wide_off,
                                    void* hws, void* wimg, cudaStream_t stream);
 cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
-                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream);
+                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream, const int* ein = nullptr);
 cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,
                              int kpad, const int* perm, const int* lo, const int* cnt, const double* gx,
                              const double* ga, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,

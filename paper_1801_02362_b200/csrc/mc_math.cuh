@@ -424,6 +424,17 @@ __device__ __forceinline__ double block_min(double v, double* scratch) {
   return r;
 }
 
+// power-of-two scale of an int8-digit row with max |v| = mx (refine_i8.cu / grad_i8.cu):
+// 2^e with mx 2^(7 - e) <= 127, so every value's 31-bit integer rint(v 2^(31 - e)) has
+// balanced base-256 digits with |d0| <= 127
+__device__ __forceinline__ int mc_digit_exp(double mx) {
+  if (!(mx > 0.0) || !isfinite(mx)) return 0;
+  int e;
+  frexp(mx, &e);  // mx < 2^e
+  if (ldexp(mx, 7 - e) > 127.0) ++e;
+  return e;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

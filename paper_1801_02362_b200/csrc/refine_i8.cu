@@ -135,7 +135,7 @@ __device__ __forceinline__ void digits4(double v, double qs, int8_t* d) {
 __global__ void __launch_bounds__(256)
 rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const double* __restrict__ w,
             const int* __restrict__ perm, const int* __restrict__ fmap, int B, int n, int kpad,
-            int8_t* __restrict__ dig, int* __restrict__ eout, int staged) {
+            int8_t* __restrict__ dig, int* __restrict__ eout, int staged, const int* __restrict__ ein) {
   extern __shared__ __align__(16) float sx[];  // the structure's 3n coordinates (staged mode)
   __shared__ double red[3][8];
   __shared__ int s_e[3];
@@ -158,6 +158,14 @@ rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const
   double c[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) c[b] = cen[3 * t + b];
+  if (ein) {  // exponents from the frame split (K1s): one pass over the coordinates
+    if (threadIdx.x < 3) {
+      const int e = ein[3 * t + threadIdx.x];
+      s_e[threadIdx.x] = e;
+      eout[3 * k + threadIdx.x] = e;
+    }
+    __syncthreads();
+  } else {
   double mx[3] = {0.0, 0.0, 0.0};
   for (int j = threadIdx.x; j < n; j += 256) {
     const double wj = w ? w[j] : 1.0;
@@ -179,6 +187,7 @@ rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const
     eout[3 * k + threadIdx.x] = e;
   }
   __syncthreads();
+  }
   // one thread per (k-step, axis, 4-atom quad): the 4 digits of 4 consecutive atoms packed
   // into one 32-bit word per digit plane, so 8 threads write a plane's 32 bytes
   const int nks = kpad / 32;
@@ -427,7 +436,7 @@ bool make_dig_map(CUtensorMap* m, const int8_t* dig, int64_t rows, int kpad, int
 }  // namespace
 
 cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
-                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream) {
+                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream, const int* ein) {
   if (B <= 0 || n <= 0) return cudaSuccess;
   if (kpad % 32 || kpad < n) return cudaErrorInvalidValue;
   // stage the structure in shared memory when it fits (n <= 16384: 192 KB)
@@ -439,7 +448,7 @@ cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, co
     if (e2 != cudaSuccess) return e2;
     attr = true;
   }
-  rdig_kernel<<<B, 256, smem, stream>>>(raw, cen, w, perm, fmap, B, n, kpad, dig, e, staged);
+  rdig_kernel<<<B, 256, smem, stream>>>(raw, cen, w, perm, fmap, B, n, kpad, dig, e, staged, w ? nullptr : ein);
   return cudaGetLastError();
 }
 

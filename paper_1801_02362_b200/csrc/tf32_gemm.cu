@@ -324,15 +324,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT)
 center_split_f16x1_uni_kernel(const float* __restrict__ coords, int64_t B, int n, int kpad, double wuni,
                               __half* __restrict__ hi, double* __restrict__ scale_inv, double* __restrict__ centroid,
                               double* __restrict__ gnorm, double* __restrict__ wbar, uint8_t* __restrict__ flags,
-                              double* __restrict__ opnorm, double* __restrict__ rnorm) {
+                              double* __restrict__ opnorm, double* __restrict__ rnorm, int* __restrict__ dexp) {
   __shared__ double scratch[6 * (NT / 32)];
+  __shared__ float s_ext[6][NT / 32];
   const int64_t b = blockIdx.x;
   const float* xb = coords + b * (int64_t)n * 3;
   const float4* x4 = reinterpret_cast<const float4*>(xb);
   const int G = n / 4;
   const double p0 = (double)__ldg(xb), p1 = (double)__ldg(xb + 1), p2 = (double)__ldg(xb + 2);
   double u[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // U1 (3), U2 (3)
-  float xmax = 0.0f;
+  // per-axis maximum and (negated) minimum of the raw coordinates: max|x - c| per axis
+  // (the frame's int8 row-digit exponents) = max(xmax - c, c - xmin), no extra pass
+  float ext[6] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll 2
   for (int gi = threadIdx.x; gi < G; gi += NT) {
     const float4 q0 = x4[3 * gi], q1 = x4[3 * gi + 1], q2 = x4[3 * gi + 2];
@@ -344,11 +347,26 @@ center_split_f16x1_uni_kernel(const float* __restrict__ coords, int64_t B, int n
         const double y = (double)f[3 * a + p] - (p == 0 ? p0 : (p == 1 ? p1 : p2));
         u[p] += y;
         u[3 + p] = fma(y, y, u[3 + p]);
-        xmax = fmaxf(xmax, fabsf(f[3 * a + p]));
+        ext[p] = fmaxf(ext[p], f[3 * a + p]);
+        ext[3 + p] = fmaxf(ext[3 + p], -f[3 * a + p]);
       }
     }
   }
-  const double xm = -block_min<NT>(-(double)xmax, scratch);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ext[k] = fmaxf(ext[k], __shfl_xor_sync(0xffffffffu, ext[k], o));
+    if ((threadIdx.x & 31) == 0) s_ext[k][threadIdx.x >> 5] = ext[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    float m = s_ext[k][0];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i) m = fmaxf(m, s_ext[k][i]);
+    ext[k] = m;
+  }
+  const double xm = (double)fmaxf(fmaxf(fmaxf(ext[0], ext[3]), fmaxf(ext[1], ext[4])), fmaxf(ext[2], ext[5]));
   block_sum_n<NT, 6>(u, scratch);
   const double inv_n = 1.0 / (double)n;
   const double c[3] = {p0 + u[0] * inv_n, p1 + u[1] * inv_n, p2 + u[2] * inv_n};
@@ -409,6 +427,9 @@ center_split_f16x1_uni_kernel(const float* __restrict__ coords, int64_t B, int n
     if (flags) flags[b] = nonfinite ? kFlagNonFinite : 0;
     const double on = sqrt(on2);
     if (opnorm) opnorm[b] = on;
+    if (dexp)  // the exponents mc_row_digits would compute for this frame (unweighted rows)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) dexp[3 * b + p] = mc_digit_exp(fmax((double)ext[p] - c[p], c[p] + (double)ext[3 + p]));
     const double cn = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
     if (rnorm)
       rnorm[b] = f32s ? sqrt(r2d) * (1.0 + 1e-5) + ldexp(1.0 + ldexp(1.0, -20), -24) * (on + 2.0 * sqrt((double)n) * cn)
@@ -419,11 +440,13 @@ center_split_f16x1_uni_kernel(const float* __restrict__ coords, int64_t B, int n
 
 cudaError_t launch_center_split16_uniform(const float* coords, int64_t B, int n, int kpad, double wuni, void* hl,
                                           double* scale_inv, double* opnorm, double* rnorm, double* centroid,
-                                          double* gnorm, double* wbar, uint8_t* flags, cudaStream_t stream) {
+                                          double* gnorm, double* wbar, uint8_t* flags, int* dexp,
+                                          cudaStream_t stream) {
   if (B <= 0) return cudaSuccess;
   if (n % 4 || kpad % 4 || (reinterpret_cast<uintptr_t>(coords) & 15) || B > 0x7fffffffLL) return cudaErrorInvalidValue;
   center_split_f16x1_uni_kernel<256><<<(unsigned)B, 256, 0, stream>>>(coords, B, n, kpad, wuni, (__half*)hl, scale_inv,
-                                                                      centroid, gnorm, wbar, flags, opnorm, rnorm);
+                                                                      centroid, gnorm, wbar, flags, opnorm, rnorm,
+                                                                      dexp);
   return cudaGetLastError();
 }
 

@@ -643,7 +643,8 @@ class PathCVTC:
         window-sorted order, then mc_refine_i8) or the fp64 DMMA kernel."""
         T = fs.count
         if self.rdl is not None:
-            self._fdbuf = K.row_digits(fr, fs.centroid, None, perm=perm, fmap=fmap, count=T, out=self._fdbuf)
+            self._fdbuf = K.row_digits(fr, fs.centroid, None, perm=perm, fmap=fmap, count=T, out=self._fdbuf,
+                                       ein=fs.dexp)
             return K.refine_i8(self.rdl, self._fdbuf, T, self.L, self.n, fs.g, self.ls.g, perm=perm, lo=lo, cnt=cnt,
                                cap=cap)
         return K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap, fmap=fmap,
@@ -707,12 +708,14 @@ class PathCVTC:
     def msd_matrix(self, frames, exact=True, out=None):
         """[T, L] fp32 aligned MSDs: exact=True every pair refit exactly (int8 tensor cores,
         or DMMA), exact=False the split-precision estimate.  out: optional [T, L] buffer."""
-        fr, fs = self._frames(frames)
+        # exact refits need only the frames' centroids / G (one-term split: the uniform-weight
+        # K1s also yields the row-digit exponents); the estimate needs the split operand
+        fr, fs = self._frames(frames, 1 if (exact and self.fmt == "f16" and self.rdl is not None) else 3)
         D = torch.empty((fr.shape[0], self.L), dtype=torch.float32, device=self.device) if out is None else out
         if not exact:
             return K.msd_estimate(fs, self._lsplit(3), D)
         if self.rdl is not None:
-            self._fdbuf = K.row_digits(fr, fs.centroid, None, count=fr.shape[0], out=self._fdbuf)
+            self._fdbuf = K.row_digits(fr, fs.centroid, None, count=fr.shape[0], out=self._fdbuf, ein=fs.dexp)
             _, _, flags = K.refine_i8(self.rdl, self._fdbuf, fr.shape[0], self.L, self.n, fs.g, self.ls.g, Dd=D)
         else:
             _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D, wuni=self.wuni)

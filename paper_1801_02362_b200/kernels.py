@@ -464,7 +464,7 @@ def gather_split(sp, idx):
             call("mc_gather_rows", ptr(sp.lo[p]), 4, sp.lo.shape[2], ptr(idx), rows, ptr(lo[p]), stream_ptr())
     g = lambda x: None if x is None else gather_rows(x, idx)  # noqa: E731
     return Split(hi, lo, g(sp.centroid), g(sp.g), g(sp.wbar), g(sp.mom), sp.flags, sp.n, sp.kpad, g(sp.scale),
-                 sp.fmt, sp.terms, g(sp.opnorm), g(sp.rnorm))
+                 sp.fmt, sp.terms, g(sp.opnorm), g(sp.rnorm), g(sp.dexp))
 
 
 def gather_rows(src, idx):
@@ -524,7 +524,7 @@ class RowDigits:
         self.dig, self.e, self.kpad, self.count = dig, e, kpad, count
 
 
-def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None):
+def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None, ein=None):
     """raw [*, n, 3] fp32 (rows read through fmap / perm), centroid [*, 3] fp64 -> RowDigits."""
     n = raw.shape[1]
     B = int(count if count is not None else (perm.numel() if perm is not None else raw.shape[0]))
@@ -535,7 +535,7 @@ def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None
     else:
         dig, e = out.dig, out.e
     call("mc_row_digits", ptr(raw.contiguous()), ptr(centroid.contiguous()), ptr(w), ptr(perm), ptr(fmap), B, n, kpad,
-         ptr(dig), ptr(e), stream_ptr())
+         ptr(dig), ptr(e), ptr(None if (ein is None or w is not None) else ein.contiguous()), stream_ptr())
     return RowDigits(dig, e, kpad, B)
 
 
@@ -598,13 +598,14 @@ class Split:
     scale = 2^-e per structure; + per-structure scalars."""
 
     __slots__ = ("hi", "lo", "scale", "fmt", "terms", "opnorm", "rnorm", "centroid", "g", "wbar", "mom", "flags", "n",
-                 "kpad", "count")
+                 "kpad", "count", "dexp")
 
     def __init__(self, hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale=None, fmt="tf32", terms=3, opnorm=None,
-                 rnorm=None):
+                 rnorm=None, dexp=None):
         self.hi, self.lo, self.centroid, self.g, self.wbar, self.mom, self.flags = hi, lo, centroid, g, wbar, mom, flags
         self.scale, self.fmt, self.terms, self.opnorm, self.rnorm = scale, fmt, terms, opnorm, rnorm
         self.n, self.kpad, self.count = n, kpad, hi.shape[1]
+        self.dexp = dexp  # [count, 3] int32 row-digit exponents (uniform-weight K1s) or None
 
 
 # uniform-weight one-term K1s (mc_center_split16_uniform); env MC_K1_UNIFORM=0 disables
@@ -644,8 +645,10 @@ def center_split(coords, w_align, w_disp, weighted, moments=False, fmt=None, ter
     flags = torch.empty((b,), dtype=U8, device=dev)
     if (fmt == "f16" and terms == 1 and wuni > 0.0 and K1_UNIFORM and not weighted and not moments
             and dt == _lib.MC_F32 and n % 4 == 0 and coords.data_ptr() % 16 == 0):
+        dexp = torch.empty((b, 3), dtype=I32, device=dev)
         call("mc_center_split16_uniform", ptr(coords), b, n, kpad, float(wuni), ptr(hi), ptr(scale), ptr(opnorm),
-             ptr(rnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(flags), stream_ptr())
+             ptr(rnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(flags), ptr(dexp), stream_ptr())
+        return Split(hi, lo, centroid, g, wbar, mom, flags, n, kpad, scale, fmt, terms, opnorm, rnorm, dexp)
     elif fmt == "f16":
         call("mc_center_split16", ptr(coords), dt, b, n, kpad, ptr(w_align), ptr(w_disp), 1 if weighted else 0,
              terms, ptr(hi), ptr(scale), ptr(opnorm), ptr(rnorm), ptr(centroid), ptr(g), ptr(wbar), ptr(mom),

@@ -180,3 +180,22 @@ def test_i8_dense_refits_near_identical_pairs(cuda_device):
     assert np.all(np.abs(D - ref) <= np.maximum(1e-6 * np.abs(ref), 1e-9 + 6e-8 * np.abs(ref)))
     d0 = np.abs(D[np.arange(20), np.arange(20)] - ref[np.arange(20), np.arange(20)])
     assert d0.max() <= 1e-9, d0.max()
+
+
+def test_row_digit_exponents_from_k1s_equal_two_pass(cuda_device):
+    """mc_row_digits with the exponents of the uniform-weight K1s (per-axis extrema of its
+    first pass; one pass over the coordinates) == the two-pass row digits: identical
+    exponents and digits, in a permuted order, with a translated and a rescaled frame."""
+    wl = synth.config4(seed=13, T=200, L=64, N=1000)
+    x = torch.from_numpy(wl.frames).cuda()
+    x[7] += 30.0
+    x[11] *= 1e-3
+    n = x.shape[1]
+    w = torch.full((n,), 1.0 / n, dtype=torch.float64, device=x.device)
+    sp = K.center_split(x, w, w, weighted=False, fmt="f16", terms=1, wuni=1.0 / n)
+    assert sp.dexp is not None
+    perm = torch.randperm(200, device=x.device).to(torch.int32)
+    a = K.row_digits(x, sp.centroid, None, perm=perm)
+    b = K.row_digits(x, sp.centroid, None, perm=perm, ein=sp.dexp)
+    assert torch.equal(a.e, b.e)
+    assert torch.equal(a.dig, b.dig)
