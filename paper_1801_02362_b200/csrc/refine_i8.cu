@@ -18,16 +18,19 @@
 // Error: each operand is exact to 2^-31 of its row maximum, so S is exact to
 // ~2^-31 sqrt(n)/n of |x||w a| -- ~1e-11 on the MSD at config 4 (tolerance 1e-9).
 //
-// Tile: M = 128 TMEM lanes = 42 landmarks x 3 axes (lanes 126, 127 unused), N = 48 =
-// 16 window-sorted frames x 3 axes; per 32-atom k-step 10 MMAs (M=128, N=48, K=32),
-// one per digit product (A = LD digit q, B = FD digit p: the K slices [32q, 32q + 32)
-// and [32p, 32p + 32) of the interleaved rows) into the TMEM columns of level p + q.
-// Accumulators 4 levels x 48 columns, double-buffered (384 of 512 TMEM columns), so a
-// tile's epilogue (staging the 9 entries of each pair in shared memory, then one thread
-// per in-window pair runs the fit) overlaps the next tile's MMAs.  A frame group takes
-// ceil(union / 42) landmark tiles of its window union.  Warp roles (256 threads,
-// persistent over frame groups): 0 TMA producer (7-stage ring of 22 KB: 16 KB of
-// landmark rows + 6 KB of frame rows per k-step), 1 MMA issuer, 2 TMEM allocator,
+// Tile: M = 128 TMEM lanes = 42 landmarks x 3 axes (lanes 126, 127 unused), N = 64 =
+// 21 window-sorted frames x 3 axes (+ one ignored row); per 32-atom k-step 10 MMAs
+// (M=128, N=64, K=32), one per digit product (A = LD digit q, B = FD digit p: the K slices
+// [32q, 32q + 32) and [32p, 32p + 32) of the interleaved rows) into the TMEM columns of
+// level p + q.  Accumulators 4 levels x 64 columns, double-buffered (all 512 TMEM
+// columns), so a tile's epilogue (staging the 9 entries of each pair in shared memory,
+// then one thread per in-window pair runs the fit) overlaps the next tile's MMAs.  21
+// frames per group (not 16) cut the operand bytes per multiply-add by 18%: the kernel is
+// bound by the L2 -> shared-memory rate of its operand boxes.  A frame group takes
+// ceil(union / 42) landmark tiles of its window union, odd tiles sweeping K backwards
+// (serpentine: they start on the frame rows still in L2).  Warp roles (256 threads,
+// persistent over frame groups): 0 TMA producer (6-stage ring of 24 KB: 16 KB of
+// landmark rows + 8 KB of frame rows per k-step), 1 MMA issuer, 2 TMEM allocator,
 // 4-7 epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -38,17 +41,18 @@
 namespace mc {
 
 namespace ri8 {
-constexpr int FG = 16;             // frames per group
-constexpr int NR = 3 * FG;         // 48 N rows
+constexpr int FG = 21;             // frames per group
+constexpr int NR = 3 * FG;         // 63 N rows used
+constexpr int NB = 64;             // MMA N and frame-digit box rows (row 63: the next group's, ignored)
 constexpr int LT = 42;             // landmarks per tile
 constexpr int MR = 128;            // M rows (TMEM lanes); 3 LT = 126 used
 constexpr int KS = 32;             // atoms per k-step
 constexpr int ROWB = 4 * KS;       // 128 bytes per row and k-step (4 digits)
 constexpr int A_ST = MR * ROWB;    // 16 KB
-constexpr int B_ST = NR * ROWB;    // 6 KB
-constexpr int STAGE = A_ST + B_ST; // 22 KB (a multiple of 1024)
-constexpr int NST = 7;
-constexpr int ACC = 4 * NR;        // 192 TMEM columns per accumulator buffer
+constexpr int B_ST = NB * ROWB;    // 8 KB
+constexpr int STAGE = A_ST + B_ST; // 24 KB (a multiple of 1024)
+constexpr int NST = 6;
+constexpr int ACC = 4 * NB;        // 256 TMEM columns per accumulator buffer (2 buffers = 512)
 constexpr int EPI = 4;             // epilogue warps (one per TMEM lane quarter)
 constexpr int NT = 32 * (4 + EPI);
 constexpr int SC_BYTES = FG * LT * 9 * 8;  // staged covariances of a tile (fp64)
@@ -84,7 +88,7 @@ __device__ __forceinline__ uint64_t desc128(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 // D = S32, A = B = signed 8 bit, K-major, N = 48, M = 128
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NR >> 3) << 17) | ((uint32_t)(MR >> 4) << 24);
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(MR >> 4) << 24);
 __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -99,6 +103,9 @@ __device__ __forceinline__ void tld8(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
+}
+__device__ __forceinline__ void tld1(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(taddr));
 }
 __device__ __forceinline__ void tld4(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
@@ -268,8 +275,12 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int g = blockIdx.x; g < groups; g += gridDim.x) {
         int wlo, whi;
         union_of(g, wlo, whi);
-        for (int l0 = wlo; l0 < whi; l0 += LT)
-          for (int ks = 0; ks < nks; ++ks, ++st) {
+        // serpentine k order: odd landmark tiles of a group sweep K backwards, so they start
+        // on the frame rows the previous tile read last (still in L2) instead of re-reading
+        // the group's frame rows from HBM in the same order
+        for (int l0 = wlo, ti = 0; l0 < whi; l0 += LT, ++ti)
+          for (int j = 0; j < nks; ++j, ++st) {
+            const int ks = (ti & 1) ? nks - 1 - j : j;
             const int s = st % NST;
             mb_wait(&empty[s], ((st / NST) & 1) ^ 1);
             mb_expect(&full[s], (uint32_t)STAGE);
@@ -290,7 +301,7 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         mb_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + (uint32_t)(ab * ACC);
-        for (int ks = 0; ks < nks; ++ks, ++st) {
+        for (int j = 0; j < nks; ++j, ++st) {  // (the k order does not matter to the MMAs)
           const int s = st % NST;
           mb_wait(&full[s], (st / NST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -302,11 +313,11 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
               for (int p = 0; p <= lvl; ++p) {
                 const int q = lvl - p;
-                mma_i8(d + (uint32_t)(NR * lvl), desc128(a + KS * q), desc128(b + KS * p),
-                       (ks > 0 || p > 0) ? 1u : 0u);
+                mma_i8(d + (uint32_t)(NB * lvl), desc128(a + KS * q), desc128(b + KS * p),
+                       (j > 0 || p > 0) ? 1u : 0u);
               }
             mma_commit(&empty[s]);
-            if (ks == nks - 1) mma_commit(&tfull[ab]);
+            if (j == nks - 1) mma_commit(&tfull[ab]);
           }
           __syncwarp();
         }
@@ -340,18 +351,18 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         __syncwarp();
         const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(ab * ACC);
 #pragma unroll 1
-        for (int fc = 0; fc < FG / 4; ++fc) {  // 4 frames (12 columns) at a time
-          uint32_t acc[4][12];
+        for (int fc = 0; fc < FG / 3; ++fc) {  // 3 frames (9 columns) at a time
+          uint32_t acc[4][9];
 #pragma unroll
           for (int lvl = 0; lvl < 4; ++lvl) {
-            tld8(tb + NR * lvl + 12 * fc, &acc[lvl][0]);
-            tld4(tb + NR * lvl + 12 * fc + 8, &acc[lvl][8]);
+            tld8(tb + NB * lvl + 9 * fc, &acc[lvl][0]);
+            tld1(tb + NB * lvl + 9 * fc + 8, &acc[lvl][8]);
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (lok) {
 #pragma unroll
-            for (int c = 0; c < 12; ++c) {
-              const int f = 4 * fc + c / 3, b = c % 3;
+            for (int c = 0; c < 9; ++c) {
+              const int f = 3 * fc + c / 3, b = c % 3;
               const double v = (double)(int)acc[0][c] * 16777216.0 + (double)(int)acc[1][c] * 65536.0 +
                                (double)(int)acc[2][c] * 256.0 + (double)(int)acc[3][c];
               sC[(f * LT + lp) * 9 + 3 * b + gg] = v * pow2d(s_eF[3 * f + b] + el - 38);
@@ -460,7 +471,7 @@ cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fd
   if (T <= 0 || L <= 0) return cudaSuccess;
   if (kpad % 32 || kpad < n || n >= 32768) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
-  if (!make_dig_map(&ma, ldig, 3LL * L, kpad, MR) || !make_dig_map(&mb, fdig, 3LL * T, kpad, NR))
+  if (!make_dig_map(&ma, ldig, 3LL * L, kpad, MR) || !make_dig_map(&mb, fdig, 3LL * T, kpad, NB))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
