@@ -247,13 +247,18 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
  * signed int8 digits, stored per 32-atom k-step interleaved: dig [3B, kpad/32, 4, 32]
  * (kpad % 32 == 0, kpad >= n).  Landmarks: weighted, once per set; frames: per call,
  * in the refit's window-sorted order.  ein [*, 3] (nullable, unweighted rows only): the
- * exponents of structure perm[k] precomputed by mc_center_split16_uniform (one pass). */
+ * exponents of structure perm[k] precomputed by mc_center_split16_uniform (one pass).
+ * planes = 1: the digit-plane layout dig [kpad/32][4][3B][32] (plane (k-step, digit) holds
+ * every row's 32 bytes) -- the FRAME operand of mc_refine_i8, whose B tile is one 3-D TMA
+ * box of 4 planes x 64 rows so one MMA covers several digit products; landmarks (A) keep
+ * planes = 0. */
 int mc_row_digits(const float* raw, const double* centroid, const double* w, const int32_t* perm,
                   const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e,
-                  const int32_t* ein, void* stream);
+                  const int32_t* ein, int32_t planes, void* stream);
 /* mc_refine on the int8 tensor cores (tcgen05.mma.kind::i8, 10 digit products, int32
  * TMEM accumulation, S exact to ~2^-31 of its scale): same outputs as mc_refine from the
- * row digits of the landmarks (ldig, eL: mc_row_digits weighted) and of the frames in
+ * row digits of the landmarks (ldig, eL: mc_row_digits weighted, planes = 0) and of the
+ * frames (planes = 1) in
  * perm order (fdig, eF); gx / ga = the structures' weighted G norms; n < 32768. */
 int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T, int32_t L,
                  int32_t n, int32_t kpad, const int32_t* perm, const int32_t* lo, const int32_t* cnt, const double* gx,

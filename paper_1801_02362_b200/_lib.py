@@ -95,7 +95,7 @@ _SIGS = {
                      _P, _P],
     "mc_property_map": [_I32, _I32, _P, _P, _P, _D, _P, _P, _P, _P],
     "mc_ldig_prep": [_P, _P, _I32, _I32, _I32, _I32, _P, _P, _P],
-    "mc_row_digits": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
+    "mc_row_digits": [_P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32, _P],
     "mc_refine_i8": [_P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _I64, _P, _P],
     "mc_pathcv_grad_i8": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P, _I32, _I32, _P, _P, _I64, _P],

@@ -232,11 +232,11 @@ int mc_pathcv_grad_i8(int32_t T, int32_t n, int32_t cap, const float* fraw, cons
 
 int mc_row_digits(const float* raw, const double* centroid, const double* w, const int32_t* perm,
                   const int32_t* fmap, int32_t B, int32_t n, int32_t kpad, int8_t* dig, int32_t* e,
-                  const int32_t* ein, void* stream) {
-  if (B < 0 || n < 2 || kpad < n || kpad % 32 != 0) return MC_ERR_CONFIG;
+                  const int32_t* ein, int32_t planes, void* stream) {
+  if (B < 0 || n < 2 || kpad < n || kpad % 32 != 0 || (planes != 0 && planes != 1)) return MC_ERR_CONFIG;
   if (B > 0 && (!raw || !centroid || !dig || !e)) return MC_ERR_CONFIG;
   if (ein && w) return MC_ERR_CONFIG;  // precomputed exponents are those of the unweighted rows
-  return cuda_status(mc::launch_rdig(raw, centroid, w, perm, fmap, B, n, kpad, dig, e, S_(stream), ein));
+  return cuda_status(mc::launch_rdig(raw, centroid, w, perm, fmap, B, n, kpad, dig, e, S_(stream), ein, planes));
 }
 
 int mc_refine_i8(const int8_t* ldig, const int32_t* eL, const int8_t* fdig, const int32_t* eF, int32_t T, int32_t L,

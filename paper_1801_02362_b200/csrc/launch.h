@@ -94,7 +94,8 @@ cudaError_t launch_cv_grad_i8_wide(int T, int n, int cap, const float* fraw, con
                                    int out_f32, int ncv, const int* wide_ids, int nwide, const long long* wide_off,
                                    void* hws, void* wimg, cudaStream_t stream);
 cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
-                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream, const int* ein = nullptr);
+                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream, const int* ein = nullptr,
+                        int planes = 0);
 cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fdig, const int* eF, int T, int L, int n,
                              int kpad, const int* perm, const int* lo, const int* cnt, const double* gx,
                              const double* ga, int cap, double* Dex, double* Rex, float* Dd, int64_t ldd,

@@ -75,6 +75,13 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void tma3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -88,12 +95,21 @@ __device__ __forceinline__ uint64_t desc128(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 // D = S32, A = B = signed 8 bit, K-major, N = 48, M = 128
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(MR >> 4) << 24);
-__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+// D = S32, A = B = signed 8 bit, K-major, N = n, M = 128
+__host__ __device__ constexpr uint32_t idesc_n(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(MR >> 4) << 24);
+}
+constexpr uint32_t IDESC = idesc_n(NB);
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// K-major SWIZZLE_32B operand (32 B rows, 8-row groups 256 B apart), layout 6
+__device__ __forceinline__ uint64_t desc32(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(reinterpret_cast<uint64_t>(bar))
@@ -142,7 +158,7 @@ __device__ __forceinline__ void digits4(double v, double qs, int8_t* d) {
 __global__ void __launch_bounds__(256)
 rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const double* __restrict__ w,
             const int* __restrict__ perm, const int* __restrict__ fmap, int B, int n, int kpad,
-            int8_t* __restrict__ dig, int* __restrict__ eout, int staged, const int* __restrict__ ein) {
+            int8_t* __restrict__ dig, int* __restrict__ eout, int staged, const int* __restrict__ ein, int planes) {
   extern __shared__ __align__(16) float sx[];  // the structure's 3n coordinates (staged mode)
   __shared__ double red[3][8];
   __shared__ int s_e[3];
@@ -211,9 +227,16 @@ rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const
 #pragma unroll
       for (int q = 0; q < 4; ++q) word[q] |= (uint32_t)(uint8_t)d[q] << (8 * i);
     }
-    uint32_t* dst = reinterpret_cast<uint32_t*>(dig + ((int64_t)(3 * k + b) * nks + ks) * 128) + qd;
+    if (planes) {  // digit planes [nks][4][3B][32]: plane (ks, q) holds every row's 32 bytes
+      const int64_t R3 = 3LL * B;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dst[8 * q] = word[q];
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint32_t*>(dig + (((int64_t)ks * 4 + q) * R3 + 3 * k + b) * 32)[qd] = word[q];
+    } else {  // interleaved [3B][nks][4][32]: one 128-byte segment per row and k-step
+      uint32_t* dst = reinterpret_cast<uint32_t*>(dig + ((int64_t)(3 * k + b) * nks + ks) * 128) + qd;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[8 * q] = word[q];
+    }
   }
 }
 
@@ -286,7 +309,7 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             mb_expect(&full[s], (uint32_t)STAGE);
             uint8_t* dst = sSt + s * STAGE;
             tma2d(&mapA, &full[s], dst, ROWB * ks, 3 * l0);
-            tma2d(&mapB, &full[s], dst + A_ST, ROWB * ks, NR * g);
+            tma3d(&mapB, &full[s], dst + A_ST, 0, NR * g, 4 * ks);
           }
       }
     }
@@ -307,15 +330,16 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (lane == 0) {
             const uint32_t a = su32(sSt + s * STAGE), b = a + A_ST;
-            // level-major order: the 10 digit products with p + q <= 3
-#pragma unroll
-            for (int lvl = 0; lvl < 4; ++lvl)
-#pragma unroll
-              for (int p = 0; p <= lvl; ++p) {
-                const int q = lvl - p;
-                mma_i8(d + (uint32_t)(NB * lvl), desc128(a + KS * q), desc128(b + KS * p),
-                       (j > 0 || p > 0) ? 1u : 0u);
-              }
+            // the 10 digit products with p + q <= 3 in 4 MMAs: the B tile holds the frame
+            // digits plane by plane ([p][64 rows][32 B]), so for landmark digit q ONE MMA with
+            // N = (4 - q) 64 reads frame digits 0..3-q and writes the TMEM columns of levels
+            // q..3 (kind::i8 with N <= 64 is issue-bound at ~45 clk per MMA, N = 256 runs at
+            // N/2 clk: tools/_diag/i8_probe.cu)
+            const uint64_t bd = desc32(b);
+            mma_i8(d, desc128(a), bd, idesc_n(4 * NB), j > 0 ? 1u : 0u);
+            mma_i8(d + (uint32_t)NB, desc128(a + KS), bd, idesc_n(3 * NB), 1u);
+            mma_i8(d + (uint32_t)(2 * NB), desc128(a + 2 * KS), bd, idesc_n(2 * NB), 1u);
+            mma_i8(d + (uint32_t)(3 * NB), desc128(a + 3 * KS), bd, idesc_n(NB), 1u);
             mma_commit(&empty[s]);
             if (j == nks - 1) mma_commit(&tfull[ab]);
           }
@@ -433,6 +457,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_ri8() {
   return fn;
 }
 
+// frame digits in planes [nks][4][rows][32 B]: a 3-D map (32 B, rows, plane) whose box
+// (32, box_rows, 4) lands in shared memory as 4 digit planes of box_rows 32-byte rows
+bool make_dig_planes_map(CUtensorMap* m, const int8_t* dig, int64_t rows, int kpad, int box_rows) {
+  auto enc = get_encode_ri8();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(4 * (kpad / 32))};
+  cuuint64_t strides[2] = {32, (cuuint64_t)(32 * rows)};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 4};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(dig), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_dig_map(CUtensorMap* m, const int8_t* dig, int64_t rows, int kpad, int box_rows) {
   auto enc = get_encode_ri8();
   if (!enc) return false;
@@ -447,7 +485,7 @@ bool make_dig_map(CUtensorMap* m, const int8_t* dig, int64_t rows, int kpad, int
 }  // namespace
 
 cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, const int* perm, const int* fmap, int B,
-                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream, const int* ein) {
+                        int n, int kpad, int8_t* dig, int* e, cudaStream_t stream, const int* ein, int planes) {
   if (B <= 0 || n <= 0) return cudaSuccess;
   if (kpad % 32 || kpad < n) return cudaErrorInvalidValue;
   // stage the structure in shared memory when it fits (n <= 16384: 192 KB)
@@ -459,7 +497,8 @@ cudaError_t launch_rdig(const float* raw, const double* cen, const double* w, co
     if (e2 != cudaSuccess) return e2;
     attr = true;
   }
-  rdig_kernel<<<B, 256, smem, stream>>>(raw, cen, w, perm, fmap, B, n, kpad, dig, e, staged, w ? nullptr : ein);
+  rdig_kernel<<<B, 256, smem, stream>>>(raw, cen, w, perm, fmap, B, n, kpad, dig, e, staged, w ? nullptr : ein,
+                                        planes);
   return cudaGetLastError();
 }
 
@@ -471,7 +510,7 @@ cudaError_t launch_refine_i8(const int8_t* ldig, const int* eL, const int8_t* fd
   if (T <= 0 || L <= 0) return cudaSuccess;
   if (kpad % 32 || kpad < n || n >= 32768) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
-  if (!make_dig_map(&ma, ldig, 3LL * L, kpad, MR) || !make_dig_map(&mb, fdig, 3LL * T, kpad, NB))
+  if (!make_dig_map(&ma, ldig, 3LL * L, kpad, MR) || !make_dig_planes_map(&mb, fdig, 3LL * T, kpad, NB))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {

@@ -319,7 +319,7 @@ class PathCV:
         lo, cnt = lo_r[src].contiguous(), cnt_r[src].contiguous()
         ld = max(1, int(cnt.max().item()))
         perm = K.sort_by_key((2 * lo + cnt).to(torch.int32), 2 * self.L + 1)
-        fdig = K.row_digits(raw, fr.centroid, None, perm=perm, count=T)
+        fdig = K.row_digits(raw, fr.centroid, None, perm=perm, count=T, planes=True)
         S, D, R, rflags = K.refine_i8_close(tc.rdl, fdig, T, self.L, self.n, fr.g, self.lm.g, perm, lo, cnt, ld,
                                             refresh)
         del fdig
@@ -644,7 +644,7 @@ class PathCVTC:
         T = fs.count
         if self.rdl is not None:
             self._fdbuf = K.row_digits(fr, fs.centroid, None, perm=perm, fmap=fmap, count=T, out=self._fdbuf,
-                                       ein=fs.dexp)
+                                       ein=fs.dexp, planes=True)
             return K.refine_i8(self.rdl, self._fdbuf, T, self.L, self.n, fs.g, self.ls.g, perm=perm, lo=lo, cnt=cnt,
                                cap=cap)
         return K.refine(fr, fs, self.lraw, self.ls, self.w, perm=perm, lo=lo, cnt=cnt, cap=cap, fmap=fmap,
@@ -715,7 +715,8 @@ class PathCVTC:
         if not exact:
             return K.msd_estimate(fs, self._lsplit(3), D)
         if self.rdl is not None:
-            self._fdbuf = K.row_digits(fr, fs.centroid, None, count=fr.shape[0], out=self._fdbuf, ein=fs.dexp)
+            self._fdbuf = K.row_digits(fr, fs.centroid, None, count=fr.shape[0], out=self._fdbuf, ein=fs.dexp,
+                                       planes=True)
             _, _, flags = K.refine_i8(self.rdl, self._fdbuf, fr.shape[0], self.L, self.n, fs.g, self.ls.g, Dd=D)
         else:
             _, _, flags = K.refine(fr, fs, self.lraw, self.ls, self.w, Dd=D, wuni=self.wuni)

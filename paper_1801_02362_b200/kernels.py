@@ -524,8 +524,9 @@ class RowDigits:
         self.dig, self.e, self.kpad, self.count = dig, e, kpad, count
 
 
-def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None, ein=None):
-    """raw [*, n, 3] fp32 (rows read through fmap / perm), centroid [*, 3] fp64 -> RowDigits."""
+def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None, ein=None, planes=False):
+    """raw [*, n, 3] fp32 (rows read through fmap / perm), centroid [*, 3] fp64 -> RowDigits.
+    planes=True: the digit-plane layout [kpad/32, 4, 3B, 32] (the frame operand of refine_i8)."""
     n = raw.shape[1]
     B = int(count if count is not None else (perm.numel() if perm is not None else raw.shape[0]))
     kpad = ((n + 31) // 32) * 32
@@ -535,7 +536,8 @@ def row_digits(raw, centroid, w=None, perm=None, fmap=None, count=None, out=None
     else:
         dig, e = out.dig, out.e
     call("mc_row_digits", ptr(raw.contiguous()), ptr(centroid.contiguous()), ptr(w), ptr(perm), ptr(fmap), B, n, kpad,
-         ptr(dig), ptr(e), ptr(None if (ein is None or w is not None) else ein.contiguous()), stream_ptr())
+         ptr(dig), ptr(e), ptr(None if (ein is None or w is not None) else ein.contiguous()), 1 if planes else 0,
+         stream_ptr())
     return RowDigits(dig, e, kpad, B)
 
 

@@ -199,3 +199,8 @@ def test_row_digit_exponents_from_k1s_equal_two_pass(cuda_device):
     b = K.row_digits(x, sp.centroid, None, perm=perm, ein=sp.dexp)
     assert torch.equal(a.e, b.e)
     assert torch.equal(a.dig, b.dig)
+    # the digit-plane layout (the refits' frame operand) is the same digits transposed
+    c = K.row_digits(x, sp.centroid, None, perm=perm, ein=sp.dexp, planes=True)
+    R3, nks = a.dig.shape[0], a.dig.shape[1]
+    assert torch.equal(c.e, a.e)
+    assert torch.equal(c.dig.reshape(nks, 4, R3, 32), a.dig.permute(1, 2, 0, 3))
