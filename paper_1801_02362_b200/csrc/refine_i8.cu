@@ -211,9 +211,38 @@ rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const
   }
   __syncthreads();
   }
+  const int nks = kpad / 32;
+  if (planes) {
+    // digit planes [nks][4][3B][32]: one thread per (k-step, axis, 16-atom half) packs the
+    // 16 atoms' digit q into one 16-byte store per plane (a plane row is 32 bytes)
+    const int64_t R3 = 3LL * B;
+    for (int task = threadIdx.x; task < 6 * nks; task += 256) {
+      const int h = task & 1, rest = task >> 1;
+      const int ks = rest / 3, b = rest - 3 * ks;
+      const double qs = ldexp(1.0, 31 - s_e[b]);
+      uint32_t word[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) word[q][u] = 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = 32 * ks + 16 * h + 4 * u + i;
+          int8_t d[4] = {0, 0, 0, 0};
+          if (j < n) ri8::digits4((w ? w[j] : 1.0) * ((double)x[3 * j + b] - c[b]), qs, d);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) word[q][u] |= (uint32_t)(uint8_t)d[q] << (8 * i);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(dig + (((int64_t)ks * 4 + q) * R3 + 3 * k + b) * 32)[h] =
+            make_uint4(word[q][0], word[q][1], word[q][2], word[q][3]);
+    }
+    return;
+  }
   // one thread per (k-step, axis, 4-atom quad): the 4 digits of 4 consecutive atoms packed
   // into one 32-bit word per digit plane, so 8 threads write a plane's 32 bytes
-  const int nks = kpad / 32;
   for (int task = threadIdx.x; task < 24 * nks; task += 256) {
     const int qd = task & 7, rest = task >> 3;
     const int ks = rest / 3, b = rest - 3 * ks;
@@ -227,16 +256,10 @@ rdig_kernel(const float* __restrict__ raw, const double* __restrict__ cen, const
 #pragma unroll
       for (int q = 0; q < 4; ++q) word[q] |= (uint32_t)(uint8_t)d[q] << (8 * i);
     }
-    if (planes) {  // digit planes [nks][4][3B][32]: plane (ks, q) holds every row's 32 bytes
-      const int64_t R3 = 3LL * B;
+    // interleaved [3B][nks][4][32]: one 128-byte segment per row and k-step
+    uint32_t* dst = reinterpret_cast<uint32_t*>(dig + ((int64_t)(3 * k + b) * nks + ks) * 128) + qd;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint32_t*>(dig + (((int64_t)ks * 4 + q) * R3 + 3 * k + b) * 32)[qd] = word[q];
-    } else {  // interleaved [3B][nks][4][32]: one 128-byte segment per row and k-step
-      uint32_t* dst = reinterpret_cast<uint32_t*>(dig + ((int64_t)(3 * k + b) * nks + ks) * 128) + qd;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dst[8 * q] = word[q];
-    }
+    for (int q = 0; q < 4; ++q) dst[8 * q] = word[q];
   }
 }
 
