@@ -347,8 +347,10 @@ def _grad_i8_call(wres, fs, ls, frames, landmarks, w, w_align, cap, perm, out_ma
     ws, nb = _grad_i8_ws(T, ncv, dev)
     plan = _grad_i8_wide(wres, cap, perm, ncv, dev, T) if GRAD_I8_WIDE and n % 4 == 0 else None
     wf = wide_flag
-    if plan is not None and wf is None:
-        wf = torch.zeros((1,), dtype=I32, device=dev)  # narrow call: leave the wide groups out
+    if wf is None and (plan is not None or (GRAD_I8_WIDE and n % 4 == 0)):
+        # a non-NULL flag keeps the wide groups out of the narrow call (the streamed-A kernel
+        # runs them) and skips the DMMA fallback launch when there are none
+        wf = torch.zeros((1,), dtype=I32, device=dev)
     call("mc_pathcv_grad_i8", T, n, cap, ptr(frames), ptr(fs.centroid), ptr(landmarks), ptr(ls.centroid), ptr(w),
          ptr(w_align), ptr(ldig.dig), ptr(ldig.eB), ldig.npad, ldig.kpad, ptr(wres["sig_idx"]),
          ptr(wres["sig_coef"]), ptr(wres["nsig"]), ptr(wres["fvec"]), ptr(dV), ptr(perm), ptr(out_map), ptr(out0),
