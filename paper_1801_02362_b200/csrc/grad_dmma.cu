@@ -104,7 +104,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
                     const double* __restrict__ wa, const int* __restrict__ sig_idx,
                     const double* __restrict__ sig_coef, const int* __restrict__ nsig,
                     const double* __restrict__ fvec, const int* __restrict__ perm, const int* __restrict__ out_map,
-                    OT* __restrict__ ds, OT* __restrict__ dz, int apb, int min_width) {
+                    OT* __restrict__ ds, OT* __restrict__ dz, int apb, int min_width, int i8_dg) {
   extern __shared__ __align__(16) double dsm[];
   double* sA = dsm;                                       // [DR][AST] coefficients
   double* sLc = dsm + DR * AST;                           // [DKMAX] landmark centroid per kk
@@ -116,7 +116,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   uint64_t* full = reinterpret_cast<uint64_t*>(sWW + 2 * DNA);
   uint64_t* empty = full + NST;
   uint64_t* xfull = empty + NST;
-  __shared__ int s_t[DG], s_raw[DG], s_ns[DG], s_flo[DG], s_fhi[DG];
+  __shared__ int s_t[DG], s_raw[DG], s_ns[DG], s_flo[DG], s_fhi[DG], s_mine[DG];
   __shared__ double s_fc[DG][3], s_fv[DG][8];
   __shared__ int s_wlo, s_whi;
   __shared__ double s_bias[DR];
@@ -141,6 +141,22 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     s_ns[tid] = ns;
     s_flo[tid] = (t >= 0 && ns > 0) ? sig_idx[(int64_t)t * cap] : 0x7fffffff;
     s_fhi[tid] = (t >= 0 && ns > 0) ? sig_idx[(int64_t)t * cap + ns - 1] + 1 : -1;
+    // min_width >= 0: this call completes only the frames of the int8 kernel's WIDE groups
+    // (i8_dg sorted frames each, union wider than min_width landmarks; grad_i8.cu did the rest)
+    int mine = 1;
+    if (min_width >= 0 && k < T) {
+      const int k0 = (k / i8_dg) * i8_dg, k1 = min(T, k0 + i8_dg);
+      int a = 0x7fffffff, b = -1;
+      for (int kk = k0; kk < k1; ++kk) {
+        const int tt = perm ? perm[kk] : kk;
+        const int nn = nsig[tt];
+        if (nn <= 0) continue;
+        a = min(a, sig_idx[(int64_t)tt * cap]);
+        b = max(b, sig_idx[(int64_t)tt * cap + nn - 1] + 1);
+      }
+      mine = b >= 0 && b - a > min_width;
+    }
+    s_mine[tid] = mine;
     if (t >= 0) {
       for (int a = 0; a < 3; ++a) s_fc[tid][a] = fcen[3 * t + a];
       const double* fv = fvec + (int64_t)t * 16;
@@ -151,8 +167,9 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   if (tid < DR) {  // epilogue row table: r = (frame f, s|z, axis b)
     const int f = tid / 6, sz = (tid % 6) / 3, b = tid % 3;
     const int t = s_t[f];
-    s_rptr[tid] = t < 0 ? 0ull
-                        : reinterpret_cast<unsigned long long>((sz ? dz : ds) + (int64_t)s_raw[f] * n * 3 + b);
+    s_rptr[tid] = (t < 0 || !s_mine[f])
+                      ? 0ull
+                      : reinterpret_cast<unsigned long long>((sz ? dz : ds) + (int64_t)s_raw[f] * n * 3 + b);
     s_rcx[tid] = t < 0 ? 0.0 : s_fc[f][b];
     s_rsc[tid] = t < 0 ? 0.0 : s_fv[f][sz];
     s_rcorr[tid] = t < 0 ? 0.0 : s_fv[f][2 + sz * 3 + b];
@@ -160,10 +177,14 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
     s_bias[tid] = 0.0;  // stays 0 when the group has no significant landmark (sharded: empty windows)
   }
   if (tid == 0) {
-    int a = 0x7fffffff, b = -1;
-    for (int f = 0; f < DG; ++f) { a = min(a, s_flo[f]); b = max(b, s_fhi[f]); }
+    int a = 0x7fffffff, b = -1, any = 0;
+    for (int f = 0; f < DG; ++f) {
+      a = min(a, s_flo[f]);
+      b = max(b, s_fhi[f]);
+      any |= s_mine[f] && s_t[f] >= 0;
+    }
     s_wlo = a;
-    s_whi = b;
+    s_whi = any ? b : -1;  // no frame of this call here: nothing to write
   }
   if (VEC) {
     if (tid == 0) {
@@ -181,9 +202,7 @@ cv_grad_dmma_kernel(int T, int n, int cap, const float* __restrict__ fraw, const
   // window lies on other shards): nothing to contract and nothing to write -- those rows
   // belong to (and are completed by) other ranks
   if (whi < 0) return;
-  // min_width >= 0: only groups whose union is wider than min_width landmarks (the
-  // int8 tensor-core kernel, grad_i8.cu, has done the others)
-  if (min_width >= 0 && whi - wlo <= min_width) return;
+
   const bool restage = whi - wlo > DWMAX;
   const int nwc = whi > wlo ? (whi - wlo + DWMAX - 1) / DWMAX : 0;
   const bool ranged = nwc <= MAXWC;  // else: each restage filters the whole list
@@ -467,7 +486,7 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
                                 const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
                                 const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream,
-                                int min_width) {
+                                int min_width, int i8_dg) {
   if (T <= 0 || n <= 0) return cudaSuccess;
   // atoms per CTA: all of them when there are enough frame groups to fill the
   // machine (the coefficient staging is then paid once per group), else split
@@ -498,7 +517,7 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
 #define MC_GD_LAUNCH(OTT, V)                                                                                         \
   cv_grad_dmma_kernel<OTT, V><<<grid, DNT, DSMEM, stream>>>(T, n, cap, fraw, fcen, lraw, lcen, w, wa, sig_idx,     \
                                                             sig_coef, nsig, fvec, perm, out_map, (OTT*)ds,     \
-                                                            (OTT*)dz, apb, min_width)
+                                                            (OTT*)dz, apb, min_width, i8_dg > 0 ? i8_dg : DG)
   if (out_f32) {
     if (vec) MC_GD_LAUNCH(float, true); else MC_GD_LAUNCH(float, false);
   } else {

@@ -591,6 +591,11 @@ cstack_prep_wide_kernel(int T, int cap, const double* __restrict__ fcen, const i
   for (int e = tid; e < (int)(sizeof(GHdr<DG>) / 16); e += 128) hd[e] = hs[e];
 }
 
+// diagnostic switch (env MC_GI8_EXP, results invalid): bit 0 = the epilogue only drains the
+// accumulators (TMEM loads, no recombination or stores) -- the MMA / TMA-side time; bit 1 =
+// no MMAs issued (commits only) -- the operand-delivery time
+__constant__ int c_gi8_exp = 0;
+
 template <typename OT, int NCV, bool WIDE>
 __global__ void __launch_bounds__(gi8::NT, 1)
 cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int npad, const float* __restrict__ fraw,
@@ -696,10 +701,12 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
             if (lane == 0) {
               const uint32_t lb = su32(sL + s * STG);
               const uint64_t bdesc = desc32(WIDE ? lb + (uint32_t)L_STAGE : cbase + (uint32_t)(j * C_KS));
-              mma_i8(d, desc128(lb), bdesc, ID0, j == 0 ? 0u : 1u);
-              mma_i8(d + R, desc128(lb + KS), bdesc, ID1, 1u);
-              mma_i8(d + 2 * R, desc128(lb + 2 * KS), bdesc, ID2, 1u);
-              mma_i8(d + 3 * R, desc128(lb + 3 * KS), bdesc, ID3, 1u);
+              if (!(c_gi8_exp & 2)) {
+                mma_i8(d, desc128(lb), bdesc, ID0, j == 0 ? 0u : 1u);
+                mma_i8(d + R, desc128(lb + KS), bdesc, ID1, 1u);
+                mma_i8(d + 2 * R, desc128(lb + 2 * KS), bdesc, ID2, 1u);
+                mma_i8(d + 3 * R, desc128(lb + 3 * KS), bdesc, ID3, 1u);
+              }
               mma_commit(&lempty[s]);
               if (j == nks - 1) mma_commit(&tfull[ab]);
             }
@@ -772,6 +779,12 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
           asm volatile("tcgen05.fence::before_thread_sync;");
           __syncwarp();
           if (lane == 0) mb_arrive(&tempty[ab]);
+          if (c_gi8_exp & 1) {
+            mb_wait(&xfull[ab], (it >> 1) & 1);
+            __syncwarp();
+            if (lane == 0) mb_arrive(&xempty[ab]);
+            continue;
+          }
           // per-atom constants: the B column scale 2^eB and the weights
           const int eb = valid ? eB[a] : 0;
           const double sxa = pow2d(14 - eb);
@@ -910,6 +923,13 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
     const char* e = getenv("MC_GI8_DBG");
     return e ? atoi(e) : 0;
   }();
+  static const bool exp_set = [] {
+    const char* e = getenv("MC_GI8_EXP");
+    if (!e) return true;
+    const int v = atoi(e);
+    return cudaMemcpyToSymbol(c_gi8_exp, &v, sizeof(int)) == cudaSuccess;
+  }();
+  (void)exp_set;
   CUtensorMap map;
   if (!make_ldig_map(&map, dig, npad, kpad)) return cudaErrorInvalidValue;
   const int sms = sm_count_i8();

@@ -70,7 +70,7 @@ cudaError_t launch_cv_grad_dmma(int T, int n, int cap, const float* fraw, const 
                                 const double* lcen, const double* w, const double* wa, const int* sig_idx,
                                 const double* sig_coef, const int* nsig, const double* fvec, const int* perm,
                                 const int* out_map, void* ds, void* dz, int out_f32, cudaStream_t stream,
-                                int min_width = -1);
+                                int min_width = -1, int i8_dg = 0);
 cudaError_t launch_ldig(const float* lraw, const double* lcen, int L, int n, int npad, int kpad, int* eB,
                         int8_t* dig, cudaStream_t stream);
 cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const double* fcen, const float* lraw,

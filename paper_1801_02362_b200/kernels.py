@@ -324,7 +324,7 @@ GRAD_I8_WIDE = __import__("os").environ.get("MC_GRAD_I8_WIDE", "1") == "1"
 def _grad_i8_wide(wres, cap, perm, ncv, dev, T):
     """Plan the wide frame groups of a mc_pathcv_grad_i8 call: (wide_ids, nwide, wide_off,
     header workspace, image workspace) or None when no group is wide (one host read)."""
-    DG = 8 if ncv == 2 else 16
+    DG = 8 if ncv == 2 else 16  # frames per group (csrc/grad_i8.cu Cfg<ncv>::DG)
     groups = (T + DG - 1) // DG
     by = torch.empty((groups,), dtype=torch.int64, device=dev)
     call("mc_grad_i8_wide_plan", T, cap, ncv, ptr(wres["sig_idx"]), ptr(wres["nsig"]), ptr(perm), ptr(by),
