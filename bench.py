@@ -282,7 +282,7 @@ class Config3:
             return "fp64_tensor_flop", 36.0 * n * float(self.last["nsig"].double().sum().item())
         if name == "mc_fit_dense":
             return "bytes", T * L * (72 + 8 + 72 + 1)
-        if name == "mc_refine_i8" and self.last is not None and "window_cnt" in self.last:
+        if name in ("mc_refine_i8", "mc_refine_i8_close") and self.last is not None and "window_cnt" in self.last:
             # pruned replay: every frame's covariances over its close structure's window
             # (9 multiply-adds per pair and atom x 10 digit products)
             return "int8_tensor_op_refine", 2.0 * 10.0 * 9.0 * n * float(self.last["window_cnt"].double().sum().item())

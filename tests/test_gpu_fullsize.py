@@ -33,6 +33,28 @@ def test_config1_fullsize_refresh_log_and_cv_vs_c_oracle(cuda_device):
         assert np.all(np.abs(got - r).reshape(300, -1).max(axis=1) <= 1e-5 * scale)
 
 
+def test_config1_fullsize_approximated_frames_vs_c_oracle(cuda_device):
+    """Config 1 at full size with a 4x larger refresh threshold, so that ~98% of the 20000
+    frames take the Eq. 5/6 approximation (the literal threshold refreshes every frame,
+    DESIGN.md H5): identical refresh log, s and z within 1e-6, D(x, y) within 1e-6, and
+    the Eq. 6 gradients (incl. the dR_xy term) of the first 300 frames within 1e-5."""
+    wl = synth.config1()
+    eps = 4.0 * wl.eps
+    out = engine.close_structure_replay(wl.frames, wl.landmarks, wl.lam, eps)
+    ref = C.close_replay(wl.frames, wl.landmarks, wl.lam, eps, grad=False)
+    np.testing.assert_array_equal(out["refresh"].cpu().numpy(), ref["refresh"])
+    assert 0.005 < ref["refresh"].mean() < 0.2
+    np.testing.assert_allclose(out["s"].cpu().numpy(), ref["s"], rtol=1e-6)
+    np.testing.assert_allclose(out["z"].cpu().numpy(), ref["z"], rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(out["dxy"].cpu().numpy()[1:], ref["dxy"][1:], rtol=1e-6, atol=1e-9)
+    sub = C.close_replay(wl.frames[:300], wl.landmarks, wl.lam, eps)
+    assert not sub["refresh"][1:].all()
+    for key in ("ds", "dz"):
+        got, r = out[key][:300].cpu().numpy(), sub[key]
+        scale = np.abs(r).reshape(300, -1).max(axis=1)
+        assert np.all(np.abs(got - r).reshape(300, -1).max(axis=1) <= 1e-5 * scale)
+
+
 def test_config4_fullsize_properties_and_spot_checks(cuda_device):
     wl = synth.interp_config_device(4, 131072, 8192, 10000, 32, cuda_device)
     pcv = engine.PathCVTC(torch.from_numpy(wl.landmarks).to(cuda_device), wl.lam, wl.q)
