@@ -430,7 +430,7 @@ class ConfigTC:
     def step_device(self):
         return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
 
-    def e2e_chunks(self):
+    def e2e_chunks(self, d2h_bound=False):
         """Chunk boundaries of the streamed step.  The H2D copy (2.16 us/frame at
         55.6 GB/s) is slower than the compute (~2.5 ms + 1.72 us/frame per chunk on
         config 4), so the step is copy-bound and ends one chunk-compute after the
@@ -446,6 +446,22 @@ class ConfigTC:
             e = max(32, (self.T // 32) // 32 * 32)
             mid = (self.T - 2 * e) // 2
             sizes = [e, mid, self.T - 2 * e - mid, e] if self.T > 4 * e else [self.T]
+            out, c0 = [], 0
+            for n in sizes:
+                out.append((c0, n))
+                c0 += n
+            return out
+        if not env and d2h_bound:
+            # the whole result back (ds, dz: 2x the input bytes): the D2H stream is the
+            # bottleneck, so it must start early -- a small first chunk, doubling to a steady
+            # size; the tail is short because every chunk's compute is far below its D2H
+            steady = max(1024, min(self.T // 8, 16384) // 32 * 32)
+            sizes, size, left = [], 1024, self.T
+            while left > 0:
+                n = min(size, left)
+                sizes.append(n)
+                left -= n
+                size = min(steady, 2 * size)
             out, c0 = [], 0
             for n in sizes:
                 out.append((c0, n))
@@ -517,7 +533,7 @@ class ConfigTC:
         comp = torch.cuda.current_stream()
         cps = self._copy_stream
         outs = []
-        chunks = self.e2e_chunks()
+        chunks = self.e2e_chunks(d2h_bound=(self.cfg == 4 and not force))
 
         def issue(ch):
             c0, n = ch

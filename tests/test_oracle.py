@@ -306,3 +306,35 @@ def test_batch_oracle_matches_per_pair():
     np.testing.assert_allclose(bat["dz"], per["dz"], atol=1e-10 * np.abs(per["dz"]).max())
     m = O.batch_msd_matrix(wl.frames, wl.landmarks)
     np.testing.assert_allclose(m, per["D"], rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("seed,eps_mult", [(3, 1.0), (5, 4.0)])
+def test_close_lifetime_window_contains_every_needed_landmark(seed, eps_mult):
+    """The certificate behind the pruned close-structure replay (engine.PathCV
+    ._close_replay_pruned, csrc/refine.cu cand_kernel): for a refresh frame y with lifetime
+    bound delta = max D(x, y) over the frames x that keep y, every landmark any such x needs
+    (lam (D~_l(x) - min D~(x)) <= thr, Eq. 5 distances) satisfies
+    d(y, a_l) <= sqrt(delta) + sqrt((sqrt(delta) + d_min(y))^2 + thr / lam)  (RMSD triangle
+    inequality).  Checked with the oracle's exact and Eq. 5 distances on a config-3-like
+    walker (accumulated noise), every frame, every landmark."""
+    wl = synth.config3(seed=seed, W=1, N=40, L=60, steps=120)
+    frames = wl.frames[0].astype(np.float64)
+    lm = wl.landmarks.astype(np.float64)
+    eps = wl.eps * eps_mult
+    out = O.close_structure_replay(frames, lm, wl.lam, eps, grad=False)
+    ref, D, dxy = out["refresh"], out["D"], out["dxy"]
+    assert ref[0] and 0 < ref.sum() < len(ref)
+    ridx = np.maximum.accumulate(np.where(ref, np.arange(len(ref)), 0))
+    thr = 27.0
+    checked = 0
+    for y in np.nonzero(ref)[0]:
+        life = np.nonzero((ridx == y) & ~ref)[0]
+        delta = dxy[life].max() if life.size else 0.0
+        dy = np.sqrt(np.maximum(D[y], 0.0))  # refresh row: exact distances of y
+        bound = np.sqrt(delta) + np.sqrt((np.sqrt(delta) + dy.min()) ** 2 + thr / wl.lam)
+        inside = dy <= bound * (1 + 1e-12)
+        for x in np.concatenate([[y], life]):
+            need = wl.lam * (D[x] - D[x].min()) <= thr
+            assert np.all(inside[need]), (y, x)
+            checked += int(need.sum())
+    assert checked > 0
