@@ -816,6 +816,9 @@ def run_ours(args, rank, world, local_rank):
     name, (cnt, tms) = max(prof.items(), key=lambda kv: kv[1][1])
     avg_ms = tms / cnt
     step_ms = tms / nprof  # the kernel's time per step (all its launches)
+    gk_names = ("mc_pathcv_grad_i8", "mc_pathcv_grad_i8_wide")
+    if name in gk_names:  # the int8 contraction's work spans its narrow and wide kernels
+        step_ms = sum(prof[k][1] for k in gk_names if k in prof) / nprof
     kind, amount = runner.kernel_work(name)
     tf32_cublas = tf32_peak_measure(device) if kind == "tensor_flop" and rank == 0 else None
     if kind == "bytes":
@@ -859,19 +862,22 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "fp64", "achieved": ach, "peak": 37.0, "unit": "TFLOP/s", "frac": ach / 37.0,
                 "peak_src": "nominal B200 FP64 37 TF/s (not measured)"}
     traffic = measured_traffic(name, cfg, runner.T)
-    roof.update({"kernel": name, "share_of_step": tms / total, "avg_launch_ms": avg_ms, "traffic": traffic,
+    roof.update({"kernel": "+".join(k for k in gk_names if k in prof) if name in gk_names else name,
+                 "share_of_step": step_ms * nprof / total, "avg_launch_ms": avg_ms, "traffic": traffic,
                  "traffic_unit": "bytes per launch (dram read + write)",
                  "traffic_src": "profiles/traffic.json (ncu --set full, same workload)" if traffic else None})
     kernels = {k: {"launches": c, "ms_per_step": t / nprof, "share": t / total}
                for k, (c, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     # the gradient contraction's own roofline (int8 tensor pipe) when it is not the top kernel
     roof_grad = None
-    if name != "mc_pathcv_grad_i8" and "mc_pathcv_grad_i8" in prof:
+    if name not in gk_names and any(k in prof for k in gk_names):
         gk, gamount = runner.kernel_work("mc_pathcv_grad_i8")
-        gc, gt = prof["mc_pathcv_grad_i8"]
+        gc = sum(prof[k][0] for k in gk_names if k in prof)
+        gt = sum(prof[k][1] for k in gk_names if k in prof)
         if gk == "int8_tensor_op":
             roof_grad = _int8_roof(gamount, gt / nprof, pk)
-            roof_grad.update({"kernel": "mc_pathcv_grad_i8", "share_of_step": gt / total, "avg_launch_ms": gt / gc})
+            roof_grad.update({"kernel": "+".join(k for k in gk_names if k in prof), "share_of_step": gt / total,
+                              "avg_launch_ms": gt / gc})
     roof_refine = None
     if name != "mc_refine_i8" and "mc_refine_i8" in prof and hasattr(runner, "pcv"):
         rk, ramount = runner.kernel_work("mc_refine_i8")
