@@ -132,6 +132,23 @@ def _flag_bits_dev(flags):
     return ((flags.flatten().to(torch.int32)[:, None] & bits) != 0).any(0)
 
 
+# 128-frame bands of the pruned screen sorted by (hull start, hull width): frames that
+# start on the same landmark tile are bucketed by how many tiles their hull spans, so a
+# band's union is close to its frames' own hulls instead of the widest hull that happens
+# to start there (env MC_BAND_WIDTH_SORT=0: by hull start only)
+BAND_WIDTH_SORT = os.environ.get("MC_BAND_WIDTH_SORT", "1") == "1"
+_WB = 16  # width buckets
+
+
+def _band_key(key, hlo, hhi, ntl):
+    """(sort key, bins) of the pruned screen's frame order: prune_plan's key (0 = wide
+    hull, 1 + hull start, ntl + 1 = empty) refined by the hull width."""
+    if not BAND_WIDTH_SORT:
+        return key, ntl + 2
+    width = (hhi - hlo).clamp(0, _WB - 1)
+    return (key * _WB + width).to(torch.int32).contiguous(), (ntl + 2) * _WB
+
+
 def _bits_value(row):
     return sum(b for b, on in zip(_FLAG_BITS, row) if on)
 
@@ -734,7 +751,7 @@ class PathCVTC:
                                      (self.cutoff + 2.0) / self.lam, self.knear, maxd=self.maxd, cstride=self.cstride,
                                      frnorm=fs0.rnorm, crnorm=self.ls_coarse.rnorm)
         ntl = self.mind.shape[1]
-        perm0 = K.sort_by_key(key, ntl + 1)
+        perm0 = K.sort_by_key(*_band_key(key, hlo, hhi, ntl))
         # sorted view of the split (operand rows + scalars gathered, no second split); the
         # raw frames stay in place and are read through perm0 (refine fmap / grad out_map)
         fss = K.gather_split(fs0, perm0)
@@ -1257,7 +1274,7 @@ class PathCVTC:
             # (empty hulls [ntl, 0) get their own last bin): ~T/G x (shards per hull) rows
             # instead of all T
             act = hhi > 0
-            perm0 = K.sort_by_key(torch.where(act, key, torch.full_like(key, ntl + 1)).contiguous(), ntl + 2)
+            perm0 = K.sort_by_key(*_band_key(torch.where(act, key, torch.full_like(key, ntl + 1)), hlo, hhi, ntl))
             nact = int(act.sum().item())
             perm0 = perm0[:nact].contiguous()
             fs = K.gather_split(fs_all, perm0)
