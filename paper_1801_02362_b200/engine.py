@@ -500,7 +500,7 @@ class PathCVTC:
     """
 
     def __init__(self, landmarks, lam, q=None, w=None, w_align=None, cutoff=25.0, window_cap=512, device=None,
-                 operand_fmt=None, screen=None, prune=None, coarse_stride=32, knear=4, shard=None, route=False,
+                 operand_fmt=None, screen=None, prune=None, coarse_stride=None, knear=4, shard=None, route=False,
                  two_phase=False):
         """shard = (rank, world[, bounds]): landmark-sharded evaluation.
         ``landmarks`` (and q) are the FULL set; this engine keeps the contiguous landmarks
@@ -637,7 +637,8 @@ class PathCVTC:
         self.prune = ((PRUNE if prune is None else bool(prune)) and self.screen == "f16x1" and ntl >= 16
                       and bool(torch.equal(self.w, self.wa)))
         if self.prune:
-            self._init_prune(int(coarse_stride), int(knear))
+            cs = coarse_stride if coarse_stride is not None else int(os.environ.get("MC_COARSE_STRIDE", "32"))
+            self._init_prune(int(cs), int(knear))
 
     def _exact_windows(self, Dest, fr, fs, cap, rlo=None, rhi=None, perm0=None, dref=None):
         """Screen estimate -> per-frame windows (mc_candidates, against dref when sharded)
