@@ -638,7 +638,8 @@ class PathCVTC:
                       and bool(torch.equal(self.w, self.wa)))
         if self.prune:
             cs = coarse_stride if coarse_stride is not None else int(os.environ.get("MC_COARSE_STRIDE", "32"))
-            self._init_prune(int(cs), int(knear))
+            kn = int(os.environ.get("MC_KNEAR", knear))
+            self._init_prune(int(cs), kn)
 
     def _exact_windows(self, Dest, fr, fs, cap, rlo=None, rhi=None, perm0=None, dref=None):
         """Screen estimate -> per-frame windows (mc_candidates, against dref when sharded)
