@@ -314,7 +314,7 @@ class ConfigTC:
         self.shard = shard
         if shard.startswith("landmarks") and cfg != 4:
             raise SystemExit("--shard landmarks applies to config 4 (path-CV)")
-        if shard in ("landmarks", "landmarks-routed"):
+        if shard in ("landmarks", "landmarks-allgather", "landmarks-routed"):
             # the north_star's variant.  "landmarks": the survey's
             # two-phase plan -- rank g screens its landmark shard for every frame (one
             # all-gather of the frames' screening operand, O(T) minima / windows), then refits
@@ -343,7 +343,10 @@ class ConfigTC:
         self.n, self.L = shp["N"], shp["L"]
         self._off, self._c0 = off, 0
         lms = torch.from_numpy(self.wl.landmarks).to(device)
-        if shard == "landmarks":
+        if shard == "landmarks":  # two-phase, phase 1 routed (each frame's operand to the shards it needs)
+            self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q, shard=(rank, world, Dd.tile_bounds(self.L, world)),
+                                       route=True, two_phase=True)
+        elif shard == "landmarks-allgather":  # two-phase, every frame's operand all-gathered
             self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q, shard=(rank, world), two_phase=True)
         elif shard == "landmarks-routed":
             self.pcv = engine.PathCVTC(lms, self.wl.lam, self.wl.q, shard=(rank, world, Dd.tile_bounds(self.L, world)),
@@ -365,6 +368,13 @@ class ConfigTC:
             self.frames_host = self.frames_dev.cpu()
             self.host_kind = "pageable (pinning failed)"
         if shard == "landmarks":
+            self.parallelism = (f"landmark-sharded x{world}, two-phase routed (NCCL: each frame's one-term screening "
+                                "operand to the shards its coarse hull meets, all-reduce MIN of the per-frame "
+                                "estimate minimum, windows back home; refits and gradients frame-sharded against "
+                                "replicated landmarks)")
+            self.scaling = "strong"
+            self.replicated_units = False
+        elif shard == "landmarks-allgather":
             self.parallelism = (f"landmark-sharded x{world}, two-phase (NCCL: one all-gather of the frames' one-term "
                                 "screening operand, all-reduce MIN of per-frame bounds, all-gather of per-shard "
                                 "windows; refits and gradients frame-sharded against replicated landmarks)")
@@ -412,7 +422,7 @@ class ConfigTC:
         elif self.shard.startswith("landmarks"):
             from paper_1801_02362_b200 import dist as Dd
 
-            if self.shard == "landmarks":
+            if self.shard in ("landmarks", "landmarks-allgather"):
                 # home offsets / totals of chunked calls follow from the gathered counts
                 steps = self.pcv.two_phase_steps(frames, None, None, grad=True)
             elif self.shard == "landmarks-routed":
@@ -1057,10 +1067,11 @@ def main():
     ap.add_argument("--frames", type=int, default=0, help="override T (configs 2/4) for quick runs")
     ap.add_argument("--walkers", type=int, default=0, help="override W (config 3) for quick runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline leg")
-    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks", "landmarks-routed",
-                                                          "landmarks-replicated"],
+    ap.add_argument("--shard", default="frames", choices=["frames", "landmarks", "landmarks-allgather",
+                                                          "landmarks-routed", "landmarks-replicated"],
                     help="multi-GPU split of config 4: frames (strong, no collective) or landmarks (strong, NCCL; "
-                         "two-phase (default), frame-routed, or with every frame replicated on every rank)")
+                         "two-phase with a routed screen (default), two-phase with the screening operand "
+                         "all-gathered, frame-routed, or with every frame replicated on every rank)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

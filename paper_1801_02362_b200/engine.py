@@ -544,14 +544,14 @@ class PathCVTC:
         self.shard = None
         self._gprune = None
         self._full = None
-        if shard is not None and two_phase:
-            if route:
-                raise ConfigError("two_phase and route are alternative landmark-sharded schemes")
+        if shard is not None and two_phase and not route:
             self._full = PathCVTC(lm, lam, q, w, w_align, cutoff, window_cap, device, operand_fmt, screen, False,
                                   coarse_stride, knear)
         if shard is not None and route:
             g = PathCVTC(lm, lam, q, w, w_align, cutoff, window_cap, device, operand_fmt, screen, True,
                          coarse_stride, knear)
+            if two_phase:  # routed two-phase: the full engine also serves the phase-2 refits
+                self._full = g
             if not g.prune:
                 raise ConfigError("frame routing needs the metric-pruned screen (>= 16 tiles, equal weights)")
             self._gprune = {"ls_coarse": g.ls_coarse, "mind": g.mind, "maxd": g.maxd, "cstride": g.cstride,
@@ -1231,6 +1231,8 @@ class PathCVTC:
 
     def two_phase_steps(self, frames, home_offset, t_total, grad=True, out_dtype=torch.float32):
         """Generator of the survey's two-phase plan.
+        With PathCVTC(..., shard=(rank, world, dist.tile_bounds(L, world)), route=True,
+        two_phase=True) phase 1 is routed instead of all-gathered (_two_phase_routed_screen).
 
         Phase 1 -- landmark-sharded screen: ("allgather_split") the one-term split of every
         rank's home frames (one all-gather: each rank then holds the screening operand of
@@ -1247,11 +1249,140 @@ class PathCVTC:
         operand once."""
         if self._full is None or self.shard is None:
             raise ConfigError("two_phase_steps needs PathCVTC(..., shard=(rank, world[, bounds]), two_phase=True)")
+        frh, fsh = self._frames(frames, 1, check=False)
+        Th = frh.shape[0]
+        if self._gprune is not None:
+            # ---- phase 1, routed: every home frame's screening operand goes only to the shards
+            # its admissible coarse hull meets (no all-gather of every frame's operand)
+            lo_h, cnt_h, cflags = yield from self._two_phase_routed_screen(frh, fsh, home_offset, t_total)
+        else:
+            lo_h, cnt_h, cflags = yield from self._two_phase_allgather_screen(frh, fsh, home_offset, t_total)
+        out = yield from self._two_phase_home(frh, fsh, lo_h, cnt_h, cflags, grad, out_dtype)
+        return out
+
+    def _two_phase_routed_screen(self, frh, fsh, home_offset, t_total):
+        """Routed phase 1 of two_phase_steps: ("gather") the home frame counts; the coarse
+        screen of the home frames against the GLOBAL coarse landmarks gives each frame's
+        admissible tile hull; ("alltoallv") the one-term operand rows + 4 scalars of each
+        frame to the shards its hull meets; each shard screens what it received (banded,
+        metric-pruned), ("min") the global estimate minimum per frame, windows against it;
+        ("alltoallv") each received frame's window (2 int32) back to its home rank, which
+        takes the hull over the shards.  NCCL bytes per step: ~60 KB (halves) + 40 B per routed
+        copy of a frame (a frame goes to the 1-2 shards its hull meets), 4 B per frame (min),
+        8 B per copy (windows) -- instead of every frame's operand on every rank."""
+        from .kernels import Split
         rank, world, off, cnt_l = self.shard
-        full = self._full
+        gp, dev = self._gprune, self.device
+        one = self.screen == "f16x1"
+        Th = frh.shape[0]
+        counts = yield ("gather", torch.tensor([Th], dtype=torch.int64, device=dev))
+        counts = [int(c) for c in counts.flatten().cpu().tolist()]
+        T = sum(counts)
+        if t_total is not None and T != int(t_total):
+            raise ConfigError(f"gathered {T} frames, expected {t_total}")
+        if home_offset is None:
+            home_offset = int(sum(counts[:rank]))
+        Dc = K.msd_estimate(fsh, gp["ls_coarse"], grid=K2_GRID)
+        hlo_g, hhi_g, _ = K.prune_plan(Dc, fsh.opnorm, gp["ls_coarse"].opnorm, self.kacc, gp["mind"],
+                                       (self.cutoff + 2.0) / self.lam, gp["knear"], maxd=gp["maxd"],
+                                       cstride=gp["cstride"], frnorm=fsh.rnorm, crnorm=gp["ls_coarse"].rnorm)
+        del Dc
+        tb = torch.tensor(self._tile_bounds, dtype=torch.int32, device=dev)
+        dest = (hlo_g[:, None] < tb[None, 1:]) & (hhi_g[:, None] > tb[None, :-1])  # [Th, G]
+        sends = [torch.nonzero(dest[:, r]).flatten() for r in range(world)]
+        gids = torch.arange(home_offset, home_offset + Th, dtype=torch.int64, device=dev)
+        hull = torch.stack([hlo_g, hhi_g], 1)
+        if world == 1:  # nothing to route: the home split is the received split (no copies)
+            got = None
+            sends = [torch.arange(Th, device=dev)]
+            src_counts, gid, R = [Th], gids, Th
+        else:
+            # per destination: the 3 operand planes of its frames (library row gathers, contiguous
+            # [k, kpad] blocks), 4 scalars and the global hull
+            scal = torch.stack([fsh.scale, fsh.opnorm, fsh.rnorm, fsh.g], 1)
+            planes = [[K.gather_rows(fsh.hi[pl].view(torch.int32), i.to(torch.int32)).view(fsh.hi.dtype)
+                       for i in sends] for pl in range(3)]
+            got = yield ("alltoallv", [[gids[i] for i in sends], *planes, [scal[i] for i in sends],
+                                       [hull[i] for i in sends]])
+            del planes
+            src_counts = [int(x.shape[0]) for x in got[0]]
+            gid = torch.cat(got[0])
+            R = int(gid.numel())
+        t0, t1 = self._tile_bounds[rank], self._tile_bounds[rank + 1]
+        ntl = t1 - t0
+        big = torch.full((T,), float("inf"), dtype=torch.float32, device=dev)
+        lo_r = cnt_r = None
+        cflags = torch.zeros((0,), dtype=torch.uint8, device=dev)
+        if R:
+            if got is None:
+                fs0, hr = fsh, hull
+            else:
+                sc = torch.cat(got[4])
+                hr = torch.cat(got[5])
+                hi_r = torch.empty((3, R, fsh.kpad), dtype=fsh.hi.dtype, device=dev)
+                for pl in range(3):  # one copy per plane into the received split
+                    torch.cat(got[1 + pl], out=hi_r[pl])
+                fs0 = Split(hi_r, None, None, sc[:, 3].contiguous(), None, None,
+                            torch.zeros(R, dtype=torch.uint8, device=dev), fsh.n, fsh.kpad, sc[:, 0].contiguous(),
+                            fsh.fmt, fsh.terms, sc[:, 1].contiguous(), sc[:, 2].contiguous())
+            del got
+            lo = (hr[:, 0].clamp(min=t0) - t0).to(torch.int32)
+            hi = (hr[:, 1].clamp(max=t1) - t0).to(torch.int32)
+            wide = max(1, (3 * ntl) // 4)
+            key = torch.where(hi - lo >= wide, torch.zeros_like(lo), 1 + lo).to(torch.int32)
+            perm0 = K.sort_by_key(*_band_key(key, lo, hi, ntl))
+            p = perm0.long()
+            fs = K.gather_split(fs0, perm0)
+            tlist, nlist, rlo, rhi = K.band_tiles(perm0, lo.contiguous(), hi.contiguous(), 128, 48, self.L, ntl)
+            Dest = torch.empty((R, self.L), dtype=torch.float32, device=dev)
+            K.msd_estimate(fs, self.ls, Dest, grid=K2_GRID, tlist=tlist, nlist=nlist)
+            fnorm = self.frame_bound(fs) if one else None
+            fcoef = 2.0 * self.lam if one else 0.0
+            _, _, dmin, _ = K.candidates(Dest, self.lam, self.cutoff + self.margin, 1, fnorm=fnorm, fcoef=fcoef,
+                                         rlo=rlo, rhi=rhi)
+            big[gid[p]] = dmin  # (a frame arrives at most once per shard)
+        else:
+            del got
+        dglob = yield ("min", big)
+        if R:
+            dref = dglob[gid[p]].contiguous()
+            lo_s, cnt_s, _, cflags = K.candidates(Dest, self.lam, self.cutoff + self.margin, self.L, fnorm=fnorm,
+                                                  fcoef=fcoef, rlo=rlo, rhi=rhi, dref=dref)
+            del Dest
+            lo_r = torch.empty_like(lo_s)
+            cnt_r = torch.empty_like(cnt_s)
+            lo_r[p], cnt_r[p] = lo_s + off, cnt_s  # received order, global landmark index
+            win = torch.stack([lo_r, cnt_r], 1)
+        else:
+            win = torch.zeros((0, 2), dtype=torch.int32, device=dev)
+        blocks, o = [], 0
+        for c in src_counts:  # each source rank's frames, in the order it sent them
+            blocks.append(win[o:o + c])
+            o += c
+        if world == 1:
+            back = [blocks]
+        else:
+            back = yield ("alltoallv", [blocks])
+        big_i = torch.iinfo(torch.int64).max
+        lo_t = torch.full((Th,), big_i, dtype=torch.int64, device=dev)
+        hi_t = torch.full((Th,), -1, dtype=torch.int64, device=dev)
+        for r in range(world):  # shard r's windows of the home frames sends[r]
+            w_r = back[0][r].long()
+            if w_r.numel() == 0:
+                continue
+            act = w_r[:, 1] > 0
+            idx = sends[r][act]
+            lo_t.scatter_reduce_(0, idx, w_r[act, 0], reduce="amin")
+            hi_t.scatter_reduce_(0, idx, w_r[act, 0] + w_r[act, 1], reduce="amax")
+        lo_h = lo_t.clamp(max=self._full.L).to(torch.int32).contiguous()
+        cnt_h = (hi_t - lo_t).clamp(min=0).to(torch.int32).contiguous()
+        return lo_h, cnt_h, cflags
+
+    def _two_phase_allgather_screen(self, frh, fsh, home_offset, t_total):
+        """Phase 1 of two_phase_steps with every frame's screening operand all-gathered."""
+        rank, world, off, cnt_l = self.shard
         dev = self.device
         one = self.screen == "f16x1"
-        frh, fsh = self._frames(frames, 1, check=False)
         Th = frh.shape[0]
         # ---- phase 1: screen all frames against this landmark shard
         fs_all, counts = yield ("allgather_split", fsh)
@@ -1316,9 +1447,17 @@ class PathCVTC:
         lo_t = torch.where(act, glo, torch.full_like(glo, big)).amin(0)
         hi_t = torch.where(act, glo + gcnt, torch.full_like(glo, -1)).amax(0)
         sl = slice(home_offset, home_offset + Th)
-        lo_h = lo_t[sl].clamp(max=full.L).to(torch.int32).contiguous()
+        lo_h = lo_t[sl].clamp(max=self._full.L).to(torch.int32).contiguous()
         cnt_h = (hi_t[sl] - lo_t[sl]).clamp(min=0).to(torch.int32).contiguous()
-        # ---- phase 2: exact refits, weights and gradients of the home frames, all landmarks
+        return lo_h, cnt_h, cflags
+
+    def _two_phase_home(self, frh, fsh, lo_h, cnt_h, cflags, grad, out_dtype):
+        """Phase 2 of two_phase_steps: exact refits, weights and gradients of the home frames
+        over their merged windows, against the replicated full landmark set (no collective)."""
+        if False:
+            yield None  # a generator like its callers (phase 2 issues no collective)
+        full = self._full
+        Th = frh.shape[0]
         cap = int(max(1, min(full.L, int(cnt_h.max().item()) if Th else 1)))
         perm = K.sort_by_key((2 * lo_h + cnt_h).to(torch.int32), 2 * full.L + 1)
         Dex, Rex, rflags = full._refine_windows(frh, fsh, perm, lo_h, cnt_h, cap)

@@ -180,8 +180,11 @@ def test_frame_routed_landmark_shards_match_unsharded(G, cuda_device):
         assert sum(received) < 1.6 * 260, received
 
 
-def _two_phase(wl, G, bounds=None, **kw):
+def _two_phase(wl, G, bounds=None, routed=False, **kw):
     T = wl.frames.shape[0]
+    if routed:  # routed phase 1: shards at landmark-tile bounds, the global coarse screen at home
+        bounds = D.tile_bounds(wl.landmarks.shape[0], G)
+        kw = dict(kw, route=True)
     engs = [engine.PathCVTC(wl.landmarks, wl.lam, shard=(g, G, bounds), two_phase=True, **kw) for g in range(G)]
     gens = []
     for g, e in enumerate(engs):
@@ -190,15 +193,18 @@ def _two_phase(wl, G, bounds=None, **kw):
     return engs, D.drive_lockstep(gens)
 
 
-@pytest.mark.parametrize("G,L", [(1, 1536), (2, 1536), (3, 1536), (4, 768)])
-def test_two_phase_landmark_shards_match_unsharded(G, L, cuda_device):
-    """The two-phase plan (landmark-sharded screen of every frame, one all-gather of the
-    screening operand, O(T) minima and windows; frame-sharded exact refits, weights and
-    gradients against the replicated landmarks): the concatenated home outputs equal the
-    unsharded evaluate -- same windows, s and z to 1e-9, ds and dz to SHARD_REL."""
+@pytest.mark.parametrize("G,L,routed", [(1, 1536, False), (2, 1536, False), (3, 1536, False), (4, 768, False),
+                                        (1, 1536, True), (2, 1536, True), (3, 1536, True), (4, 768, True)])
+def test_two_phase_landmark_shards_match_unsharded(G, L, routed, cuda_device):
+    """The two-phase plan (landmark-sharded screen, O(T) minima and windows; frame-sharded
+    exact refits, weights and gradients against the replicated landmarks), with phase 1
+    all-gathered (every frame's screening operand on every rank) or routed (each frame's
+    operand only to the shards its coarse hull meets, windows back to the home rank): the
+    concatenated home outputs equal the unsharded evaluate -- same windows, s and z to
+    1e-9, ds and dz to SHARD_REL."""
     wl = synth.config4(T=260, L=L, N=240)
     ref = engine.PathCVTC(wl.landmarks, wl.lam).evaluate(wl.frames, out_dtype=torch.float64)
-    engs, outs = _two_phase(wl, G)
+    engs, outs = _two_phase(wl, G, routed=routed)
     assert all(e.L < L for e in engs) or G == 1
     s = torch.cat([o["s"] for o in outs]).cpu().numpy()
     z = torch.cat([o["z"] for o in outs]).cpu().numpy()
