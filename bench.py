@@ -440,7 +440,7 @@ class ConfigTC:
     def step_device(self):
         return self._step(self.frames_dev, self.D if self.cfg == 2 else None)
 
-    def e2e_chunks(self, d2h_bound=False):
+    def e2e_chunks(self, d2h_bound=False, taper=False):
         """Chunk boundaries of the streamed step.  The H2D copy (2.16 us/frame at
         55.6 GB/s) is slower than the compute (~2.5 ms + 1.72 us/frame per chunk on
         config 4), so the step is copy-bound and ends one chunk-compute after the
@@ -466,12 +466,22 @@ class ConfigTC:
             # bottleneck, so it must start early -- a small first chunk, doubling to a steady
             # size; the tail is short because every chunk's compute is far below its D2H
             steady = max(1024, min(self.T // 8, 16384) // 32 * 32)
-            sizes, size, left = [], 1024, self.T
-            while left > 0:
-                n = min(size, left)
+            ramp = []
+            size = 1024
+            while size < steady:
+                ramp.append(size)
+                size *= 2
+            # taper (the fused-force step, as many bytes back as in): the last chunks shrink
+            # again so the final compute + D2H after the last H2D is short
+            tail = list(reversed(ramp)) if taper and self.T > 2 * sum(ramp) + steady else []
+            sizes, left = [], self.T - sum(tail)
+            for n in ramp + [steady] * max(0, left):
+                if left <= 0:
+                    break
+                n = min(n, left)
                 sizes.append(n)
                 left -= n
-                size = min(steady, 2 * size)
+            sizes += tail
             out, c0 = [], 0
             for n in sizes:
                 out.append((c0, n))
@@ -543,7 +553,7 @@ class ConfigTC:
         comp = torch.cuda.current_stream()
         cps = self._copy_stream
         outs = []
-        chunks = self.e2e_chunks(d2h_bound=(self.cfg == 4 and not force))
+        chunks = self.e2e_chunks(d2h_bound=(self.cfg == 4), taper=force)
 
         def issue(ch):
             c0, n = ch

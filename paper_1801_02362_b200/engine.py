@@ -1289,7 +1289,11 @@ class PathCVTC:
         del Dc
         tb = torch.tensor(self._tile_bounds, dtype=torch.int32, device=dev)
         dest = (hlo_g[:, None] < tb[None, 1:]) & (hhi_g[:, None] > tb[None, :-1])  # [Th, G]
-        sends = [torch.nonzero(dest[:, r]).flatten() for r in range(world)]
+        # every (destination, frame) pair in destination-major order with one host read of the
+        # per-destination counts (instead of G nonzero round trips)
+        pairs = torch.nonzero(dest.T)
+        ncopy = dest.sum(0).cpu().tolist()
+        sends = list(torch.split(pairs[:, 1], ncopy))
         gids = torch.arange(home_offset, home_offset + Th, dtype=torch.int64, device=dev)
         hull = torch.stack([hlo_g, hhi_g], 1)
         if world == 1:  # nothing to route: the home split is the received split (no copies)
