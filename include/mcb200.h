@@ -455,14 +455,21 @@ int mc_mtd_force(const double* dV, int32_t T, int32_t d, const void* g0, const v
  *   traj [W, ceil(steps / traj_stride), n, 3] positions at the start of steps
  *   step0 + k traj_stride (traj_stride 0: none; step0 % traj_stride == 0), flags [W]
  *   (|= NoConverge / NonFinite / SigOverflow = hill capacity exceeded).  Continuing a run:
- *   call again with step0 += steps and the same state arrays. */
+ *   call again with step0 += steps and the same state arrays.  Neighbour list (SPEC
+ *   neighbourlist; nl_m = M > 0, modes 1 and 2): state act [W, L] (uint8
+ *   members) and nl_last [W] (last update step, -1 = none); updated on the first step and
+ *   whenever step - nl_last >= nl_stride from that step's distances to all N (exact, or the
+ *   Eq. 5 approximations in close mode) as the M smallest (ties by lower index); between
+ *   updates only the members are evaluated (M expensive / cheap) and s, z and the bias
+ *   force sum over them. */
 int mc_toysim_run(int32_t W, int32_t n, int32_t L, int32_t steps, int64_t step0, int32_t mode, int32_t tau_g,
                   int32_t max_hills, int32_t traj_stride, double bond_k, double bond_r0, double angle_k,
                   double theta0, double mob, double noise, double lam, double eps, double hill_h, double hill_sigma,
                   uint64_t seed, const double* refs, const double* refg, const double* refmom, const double* q,
                   const double* w, const double* wa, double* x, double* y, double* rays, int32_t* hasy,
                   double* hills, int32_t* nhills, int64_t* counters, double* cv, uint8_t* rlog, double* traj,
-                  uint8_t* flags, void* stream);
+                  uint8_t* flags, int32_t nl_m, int32_t nl_stride, uint8_t* act,
+                  int64_t* nl_last, void* stream);
 
 #ifdef __cplusplus
 }

@@ -101,14 +101,25 @@ def bonded_force(x, p):
 
 def run(p, refs, q, x0, steps, mode, walker=0, step0=0, state=None, traj_stride=0):
     """One walker.  p: dict of ToyParams fields (bond_k, bond_r0, angle_k, theta0, mob,
-    noise, lam, eps, hill_h, hill_sigma, tau_g, seed); refs [L, n, 3] centred; mode
-    0 free / 1 original / 2 close.  Returns (cv [steps, 4], refresh [steps], counters
-    [3], final x, traj, state) -- state carries y, saved rotations and hills."""
+    noise, lam, eps, hill_h, hill_sigma, tau_g, seed; optional nl_m, nl_stride: the SPEC
+    neighbour list); refs [L, n, 3] centred; mode 0 free / 1 original /
+    2 close.  Returns (cv [steps, 4], refresh [steps], counters [3], final x, traj, state)
+    -- state carries y, saved rotations, hills and the neighbour list.
+
+    Neighbour list (nl_m = M > 0, stride nl_stride): updated on the first step and then
+    whenever step - last_update >= stride (maybe_update) from that step's
+    distances to ALL references -- exact in the original mode (N expensive), the Eq. 5
+    approximations in the close mode (N cheap) or the exact refit of a reassignment step --
+    as the M smallest, ties by lower index; between updates only the M members are
+    evaluated (M expensive / M cheap) and s, z and their gradients sum over them
+    (SPEC.md:252)."""
     x = np.array(x0, dtype=np.float64)
     n = x.shape[0]
     L = 0 if refs is None else refs.shape[0]
     w = np.full(n, 1.0 / n)
-    st = state or {"y": None, "rays": None, "hills": [], "counters": np.zeros(3, dtype=np.int64)}
+    nl_m, nl_stride = int(p.get("nl_m", 0)), int(p.get("nl_stride", 1))
+    st = state or {"y": None, "rays": None, "hills": [], "counters": np.zeros(3, dtype=np.int64),
+                   "active": None, "nl_last": None}
     cv = np.zeros((steps, 4))
     rlog = np.zeros(steps, dtype=np.uint8)
     traj = []
@@ -129,18 +140,29 @@ def run(p, refs, q, x0, steps, mode, walker=0, step0=0, state=None, traj_stride=
                 dxy, refresh = 0.0, True
             dist = np.zeros(L)
             grads = np.zeros((L, n, 3))
+            update = nl_m > 0 and (st["nl_last"] is None or t - st["nl_last"] >= nl_stride)
+            # the references evaluated this step: all (no list, an update, or a close-mode
+            # reassignment, which refits every saved rotation) or the list members
+            every = nl_m == 0 or update or (mode == 2 and refresh)
+            todo = range(L) if every else st["active"]
             if refresh:
-                rots = np.zeros((L, 3, 3))
-                for i in range(L):
+                rots = np.zeros((L, 3, 3)) if mode == 2 else None
+                for i in todo:
                     dist[i], grads[i], fit = O.exact_distance(xc, refs[i], w, w, with_rot_term=False)
-                    rots[i] = fit["rot"]
+                    if mode == 2:
+                        rots[i] = fit["rot"]
                 if mode == 2:
                     st["y"], st["rays"] = xc.copy(), rots
             else:
-                for i in range(L):
+                for i in todo:
                     dist[i], grads[i] = O.approx_distance(xc, refs[i], st["rays"][i], fit_xy, w, w)
-            s, gs = O.property_map(dist, grads, q, p["lam"])
-            z, _ = O.path_z(dist, grads, p["lam"])
+            if update:
+                st["active"] = np.sort(np.argsort(dist, kind="stable")[:nl_m])
+                st["nl_last"] = t
+            act = np.arange(L) if nl_m == 0 else st["active"]
+            s, gsa = O.property_map(dist[act], grads[act], q[act], p["lam"])
+            z, _ = O.path_z(dist[act], grads[act], p["lam"])
+            gs = gsa
             V = 0.0
             for c in st["hills"]:
                 d = s - c
@@ -149,15 +171,17 @@ def run(p, refs, q, x0, steps, mode, walker=0, step0=0, state=None, traj_stride=
                 dvds -= e * d / p["hill_sigma"] ** 2
             cv[it] = (s, z, V, dxy)
             rlog[it] = 1 if (mode == 2 and refresh) else 0
+            # counters (SPEC msd-engine / neighbourlist: an update step evaluates all N)
+            nev = L if every else nl_m
             if mode == 1:
-                st["counters"][0] += L
+                st["counters"][0] += nev
             else:
                 st["counters"][0] += 1
                 if refresh:
                     st["counters"][0] += L
                     st["counters"][2] += 1
                 else:
-                    st["counters"][1] += L
+                    st["counters"][1] += nev
         F = bonded_force(x, p)
         if gs is not None:
             F = F - dvds * gs

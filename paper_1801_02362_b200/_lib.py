@@ -73,7 +73,7 @@ _SIGS = {
     "mc_msd_f16_2sm": [_P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I64, _I32, _P],
     "mc_pathcv_grad_block": [_I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P],
     "mc_toysim_run": [_I32, _I32, _I32, _I32, _I64, _I32, _I32, _I32, _I32] + [_D] * 10 + [ctypes.c_uint64]
-    + [_P] * 18,
+    + [_P] * 17 + [_I32, _I32, _P, _P, _P],
     "mc_shard_rescale": [_I32, _I32, _P, _P, _P, _P, _P, _P],
     "mc_candidates": [_P, _I32, _I32, _I64, _D, _D, _P, _D, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
     "mc_grad_i8_wide_plan": [_I32, _I32, _I32, _P, _P, _P, _P, _P],

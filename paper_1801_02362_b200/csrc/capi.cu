@@ -544,10 +544,12 @@ int mc_toysim_run(int32_t W, int32_t n, int32_t L, int32_t steps, int64_t step0,
                   uint64_t seed, const double* refs, const double* refg, const double* refmom, const double* q,
                   const double* w, const double* wa, double* x, double* y, double* rays, int32_t* hasy,
                   double* hills, int32_t* nhills, int64_t* counters, double* cv, uint8_t* rlog, double* traj,
-                  uint8_t* flags, void* stream) {
+                  uint8_t* flags, int32_t nl_m, int32_t nl_stride, uint8_t* act, int64_t* nl_last, void* stream) {
   if (W < 0 || n < 3 || n > 64 || steps < 0 || step0 < 0 || mode < 0 || mode > 2 || tau_g < 0 || max_hills < 0 ||
       traj_stride < 0 || !(mob > 0.0) || !(noise >= 0.0) || !(bond_r0 > 0.0))
     return MC_ERR_CONFIG;
+  if (nl_m < 0 || (nl_m > 0 && (mode == 0 || nl_m > L || nl_stride < 1 || (W > 0 && (!act || !nl_last)))))
+    return MC_ERR_CONFIG;  // neighbour list: 1 <= M <= N, stride >= 1
   if (mode != 0 && (L < 1 || L > 128 || !(lam > 0.0) || !(eps >= 0.0) || !(hill_sigma > 0.0) || !(hill_h >= 0.0)))
     return MC_ERR_CONFIG;
   if (traj_stride > 0 && step0 % traj_stride != 0) return MC_ERR_CONFIG;
@@ -558,9 +560,10 @@ int mc_toysim_run(int32_t W, int32_t n, int32_t L, int32_t steps, int64_t step0,
     if (mode == 2 && !rays) return MC_ERR_CONFIG;
   }
   mc::ToyParams P{n, L, steps, mode, tau_g, max_hills, traj_stride, (long long)step0, bond_k, bond_r0, angle_k,
-                  theta0, mob, noise, lam, eps, hill_h, hill_sigma, (unsigned long long)seed};
+                  theta0, mob, noise, lam, eps, hill_h, hill_sigma, (unsigned long long)seed, nl_m, nl_stride};
   return cuda_status(mc::launch_toysim(P, W, refs, refg, refmom, q, w, wa, x, y, rays, hasy, hills, nhills,
-                                       reinterpret_cast<long long*>(counters), cv, rlog, traj, flags, S_(stream)));
+                                       reinterpret_cast<long long*>(counters), cv, rlog, traj, flags, S_(stream), act,
+                                       reinterpret_cast<long long*>(nl_last)));
 }
 
 }  // extern "C"

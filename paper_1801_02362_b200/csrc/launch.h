@@ -160,9 +160,11 @@ struct ToyParams {  // csrc/toysim.cu
   long long step0;
   double bond_k, bond_r0, angle_k, theta0, mob, noise, lam, eps, hill_h, hill_sigma;
   unsigned long long seed;
+  int nl_m, nl_stride;  // neighbour list (SPEC neighbourlist): size M (0: none) and stride
 };
 cudaError_t launch_toysim(const ToyParams& P, int W, const double* refs, const double* refg, const double* refmom,
                           const double* q, const double* w, const double* wa, double* xs, double* ys, double* rays,
                           int* hasy, double* hills, int* nhills, long long* counters, double* cv, uint8_t* rlog,
-                          double* traj, uint8_t* flags, cudaStream_t stream);
+                          double* traj, uint8_t* flags, cudaStream_t stream, uint8_t* act = nullptr,
+                          long long* nl_last = nullptr);
 }  // namespace mc

@@ -120,7 +120,8 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
               const double* __restrict__ wa, double* __restrict__ xs, double* __restrict__ ys,
               double* __restrict__ rays, int* __restrict__ hasy, double* __restrict__ hills,
               int* __restrict__ nhills, long long* __restrict__ counters, double* __restrict__ cv,
-              uint8_t* __restrict__ rlog, double* __restrict__ traj, uint8_t* __restrict__ flags) {
+              uint8_t* __restrict__ rlog, double* __restrict__ traj, uint8_t* __restrict__ flags,
+              uint8_t* __restrict__ act, long long* __restrict__ nl_last) {
   const int wk = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = P.n, L = P.L;
   __shared__ double sx[TMAXN * 3], sxn[TMAXN * 3], sxc[TMAXN * 3], sy[TMAXN * 3], sg[2][TMAXN * 3];
@@ -130,6 +131,10 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
   __shared__ double s_gx, s_dxy, s_rxy[9], s_eig[4], s_V[16], s_v[2][4], s_sum[2], s_gsum[6];
   __shared__ double s_s, s_z, s_bias, s_dvds;
   __shared__ int s_refresh, s_hasy, s_nh;
+  // neighbour list (SPEC neighbourlist): the members (s_act), the last update step
+  __shared__ uint8_t s_act[TMAXL];
+  __shared__ long long s_nl_last;
+  const bool nl = P.nl_m > 0;
   __shared__ unsigned s_flags;
   for (int e = tid; e < 3 * n; e += TNT) {
     sx[e] = xs[(int64_t)wk * 3 * n + e];
@@ -138,7 +143,10 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
   for (int j = tid; j < n; j += TNT) { sw[j] = w[j]; swa[j] = wa[j]; }
   if (P.mode == 2)
     for (int e = tid; e < 9 * L; e += TNT) sRay[e] = rays[(int64_t)wk * 9 * L + e];
+  if (nl)
+    for (int i = tid; i < L; i += TNT) s_act[i] = act[(int64_t)wk * L + i];
   if (tid == 0) {
+    s_nl_last = nl ? nl_last[wk] : -1;
     s_hasy = hasy[wk];
     s_nh = nhills[wk];
     s_flags = 0u;
@@ -218,8 +226,17 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
       }
       __syncthreads();
       const bool exact = s_refresh != 0;
+      // neighbour list: update on the first step and whenever t - last >= stride
+      // (maybe_update); the references evaluated: all (no list, an update, or a close-mode
+      // reassignment refitting every saved rotation), else only the list members
+      const bool update = nl && (s_nl_last < 0 || t - s_nl_last >= P.nl_stride);
+      const bool every = !nl || update || (P.mode == 2 && exact);
       // C: one thread per reference: covariance, then the exact fit (Eq. 3) or Eq. 5
       for (int i = tid; i < L; i += TNT) {
+        if (!every && !s_act[i]) {
+          sD[i] = INFINITY;  // not evaluated this step (outside the list)
+          continue;
+        }
         const double* a = refs + (int64_t)i * n * 3;
         double S[9];
 #pragma unroll
@@ -264,13 +281,28 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
         }
       }
       __syncthreads();
-      // D: property map (Eq. 2 with the min-D shift) and z, coefficients (warp 0)
+      if (update) {
+        // the M smallest distances, ties by lower index (rank = #{j: D_j < D_i or
+        // D_j == D_i and j < i}); the members are a set (ascending-index order)
+        for (int i = tid; i < L; i += TNT) {
+          const double di = sD[i];
+          int rank = 0;
+          for (int j = 0; j < L; ++j) rank += (sD[j] < di || (sD[j] == di && j < i)) ? 1 : 0;
+          s_act[i] = rank < P.nl_m ? 1 : 0;
+        }
+        if (tid == 0) s_nl_last = t;
+        __syncthreads();
+      }
+      // D: property map (Eq. 2 with the min-D shift) and z, coefficients (warp 0), over the
+      // list members only when a neighbour list is on
       if (warp == 0) {
         double dmin = INFINITY;
-        for (int i = lane; i < L; i += 32) dmin = fmin(dmin, sD[i]);
+        for (int i = lane; i < L; i += 32)
+          if (!nl || s_act[i]) dmin = fmin(dmin, sD[i]);
         dmin = warp_min_d(dmin);
         double zs = 0.0, qs = 0.0;
         for (int i = lane; i < L; i += 32) {
+          if (nl && !s_act[i]) continue;
           const double e = exp(-P.lam * (sD[i] - dmin));
           zs += e;
           qs = fma(q[i], e, qs);
@@ -280,8 +312,9 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
         const double sval = qs / zs, zval = dmin - log(zs) / P.lam;
         double ss = 0.0, sz = 0.0;
         for (int i = lane; i < L; i += 32) {
-          const double p = exp(-P.lam * (sD[i] - dmin)) / zs;
-          scs[i] = -P.lam * p * (q[i] - sval);
+          const bool on = !nl || s_act[i];
+          const double p = on ? exp(-P.lam * (sD[i] - dmin)) / zs : 0.0;
+          scs[i] = on ? -P.lam * p * (q[i] - sval) : 0.0;
           scz[i] = p;
           ss += scs[i];
           sz += p;
@@ -302,6 +335,10 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
       // parallel (thread i -> sPart[i][36]), summed in index order by warp 0 below.
       if (!exact) {
         for (int i = tid; i < L; i += TNT) {
+          if (nl && !s_act[i]) {  // outside the list: no Eq. 6 term
+            for (int e = 0; e < 36; ++e) sPart[36 * i + e] = 0.0;
+            continue;
+          }
           const double* Si = sS + 9 * i;
           const double* Ri = sRay + 9 * i;
           const double* m = refmom + 6 * (int64_t)i;
@@ -396,6 +433,7 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
       for (int k = tid; k < n; k += TNT) {
         double us[3] = {0.0, 0.0, 0.0}, uz[3] = {0.0, 0.0, 0.0};
         for (int i = 0; i < L; ++i) {
+          if (nl && !s_act[i]) continue;
           const double* a = refs + ((int64_t)i * n + k) * 3;
           const double* Rh = sRh + 9 * i;
 #pragma unroll
@@ -457,12 +495,14 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
         cv[4 * o + 3] = s_dxy;
         rlog[o] = (P.mode == 2 && exact) ? 1 : 0;
         // counters (SPEC msd-engine): original = L exact per step; close = 1 (x<->y) + L on
-        // reassignment, else L cheap
+        // reassignment, else L cheap; with a neighbour list M instead of L except on update
+        // steps (SPEC neighbourlist: an update evaluates all N)
+        const long long nev = every ? L : P.nl_m;
         if (P.mode == 1) {
-          c_exp += L;
+          c_exp += nev;
         } else {
           c_exp += 1;
-          if (exact) { c_exp += L; c_reas += 1; } else { c_cheap += L; }
+          if (exact) { c_exp += L; c_reas += 1; } else { c_cheap += nev; }
         }
       }
       __syncthreads();
@@ -497,7 +537,10 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
   }
   if (P.mode == 2)
     for (int e = tid; e < 9 * L; e += TNT) rays[(int64_t)wk * 9 * L + e] = sRay[e];
+  if (nl)
+    for (int i = tid; i < L; i += TNT) act[(int64_t)wk * L + i] = s_act[i];
   if (tid == 0) {
+    if (nl) nl_last[wk] = s_nl_last;
     hasy[wk] = s_hasy;
     nhills[wk] = s_nh;
     counters[3 * wk] += c_exp;
@@ -510,8 +553,10 @@ toysim_kernel(ToyParams P, const double* __restrict__ refs, const double* __rest
 cudaError_t launch_toysim(const ToyParams& P, int W, const double* refs, const double* refg, const double* refmom,
                           const double* q, const double* w, const double* wa, double* xs, double* ys, double* rays,
                           int* hasy, double* hills, int* nhills, long long* counters, double* cv, uint8_t* rlog,
-                          double* traj, uint8_t* flags, cudaStream_t stream) {
+                          double* traj, uint8_t* flags, cudaStream_t stream, uint8_t* act, long long* nl_last) {
   if (W <= 0 || P.steps <= 0) return cudaSuccess;
+  if (P.nl_m > 0 && (!act || !nl_last || P.nl_m > P.L || P.nl_stride < 1 || P.mode == 0))
+    return cudaErrorInvalidValue;
   const size_t dsm = sizeof(double) * 36 * (P.L + 1);  // <= 37 KB (L <= 128)
   static bool attr = false;
   if (!attr) {
@@ -519,7 +564,7 @@ cudaError_t launch_toysim(const ToyParams& P, int W, const double* refs, const d
     attr = true;
   }
   toysim_kernel<<<W, TNT, dsm, stream>>>(P, refs, refg, refmom, q, w, wa, xs, ys, rays, hasy, hills, nhills, counters,
-                                       cv, rlog, traj, flags);
+                                       cv, rlog, traj, flags, act, nl_last);
   return cudaGetLastError();
 }
 

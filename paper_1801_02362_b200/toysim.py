@@ -15,9 +15,12 @@ Mirror of the spec's types and operation:
 * ``make_references`` — the seeded unbiased pre-run snapshotted at fixed
   intervals, then centred, q_i = i.
 
-The neighbour list of the toy run is not modelled (``nl_config`` must be None or
-disabled: M = N, L = 1); the batched neighbour-list machinery lives in
-``engine.PathCV.close_replay``.
+Neighbour list (``nl_config``: a ``neighbourlist.NeighbourList`` or an object with
+``size`` M, ``stride`` L and ``enabled``): each walker keeps its own
+list on the device, updated on the first step and whenever step − last_update ≥ L from
+that step's distances to all N references (exact in the original mode, the Eq. 5
+approximations in the close mode), the M smallest with ties by the lower index; between
+updates only the M members are evaluated and s, z and the bias force sum over them.
 """
 
 from __future__ import annotations
@@ -105,7 +108,7 @@ class ToySim:
     """W walkers of one ToySystem against one reference set, state on the device."""
 
     def __init__(self, system: ToySystem, refs, mode="close", lam=100.0, eps=0.01, mtd: MtdConfig | None = None,
-                 walkers=1, x0=None, q=None, max_hills=1024, device=None):
+                 walkers=1, x0=None, q=None, max_hills=1024, device=None, nl_config=None):
         K.require_cuda()
         if mode not in MODES:
             raise ConfigError(f"mode {mode!r}")
@@ -151,6 +154,19 @@ class ToySim:
         self.counters = torch.zeros((self.W, 3), dtype=torch.int64, device=self.dev)
         self.flags = torch.zeros((self.W,), dtype=torch.uint8, device=self.dev)
         self.step = 0
+        # neighbour list (SPEC neighbourlist): M, stride; per-walker members + last update
+        self.nl_m, self.nl_stride = 0, 1
+        if nl_config is not None and getattr(nl_config, "enabled", True):
+            if mode == "free":
+                raise ConfigError("a neighbour list needs the path CV (mode original or close)")
+            m, st = int(nl_config.size), int(getattr(nl_config, "stride", 1))
+            if not 1 <= m <= self.L:
+                raise ConfigError("neighbour list size must satisfy 1 <= M <= N")
+            if st < 1:
+                raise ConfigError("neighbour list stride must be >= 1")
+            self.nl_m, self.nl_stride = m, st
+        self.act = torch.zeros((self.W, self.L), dtype=torch.uint8, device=self.dev)
+        self.nl_last = torch.full((self.W,), -1, dtype=torch.int64, device=self.dev)
 
     def run(self, n_steps, traj_stride=0):
         """Advance every walker n_steps (one launch).  Returns a dict of device tensors:
@@ -170,7 +186,8 @@ class ToySim:
              float(s.mobility), float(s.noise), self.lam, self.eps, float(self.mtd.height), float(self.mtd.sigma),
              int(s.rng_seed) & 0xFFFFFFFFFFFFFFFF, ptr(self.refs), ptr(self.refg), ptr(self.refmom), ptr(self.q),
              ptr(self.w), ptr(self.w), ptr(self.x), ptr(self.y), ptr(self.rays), ptr(self.hasy), ptr(self.hills),
-             ptr(self.nhills), ptr(self.counters), ptr(cv), ptr(rlog), ptr(traj), ptr(self.flags), stream_ptr())
+             ptr(self.nhills), ptr(self.counters), ptr(cv), ptr(rlog), ptr(traj), ptr(self.flags), self.nl_m,
+             self.nl_stride, ptr(self.act), ptr(self.nl_last), stream_ptr())
         self.step += n_steps
         return {"cv": cv[:, :n_steps], "refresh": rlog[:, :n_steps], "traj": traj}
 
@@ -203,12 +220,10 @@ def make_references(system: ToySystem, n_refs=16, stride=200, warmup=0, walker=0
 def run(system: ToySystem, ref, mode="close", nl_config=None, mtd_config: MtdConfig | None = None, n_steps=5000,
         lam=100.0, eps=0.01):
     """SPEC toysim.run: one walker, returns a RunReport."""
-    if nl_config is not None and getattr(nl_config, "enabled", True):
-        raise ConfigError("the toy run models no neighbour list (M = N, L = 1); see engine.PathCV.close_replay")
     refs = ref.coords if hasattr(ref, "coords") else ref
     mtd = mtd_config or MtdConfig()
     cap = mtd.max_hills or (n_steps // max(1, mtd.tau_g) + 1)
-    sim = ToySim(system, refs, mode=mode, lam=lam, eps=eps, mtd=mtd, walkers=1, max_hills=cap)
+    sim = ToySim(system, refs, mode=mode, lam=lam, eps=eps, mtd=mtd, walkers=1, max_hills=cap, nl_config=nl_config)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     out = sim.run(n_steps)

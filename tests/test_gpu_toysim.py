@@ -126,3 +126,50 @@ def test_bad_configuration_raises(refs, cuda_device):
         ToySim(ToySystem(n_beads=9), refs)
     with pytest.raises(ConfigError):
         ToySystem(dt=0.0)
+
+
+@pytest.mark.parametrize("mode,eps,M,stride", [("original", 0.01, 2, 7), ("close", 4e-4, 3, 5), ("close", 0.01, 1, 9)])
+def test_device_neighbour_list_run_matches_oracle(mode, eps, M, stride, refs, cuda_device):
+    """The toy loop with a SPEC neighbour list (M members, refreshed every `stride` steps
+    from the distances to all references; s, z and the bias force over the members): per-step
+    CV, reassignment log, counters, final coordinates and the final members equal the numpy
+    restatement; a run in two chunks equals one run."""
+    from paper_1801_02362_b200.neighbourlist import NeighbourList
+
+    sysm = ToySystem(rng_seed=5)
+    nl = NeighbourList(6, M, stride=stride, device=cuda_device)
+    sim = ToySim(sysm, refs, mode=mode, eps=eps, mtd=MtdConfig(tau_g=10, sigma=0.3, height=2.0), walkers=2,
+                 nl_config=nl)
+    steps = 120
+    out = sim.run(steps)
+    sim.check()
+    p = dict(_params(sysm, sim), nl_m=M, nl_stride=stride)
+    for wk in range(2):
+        cv, rlog, counters, x, _, st = OT.run(p, refs - refs.mean(axis=1, keepdims=True), np.arange(6.0),
+                                              sysm.initial_chain(), steps, mode=2 if mode == "close" else 1,
+                                              walker=wk)
+        got = out["cv"][wk].cpu().numpy()
+        np.testing.assert_allclose(got[:, 0], cv[:, 0], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(got[:, 1], cv[:, 1], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(got[:, 2], cv[:, 2], rtol=1e-9, atol=1e-12)
+        assert np.array_equal(out["refresh"][wk].cpu().numpy(), rlog)
+        assert sim.counters[wk].cpu().tolist() == counters.tolist()
+        np.testing.assert_allclose(sim.x[wk].cpu().numpy(), x, atol=1e-10)
+        assert np.nonzero(sim.act[wk].cpu().numpy())[0].tolist() == st["active"].tolist()
+    # chunked: 50 + 70 steps = 120 steps
+    sim2 = ToySim(sysm, refs, mode=mode, eps=eps, mtd=MtdConfig(tau_g=10, sigma=0.3, height=2.0), walkers=2,
+                  nl_config=nl)
+    a = sim2.run(50)["cv"].cpu().numpy()
+    b = sim2.run(70)["cv"].cpu().numpy()
+    np.testing.assert_array_equal(np.concatenate([a, b], axis=1), out["cv"].cpu().numpy())
+    assert torch.equal(sim2.counters, sim.counters)
+
+
+def test_run_with_neighbour_list_counts_per_spec(refs, cuda_device):
+    """SPEC toysim.run(..., nl_config, ...) in the original mode: expensive computations per
+    step = M + (N - M) updates / steps exactly."""
+    from paper_1801_02362_b200.neighbourlist import NeighbourList
+
+    rep = run(ToySystem(rng_seed=2), refs, mode="original", nl_config=NeighbourList(6, 2, stride=25),
+              n_steps=200)
+    assert rep.expensive_count == 2 * 200 + (6 - 2) * 8

@@ -64,3 +64,48 @@ def test_zero_temperature_fixed_point():
          "mob": sysm.mobility, "noise": sysm.noise, "seed": 1, "tau_g": 0}
     _, _, _, x, _, _ = OT.run(p, None, None, x0, 200, mode=0)
     assert np.abs(x - x0).max() < 1e-12
+
+
+def _toy_params(**kw):
+    p = {"bond_k": 2000.0, "bond_r0": 0.15, "angle_k": 100.0, "theta0": 1.9106332362490186, "mob": 8.3e-6,
+         "noise": 4.0e-3, "seed": 3, "tau_g": 10, "lam": 100.0, "eps": 4e-4, "hill_h": 1.0, "hill_sigma": 0.3}
+    p.update(kw)
+    return p
+
+
+def _chain(n=8):
+    x = np.zeros((n, 3))
+    for k in range(1, n):
+        a = 1.9106332362490186 * (k % 2)
+        x[k] = x[k - 1] + 0.15 * np.array([math.cos(0.3 * k), math.sin(0.3 * k) * math.cos(a), math.sin(a) * 0.2])
+    return x
+
+
+def _refs(L=6, n=8):
+    rng = np.random.default_rng(4)
+    base = _chain(n)
+    r = np.stack([base + rng.normal(0.0, 0.02 * (1 + k), size=base.shape) for k in range(L)])
+    return r - r.mean(axis=1, keepdims=True)
+
+
+def test_toy_neighbour_list_counters_and_degenerate_case():
+    """SPEC neighbourlist in the toy loop: original mode with M < N charges exactly
+    M + (N - M) updates / steps expensive computations per step (SPEC.md:400 identity); M = N
+    with stride 1 reproduces the run without a list (same CV series and counters) in both
+    modes; the members are the M nearest at each update."""
+    refs, q, x0, steps = _refs(), np.arange(6.0), _chain(), 60
+    for mode in (1, 2):
+        a = OT.run(_toy_params(), refs, q, x0, steps, mode)
+        b = OT.run(_toy_params(nl_m=6, nl_stride=1), refs, q, x0, steps, mode)
+        np.testing.assert_allclose(b[0], a[0], rtol=1e-12, atol=1e-15)
+        assert np.array_equal(b[2], a[2])
+    M, stride = 2, 7
+    cv, rlog, counters, x, _, st = OT.run(_toy_params(nl_m=M, nl_stride=stride), refs, q, x0, steps, 1)
+    updates = len(range(0, steps, stride))
+    assert counters[0] == M * steps + (6 - M) * updates
+    assert st["active"].shape == (M,) and np.all(np.diff(st["active"]) > 0)
+    # close mode: one expensive x<->y fit per step + N on reassignment; M cheap otherwise
+    cv, rlog, counters, x, _, st = OT.run(_toy_params(nl_m=M, nl_stride=stride), refs, q, x0, steps, 2)
+    reas = int(rlog.sum())
+    assert counters[2] == reas and counters[0] == steps + 6 * reas
+    assert counters[1] >= M * (steps - reas)
