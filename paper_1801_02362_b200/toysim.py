@@ -102,6 +102,32 @@ class RunReport:
     refresh_log: np.ndarray
     wall_time: float
     final_coords: np.ndarray = field(repr=False, default=None)
+    trajectory: np.ndarray = field(repr=False, default=None)  # [frames, n, 3] every traj_stride steps
+    traj_stride: int = 0
+
+    # SPEC toysim "External Interfaces"
+    def write_cv_csv(self, path):
+        """CV series: CSV "step,cv_value,bias", one row per step."""
+        with open(path, "w") as f:
+            f.write("step,cv_value,bias\n")
+            for k, (c, b) in enumerate(zip(self.cv_series, self.bias_series)):
+                f.write(f"{k},{float(c)!r},{float(b)!r}\n")
+
+    def write_trajectory(self, path):
+        """Trajectory: plain-text frames -- the step, then n_beads lines "x y z"."""
+        if self.trajectory is None:
+            raise ConfigError("no trajectory recorded (run with traj_stride > 0)")
+        with open(path, "w") as f:
+            for k, x in enumerate(self.trajectory):
+                f.write(f"{k * self.traj_stride}\n")
+                for r in x:
+                    f.write(f"{float(r[0])!r} {float(r[1])!r} {float(r[2])!r}\n")
+
+    def counter_report(self):
+        """The counters the SPEC perf identities are checked against."""
+        return {"steps": self.steps, "mode": self.mode, "expensive_count": self.expensive_count,
+                "cheap_count": self.cheap_count, "reassign_count": self.reassign_count,
+                "measured_K": self.measured_K, "expensive_per_step": self.expensive_count / max(1, self.steps)}
 
 
 class ToySim:
@@ -218,7 +244,7 @@ def make_references(system: ToySystem, n_refs=16, stride=200, warmup=0, walker=0
 
 
 def run(system: ToySystem, ref, mode="close", nl_config=None, mtd_config: MtdConfig | None = None, n_steps=5000,
-        lam=100.0, eps=0.01):
+        lam=100.0, eps=0.01, traj_stride=0):
     """SPEC toysim.run: one walker, returns a RunReport."""
     refs = ref.coords if hasattr(ref, "coords") else ref
     mtd = mtd_config or MtdConfig()
@@ -226,7 +252,7 @@ def run(system: ToySystem, ref, mode="close", nl_config=None, mtd_config: MtdCon
     sim = ToySim(system, refs, mode=mode, lam=lam, eps=eps, mtd=mtd, walkers=1, max_hills=cap, nl_config=nl_config)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    out = sim.run(n_steps)
+    out = sim.run(n_steps, traj_stride=traj_stride)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     sim.check()
@@ -236,4 +262,6 @@ def run(system: ToySystem, ref, mode="close", nl_config=None, mtd_config: MtdCon
     return RunReport(steps=n_steps, mode=mode, expensive_count=int(c[0]), cheap_count=int(c[1]), reassign_count=reas,
                      measured_K=(n_steps / reas) if reas else float("inf"), cv_series=cv[:, 0], bias_series=cv[:, 2],
                      z_series=cv[:, 1], dxy_series=cv[:, 3], refresh_log=out["refresh"][0].cpu().numpy(),
-                     wall_time=wall, final_coords=sim.x[0].cpu().numpy())
+                     wall_time=wall, final_coords=sim.x[0].cpu().numpy(),
+                     trajectory=None if out["traj"] is None else out["traj"][0].cpu().numpy(),
+                     traj_stride=int(traj_stride))

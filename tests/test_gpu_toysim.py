@@ -173,3 +173,22 @@ def test_run_with_neighbour_list_counts_per_spec(refs, cuda_device):
     rep = run(ToySystem(rng_seed=2), refs, mode="original", nl_config=NeighbourList(6, 2, stride=25),
               n_steps=200)
     assert rep.expensive_count == 2 * 200 + (6 - 2) * 8
+
+
+def test_run_report_files(refs, tmp_path, cuda_device):
+    """SPEC toysim external interfaces: the CV series as CSV "step,cv_value,bias" and the
+    trajectory as plain-text frames (step line, then n_beads lines "x y z"), read back equal."""
+    rep = run(ToySystem(rng_seed=4), refs, mode="close", eps=4e-4, n_steps=40, traj_stride=10)
+    rep.write_cv_csv(tmp_path / "cv.csv")
+    rows = (tmp_path / "cv.csv").read_text().splitlines()
+    assert rows[0] == "step,cv_value,bias" and len(rows) == 41
+    got = np.array([[float(v) for v in r.split(",")] for r in rows[1:]])
+    np.testing.assert_array_equal(got[:, 1], rep.cv_series)
+    np.testing.assert_array_equal(got[:, 2], rep.bias_series)
+    rep.write_trajectory(tmp_path / "traj.txt")
+    lines = (tmp_path / "traj.txt").read_text().splitlines()
+    n = rep.trajectory.shape[1]
+    assert len(lines) == 4 * (n + 1) and [int(lines[k * (n + 1)]) for k in range(4)] == [0, 10, 20, 30]
+    back = np.array([[float(v) for v in lines[k * (n + 1) + 1 + j].split()] for k in range(4) for j in range(n)])
+    np.testing.assert_array_equal(back.reshape(4, n, 3), rep.trajectory)
+    assert rep.counter_report()["expensive_count"] == rep.expensive_count
