@@ -53,7 +53,8 @@ constexpr int B_ST = NB * ROWB;    // 8 KB
 constexpr int STAGE = A_ST + B_ST; // 24 KB (a multiple of 1024)
 constexpr int NST = 6;
 constexpr int ACC = 4 * NB;        // 256 TMEM columns per accumulator buffer (2 buffers = 512)
-constexpr int EPI = 4;             // epilogue warps (one per TMEM lane quarter)
+constexpr int EPI = 8;             // epilogue warps: 4 drain the accumulators (one per TMEM lane
+constexpr int EPI_D = 4;           // quarter), all 8 run the fused fits
 constexpr int NT = 32 * (4 + EPI);
 constexpr int SC_BYTES = FG * LT * 9 * 8;  // staged covariances of a tile (fp64)
 constexpr int SMEM = NST * STAGE + SC_BYTES + 1024 + 512;
@@ -288,7 +289,7 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
     for (int s = 0; s < NST; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mb_init(&tfull[b], 1); mb_init(&tempty[b], EPI); }
+    for (int b = 0; b < 2; ++b) { mb_init(&tfull[b], 1); mb_init(&tempty[b], EPI_D); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -393,6 +394,7 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int l = l0 + lp;
         const bool lok = r < 3 * LT && l < L;
         const int el = lok ? eL[3 * l + gg] : 0;
+        if (warp < 4 + EPI_D) {  // the accumulator drain (warps 4-7: TMEM lane quarters)
         mb_wait(&tfull[ab], (it >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         __syncwarp();
@@ -419,8 +421,9 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mb_arrive(&tempty[ab]);
+        }
         epi_bar();
-        // fused fit of the in-window pairs (exact fp64)
+        // fused fit of the in-window pairs (exact fp64), all epilogue warps
         for (int pi = et; pi < FG * LT; pi += 32 * EPI) {
           const int f = pi / LT, li = pi - f * LT;
           const int t = s_t[f], ll = l0 + li;
