@@ -31,7 +31,7 @@
 // (serpentine: they start on the frame rows still in L2).  Warp roles (256 threads,
 // persistent over frame groups): 0 TMA producer (6-stage ring of 24 KB: 16 KB of
 // landmark rows + 8 KB of frame rows per k-step), 1 MMA issuer, 2 TMEM allocator,
-// 4-7 epilogue.
+// 4-15 epilogue (4-7 drain the accumulators, all twelve run the fused fits).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -53,8 +53,8 @@ constexpr int B_ST = NB * ROWB;    // 8 KB
 constexpr int STAGE = A_ST + B_ST; // 24 KB (a multiple of 1024)
 constexpr int NST = 6;
 constexpr int ACC = 4 * NB;        // 256 TMEM columns per accumulator buffer (2 buffers = 512)
-constexpr int EPI = 8;             // epilogue warps: 4 drain the accumulators (one per TMEM lane
-constexpr int EPI_D = 4;           // quarter), all 8 run the fused fits
+constexpr int EPI = 12;            // epilogue warps: 4 drain the accumulators (one per TMEM lane
+constexpr int EPI_D = 4;           // quarter), all 12 run the fused fits
 constexpr int NT = 32 * (4 + EPI);
 constexpr int SC_BYTES = FG * LT * 9 * 8;  // staged covariances of a tile (fp64)
 constexpr int SMEM = NST * STAGE + SC_BYTES + 1024 + 512;
