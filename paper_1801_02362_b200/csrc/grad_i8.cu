@@ -40,8 +40,10 @@
 // 4-19 epilogue (TMEM lane quarter = warp % 4, 12 rows = 2 frames (or 4 in
 // FORCE mode) per warp).  Groups whose union is wider than WMAX landmarks (or
 // n % 4 != 0) are left to the DMMA kernel (launch_cv_grad_dmma, min_width).
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -68,21 +70,29 @@ constexpr int ACC = NDIG * R;  // TMEM columns per accumulator buffer
 constexpr int FVEC = 16;
 constexpr int RPW = R / 4;     // rows per epilogue warp (12)
 
+// k-steps per pipeline stage: the MMA thread's barrier wait, tcgen05 fence and commit cost
+// ~260 clk per stage (clock64 accounting, tools/_diag/r02_s4_gi8_prof.sh) against ~260 clk of
+// tensor-pipe work per k-step, so they are paid once per KPS k-steps
+constexpr int KPS = 2;
+// per-atom constants of a tile (eB int32, w fp64, w' fp64), bulk-copied behind the tile's
+// frame rows so the epilogue reads them from shared memory (as global loads their L2 latency
+// was exposed once per tile: the 16 epilogue warps run the tile phases in lockstep)
+constexpr int XC_BYTES = BMA * (4 + 8 + 8);
 template <int NCV>
-struct Cfg;  // frames per group, B-digit pipeline stages, frame-row buffer bytes
+struct Cfg;  // frames per group, B-digit pipeline stages (of KPS k-steps), frame-row buffer bytes
 template <>
 struct Cfg<2> {
   static constexpr int DG = 8;
-  static constexpr int NST = 7;
-  static constexpr int NST_W = 8;  // stages of the streamed-A (wide) kernel
-  static constexpr int X_BUF = DG * BMA * 12;
+  static constexpr int NST = 3;
+  static constexpr int NST_W = 4;  // stages of the streamed-A (wide) kernel
+  static constexpr int X_BUF = DG * BMA * 12 + XC_BYTES;
 };
 template <>
 struct Cfg<1> {
   static constexpr int DG = 16;
-  static constexpr int NST = 6;
-  static constexpr int NST_W = 7;
-  static constexpr int X_BUF = DG * BMA * 12;
+  static constexpr int NST = 3;
+  static constexpr int NST_W = 3;
+  static constexpr int X_BUF = DG * BMA * 12 + XC_BYTES;
 };
 
 struct RowC {
@@ -105,7 +115,7 @@ struct __align__(16) GHdr {
 constexpr int W_STAGE = L_STAGE + C_KS;  // 22 KB
 template <int NCV, bool WIDE = false>
 constexpr int smem_bytes() {
-  return (WIDE ? Cfg<NCV>::NST_W * W_STAGE : Cfg<NCV>::NST * L_STAGE + C_IMG) + 2 * Cfg<NCV>::X_BUF +
+  return (WIDE ? Cfg<NCV>::NST_W * KPS * W_STAGE : Cfg<NCV>::NST * KPS * L_STAGE + C_IMG) + 2 * Cfg<NCV>::X_BUF +
          (int)sizeof(GHdr<Cfg<NCV>::DG>) + 32 * 8 + 1024;
 }
 
@@ -184,6 +194,13 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.b32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(reinterpret_cast<uint64_t>(bar))
                : "memory");
@@ -197,6 +214,42 @@ __device__ __forceinline__ void tld4(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(taddr));
+}
+
+// Shared-state-space loads for the epilogue.  The header and the frame rows are read
+// through these (not through generic pointers) so the compiler knows they cannot alias the
+// global gradient stores and may schedule the loads of later rows above earlier stores
+// (with generic loads every row was a serial load -> fp64 chain -> store sequence).  They are
+// plain (non-volatile) asm: the address operand must derive from a token produced by an
+// asm volatile AFTER the barrier wait that makes the data visible (shared_token).
+__device__ __forceinline__ uint32_t shared_token(const void* p) {
+  uint32_t t;
+  asm volatile("mov.b32 %0, %1;" : "=r"(t) : "r"(su32(p)));
+  return t;
+}
+__device__ __forceinline__ int lds_i32(uint32_t a) {
+  int v;
+  asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ RowC lds_rowc(uint32_t a) {
+  uint32_t x, y, z, u;
+  asm("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(u) : "r"(a));
+  RowC r;
+  r.scp = __hiloint2double((int)y, (int)x);
+  r.P = __uint_as_float(z);
+  r.corr = __uint_as_float(u);
+  return r;
 }
 
 // byte offset of (row, kk) in a K-major SWIZZLE_32B operand made of 32-byte-K blocks of
@@ -593,8 +646,33 @@ cstack_prep_wide_kernel(int T, int cap, const double* __restrict__ fcen, const i
 
 // diagnostic switch (env MC_GI8_EXP, results invalid): bit 0 = the epilogue only drains the
 // accumulators (TMEM loads, no recombination or stores) -- the MMA / TMA-side time; bit 1 =
-// no MMAs issued (commits only) -- the operand-delivery time
+// no MMAs issued (commits only) -- the operand-delivery time; bit 2 = no B-digit boxes loaded
+// (the producer only arrives) -- the MMA + epilogue time without L2 -> shared-memory delivery
 __constant__ int c_gi8_exp = 0;
+
+// -DMC_GI8_PROF (diagnostic build, tools/_diag/r02_s4_gi8_prof.sh): clock64 accounting of
+// block 0's producer / MMA / frame-row / epilogue (warp 4) threads, printed by the launcher
+#ifdef MC_GI8_PROF
+__device__ unsigned long long g_gi8_prof[32];
+#define GP_DECL unsigned long long gp_t = clock64(), gp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define GP_LAP(i)                               \
+  do {                                          \
+    const unsigned long long gp_n = clock64();  \
+    gp_acc[i] += gp_n - gp_t;                   \
+    gp_t = gp_n;                                \
+  } while (0)
+#define GP_CNT(i) (++gp_acc[i])
+#define GP_FLUSH(base, cond)                                                    \
+  do {                                                                          \
+    if (blockIdx.x == 0 && (cond))                                              \
+      for (int gp_i = 0; gp_i < 8; ++gp_i) atomicAdd(&g_gi8_prof[(base) + gp_i], gp_acc[gp_i]); \
+  } while (0)
+#else
+#define GP_DECL
+#define GP_LAP(i)
+#define GP_CNT(i)
+#define GP_FLUSH(base, cond)
+#endif
 
 template <typename OT, int NCV, bool WIDE>
 __global__ void __launch_bounds__(gi8::NT, 1)
@@ -605,12 +683,13 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
   using namespace gi8;
   constexpr int DG = Cfg<NCV>::DG;
   constexpr int NST = WIDE ? Cfg<NCV>::NST_W : Cfg<NCV>::NST;
-  constexpr int STG = WIDE ? W_STAGE : L_STAGE;  // stage bytes (WIDE: B box + the k-step's A block)
+  constexpr int SUB = WIDE ? W_STAGE : L_STAGE;  // bytes of one k-step (WIDE: B box + the k-step's A block)
+  constexpr int STG = KPS * SUB;                 // stage bytes
   constexpr int X_BUF = Cfg<NCV>::X_BUF;
   using Hdr = GHdr<DG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sL = sm;                  // [NST][128 atoms][4 digits x 32 B] (SWIZZLE_128B) [+ A block]
+  uint8_t* sL = sm;                  // [NST][KPS][128 atoms][4 digits x 32 B] (SWIZZLE_128B) [+ A block]
   uint8_t* sC = sL + NST * STG;      // [NKS_MAX][192 rows x 32 B] (narrow groups only)
   uint8_t* sX = sC + (WIDE ? 0 : C_IMG);  // [2][DG][128 atoms x 3] fp32
   Hdr* hdr = reinterpret_cast<Hdr*>(sX + 2 * X_BUF);
@@ -657,10 +736,13 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
       int i = 0;
       uint32_t st = 0;
       const uint64_t keep = policy_evict_last();
+      GP_DECL;
       for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
         const Hdr* hg = hdrs + g;
         const int active = hg->active, nks = hg->nks, k0 = hg->k0;
+        GP_LAP(0);
         mb_wait(cempty, (i & 1) ^ 1);  // the previous group's MMAs, frame rows and epilogue are done
+        GP_LAP(1);
         mb_expect(cfull, (uint32_t)(sizeof(Hdr) + ((active && !WIDE) ? nks * C_KS : 0)));
         bulk_g2s(hdr, hg, (uint32_t)sizeof(Hdr), cfull);
         if (active && !WIDE) bulk_g2s(sC, cimg + (int64_t)g * C_IMG, (uint32_t)(nks * C_KS), cfull);
@@ -668,66 +750,102 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
         const uint8_t* aimg = WIDE ? cimg + hg->img : nullptr;
         for (int tl = 0; tl < ntile; ++tl) {
           const int a0 = tl * BMA;
-          for (int j = 0; j < nks; ++j, ++st) {
+          for (int j = 0; j < nks; j += KPS, ++st) {
             const int s = st % NST;
+            const int nk = min(KPS, nks - j);
+            GP_LAP(0);
             mb_wait(&lempty[s], ((st / NST) & 1) ^ 1);
-            mb_expect(&lfull[s], (uint32_t)STG);
-            tma2d(&mapB, &lfull[s], sL + s * STG, 4 * (k0 + KS * j), a0, keep);
-            if (WIDE) bulk_g2s(sL + s * STG + L_STAGE, aimg + (int64_t)j * C_KS, (uint32_t)C_KS, &lfull[s]);
+            GP_LAP(2);
+            if (c_gi8_exp & 4) {  // diagnostic: no operand delivery (the MMAs read stale stages)
+              mb_arrive(&lfull[s]);
+              continue;
+            }
+            mb_expect(&lfull[s], (uint32_t)(nk * SUB));
+            for (int u = 0; u < nk; ++u) {
+              uint8_t* dst = sL + s * STG + u * SUB;
+              tma2d(&mapB, &lfull[s], dst, 4 * (k0 + KS * (j + u)), a0, keep);
+              if (WIDE) bulk_g2s(dst + L_STAGE, aimg + (int64_t)(j + u) * C_KS, (uint32_t)C_KS, &lfull[s]);
+            }
           }
         }
       }
+      GP_LAP(0);
+      GP_FLUSH(0, true);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // The whole warp walks the loop converged and one lane chosen by elect.sync issues: under
+    // `if (lane == 0)` ptxas wraps every tcgen05.mma / commit in an ELECT ... BRA.U.ANY retry
+    // loop (it cannot prove a single active thread), ~85 clk of issue path per MMA against
+    // ~65 clk of tensor-pipe work.
     int i = 0;
     uint32_t it = 0, st = 0;
     constexpr uint32_t ID0 = idesc_i8(4 * R), ID1 = idesc_i8(3 * R), ID2 = idesc_i8(2 * R), ID3 = idesc_i8(R);
-    const uint32_t cbase = su32(sC);
+    const uint32_t cbase = su32(sC), lbase = su32(sL);
+    const bool no_mma = c_gi8_exp & 2;
+    GP_DECL;
     for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
+      GP_LAP(0);
       mb_wait(cfull, i & 1);
+      GP_LAP(1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int active = hdr->active, nks = hdr->nks;
       if (active) {
         for (int tl = 0; tl < ntile; ++tl, ++it) {
           const int ab = it & 1;
+          GP_LAP(0);
           mb_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
+          GP_LAP(2);
+          GP_CNT(6);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t d = tmem + (uint32_t)(ab * ACC);
-          for (int j = 0; j < nks; ++j, ++st) {
+          for (int j = 0; j < nks; j += KPS, ++st) {
             const int s = st % NST;
+            const int nk = min(KPS, nks - j);
+            GP_LAP(0);
             mb_wait(&lfull[s], (st / NST) & 1);
+            GP_LAP(3);
+            GP_CNT(7);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
-              const uint32_t lb = su32(sL + s * STG);
-              const uint64_t bdesc = desc32(WIDE ? lb + (uint32_t)L_STAGE : cbase + (uint32_t)(j * C_KS));
-              if (!(c_gi8_exp & 2)) {
-                mma_i8(d, desc128(lb), bdesc, ID0, j == 0 ? 0u : 1u);
-                mma_i8(d + R, desc128(lb + KS), bdesc, ID1, 1u);
-                mma_i8(d + 2 * R, desc128(lb + 2 * KS), bdesc, ID2, 1u);
-                mma_i8(d + 3 * R, desc128(lb + 3 * KS), bdesc, ID3, 1u);
+            if (elect_one()) {
+              if (!no_mma) {
+                for (int u = 0; u < nk; ++u) {
+                  const uint32_t lb = lbase + (uint32_t)(s * STG + u * SUB);
+                  const uint64_t bdesc = desc32(WIDE ? lb + (uint32_t)L_STAGE : cbase + (uint32_t)((j + u) * C_KS));
+                  const uint64_t adesc = desc128(lb);  // digit q: the K slice [32 q, 32 q + 32) of the 128-byte rows
+                  mma_i8(d, adesc, bdesc, ID0, (j + u) == 0 ? 0u : 1u);
+                  mma_i8(d + R, adesc + (KS >> 4), bdesc, ID1, 1u);
+                  mma_i8(d + 2 * R, adesc + 2 * (KS >> 4), bdesc, ID2, 1u);
+                  mma_i8(d + 3 * R, adesc + 3 * (KS >> 4), bdesc, ID3, 1u);
+                }
               }
               mma_commit(&lempty[s]);
-              if (j == nks - 1) mma_commit(&tfull[ab]);
+              if (j + KPS >= nks) mma_commit(&tfull[ab]);
             }
             __syncwarp();
+            GP_LAP(4);
           }
         }
       }
-      if (lane == 0) {
+      if (elect_one()) {
         if (active) mma_commit(cempty);  // arrives once the group's MMAs have read the image
         else mb_arrive(cempty);
       }
       __syncwarp();
     }
+    GP_LAP(0);
+    GP_FLUSH(8, lane == 0);
   } else if (warp == 2) {
     // ------------------------------------------------------------ frame-row producer
     if (lane == 0) {
       int i = 0;
       uint32_t it = 0;
       const uint64_t once = policy_evict_first();
+      GP_DECL;
       for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
+        GP_LAP(0);
         mb_wait(cfull, i & 1);
+        GP_LAP(1);
         if (hdr->active) {
           int rows = 0, raw[DG];
 #pragma unroll
@@ -738,9 +856,15 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
           for (int tl = 0; tl < ntile; ++tl, ++it) {
             const int a0 = tl * BMA, nat = min(BMA, n - a0);
             const int xb = it & 1;
+            GP_LAP(0);
             mb_wait(&xempty[xb], ((it >> 1) & 1) ^ 1);
-            mb_expect(&xfull[xb], (uint32_t)(rows * 12 * nat));
+            GP_LAP(2);
+            mb_expect(&xfull[xb], (uint32_t)((rows * 12 + 20) * nat));
             uint8_t* X = sX + xb * X_BUF;
+            uint8_t* XC = X + DG * BMA * 12;
+            bulk_g2s(XC, eB + a0, (uint32_t)(4 * nat), &xfull[xb]);
+            bulk_g2s(XC + 4 * BMA, w + a0, (uint32_t)(8 * nat), &xfull[xb]);
+            bulk_g2s(XC + 12 * BMA, wa + a0, (uint32_t)(8 * nat), &xfull[xb]);
 #pragma unroll
             for (int f = 0; f < DG; ++f)
               if (raw[f] >= 0)
@@ -750,6 +874,8 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
         }
         mb_arrive(cempty);
       }
+      GP_LAP(0);
+      GP_FLUSH(16, true);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
@@ -757,15 +883,33 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
     constexpr int FPW = RPW / (3 * NCV);            // frames per warp (2, or 4 in FORCE mode)
     int i = 0;
     uint32_t it = 0;
+    GP_DECL;
     for (int g = blockIdx.x; g < groups; g += gridDim.x, ++i) {
+      GP_LAP(0);
       mb_wait(cfull, i & 1);
+      GP_LAP(1);
+      const uint32_t hs = shared_token(hdr);  // the group's header, shared state space
       if (hdr->active) {
         for (int tl = 0; tl < ntile; ++tl, ++it) {
           const int ab = it & 1;
           const int al = qd * 32 + lane;
           const int a = tl * BMA + al;
           const bool valid = a < n;
+          // the tile's frame rows and per-atom constants (the B column scale 2^eB and the
+          // weights) are in shared memory well before its accumulators are complete
+          GP_LAP(0);
+          mb_wait(&xfull[ab], (it >> 1) & 1);
+          GP_LAP(4);
+          const uint32_t xs0 = shared_token(sX + ab * X_BUF);
+          const uint32_t xcs = xs0 + (uint32_t)(DG * BMA * 12);
+          const int eb = valid ? lds_i32(xcs + 4 * al) : 0;
+          const double sxa = pow2d(14 - eb);
+          const double q2w = valid ? 2.0 * lds_f64(xcs + 4 * BMA + 8 * al) * pow2d(eb - 14) : 0.0;
+          const double wak = valid ? lds_f64(xcs + 12 * BMA + 8 * al) : 0.0;
+          const float q2wf = (float)q2w, wakf = (float)wak;
+          GP_LAP(0);
           mb_wait(&tfull[ab], (it >> 1) & 1);
+          GP_LAP(2);
           asm volatile("tcgen05.fence::after_thread_sync;");
           __syncwarp();  // tcgen05.ld is .sync.aligned: the whole warp, converged
           uint32_t acc[NDIG][RPW];
@@ -779,35 +923,30 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
           asm volatile("tcgen05.fence::before_thread_sync;");
           __syncwarp();
           if (lane == 0) mb_arrive(&tempty[ab]);
+          GP_LAP(3);
           if (c_gi8_exp & 1) {
-            mb_wait(&xfull[ab], (it >> 1) & 1);
             __syncwarp();
             if (lane == 0) mb_arrive(&xempty[ab]);
             continue;
           }
-          // per-atom constants: the B column scale 2^eB and the weights
-          const int eb = valid ? eB[a] : 0;
-          const double sxa = pow2d(14 - eb);
-          const double q2w = valid ? 2.0 * w[a] * pow2d(eb - 14) : 0.0;
-          const double wak = valid ? wa[a] : 0.0;
-          const float q2wf = (float)q2w, wakf = (float)wak;
-          mb_wait(&xfull[ab], (it >> 1) & 1);
-          const float* X = reinterpret_cast<const float*>(sX + ab * X_BUF);
+          const uint32_t xs = xs0 + (uint32_t)(al * 12);
 #pragma unroll
           for (int fl = 0; fl < FPW; ++fl) {
             const int f = part * FPW + fl;
-            const int raw = hdr->raw[f];
+            const int raw = lds_i32(hs + (uint32_t)(offsetof(Hdr, raw) + 4 * f));
             if (raw < 0) continue;  // warp-uniform
             double xc[3];
 #pragma unroll
-            for (int b = 0; b < 3; ++b) xc[b] = ((double)X[(f * BMA + al) * 3 + b] - hdr->cx[f][b]) * sxa;
+            for (int b = 0; b < 3; ++b)
+              xc[b] = ((double)lds_f32(xs + (uint32_t)((f * BMA * 3 + b) * 4)) -
+                       lds_f64(hs + (uint32_t)(offsetof(Hdr, cx) + 8 * (3 * f + b)))) * sxa;
 #pragma unroll
             for (int cv = 0; cv < NCV; ++cv) {
               OT* dst = (cv ? out1 : out0) + ((int64_t)raw * n + a) * 3;
 #pragma unroll
               for (int b = 0; b < 3; ++b) {
                 const int rl = fl * 3 * NCV + cv * 3 + b;
-                const RowC rc = hdr->rc[part * RPW + rl];
+                const RowC rc = lds_rowc(hs + (uint32_t)(offsetof(Hdr, rc) + 16 * (part * RPW + rl)));
                 const float lo = fmaf((float)(int)acc[3][rl], 5.9604644775390625e-8f,
                                       fmaf((float)(int)acc[2][rl], 1.52587890625e-5f,
                                            (float)(int)acc[1][rl] * 3.90625e-3f));
@@ -829,11 +968,14 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
           }
           __syncwarp();
           if (lane == 0) mb_arrive(&xempty[ab]);
+          GP_LAP(5);
         }
       }
       __syncwarp();
       if (lane == 0) mb_arrive(cempty);
     }
+    GP_LAP(0);
+    GP_FLUSH(24, warp == 4 && lane == 0);
   }
   __syncthreads();
   if (warp == 2) {
@@ -963,6 +1105,21 @@ cudaError_t launch_cv_grad_i8(int T, int n, int cap, const float* fraw, const do
     if (out_f32) MC_GI8(float, 1); else MC_GI8(double, 1);
   }
 #undef MC_GI8
+#ifdef MC_GI8_PROF
+  {
+    unsigned long long h[32];
+    cudaStreamSynchronize(stream);
+    cudaMemcpyFromSymbol(h, g_gi8_prof, sizeof(h));
+    fprintf(stderr, "gi8prof producer: other %llu wait_cempty %llu wait_lempty %llu\n", h[0], h[1], h[2]);
+    fprintf(stderr, "gi8prof mma: other %llu wait_cfull %llu wait_tempty %llu wait_lfull %llu issue %llu tiles %llu ksteps %llu\n",
+            h[8], h[9], h[10], h[11], h[12], h[14], h[15]);
+    fprintf(stderr, "gi8prof rows: other %llu wait_cfull %llu wait_xempty %llu\n", h[16], h[17], h[18]);
+    fprintf(stderr, "gi8prof epi: other %llu wait_cfull %llu wait_tfull %llu tmem_ld %llu wait_xfull %llu math_store %llu\n",
+            h[24], h[25], h[26], h[27], h[28], h[29]);
+    memset(h, 0, sizeof(h));
+    cudaMemcpyToSymbol(g_gi8_prof, h, sizeof(h));
+  }
+#endif
   cudaError_t e = cudaGetLastError();
   // ncv = 2 with wide_flag: the caller runs the wide groups on launch_cv_grad_i8_wide
   if (e != cudaSuccess || ncv != 2 || (dbg & 16) || wide_flag) return e;
