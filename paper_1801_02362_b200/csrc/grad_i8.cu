@@ -732,7 +732,8 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // (the warp walks the loops converged, one elect.sync lane issues the copies)
+    {
       int i = 0;
       uint32_t st = 0;
       const uint64_t keep = policy_evict_last();
@@ -743,9 +744,12 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
         GP_LAP(0);
         mb_wait(cempty, (i & 1) ^ 1);  // the previous group's MMAs, frame rows and epilogue are done
         GP_LAP(1);
-        mb_expect(cfull, (uint32_t)(sizeof(Hdr) + ((active && !WIDE) ? nks * C_KS : 0)));
-        bulk_g2s(hdr, hg, (uint32_t)sizeof(Hdr), cfull);
-        if (active && !WIDE) bulk_g2s(sC, cimg + (int64_t)g * C_IMG, (uint32_t)(nks * C_KS), cfull);
+        if (elect_one()) {
+          mb_expect(cfull, (uint32_t)(sizeof(Hdr) + ((active && !WIDE) ? nks * C_KS : 0)));
+          bulk_g2s(hdr, hg, (uint32_t)sizeof(Hdr), cfull);
+          if (active && !WIDE) bulk_g2s(sC, cimg + (int64_t)g * C_IMG, (uint32_t)(nks * C_KS), cfull);
+        }
+        __syncwarp();
         if (!active) continue;
         const uint8_t* aimg = WIDE ? cimg + hg->img : nullptr;
         for (int tl = 0; tl < ntile; ++tl) {
@@ -756,21 +760,24 @@ cv_grad_i8_kernel(const __grid_constant__ CUtensorMap mapB, int T, int n, int np
             GP_LAP(0);
             mb_wait(&lempty[s], ((st / NST) & 1) ^ 1);
             GP_LAP(2);
-            if (c_gi8_exp & 4) {  // diagnostic: no operand delivery (the MMAs read stale stages)
-              mb_arrive(&lfull[s]);
-              continue;
+            if (elect_one()) {
+              if (c_gi8_exp & 4) {  // diagnostic: no operand delivery (the MMAs read stale stages)
+                mb_arrive(&lfull[s]);
+              } else {
+                mb_expect(&lfull[s], (uint32_t)(nk * SUB));
+                for (int u = 0; u < nk; ++u) {
+                  uint8_t* dst = sL + s * STG + u * SUB;
+                  tma2d(&mapB, &lfull[s], dst, 4 * (k0 + KS * (j + u)), a0, keep);
+                  if (WIDE) bulk_g2s(dst + L_STAGE, aimg + (int64_t)(j + u) * C_KS, (uint32_t)C_KS, &lfull[s]);
+                }
+              }
             }
-            mb_expect(&lfull[s], (uint32_t)(nk * SUB));
-            for (int u = 0; u < nk; ++u) {
-              uint8_t* dst = sL + s * STG + u * SUB;
-              tma2d(&mapB, &lfull[s], dst, 4 * (k0 + KS * (j + u)), a0, keep);
-              if (WIDE) bulk_g2s(dst + L_STAGE, aimg + (int64_t)(j + u) * C_KS, (uint32_t)C_KS, &lfull[s]);
-            }
+            __syncwarp();
           }
         }
       }
       GP_LAP(0);
-      GP_FLUSH(0, true);
+      GP_FLUSH(0, lane == 0);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer

@@ -50,14 +50,19 @@ constexpr int KS = 32;             // atoms per k-step
 constexpr int ROWB = 4 * KS;       // 128 bytes per row and k-step (4 digits)
 constexpr int A_ST = MR * ROWB;    // 16 KB
 constexpr int B_ST = NB * ROWB;    // 8 KB
-constexpr int STAGE = A_ST + B_ST; // 24 KB (a multiple of 1024)
-constexpr int NST = 6;
+constexpr int STAGE = A_ST + B_ST; // 24 KB per k-step (a multiple of 1024)
+// k-steps per pipeline stage: the MMA warp's barrier wait, tcgen05 fence and commit are paid
+// once per KPS k-steps (grad_i8.cu: ~260 clk per stage against ~320 clk of tensor-pipe work
+// per k-step here)
+constexpr int KPS = 2;
+constexpr int STG = KPS * STAGE;   // 48 KB per stage
+constexpr int NST = 3;
 constexpr int ACC = 4 * NB;        // 256 TMEM columns per accumulator buffer (2 buffers = 512)
 constexpr int EPI = 12;            // epilogue warps: 4 drain the accumulators (one per TMEM lane
 constexpr int EPI_D = 4;           // quarter), all 12 run the fused fits
 constexpr int NT = 32 * (4 + EPI);
 constexpr int SC_BYTES = FG * LT * 9 * 8;  // staged covariances of a tile (fp64)
-constexpr int SMEM = NST * STAGE + SC_BYTES + 1024 + 512;
+constexpr int SMEM = NST * STG + SC_BYTES + 1024 + 512;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
@@ -111,6 +116,13 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
 __device__ __forceinline__ uint64_t desc32(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.b32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(reinterpret_cast<uint64_t>(bar))
@@ -274,9 +286,9 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   using namespace ri8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sSt = sm;                                                  // [NST][A 16 KB | B 6 KB]
-  double* sC = reinterpret_cast<double*>(sm + NST * STAGE);          // [FG][LT][9]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NST * STAGE + SC_BYTES);
+  uint8_t* sSt = sm;                                                  // [NST][KPS][A 16 KB | B 8 KB]
+  double* sC = reinterpret_cast<double*>(sm + NST * STG);            // [FG][LT][9]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NST * STG + SC_BYTES);
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;  // [2]
   uint64_t* tempty = tfull + 2;   // [2]
@@ -316,8 +328,8 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   };
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    // ------------------------------------------------------------ TMA producer (one elect.sync lane issues)
+    {
       uint32_t st = 0;
       for (int g = blockIdx.x; g < groups; g += gridDim.x) {
         int wlo, whi;
@@ -326,20 +338,27 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         // on the frame rows the previous tile read last (still in L2) instead of re-reading
         // the group's frame rows from HBM in the same order
         for (int l0 = wlo, ti = 0; l0 < whi; l0 += LT, ++ti)
-          for (int j = 0; j < nks; ++j, ++st) {
-            const int ks = (ti & 1) ? nks - 1 - j : j;
+          for (int j = 0; j < nks; j += KPS, ++st) {
             const int s = st % NST;
+            const int nk = min(KPS, nks - j);
             mb_wait(&empty[s], ((st / NST) & 1) ^ 1);
-            mb_expect(&full[s], (uint32_t)STAGE);
-            uint8_t* dst = sSt + s * STAGE;
-            tma2d(&mapA, &full[s], dst, ROWB * ks, 3 * l0);
-            tma3d(&mapB, &full[s], dst + A_ST, 0, NR * g, 4 * ks);
+            if (elect_one()) {
+              mb_expect(&full[s], (uint32_t)(nk * STAGE));
+              for (int u = 0; u < nk; ++u) {
+                const int ks = (ti & 1) ? nks - 1 - (j + u) : j + u;
+                uint8_t* dst = sSt + s * STG + u * STAGE;
+                tma2d(&mapA, &full[s], dst, ROWB * ks, 3 * l0);
+                tma3d(&mapB, &full[s], dst + A_ST, 0, NR * g, 4 * ks);
+              }
+            }
+            __syncwarp();
           }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     uint32_t st = 0, it = 0;
+    const uint32_t sbase = su32(sSt);
     for (int g = blockIdx.x; g < groups; g += gridDim.x) {
       int wlo, whi;
       union_of(g, wlo, whi);
@@ -348,24 +367,29 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         mb_wait(&tempty[ab], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + (uint32_t)(ab * ACC);
-        for (int j = 0; j < nks; ++j, ++st) {  // (the k order does not matter to the MMAs)
+        for (int j = 0; j < nks; j += KPS, ++st) {  // (the k order does not matter to the MMAs)
           const int s = st % NST;
+          const int nk = min(KPS, nks - j);
           mb_wait(&full[s], (st / NST) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          if (lane == 0) {
-            const uint32_t a = su32(sSt + s * STAGE), b = a + A_ST;
-            // the 10 digit products with p + q <= 3 in 4 MMAs: the B tile holds the frame
-            // digits plane by plane ([p][64 rows][32 B]), so for landmark digit q ONE MMA with
-            // N = (4 - q) 64 reads frame digits 0..3-q and writes the TMEM columns of levels
-            // q..3 (kind::i8 with N <= 64 is issue-bound at ~45 clk per MMA, N = 256 runs at
-            // N/2 clk: tools/_diag/i8_probe.cu)
-            const uint64_t bd = desc32(b);
-            mma_i8(d, desc128(a), bd, idesc_n(4 * NB), j > 0 ? 1u : 0u);
-            mma_i8(d + (uint32_t)NB, desc128(a + KS), bd, idesc_n(3 * NB), 1u);
-            mma_i8(d + (uint32_t)(2 * NB), desc128(a + 2 * KS), bd, idesc_n(2 * NB), 1u);
-            mma_i8(d + (uint32_t)(3 * NB), desc128(a + 3 * KS), bd, idesc_n(NB), 1u);
+          // one lane chosen by elect.sync issues (under `if (lane == 0)` ptxas wraps every
+          // tcgen05.mma / commit in an ELECT ... BRA.U.ANY retry loop)
+          if (elect_one()) {
+            for (int u = 0; u < nk; ++u) {
+              const uint32_t a = sbase + (uint32_t)(s * STG + u * STAGE), b = a + A_ST;
+              // the 10 digit products with p + q <= 3 in 4 MMAs: the B tile holds the frame
+              // digits plane by plane ([p][64 rows][32 B]), so for landmark digit q ONE MMA with
+              // N = (4 - q) 64 reads frame digits 0..3-q and writes the TMEM columns of levels
+              // q..3 (kind::i8 with N <= 64 is issue-bound at ~45 clk per MMA, N = 256 runs at
+              // N/2 clk: tools/_diag/i8_probe.cu)
+              const uint64_t bd = desc32(b), ad = desc128(a);
+              mma_i8(d, ad, bd, idesc_n(4 * NB), (j + u) > 0 ? 1u : 0u);
+              mma_i8(d + (uint32_t)NB, ad + (KS >> 4), bd, idesc_n(3 * NB), 1u);
+              mma_i8(d + (uint32_t)(2 * NB), ad + 2 * (KS >> 4), bd, idesc_n(2 * NB), 1u);
+              mma_i8(d + (uint32_t)(3 * NB), ad + 3 * (KS >> 4), bd, idesc_n(NB), 1u);
+            }
             mma_commit(&empty[s]);
-            if (j == nks - 1) mma_commit(&tfull[ab]);
+            if (j + KPS >= nks) mma_commit(&tfull[ab]);
           }
           __syncwarp();
         }

@@ -602,6 +602,13 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t b
 // the .shared::cluster form (a cluster-window address) stalls the issuing
 // thread for roughly the MMA pipeline depth on every commit (one commit per 18
 // MMAs: 649 TF32 TF/s); the generic local-shared address does not (908 TF/s).
+// one lane of the (converged) warp
+__device__ __forceinline__ bool umma_elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.b32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(
                    reinterpret_cast<uint64_t>(bar))
@@ -686,8 +693,8 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer
-    if (lane == 0) {
+    // ---------------- TMA producer (the warp walks the loop converged; one elect.sync lane issues)
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -708,10 +715,12 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
           uint8_t* st = smem + stage * STAGE_BYTES;
 #ifdef MC_TF32_NOTMA
           // diagnostic build only: MMAs run on stale shared memory, no operand traffic
-          mbar_arrive(&full[stage]);
+          if (umma_elect_one()) mbar_arrive(&full[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
 #endif
+          if (umma_elect_one()) {
 #if defined(MC_DIAG_NOA)
           if (!F16) mbar_expect_tx(&full[stage], STAGE_BYTES); else asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(3 * BP2_BYTES) : "memory");
 #elif defined(MC_DIAG_NOB)
@@ -749,6 +758,8 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
               tma_load_2d(&mll, &full[stage], bl + g * BP_BYTES, k0, g * L + l0);
             }
           }
+          }
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -780,7 +791,10 @@ msd_tf32_kernel(const __grid_constant__ CUtensorMap mfh, const __grid_constant__
         mbar_wait(&full[stage], phase);
 #endif
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) {
+        // one lane chosen by elect.sync issues: under `if (lane == 0)` ptxas wraps every
+        // tcgen05.mma / commit in an ELECT ... BRA.U.ANY retry loop (~85 clk of issue path per
+        // MMA against 72 clk of tensor-pipe work for M = 128, N = 144, K = 16)
+        if (umma_elect_one()) {
           const uint32_t st = smem_u32(smem + stage * STAGE_BYTES);
           if constexpr (F16) {
             // 128 B rows: hi atoms at byte 0..63, lo at 64..127; one MMA = 16 atoms = 32 B
