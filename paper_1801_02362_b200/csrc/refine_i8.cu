@@ -58,8 +58,8 @@ constexpr int KPS = 2;
 constexpr int STG = KPS * STAGE;   // 48 KB per stage
 constexpr int NST = 3;
 constexpr int ACC = 4 * NB;        // 256 TMEM columns per accumulator buffer (2 buffers = 512)
-constexpr int EPI = 12;            // epilogue warps: 4 drain the accumulators (one per TMEM lane
-constexpr int EPI_D = 4;           // quarter), all 12 run the fused fits
+constexpr int EPI = 12;            // epilogue warps: all drain the accumulators (3 per TMEM lane
+                                   // quarter) and run the fused fits
 constexpr int NT = 32 * (4 + EPI);
 constexpr int SC_BYTES = FG * LT * 9 * 8;  // staged covariances of a tile (fp64)
 constexpr int SMEM = NST * STG + SC_BYTES + 1024 + 512;
@@ -301,7 +301,7 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
     for (int s = 0; s < NST; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mb_init(&tfull[b], 1); mb_init(&tempty[b], EPI_D); }
+    for (int b = 0; b < 2; ++b) { mb_init(&tfull[b], 1); mb_init(&tempty[b], EPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -418,13 +418,15 @@ refine_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int l = l0 + lp;
         const bool lok = r < 3 * LT && l < L;
         const int el = lok ? eL[3 * l + gg] : 0;
-        if (warp < 4 + EPI_D) {  // the accumulator drain (warps 4-7: TMEM lane quarters)
+        {  // the accumulator drain: every epilogue warp (TMEM lane quarter = warp % 4), the
+           // 7 three-frame column chunks dealt round-robin over the quarter's 3 warps (with only
+           // warps 4-7 draining, one warp per scheduler converted all 63 columns serially)
         mb_wait(&tfull[ab], (it >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         __syncwarp();
         const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(ab * ACC);
 #pragma unroll 1
-        for (int fc = 0; fc < FG / 3; ++fc) {  // 3 frames (9 columns) at a time
+        for (int fc = (warp - 4) >> 2; fc < FG / 3; fc += EPI / 4) {  // 3 frames (9 columns) at a time
           uint32_t acc[4][9];
 #pragma unroll
           for (int lvl = 0; lvl < 4; ++lvl) {
