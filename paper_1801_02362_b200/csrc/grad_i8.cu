@@ -26,8 +26,9 @@
 //    per-row constants), written to a caller workspace;
 //  * cv_grad_i8_kernel (persistent, one CTA per SM): per group the header and
 //    image are bulk-copied into shared memory once; per atom tile of 128 the B
-//    digits stream through a 7-stage ring of 16 KB TMA boxes (128 atoms x one
-//    128-byte row = the 4 digits of one 32-byte k-step, SWIZZLE_128B, so digit q
+//    digits stream through a 3-stage ring of 2 x 16 KB TMA boxes (two k-steps
+//    per stage; a box = 128 atoms x one 128-byte row = the 4 digits of one
+//    32-byte k-step, SWIZZLE_128B, so digit q
 //    is the K slice [32q, 32q + 32) of the row and the TMA moves 128-byte row
 //    segments, not 32-byte ones); per k-step 4 MMAs with M = 128 atoms (TMEM
 //    lanes), K = 32, and the A digits stacked along N: for B digit q one MMA
@@ -36,7 +37,8 @@
 //    double-buffered (384 of 512 TMEM columns), so the epilogue of one atom
 //    tile overlaps the next tile's MMAs.
 // Warp roles (640 threads): 0 TMA producer (header/image, B digits); 1 MMA
-// issuer (one lane); 2 TMEM allocator + frame-row producer (1-D bulk copies);
+// issuer (the warp converged, one elect.sync lane issues); 2 TMEM allocator +
+// producer of the frame rows and per-atom constants (1-D bulk copies);
 // 4-19 epilogue (TMEM lane quarter = warp % 4, 12 rows = 2 frames (or 4 in
 // FORCE mode) per warp).  Groups whose union is wider than WMAX landmarks (or
 // n % 4 != 0) are left to the DMMA kernel (launch_cv_grad_dmma, min_width).

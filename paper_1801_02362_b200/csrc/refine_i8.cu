@@ -29,9 +29,9 @@
 // bound by the L2 -> shared-memory rate of its operand boxes.  A frame group takes
 // ceil(union / 42) landmark tiles of its window union, odd tiles sweeping K backwards
 // (serpentine: they start on the frame rows still in L2).  Warp roles (256 threads,
-// persistent over frame groups): 0 TMA producer (6-stage ring of 24 KB: 16 KB of
+// persistent over frame groups): 0 TMA producer (3-stage ring of 2 x 24 KB: 16 KB of
 // landmark rows + 8 KB of frame rows per k-step), 1 MMA issuer, 2 TMEM allocator,
-// 4-15 epilogue (4-7 drain the accumulators, all twelve run the fused fits).
+// 4-15 epilogue (all twelve drain the accumulators and run the fused fits).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
