@@ -204,3 +204,29 @@ def test_row_digit_exponents_from_k1s_equal_two_pass(cuda_device):
     R3, nks = a.dig.shape[0], a.dig.shape[1]
     assert torch.equal(c.e, a.e)
     assert torch.equal(c.dig.reshape(nks, 4, R3, 32), a.dig.permute(1, 2, 0, 3))
+
+
+@pytest.mark.gpu
+def test_row_digit_planes_chunked_kernel_equals_two_pass(cuda_device):
+    """The shared-memory-staged plane kernel (exponents from the K1s, w = 1; several 1280-atom
+    chunks with a partial last one, rows gathered through perm and fmap) writes exactly the
+    digits of the two-pass kernel."""
+    rng = np.random.default_rng(5)
+    T, n = 37, 2692
+    x = torch.from_numpy(rng.normal(size=(T, n, 3)).astype(np.float32)).cuda()
+    x[3] += 12.5
+    w = torch.full((n,), 1.0 / n, dtype=torch.float64, device=x.device)
+    sp = K.center_split(x, w, w, weighted=False, fmt="f16", terms=1, wuni=1.0 / n)
+    perm = torch.randperm(T, device=x.device).to(torch.int32)
+    a = K.row_digits(x, sp.centroid, None, perm=perm)
+    c = K.row_digits(x, sp.centroid, None, perm=perm, ein=sp.dexp, planes=True)
+    R3, nks = a.dig.shape[0], a.dig.shape[1]
+    assert nks > 80  # more than two chunks
+    assert torch.equal(c.e, a.e)
+    assert torch.equal(c.dig.reshape(nks, 4, R3, 32), a.dig.permute(1, 2, 0, 3))
+    # frames stored in another order, read through fmap (sorted position -> raw row)
+    fmap = torch.randperm(T, device=x.device).to(torch.int32)
+    xs = torch.empty_like(x)
+    xs[fmap.long()] = x
+    d = K.row_digits(xs, sp.centroid, None, perm=perm, fmap=fmap, count=T, ein=sp.dexp, planes=True)
+    assert torch.equal(d.dig, c.dig) and torch.equal(d.e, c.e)
