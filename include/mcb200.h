@@ -422,7 +422,8 @@ int mc_property_map(int32_t L, int32_t n, const double* D, const double* grads, 
  *   arrays of d values; nodes lo + k h, k = 0..bins, row-major [bins0+1][bins1+1]); val, dgrid
  *   [d][nodes] and (d = 2) the cross derivative dxy store the cubic Hermite data.  deposit adds
  *   one hill (device center/sigma [d]) to every node within `cutoff` sigmas (SPEC: 6);
- *   *flag = MC_FLAG_OUT_OF_GRID for a centre off the grid.  eval interpolates V, dV per frame;
+ *   *flag = MC_FLAG_OUT_OF_GRID for a centre off the grid (the grid is then left unchanged).
+ *   eval interpolates V, dV per frame;
  *   flags[t] = MC_FLAG_OUT_OF_GRID (V = dV = 0) for a CV off the grid.
  * mc_mtd_force: F[t,k,c] = -sum_i dV[t,i] G_i[t,k,c] (physical sign, SPEC design decision),
  *   G_i = g0, g1, g2 the CV gradients [T, n, 3] (dtype f32/f64, F likewise). */

@@ -77,12 +77,12 @@ mtd_deposit_kernel(double* __restrict__ val, double* __restrict__ dgrid, double*
   const int64_t e = (int64_t)blockIdx.x * MNT + threadIdx.x;
   const double c0 = center[0], s0 = sigma[0];
   const double c1 = gg.d == 2 ? center[1] : 0.0, s1 = gg.d == 2 ? sigma[1] : 1.0;
-  if (e == 0 && flag) {
-    bool out = !(c0 >= gg.lo[0] && c0 <= gg.lo[0] + gg.h[0] * gg.bins[0]);
-    if (gg.d == 2) out = out || !(c1 >= gg.lo[1] && c1 <= gg.lo[1] + gg.h[1] * gg.bins[1]);
-    *flag = out ? kFlagOutOfGrid : 0;
-  }
-  if (e >= nodes) return;
+  // a centre off the grid is rejected by every thread: the grid stays untouched, so grid and
+  // direct-sum V agree for any deposition history (also for callers of the C ABI)
+  bool out = !(c0 >= gg.lo[0] && c0 <= gg.lo[0] + gg.h[0] * gg.bins[0]);
+  if (gg.d == 2) out = out || !(c1 >= gg.lo[1] && c1 <= gg.lo[1] + gg.h[1] * gg.bins[1]);
+  if (e == 0 && flag) *flag = out ? kFlagOutOfGrid : 0;
+  if (out || e >= nodes) return;
   const int i0 = (int)(e / n1), i1 = (int)(e - (int64_t)i0 * n1);
   const double u0 = (gg.lo[0] + gg.h[0] * i0 - c0) / s0;
   if (!(fabs(u0) <= cutoff)) return;
