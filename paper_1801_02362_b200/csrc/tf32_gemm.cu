@@ -517,7 +517,10 @@ constexpr int TMEM_COLS = 512;
 // warps 4.. are the epilogue: two per TMEM lane quarter, each finishing half
 // of the 8-landmark column chunks, so the latency-bound fp64 Newton runs on
 // two warps per SM sub-partition and the accumulator is released sooner
-constexpr int EPI_WARPS = 8;
+#ifndef MC_K2_EPI_WARPS
+#define MC_K2_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = MC_K2_EPI_WARPS;  // 8 measured best (12: 128-register cap)
 constexpr int NT = 32 * (4 + EPI_WARPS);
 }  // namespace gemm
 
